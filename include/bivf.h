@@ -1,0 +1,190 @@
+/*
+ * bivf.h — C-ABI of the B200-native online IVF-Flat path (libbivf_gpu.so).
+ *
+ * This is the drop-in boundary for the reference's index plugin API
+ * (blockivf::VectorIndex, /root/reference/proj/include/blockivf/vector_index.hpp:19-44,
+ * and the concrete ClusterIndex surface, include/blockivf/ivf_index.hpp:47-103).
+ * Every entry point cites the reference interface it replaces.  Plain
+ * pointers and sizes only; all array arguments are HOST memory unless the
+ * name says _device.  No exceptions cross the ABI: every call returns a
+ * bivf_status and bivf_last_error() holds the thread-local message.
+ *
+ * Status -> reference exception (so C++/Python wrappers can rethrow):
+ *   BIVF_EINVAL   std::invalid_argument          (ivf_index.cpp:126-129, :266-269)
+ *   BIVF_EPOOL    PoolExhaustedError(inserted)    (types.hpp:19-30)
+ *   BIVF_ECORRUPT CorruptListError                (types.hpp:34-36)
+ *   BIVF_ERANGE   std::out_of_range               (ivf_index.cpp:477, block_store.cpp:51)
+ *   BIVF_ELOGIC   std::logic_error                (block_store.cpp:58-62)
+ *   BIVF_EIO      std::runtime_error (snapshot)   (ivf_index.cpp:537, :569-575)
+ *   BIVF_ECUDA    CUDA/driver failure (no GPU, launch error) — no CPU fallback exists
+ *   BIVF_EBUSY    all leases busy (executor fail-fast reject, executor.cpp:165-170)
+ */
+#ifndef BIVF_H
+#define BIVF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BIVF_OK = 0,
+    BIVF_EINVAL = 1,
+    BIVF_EPOOL = 2,
+    BIVF_ECORRUPT = 3,
+    BIVF_ERANGE = 4,
+    BIVF_ELOGIC = 5,
+    BIVF_EIO = 6,
+    BIVF_ECUDA = 7,
+    BIVF_EBUSY = 8,
+    BIVF_ENOMEM = 9
+} bivf_status;
+
+typedef enum { BIVF_METRIC_L2 = 0, BIVF_METRIC_IP = 1 } bivf_metric;
+
+/* IndexConfig + PoolConfig (ivf_index.hpp:20-30, block_store.hpp:16-33), plus
+ * device placement.  Zero fields take the reference defaults noted. */
+typedef struct {
+    uint64_t num_clusters;        /* N (default 100) */
+    uint64_t dim;                 /* D (required) */
+    uint64_t nprobe_default;      /* default 8 */
+    uint64_t rearrange_threshold; /* T'_m (default 256) */
+    uint64_t kmeans_iters;        /* default 25 */
+    uint64_t kmeans_seed;         /* default 42 (use kmeans_seed_set=1 to pass 0) */
+    uint64_t num_blocks;          /* |P| (default 1024) */
+    uint64_t block_capacity;      /* T_m (default 64) */
+    double alert_watermark;       /* default 0.9 */
+    int32_t metric;               /* bivf_metric (extension; default L2) */
+    int32_t device;               /* CUDA device ordinal (default 0) */
+    uint32_t num_leases;          /* search leases = streams+workspaces (default 32) */
+    uint32_t max_list_blocks;     /* per-list block-table row length (default num_blocks) */
+    uint32_t kmeans_seed_set;     /* 1: kmeans_seed is explicit even if 0 */
+    uint32_t reserved[7];
+} bivf_config;
+
+typedef struct bivf_index bivf_index;
+
+/* thread-local message of the last failing call on this thread */
+const char* bivf_last_error(void);
+/* "bivf <version> sm_100a" */
+const char* bivf_version(void);
+/* number of visible CUDA devices (0 on a host without GPU) */
+int bivf_device_count(void);
+
+/* ---- lifecycle ------------------------------------------------------- */
+/* ClusterIndex(IndexConfig) storage (ivf_index.cpp:36-45): allocates the whole
+ * device arena up front (block_store.cpp:19-29). */
+bivf_status bivf_create(const bivf_config* cfg, bivf_index** out);
+bivf_status bivf_destroy(bivf_index* h);
+bivf_status bivf_get_config(const bivf_index* h, bivf_config* out);
+
+/* ClusterIndex(offline, n, cfg) (ivf_index.cpp:47-59): k-means (kmeans.cpp:31-142,
+ * assignment sweeps on the GPU, bit-identical to the reference) then the
+ * offline bulk load; ids 0..n-1, auto ids continue at n. */
+bivf_status bivf_train(bivf_index* h, const float* x, uint64_t n);
+/* centroids row-major [num_clusters x dim] (ClusterIndex::centroids()) */
+bivf_status bivf_set_centroids(bivf_index* h, const float* centroids);
+bivf_status bivf_get_centroids(const bivf_index* h, float* out);
+/* build_offline (ivf_index.cpp:61-82).  assignment NULL -> assign on device;
+ * ids NULL -> 0..n-1 (offline range, like the trained constructor), else the
+ * given ids are recorded as supplied ids. */
+bivf_status bivf_bulk_load(bivf_index* h, const float* x, uint64_t n, const uint32_t* assignment,
+                           const int64_t* ids);
+
+/* BIVFSNAP v1 (ivf_index.cpp:515-619; format proj/README.md:132-150) */
+bivf_status bivf_save_snapshot(const bivf_index* h, const char* path);
+/* cfg_override may be NULL; its device / num_leases / max_list_blocks fields apply */
+bivf_status bivf_load_snapshot(const char* path, const bivf_config* cfg_override,
+                               bivf_index** out);
+
+/* ---- the hot path ----------------------------------------------------- */
+/* VectorIndex::insert (vector_index.hpp:25-27, ivf_index.cpp:122-164).
+ * ids NULL -> contiguous auto ids.  out_ids[i] = id or -1 (rejected duplicate
+ * or failed on pool exhaustion).  Returns BIVF_EPOOL with *inserted set when
+ * the pool ran out mid-batch (PoolExhaustedError(inserted)). */
+bivf_status bivf_add(bivf_index* h, const float* x, uint64_t n, const int64_t* ids,
+                     int64_t* out_ids, uint64_t* inserted);
+/* Batched VectorIndex::search (vector_index.hpp:28-29, ivf_index.cpp:262-298):
+ * nq queries, row-major.  out_ids/out_dists are [nq x k]; out_counts[q] =
+ * min(k, scanned); unused tail entries are id -1.  Distances are
+ * bit-identical to l2_sqr_strided (L2) or -<q,x> (IP).  k <= 256, and nprobe
+ * <= 256 or nprobe == num_clusters. */
+bivf_status bivf_search(bivf_index* h, const float* queries, uint64_t nq, uint64_t k,
+                        uint64_t nprobe, int64_t* out_ids, float* out_dists, uint32_t* out_counts);
+/* Same with device-resident inputs/outputs on the caller's CUDA stream
+ * (cudaStream_t passed as void*; NULL = legacy default).  Asynchronous. */
+bivf_status bivf_search_device(bivf_index* h, const float* queries_device, uint64_t nq,
+                               uint64_t k, uint64_t nprobe, int64_t* out_ids_device,
+                               float* out_dists_device, uint32_t* out_counts_device,
+                               void* stream);
+/* ClusterIndex::assign (ivf_index.cpp:93-105) for n vectors */
+bivf_status bivf_assign(bivf_index* h, const float* y, uint64_t n, uint32_t* out);
+/* probe sets (ivf_index.cpp:271-276): out [nq x nprobe] ascending by (key, cluster) */
+bivf_status bivf_probes(bivf_index* h, const float* queries, uint64_t nq, uint64_t nprobe,
+                        uint32_t* out);
+/* Delete (extension; the reference has none; rules in DESIGN.md
+ * §Delete): in request order, fill each hole with the last vector of its part
+ * (offline segment or online list).  found may be NULL. */
+bivf_status bivf_remove(bivf_index* h, const int64_t* ids, uint64_t n, uint64_t* removed,
+                        uint8_t* found);
+
+/* ---- rearrangement (Alg. 3) -------------------------------------------- */
+bivf_status bivf_exceed(const bivf_index* h, uint32_t cluster, int* out);     /* ivf_index.cpp:300-311 */
+bivf_status bivf_rearrange(bivf_index* h, uint32_t cluster);                  /* ivf_index.cpp:476-505 */
+bivf_status bivf_rearrange_sweep(bivf_index* h);                              /* ivf_index.cpp:507-511 */
+/* RearrangeEvent (ivf_index.hpp:33-39): 5 doubles per event (cluster,
+ * hops_before, hops_after, merges, duration_us); returns count via *n */
+bivf_status bivf_take_rearrange_events(bivf_index* h, double* out5, uint64_t cap, uint64_t* n);
+
+/* ---- introspection (ivf_index.hpp:84-103, block_store.hpp:75-132) -------- */
+bivf_status bivf_size(const bivf_index* h, uint64_t* out);
+bivf_status bivf_scalars_copied(const bivf_index* h, uint64_t* out);
+bivf_status bivf_list_length(const bivf_index* h, uint32_t cluster, uint64_t* out);
+bivf_status bivf_offline_count(const bivf_index* h, uint32_t cluster, uint64_t* out);
+bivf_status bivf_hop_count(const bivf_index* h, uint32_t cluster, uint64_t* out);
+bivf_status bivf_online_head(const bivf_index* h, uint32_t cluster, int32_t* out);
+bivf_status bivf_allocated_blocks(const bivf_index* h, uint64_t* out);
+/* header: prev, next, size(committed), owner, merged_with_prev */
+bivf_status bivf_block_header(const bivf_index* h, int32_t block, int32_t* out5);
+bivf_status bivf_block_ids(const bivf_index* h, int32_t block, int64_t* out /* [T_m] */);
+bivf_status bivf_block_payload(const bivf_index* h, int32_t block,
+                               float* out /* [ceil(T_m/32)*32*D] */);
+/* offline then online contents (ivf_index.cpp:505-523); ids NULL -> count only */
+bivf_status bivf_cluster_contents(const bivf_index* h, uint32_t cluster, int64_t* ids,
+                                  float* vecs, uint64_t* count);
+/* dump_pool text (block_store.cpp:188-201); *len = bytes needed incl. NUL */
+bivf_status bivf_dump_pool(const bivf_index* h, char* buf, uint64_t cap, uint64_t* len);
+bivf_status bivf_next_id(const bivf_index* h, int64_t* out);
+
+/* ---- data helpers (either side of the path) ----------------------------- */
+/* synthetic_dataset (dataset.cpp:92-112): same std::mt19937_64 stream, same
+ * libstdc++ distributions -> identical bits to the reference on this image. */
+bivf_status bivf_synthetic_dataset(uint64_t n, uint64_t dim, uint64_t components, uint64_t seed,
+                                   float* out);
+/* k-means (kmeans.cpp:31-142): seeding + assignment sweeps on device, the
+ * double-precision updates on the host in the reference's order. */
+bivf_status bivf_kmeans(const float* points, uint64_t n, uint64_t dim, uint64_t k,
+                        uint64_t max_iters, uint64_t seed, int32_t device, float* centroids,
+                        uint32_t* assignment, uint64_t* iters_run);
+
+/* ---- multi-GPU merge (north star (5)) ------------------------------------ */
+/* Merge G per-shard top-k lists ([G][nq][k], ascending runs, id -1 = empty)
+ * into the global top-k under (dist, id) order — the step after the NCCL
+ * all-gather of per-GPU results.  Device pointers, async on `stream`. */
+bivf_status bivf_merge_topk_device(int32_t device, const float* dists, const int64_t* ids,
+                                   uint64_t G, uint64_t nq, uint64_t k, float* out_dists,
+                                   int64_t* out_ids, uint32_t* out_counts, void* stream);
+
+/* ---- instrumentation ------------------------------------------------------ */
+/* kernel launches issued by this library since load (bench's gpu_launches) */
+uint64_t bivf_kernel_launches(void);
+/* device time (ms) of the last bivf_search's scan kernel, -1 if not timed */
+bivf_status bivf_set_timing(bivf_index* h, int enable);
+bivf_status bivf_last_timings(const bivf_index* h, float* out4 /* quantizer, plan, scan, merge ms */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BIVF_H */

@@ -1,0 +1,1480 @@
+// GpuIndex implementation (see index.h for the ownership / concurrency model).
+#include "index.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <fstream>
+#include <sstream>
+#include <unordered_map>
+
+#include "launches.h"
+#include "maint.cuh"
+
+namespace bivf {
+
+std::atomic<uint64_t> g_launches{0};
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error(BIVF_ECUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+    }
+}
+
+DevBuf::~DevBuf() {
+    if (p) cudaFree(p);
+}
+void DevBuf::alloc(size_t n) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (n == 0) n = 16;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        throw Error(BIVF_ENOMEM, "device allocation of " + std::to_string(n) + " bytes failed: " +
+                                     cudaGetErrorString(e));
+    }
+    bytes = n;
+}
+void DevBuf::ensure(size_t n) {
+    if (n <= bytes && p) return;
+    size_t grow = std::max(n, bytes + bytes / 2);
+    alloc(grow);
+}
+PinBuf::~PinBuf() {
+    if (p) cudaFreeHost(p);
+}
+void PinBuf::ensure(size_t n) {
+    if (n <= bytes && p) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    size_t grow = std::max<size_t>(std::max(n, bytes + bytes / 2), 4096);
+    BIVF_CUDA(cudaHostAlloc(&p, grow, cudaHostAllocDefault));
+    bytes = grow;
+}
+
+namespace {
+
+int log_level() {
+    const char* v = std::getenv("BIVF_LOG");
+    if (!v) v = std::getenv("BLOCKIVF_LOG");  // log.hpp:9-20
+    if (!v) return 1;
+    std::string s(v);
+    if (s == "quiet") return 0;
+    if (s == "info") return 2;
+    if (s == "debug") return 3;
+    return 1;
+}
+
+void log_warn(const std::string& m) {
+    if (log_level() >= 1) std::fprintf(stderr, "[bivf] %s\n", m.c_str());
+}
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+uint32_t ceil_div(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
+
+bivf_config normalized(bivf_config c) {
+    if (c.num_clusters == 0) c.num_clusters = 100;
+    if (c.nprobe_default == 0) c.nprobe_default = std::min<uint64_t>(8, c.num_clusters);
+    if (c.rearrange_threshold == 0) c.rearrange_threshold = 256;
+    if (c.kmeans_iters == 0) c.kmeans_iters = 25;
+    if (c.kmeans_seed == 0 && !c.kmeans_seed_set) c.kmeans_seed = 42;
+    if (c.num_blocks == 0) c.num_blocks = 1024;
+    if (c.block_capacity == 0) c.block_capacity = 64;
+    if (c.alert_watermark == 0.0) c.alert_watermark = 0.9;
+    if (c.num_leases == 0) c.num_leases = 32;
+    if (c.max_list_blocks == 0) c.max_list_blocks = (uint32_t)c.num_blocks;
+    return c;
+}
+
+// IndexConfig::validate + PoolConfig::validate (ivf_index.cpp:28-35, block_store.cpp:9-17)
+void validate(const bivf_config& c) {
+    if (c.dim < 1) throw Error(BIVF_EINVAL, "PoolConfig: dim must be >= 1");
+    if (c.num_clusters < 1) throw Error(BIVF_EINVAL, "IndexConfig: num_clusters must be >= 1");
+    if (c.nprobe_default < 1 || c.nprobe_default > c.num_clusters)
+        throw Error(BIVF_EINVAL, "IndexConfig: nprobe_default out of [1, num_clusters]");
+    if (c.alert_watermark <= 0.0 || c.alert_watermark > 1.0)
+        throw Error(BIVF_EINVAL, "PoolConfig: alert_watermark must be in (0, 1]");
+    if (c.metric != BIVF_METRIC_L2 && c.metric != BIVF_METRIC_IP)
+        throw Error(BIVF_EINVAL, "metric must be BIVF_METRIC_L2 or BIVF_METRIC_IP");
+    if (c.num_blocks > 0x7fffffffull) throw Error(BIVF_EINVAL, "num_blocks exceeds int32 block ids");
+    if (c.dim > 65536) throw Error(BIVF_EINVAL, "dim above 65536 is not supported");
+}
+
+}  // namespace
+
+// ========================================================================
+// construction
+// ========================================================================
+
+GpuIndex::GpuIndex(const bivf_config& in) : cfg_(normalized(in)) {
+    validate(cfg_);
+    C_ = (uint32_t)cfg_.num_clusters;
+    D_ = (uint32_t)cfg_.dim;
+    Dp_ = pad4(D_);
+    T_ = (uint32_t)cfg_.block_capacity;
+    gpb_ = ceil_div(T_, 32);
+    PS_ = (uint64_t)gpb_ * 32u * D_;
+    NB_ = (uint32_t)cfg_.num_blocks;
+    MLB_ = std::min<uint32_t>(cfg_.max_list_blocks, NB_);
+    device_ = cfg_.device;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        throw Error(BIVF_ECUDA, "no CUDA device visible: the B200 path has no CPU fallback");
+    }
+    if (device_ < 0 || device_ >= ndev) throw Error(BIVF_EINVAL, "device ordinal out of range");
+    BIVF_CUDA(cudaSetDevice(device_));
+    BIVF_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device_));
+    alloc_device();
+    BIVF_CUDA(cudaStreamCreateWithFlags(&data_stream_, cudaStreamNonBlocking));
+    BIVF_CUDA(cudaEventCreateWithFlags(&maint_evt_, cudaEventDisableTiming));
+    for (uint32_t i = 0; i < cfg_.num_leases; ++i) {
+        auto l = std::make_unique<Lease>();
+        l->id = (int)i;
+        leases_.push_back(std::move(l));
+    }
+    h_len_.assign(C_, 0);
+    h_off_count_.assign(C_, 0);
+    h_nblocks_.assign(C_, 0);
+    h_off_start_.assign(C_, 0);
+    h_head_.assign(C_, -1);
+    h_tail_.assign(C_, -1);
+    h_blocks_.assign(C_, {});
+    h_prev_.assign(NB_, -1);
+    h_next_.assign(NB_, -1);
+    h_owner_.assign(NB_, -1);
+    h_mid_.assign(NB_, -1);
+    h_merged_.assign(NB_, 0);
+}
+
+GpuIndex::~GpuIndex() {
+    cudaSetDevice(device_);
+    cudaDeviceSynchronize();
+    for (auto& l : leases_) {
+        if (l->stream) cudaStreamDestroy(l->stream);
+        for (cudaEvent_t e : {l->done, l->t0, l->t1, l->t2, l->t3, l->t4})
+            if (e) cudaEventDestroy(e);
+    }
+    if (data_stream_) cudaStreamDestroy(data_stream_);
+    if (maint_evt_) cudaEventDestroy(maint_evt_);
+}
+
+void GpuIndex::alloc_device() {
+    // block_store.cpp:19-29: whole arena reserved and zero-filled up front,
+    // ids -1; here in HBM.
+    d_cent_.alloc((size_t)C_ * D_ * 4);
+    d_cent_il_.alloc((size_t)ceil_div(C_, 32) * 32 * D_ * 4);
+    BIVF_CUDA(cudaMemset(d_cent_.p, 0, d_cent_.bytes));
+    BIVF_CUDA(cudaMemset(d_cent_il_.p, 0, d_cent_il_.bytes));
+    d_off_start_.alloc((size_t)C_ * 8);
+    d_off_count_.alloc((size_t)C_ * 4);
+    BIVF_CUDA(cudaMemset(d_off_start_.p, 0, d_off_start_.bytes));
+    BIVF_CUDA(cudaMemset(d_off_count_.p, 0, d_off_count_.bytes));
+    ensure_offline_capacity(32);
+    d_arena_.alloc((size_t)NB_ * PS_ * 4);
+    BIVF_CUDA(cudaMemset(d_arena_.p, 0, d_arena_.bytes));
+    d_bids_.alloc((size_t)NB_ * T_ * 8);
+    BIVF_CUDA(cudaMemset(d_bids_.p, 0xff, d_bids_.bytes));
+    d_owner_.alloc((size_t)NB_ * 4);
+    BIVF_CUDA(cudaMemset(d_owner_.p, 0xff, d_owner_.bytes));
+    d_cursor_.alloc(16);
+    BIVF_CUDA(cudaMemset(d_cursor_.p, 0, 16));
+    d_len_.alloc((size_t)C_ * 4);
+    d_nblocks_.alloc((size_t)C_ * 4);
+    d_fail_.alloc((size_t)C_);
+    d_table_.alloc((size_t)C_ * MLB_ * 4);
+    BIVF_CUDA(cudaMemset(d_len_.p, 0, d_len_.bytes));
+    BIVF_CUDA(cudaMemset(d_nblocks_.p, 0, d_nblocks_.bytes));
+    BIVF_CUDA(cudaMemset(d_fail_.p, 0, d_fail_.bytes));
+    BIVF_CUDA(cudaMemset(d_table_.p, 0xff, d_table_.bytes));
+    d_run_.alloc((size_t)C_ * 4);
+    d_failfrom_.alloc((size_t)C_ * 4);
+    d_newlen_.alloc((size_t)C_ * 4);
+    d_ctr_.alloc(16);
+    BIVF_CUDA(cudaDeviceSynchronize());
+}
+
+void GpuIndex::ensure_offline_capacity(uint64_t slots) {
+    slots = std::max<uint64_t>(32, (slots + 31) / 32 * 32);
+    if (slots <= off_slots_cap_) return;
+    d_off_pay_.alloc((size_t)slots * D_ * 4);
+    d_off_ids_.alloc((size_t)slots * 8);
+    BIVF_CUDA(cudaMemset(d_off_pay_.p, 0, d_off_pay_.bytes));
+    BIVF_CUDA(cudaMemset(d_off_ids_.p, 0xff, d_off_ids_.bytes));
+    off_slots_cap_ = slots;
+}
+
+DevLists GpuIndex::dev_lists() const {
+    DevLists L;
+    L.C = C_;
+    L.D = D_;
+    L.T = T_;
+    L.gpb = gpb_;
+    L.PS = PS_;
+    L.MLB = MLB_;
+    L.off_payload = d_off_pay_.as<float>();
+    L.off_ids = d_off_ids_.as<long long>();
+    L.off_start = d_off_start_.as<uint64_t>();
+    L.off_count = d_off_count_.as<uint32_t>();
+    L.arena = d_arena_.as<float>();
+    L.bids = d_bids_.as<long long>();
+    L.table = d_table_.as<int32_t>();
+    L.len = d_len_.as<uint32_t>();
+    return L;
+}
+
+InsertState GpuIndex::insert_state() {
+    InsertState S;
+    S.C = C_;
+    S.D = D_;
+    S.T = T_;
+    S.MLB = MLB_;
+    S.num_blocks = NB_;
+    S.PS = PS_;
+    S.arena = d_arena_.as<float>();
+    S.bids = d_bids_.as<long long>();
+    S.owner = d_owner_.as<int32_t>();
+    S.cursor = d_cursor_.as<uint32_t>();
+    S.len = d_len_.as<uint32_t>();
+    S.nblocks = d_nblocks_.as<uint32_t>();
+    S.fail = d_fail_.as<uint8_t>();
+    S.table = d_table_.as<int32_t>();
+    S.run = d_run_.as<uint32_t>();
+    S.fail_from = d_failfrom_.as<uint32_t>();
+    S.newlen = d_newlen_.as<uint32_t>();
+    return S;
+}
+
+// ========================================================================
+// centroids, training, bulk load
+// ========================================================================
+
+void GpuIndex::upload_centroids() {
+    // row-major copy (interchange) + interleaved copy (quantizer scan source)
+    BIVF_CUDA(launch_interleave(d_cent_.as<float>(), C_, D_, d_cent_il_.as<float>(), data_stream_));
+    BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+}
+
+void GpuIndex::set_centroids(const float* c) {
+    std::lock_guard<std::mutex> lk(data_mu_);
+    BIVF_CUDA(cudaSetDevice(device_));
+    BIVF_CUDA(cudaMemcpy(d_cent_.p, c, (size_t)C_ * D_ * 4, cudaMemcpyHostToDevice));
+    upload_centroids();
+    trained_ = true;
+}
+
+void GpuIndex::get_centroids(float* out) const {
+    BIVF_CUDA(cudaSetDevice(device_));
+    BIVF_CUDA(cudaMemcpy(out, d_cent_.p, (size_t)C_ * D_ * 4, cudaMemcpyDeviceToHost));
+}
+
+void GpuIndex::train(const float* x, uint64_t n) {
+    // ivf_index.cpp:47-59
+    if (n < C_) throw Error(BIVF_EINVAL, "train: need at least num_clusters offline vectors");
+    std::vector<float> cent((size_t)C_ * D_);
+    std::vector<uint32_t> asg(n);
+    kmeans_gpu(x, n, D_, C_, cfg_.kmeans_iters, cfg_.kmeans_seed, device_, cent.data(),
+               asg.data());
+    set_centroids(cent.data());
+    bulk_load(x, n, asg.data(), nullptr);
+}
+
+void GpuIndex::bulk_load(const float* x, uint64_t n, const uint32_t* assignment,
+                         const int64_t* ids) {
+    std::vector<uint32_t> asg_local;
+    if (!assignment) {
+        if (!trained_) throw Error(BIVF_ELOGIC, "bulk_load: index has no centroids");
+        asg_local.resize(n);
+        assign(x, n, asg_local.data());
+        assignment = asg_local.data();
+    }
+    std::lock_guard<std::mutex> lk(data_mu_);
+    BIVF_CUDA(cudaSetDevice(device_));
+    // ivf_index.cpp:61-82: per-cluster counts; rows appended in ascending row
+    // order; each segment padded to whole groups.
+    std::vector<uint64_t> counts(C_, 0);
+    for (uint64_t i = 0; i < n; ++i) {
+        if (assignment[i] >= C_) throw Error(BIVF_EINVAL, "bulk_load: assignment out of range");
+        counts[assignment[i]]++;
+    }
+    for (uint32_t c = 0; c < C_; ++c)
+        if (counts[c] > 0xffffffffull) throw Error(BIVF_EINVAL, "bulk_load: list too long");
+    uint64_t total = 0;
+    for (uint32_t c = 0; c < C_; ++c) {
+        h_off_start_[c] = total;
+        total += (counts[c] + 31) / 32 * 32;
+    }
+    ensure_offline_capacity(total);
+    BIVF_CUDA(cudaMemset(d_off_ids_.p, 0xff, d_off_ids_.bytes));
+    std::vector<uint64_t> fill(C_, 0);
+    const uint64_t chunk = 1ull << 20;
+    DevBuf dx, ddest, dids;
+    PinBuf pin;
+    std::vector<uint64_t> dest;
+    std::vector<long long> idv;
+    for (uint64_t s = 0; s < n; s += chunk) {
+        const uint64_t m = std::min(chunk, n - s);
+        dest.resize(m);
+        idv.resize(m);
+        for (uint64_t i = 0; i < m; ++i) {
+            const uint32_t c = assignment[s + i];
+            dest[i] = h_off_start_[c] + fill[c]++;
+            idv[i] = ids ? ids[s + i] : (long long)(s + i);
+        }
+        dx.ensure(m * D_ * 4);
+        ddest.ensure(m * 8);
+        dids.ensure(m * 8);
+        BIVF_CUDA(cudaMemcpy(dx.p, x + s * D_, m * D_ * 4, cudaMemcpyHostToDevice));
+        BIVF_CUDA(cudaMemcpy(ddest.p, dest.data(), m * 8, cudaMemcpyHostToDevice));
+        BIVF_CUDA(cudaMemcpy(dids.p, idv.data(), m * 8, cudaMemcpyHostToDevice));
+        BIVF_CUDA(launch_scatter_rows(dx.as<float>(), (uint32_t)m, D_, ddest.as<uint64_t>(),
+                                      dids.as<long long>(), d_off_pay_.as<float>(),
+                                      d_off_ids_.as<long long>(), data_stream_));
+        BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+    }
+    for (uint32_t c = 0; c < C_; ++c) h_off_count_[c] = (uint32_t)counts[c];
+    BIVF_CUDA(cudaMemcpy(d_off_start_.p, h_off_start_.data(), (size_t)C_ * 8,
+                         cudaMemcpyHostToDevice));
+    BIVF_CUDA(cudaMemcpy(d_off_count_.p, h_off_count_.data(), (size_t)C_ * 4,
+                         cudaMemcpyHostToDevice));
+    if (ids) {
+        int64_t mx = -1;
+        for (uint64_t i = 0; i < n; ++i) {
+            supplied_.insert(ids[i]);
+            mx = std::max<int64_t>(mx, ids[i]);
+        }
+        next_id_ = std::max<int64_t>(next_id_, mx + 1);
+    } else {
+        next_id_ = (int64_t)n;
+        offline_end_ = (int64_t)n;
+    }
+}
+
+// ========================================================================
+// leases
+// ========================================================================
+
+Lease* GpuIndex::acquire_lease() {
+    std::unique_lock<std::mutex> lk(lease_mu_);
+    for (;;) {
+        for (auto& l : leases_) {
+            if (!l->busy) {
+                l->busy = true;
+                if (!l->stream) {
+                    BIVF_CUDA(cudaSetDevice(device_));
+                    BIVF_CUDA(cudaStreamCreateWithFlags(&l->stream, cudaStreamNonBlocking));
+                    BIVF_CUDA(cudaEventCreateWithFlags(&l->done, cudaEventDisableTiming));
+                    for (cudaEvent_t* e : {&l->t0, &l->t1, &l->t2, &l->t3, &l->t4})
+                        BIVF_CUDA(cudaEventCreate(e));
+                }
+                return l.get();
+            }
+        }
+        lease_cv_.wait(lk);
+    }
+}
+
+void GpuIndex::release_lease(Lease* l) {
+    {
+        std::lock_guard<std::mutex> lk(lease_mu_);
+        l->busy = false;
+    }
+    lease_cv_.notify_one();
+}
+
+Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_t maxch,
+                          uint32_t fnch) {
+    const uint64_t npairs = (uint64_t)nq * P;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += align_up(bytes);
+        return o;
+    };
+    const size_t o_qraw = take((size_t)nq * D_ * 4);
+    const size_t o_q = take((size_t)nq * Dp_ * 4);
+    const size_t o_probes = take(npairs * 8);
+    const size_t o_pdist = take(npairs * 4);
+    const size_t ncf = (size_t)nq * fnch * P;
+    const size_t o_fcd = take(ncf * 4);
+    const size_t o_fci = take(ncf * 8);
+    const size_t ncand = npairs * maxch * k;
+    const size_t o_cd = take(ncand * 4);
+    const size_t o_ci = take(ncand * 8);
+    const size_t o_od = take((size_t)nq * k * 4);
+    const size_t o_oi = take((size_t)nq * k * 8);
+    const size_t o_oc = take((size_t)nq * 4);
+    const size_t o_ctr = take(16);
+    const size_t o_plan = take((size_t)C_ * 4 * 5 + (size_t)(C_ + 1) * 4 * 2 + 16);
+    const size_t o_ppos = take(npairs * 4);
+    const size_t o_plist = take(npairs * 4);
+    l.ws.ensure(off);
+    char* b = static_cast<char*>(l.ws.p);
+    Workspace w;
+    w.qraw = reinterpret_cast<float*>(b + o_qraw);
+    w.queries = reinterpret_cast<float*>(b + o_q);
+    w.probes = reinterpret_cast<long long*>(b + o_probes);
+    w.pdist = reinterpret_cast<float*>(b + o_pdist);
+    w.fcand_d = reinterpret_cast<float*>(b + o_fcd);
+    w.fcand_i = reinterpret_cast<long long*>(b + o_fci);
+    w.cand_d = reinterpret_cast<float*>(b + o_cd);
+    w.cand_i = reinterpret_cast<long long*>(b + o_ci);
+    w.out_d = reinterpret_cast<float*>(b + o_od);
+    w.out_i = reinterpret_cast<long long*>(b + o_oi);
+    w.out_cnt = reinterpret_cast<uint32_t*>(b + o_oc);
+    w.ctr = reinterpret_cast<uint32_t*>(b + o_ctr);
+    uint32_t* pl = reinterpret_cast<uint32_t*>(b + o_plan);
+    w.plan.snap_off = pl;
+    w.plan.snap_len = pl + C_;
+    w.plan.gc = pl + 2 * C_;
+    w.plan.nch = pl + 3 * C_;
+    w.plan.cnt = pl + 4 * C_;
+    w.plan.qoff = pl + 5 * C_;
+    w.plan.item_off = pl + 6 * C_ + 1;
+    w.plan.n_items = pl + 7 * C_ + 2;
+    w.plan.item_ctr = pl + 7 * C_ + 3;
+    w.plan.ppos = reinterpret_cast<uint32_t*>(b + o_ppos);
+    w.plan.plist = reinterpret_cast<uint32_t*>(b + o_plist);
+    return w;
+}
+
+namespace {
+struct LaunchShape {
+    uint32_t maxch, gcmin, fnch;
+};
+LaunchShape pick_shape(uint32_t nq, uint32_t k, uint32_t P, uint32_t C, int sms) {
+    LaunchShape s;
+    const uint64_t target = (uint64_t)sms * 8;
+    const uint64_t npairs = (uint64_t)nq * P;
+    s.maxch = (uint32_t)std::min<uint64_t>(32, std::max<uint64_t>(1, (target + npairs - 1) / npairs));
+    s.gcmin = 2;
+    const uint32_t qtq = qt_for(P, 0);
+    const uint64_t tiles = (nq + qtq - 1) / qtq;
+    const uint32_t ng = (C + 31) / 32;
+    s.fnch = (uint32_t)std::min<uint64_t>(ng, std::max<uint64_t>(1, (target + tiles - 1) / tiles));
+    (void)k;
+    return s;
+}
+}  // namespace
+
+void GpuIndex::validate_search(uint64_t k, uint64_t nprobe) const {
+    // ivf_index.cpp:266-269
+    if (k < 1) throw Error(BIVF_EINVAL, "search: k must be >= 1");
+    if (nprobe < 1 || nprobe > C_) throw Error(BIVF_EINVAL, "search: nprobe out of [1, num_clusters]");
+    if (k > 256) throw Error(BIVF_EINVAL, "search: k above the device top-k capacity (256)");
+    if (nprobe > 256 && nprobe != C_)
+        throw Error(BIVF_EINVAL, "search: nprobe must be <= 256 or == num_clusters");
+    if (!trained_) throw Error(BIVF_ELOGIC, "search: index has no centroids");
+}
+
+// Enqueue one search slice on the lease stream: pad -> quantizer -> plan ->
+// scan -> merge.  Caller holds gate_ shared.
+void GpuIndex::enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uint32_t k,
+                              uint32_t P, Workspace& w) {
+    const LaunchShape sh = pick_shape(nq, k, P, C_, num_sms_);
+    if (timing_) BIVF_CUDA(cudaEventRecord(l.t0, l.stream));
+    BIVF_CUDA(launch_pad_rows(q_dev_raw, nq, D_, Dp_, w.queries, l.stream));
+    if (P == C_) {
+        BIVF_CUDA(launch_all_probes(w.probes, nq, C_, l.stream));
+    } else {
+        BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, w.queries, nq, P, cfg_.metric,
+                                   sh.fnch, w.fcand_d, w.fcand_i, w.pdist, w.probes, nullptr,
+                                   w.ctr, num_sms_, l.stream));
+    }
+    if (timing_) BIVF_CUDA(cudaEventRecord(l.t1, l.stream));
+    SearchShape ss;
+    ss.nq = nq;
+    ss.k = k;
+    ss.P = P;
+    ss.maxch = sh.maxch;
+    ss.gcmin = sh.gcmin;
+    ss.QT = qt_for(k, D_);
+    ss.metric = cfg_.metric;
+    BIVF_CUDA(launch_ivf_search(dev_lists(), w.plan, w.probes, w.queries, ss, w.cand_d, w.cand_i,
+                                w.out_d, w.out_i, w.out_cnt, num_sms_, l.stream));
+    if (timing_) BIVF_CUDA(cudaEventRecord(l.t4, l.stream));
+}
+
+void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, int64_t* out_ids,
+                      float* out_d, uint32_t* out_cnt) {
+    validate_search(k, nprobe);
+    if (nq == 0) return;
+    BIVF_CUDA(cudaSetDevice(device_));
+    Lease* l = acquire_lease();
+    struct Rel {
+        GpuIndex* g;
+        Lease* l;
+        ~Rel() { g->release_lease(l); }
+    } rel{this, l};
+    const uint64_t slice = 32768;
+    for (uint64_t s = 0; s < nq; s += slice) {
+        const uint32_t m = (uint32_t)std::min(slice, nq - s);
+        const LaunchShape sh = pick_shape(m, (uint32_t)k, (uint32_t)nprobe, C_, num_sms_);
+        Workspace w = carve(*l, m, (uint32_t)k, (uint32_t)nprobe, sh.maxch, sh.fnch);
+        const size_t in_b = (size_t)m * D_ * 4;
+        const size_t out_b = (size_t)m * k * 12 + (size_t)m * 4;
+        l->pin.ensure(in_b + out_b + 256);
+        char* pin = l->pin.as<char>();
+        std::memcpy(pin, q + s * D_, in_b);
+        float* pd = reinterpret_cast<float*>(pin + align_up(in_b, 64));
+        long long* pi = reinterpret_cast<long long*>(pd + (size_t)m * k + ((m * k) & 1));
+        uint32_t* pc = reinterpret_cast<uint32_t*>(pi + (size_t)m * k);
+        {
+            std::shared_lock<std::shared_mutex> g(gate_);
+            const uint64_t gen = maint_gen_.load();
+            if (l->seen_maint != gen) {
+                BIVF_CUDA(cudaStreamWaitEvent(l->stream, maint_evt_, 0));
+                l->seen_maint = gen;
+            }
+            BIVF_CUDA(cudaMemcpyAsync(w.qraw, pin, in_b, cudaMemcpyHostToDevice, l->stream));
+            enqueue_search(*l, w.qraw, m, (uint32_t)k, (uint32_t)nprobe, w);
+            BIVF_CUDA(cudaMemcpyAsync(pd, w.out_d, (size_t)m * k * 4, cudaMemcpyDeviceToHost, l->stream));
+            BIVF_CUDA(cudaMemcpyAsync(pi, w.out_i, (size_t)m * k * 8, cudaMemcpyDeviceToHost, l->stream));
+            BIVF_CUDA(cudaMemcpyAsync(pc, w.out_cnt, (size_t)m * 4, cudaMemcpyDeviceToHost, l->stream));
+            BIVF_CUDA(cudaEventRecord(l->done, l->stream));
+        }
+        BIVF_CUDA(cudaEventSynchronize(l->done));
+        std::memcpy(out_d + s * k, pd, (size_t)m * k * 4);
+        std::memcpy(out_ids + s * k, pi, (size_t)m * k * 8);
+        if (out_cnt) std::memcpy(out_cnt + s, pc, (size_t)m * 4);
+        if (timing_) {
+            cudaEventElapsedTime(&last_ms_[0], l->t0, l->t1);
+            cudaEventElapsedTime(&last_ms_[2], l->t1, l->t4);
+            last_ms_[1] = 0;
+            last_ms_[3] = 0;
+        }
+    }
+}
+
+void GpuIndex::search_device(const float* q_dev, uint64_t nq, uint64_t k, uint64_t nprobe,
+                             int64_t* ids_dev, float* d_dev, uint32_t* cnt_dev,
+                             cudaStream_t user) {
+    validate_search(k, nprobe);
+    if (nq == 0) return;
+    if (nq > 0xffffffffull / std::max<uint64_t>(1, nprobe))
+        throw Error(BIVF_EINVAL, "search_device: nq * nprobe too large for one call");
+    BIVF_CUDA(cudaSetDevice(device_));
+    Lease* l = acquire_lease();
+    struct Rel {
+        GpuIndex* g;
+        Lease* l;
+        ~Rel() { g->release_lease(l); }
+    } rel{this, l};
+    const uint32_t m = (uint32_t)nq;
+    const LaunchShape sh = pick_shape(m, (uint32_t)k, (uint32_t)nprobe, C_, num_sms_);
+    Workspace w = carve(*l, m, (uint32_t)k, (uint32_t)nprobe, sh.maxch, sh.fnch);
+    cudaEvent_t ue;
+    BIVF_CUDA(cudaEventCreateWithFlags(&ue, cudaEventDisableTiming));
+    BIVF_CUDA(cudaEventRecord(ue, user));
+    {
+        std::shared_lock<std::shared_mutex> g(gate_);
+        const uint64_t gen = maint_gen_.load();
+        if (l->seen_maint != gen) {
+            BIVF_CUDA(cudaStreamWaitEvent(l->stream, maint_evt_, 0));
+            l->seen_maint = gen;
+        }
+        BIVF_CUDA(cudaStreamWaitEvent(l->stream, ue, 0));
+        w.out_d = d_dev;
+        w.out_i = reinterpret_cast<long long*>(ids_dev);
+        w.out_cnt = cnt_dev;
+        enqueue_search(*l, q_dev, m, (uint32_t)k, (uint32_t)nprobe, w);
+        BIVF_CUDA(cudaEventRecord(l->done, l->stream));
+    }
+    BIVF_CUDA(cudaStreamWaitEvent(user, l->done, 0));
+    cudaEventDestroy(ue);
+    // the lease workspace is reused by the next caller only after `done`
+    BIVF_CUDA(cudaEventSynchronize(l->done));
+    if (timing_) {
+        cudaEventElapsedTime(&last_ms_[0], l->t0, l->t1);
+        cudaEventElapsedTime(&last_ms_[2], l->t1, l->t4);
+    }
+}
+
+void GpuIndex::last_timings(float* out4) const {
+    for (int i = 0; i < 4; ++i) out4[i] = last_ms_[i];
+}
+
+void GpuIndex::assign(const float* y, uint64_t n, uint32_t* out) {
+    if (!trained_) throw Error(BIVF_ELOGIC, "assign: index has no centroids");
+    if (n == 0) return;
+    probes(y, n, 1, out);
+}
+
+void GpuIndex::probes(const float* q, uint64_t nq, uint64_t nprobe, uint32_t* out) {
+    if (nprobe < 1 || nprobe > C_) throw Error(BIVF_EINVAL, "probes: nprobe out of [1, num_clusters]");
+    if (nprobe > 256 && nprobe != C_) throw Error(BIVF_EINVAL, "probes: nprobe must be <= 256 or == num_clusters");
+    if (!trained_) throw Error(BIVF_ELOGIC, "probes: index has no centroids");
+    if (nq == 0) return;
+    BIVF_CUDA(cudaSetDevice(device_));
+    Lease* l = acquire_lease();
+    struct Rel {
+        GpuIndex* g;
+        Lease* l;
+        ~Rel() { g->release_lease(l); }
+    } rel{this, l};
+    const uint64_t slice = 65536;
+    std::vector<long long> tmp;
+    for (uint64_t s = 0; s < nq; s += slice) {
+        const uint32_t m = (uint32_t)std::min(slice, nq - s);
+        const LaunchShape sh = pick_shape(m, 1, (uint32_t)nprobe, C_, num_sms_);
+        Workspace w = carve(*l, m, 1, (uint32_t)nprobe, 1, sh.fnch);
+        tmp.resize((size_t)m * nprobe);
+        BIVF_CUDA(cudaMemcpyAsync(w.qraw, q + s * D_, (size_t)m * D_ * 4, cudaMemcpyHostToDevice,
+                                  l->stream));
+        BIVF_CUDA(launch_pad_rows(w.qraw, m, D_, Dp_, w.queries, l->stream));
+        if (nprobe == C_) {
+            BIVF_CUDA(launch_all_probes(w.probes, m, C_, l->stream));
+        } else {
+            BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, w.queries, m,
+                                       (uint32_t)nprobe, cfg_.metric, sh.fnch, w.fcand_d,
+                                       w.fcand_i, w.pdist, w.probes, nullptr, w.ctr, num_sms_,
+                                       l->stream));
+        }
+        BIVF_CUDA(cudaMemcpyAsync(tmp.data(), w.probes, tmp.size() * 8, cudaMemcpyDeviceToHost,
+                                  l->stream));
+        BIVF_CUDA(cudaStreamSynchronize(l->stream));
+        for (size_t i = 0; i < tmp.size(); ++i) out[s * nprobe + i] = (uint32_t)tmp[i];
+    }
+}
+
+// ========================================================================
+// insert (ivf_index.cpp:107-164)
+// ========================================================================
+
+bool GpuIndex::is_duplicate_id(int64_t id) {
+    if (id < 0) return true;
+    if (id < offline_end_) return true;
+    for (const auto& r : auto_ranges_)
+        if (id >= r.first && id < r.second) return true;
+    if (!supplied_.insert(id).second) return true;
+    if (id >= next_id_) next_id_ = id + 1;
+    return false;
+}
+
+void GpuIndex::absorb_new_blocks(uint32_t cursor_old, uint32_t cursor_new) {
+    if (cursor_new <= cursor_old) return;
+    std::vector<int32_t> own(cursor_new - cursor_old);
+    BIVF_CUDA(cudaMemcpy(own.data(), d_owner_.as<int32_t>() + cursor_old, own.size() * 4,
+                         cudaMemcpyDeviceToHost));
+    // Blocks are handed out in batch order, which is each list's logical
+    // order: append = link after the tail (block_store.cpp:55-65).
+    for (uint32_t b = cursor_old; b < cursor_new; ++b) {
+        const int32_t c = own[b - cursor_old];
+        if (c < 0 || (uint32_t)c >= C_) throw Error(BIVF_ECORRUPT, "insert: new block without owner");
+        h_owner_[b] = c;
+        h_mid_[b] = (int32_t)h_blocks_[c].size();
+        const int32_t t = h_tail_[c];
+        h_prev_[b] = t;
+        h_next_[b] = -1;
+        h_merged_[b] = 0;
+        if (t >= 0) h_next_[t] = (int32_t)b;
+        else h_head_[c] = (int32_t)b;
+        h_tail_[c] = (int32_t)b;
+        h_blocks_[c].push_back((int32_t)b);
+        h_nblocks_[c] = (uint32_t)h_blocks_[c].size();
+    }
+    h_cursor_ = cursor_new;
+    // one-shot utilization alert (block_store.cpp:41-46)
+    if (!alert_fired_ && (double)h_cursor_ / (double)NB_ > cfg_.alert_watermark) {
+        alert_fired_ = true;
+        log_warn("central pool utilization " + std::to_string(h_cursor_) + "/" +
+                 std::to_string(NB_) + " exceeds watermark");
+    }
+}
+
+void GpuIndex::refresh_lengths() {
+    BIVF_CUDA(cudaMemcpy(h_len_.data(), d_len_.p, (size_t)C_ * 4, cudaMemcpyDeviceToHost));
+}
+
+uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_t* out_ids) {
+    for (uint64_t i = 0; i < n; ++i) out_ids[i] = -1;
+    if (n == 0) return 0;
+    if (!trained_) throw Error(BIVF_ELOGIC, "insert: index has no centroids");
+    std::lock_guard<std::mutex> lk(data_mu_);
+    BIVF_CUDA(cudaSetDevice(device_));
+    // ids: contiguous auto range, or supplied ids checked in batch order
+    std::vector<long long> idv(n);
+    if (!ids) {
+        const int64_t base = next_id_;
+        next_id_ += (int64_t)n;
+        if (!auto_ranges_.empty() && auto_ranges_.back().second == base)
+            auto_ranges_.back().second = base + (int64_t)n;
+        else
+            auto_ranges_.emplace_back(base, base + (int64_t)n);
+        for (uint64_t i = 0; i < n; ++i) idv[i] = base + (int64_t)i;
+    } else {
+        for (uint64_t i = 0; i < n; ++i) idv[i] = is_duplicate_id(ids[i]) ? -1 : ids[i];
+    }
+    uint64_t inserted = 0;
+    bool exhausted = false;
+    const uint64_t chunk = 1ull << 18;
+    std::vector<int32_t> blk;
+    for (uint64_t s = 0; s < n; s += chunk) {
+        const uint32_t m = (uint32_t)std::min(chunk, n - s);
+        d_x_.ensure((size_t)m * D_ * 4);
+        d_qtmp_.ensure((size_t)m * Dp_ * 4);
+        d_ids_.ensure((size_t)m * 8);
+        d_asg_.ensure((size_t)m * 4);
+        d_blk_.ensure((size_t)m * 4);
+        d_did_.ensure((size_t)m * 4);
+        const LaunchShape sh = pick_shape(m, 1, 1, C_, num_sms_);
+        d_fc_d_.ensure((size_t)m * sh.fnch * 4);
+        d_fc_i_.ensure((size_t)m * sh.fnch * 8);
+        d_fo_i_.ensure((size_t)m * 8);
+        d_fo_d_.ensure((size_t)m * 4);
+        h_stage_.ensure((size_t)m * D_ * 4 + (size_t)m * 8 + 64);
+        float* px = h_stage_.as<float>();
+        std::memcpy(px, x + s * D_, (size_t)m * D_ * 4);
+        long long* pid = reinterpret_cast<long long*>(h_stage_.as<char>() + align_up((size_t)m * D_ * 4, 64));
+        std::memcpy(pid, idv.data() + s, (size_t)m * 8);
+        cudaStream_t st = data_stream_;
+        BIVF_CUDA(cudaMemcpyAsync(d_x_.p, px, (size_t)m * D_ * 4, cudaMemcpyHostToDevice, st));
+        BIVF_CUDA(cudaMemcpyAsync(d_ids_.p, pid, (size_t)m * 8, cudaMemcpyHostToDevice, st));
+        // assign (ivf_index.cpp:93-105) = quantizer top-1 on device
+        BIVF_CUDA(launch_pad_rows(d_x_.as<float>(), m, D_, Dp_, d_qtmp_.as<float>(), st));
+        BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, d_qtmp_.as<float>(), m, 1,
+                                   cfg_.metric, sh.fnch, d_fc_d_.as<float>(),
+                                   d_fc_i_.as<long long>(), d_fo_d_.as<float>(),
+                                   d_fo_i_.as<long long>(), nullptr, d_ctr_.as<uint32_t>(),
+                                   num_sms_, st));
+        BIVF_CUDA(launch_make_asg(d_fo_i_.as<long long>(), d_ids_.as<long long>(), m,
+                                  d_asg_.as<uint32_t>(), st));
+        const uint32_t cursor_old = h_cursor_;
+        BIVF_CUDA(launch_insert(insert_state(), m, d_x_.as<float>(), d_ids_.as<long long>(),
+                                d_asg_.as<uint32_t>(), d_blk_.as<int32_t>(),
+                                d_did_.as<uint32_t>(), st));
+        blk.resize(m);
+        uint32_t cursor_new = 0;
+        BIVF_CUDA(cudaMemcpyAsync(blk.data(), d_blk_.p, (size_t)m * 4, cudaMemcpyDeviceToHost, st));
+        BIVF_CUDA(cudaMemcpyAsync(h_len_.data(), d_len_.p, (size_t)C_ * 4, cudaMemcpyDeviceToHost, st));
+        BIVF_CUDA(cudaMemcpyAsync(&cursor_new, d_cursor_.p, 4, cudaMemcpyDeviceToHost, st));
+        BIVF_CUDA(cudaStreamSynchronize(st));
+        absorb_new_blocks(cursor_old, cursor_new);
+        for (uint32_t i = 0; i < m; ++i) {
+            if (idv[s + i] < 0) continue;  // rejected duplicate
+            if (blk[i] >= 0) {
+                out_ids[s + i] = idv[s + i];
+                ++inserted;
+            } else {
+                exhausted = true;
+            }
+        }
+    }
+    scalars_copied_ += inserted * D_;
+    if (exhausted) {
+        Error e(BIVF_EPOOL, "central memory pool exhausted after inserting " +
+                                std::to_string(inserted) + " vectors of the batch");
+        e.inserted = inserted;
+        throw e;
+    }
+    return inserted;
+}
+
+// ========================================================================
+// maintenance fencing
+// ========================================================================
+
+void GpuIndex::begin_maintenance() {
+    // caller holds data_mu_ and gate_ exclusively (see rearrange/remove)
+    std::lock_guard<std::mutex> lk(lease_mu_);
+    for (auto& l : leases_)
+        if (l->done) BIVF_CUDA(cudaStreamWaitEvent(data_stream_, l->done, 0));
+}
+
+void GpuIndex::end_maintenance() {
+    BIVF_CUDA(cudaEventRecord(maint_evt_, data_stream_));
+    maint_gen_.fetch_add(1);
+}
+
+// ========================================================================
+// delete (extension)
+// ========================================================================
+
+uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
+    if (found)
+        for (uint64_t i = 0; i < n; ++i) found[i] = 0;
+    if (n == 0) return 0;
+    std::lock_guard<std::mutex> lk(data_mu_);
+    BIVF_CUDA(cudaSetDevice(device_));
+    cudaStream_t st = data_stream_;
+    // request hash (first occurrence of each id)
+    uint32_t hcap = 64;
+    while (hcap < 2 * n) hcap <<= 1;
+    std::vector<long long> hk(hcap, -1);
+    std::vector<uint32_t> hv(hcap, 0);
+    auto mix = [](uint64_t x) {
+        x ^= x >> 33;
+        x *= 0xff51afd7ed558ccdULL;
+        x ^= x >> 33;
+        x *= 0xc4ceb9fe1a85ec53ULL;
+        x ^= x >> 33;
+        return x;
+    };
+    for (uint64_t r = 0; r < n; ++r) {
+        if (ids[r] < 0) continue;
+        uint32_t h = (uint32_t)mix((uint64_t)ids[r]) & (hcap - 1);
+        while (hk[h] >= 0 && hk[h] != ids[r]) h = (h + 1) & (hcap - 1);
+        if (hk[h] < 0) {
+            hk[h] = ids[r];
+            hv[h] = (uint32_t)r;
+        }
+    }
+    DevBuf dk, dv, dloc;
+    dk.alloc(hcap * 8);
+    dv.alloc(hcap * 4);
+    dloc.alloc(n * 8);
+    BIVF_CUDA(cudaMemcpyAsync(dk.p, hk.data(), hcap * 8, cudaMemcpyHostToDevice, st));
+    BIVF_CUDA(cudaMemcpyAsync(dv.p, hv.data(), hcap * 4, cudaMemcpyHostToDevice, st));
+    BIVF_CUDA(cudaMemsetAsync(dloc.p, 0xff, n * 8, st));
+    uint64_t off_total = 0;
+    for (uint32_t c = 0; c < C_; ++c)
+        off_total = std::max<uint64_t>(off_total, h_off_start_[c] + (h_off_count_[c] + 31) / 32 * 32);
+    BIVF_CUDA(launch_locate(d_off_ids_.as<long long>(), off_total, false, dk.as<long long>(),
+                            dv.as<uint32_t>(), hcap - 1, dloc.as<uint64_t>(), st));
+    BIVF_CUDA(launch_locate(d_bids_.as<long long>(), (uint64_t)h_cursor_ * T_, true,
+                            dk.as<long long>(), dv.as<uint32_t>(), hcap - 1, dloc.as<uint64_t>(), st));
+    std::vector<uint64_t> loc(n);
+    BIVF_CUDA(cudaMemcpyAsync(loc.data(), dloc.p, n * 8, cudaMemcpyDeviceToHost, st));
+    BIVF_CUDA(cudaStreamSynchronize(st));
+
+    // Plan on the host, part by part, in request order: the hole takes the
+    // part's last vector.  Part key: 2c (offline) or
+    // 2c+1 (online); positions are offline slot index / list position `did`.
+    struct Part {
+        uint32_t count;                       // live count while planning
+        std::unordered_map<uint64_t, uint64_t> content;  // pos -> original pos
+        std::unordered_map<uint64_t, uint64_t> where;    // original pos -> current pos
+    };
+    std::unordered_map<uint64_t, Part> parts;
+    auto part_of = [&](uint64_t a, uint64_t& key, uint64_t& pos) {
+        if (a & kArenaBit) {
+            const uint64_t g = a & ~kArenaBit;
+            const uint32_t b = (uint32_t)(g / T_), slot = (uint32_t)(g % T_);
+            const int32_t c = h_owner_[b];
+            key = 2ull * (uint32_t)c + 1;
+            pos = (uint64_t)h_mid_[b] * T_ + slot;
+        } else {
+            // last cluster whose (group-aligned) segment starts at or before a;
+            // empty clusters share their start with the next one
+            const auto it = std::upper_bound(h_off_start_.begin(), h_off_start_.end(), a);
+            const uint32_t c = (uint32_t)(it - h_off_start_.begin()) - 1;
+            key = 2ull * c;
+            pos = a - h_off_start_[c];
+        }
+    };
+    uint64_t removed = 0;
+    for (uint64_t r = 0; r < n; ++r) {
+        if (loc[r] == ~0ull) continue;
+        uint64_t key, pos0;
+        part_of(loc[r], key, pos0);
+        const uint32_t c = (uint32_t)(key / 2);
+        auto ins = parts.try_emplace(key);
+        Part& P = ins.first->second;
+        if (ins.second) P.count = (key & 1) ? h_len_[c] : h_off_count_[c];
+        // current position of this request's vector
+        auto w = P.where.find(pos0);
+        const uint64_t pos = w == P.where.end() ? pos0 : w->second;
+        if (pos == ~0ull || pos >= P.count) continue;  // already gone
+        const uint64_t last = P.count - 1;
+        auto content_at = [&](uint64_t p) {
+            auto it = P.content.find(p);
+            return it == P.content.end() ? p : it->second;
+        };
+        const uint64_t moved_orig = content_at(last);
+        const uint64_t gone_orig = content_at(pos);
+        if (pos != last) {
+            P.content[pos] = moved_orig;
+            P.where[moved_orig] = pos;
+        }
+        P.content[last] = ~0ull;
+        P.where[gone_orig] = ~0ull;
+        P.count = (uint32_t)last;
+        if (found) found[r] = 1;
+        ++removed;
+    }
+    if (removed == 0) return 0;
+    // addresses
+    auto pay_addr = [&](uint64_t key, uint64_t pos) -> uint64_t {
+        const uint32_t c = (uint32_t)(key / 2);
+        if (key & 1) {
+            const int32_t b = h_blocks_[c][pos / T_];
+            const uint32_t slot = (uint32_t)(pos % T_);
+            return kArenaBit | ((uint64_t)b * PS_ + (uint64_t)(slot / 32) * 32 * D_ + slot % 32);
+        }
+        const uint64_t s = h_off_start_[c] + pos;
+        return (s / 32) * 32 * D_ + s % 32;
+    };
+    auto id_addr = [&](uint64_t key, uint64_t pos) -> uint64_t {
+        const uint32_t c = (uint32_t)(key / 2);
+        if (key & 1) {
+            const int32_t b = h_blocks_[c][pos / T_];
+            return kArenaBit | ((uint64_t)b * T_ + pos % T_);
+        }
+        return h_off_start_[c] + pos;
+    };
+    std::vector<uint64_t> msrc_p, mdst_p, msrc_i, mdst_i, clear;
+    std::vector<uint32_t> len_idx, len_val, off_idx, off_val;
+    for (auto& kv : parts) {
+        const uint64_t key = kv.first;
+        Part& P = kv.second;
+        const uint32_t c = (uint32_t)(key / 2);
+        const uint32_t old_count = (key & 1) ? h_len_[c] : h_off_count_[c];
+        for (auto& pc : P.content) {
+            const uint64_t pos = pc.first, orig = pc.second;
+            if (pos >= P.count) {
+                clear.push_back(id_addr(key, pos));
+            } else if (orig != pos) {
+                msrc_p.push_back(pay_addr(key, orig));
+                mdst_p.push_back(pay_addr(key, pos));
+                msrc_i.push_back(id_addr(key, orig));
+                mdst_i.push_back(id_addr(key, pos));
+            }
+        }
+        (void)old_count;
+        if (key & 1) {
+            len_idx.push_back(c);
+            len_val.push_back(P.count);
+        } else {
+            off_idx.push_back(c);
+            off_val.push_back(P.count);
+        }
+    }
+    const uint32_t nm = (uint32_t)msrc_p.size();
+    std::vector<uint64_t> pa(msrc_p), ia(msrc_i);
+    pa.insert(pa.end(), mdst_p.begin(), mdst_p.end());
+    ia.insert(ia.end(), mdst_i.begin(), mdst_i.end());
+    DevBuf dpa, dia, dscr_p, dscr_i, dclr, dli, dlv, doi, dov;
+    dpa.alloc(std::max<size_t>(pa.size(), 1) * 8);
+    dia.alloc(std::max<size_t>(ia.size(), 1) * 8);
+    dscr_p.alloc(std::max<size_t>((size_t)nm * D_, 1) * 4);
+    dscr_i.alloc(std::max<size_t>(nm, 1) * 8);
+    dclr.alloc(std::max<size_t>(clear.size(), 1) * 8);
+    dli.alloc(std::max<size_t>(len_idx.size(), 1) * 4);
+    dlv.alloc(std::max<size_t>(len_idx.size(), 1) * 4);
+    doi.alloc(std::max<size_t>(off_idx.size(), 1) * 4);
+    dov.alloc(std::max<size_t>(off_idx.size(), 1) * 4);
+    if (!pa.empty()) {
+        BIVF_CUDA(cudaMemcpyAsync(dpa.p, pa.data(), pa.size() * 8, cudaMemcpyHostToDevice, st));
+        BIVF_CUDA(cudaMemcpyAsync(dia.p, ia.data(), ia.size() * 8, cudaMemcpyHostToDevice, st));
+    }
+    if (!clear.empty())
+        BIVF_CUDA(cudaMemcpyAsync(dclr.p, clear.data(), clear.size() * 8, cudaMemcpyHostToDevice, st));
+    if (!len_idx.empty()) {
+        BIVF_CUDA(cudaMemcpyAsync(dli.p, len_idx.data(), len_idx.size() * 4, cudaMemcpyHostToDevice, st));
+        BIVF_CUDA(cudaMemcpyAsync(dlv.p, len_val.data(), len_val.size() * 4, cudaMemcpyHostToDevice, st));
+    }
+    if (!off_idx.empty()) {
+        BIVF_CUDA(cudaMemcpyAsync(doi.p, off_idx.data(), off_idx.size() * 4, cudaMemcpyHostToDevice, st));
+        BIVF_CUDA(cudaMemcpyAsync(dov.p, off_val.data(), off_val.size() * 4, cudaMemcpyHostToDevice, st));
+    }
+    {
+        std::unique_lock<std::shared_mutex> g(gate_);
+        begin_maintenance();
+        BIVF_CUDA(launch_slot_moves(d_off_pay_.as<float>(), d_off_ids_.as<long long>(),
+                                    d_arena_.as<float>(), d_bids_.as<long long>(), D_,
+                                    dpa.as<uint64_t>(), dia.as<uint64_t>(), nm,
+                                    dscr_p.as<float>(), dscr_i.as<long long>(), st));
+        BIVF_CUDA(launch_clear_ids(d_off_ids_.as<long long>(), d_bids_.as<long long>(),
+                                   dclr.as<uint64_t>(), (uint32_t)clear.size(), st));
+        BIVF_CUDA(launch_set_u32(d_len_.as<uint32_t>(), dli.as<uint32_t>(), dlv.as<uint32_t>(),
+                                 (uint32_t)len_idx.size(), st));
+        BIVF_CUDA(launch_set_u32(d_off_count_.as<uint32_t>(), doi.as<uint32_t>(),
+                                 dov.as<uint32_t>(), (uint32_t)off_idx.size(), st));
+        end_maintenance();
+    }
+    BIVF_CUDA(cudaStreamSynchronize(st));
+    for (size_t i = 0; i < len_idx.size(); ++i) h_len_[len_idx[i]] = len_val[i];
+    for (size_t i = 0; i < off_idx.size(); ++i) h_off_count_[off_idx[i]] = off_val[i];
+    return removed;
+}
+
+// ========================================================================
+// rearrangement (Alg. 3, ivf_index.cpp:356-511) — planned on the header
+// mirror, applied on device as one block permutation
+// ========================================================================
+
+bool GpuIndex::exceed(uint32_t c) const {
+    if (c >= C_) throw Error(BIVF_ERANGE, "exceed: bad cluster");
+    std::lock_guard<std::mutex> lk(data_mu_);
+    // Eq. 3: sum of committed slots over the online list (= its length), strict
+    return (uint64_t)h_len_[c] > cfg_.rearrange_threshold;
+}
+
+namespace {
+// Planner state shared by rearrange / sweep: the mirror plus the content
+// permutation accumulated by the swaps (content_at[x] = original block whose
+// data now sits at physical x).
+struct Planner {
+    std::vector<int32_t>& prev;
+    std::vector<int32_t>& next;
+    std::vector<int32_t>& owner;
+    std::vector<int32_t>& mid;
+    std::vector<uint8_t>& merged;
+    std::vector<int32_t>& head;
+    std::vector<int32_t>& tail;
+    std::vector<std::vector<int32_t>>& blocks;
+    std::vector<int32_t> content_at;
+    uint32_t allocated;
+    uint32_t C;
+    std::deque<uint32_t> work;
+    std::vector<char> queued;
+    uint64_t merges = 0;
+    std::vector<char> list_touched;
+
+    static int32_t remap(int32_t x, int32_t a, int32_t b) { return x == a ? b : (x == b ? a : x); }
+
+    void enqueue(int32_t blk) {
+        const int32_t o = owner[blk];
+        if (o < 0) return;
+        if (!queued[o]) {
+            queued[o] = 1;
+            work.push_back((uint32_t)o);
+        }
+    }
+    // ivf_index.cpp:585-605
+    void split_runs_around(int32_t x) {
+        if (merged[x]) {
+            merged[x] = 0;
+            enqueue(x);
+        }
+        const int32_t nx = next[x];
+        if (nx >= 0 && merged[nx]) {
+            merged[nx] = 0;
+            enqueue(x);
+        }
+    }
+    // ivf_index.cpp:541-583 (headers), data via content_at
+    void swap_blocks(int32_t a, int32_t b) {
+        if (a == b) return;
+        const int32_t pa = prev[a], na = next[a], pb = prev[b], nb = next[b];
+        const int32_t oa = owner[a], ob = owner[b];
+        const int32_t ma = mid[a], mb = mid[b];
+        std::swap(content_at[a], content_at[b]);
+        prev[a] = remap(pb, a, b);
+        next[a] = remap(nb, a, b);
+        owner[a] = ob;
+        mid[a] = mb;
+        prev[b] = remap(pa, a, b);
+        next[b] = remap(na, a, b);
+        owner[b] = oa;
+        mid[b] = ma;
+        merged[a] = 0;
+        merged[b] = 0;
+        if (pa >= 0 && pa != a && pa != b) next[pa] = b;
+        if (na >= 0 && na != a && na != b) prev[na] = b;
+        if (pb >= 0 && pb != a && pb != b) next[pb] = a;
+        if (nb >= 0 && nb != a && nb != b) prev[nb] = a;
+        auto fix_list = [&](int32_t c) {
+            if (head[c] == a || head[c] == b) head[c] = remap(head[c], a, b);
+            if (tail[c] == a || tail[c] == b) tail[c] = remap(tail[c], a, b);
+            list_touched[c] = 1;
+        };
+        if (oa >= 0) fix_list(oa);
+        if (ob >= 0 && ob != oa) fix_list(ob);
+        // the per-list block tables follow the content
+        if (ob >= 0) blocks[ob][mb] = a;
+        if (oa >= 0) blocks[oa][ma] = b;
+    }
+    // ivf_index.cpp:607-645
+    void rearrange_list(uint32_t c) {
+        int32_t u = head[c];
+        if (u < 0) return;
+        const uint64_t cap = 4ull * allocated + 64;
+        for (uint64_t guard = 0; guard < cap; ++guard) {
+            const int32_t v = next[u];
+            if (v < 0) break;
+            if (merged[v]) {
+                u = v;
+                continue;
+            }
+            const int32_t p = u + 1;
+            if ((uint32_t)p >= allocated) {
+                u = v;
+                continue;
+            }
+            if (p == v) {
+                merged[v] = 1;
+                ++merges;
+                u = v;
+                continue;
+            }
+            split_runs_around(p);
+            split_runs_around(v);
+            swap_blocks(p, v);
+            merged[p] = 1;
+            ++merges;
+            u = p;
+        }
+    }
+    // ivf_index.cpp:476-505 (work queue bounded by 2C+8 rounds)
+    void rearrange(uint32_t k) {
+        work.clear();
+        std::fill(queued.begin(), queued.end(), 0);
+        work.push_back(k);
+        queued[k] = 1;
+        uint64_t rounds = 0;
+        while (!work.empty() && rounds++ < 2ull * C + 8) {
+            const uint32_t c = work.front();
+            work.pop_front();
+            queued[c] = 0;
+            rearrange_list(c);
+        }
+    }
+};
+}  // namespace
+
+uint64_t GpuIndex::hop_count(uint32_t c) const {
+    if (c >= C_) throw Error(BIVF_ERANGE, "hop_count: bad cluster");
+    std::lock_guard<std::mutex> lk(data_mu_);
+    uint64_t hops = 0, visited = 0;
+    for (int32_t b = h_head_[c]; b >= 0; b = h_next_[b]) {
+        if (++visited > NB_) throw Error(BIVF_ECORRUPT, "hop_count: cycle detected");
+        const int32_t nx = h_next_[b];
+        if (nx >= 0 && !h_merged_[nx]) ++hops;
+    }
+    return hops;
+}
+
+void GpuIndex::rearrange(uint32_t c) {
+    if (c >= C_) throw Error(BIVF_ERANGE, "rearrange: bad cluster");
+    std::lock_guard<std::mutex> lk(data_mu_);
+    BIVF_CUDA(cudaSetDevice(device_));
+    const auto t0 = std::chrono::steady_clock::now();
+    auto hops_of = [&](uint32_t k) {
+        uint64_t hops = 0, visited = 0;
+        for (int32_t b = h_head_[k]; b >= 0; b = h_next_[b]) {
+            if (++visited > NB_) throw Error(BIVF_ECORRUPT, "hop_count: cycle detected");
+            const int32_t nx = h_next_[b];
+            if (nx >= 0 && !h_merged_[nx]) ++hops;
+        }
+        return hops;
+    };
+    Planner P{h_prev_, h_next_, h_owner_, h_mid_, h_merged_, h_head_, h_tail_, h_blocks_};
+    P.allocated = h_cursor_;
+    P.C = C_;
+    P.queued.assign(C_, 0);
+    P.list_touched.assign(C_, 0);
+    P.content_at.resize(h_cursor_);
+    for (uint32_t b = 0; b < h_cursor_; ++b) P.content_at[b] = (int32_t)b;
+    RearrangeEvent ev{c, hops_of(c), 0, 0, 0.0};
+    P.rearrange(c);
+    ev.hops_after = hops_of(c);
+    ev.merges = P.merges;
+    // apply the accumulated permutation on device
+    std::vector<int32_t> src, dst;
+    for (uint32_t x = 0; x < h_cursor_; ++x)
+        if (P.content_at[x] != (int32_t)x) {
+            src.push_back(P.content_at[x]);
+            dst.push_back((int32_t)x);
+        }
+    if (!src.empty()) {
+        const uint32_t nm = (uint32_t)src.size();
+        DevBuf ds, dd, sp, si, own;
+        ds.alloc(nm * 4);
+        dd.alloc(nm * 4);
+        sp.alloc((size_t)nm * PS_ * 4);
+        si.alloc((size_t)nm * T_ * 8);
+        cudaStream_t st = data_stream_;
+        BIVF_CUDA(cudaMemcpyAsync(ds.p, src.data(), nm * 4, cudaMemcpyHostToDevice, st));
+        BIVF_CUDA(cudaMemcpyAsync(dd.p, dst.data(), nm * 4, cudaMemcpyHostToDevice, st));
+        // updated table rows for every touched list, and owners
+        std::vector<int32_t> rows;
+        std::vector<uint32_t> rowc;
+        for (uint32_t k = 0; k < C_; ++k)
+            if (P.list_touched[k]) rowc.push_back(k);
+        std::vector<std::vector<int32_t>> staged;
+        {
+            std::unique_lock<std::shared_mutex> g(gate_);
+            begin_maintenance();
+            BIVF_CUDA(launch_block_moves(d_arena_.as<float>(), d_bids_.as<long long>(), PS_, T_,
+                                         ds.as<int32_t>(), dd.as<int32_t>(), nm, sp.as<float>(),
+                                         si.as<long long>(), st));
+            for (uint32_t k : rowc) {
+                staged.push_back(h_blocks_[k]);
+                auto& r = staged.back();
+                if (!r.empty())
+                    BIVF_CUDA(cudaMemcpyAsync(d_table_.as<int32_t>() + (size_t)k * MLB_, r.data(),
+                                              r.size() * 4, cudaMemcpyHostToDevice, st));
+            }
+            BIVF_CUDA(cudaMemcpyAsync(d_owner_.p, h_owner_.data(), (size_t)h_cursor_ * 4,
+                                      cudaMemcpyHostToDevice, st));
+            end_maintenance();
+        }
+        BIVF_CUDA(cudaStreamSynchronize(st));
+    }
+    ev.duration_us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    std::lock_guard<std::mutex> lk2(events_mu_);
+    events_.push_back(ev);
+}
+
+void GpuIndex::rearrange_sweep() {
+    // ivf_index.cpp:507-511
+    for (uint32_t c = 0; c < C_; ++c) {
+        bool ex;
+        {
+            std::lock_guard<std::mutex> lk(data_mu_);
+            ex = (uint64_t)h_len_[c] > cfg_.rearrange_threshold;
+        }
+        if (ex) rearrange(c);
+    }
+}
+
+std::vector<RearrangeEvent> GpuIndex::take_events() {
+    std::lock_guard<std::mutex> lk(events_mu_);
+    std::vector<RearrangeEvent> out;
+    out.swap(events_);
+    return out;
+}
+
+// ========================================================================
+// introspection
+// ========================================================================
+
+uint64_t GpuIndex::size() const {
+    std::lock_guard<std::mutex> lk(data_mu_);
+    uint64_t t = 0;
+    for (uint32_t c = 0; c < C_; ++c) t += (uint64_t)h_off_count_[c] + h_len_[c];
+    return t;
+}
+
+uint64_t GpuIndex::list_length(uint32_t c) const {
+    if (c >= C_) throw Error(BIVF_ERANGE, "list_length: bad cluster");
+    std::lock_guard<std::mutex> lk(data_mu_);
+    return h_len_[c];
+}
+
+uint64_t GpuIndex::offline_count(uint32_t c) const {
+    if (c >= C_) throw Error(BIVF_ERANGE, "offline_count: bad cluster");
+    std::lock_guard<std::mutex> lk(data_mu_);
+    return h_off_count_[c];
+}
+
+int32_t GpuIndex::online_head(uint32_t c) const {
+    if (c >= C_) throw Error(BIVF_ERANGE, "online_head: bad cluster");
+    std::lock_guard<std::mutex> lk(data_mu_);
+    return h_head_[c];
+}
+
+uint64_t GpuIndex::allocated_blocks() const {
+    std::lock_guard<std::mutex> lk(data_mu_);
+    return h_cursor_;
+}
+
+void GpuIndex::check_block(int32_t b) const {
+    if (b < 0 || (uint32_t)b >= h_cursor_)
+        throw Error(BIVF_ERANGE, "block index " + std::to_string(b) + " not allocated");
+}
+
+uint32_t GpuIndex::committed_of(int32_t b) const {
+    const int32_t c = h_owner_[b];
+    if (c < 0) return 0;
+    const int64_t v = (int64_t)h_len_[c] - (int64_t)h_mid_[b] * T_;
+    return (uint32_t)std::max<int64_t>(0, std::min<int64_t>(T_, v));
+}
+
+void GpuIndex::block_header(int32_t b, int32_t* out5) const {
+    std::lock_guard<std::mutex> lk(data_mu_);
+    check_block(b);
+    out5[0] = h_prev_[b];
+    out5[1] = h_next_[b];
+    out5[2] = (int32_t)committed_of(b);
+    out5[3] = h_owner_[b];
+    out5[4] = h_merged_[b];
+}
+
+void GpuIndex::block_ids(int32_t b, int64_t* out) const {
+    std::lock_guard<std::mutex> lk(data_mu_);
+    check_block(b);
+    BIVF_CUDA(cudaSetDevice(device_));
+    BIVF_CUDA(cudaMemcpy(out, d_bids_.as<long long>() + (size_t)b * T_, (size_t)T_ * 8,
+                         cudaMemcpyDeviceToHost));
+}
+
+void GpuIndex::block_payload(int32_t b, float* out) const {
+    std::lock_guard<std::mutex> lk(data_mu_);
+    check_block(b);
+    BIVF_CUDA(cudaSetDevice(device_));
+    BIVF_CUDA(cudaMemcpy(out, d_arena_.as<float>() + (size_t)b * PS_, (size_t)PS_ * 4,
+                         cudaMemcpyDeviceToHost));
+}
+
+uint64_t GpuIndex::cluster_contents(uint32_t c, int64_t* ids, float* vecs) const {
+    if (c >= C_) throw Error(BIVF_ERANGE, "cluster_contents: bad cluster");
+    std::lock_guard<std::mutex> lk(data_mu_);
+    const uint64_t noff = h_off_count_[c], non = h_len_[c];
+    if (!ids) return noff + non;
+    BIVF_CUDA(cudaSetDevice(device_));
+    uint64_t n = 0;
+    if (noff) {
+        const uint64_t groups = (noff + 31) / 32;
+        std::vector<float> pay(groups * 32 * D_);
+        std::vector<long long> oid(noff);
+        const uint64_t s0 = h_off_start_[c];
+        BIVF_CUDA(cudaMemcpy(pay.data(), d_off_pay_.as<float>() + s0 * D_, pay.size() * 4,
+                             cudaMemcpyDeviceToHost));
+        BIVF_CUDA(cudaMemcpy(oid.data(), d_off_ids_.as<long long>() + s0, noff * 8,
+                             cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < noff; ++i, ++n) {
+            ids[n] = oid[i];
+            const float* base = pay.data() + (i / 32) * 32 * D_ + i % 32;
+            for (uint32_t d = 0; d < D_; ++d) vecs[n * D_ + d] = base[(size_t)d * 32];
+        }
+    }
+    std::vector<float> pay(PS_);
+    std::vector<long long> bid(T_);
+    uint64_t left = non;
+    for (int32_t b : h_blocks_[c]) {
+        if (!left) break;
+        const uint32_t m = (uint32_t)std::min<uint64_t>(T_, left);
+        BIVF_CUDA(cudaMemcpy(pay.data(), d_arena_.as<float>() + (size_t)b * PS_, PS_ * 4,
+                             cudaMemcpyDeviceToHost));
+        BIVF_CUDA(cudaMemcpy(bid.data(), d_bids_.as<long long>() + (size_t)b * T_, (size_t)T_ * 8,
+                             cudaMemcpyDeviceToHost));
+        for (uint32_t s = 0; s < m; ++s, ++n) {
+            ids[n] = bid[s];
+            const float* base = pay.data() + (s / 32) * 32 * D_ + s % 32;
+            for (uint32_t d = 0; d < D_; ++d) vecs[n * D_ + d] = base[(size_t)d * 32];
+        }
+        left -= m;
+    }
+    return n;
+}
+
+std::string GpuIndex::dump_pool() const {
+    // block_store.cpp:188-201 line format
+    std::lock_guard<std::mutex> lk(data_mu_);
+    std::ostringstream os;
+    std::vector<long long> all((size_t)h_cursor_ * T_);
+    if (h_cursor_) {
+        BIVF_CUDA(cudaSetDevice(device_));
+        BIVF_CUDA(cudaMemcpy(all.data(), d_bids_.p, all.size() * 8, cudaMemcpyDeviceToHost));
+    }
+    for (uint32_t b = 0; b < h_cursor_; ++b) {
+        const uint32_t sz = committed_of((int32_t)b);
+        os << b << " prev=" << h_prev_[b] << " next=" << h_next_[b] << " size=" << sz << " ids=";
+        for (uint32_t s = 0; s < sz; ++s) {
+            if (s) os << ',';
+            os << all[(size_t)b * T_ + s];
+        }
+        os << '\n';
+    }
+    return os.str();
+}
+
+// ========================================================================
+// BIVFSNAP v1 (ivf_index.cpp:515-619)
+// ========================================================================
+
+namespace {
+constexpr char kMagic[8] = {'B', 'I', 'V', 'F', 'S', 'N', 'A', 'P'};
+template <class T>
+void put(std::ostream& os, const T& v) {
+    os.write(reinterpret_cast<const char*>(&v), sizeof(v));
+}
+template <class T>
+T get(std::istream& is) {
+    T v{};
+    is.read(reinterpret_cast<char*>(&v), sizeof(v));
+    if (!is) throw Error(BIVF_EIO, "snapshot: truncated file");
+    return v;
+}
+}  // namespace
+
+void GpuIndex::save(const std::string& path) const {
+    std::ofstream os(path, std::ios::binary | std::ios::trunc);
+    if (!os) throw Error(BIVF_EIO, "snapshot: cannot open " + path + " for writing");
+    os.write(kMagic, 8);
+    put<uint32_t>(os, 1);
+    put<uint64_t>(os, C_);
+    put<uint64_t>(os, D_);
+    put<uint64_t>(os, cfg_.nprobe_default);
+    put<uint64_t>(os, cfg_.rearrange_threshold);
+    put<uint64_t>(os, cfg_.kmeans_iters);
+    put<uint64_t>(os, cfg_.kmeans_seed);
+    put<uint64_t>(os, NB_);
+    put<uint64_t>(os, T_);
+    put<uint64_t>(os, 32);
+    put<double>(os, cfg_.alert_watermark);
+    put<int64_t>(os, next_id_);
+    std::vector<float> cent((size_t)C_ * D_);
+    get_centroids(cent.data());
+    os.write(reinterpret_cast<const char*>(cent.data()), cent.size() * 4);
+    // online lists flattened into the offline segments (ivf_index.cpp:554-563)
+    std::vector<int64_t> ids;
+    std::vector<float> vecs;
+    for (uint32_t c = 0; c < C_; ++c) {
+        const uint64_t n = cluster_contents(c, nullptr, nullptr);
+        ids.resize(n);
+        vecs.resize(n * D_);
+        cluster_contents(c, ids.data(), vecs.data());
+        put<uint64_t>(os, n);
+        for (uint64_t i = 0; i < n; ++i) {
+            put<int64_t>(os, ids[i]);
+            os.write(reinterpret_cast<const char*>(vecs.data() + i * D_), (std::streamsize)D_ * 4);
+        }
+    }
+    if (!os) throw Error(BIVF_EIO, "snapshot: write failed for " + path);
+}
+
+std::unique_ptr<GpuIndex> GpuIndex::load(const std::string& path, const bivf_config* ov) {
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw Error(BIVF_EIO, "snapshot: cannot open " + path);
+    char magic[8];
+    is.read(magic, 8);
+    if (!is || std::memcmp(magic, kMagic, 8) != 0) throw Error(BIVF_EIO, "snapshot: bad magic in " + path);
+    if (get<uint32_t>(is) != 1) throw Error(BIVF_EIO, "snapshot: unsupported version in " + path);
+    bivf_config cfg{};
+    if (ov) cfg = *ov;
+    cfg.num_clusters = get<uint64_t>(is);
+    cfg.dim = get<uint64_t>(is);
+    cfg.nprobe_default = get<uint64_t>(is);
+    cfg.rearrange_threshold = get<uint64_t>(is);
+    cfg.kmeans_iters = get<uint64_t>(is);
+    cfg.kmeans_seed = get<uint64_t>(is);
+    cfg.kmeans_seed_set = 1;
+    cfg.num_blocks = get<uint64_t>(is);
+    cfg.block_capacity = get<uint64_t>(is);
+    if (get<uint64_t>(is) != 32) throw Error(BIVF_EIO, "snapshot: interleave_group must be 32");
+    cfg.alert_watermark = get<double>(is);
+    const int64_t next_id = get<int64_t>(is);
+    if (!ov || ov->max_list_blocks == 0) cfg.max_list_blocks = 0;
+    auto idx = std::make_unique<GpuIndex>(cfg);
+    std::vector<float> cent(cfg.num_clusters * cfg.dim);
+    is.read(reinterpret_cast<char*>(cent.data()), (std::streamsize)cent.size() * 4);
+    if (!is) throw Error(BIVF_EIO, "snapshot: truncated centroids in " + path);
+    idx->set_centroids(cent.data());
+    std::vector<float> rows;
+    std::vector<int64_t> ids;
+    std::vector<uint32_t> asg;
+    const uint32_t D = (uint32_t)cfg.dim;
+    for (uint64_t c = 0; c < cfg.num_clusters; ++c) {
+        const uint64_t n = get<uint64_t>(is);
+        const size_t r0 = ids.size();
+        ids.resize(r0 + n);
+        asg.resize(r0 + n, (uint32_t)c);
+        rows.resize((r0 + n) * D);
+        for (uint64_t i = 0; i < n; ++i) {
+            ids[r0 + i] = get<int64_t>(is);
+            is.read(reinterpret_cast<char*>(rows.data() + (r0 + i) * D), (std::streamsize)D * 4);
+            if (!is) throw Error(BIVF_EIO, "snapshot: truncated vectors in " + path);
+        }
+    }
+    idx->bulk_load(rows.data(), ids.size(), asg.data(), ids.data());
+    // flattened contents carry every id ever handed out (ivf_index.cpp:615-617)
+    idx->supplied_.clear();
+    idx->next_id_ = next_id;
+    idx->offline_end_ = next_id;
+    return idx;
+}
+
+}  // namespace bivf

@@ -1,0 +1,246 @@
+// GpuIndex — host runtime of the B200-native online IVF-Flat path.
+//
+// Ownership split:
+//   device  : centroids (+ interleaved copy), offline segments, pool arena +
+//             ids, per-list block table / length / block count / fail flag,
+//             allocation cursor, block owners.  Everything the scan and the
+//             insert kernels read or write.
+//   host    : the block-header mirror (prev/next/owner/merged, derived
+//             committed), list head/tail, id bookkeeping (auto ranges,
+//             supplied ids), counters, rearrangement planning.  Updated from
+//             the device's own results after every insert (new block owners
+//             + lengths), never guessed.
+// Concurrency (the reference's contract, block_store.hpp:56-59):
+//   search || search, search || insert: searches run on leased streams and
+//     read only release-published prefixes (len) of append-only storage.
+//   insert / remove / rearrange: serialized on the data stream (data_mu_),
+//     like the reference's single data lane + insert_gate_.
+//   remove / rearrange vs search: quiescence — the data stream waits on every
+//     lease's last event, later searches wait on the maintenance event
+//     (stream-ordered, no host spin), so searches never observe a move.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <shared_mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/bivf.h"
+#include "insert.cuh"
+#include "scan.cuh"
+
+namespace bivf {
+
+struct Error : std::runtime_error {
+    bivf_status code;
+    uint64_t inserted = 0;
+    Error(bivf_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define BIVF_CUDA(x) ::bivf::cuda_check((x), #x)
+
+extern std::atomic<uint64_t> g_launches;
+
+// RAII device allocation
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf();
+    void alloc(size_t n);         // exact size, contents undefined
+    void ensure(size_t n);        // grow (no copy)
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    PinBuf() = default;
+    PinBuf(const PinBuf&) = delete;
+    PinBuf& operator=(const PinBuf&) = delete;
+    ~PinBuf();
+    void ensure(size_t n);
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// A search lease: one stream + its device workspace + pinned staging
+// (Alg. 4's per-request resource).
+struct Lease {
+    int id = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr, t3 = nullptr, t4 = nullptr;
+    DevBuf ws;
+    PinBuf pin;
+    uint64_t seen_maint = 0;
+    bool busy = false;
+};
+
+struct Workspace {  // carved from Lease::ws
+    float* queries;        // [nq][Dp]
+    float* qraw;           // [nq][D] (H2D target)
+    long long* probes;     // [nq][P]
+    float* pdist;          // [nq][P] probe keys
+    float* fcand_d;        // quantizer candidates
+    long long* fcand_i;
+    float* cand_d;         // scan candidates
+    long long* cand_i;
+    float* out_d;
+    long long* out_i;
+    uint32_t* out_cnt;
+    uint32_t* ctr;
+    PlanBufs plan;
+};
+
+struct RearrangeEvent {
+    uint32_t cluster;
+    uint64_t hops_before, hops_after, merges;
+    double duration_us;
+};
+
+class GpuIndex {
+public:
+    explicit GpuIndex(const bivf_config& cfg);
+    ~GpuIndex();
+
+    const bivf_config& config() const { return cfg_; }
+    uint32_t C() const { return C_; }
+    uint32_t D() const { return D_; }
+
+    void train(const float* x, uint64_t n);
+    void set_centroids(const float* c);
+    void get_centroids(float* out) const;
+    void bulk_load(const float* x, uint64_t n, const uint32_t* assignment, const int64_t* ids);
+
+    uint64_t insert(const float* x, uint64_t n, const int64_t* ids, int64_t* out_ids);
+    void search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, int64_t* out_ids,
+                float* out_d, uint32_t* out_cnt);
+    void search_device(const float* q_dev, uint64_t nq, uint64_t k, uint64_t nprobe,
+                       int64_t* ids_dev, float* d_dev, uint32_t* cnt_dev, cudaStream_t user);
+    void assign(const float* y, uint64_t n, uint32_t* out);
+    void probes(const float* q, uint64_t nq, uint64_t nprobe, uint32_t* out);
+    uint64_t remove(const int64_t* ids, uint64_t n, uint8_t* found);
+
+    bool exceed(uint32_t c) const;
+    void rearrange(uint32_t c);
+    void rearrange_sweep();
+    std::vector<RearrangeEvent> take_events();
+
+    uint64_t size() const;
+    uint64_t scalars_copied() const { return scalars_copied_; }
+    uint64_t list_length(uint32_t c) const;
+    uint64_t offline_count(uint32_t c) const;
+    uint64_t hop_count(uint32_t c) const;
+    int32_t online_head(uint32_t c) const;
+    uint64_t allocated_blocks() const;
+    void block_header(int32_t b, int32_t* out5) const;
+    void block_ids(int32_t b, int64_t* out) const;
+    void block_payload(int32_t b, float* out) const;
+    uint64_t cluster_contents(uint32_t c, int64_t* ids, float* vecs) const;
+    std::string dump_pool() const;
+    int64_t next_id() const { return next_id_; }
+
+    void save(const std::string& path) const;
+    static std::unique_ptr<GpuIndex> load(const std::string& path, const bivf_config* ov);
+
+    void set_timing(bool on) { timing_ = on; }
+    void last_timings(float* out4) const;
+
+private:
+    // --- device storage
+    void alloc_device();
+    void ensure_offline_capacity(uint64_t slots);
+    DevLists dev_lists() const;
+    InsertState insert_state();
+    void upload_centroids();
+
+    // --- leases / maintenance fencing
+    Lease* acquire_lease();
+    void release_lease(Lease* l);
+    Workspace carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_t maxch,
+                    uint32_t fnch);
+    void enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uint32_t k,
+                        uint32_t P, Workspace& w);
+    void begin_maintenance();   // caller holds data_mu_; takes gate_ exclusively
+    void end_maintenance();
+
+    // --- host mirror
+    void absorb_new_blocks(uint32_t cursor_old, uint32_t cursor_new);
+    void refresh_lengths();
+    uint32_t committed_of(int32_t b) const;
+    void check_block(int32_t b) const;
+    bool is_duplicate_id(int64_t id);
+    void validate_search(uint64_t k, uint64_t nprobe) const;
+
+    bivf_config cfg_;
+    uint32_t C_, D_, Dp_, T_, gpb_, NB_, MLB_;
+    uint64_t PS_;
+    int device_;
+    int num_sms_ = 148;
+
+    // device
+    DevBuf d_cent_, d_cent_il_;
+    DevBuf d_off_pay_, d_off_ids_, d_off_start_, d_off_count_;
+    uint64_t off_slots_cap_ = 0;
+    DevBuf d_arena_, d_bids_, d_owner_;
+    DevBuf d_cursor_, d_len_, d_nblocks_, d_fail_, d_table_;
+    DevBuf d_run_, d_failfrom_, d_newlen_;
+    // data-lane staging
+    cudaStream_t data_stream_ = nullptr;
+    DevBuf d_x_, d_ids_, d_asg_, d_blk_, d_did_, d_qtmp_, d_fc_d_, d_fc_i_, d_fo_d_, d_fo_i_,
+        d_ctr_;
+    PinBuf h_stage_;
+
+    // host mirror
+    std::vector<uint32_t> h_len_, h_off_count_, h_nblocks_;
+    std::vector<uint64_t> h_off_start_;
+    std::vector<int32_t> h_prev_, h_next_, h_owner_, h_mid_;
+    std::vector<uint8_t> h_merged_;
+    std::vector<int32_t> h_head_, h_tail_;
+    std::vector<std::vector<int32_t>> h_blocks_;  // per list, logical order (table row)
+    uint32_t h_cursor_ = 0;
+    bool alert_fired_ = false;
+    bool trained_ = false;
+
+    // ids (ivf_index.cpp:107-141)
+    int64_t next_id_ = 0, offline_end_ = 0;
+    std::vector<std::pair<int64_t, int64_t>> auto_ranges_;
+    std::unordered_set<int64_t> supplied_;
+    uint64_t scalars_copied_ = 0;
+
+    std::vector<RearrangeEvent> events_;
+    std::mutex events_mu_;
+
+    // concurrency
+    mutable std::mutex data_mu_;
+    std::shared_mutex gate_;
+    std::mutex lease_mu_;
+    std::condition_variable lease_cv_;
+    std::vector<std::unique_ptr<Lease>> leases_;
+    cudaEvent_t maint_evt_ = nullptr;
+    std::atomic<uint64_t> maint_gen_{0};
+
+    bool timing_ = false;
+    float last_ms_[4] = {-1, -1, -1, -1};
+};
+
+// helpers implemented in host_algos.cpp
+void synthetic_dataset(uint64_t n, uint64_t dim, uint64_t comps, uint64_t seed, float* out);
+uint64_t kmeans_gpu(const float* points, uint64_t n, uint64_t dim, uint64_t k, uint64_t iters,
+                    uint64_t seed, int device, float* centroids, uint32_t* assignment);
+float host_l2(const float* a, const float* b, uint32_t dim);
+
+}  // namespace bivf

@@ -1,0 +1,243 @@
+// Maintenance kernels: in-place rearrangement data moves (Alg. 3, K7),
+// delete (K6: locate + tail-into-hole compaction moves), the multi-GPU top-k
+// merge (K8) and small glue kernels.  sm_100a.
+//
+// Reference semantics:
+//   swap_blocks data part       src/ivf_index.cpp:541-557 (ids + payload + committed)
+//   delete                      none in the reference; rules: DESIGN.md §Delete
+// Moves are planned on the host mirror; here every move is a gather of the
+// source slots/blocks into a scratch area followed by a scatter, so a whole
+// plan (any chain of swaps or tail moves) applies in two order-free passes.
+#include <algorithm>
+
+#include "common.cuh"
+#include "launches.h"
+#include "maint.cuh"
+
+namespace bivf {
+
+namespace {
+
+__global__ void make_asg_kernel(const long long* nearest, const long long* ids, uint32_t n,
+                                uint32_t* asg) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) asg[i] = ids[i] < 0 ? 0xffffffffu : (uint32_t)nearest[i];
+}
+
+// whole-block moves: phase 0 src -> scratch[m], phase 1 scratch[m] -> dst
+__global__ void block_move_kernel(float* arena, long long* bids, uint64_t PS, uint32_t T,
+                                  const int32_t* src, const int32_t* dst, uint32_t nmoves,
+                                  float* scr_pay, long long* scr_ids, int phase) {
+    const uint32_t m = blockIdx.y;
+    if (m >= nmoves) return;
+    const uint64_t b = phase == 0 ? (uint64_t)src[m] : (uint64_t)dst[m];
+    float* blk_pay = arena + b * PS;
+    long long* blk_ids = bids + b * T;
+    float* sp = scr_pay + (uint64_t)m * PS;
+    long long* si = scr_ids + (uint64_t)m * T;
+    const float4* from4 = reinterpret_cast<const float4*>(phase == 0 ? blk_pay : sp);
+    float4* to4 = reinterpret_cast<float4*>(phase == 0 ? sp : blk_pay);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < PS / 4;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        to4[i] = from4[i];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (phase == 0) si[i] = blk_ids[i];
+        else blk_ids[i] = si[i];
+    }
+}
+
+// slot moves (delete compaction).  A slot address is the float offset of its
+// dimension-0 element within its pool (offline segments or arena; bit 63
+// selects the arena) and the index of its id.
+__device__ __forceinline__ float* slot_pay(float* off_pay, float* arena, uint64_t a) {
+    return (a >> 63) ? arena + (a & ~(1ull << 63)) : off_pay + a;
+}
+__device__ __forceinline__ long long* slot_id(long long* off_ids, long long* bids, uint64_t a) {
+    return (a >> 63) ? bids + (a & ~(1ull << 63)) : off_ids + a;
+}
+
+__global__ void slot_move_kernel(float* off_pay, long long* off_ids, float* arena,
+                                 long long* bids, uint32_t D, const uint64_t* pay_addr,
+                                 const uint64_t* id_addr, uint32_t nmoves, float* scr_pay,
+                                 long long* scr_ids, int phase) {
+    // pay_addr/id_addr: [2*nmoves] = src..., dst...
+    const uint64_t total = (uint64_t)nmoves * D;
+    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
+         o += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t m = (uint32_t)(o / D), d = (uint32_t)(o - (uint64_t)m * D);
+        if (phase == 0) {
+            scr_pay[o] = slot_pay(off_pay, arena, pay_addr[m])[(uint64_t)d * 32u];
+            if (d == 0) scr_ids[m] = *slot_id(off_ids, bids, id_addr[m]);
+        } else {
+            slot_pay(off_pay, arena, pay_addr[nmoves + m])[(uint64_t)d * 32u] = scr_pay[o];
+            if (d == 0) *slot_id(off_ids, bids, id_addr[nmoves + m]) = scr_ids[m];
+        }
+    }
+}
+
+__global__ void clear_ids_kernel(long long* off_ids, long long* bids, const uint64_t* id_addr,
+                                 uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) *slot_id(off_ids, bids, id_addr[i]) = -1;
+}
+
+__global__ void set_u32_kernel(uint32_t* arr, const uint32_t* idx, const uint32_t* val,
+                               uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) arr[idx[i]] = val[i];
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return x;
+}
+
+// locate: every live id (offline slots, then pool slots) probed against the
+// request hash table; a hit records the slot's global address.
+__global__ void locate_kernel(const long long* ids, uint64_t nslots, uint64_t arena_flag,
+                              const long long* hkeys, const uint32_t* hvals, uint32_t hmask,
+                              uint64_t* loc) {
+    for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nslots;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const long long id = ids[s];
+        if (id < 0) continue;
+        uint32_t h = (uint32_t)mix64((uint64_t)id) & hmask;
+        for (;;) {
+            const long long k = hkeys[h];
+            if (k < 0) break;
+            if (k == id) {
+                loc[hvals[h]] = s | arena_flag;
+                break;
+            }
+            h = (h + 1) & hmask;
+        }
+    }
+}
+
+// K8: merge G shard runs per query ([G][nq][k]) into the global top-k.
+template <int KPL>
+__global__ void merge_shards_kernel(const float* dists, const long long* ids, uint32_t G,
+                                    uint32_t nq, uint32_t k, float* out_d, long long* out_i,
+                                    uint32_t* out_cnt) {
+    const uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (q >= nq) return;
+    WarpTopK<KPL> tk;
+    tk.init();
+    for (uint32_t g = 0; g < G; ++g) {
+        const uint64_t base = ((uint64_t)g * nq + q) * k;
+        for (uint32_t e0 = 0; e0 < k; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            const float cd = e < k ? dists[base + e] : 0.f;
+            const long long ci = e < k ? ids[base + e] : -1;
+            const bool pass = e < k && ci >= 0 && tk.admits(cd, ci);
+            unsigned m = __ballot_sync(0xffffffffu, pass);
+            if (!m) break;
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const float bd = __shfl_sync(0xffffffffu, cd, src);
+                const long long bi = __shfl_sync(0xffffffffu, ci, src);
+                if (tk.admits(bd, bi)) tk.insert(bd, bi, (int)k, lane);
+            }
+        }
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int r = 0; r < KPL; ++r) {
+        const uint32_t e = r * 32 + lane;
+        cnt += __popc(__ballot_sync(0xffffffffu, e < k && tk.id[r] >= 0));
+        if (e < k) {
+            out_d[(uint64_t)q * k + e] = tk.d[r];
+            out_i[(uint64_t)q * k + e] = tk.id[r];
+        }
+    }
+    if (lane == 0 && out_cnt) out_cnt[q] = cnt;
+}
+
+unsigned grid_for(uint64_t work, unsigned cap = 148 * 16) {
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, cap));
+}
+
+}  // namespace
+
+cudaError_t launch_make_asg(const long long* nearest, const long long* ids, uint32_t n,
+                            uint32_t* asg, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    make_asg_kernel<<<(n + 255) / 256, 256, 0, s>>>(nearest, ids, n, asg);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block_moves(float* arena, long long* bids, uint64_t PS, uint32_t T,
+                               const int32_t* src, const int32_t* dst, uint32_t nmoves,
+                               float* scr_pay, long long* scr_ids, cudaStream_t s) {
+    if (!nmoves) return cudaSuccess;
+    const unsigned gx = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((PS / 4 + 255) / 256, 64));
+    for (int phase = 0; phase < 2; ++phase) {
+        block_move_kernel<<<dim3(gx, nmoves), 256, 0, s>>>(arena, bids, PS, T, src, dst, nmoves,
+                                                           scr_pay, scr_ids, phase);
+        count_launch();
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_slot_moves(float* off_pay, long long* off_ids, float* arena, long long* bids,
+                              uint32_t D, const uint64_t* pay_addr, const uint64_t* id_addr,
+                              uint32_t nmoves, float* scr_pay, long long* scr_ids,
+                              cudaStream_t s) {
+    if (!nmoves) return cudaSuccess;
+    for (int phase = 0; phase < 2; ++phase) {
+        slot_move_kernel<<<grid_for((uint64_t)nmoves * D), 256, 0, s>>>(
+            off_pay, off_ids, arena, bids, D, pay_addr, id_addr, nmoves, scr_pay, scr_ids, phase);
+        count_launch();
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_clear_ids(long long* off_ids, long long* bids, const uint64_t* id_addr,
+                             uint32_t n, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    clear_ids_kernel<<<(n + 255) / 256, 256, 0, s>>>(off_ids, bids, id_addr, n);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_u32(uint32_t* arr, const uint32_t* idx, const uint32_t* val, uint32_t n,
+                           cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    set_u32_kernel<<<(n + 255) / 256, 256, 0, s>>>(arr, idx, val, n);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_locate(const long long* ids, uint64_t nslots, bool arena,
+                          const long long* hkeys, const uint32_t* hvals, uint32_t hmask,
+                          uint64_t* loc, cudaStream_t s) {
+    if (!nslots) return cudaSuccess;
+    locate_kernel<<<grid_for(nslots, 148 * 32), 256, 0, s>>>(ids, nslots, arena ? (1ull << 63) : 0,
+                                                             hkeys, hvals, hmask, loc);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge_shards(const float* dists, const long long* ids, uint32_t G, uint32_t nq,
+                                uint32_t k, float* out_d, long long* out_i, uint32_t* out_cnt,
+                                cudaStream_t s) {
+    if (!nq) return cudaSuccess;
+    const unsigned grid = (nq + 3) / 4;
+    if (k <= 32) merge_shards_kernel<1><<<grid, 128, 0, s>>>(dists, ids, G, nq, k, out_d, out_i, out_cnt);
+    else if (k <= 64) merge_shards_kernel<2><<<grid, 128, 0, s>>>(dists, ids, G, nq, k, out_d, out_i, out_cnt);
+    else if (k <= 128) merge_shards_kernel<4><<<grid, 128, 0, s>>>(dists, ids, G, nq, k, out_d, out_i, out_cnt);
+    else if (k <= 256) merge_shards_kernel<8><<<grid, 128, 0, s>>>(dists, ids, G, nq, k, out_d, out_i, out_cnt);
+    else return cudaErrorInvalidValue;
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace bivf

@@ -1,0 +1,32 @@
+// Host-visible declarations for maint.cu.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bivf {
+
+cudaError_t launch_make_asg(const long long* nearest, const long long* ids, uint32_t n,
+                            uint32_t* asg, cudaStream_t s);
+cudaError_t launch_block_moves(float* arena, long long* bids, uint64_t PS, uint32_t T,
+                               const int32_t* src, const int32_t* dst, uint32_t nmoves,
+                               float* scr_pay, long long* scr_ids, cudaStream_t s);
+// pay_addr/id_addr hold 2*nmoves entries: sources then destinations
+cudaError_t launch_slot_moves(float* off_pay, long long* off_ids, float* arena, long long* bids,
+                              uint32_t D, const uint64_t* pay_addr, const uint64_t* id_addr,
+                              uint32_t nmoves, float* scr_pay, long long* scr_ids,
+                              cudaStream_t s);
+cudaError_t launch_clear_ids(long long* off_ids, long long* bids, const uint64_t* id_addr,
+                             uint32_t n, cudaStream_t s);
+cudaError_t launch_set_u32(uint32_t* arr, const uint32_t* idx, const uint32_t* val, uint32_t n,
+                           cudaStream_t s);
+cudaError_t launch_locate(const long long* ids, uint64_t nslots, bool arena,
+                          const long long* hkeys, const uint32_t* hvals, uint32_t hmask,
+                          uint64_t* loc, cudaStream_t s);
+cudaError_t launch_merge_shards(const float* dists, const long long* ids, uint32_t G, uint32_t nq,
+                                uint32_t k, float* out_d, long long* out_i, uint32_t* out_cnt,
+                                cudaStream_t s);
+
+constexpr uint64_t kArenaBit = 1ull << 63;
+
+}  // namespace bivf

@@ -1,0 +1,73 @@
+// Host-visible declarations for the scan/merge/plan kernels (scan.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bivf {
+
+// Device view of the index's storage (all pointers device memory).
+struct DevLists {
+    uint32_t C, D, T, gpb;   // clusters, dim, block capacity, groups per block
+    uint64_t PS;             // payload scalars per block = gpb*32*D
+    uint32_t MLB;            // max blocks per list (row length of `table`)
+    const float* off_payload;     // offline segments, interleaved, group-aligned
+    const long long* off_ids;     // per slot
+    const uint64_t* off_start;    // per cluster, slot offset (multiple of 32)
+    const uint32_t* off_count;    // per cluster (changed only under quiescence)
+    const float* arena;           // pool payload, num_blocks * PS
+    const long long* bids;        // pool ids, num_blocks * T
+    const int32_t* table;         // per-list block table, C * MLB
+    const uint32_t* len;          // per-list online length (published, acquire)
+};
+
+// Per-search scratch (lease workspace), device pointers.
+struct PlanBufs {
+    uint32_t* snap_off;   // [C]
+    uint32_t* snap_len;   // [C]
+    uint32_t* gc;         // [C] groups per chunk
+    uint32_t* nch;        // [C] chunks
+    uint32_t* cnt;        // [C] pairs per list
+    uint32_t* qoff;       // [C+1]
+    uint32_t* item_off;   // [C+1]
+    uint32_t* n_items;    // [1]
+    uint32_t* item_ctr;   // [1]
+    uint32_t* ppos;       // [npairs]
+    uint32_t* plist;      // [npairs]
+};
+
+struct SearchShape {
+    uint32_t nq, k, P, maxch, gcmin, QT;
+    int metric;
+};
+
+// Picks the device top-k width for k (1,2,4,8 registers per lane).
+int kpl_for(uint32_t k);
+uint32_t qt_for(uint32_t k, uint32_t D);
+
+// Coarse quantizer on CUDA cores (K2 semantics, exact): probes[q*P + p] are
+// the P lowest (key, cluster) pairs; cand_* is scratch of nq*flat_nch*P.
+cudaError_t launch_flat_topk(const float* flat_il, uint32_t n, uint32_t D, const float* queries,
+                             uint32_t nq, uint32_t k, int metric, uint32_t nch, float* cand_d,
+                             long long* cand_i, float* out_d, long long* out_i, uint32_t* out_cnt,
+                             uint32_t* item_ctr, int num_sms, cudaStream_t s);
+
+// The list scan: plan (snapshot, invert probe map, items) + scan + merge.
+cudaError_t launch_ivf_search(const DevLists& L, const PlanBufs& B, const long long* probes,
+                              const float* queries, const SearchShape& sh, float* cand_d,
+                              long long* cand_i, float* out_d, long long* out_i,
+                              uint32_t* out_cnt, int num_sms, cudaStream_t s);
+
+cudaError_t launch_all_probes(long long* probes, uint32_t nq, uint32_t C, cudaStream_t s);
+
+// Copy row-major fp32 rows [n][D] into the 32-interleaved group layout
+// (block_store.hpp:37-40), zero-padding the last group; and the query
+// staging layout [n][Dp] (Dp = D rounded up to 4, zero padded).
+cudaError_t launch_interleave(const float* rows, uint32_t n, uint32_t D, float* out,
+                              cudaStream_t s);
+cudaError_t launch_pad_rows(const float* rows, uint32_t n, uint32_t D, uint32_t Dp, float* out,
+                            cudaStream_t s);
+
+inline uint32_t pad4(uint32_t d) { return (d + 3u) & ~3u; }
+
+}  // namespace bivf
