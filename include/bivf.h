@@ -121,7 +121,8 @@ bivf_status bivf_search_device(bivf_index* h, const float* queries_device, uint6
                                void* stream);
 /* ClusterIndex::assign (ivf_index.cpp:93-105) for n vectors */
 bivf_status bivf_assign(bivf_index* h, const float* y, uint64_t n, uint32_t* out);
-/* probe sets (ivf_index.cpp:271-276): out [nq x nprobe] ascending by (key, cluster) */
+/* probe sets (ivf_index.cpp:271-276): out [nq x nprobe] ascending by (key, cluster)
+ * (nprobe == num_clusters > 256: every cluster, in cluster-id order) */
 bivf_status bivf_probes(bivf_index* h, const float* queries, uint64_t nq, uint64_t nprobe,
                         uint32_t* out);
 /* Delete (extension; the reference has none; rules in DESIGN.md

@@ -631,7 +631,7 @@ void GpuIndex::probes(const float* q, uint64_t nq, uint64_t nprobe, uint32_t* ou
         BIVF_CUDA(cudaMemcpyAsync(w.qraw, q + s * D_, (size_t)m * D_ * 4, cudaMemcpyHostToDevice,
                                   l->stream));
         BIVF_CUDA(launch_pad_rows(w.qraw, m, D_, Dp_, w.queries, l->stream));
-        if (nprobe == C_) {
+        if (nprobe > 256) {  // == C_: every cluster (cluster-id order)
             BIVF_CUDA(launch_all_probes(w.probes, m, C_, l->stream));
         } else {
             BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, w.queries, m,
