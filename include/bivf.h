@@ -181,9 +181,10 @@ bivf_status bivf_merge_topk_device(int32_t device, const float* dists, const int
 /* ---- instrumentation ------------------------------------------------------ */
 /* kernel launches issued by this library since load (bench's gpu_launches) */
 uint64_t bivf_kernel_launches(void);
-/* device time (ms) of the last bivf_search's scan kernel, -1 if not timed */
+/* enable CUDA-event timing of the search phases (on the lease stream) */
 bivf_status bivf_set_timing(bivf_index* h, int enable);
-bivf_status bivf_last_timings(const bivf_index* h, float* out4 /* quantizer, plan, scan, merge ms */);
+/* device ms of the last timed search slice: quantizer, plan, scan kernel, merge */
+bivf_status bivf_last_timings(const bivf_index* h, float* out4);
 
 #ifdef __cplusplus
 }

@@ -417,6 +417,10 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     const size_t o_plan = take((size_t)C_ * 4 * 5 + (size_t)(C_ + 1) * 4 * 2 + 16);
     const size_t o_ppos = take(npairs * 4);
     const size_t o_plist = take(npairs * 4);
+    if (off > l.ws.bytes && l.stream) {
+        // work already queued on this lease may still use the old workspace
+        BIVF_CUDA(cudaStreamSynchronize(l.stream));
+    }
     l.ws.ensure(off);
     char* b = static_cast<char*>(l.ws.p);
     Workspace w;
@@ -457,6 +461,10 @@ LaunchShape pick_shape(uint32_t nq, uint32_t k, uint32_t P, uint32_t C, int sms)
     const uint64_t npairs = (uint64_t)nq * P;
     s.maxch = (uint32_t)std::min<uint64_t>(32, std::max<uint64_t>(1, (target + npairs - 1) / npairs));
     s.gcmin = 2;
+    if (P > 256) {  // nprobe == num_clusters: no quantizer pass
+        s.fnch = 1;
+        return s;
+    }
     const uint32_t qtq = qt_for(P, 0);
     const uint64_t tiles = (nq + qtq - 1) / qtq;
     const uint32_t ng = (C + 31) / 32;
@@ -500,7 +508,8 @@ void GpuIndex::enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uin
     ss.QT = qt_for(k, D_);
     ss.metric = cfg_.metric;
     BIVF_CUDA(launch_ivf_search(dev_lists(), w.plan, w.probes, w.queries, ss, w.cand_d, w.cand_i,
-                                w.out_d, w.out_i, w.out_cnt, num_sms_, l.stream));
+                                w.out_d, w.out_i, w.out_cnt, num_sms_, l.stream,
+                                timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr));
     if (timing_) BIVF_CUDA(cudaEventRecord(l.t4, l.stream));
 }
 
@@ -546,12 +555,7 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
         std::memcpy(out_d + s * k, pd, (size_t)m * k * 4);
         std::memcpy(out_ids + s * k, pi, (size_t)m * k * 8);
         if (out_cnt) std::memcpy(out_cnt + s, pc, (size_t)m * 4);
-        if (timing_) {
-            cudaEventElapsedTime(&last_ms_[0], l->t0, l->t1);
-            cudaEventElapsedTime(&last_ms_[2], l->t1, l->t4);
-            last_ms_[1] = 0;
-            last_ms_[3] = 0;
-        }
+        if (timing_) record_timings(*l);
     }
 }
 
@@ -591,12 +595,19 @@ void GpuIndex::search_device(const float* q_dev, uint64_t nq, uint64_t k, uint64
     }
     BIVF_CUDA(cudaStreamWaitEvent(user, l->done, 0));
     cudaEventDestroy(ue);
-    // the lease workspace is reused by the next caller only after `done`
-    BIVF_CUDA(cudaEventSynchronize(l->done));
+    // No host sync: the lease's workspace is only ever used on the lease's own
+    // stream, so the next search on this lease is stream-ordered after this one.
     if (timing_) {
-        cudaEventElapsedTime(&last_ms_[0], l->t0, l->t1);
-        cudaEventElapsedTime(&last_ms_[2], l->t1, l->t4);
+        BIVF_CUDA(cudaEventSynchronize(l->done));
+        record_timings(*l);
     }
+}
+
+void GpuIndex::record_timings(Lease& l) {
+    cudaEventElapsedTime(&last_ms_[0], l.t0, l.t1);
+    cudaEventElapsedTime(&last_ms_[1], l.t1, l.t2);
+    cudaEventElapsedTime(&last_ms_[2], l.t2, l.t3);
+    cudaEventElapsedTime(&last_ms_[3], l.t3, l.t4);
 }
 
 void GpuIndex::last_timings(float* out4) const {

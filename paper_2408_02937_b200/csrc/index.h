@@ -158,6 +158,7 @@ public:
 
     void set_timing(bool on) { timing_ = on; }
     void last_timings(float* out4) const;
+    void record_timings(Lease& l);
 
 private:
     // --- device storage

@@ -697,7 +697,8 @@ cudaError_t launch_flat_topk(const float* flat_il, uint32_t n, uint32_t D, const
 cudaError_t launch_ivf_search(const DevLists& L, const PlanBufs& B, const long long* probes,
                               const float* queries, const SearchShape& sh, float* cand_d,
                               long long* cand_i, float* out_d, long long* out_i,
-                              uint32_t* out_cnt, int num_sms, cudaStream_t s) {
+                              uint32_t* out_cnt, int num_sms, cudaStream_t s,
+                              cudaEvent_t ev_scan0, cudaEvent_t ev_scan1) {
     if (sh.nq == 0) return cudaSuccess;
     const int kpl = kpl_for(sh.k);
     if (!kpl) return cudaErrorInvalidValue;
@@ -733,8 +734,10 @@ cudaError_t launch_ivf_search(const DevLists& L, const PlanBufs& B, const long l
     p.cand_i = cand_i;
     p.NS = stages_for(L.D);
     p.nslab = (L.D + kSlabDims - 1) / kSlabDims;
+    if (ev_scan0) cudaEventRecord(ev_scan0, s);
     e = launch_scan<false>(kpl, sh.metric, p, num_sms, s);
     if (e != cudaSuccess) return e;
+    if (ev_scan1) cudaEventRecord(ev_scan1, s);
     return launch_merge<false>(kpl, sh.nq, sh.P, sh.maxch, sh.k, probes, B.nch, 0, cand_d, cand_i,
                                out_d, out_i, out_cnt, s);
 }

@@ -56,7 +56,8 @@ cudaError_t launch_flat_topk(const float* flat_il, uint32_t n, uint32_t D, const
 cudaError_t launch_ivf_search(const DevLists& L, const PlanBufs& B, const long long* probes,
                               const float* queries, const SearchShape& sh, float* cand_d,
                               long long* cand_i, float* out_d, long long* out_i,
-                              uint32_t* out_cnt, int num_sms, cudaStream_t s);
+                              uint32_t* out_cnt, int num_sms, cudaStream_t s,
+                              cudaEvent_t ev_scan0 = nullptr, cudaEvent_t ev_scan1 = nullptr);
 
 cudaError_t launch_all_probes(long long* probes, uint32_t nq, uint32_t C, cudaStream_t s);
 

@@ -252,6 +252,14 @@ def test_large_batch_matches_oracle(gpu_ready):
         assert np.array_equal(bits(d100[j, : cnt100[j]]), bits(od))
 
 
+def test_full_probe_many_clusters(gpu_ready):
+    # nprobe == num_clusters > 256 takes the all-probes path (no quantizer pass)
+    ix, orc = make_pair(8, 300, 16, 64, 3000, 300, 5)
+    q = bivf.synthetic_dataset(20, 8, 300, 6)
+    assert_search_equal(ix, orc, q, 10, 300)
+    assert ix.probes(q, 300).shape == (20, 300)
+
+
 def test_snapshot_roundtrip(gpu_ready, tmp_path):
     sc = load_scenario("s1_smoke")
     ix = gpu_from_scenario(sc)
