@@ -242,6 +242,12 @@ def run_ours(args, dist):
     e2e_s = max_over_ranks(dist, time.perf_counter() - t)
     ins_stats = ins.finish()
 
+    # --- p50/p99 of executor requests (10-query batches, the reference's
+    # max_search_batch) without and with the 10K vec/s insert stream
+    latency = None
+    if rank == 0 and world == 1 and not args.no_latency:
+        latency = latency_phase(ix, hq, pool[len(pool) // 2:])
+
     # --- per-kernel timing of the dominant kernel (scan) on its lease stream
     ix.set_timing(True)
     scan_ms = []
@@ -302,11 +308,38 @@ def run_ours(args, dist):
             "gpu_launches": int(launches),
             "clocks": clk,
         }
+        if latency:
+            result["latency"] = latency
         if not args.no_cpu_baseline and world == 1:
             result["cpu_baseline"] = cpu_baseline_from_snapshot(ix, hq)
     barrier(dist)
     ix.close()
     return result
+
+
+LAT_QPS = 1000.0      # search requests / s (x 10 queries each)
+LAT_SECONDS = 4.0
+
+
+def latency_phase(ix, queries, inserts):
+    """Open-loop replay through the native executor (32 lanes): p50/p99 search
+    latency with no inserts and with 10K vec/s inserts (78 req/s x 128)."""
+    from paper_2408_02937_b200.executor import Executor, replay
+    ex = Executor(ix, num_lanes=32)
+    common = dict(k=K, nprobe=NPROBE, search_batch=10, insert_batch=INSERT_BATCH, seed=1,
+                  poisson=True)
+    base = replay(ex, queries, inserts, LAT_QPS, 0.0, LAT_SECONDS, **common)
+    live = replay(ex, queries, inserts, LAT_QPS, INSERT_RATE / INSERT_BATCH, LAT_SECONDS, **common)
+    ex.shutdown()
+    ex.close()
+    p99a, p99b = base["search"]["p99_ms"], live["search"]["p99_ms"]
+    return {"arrivals": "poisson", "search_req_s": LAT_QPS, "queries_per_req": 10,
+            "insert_vec_s": INSERT_RATE, "seconds": LAT_SECONDS,
+            "search_no_inserts_ms": {k2: round(v, 4) for k2, v in base["search"].items()},
+            "search_live_inserts_ms": {k2: round(v, 4) for k2, v in live["search"].items()},
+            "insert_request_ms": {k2: round(v, 4) for k2, v in live["insert"].items()},
+            "p99_ratio_live_vs_idle": round(p99b / p99a, 3) if p99a > 0 else None,
+            "rejected": base["rejected"] + live["rejected"]}
 
 
 def cpu_baseline_from_snapshot(ix, queries):
@@ -391,6 +424,10 @@ def run_reference(args, dist):
         tot += step()
     ins_stats = ins.finish()
     qps = len(sample) * args.steps / tot
+    lat = None
+    if not args.no_latency:
+        lat = ref_latency_phase(L, ref, np.ascontiguousarray(queries[:2000]),
+                                np.ascontiguousarray(pool[len(pool) // 2:]))
     return {
         "metric": METRIC, "value": round(qps, 1), "unit": "queries/s", "n_gpus": dist["world"],
         "steps": args.steps, "warmup": args.warmup,
@@ -408,7 +445,35 @@ def run_reference(args, dist):
                          "sample": f"{len(sample)} queries per step, {cores} threads"},
         "e2e": {"value": round(qps, 1), "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "latency": lat,
     }
+
+
+def ref_latency_phase(L, ref, queries, inserts):
+    """The reference Executor (32 lanes) under the same open-loop load; the
+    request rate is scaled down when the CPU cannot sustain it."""
+    import ctypes as C
+
+    from paper_2408_02937_b200.executor import summarize_latencies
+    out = {}
+    qps = 50.0  # 10-query requests / s: what the host can serve without saturating
+    for name, irate in (("search_no_inserts_ms", 0.0), ("search_live_inserts_ms", INSERT_RATE)):
+        ex = L.ref_exec_create(ref._h, 32, 0)
+        nreq = int(qps * LAT_SECONDS)
+        lat = np.zeros(nreq, np.float64)
+        rej = C.c_uint64(0)
+        rc = L.ref_exec_replay_dim(ex, DIM, queries, nreq, 10, K, NPROBE, qps, inserts,
+                                   len(inserts) if irate > 0 else 0, irate, lat, C.byref(rej))
+        L.ref_exec_destroy(ex)
+        if rc != 0:
+            return {"unavailable": L.ref_last_error().decode()}
+        out[name] = summarize_latencies([v / 1e3 for v in lat if v >= 0])
+        out[name + "_rejected"] = int(rej.value)
+    out["search_req_s"] = qps
+    out["queries_per_req"] = 10
+    a, b = out["search_no_inserts_ms"]["p99_ms"], out["search_live_inserts_ms"]["p99_ms"]
+    out["p99_ratio_live_vs_idle"] = round(b / a, 3) if a > 0 else None
+    return out
 
 
 # --------------------------------------------------------------------------- plumbing
@@ -461,6 +526,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-sample", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

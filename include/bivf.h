@@ -178,6 +178,67 @@ bivf_status bivf_merge_topk_device(int32_t device, const float* dists, const int
                                    uint64_t G, uint64_t nq, uint64_t k, float* out_dists,
                                    int64_t* out_ids, uint32_t* out_counts, void* stream);
 
+/* ---- executor: the multi-lane resource pool (Alg. 4) ---------------------- */
+/* Mirrors blockivf::Executor (include/blockivf/executor.hpp:21-196,
+ * src/executor.cpp): search lanes (thread + GPU lease each) with fail-fast
+ * reject, a dedicated insertion lane with the 128-multiple / cap / interval
+ * batcher, serialized FIFO mode, tickets with submit/start/end stamps. */
+typedef struct bivf_executor bivf_executor;
+typedef struct bivf_ticket bivf_ticket;
+typedef struct {
+    uint32_t num_lanes;          /* default 32 */
+    uint32_t central_grants;     /* default 4 */
+    uint64_t lane_cache_bytes;   /* default 512 KiB (paper 50 MB) */
+    uint64_t central_grant_bytes;/* default 2 MiB (paper 200 MB) */
+    uint32_t flush_interval_ms;  /* default 1000 */
+    uint32_t batch_multiple;     /* default 128 */
+    uint32_t batch_cap;          /* default 1024 */
+    uint32_t max_search_batch;   /* default 10 */
+    int32_t serialized;          /* 0 parallel, 1 serialized FIFO */
+    uint32_t reserved[5];
+} bivf_executor_config;
+typedef struct {
+    int32_t status;   /* 0 pending, 1 done, 2 rejected, 3 error */
+    int32_t type;     /* 0 search, 1 insert */
+    int32_t lane;     /* search lane, num_lanes = data lane */
+    uint32_t nq, k;   /* search shape */
+    uint64_t n;       /* insert: vectors */
+    double latency_us, queue_us, exec_us;
+} bivf_ticket_info;
+typedef struct {
+    double qps_search, qps_insert, duration_s;
+    uint32_t search_batch, insert_batch, k, nprobe;
+    uint64_t seed;
+    int32_t poisson;
+    uint32_t reserved[5];
+} bivf_replay_spec;
+
+bivf_status bivf_executor_create(bivf_index* h, const bivf_executor_config* cfg,
+                                 bivf_executor** out);                        /* Executor ctor */
+bivf_status bivf_executor_destroy(bivf_executor* e);                          /* shutdown + free */
+bivf_status bivf_executor_submit_search(bivf_executor* e, const float* queries, uint64_t nq,
+                                        uint64_t k, uint64_t nprobe, bivf_ticket** out);
+bivf_status bivf_executor_submit_insert(bivf_executor* e, const float* x, uint64_t n,
+                                        const int64_t* ids, bivf_ticket** out);
+bivf_status bivf_executor_flush(bivf_executor* e);                            /* flush_insertions */
+bivf_status bivf_executor_set_mode(bivf_executor* e, int serialized);         /* set_mode */
+bivf_status bivf_executor_shutdown(bivf_executor* e);
+/* rejected, completed, in_flight, grants_outstanding, grants_total,
+ * lane_cache_allocations, lane_double_hold_violations, largest_flush */
+bivf_status bivf_executor_stats(const bivf_executor* e, uint64_t* out8);
+bivf_status bivf_ticket_wait(bivf_ticket* t, bivf_ticket_info* info);       /* Ticket::get */
+/* search: ids/dists [nq x k] + counts [nq]; insert: ids [n] (dists/counts ignored) */
+bivf_status bivf_ticket_results(bivf_ticket* t, int64_t* ids, float* dists, uint32_t* counts);
+bivf_status bivf_ticket_error(bivf_ticket* t, char* buf, uint64_t cap);
+bivf_status bivf_ticket_free(bivf_ticket* t);
+/* open-loop replay (workload.cpp:114-269): per-request latencies in us
+ * (-1 rejected, -2 error), issue order */
+bivf_status bivf_replay(bivf_executor* e, const bivf_replay_spec* spec, const float* queries,
+                        uint64_t nqueries, const float* inserts, uint64_t ninserts,
+                        double* search_lat_us, uint64_t search_cap, uint64_t* n_search,
+                        double* insert_lat_us, uint64_t insert_cap, uint64_t* n_insert,
+                        uint64_t* rejected, uint64_t* errors);
+
 /* ---- instrumentation ------------------------------------------------------ */
 /* kernel launches issued by this library since load (bench's gpu_launches) */
 uint64_t bivf_kernel_launches(void);

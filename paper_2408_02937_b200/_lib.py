@@ -64,6 +64,50 @@ class Config(C.Structure):
     ]
 
 
+class ExecutorConfig(C.Structure):
+    _fields_ = [
+        ("num_lanes", C.c_uint32),
+        ("central_grants", C.c_uint32),
+        ("lane_cache_bytes", C.c_uint64),
+        ("central_grant_bytes", C.c_uint64),
+        ("flush_interval_ms", C.c_uint32),
+        ("batch_multiple", C.c_uint32),
+        ("batch_cap", C.c_uint32),
+        ("max_search_batch", C.c_uint32),
+        ("serialized", C.c_int32),
+        ("reserved", C.c_uint32 * 5),
+    ]
+
+
+class TicketInfo(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32),
+        ("type", C.c_int32),
+        ("lane", C.c_int32),
+        ("nq", C.c_uint32),
+        ("k", C.c_uint32),
+        ("n", C.c_uint64),
+        ("latency_us", C.c_double),
+        ("queue_us", C.c_double),
+        ("exec_us", C.c_double),
+    ]
+
+
+class ReplaySpec(C.Structure):
+    _fields_ = [
+        ("qps_search", C.c_double),
+        ("qps_insert", C.c_double),
+        ("duration_s", C.c_double),
+        ("search_batch", C.c_uint32),
+        ("insert_batch", C.c_uint32),
+        ("k", C.c_uint32),
+        ("nprobe", C.c_uint32),
+        ("seed", C.c_uint64),
+        ("poisson", C.c_int32),
+        ("reserved", C.c_uint32 * 5),
+    ]
+
+
 _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
@@ -114,6 +158,20 @@ SIGNATURES = {
     "bivf_synthetic_dataset": (C.c_int, [u64, u64, u64, u64, _f32p]),
     "bivf_kmeans": (C.c_int, [_f32p, u64, u64, u64, u64, u64, i32, _f32p, _u32p, pu64]),
     "bivf_merge_topk_device": (C.c_int, [i32, vp, vp, u64, u64, u64, vp, vp, vp, vp]),
+    "bivf_executor_create": (C.c_int, [vp, C.POINTER(ExecutorConfig), C.POINTER(vp)]),
+    "bivf_executor_destroy": (C.c_int, [vp]),
+    "bivf_executor_submit_search": (C.c_int, [vp, vp, u64, u64, u64, C.POINTER(vp)]),
+    "bivf_executor_submit_insert": (C.c_int, [vp, vp, u64, vp, C.POINTER(vp)]),
+    "bivf_executor_flush": (C.c_int, [vp]),
+    "bivf_executor_set_mode": (C.c_int, [vp, C.c_int]),
+    "bivf_executor_shutdown": (C.c_int, [vp]),
+    "bivf_executor_stats": (C.c_int, [vp, vp]),
+    "bivf_ticket_wait": (C.c_int, [vp, C.POINTER(TicketInfo)]),
+    "bivf_ticket_results": (C.c_int, [vp, vp, vp, vp]),
+    "bivf_ticket_error": (C.c_int, [vp, C.c_char_p, u64]),
+    "bivf_ticket_free": (C.c_int, [vp]),
+    "bivf_replay": (C.c_int, [vp, C.POINTER(ReplaySpec), vp, u64, vp, u64, vp, u64, pu64, vp, u64,
+                              pu64, pu64, pu64]),
     "bivf_kernel_launches": (u64, []),
     "bivf_set_timing": (C.c_int, [vp, C.c_int]),
     "bivf_last_timings": (C.c_int, [vp, C.POINTER(C.c_float)]),

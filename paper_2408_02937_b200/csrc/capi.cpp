@@ -5,6 +5,7 @@
 #include <string>
 
 #include "../../include/bivf.h"
+#include "executor.h"
 #include "index.h"
 #include "launches.h"
 #include "maint.cuh"
@@ -14,6 +15,12 @@ using bivf::GpuIndex;
 
 struct bivf_index {
     std::unique_ptr<GpuIndex> impl;
+};
+struct bivf_executor {
+    std::unique_ptr<bivf::Executor> impl;
+};
+struct bivf_ticket {
+    bivf::Ticket t;
 };
 
 namespace {
@@ -362,6 +369,156 @@ bivf_status bivf_merge_topk_device(int32_t device, const float* dists, const int
                                             (uint32_t)G, (uint32_t)nq, (uint32_t)k, od,
                                             reinterpret_cast<long long*>(oi), oc,
                                             static_cast<cudaStream_t>(stream)));
+    });
+}
+
+bivf_status bivf_executor_create(bivf_index* h, const bivf_executor_config* cfg,
+                                 bivf_executor** out) {
+    return guard([&] {
+        need(out, "out");
+        *out = nullptr;
+        bivf::ExecConfig c;
+        if (cfg) {
+            if (cfg->num_lanes) c.num_lanes = cfg->num_lanes;
+            if (cfg->central_grants) c.central_grants = cfg->central_grants;
+            if (cfg->lane_cache_bytes) c.lane_cache_bytes = cfg->lane_cache_bytes;
+            if (cfg->central_grant_bytes) c.central_grant_bytes = cfg->central_grant_bytes;
+            if (cfg->flush_interval_ms) c.flush_interval_ms = cfg->flush_interval_ms;
+            if (cfg->batch_multiple) c.batch_multiple = cfg->batch_multiple;
+            if (cfg->batch_cap) c.batch_cap = cfg->batch_cap;
+            if (cfg->max_search_batch) c.max_search_batch = cfg->max_search_batch;
+            c.serialized = cfg->serialized != 0;
+        }
+        auto e = new bivf_executor;
+        try {
+            e->impl = std::make_unique<bivf::Executor>(I(h), c);
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        *out = e;
+    });
+}
+
+namespace {
+bivf::Executor& X(bivf_executor* e) {
+    if (!e || !e->impl) throw Error(BIVF_EINVAL, "null executor handle");
+    return *e->impl;
+}
+}  // namespace
+
+bivf_status bivf_executor_destroy(bivf_executor* e) {
+    return guard([&] { delete e; });
+}
+
+bivf_status bivf_executor_submit_search(bivf_executor* e, const float* q, uint64_t nq, uint64_t k,
+                                        uint64_t nprobe, bivf_ticket** out) {
+    return guard([&] {
+        need(q, "queries");
+        need(out, "out");
+        auto t = X(e).submit_search(q, (uint32_t)nq, (uint32_t)k, (uint32_t)nprobe);
+        *out = new bivf_ticket{t};
+    });
+}
+
+bivf_status bivf_executor_submit_insert(bivf_executor* e, const float* x, uint64_t n,
+                                        const int64_t* ids, bivf_ticket** out) {
+    return guard([&] {
+        need(x, "x");
+        need(out, "out");
+        auto t = X(e).submit_insert(x, n, ids);
+        *out = new bivf_ticket{t};
+    });
+}
+
+bivf_status bivf_executor_flush(bivf_executor* e) {
+    return guard([&] { X(e).flush_insertions(); });
+}
+
+bivf_status bivf_executor_set_mode(bivf_executor* e, int serialized) {
+    return guard([&] { X(e).set_mode(serialized != 0); });
+}
+
+bivf_status bivf_executor_shutdown(bivf_executor* e) {
+    return guard([&] { X(e).shutdown(); });
+}
+
+bivf_status bivf_executor_stats(const bivf_executor* e, uint64_t* out8) {
+    return guard([&] {
+        need(out8, "out");
+        X(const_cast<bivf_executor*>(e)).stats(out8);
+    });
+}
+
+bivf_status bivf_ticket_wait(bivf_ticket* t, bivf_ticket_info* info) {
+    return guard([&] {
+        if (!t || !t->t) throw Error(BIVF_EINVAL, "null ticket");
+        t->t->wait();
+        if (info) {
+            auto& s = *t->t;
+            info->status = (int32_t)s.status;
+            info->type = (int32_t)s.type;
+            info->lane = s.lane;
+            info->nq = s.nq;
+            info->k = s.k;
+            info->n = s.type == bivf::RequestType::Insert ? s.ids.size() : 0;
+            info->latency_us = s.latency_us();
+            info->queue_us = s.queue_us();
+            info->exec_us = s.exec_us();
+        }
+    });
+}
+
+bivf_status bivf_ticket_results(bivf_ticket* t, int64_t* ids, float* dists, uint32_t* counts) {
+    return guard([&] {
+        if (!t || !t->t) throw Error(BIVF_EINVAL, "null ticket");
+        auto& s = *t->t;
+        s.wait();
+        if (ids && !s.ids.empty()) std::memcpy(ids, s.ids.data(), s.ids.size() * 8);
+        if (dists && !s.dists.empty()) std::memcpy(dists, s.dists.data(), s.dists.size() * 4);
+        if (counts && !s.counts.empty()) std::memcpy(counts, s.counts.data(), s.counts.size() * 4);
+    });
+}
+
+bivf_status bivf_ticket_error(bivf_ticket* t, char* buf, uint64_t cap) {
+    return guard([&] {
+        if (!t || !t->t) throw Error(BIVF_EINVAL, "null ticket");
+        if (buf && cap) {
+            const std::string& m = t->t->error;
+            const size_t n = std::min<size_t>(cap - 1, m.size());
+            std::memcpy(buf, m.data(), n);
+            buf[n] = 0;
+        }
+    });
+}
+
+bivf_status bivf_ticket_free(bivf_ticket* t) {
+    return guard([&] { delete t; });
+}
+
+bivf_status bivf_replay(bivf_executor* e, const bivf_replay_spec* spec, const float* queries,
+                        uint64_t nqueries, const float* inserts, uint64_t ninserts,
+                        double* slat, uint64_t scap, uint64_t* ns, double* ilat, uint64_t icap,
+                        uint64_t* ni, uint64_t* rejected, uint64_t* errors) {
+    return guard([&] {
+        need(spec, "spec");
+        bivf::ReplaySpec r;
+        r.qps_search = spec->qps_search;
+        r.qps_insert = spec->qps_insert;
+        r.duration_s = spec->duration_s;
+        r.search_batch = spec->search_batch ? spec->search_batch : 1;
+        r.insert_batch = spec->insert_batch ? spec->insert_batch : 1;
+        r.k = spec->k ? spec->k : 10;
+        r.nprobe = spec->nprobe ? spec->nprobe : 8;
+        r.seed = spec->seed;
+        r.poisson = spec->poisson != 0;
+        auto out = bivf::replay(X(e), r, queries, nqueries, inserts, ninserts);
+        if (ns) *ns = out.search_us.size();
+        if (ni) *ni = out.insert_us.size();
+        if (slat) std::memcpy(slat, out.search_us.data(), std::min<uint64_t>(scap, out.search_us.size()) * 8);
+        if (ilat) std::memcpy(ilat, out.insert_us.data(), std::min<uint64_t>(icap, out.insert_us.size()) * 8);
+        if (rejected) *rejected = out.rejected;
+        if (errors) *errors = out.errors;
     });
 }
 

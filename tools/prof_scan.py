@@ -1,0 +1,41 @@
+"""Profiling driver: build the bench's cfg2 index and run a few 10K-query
+searches (no live inserts), for ncu captures of the scan kernel.
+
+    ncu --set full --clock-control none --import-source on -k regex:scan_kernel \
+        -s 2 -c 1 -o gpurun_out/prof_scan python tools/prof_scan.py
+"""
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2408_02937_b200 as bivf  # noqa: E402
+
+
+def main():
+    n_base = int(os.environ.get("PROF_NBASE", 1_000_000))
+    nq = int(os.environ.get("PROF_NQ", 10_000))
+    nprobe = int(os.environ.get("PROF_NPROBE", 32))
+    k = int(os.environ.get("PROF_K", 10))
+    reps = int(os.environ.get("PROF_REPS", 4))
+    x = bivf.synthetic_dataset(n_base + nq, 128, 4096, 2)
+    np.maximum(np.rint(x, out=x), 0, out=x)
+    base, q = x[:n_base], x[n_base:]
+    cent, _, _ = bivf.kmeans(base[:100_000], 1024, 10, 42)
+    ix = bivf.ClusterIndex.empty(128, 1024, block_capacity=1024, num_blocks=4096)
+    ix.set_centroids(cent)
+    ix.bulk_load(base, ix.assign_batch(base))
+    ix.set_timing(True)
+    for r in range(reps):
+        t = time.perf_counter()
+        ix.search_batch(q, k, nprobe)
+        print(f"rep {r}: {1e3 * (time.perf_counter() - t):.2f} ms wall, phases(ms)="
+              f"{[round(v, 3) for v in ix.last_timings()]}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
