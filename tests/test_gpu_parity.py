@@ -252,6 +252,31 @@ def test_large_batch_matches_oracle(gpu_ready):
         assert np.array_equal(bits(d100[j, : cnt100[j]]), bits(od))
 
 
+def test_quantizer_exact_at_scale(gpu_ready):
+    """cfg2 shape: k-means centroids (C=1024) of SIFT-like data; probe sets and
+    assignments must equal a numpy fp32 sequential-sum ground truth."""
+    x = bivf.synthetic_dataset(120_000, 128, 4096, 2)
+    np.maximum(np.rint(x, out=x), 0, out=x)
+    cent, _, _ = bivf.kmeans(x[:100_000], 1024, 4, 42)
+    ix = ClusterIndex.empty(128, 1024, block_capacity=1024, num_blocks=64)
+    ix.set_centroids(cent)
+    q = x[100_000:100_100]
+
+    def keys(v):
+        acc = np.zeros(1024, np.float32)
+        for d in range(128):
+            t = (v[d] - cent[:, d]).astype(np.float32)
+            acc = (acc + (t * t).astype(np.float32)).astype(np.float32)
+        return acc
+
+    pr = ix.probes(q, 32)
+    asg = ix.assign_batch(x[:3000])
+    for j in range(len(q)):
+        assert np.array_equal(pr[j], np.lexsort((np.arange(1024), keys(q[j])))[:32]), j
+    for i in range(0, 3000, 29):
+        assert asg[i] == int(np.lexsort((np.arange(1024), keys(x[i])))[0]), i
+
+
 def test_full_probe_many_clusters(gpu_ready):
     # nprobe == num_clusters > 256 takes the all-probes path (no quantizer pass)
     ix, orc = make_pair(8, 300, 16, 64, 3000, 300, 5)
