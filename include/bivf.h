@@ -242,6 +242,9 @@ bivf_status bivf_replay(bivf_executor* e, const bivf_replay_spec* spec, const fl
 /* ---- instrumentation ------------------------------------------------------ */
 /* kernel launches issued by this library since load (bench's gpu_launches) */
 uint64_t bivf_kernel_launches(void);
+/* scan kernel selection: 0 auto (tensor-core filtered scan when supported:
+ * L2, k <= 32, 8 <= D <= 128), 1 CUDA-core exact scan only, 2 = auto */
+bivf_status bivf_set_scan_mode(bivf_index* h, int mode);
 /* enable CUDA-event timing of the search phases (on the lease stream) */
 bivf_status bivf_set_timing(bivf_index* h, int enable);
 /* device ms of the last timed search slice: quantizer, plan, scan kernel, merge */

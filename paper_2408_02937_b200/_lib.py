@@ -173,6 +173,7 @@ SIGNATURES = {
     "bivf_replay": (C.c_int, [vp, C.POINTER(ReplaySpec), vp, u64, vp, u64, vp, u64, pu64, vp, u64,
                               pu64, pu64, pu64]),
     "bivf_kernel_launches": (u64, []),
+    "bivf_set_scan_mode": (C.c_int, [vp, C.c_int]),
     "bivf_set_timing": (C.c_int, [vp, C.c_int]),
     "bivf_last_timings": (C.c_int, [vp, C.POINTER(C.c_float)]),
 }

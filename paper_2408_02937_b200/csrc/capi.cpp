@@ -522,6 +522,13 @@ bivf_status bivf_replay(bivf_executor* e, const bivf_replay_spec* spec, const fl
     });
 }
 
+bivf_status bivf_set_scan_mode(bivf_index* h, int mode) {
+    return guard([&] {
+        if (mode < 0 || mode > 2) throw Error(BIVF_EINVAL, "scan mode must be 0, 1 or 2");
+        I(h).set_scan_mode(mode);
+    });
+}
+
 bivf_status bivf_set_timing(bivf_index* h, int enable) {
     return guard([&] { I(h).set_timing(enable != 0); });
 }

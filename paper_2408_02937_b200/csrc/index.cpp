@@ -182,6 +182,8 @@ void GpuIndex::alloc_device() {
     ensure_offline_capacity(32);
     d_arena_.alloc((size_t)NB_ * PS_ * 4);
     BIVF_CUDA(cudaMemset(d_arena_.p, 0, d_arena_.bytes));
+    tc_ok_ = make_group_map(d_arena_.as<float>(), (uint64_t)NB_ * gpb_ * D_, D_, &map_arena_) ==
+             cudaSuccess;
     d_bids_.alloc((size_t)NB_ * T_ * 8);
     BIVF_CUDA(cudaMemset(d_bids_.p, 0xff, d_bids_.bytes));
     d_owner_.alloc((size_t)NB_ * 4);
@@ -196,6 +198,11 @@ void GpuIndex::alloc_device() {
     BIVF_CUDA(cudaMemset(d_nblocks_.p, 0, d_nblocks_.bytes));
     BIVF_CUDA(cudaMemset(d_fail_.p, 0, d_fail_.bytes));
     BIVF_CUDA(cudaMemset(d_table_.p, 0xff, d_table_.bytes));
+    if (D_ > 256) tc_ok_ = false;
+    if (const char* m = std::getenv("BIVF_SCAN")) {
+        if (std::string(m) == "cuda") scan_mode_ = 1;
+        if (std::string(m) == "tc") scan_mode_ = 2;
+    }
     d_run_.alloc((size_t)C_ * 4);
     d_failfrom_.alloc((size_t)C_ * 4);
     d_newlen_.alloc((size_t)C_ * 4);
@@ -211,6 +218,8 @@ void GpuIndex::ensure_offline_capacity(uint64_t slots) {
     BIVF_CUDA(cudaMemset(d_off_pay_.p, 0, d_off_pay_.bytes));
     BIVF_CUDA(cudaMemset(d_off_ids_.p, 0xff, d_off_ids_.bytes));
     off_slots_cap_ = slots;
+    if (make_group_map(d_off_pay_.as<float>(), slots / 32 * D_, D_, &map_off_) != cudaSuccess)
+        tc_ok_ = false;
 }
 
 DevLists GpuIndex::dev_lists() const {
@@ -415,6 +424,11 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     const size_t o_oc = take((size_t)nq * 4);
     const size_t o_ctr = take(16);
     const size_t o_plan = take((size_t)C_ * 4 * 5 + (size_t)(C_ + 1) * 4 * 2 + 16);
+    const size_t runs = npairs * maxch;
+    const size_t o_ub = take(runs * k * 4);
+    const size_t o_cc = take(runs * 4);
+    const size_t o_clb = take(runs * kKC * 4);
+    const size_t o_clo = take(runs * kKC * 4);
     const size_t o_ppos = take(npairs * 4);
     const size_t o_plist = take(npairs * 4);
     if (off > l.ws.bytes && l.stream) {
@@ -446,6 +460,10 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     w.plan.item_off = pl + 6 * C_ + 1;
     w.plan.n_items = pl + 7 * C_ + 2;
     w.plan.item_ctr = pl + 7 * C_ + 3;
+    w.tc.ub = reinterpret_cast<float*>(b + o_ub);
+    w.tc.ccount = reinterpret_cast<uint32_t*>(b + o_cc);
+    w.tc.clb = reinterpret_cast<float*>(b + o_clb);
+    w.tc.cloc = reinterpret_cast<uint32_t*>(b + o_clo);
     w.plan.ppos = reinterpret_cast<uint32_t*>(b + o_ppos);
     w.plan.plist = reinterpret_cast<uint32_t*>(b + o_plist);
     return w;
@@ -473,6 +491,11 @@ LaunchShape pick_shape(uint32_t nq, uint32_t k, uint32_t P, uint32_t C, int sms)
     return s;
 }
 }  // namespace
+
+bool GpuIndex::use_tc(uint32_t k) const {
+    if (scan_mode_ == 1 || !tc_ok_) return false;
+    return tc_supported(D_, k, cfg_.metric);
+}
 
 void GpuIndex::validate_search(uint64_t k, uint64_t nprobe) const {
     // ivf_index.cpp:266-269
@@ -507,9 +530,16 @@ void GpuIndex::enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uin
     ss.gcmin = sh.gcmin;
     ss.QT = qt_for(k, D_);
     ss.metric = cfg_.metric;
-    BIVF_CUDA(launch_ivf_search(dev_lists(), w.plan, w.probes, w.queries, ss, w.cand_d, w.cand_i,
-                                w.out_d, w.out_i, w.out_cnt, num_sms_, l.stream,
-                                timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr));
+    if (use_tc(k)) {
+        BIVF_CUDA(launch_ivf_search_tc(dev_lists(), w.plan, w.probes, w.queries,
+                                       d_cent_.as<float>(), ss, map_off_, map_arena_, w.tc, w.out_d,
+                                       w.out_i, w.out_cnt, num_sms_, l.stream,
+                                       timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr));
+    } else {
+        BIVF_CUDA(launch_ivf_search(dev_lists(), w.plan, w.probes, w.queries, ss, w.cand_d,
+                                    w.cand_i, w.out_d, w.out_i, w.out_cnt, num_sms_, l.stream,
+                                    timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr));
+    }
     if (timing_) BIVF_CUDA(cudaEventRecord(l.t4, l.stream));
 }
 

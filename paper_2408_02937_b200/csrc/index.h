@@ -36,6 +36,7 @@
 #include "../../include/bivf.h"
 #include "insert.cuh"
 #include "scan.cuh"
+#include "scan_tc.cuh"
 
 namespace bivf {
 
@@ -103,6 +104,7 @@ struct Workspace {  // carved from Lease::ws
     uint32_t* out_cnt;
     uint32_t* ctr;
     PlanBufs plan;
+    TcBufs tc;
 };
 
 struct RearrangeEvent {
@@ -157,6 +159,8 @@ public:
     static std::unique_ptr<GpuIndex> load(const std::string& path, const bivf_config* ov);
 
     void set_timing(bool on) { timing_ = on; }
+    void set_scan_mode(int m) { scan_mode_ = m; }
+    bool use_tc(uint32_t k) const;
     void last_timings(float* out4) const;
     void record_timings(Lease& l);
 
@@ -234,6 +238,9 @@ private:
     cudaEvent_t maint_evt_ = nullptr;
     std::atomic<uint64_t> maint_gen_{0};
 
+    CUtensorMap map_off_{}, map_arena_{};
+    bool tc_ok_ = false;
+    int scan_mode_ = 0;  // 0 auto, 1 CUDA-core only, 2 tensor-core when supported
     bool timing_ = false;
     float last_ms_[4] = {-1, -1, -1, -1};
 };

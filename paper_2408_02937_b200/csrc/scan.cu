@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "launches.h"
 #include "scan.cuh"
+#include "scan_common.cuh"
 
 namespace bivf {
 
@@ -53,41 +54,6 @@ struct ScanParams {
     long long* cand_i;
     uint32_t NS, nslab;
 };
-
-struct GroupRef {
-    const float* base;
-    const long long* ids;  // nullptr -> implicit id0 + slot
-    long long id0;
-    uint32_t nvalid;
-};
-
-__device__ __forceinline__ uint32_t ivf_ngroups(const DevLists& L, uint32_t off, uint32_t len) {
-    const uint32_t og = (off + 31u) >> 5;
-    const uint32_t full = len / L.T, rem = len - full * L.T;
-    return og + full * L.gpb + ((rem + 31u) >> 5);
-}
-
-__device__ __forceinline__ GroupRef ivf_group(const DevLists& L, uint32_t c, uint32_t off,
-                                              uint32_t len, uint32_t j) {
-    GroupRef g;
-    const uint32_t og = (off + 31u) >> 5;
-    if (j < og) {
-        const uint64_t slot0 = L.off_start[c] + 32ull * j;
-        g.base = L.off_payload + slot0 * L.D;
-        g.ids = L.off_ids + slot0;
-        g.nvalid = min(32u, off - 32u * j);
-    } else {
-        const uint32_t jj = j - og;
-        const uint32_t mid = jj / L.gpb, gi = jj - mid * L.gpb;
-        const int32_t blk = L.table[(uint64_t)c * L.MLB + mid];
-        const uint32_t cnt_mid = min(L.T, len - mid * L.T);
-        g.base = L.arena + (uint64_t)blk * L.PS + (uint64_t)gi * 32u * L.D;
-        g.ids = L.bids + (uint64_t)blk * L.T + 32u * gi;
-        g.nvalid = min(32u, cnt_mid - 32u * gi);
-    }
-    g.id0 = 0;
-    return g;
-}
 
 struct ItemDesc {
     uint32_t c, pair0, npairs, g0, g1, chunk, off, len;
@@ -692,6 +658,19 @@ cudaError_t launch_flat_topk(const float* flat_il, uint32_t n, uint32_t D, const
     if (e != cudaSuccess) return e;
     return launch_merge<true>(kpl, nq, 1, p.maxch, k, nullptr, nullptr, p.flat_nch, cand_d, cand_i,
                               out_d, out_i, out_cnt, s);
+}
+
+cudaError_t launch_plan(const DevLists& L, const PlanBufs& B, const long long* probes,
+                        const SearchShape& sh, cudaStream_t s) {
+    const uint32_t npairs = sh.nq * sh.P;
+    plan_snapshot<<<(L.C + 255) / 256, 256, 0, s>>>(L, sh.maxch, sh.gcmin, B.snap_off, B.snap_len,
+                                                   B.gc, B.nch, B.cnt);
+    plan_count<<<(npairs + 255) / 256, 256, 0, s>>>(probes, npairs, B.cnt, B.ppos);
+    plan_scan<<<1, 1024, 0, s>>>(L.C, sh.QT, B.cnt, B.nch, B.qoff, B.item_off, B.n_items,
+                                 B.item_ctr);
+    plan_scatter<<<(npairs + 255) / 256, 256, 0, s>>>(probes, npairs, B.qoff, B.ppos, B.plist);
+    count_launch(4);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_ivf_search(const DevLists& L, const PlanBufs& B, const long long* probes,

@@ -61,6 +61,10 @@ cudaError_t launch_ivf_search(const DevLists& L, const PlanBufs& B, const long l
 
 cudaError_t launch_all_probes(long long* probes, uint32_t nq, uint32_t C, cudaStream_t s);
 
+// Only the plan kernels (snapshot, count, scan, scatter) of launch_ivf_search.
+cudaError_t launch_plan(const DevLists& L, const PlanBufs& B, const long long* probes,
+                        const SearchShape& sh, cudaStream_t s);
+
 // Copy row-major fp32 rows [n][D] into the 32-interleaved group layout
 // (block_store.hpp:37-40), zero-padding the last group; and the query
 // staging layout [n][Dp] (Dp = D rounded up to 4, zero padded).

@@ -1,0 +1,48 @@
+// Device helpers shared by the CUDA-core scan (scan.cu) and the tensor-core
+// scan (scan_tc.cu): where group j of list c lives (offline segment groups
+// first, then the online blocks through the list's block table).
+#pragma once
+
+#include <cstdint>
+
+#include "scan.cuh"
+
+namespace bivf {
+
+struct GroupRef {
+    const float* base;
+    const long long* ids;  // nullptr -> implicit id0 + slot
+    long long id0;
+    uint32_t nvalid;
+};
+
+__device__ __forceinline__ uint32_t ivf_ngroups(const DevLists& L, uint32_t off, uint32_t len) {
+    const uint32_t og = (off + 31u) >> 5;
+    const uint32_t full = len / L.T, rem = len - full * L.T;
+    return og + full * L.gpb + ((rem + 31u) >> 5);
+}
+
+__device__ __forceinline__ GroupRef ivf_group(const DevLists& L, uint32_t c, uint32_t off,
+                                              uint32_t len, uint32_t j) {
+    GroupRef g;
+    const uint32_t og = (off + 31u) >> 5;
+    if (j < og) {
+        const uint64_t slot0 = L.off_start[c] + 32ull * j;
+        g.base = L.off_payload + slot0 * L.D;
+        g.ids = L.off_ids + slot0;
+        g.nvalid = min(32u, off - 32u * j);
+    } else {
+        const uint32_t jj = j - og;
+        const uint32_t mid = jj / L.gpb, gi = jj - mid * L.gpb;
+        const int32_t blk = L.table[(uint64_t)c * L.MLB + mid];
+        const uint32_t cnt_mid = min(L.T, len - mid * L.T);
+        g.base = L.arena + (uint64_t)blk * L.PS + (uint64_t)gi * 32u * L.D;
+        g.ids = L.bids + (uint64_t)blk * L.T + 32u * gi;
+        g.nvalid = min(32u, cnt_mid - 32u * gi);
+    }
+    g.id0 = 0;
+    return g;
+}
+
+
+}  // namespace bivf

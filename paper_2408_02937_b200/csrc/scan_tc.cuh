@@ -1,0 +1,37 @@
+// Host-visible declarations for the tensor-core filtered scan (scan_tc.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "scan.cuh"
+
+namespace bivf {
+
+constexpr uint32_t kKC = 32;  // candidate slots per (query, list chunk) run
+
+// per-search scratch of the TC path (lease workspace)
+struct TcBufs {
+    float* ub;          // [runs][k]  upper bounds (k smallest)
+    uint32_t* ccount;   // [runs]     candidates kept (kKC + 1 = overflow -> exact rescan)
+    float* clb;         // [runs][kKC] lower bounds
+    uint32_t* cloc;     // [runs][kKC] group << 5 | slot
+};
+
+bool tc_supported(uint32_t D, uint32_t k, int metric);
+
+// 2-D TMA map over a region of 32-float rows (one dim of one 32-vector
+// group per row), box = {32, D}, SWIZZLE_128B.
+cudaError_t make_group_map(const float* base, uint64_t rows, uint32_t D, CUtensorMap* out);
+
+cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,
+                                 const float* queries, const float* centroids,
+                                 const SearchShape& sh, const CUtensorMap& map_off,
+                                 const CUtensorMap& map_arena, const TcBufs& T, float* out_d,
+                                 long long* out_i, uint32_t* out_cnt, int num_sms,
+                                 cudaStream_t s, cudaEvent_t ev0 = nullptr,
+                                 cudaEvent_t ev1 = nullptr);
+
+}  // namespace bivf

@@ -327,7 +327,12 @@ class ClusterIndex:
         check(lib().bivf_load_snapshot(str(path).encode(), C.byref(ov), C.byref(h)))
         return ClusterIndex(_handle=h.value)
 
-    # ------------------------------------------------------------ timing
+    # ------------------------------------------------------------ kernels / timing
+    def set_scan_mode(self, mode="auto"):
+        """'auto' (tensor-core filtered scan where supported), 'cuda' (CUDA-core exact scan)."""
+        m = {"auto": 0, "cuda": 1, "tc": 2}[mode]
+        check(lib().bivf_set_scan_mode(self._h, m))
+
     def set_timing(self, on=True):
         check(lib().bivf_set_timing(self._h, 1 if on else 0))
 
