@@ -8,8 +8,8 @@
 // Design.  Exact distances are sequential fp32 sums, so
 // tensor cores can only FILTER: per work item (list c, tile of <=128 queries,
 // chunk of groups) a persistent CTA
-//   producer warp : TMA (cp.async.bulk.tensor.2d, SWIZZLE_128B) of each
-//                   32-vector group, dims as rows -> an MN-major SW128 B tile
+//   producer warp : TMA (cp.async.bulk.tensor.2d, SWIZZLE_128B_ATOM_32B) of
+//                   each 32-vector group, dims as rows -> MN-major B tile
 //   math warps    : centre the tile in place (x - c_list), per-slot residual
 //                   norms, and build A = centred queries (K-major SW128)
 //   MMA warp      : tcgen05.mma.kind::tf32 128x32xD into TMEM (4 buffers)
@@ -45,7 +45,9 @@ constexpr int kNS = 4;              // smem stages (one group each)
 constexpr int kNB = 4;              // TMEM accumulator buffers (32 columns each)
 constexpr int kMaxD = 128;
 constexpr int kStageBytes = kMaxD * 128;       // 128 rows (dims) x 128 B
-constexpr int kABytes = kMaxD * kM * 4;        // 4 K-blocks x 128 rows x 128 B
+constexpr int kStagePair = 2 * kStageBytes;    // s_hi (TMA target, split in place) + s_lo
+// TMEM columns: A_hi [0,128), A_lo [128,256), accumulators [256, 256 + 32*kNB)
+constexpr uint32_t kColAlo = 128, kColAcc = 256, kTmemCols = 512;
 
 struct TcParams {
     DevLists L;
@@ -89,14 +91,19 @@ __device__ __forceinline__ void tc_fence_after() {
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-// SW128 smem matrix descriptor (version 1, layout type 2 = SWIZZLE_128B)
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA smem matrix descriptor (version 1).  layout 2 = SWIZZLE_128B (A: K-major,
+// 8 rows x 128 B atoms); layout 1 = SWIZZLE_128B_BASE32B (B: MN-major 32-bit,
+// 4 rows x 128 B atoms with 32-byte chunks swizzled by row, which is what TMA
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B writes; the plain 128B swizzle is not a
+// valid MN-major TF32 operand).  Verified on B200 by tools/tc_probe.cu.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
     d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
     d |= 1ull << 46;
-    d |= 2ull << 61;
+    d |= (uint64_t)layout << 61;
     return d;
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
@@ -107,6 +114,29 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
         : "memory");
+}
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+#define BIVF_TMEM_ST32(addr, v)                                                                  \
+    asm volatile(                                                                                \
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12," \
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::     \
+            "r"(addr),                                                                           \
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),  \
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),        \
+        "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),      \
+        "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),      \
+        "r"(v[29]), "r"(v[30]), "r"(v[31])                                                       \
+        : "memory")
+__device__ __forceinline__ float tf32_trunc(float x) {
+    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile(
@@ -132,16 +162,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// Bound on |a - e| where a = approximate (TF32 MMA on centred residuals) and
-// e = the reference's sequential fp32 l2_sqr.  With r = q-c, s = x-c rounded to
-// fp32 and TF32 operands (<= 2^-10 relative each, truncation), fp32 tensor
-// accumulation over K <= 128 terms and fp32 norms:
-//   |P - r.s| <= (2^-9 + 2^-16) |r||s|,   |nq - |r|^2| <= 2^-17 |r|^2 (same for s),
-//   |e - |q-x|^2| <= (D+2) 2^-24 |q-x|^2,  | |r-s| - |q-x| | <= 2^-23 (|r|+|s|).
-// Constants below carry a 2x margin (DESIGN.md §Scan-TC error bound).
+// Bound on |a - e| where a = nq + ns - 2P is the tensor-core approximation and e
+// the reference's sequential fp32 l2_sqr (DESIGN.md §Scan-TC error bound).
+// r = fl(q-c), s = fl(x-c); 3xTF32: P = r_hi.s_hi + r_hi.s_lo + r_lo.s_hi with
+// explicit truncation (r = r_hi + r_lo exactly), so the dropped r_lo.s_lo and the
+// TF32 truncation of the lo parts are <= ~2^-20 sum|r_d s_d|; fp32 accumulation of
+// 3*D/8 MMA steps adds <= 48*2^-24 sum|r_d s_d| (D=128): |P - r.s| <= 2^-16 |r||s|
+// (measured worst 2^-20.3 on B200, tools/tc_probe_ts.cu).  Norms: sequential fp32,
+// |nq - |r|^2| <= (D+1) 2^-24 |r|^2; exact value: |e - |q-x|^2| <= (D+2) 2^-24 |q-x|^2;
+// centring: | |r-s|^2 - |q-x|^2 | <= 2^-22 (|r|^2 + |s|^2).  Constants carry >= 2x margin.
+constexpr float kEpsCross = 1.0f / 16384.0f;  // 2 * 2^-15 >= 2 * 2 * 2^-16 on |r||s|
+constexpr float kEpsRel = 1.0f / 32768.0f;    // 2^-15 on (nq+ns) and on |a|
 __device__ __forceinline__ float err_bound(float nq, float ns, float a) {
-    const float rs = sqrtf(nq * ns);
-    return 0.0078125f * rs + 6.2e-5f * (nq + ns) + 6.2e-5f * fabsf(a) + 1e-30f;
+    return kEpsCross * sqrtf(nq * ns) + kEpsRel * (nq + ns) + kEpsRel * fabsf(a) + 1e-30f;
 }
 
 struct TcItem {
@@ -189,6 +222,100 @@ __device__ __forceinline__ void group_row(const DevLists& L, uint32_t c, uint32_
     }
 }
 
+// One accumulator buffer (32 dot products of this thread's query) -> bounds,
+// k smallest upper bounds, candidate buffer.
+template <int KT>
+__device__ __forceinline__ void tc_epilogue(const TcParams& p, const TcItem& d, uint32_t eunit,
+                                            uint32_t j, uint64_t* acc_full, uint64_t* acc_empty,
+                                            const float* nsum, const float* ssq, uint32_t tmem_base,
+                                            uint32_t taddr_lane, int lane, bool active, float nq,
+                                            float sqq, float (&ubl)[KT], float& ubk,
+                                            uint32_t& ncand, bool& overflow, float* my_lb,
+                                            uint32_t* my_loc, float* scratch) {
+    const uint32_t b = eunit % kNB;
+    mbar_wait(&acc_full[b], (eunit / kNB) & 1);
+    tc_fence_after();
+    float dot[32];
+    tmem_ld32(tmem_base + taddr_lane + kColAcc + b * 32, dot);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&acc_empty[b]);
+    if (!active) return;
+    // valid slots of group j, from the snapshot (no table lookups)
+    uint32_t nvalid;
+    {
+        const uint32_t og = (d.off + 31u) >> 5;
+        if (j < og) {
+            nvalid = min(32u, d.off - 32u * j);
+        } else {
+            const uint32_t jj = j - og, mid = jj / p.L.gpb, gi = jj - mid * p.L.gpb;
+            nvalid = min(32u, min(p.L.T, d.len - mid * p.L.T) - 32u * gi);
+        }
+    }
+    const float* ns = nsum + b * 32;
+    const float* ss = ssq + b * 32;
+    const uint32_t jl = j << 5;
+    // pass 1 (unrolled, registers only): which slots could still enter the top-k
+    uint32_t need = 0;
+#pragma unroll
+    for (uint32_t n = 0; n < 32; ++n) {
+        const float nx = ns[n];
+        const float a = fmaf(-2.f, dot[n], nq + nx);
+        // err_bound(nq, nx, a) with sqrt(nq*nx) = sqrt(nq)*sqrt(nx) precomputed
+        const float e = fmaf(kEpsCross * sqq, ss[n],
+                             fmaf(kEpsRel, fabsf(a), fmaf(kEpsRel, nq + nx, 1e-30f)));
+        need |= (n < nvalid && a - e <= ubk) ? (1u << n) : 0u;  // hi < ubk implies lo <= ubk
+    }
+    if (!need) return;
+    // pass 2 (rare): park the dot products in this thread's scratch, walk the slots in order
+#pragma unroll
+    for (uint32_t n = 0; n < 32; ++n) scratch[n * kM] = dot[n];
+    while (need) {
+        const uint32_t n = __ffs(need) - 1;
+        need &= need - 1;
+        const float nx = ns[n];
+        const float a = fmaf(-2.f, scratch[n * kM], nq + nx);
+        const float e = fmaf(kEpsCross * sqq, ss[n],
+                             fmaf(kEpsRel, fabsf(a), fmaf(kEpsRel, nq + nx, 1e-30f)));
+        const float h = a + e, l = a - e;
+        if (h < ubk) {  // keep the k smallest upper bounds, sorted
+            float x = h;
+#pragma unroll
+            for (int i = 0; i < KT; ++i) {
+                if (i < (int)p.k && x < ubl[i]) {
+                    const float t = ubl[i];
+                    ubl[i] = x;
+                    x = t;
+                }
+            }
+            float kk = ubl[0];
+#pragma unroll
+            for (int i = 1; i < KT; ++i)
+                if (i == (int)p.k - 1) kk = ubl[i];
+            ubk = kk;
+        }
+        if (l <= ubk && !overflow) {
+            if (ncand == kKC) {  // compact against the tighter threshold
+                uint32_t w = 0;
+                for (uint32_t i = 0; i < kKC; ++i)
+                    if (my_lb[i * kM] <= ubk) {
+                        my_lb[w * kM] = my_lb[i * kM];
+                        my_loc[w * kM] = my_loc[i * kM];
+                        ++w;
+                    }
+                ncand = w;
+            }
+            if (ncand < kKC) {
+                my_lb[ncand * kM] = l;
+                my_loc[ncand * kM] = jl | n;
+                ++ncand;
+            } else {
+                overflow = true;
+            }
+        }
+    }
+}
+
 template <int KT>
 __global__ void __launch_bounds__(kTcThreads, 1)
     scan_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_off,
@@ -197,14 +324,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // 1024-align the dynamic smem base (SWIZZLE_128B atoms)
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    unsigned char* sA = smem;                                  // kABytes
-    unsigned char* sB = sA + kABytes;                          // kNS * kStageBytes
-    float* cent_s = reinterpret_cast<float*>(sB + kNS * kStageBytes);       // kMaxD
-    float* npart = cent_s + kMaxD;                             // [kNB][4][32]
-    float* nsum = npart + kNB * 4 * 32;                        // [kNB][32]
-    float* cand_lb = nsum + kNB * 32;                          // [128][kKC]
+    unsigned char* sB = smem;                                  // kNS * kStagePair
+    float* cent_s = reinterpret_cast<float*>(sB + kNS * kStagePair);        // kMaxD
+    float* npart = cent_s + kMaxD;                             // [kNB][16][32]
+    float* nsum = npart + kNB * 16 * 32;                       // [kNB][32]
+    float* ssq = nsum + kNB * 32;                              // [kNB][32] sqrt(nsum)
+    float* cand_lb = ssq + kNB * 32;                           // [kKC][128] (index-major)
     uint32_t* cand_loc = reinterpret_cast<uint32_t*>(cand_lb + kM * kKC);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(cand_loc + kM * kKC);
+    float* scr = reinterpret_cast<float*>(cand_loc + kM * kKC);  // [32][128] epilogue scratch
+    uint64_t* bars = reinterpret_cast<uint64_t*>(scr + 32 * kM);
     uint64_t* full = bars;                // kNS
     uint64_t* empty = full + kNS;         // kNS
     uint64_t* cent_full = empty + kNS;    // kNS
@@ -239,14 +367,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (p.Dk != D) {
         for (uint32_t i = threadIdx.x; i < kNS * (p.Dk - D) * 32; i += blockDim.x) {
             const uint32_t s = i / ((p.Dk - D) * 32), r = i % ((p.Dk - D) * 32);
-            reinterpret_cast<float*>(sB + s * kStageBytes + D * 128)[r] = 0.f;
+            reinterpret_cast<float*>(sB + s * kStagePair + D * 128)[r] = 0.f;
+            reinterpret_cast<float*>(sB + s * kStagePair + kStageBytes + D * 128)[r] = 0.f;
         }
     }
     fence_proxy_async();  // the zeroed padding rows are read by the async proxy
     if (warp == 1) {  // TMEM: kNB accumulators x 32 fp32 columns
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"(kNB * 32)
+                     "r"(kTmemCols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -276,7 +405,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     int row;
                     group_row(p.L, d.c, d.off, j, ar, row);
                     mbar_arrive_expect_tx(&full[st], D * 128u);
-                    tma_load_2d(sB + st * kStageBytes, ar ? &map_arena : &map_off, 0, row, &full[st]);
+                    tma_load_2d(sB + st * kStagePair, ar ? &map_arena : &map_off, 0, row, &full[st]);
                 }
             }
         }
@@ -302,12 +431,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 mbar_wait(&acc_empty[b], ((unit / kNB) & 1) ^ 1);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB + st * kStageBytes);
+                    // 3xTF32: A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (A from TMEM, B from smem)
+                    const uint32_t bh0 = smem_u32(sB + st * kStagePair), bl0 = bh0 + kStageBytes;
+                    const uint32_t dcol = tmem_base + kColAcc + b * 32;
                     for (uint32_t ks = 0; ks < p.Dk / 8; ++ks) {
-                        const uint32_t kb = ks >> 2, kin = ks & 3;
-                        const uint64_t ad = sw128_desc(a0 + kb * (kM * 128) + kin * 32, 16, 1024);
-                        const uint64_t bd = sw128_desc(b0 + ks * 1024, 4096, 1024);
-                        mma_tf32(tmem_base + b * 32, ad, bd, idesc, ks > 0 ? 1u : 0u);
+                        const uint64_t bh = umma_desc(bh0 + ks * 1024, 16384, 512, 1);
+                        const uint64_t bl = umma_desc(bl0 + ks * 1024, 16384, 512, 1);
+                        const uint32_t ah = tmem_base + ks * 8, al = tmem_base + kColAlo + ks * 8;
+                        mma_tf32_ts(dcol, ah, bh, idesc, ks > 0 ? 1u : 0u);
+                        mma_tf32_ts(dcol, ah, bl, idesc, 1u);
+                        mma_tf32_ts(dcol, al, bh, idesc, 1u);
                     }
                     mma_commit(&acc_full[b]);
                     mma_commit(&empty[st]);
@@ -320,8 +453,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int mt = threadIdx.x - 64;             // 0..127
         const int m = 32 * (warp & 3) + lane;        // TMEM lane / query row of the tile
         const uint32_t taddr_lane = (uint32_t)(32 * (warp & 3)) << 16;
-        float* my_lb = cand_lb + m * kKC;
-        uint32_t* my_loc = cand_loc + m * kKC;
+        float* my_lb = cand_lb + m;       // entry i at my_lb[i * kM]
+        uint32_t* my_loc = cand_loc + m;
+        float* my_scr = scr + m;
         uint32_t unit = 0;
         for (uint32_t seq = 0;; ++seq) {
             const uint32_t rs = seq & 1;
@@ -334,36 +468,33 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             // centroid of the list
             for (uint32_t i = mt; i < D; i += 128) cent_s[i] = p.centroids[(uint64_t)d.c * D + i];
             named_bar(1, 128);
-            // A = centred queries, K-major SW128: row m, K-block kb at kb*16KB + m*128,
-            // 16-byte chunk (k%32)/4 swizzled by m%8.
+            // A = centred queries r = q - c, split r = r_hi + r_lo (r_hi = TF32 truncation,
+            // r_lo exact in fp32) into TMEM: lane m = query row, columns = dims.
             const bool active = (uint32_t)m < d.npairs;
             uint32_t pair = 0;
             float nq = 0.f;
+            const float* q = nullptr;
             if (active) {
                 pair = d.pairs[m];
-                const float* q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
-                for (uint32_t k0 = 0; k0 < p.Dk; k0 += 4) {
-                    float4 r;
-                    r.x = k0 + 0 < D ? __fsub_rn(q[k0 + 0], cent_s[k0 + 0]) : 0.f;
-                    r.y = k0 + 1 < D ? __fsub_rn(q[k0 + 1], cent_s[k0 + 1]) : 0.f;
-                    r.z = k0 + 2 < D ? __fsub_rn(q[k0 + 2], cent_s[k0 + 2]) : 0.f;
-                    r.w = k0 + 3 < D ? __fsub_rn(q[k0 + 3], cent_s[k0 + 3]) : 0.f;
-                    nq = __fadd_rn(nq, __fmul_rn(r.x, r.x));
-                    nq = __fadd_rn(nq, __fmul_rn(r.y, r.y));
-                    nq = __fadd_rn(nq, __fmul_rn(r.z, r.z));
-                    nq = __fadd_rn(nq, __fmul_rn(r.w, r.w));
-                    const uint32_t kb = k0 >> 5, ch = (k0 & 31) >> 2;
-                    *reinterpret_cast<float4*>(sA + kb * (kM * 128) + m * 128 +
-                                               ((ch ^ (m & 7)) << 4)) = r;
-                }
-            } else {
-                for (uint32_t k0 = 0; k0 < p.Dk; k0 += 4) {
-                    const uint32_t kb = k0 >> 5, ch = (k0 & 31) >> 2;
-                    *reinterpret_cast<float4*>(sA + kb * (kM * 128) + m * 128 +
-                                               ((ch ^ (m & 7)) << 4)) = make_float4(0, 0, 0, 0);
-                }
+                q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
             }
-            fence_proxy_async();
+            for (uint32_t c0 = 0; c0 < p.Dk; c0 += 32) {
+                uint32_t vh[32], vl[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const uint32_t k = c0 + i;
+                    float r = 0.f;
+                    if (active && k < D) r = __fsub_rn(q[k], cent_s[k]);
+                    nq = __fadd_rn(nq, __fmul_rn(r, r));
+                    const float h = tf32_trunc(r);
+                    vh[i] = __float_as_uint(h);
+                    vl[i] = __float_as_uint(__fsub_rn(r, h));
+                }
+                BIVF_TMEM_ST32(tmem_base + taddr_lane + c0, vh);
+                BIVF_TMEM_ST32(tmem_base + taddr_lane + kColAlo + c0, vl);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
             named_bar(1, 128);
             if (mt == 0 && d.g1 > d.g0) mbar_arrive(a_full);
 
@@ -375,94 +506,59 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             uint32_t ncand = 0;
             bool overflow = false;
 
-            auto epilogue = [&](uint32_t eunit, uint32_t j) {
-                const uint32_t b = eunit % kNB;
-                mbar_wait(&acc_full[b], (eunit / kNB) & 1);
-                tc_fence_after();
-                float dot[32];
-                tmem_ld32(tmem_base + taddr_lane + b * 32, dot);
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&acc_empty[b]);
-                if (!active) return;
-                const GroupRef g = ivf_group(p.L, d.c, d.off, d.len, j);
-                const float* ns = nsum + b * 32;
-                const uint32_t jl = j << 5;
-#pragma unroll 4
-                for (uint32_t n = 0; n < 32; ++n) {
-                    if (n >= g.nvalid) break;
-                    const float nx = ns[n];
-                    const float a = nq + nx - 2.f * dot[n];
-                    const float e = err_bound(nq, nx, a);
-                    const float hi = a + e, lo = a - e;
-                    if (hi < ubk) {  // keep the KT smallest upper bounds, sorted
-                        float x = hi;
-#pragma unroll
-                        for (int i = 0; i < KT; ++i) {
-                            if (i < (int)p.k && x < ubl[i]) {
-                                const float t = ubl[i];
-                                ubl[i] = x;
-                                x = t;
-                            }
-                        }
-                        float kk = ubl[0];
-#pragma unroll
-                        for (int i = 1; i < KT; ++i)
-                            if (i == (int)p.k - 1) kk = ubl[i];
-                        ubk = kk;
-                    }
-                    if (lo <= ubk && !overflow) {
-                        if (ncand == kKC) {  // compact against the tighter threshold
-                            uint32_t w = 0;
-                            for (uint32_t i = 0; i < kKC; ++i)
-                                if (my_lb[i] <= ubk) {
-                                    my_lb[w] = my_lb[i];
-                                    my_loc[w] = my_loc[i];
-                                    ++w;
-                                }
-                            ncand = w;
-                        }
-                        if (ncand < kKC) {
-                            my_lb[ncand] = lo;
-                            my_loc[ncand] = jl | n;
-                            ++ncand;
-                        } else {
-                            overflow = true;
-                        }
-                    }
-                }
-            };
-
-            uint32_t first_unit = unit;
+            const float sqq = sqrtf(nq);
             for (uint32_t j = d.g0; j < d.g1; ++j, ++unit) {
                 const uint32_t st = unit % kNS, b = unit % kNB;
                 mbar_wait(&full[st], (unit / kNS) & 1);
-                // centre in place: thread -> slot (mt & 31), rows (mt >> 5) + 4i
+                // centre in place; thread -> slots 4*(mt&7)..+3, rows (mt>>3) + 16i.
+                // 128B_ATOM_32B swizzle: 32-byte chunk (slot/8) ^ (row % 4).
                 {
-                    const uint32_t slot = mt & 31, r0 = mt >> 5;
-                    unsigned char* base = sB + st * kStageBytes;
-                    float part = 0.f;
-                    for (uint32_t k = r0; k < D; k += 4) {
-                        float* px = reinterpret_cast<float*>(
-                            base + k * 128 + ((((slot >> 2) ^ (k & 7))) << 4) + (slot & 3) * 4);
-                        const float sv = __fsub_rn(*px, cent_s[k]);
-                        *px = sv;
-                        part = __fadd_rn(part, __fmul_rn(sv, sv));
+                    const uint32_t sq = mt & 7, r0 = mt >> 3;
+                    unsigned char* base = sB + st * kStagePair;
+                    float4 part = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (uint32_t k = r0; k < D; k += 16) {
+                        const uint32_t off = k * 128 + (((sq >> 1) ^ (k & 3)) << 5) + (sq & 1) * 16;
+                        float4* px = reinterpret_cast<float4*>(base + off);
+                        float4* pl = reinterpret_cast<float4*>(base + kStageBytes + off);
+                        float4 v = *px;
+                        const float cc = cent_s[k];
+                        v.x = __fsub_rn(v.x, cc);
+                        v.y = __fsub_rn(v.y, cc);
+                        v.z = __fsub_rn(v.z, cc);
+                        v.w = __fsub_rn(v.w, cc);
+                        part.x = fmaf(v.x, v.x, part.x);
+                        part.y = fmaf(v.y, v.y, part.y);
+                        part.z = fmaf(v.z, v.z, part.z);
+                        part.w = fmaf(v.w, v.w, part.w);
+                        const float4 h = make_float4(tf32_trunc(v.x), tf32_trunc(v.y), tf32_trunc(v.z),
+                                                     tf32_trunc(v.w));
+                        *px = h;
+                        *pl = make_float4(__fsub_rn(v.x, h.x), __fsub_rn(v.y, h.y),
+                                          __fsub_rn(v.z, h.z), __fsub_rn(v.w, h.w));
                     }
-                    npart[(b * 4 + r0) * 32 + slot] = part;
+                    *reinterpret_cast<float4*>(npart + (b * 16 + r0) * 32 + 4 * sq) = part;
                 }
                 fence_proxy_async();
                 named_bar(1, 128);
                 if (mt < 32) {
-                    const float* pp = npart + b * 128;
-                    nsum[b * 32 + mt] = pp[mt] + pp[32 + mt] + pp[64 + mt] + pp[96 + mt];
+                    const float* pp = npart + b * 512 + mt;
+                    float t = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) t += pp[32 * i];
+                    nsum[b * 32 + mt] = t;
+                    ssq[b * 32 + mt] = sqrtf(t);
                 }
                 if (mt == 0) mbar_arrive(&cent_full[st]);
                 named_bar(1, 128);
-                if (j > d.g0) epilogue(unit - 1, j - 1);
+                if (j > d.g0)
+                    tc_epilogue<KT>(p, d, unit - 1, j - 1, acc_full, acc_empty, nsum, ssq, tmem_base,
+                                    taddr_lane, lane, active, nq, sqq, ubl, ubk, ncand, overflow,
+                                    my_lb, my_loc, my_scr);
             }
-            if (d.g1 > d.g0) epilogue(unit - 1, d.g1 - 1);
-            (void)first_unit;
+            if (d.g1 > d.g0)
+                tc_epilogue<KT>(p, d, unit - 1, d.g1 - 1, acc_full, acc_empty, nsum, ssq, tmem_base,
+                                taddr_lane, lane, active, nq, sqq, ubl, ubk, ncand, overflow, my_lb,
+                                my_loc, my_scr);
 
             // item output: k upper bounds + surviving candidates
             if (active) {
@@ -473,9 +569,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 uint32_t w = 0;
                 if (!overflow) {
                     for (uint32_t i = 0; i < ncand; ++i)
-                        if (my_lb[i] <= ubk) {
-                            p.clb[run * kKC + w] = my_lb[i];
-                            p.cloc[run * kKC + w] = my_loc[i];
+                        if (my_lb[i * kM] <= ubk) {
+                            p.clb[run * kKC + w] = my_lb[i * kM];
+                            p.cloc[run * kKC + w] = my_loc[i * kM];
                             ++w;
                         }
                 }
@@ -488,23 +584,42 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(kNB * 32)
+                     "r"(kTmemCols)
                      : "memory");
     }
 }
 
 // ------------------------------------------------------------------ refine
 // One warp per query: threshold = k-th smallest upper bound over all of the
-// query's (probe, chunk) runs; exact fp32 distance of every surviving
-// candidate; exact top-k.  Overflowed runs are rescanned exactly.
+// query's (probe, chunk) runs; the surviving candidates (lower bound <=
+// threshold) are compacted into a per-warp queue and recomputed EXACTLY
+// (sequential fp32, the reference's bits), 32 at a time, loads batched for
+// memory-level parallelism; exact top-k.  Overflowed runs are rescanned.
+__device__ __forceinline__ float exact_l2(const float* qs, const float* x, uint32_t D) {
+    float acc = 0.f;
+    uint32_t d0 = 0;
+    for (; d0 + 16 <= D; d0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = x[(d0 + i) * 32];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc = l2_step(acc, qs[d0 + i], v[i]);
+    }
+    for (; d0 < D; ++d0) acc = l2_step(acc, qs[d0], x[d0 * 32]);
+    return acc;
+}
+
 template <int KPL>
 __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d, long long* out_i,
                               uint32_t* out_cnt, uint32_t nq) {
-    extern __shared__ float qsm[];  // [warps][Dp]
+    extern __shared__ float qsm[];  // [warps][Dp] queries, then [warps][32] x 2 queue
+    const uint32_t nw = blockDim.x >> 5;
     const uint32_t wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t q = blockIdx.x * (blockDim.x >> 5) + wq;
+    const uint32_t q = blockIdx.x * nw + wq;
     if (q >= nq) return;
     float* qs = qsm + wq * p.Dp;
+    uint32_t* qc = reinterpret_cast<uint32_t*>(qsm + nw * p.Dp) + wq * 64;  // list
+    uint32_t* ql = qc + 32;                                                  // loc
     for (uint32_t i = lane; i < p.D; i += 32) qs[i] = p.queries[(uint64_t)q * p.Dp + i];
     __syncwarp();
     // 1. threshold
@@ -533,7 +648,7 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
         }
     }
     const float theta = th.thr_d;  // +inf if fewer than k vectors were scanned
-    // 2. exact top-k over surviving candidates
+    // 2. exact top-k over the surviving candidates
     WarpTopK<KPL> tk;
     tk.init();
     auto offer = [&](float dist, long long id, bool valid) {
@@ -547,6 +662,21 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
             if (tk.admits(bd, bi)) tk.insert(bd, bi, (int)p.k, lane);
         }
     };
+    uint32_t qn = 0;  // queued candidates (warp-uniform)
+    auto flush = [&]() {
+        bool ok = lane < qn;
+        float dist = 0.f;
+        long long id = -1;
+        if (ok) {
+            const uint32_t c = qc[lane], loc = ql[lane];
+            const GroupRef g = ivf_group(p.L, c, p.snap_off[c], p.snap_len[c], loc >> 5);
+            dist = exact_l2(qs, g.base + (loc & 31), p.D);
+            id = g.ids[loc & 31];
+        }
+        offer(dist, id, ok);
+        qn = 0;
+        __syncwarp();
+    };
     for (uint32_t pi = 0; pi < p.P; ++pi) {
         const uint32_t c = (uint32_t)probes[(uint64_t)q * p.P + pi];
         const uint32_t n = p.nch[c];
@@ -555,36 +685,30 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
             const uint64_t run = ((uint64_t)q * p.P + pi) * p.maxch + h;
             const uint32_t cnt = p.ccount[run];
             if (cnt <= kKC) {
-                for (uint32_t e0 = 0; e0 < cnt; e0 += 32) {
-                    const uint32_t e = e0 + lane;
-                    bool ok = e < cnt && p.clb[run * kKC + e] <= theta;
-                    float dist = 0.f;
-                    long long id = -1;
-                    if (ok) {
-                        const uint32_t loc = p.cloc[run * kKC + e];
-                        const GroupRef g = ivf_group(p.L, c, off, len, loc >> 5);
-                        const uint32_t sl = loc & 31;
-                        const float* x = g.base + sl;
-                        float acc = 0.f;
-                        for (uint32_t dd = 0; dd < p.D; ++dd) acc = l2_step(acc, qs[dd], x[dd * 32]);
-                        dist = acc;
-                        id = g.ids[sl];
-                    }
-                    offer(dist, id, ok);
+                const bool pass = lane < cnt && p.clb[run * kKC + lane] <= theta;
+                const unsigned msk = __ballot_sync(0xffffffffu, pass);
+                const uint32_t np = __popc(msk);
+                if (qn + np > 32) flush();
+                if (pass) {
+                    const uint32_t slot = qn + __popc(msk & ((1u << lane) - 1u));
+                    qc[slot] = c;
+                    ql[slot] = p.cloc[run * kKC + lane];
                 }
+                qn += np;
+                __syncwarp();
             } else {  // overflow: exact rescan of the chunk
                 const uint32_t ng = ivf_ngroups(p.L, off, len);
                 const uint32_t g0 = h * p.gc[c], g1 = min(ng, g0 + p.gc[c]);
                 for (uint32_t j = g0; j < g1; ++j) {
                     const GroupRef g = ivf_group(p.L, c, off, len, j);
                     const bool ok = lane < g.nvalid;
-                    float acc = 0.f;
-                    for (uint32_t dd = 0; dd < p.D; ++dd) acc = l2_step(acc, qs[dd], g.base[dd * 32 + lane]);
-                    offer(acc, ok ? g.ids[lane] : -1, ok);
+                    const float dist = exact_l2(qs, g.base + lane, p.D);
+                    offer(dist, ok ? g.ids[lane] : -1, ok);
                 }
             }
         }
     }
+    if (qn) flush();
     uint32_t cntq = 0;
 #pragma unroll
     for (int r = 0; r < KPL; ++r) {
@@ -599,8 +723,8 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
 }
 
 size_t tc_smem_bytes() {
-    return 1024 + kABytes + kNS * kStageBytes + kMaxD * 4 + kNB * 4 * 32 * 4 + kNB * 32 * 4 +
-           kM * kKC * 8 + 32 * 8 + 64;
+    return 1024 + kNS * kStagePair + kMaxD * 4 + kNB * 16 * 32 * 4 + 2 * kNB * 32 * 4 +
+           kM * kKC * 8 + 32 * kM * 4 + 32 * 8 + 64;
 }
 
 }  // namespace
@@ -633,7 +757,8 @@ cudaError_t make_group_map(const float* base, uint64_t rows, uint32_t D, CUtenso
     cuuint32_t box[2] = {32, D};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -691,8 +816,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     if (e != cudaSuccess) return e;
     if (ev1) cudaEventRecord(ev1, s);
     const uint32_t wpb = 4;
-    refine_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * p.Dp * 4, s>>>(p, probes, out_d,
-                                                                              out_i, out_cnt, sh.nq);
+    refine_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
+        p, probes, out_d, out_i, out_cnt, sh.nq);
     count_launch();
     return cudaGetLastError();
 }

@@ -23,7 +23,7 @@ struct TcBufs {
 bool tc_supported(uint32_t D, uint32_t k, int metric);
 
 // 2-D TMA map over a region of 32-float rows (one dim of one 32-vector
-// group per row), box = {32, D}, SWIZZLE_128B.
+// group per row), box = {32, D}, SWIZZLE_128B_ATOM_32B.
 cudaError_t make_group_map(const float* base, uint64_t rows, uint32_t D, CUtensorMap* out);
 
 cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,
