@@ -287,7 +287,10 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const ScanParams p) {
             }
         }
 
-        // merge the parts of a subset (warps that split the groups)
+        // merge the parts of a subset (warps that split the groups).  Warps may
+        // already be in different items, so each barrier id has ONE fixed warp
+        // set: id 1 = warps {0,1}, id 2 = {2,3} (wps 2), id 3 = {0,1,2,3} (wps 4).
+        const uint32_t bar_id = wps == 4 ? 3u : 1u + sub;
         if (active && wps > 1) {
             float* sd = scr_d + warp * QW * K;
             long long* si = scr_i + warp * QW * K;
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const ScanParams p) {
                         si[qi * K + r * 32 + lane] = tk[qi].id[r];
                     }
             }
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + sub), "r"(wps * 32) : "memory");
+            asm volatile("barrier.sync %0, %1;" ::"r"(bar_id), "r"(wps * 32) : "memory");
             if (part == 0) {
                 for (uint32_t w2 = 1; w2 < wps; ++w2) {
                     const float* od = scr_d + (warp + w2) * QW * K;
@@ -325,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const ScanParams p) {
                     }
                 }
             }
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + sub), "r"(wps * 32) : "memory");
+            asm volatile("barrier.sync %0, %1;" ::"r"(bar_id), "r"(wps * 32) : "memory");
         }
 
         // write the (pair, chunk) candidate runs

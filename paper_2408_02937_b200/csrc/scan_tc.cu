@@ -89,7 +89,7 @@ __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 __device__ __forceinline__ void named_bar(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(n) : "memory");  // non-.aligned: tolerates divergence
 }
 // UMMA smem matrix descriptor (version 1).  layout 2 = SWIZZLE_128B (A: K-major,
 // 8 rows x 128 B atoms); layout 1 = SWIZZLE_128B_BASE32B (B: MN-major 32-bit,
@@ -234,6 +234,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, const TcItem& d, 
                                             uint32_t* my_loc, float* scratch) {
     const uint32_t b = eunit % kNB;
     mbar_wait(&acc_full[b], (eunit / kNB) & 1);
+    __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread spin
     tc_fence_after();
     float dot[32];
     tmem_ld32(tmem_base + taddr_lane + kColAcc + b * 32, dot);
@@ -429,6 +430,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint32_t st = unit % kNS, b = unit % kNB;
                 mbar_wait(&cent_full[st], (unit / kNS) & 1);
                 mbar_wait(&acc_empty[b], ((unit / kNB) & 1) ^ 1);
+                __syncwarp();
                 tc_fence_after();
                 if (lane == 0) {
                     // 3xTF32: A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (A from TMEM, B from smem)
@@ -478,6 +480,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 pair = d.pairs[m];
                 q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
             }
+            __syncwarp();  // tcgen05.st is .sync.aligned
             for (uint32_t c0 = 0; c0 < p.Dk; c0 += 32) {
                 uint32_t vh[32], vl[32];
 #pragma unroll
@@ -490,9 +493,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     vh[i] = __float_as_uint(h);
                     vl[i] = __float_as_uint(__fsub_rn(r, h));
                 }
+                __syncwarp();
                 BIVF_TMEM_ST32(tmem_base + taddr_lane + c0, vh);
                 BIVF_TMEM_ST32(tmem_base + taddr_lane + kColAlo + c0, vl);
             }
+            __syncwarp();
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             named_bar(1, 128);
@@ -582,6 +587,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     __syncthreads();
     if (warp == 1) {
+        __syncwarp();
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                      "r"(kTmemCols)

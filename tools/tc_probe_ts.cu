@@ -81,7 +81,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap mapB, const float* A, 
             : "memory");
     }
     mbar_wait(&bar, 0);
-    for (int i = t; i < K * 32; i += blockDim.x) {  // split B in place (offsets unchanged)
+    for (int i = t; i < K * 32 && mode != 0; i += blockDim.x) {  // split B in place (offsets unchanged)
         float* p = reinterpret_cast<float*>(sB) + i;
         const float x = *p, h = trunc_tf32(x);
         *p = h;
@@ -93,7 +93,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap mapB, const float* A, 
         for (int c0 = 0; c0 < K; c0 += 32) {
             uint32_t h[32], l[32];
             for (int i = 0; i < 32; ++i) {
-                const float x = A[m * K + c0 + i], hh = trunc_tf32(x);
+                const float x = A[m * K + c0 + i], hh = mode == 0 ? x : trunc_tf32(x);
                 h[i] = __float_as_uint(hh);
                 l[i] = __float_as_uint(x - hh);
             }
@@ -189,6 +189,18 @@ int main() {
     enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dB, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 40 * 1024);
+    {   // conversion rule: raw fp32 operands (no explicit truncation), A = 1, B = 1 + 2^-11 + 2^-20
+        std::vector<float> A1(128 * K, 1.0f), B1(K * 32, 1.0f + ldexpf(1.f, -11) + ldexpf(1.f, -20));
+        cudaMemcpy(dA, A1.data(), A1.size() * 4, cudaMemcpyHostToDevice);
+        cudaMemcpy(dB, B1.data(), B1.size() * 4, cudaMemcpyHostToDevice);
+        probe<<<1, 128, 40 * 1024>>>(map, dA, dO, K, 0);
+        cudaDeviceSynchronize();
+        float o = 0;
+        cudaMemcpy(&o, dO, 4, cudaMemcpyDeviceToHost);
+        printf("raw-fp32 conversion: K*B = %.9g  (truncate -> %.9g, round-nearest -> %.9g)\n", o, (double)K,
+               K * (1.0 + ldexp(1.0, -10)));
+        cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
+    }
     for (int mode : {1, 3}) {
         cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
         probe<<<1, 128, 40 * 1024>>>(map, dA, dO, K, mode);
