@@ -22,7 +22,7 @@ BUILD = os.path.join(ROOT, "build", "bivf")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-ffp-contract=off", "-Xcompiler", "-Wall", "-I", CSRC, "-I", os.path.join(ROOT, "include")]
-SOURCES = ["scan.cu", "scan_tc.cu", "insert.cu", "maint.cu", "index.cpp", "host_algos.cpp", "executor.cpp",
+SOURCES = ["scan.cu", "scan_tc.cu", "insert.cu", "maint.cu", "mirror.cu", "index.cpp", "host_algos.cpp", "executor.cpp",
            "capi.cpp"]
 
 

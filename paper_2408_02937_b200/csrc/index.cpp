@@ -60,6 +60,22 @@ void PinBuf::ensure(size_t n) {
     bytes = grow;
 }
 
+cudaError_t GpuIndex::h2d(void* dst, const void* src, size_t n) const {
+    if (!n) return cudaSuccess;
+    cudaError_t e = cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, data_stream_);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(data_stream_);
+}
+cudaError_t GpuIndex::d2h(void* dst, const void* src, size_t n) const {
+    if (!n) return cudaSuccess;
+    cudaError_t e = cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, data_stream_);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(data_stream_);
+}
+cudaError_t GpuIndex::dset(void* p, int v, size_t n) const {
+    if (!n) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(p, v, n, data_stream_);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(data_stream_);
+}
+
 namespace {
 
 int log_level() {
@@ -134,8 +150,11 @@ GpuIndex::GpuIndex(const bivf_config& in) : cfg_(normalized(in)) {
     if (device_ < 0 || device_ >= ndev) throw Error(BIVF_EINVAL, "device ordinal out of range");
     BIVF_CUDA(cudaSetDevice(device_));
     BIVF_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device_));
-    alloc_device();
+    // every host<->device copy/memset of the index goes through data_stream_
+    // (h2d/d2h/dset): the legacy stream does not order against the index's
+    // non-blocking streams, and a pageable cudaMemcpy may return before its DMA lands.
     BIVF_CUDA(cudaStreamCreateWithFlags(&data_stream_, cudaStreamNonBlocking));
+    alloc_device();
     BIVF_CUDA(cudaEventCreateWithFlags(&maint_evt_, cudaEventDisableTiming));
     for (uint32_t i = 0; i < cfg_.num_leases; ++i) {
         auto l = std::make_unique<Lease>();
@@ -173,32 +192,45 @@ void GpuIndex::alloc_device() {
     // ids -1; here in HBM.
     d_cent_.alloc((size_t)C_ * D_ * 4);
     d_cent_il_.alloc((size_t)ceil_div(C_, 32) * 32 * D_ * 4);
-    BIVF_CUDA(cudaMemset(d_cent_.p, 0, d_cent_.bytes));
-    BIVF_CUDA(cudaMemset(d_cent_il_.p, 0, d_cent_il_.bytes));
+    BIVF_CUDA(dset(d_cent_.p, 0, d_cent_.bytes));
+    BIVF_CUDA(dset(d_cent_il_.p, 0, d_cent_il_.bytes));
     d_off_start_.alloc((size_t)C_ * 8);
     d_off_count_.alloc((size_t)C_ * 4);
-    BIVF_CUDA(cudaMemset(d_off_start_.p, 0, d_off_start_.bytes));
-    BIVF_CUDA(cudaMemset(d_off_count_.p, 0, d_off_count_.bytes));
+    BIVF_CUDA(dset(d_off_start_.p, 0, d_off_start_.bytes));
+    BIVF_CUDA(dset(d_off_count_.p, 0, d_off_count_.bytes));
+    // the scan mirror exists iff the tensor-core scan can serve this index
+    // (L2, 8 <= D <= 128) and it was not disabled (BIVF_SCAN=cuda)
+    {
+        const char* m = std::getenv("BIVF_SCAN");
+        mir_on_ = tc_supported(D_, 1, cfg_.metric) && !(m && std::string(m) == "cuda");
+        GF_ = mirror_group_floats(D_);
+        MPS_ = (uint64_t)gpb_ * GF_;
+        tc_ok_ = mir_on_;
+    }
     ensure_offline_capacity(32);
     d_arena_.alloc((size_t)NB_ * PS_ * 4);
-    BIVF_CUDA(cudaMemset(d_arena_.p, 0, d_arena_.bytes));
-    tc_ok_ = make_group_map(d_arena_.as<float>(), (uint64_t)NB_ * gpb_ * D_, D_, &map_arena_) ==
-             cudaSuccess;
+    BIVF_CUDA(dset(d_arena_.p, 0, d_arena_.bytes));
+    if (mir_on_) {
+        d_arena_mir_.alloc((size_t)NB_ * MPS_ * 4);
+        BIVF_CUDA(dset(d_arena_mir_.p, 0, d_arena_mir_.bytes));
+        tc_ok_ = make_mirror_map(d_arena_mir_.as<float>(), (uint64_t)NB_ * gpb_, D_, &map_arena_) ==
+                 cudaSuccess;
+    }
+    mirror_ = mirror_view();
     d_bids_.alloc((size_t)NB_ * T_ * 8);
-    BIVF_CUDA(cudaMemset(d_bids_.p, 0xff, d_bids_.bytes));
+    BIVF_CUDA(dset(d_bids_.p, 0xff, d_bids_.bytes));
     d_owner_.alloc((size_t)NB_ * 4);
-    BIVF_CUDA(cudaMemset(d_owner_.p, 0xff, d_owner_.bytes));
+    BIVF_CUDA(dset(d_owner_.p, 0xff, d_owner_.bytes));
     d_cursor_.alloc(16);
-    BIVF_CUDA(cudaMemset(d_cursor_.p, 0, 16));
+    BIVF_CUDA(dset(d_cursor_.p, 0, 16));
     d_len_.alloc((size_t)C_ * 4);
     d_nblocks_.alloc((size_t)C_ * 4);
     d_fail_.alloc((size_t)C_);
     d_table_.alloc((size_t)C_ * MLB_ * 4);
-    BIVF_CUDA(cudaMemset(d_len_.p, 0, d_len_.bytes));
-    BIVF_CUDA(cudaMemset(d_nblocks_.p, 0, d_nblocks_.bytes));
-    BIVF_CUDA(cudaMemset(d_fail_.p, 0, d_fail_.bytes));
-    BIVF_CUDA(cudaMemset(d_table_.p, 0xff, d_table_.bytes));
-    if (D_ > 256) tc_ok_ = false;
+    BIVF_CUDA(dset(d_len_.p, 0, d_len_.bytes));
+    BIVF_CUDA(dset(d_nblocks_.p, 0, d_nblocks_.bytes));
+    BIVF_CUDA(dset(d_fail_.p, 0, d_fail_.bytes));
+    BIVF_CUDA(dset(d_table_.p, 0xff, d_table_.bytes));
     if (const char* m = std::getenv("BIVF_SCAN")) {
         if (std::string(m) == "cuda") scan_mode_ = 1;
         if (std::string(m) == "tc") scan_mode_ = 2;
@@ -215,11 +247,64 @@ void GpuIndex::ensure_offline_capacity(uint64_t slots) {
     if (slots <= off_slots_cap_) return;
     d_off_pay_.alloc((size_t)slots * D_ * 4);
     d_off_ids_.alloc((size_t)slots * 8);
-    BIVF_CUDA(cudaMemset(d_off_pay_.p, 0, d_off_pay_.bytes));
-    BIVF_CUDA(cudaMemset(d_off_ids_.p, 0xff, d_off_ids_.bytes));
+    BIVF_CUDA(dset(d_off_pay_.p, 0, d_off_pay_.bytes));
+    BIVF_CUDA(dset(d_off_ids_.p, 0xff, d_off_ids_.bytes));
     off_slots_cap_ = slots;
-    if (make_group_map(d_off_pay_.as<float>(), slots / 32 * D_, D_, &map_off_) != cudaSuccess)
-        tc_ok_ = false;
+    if (mir_on_) {
+        d_off_mir_.alloc((size_t)(slots / 32) * GF_ * 4);
+        BIVF_CUDA(dset(d_off_mir_.p, 0, d_off_mir_.bytes));
+        if (make_mirror_map(d_off_mir_.as<float>(), slots / 32, D_, &map_off_) != cudaSuccess)
+            tc_ok_ = false;
+    }
+    mirror_ = mirror_view();
+}
+
+MirrorView GpuIndex::mirror_view() const {
+    MirrorView M{};
+    M.off_mir = d_off_mir_.as<float>();
+    M.arena_mir = d_arena_mir_.as<float>();
+    M.cent = d_cent_.as<float>();
+    M.D = D_;
+    M.T = T_;
+    M.gpb = gpb_;
+    M.GF = GF_;
+    M.MPS = MPS_;
+    return M;
+}
+
+// Recompute the whole mirror from the payload (centroids changed under data).
+// Caller holds data_mu_.
+void GpuIndex::rebuild_mirror() {
+    if (!mir_on_) return;
+    std::vector<uint64_t> g;
+    std::vector<uint32_t> cl;
+    for (uint32_t c = 0; c < C_; ++c)
+        for (uint64_t j = 0; j < (h_off_count_[c] + 31ull) / 32; ++j) {
+            g.push_back(h_off_start_[c] / 32 + j);
+            cl.push_back(c);
+        }
+    std::vector<uint64_t> ga;
+    std::vector<uint32_t> cla;
+    for (uint32_t b = 0; b < h_cursor_; ++b)
+        if (h_owner_[b] >= 0)
+            for (uint32_t j = 0; j < gpb_; ++j) {
+                ga.push_back((uint64_t)b * gpb_ + j);
+                cla.push_back((uint32_t)h_owner_[b]);
+            }
+    DevBuf dg, dc;
+    for (int pass = 0; pass < 2; ++pass) {
+        auto& G = pass ? ga : g;
+        auto& CL = pass ? cla : cl;
+        if (G.empty()) continue;
+        dg.ensure(G.size() * 8);
+        dc.ensure(CL.size() * 4);
+        BIVF_CUDA(h2d(dg.p, G.data(), G.size() * 8));
+        BIVF_CUDA(h2d(dc.p, CL.data(), CL.size() * 4));
+        BIVF_CUDA(launch_mirror_groups(mirror_, pass ? d_arena_.as<float>() : d_off_pay_.as<float>(),
+                                       pass == 1, PS_, dg.as<uint64_t>(), dc.as<uint32_t>(),
+                                       (uint32_t)G.size(), data_stream_));
+        BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+    }
 }
 
 DevLists GpuIndex::dev_lists() const {
@@ -276,14 +361,17 @@ void GpuIndex::upload_centroids() {
 void GpuIndex::set_centroids(const float* c) {
     std::lock_guard<std::mutex> lk(data_mu_);
     BIVF_CUDA(cudaSetDevice(device_));
-    BIVF_CUDA(cudaMemcpy(d_cent_.p, c, (size_t)C_ * D_ * 4, cudaMemcpyHostToDevice));
+    BIVF_CUDA(h2d(d_cent_.p, c, (size_t)C_ * D_ * 4));
     upload_centroids();
     trained_ = true;
+    bool any = false;
+    for (uint32_t k = 0; k < C_ && !any; ++k) any = h_off_count_[k] > 0 || h_len_[k] > 0;
+    if (any) rebuild_mirror();
 }
 
 void GpuIndex::get_centroids(float* out) const {
     BIVF_CUDA(cudaSetDevice(device_));
-    BIVF_CUDA(cudaMemcpy(out, d_cent_.p, (size_t)C_ * D_ * 4, cudaMemcpyDeviceToHost));
+    BIVF_CUDA(d2h(out, d_cent_.p, (size_t)C_ * D_ * 4));
 }
 
 void GpuIndex::train(const float* x, uint64_t n) {
@@ -323,10 +411,10 @@ void GpuIndex::bulk_load(const float* x, uint64_t n, const uint32_t* assignment,
         total += (counts[c] + 31) / 32 * 32;
     }
     ensure_offline_capacity(total);
-    BIVF_CUDA(cudaMemset(d_off_ids_.p, 0xff, d_off_ids_.bytes));
+    BIVF_CUDA(dset(d_off_ids_.p, 0xff, d_off_ids_.bytes));
     std::vector<uint64_t> fill(C_, 0);
     const uint64_t chunk = 1ull << 20;
-    DevBuf dx, ddest, dids;
+    DevBuf dx, ddest, dids, dasg;
     PinBuf pin;
     std::vector<uint64_t> dest;
     std::vector<long long> idv;
@@ -342,19 +430,24 @@ void GpuIndex::bulk_load(const float* x, uint64_t n, const uint32_t* assignment,
         dx.ensure(m * D_ * 4);
         ddest.ensure(m * 8);
         dids.ensure(m * 8);
-        BIVF_CUDA(cudaMemcpy(dx.p, x + s * D_, m * D_ * 4, cudaMemcpyHostToDevice));
-        BIVF_CUDA(cudaMemcpy(ddest.p, dest.data(), m * 8, cudaMemcpyHostToDevice));
-        BIVF_CUDA(cudaMemcpy(dids.p, idv.data(), m * 8, cudaMemcpyHostToDevice));
+        BIVF_CUDA(h2d(dx.p, x + s * D_, m * D_ * 4));
+        BIVF_CUDA(h2d(ddest.p, dest.data(), m * 8));
+        BIVF_CUDA(h2d(dids.p, idv.data(), m * 8));
         BIVF_CUDA(launch_scatter_rows(dx.as<float>(), (uint32_t)m, D_, ddest.as<uint64_t>(),
                                       dids.as<long long>(), d_off_pay_.as<float>(),
                                       d_off_ids_.as<long long>(), data_stream_));
+        if (mir_on_) {
+            dasg.ensure(m * 4);
+            BIVF_CUDA(h2d(dasg.p, assignment + s, m * 4));
+            BIVF_CUDA(launch_mirror_offline(mirror_, (uint32_t)m, dx.as<float>(),
+                                            ddest.as<uint64_t>(), dasg.as<uint32_t>(),
+                                            data_stream_));
+        }
         BIVF_CUDA(cudaStreamSynchronize(data_stream_));
     }
     for (uint32_t c = 0; c < C_; ++c) h_off_count_[c] = (uint32_t)counts[c];
-    BIVF_CUDA(cudaMemcpy(d_off_start_.p, h_off_start_.data(), (size_t)C_ * 8,
-                         cudaMemcpyHostToDevice));
-    BIVF_CUDA(cudaMemcpy(d_off_count_.p, h_off_count_.data(), (size_t)C_ * 4,
-                         cudaMemcpyHostToDevice));
+    BIVF_CUDA(h2d(d_off_start_.p, h_off_start_.data(), (size_t)C_ * 8));
+    BIVF_CUDA(h2d(d_off_count_.p, h_off_count_.data(), (size_t)C_ * 4));
     if (ids) {
         int64_t mx = -1;
         for (uint64_t i = 0; i < n; ++i) {
@@ -424,7 +517,7 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     const size_t o_oc = take((size_t)nq * 4);
     const size_t o_ctr = take(16);
     const size_t o_plan = take((size_t)C_ * 4 * 5 + (size_t)(C_ + 1) * 4 * 2 + 16);
-    const size_t runs = npairs * maxch;
+    const size_t runs = npairs * maxch * 2;  // TC scan: one run per chunk and warpgroup
     const size_t o_ub = take(runs * k * 4);
     const size_t o_cc = take(runs * 4);
     const size_t o_clb = take(runs * kKC * 4);
@@ -704,8 +797,7 @@ bool GpuIndex::is_duplicate_id(int64_t id) {
 void GpuIndex::absorb_new_blocks(uint32_t cursor_old, uint32_t cursor_new) {
     if (cursor_new <= cursor_old) return;
     std::vector<int32_t> own(cursor_new - cursor_old);
-    BIVF_CUDA(cudaMemcpy(own.data(), d_owner_.as<int32_t>() + cursor_old, own.size() * 4,
-                         cudaMemcpyDeviceToHost));
+    BIVF_CUDA(d2h(own.data(), d_owner_.as<int32_t>() + cursor_old, own.size() * 4));
     // Blocks are handed out in batch order, which is each list's logical
     // order: append = link after the tail (block_store.cpp:55-65).
     for (uint32_t b = cursor_old; b < cursor_new; ++b) {
@@ -733,7 +825,7 @@ void GpuIndex::absorb_new_blocks(uint32_t cursor_old, uint32_t cursor_new) {
 }
 
 void GpuIndex::refresh_lengths() {
-    BIVF_CUDA(cudaMemcpy(h_len_.data(), d_len_.p, (size_t)C_ * 4, cudaMemcpyDeviceToHost));
+    BIVF_CUDA(d2h(h_len_.data(), d_len_.p, (size_t)C_ * 4));
 }
 
 uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_t* out_ids) {
@@ -792,7 +884,7 @@ uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_
         const uint32_t cursor_old = h_cursor_;
         BIVF_CUDA(launch_insert(insert_state(), m, d_x_.as<float>(), d_ids_.as<long long>(),
                                 d_asg_.as<uint32_t>(), d_blk_.as<int32_t>(),
-                                d_did_.as<uint32_t>(), st));
+                                d_did_.as<uint32_t>(), mirror_ptr(), st));
         blk.resize(m);
         uint32_t cursor_new = 0;
         BIVF_CUDA(cudaMemcpyAsync(blk.data(), d_blk_.p, (size_t)m * 4, cudaMemcpyDeviceToHost, st));
@@ -996,7 +1088,7 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
     DevBuf dpa, dia, dscr_p, dscr_i, dclr, dli, dlv, doi, dov;
     dpa.alloc(std::max<size_t>(pa.size(), 1) * 8);
     dia.alloc(std::max<size_t>(ia.size(), 1) * 8);
-    dscr_p.alloc(std::max<size_t>((size_t)nm * D_, 1) * 4);
+    dscr_p.alloc(std::max<size_t>((size_t)nm * (mir_on_ ? 2 * D_ + 2 : D_), 1) * 4);
     dscr_i.alloc(std::max<size_t>(nm, 1) * 8);
     dclr.alloc(std::max<size_t>(clear.size(), 1) * 8);
     dli.alloc(std::max<size_t>(len_idx.size(), 1) * 4);
@@ -1024,6 +1116,9 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
                                     d_arena_.as<float>(), d_bids_.as<long long>(), D_,
                                     dpa.as<uint64_t>(), dia.as<uint64_t>(), nm,
                                     dscr_p.as<float>(), dscr_i.as<long long>(), st));
+        if (mir_on_)
+            BIVF_CUDA(launch_mirror_slot_moves(mirror_, dia.as<uint64_t>(), nm, dscr_p.as<float>(),
+                                               st));
         BIVF_CUDA(launch_clear_ids(d_off_ids_.as<long long>(), d_bids_.as<long long>(),
                                    dclr.as<uint64_t>(), (uint32_t)clear.size(), st));
         BIVF_CUDA(launch_set_u32(d_len_.as<uint32_t>(), dli.as<uint32_t>(), dlv.as<uint32_t>(),
@@ -1222,7 +1317,7 @@ void GpuIndex::rearrange(uint32_t c) {
         DevBuf ds, dd, sp, si, own;
         ds.alloc(nm * 4);
         dd.alloc(nm * 4);
-        sp.alloc((size_t)nm * PS_ * 4);
+        sp.alloc((size_t)nm * std::max<uint64_t>(PS_, mir_on_ ? MPS_ : 0) * 4);
         si.alloc((size_t)nm * T_ * 8);
         cudaStream_t st = data_stream_;
         BIVF_CUDA(cudaMemcpyAsync(ds.p, src.data(), nm * 4, cudaMemcpyHostToDevice, st));
@@ -1239,6 +1334,10 @@ void GpuIndex::rearrange(uint32_t c) {
             BIVF_CUDA(launch_block_moves(d_arena_.as<float>(), d_bids_.as<long long>(), PS_, T_,
                                          ds.as<int32_t>(), dd.as<int32_t>(), nm, sp.as<float>(),
                                          si.as<long long>(), st));
+            if (mir_on_)
+                BIVF_CUDA(launch_block_moves(d_arena_mir_.as<float>(), nullptr, MPS_, T_,
+                                             ds.as<int32_t>(), dd.as<int32_t>(), nm, sp.as<float>(),
+                                             nullptr, st));
             for (uint32_t k : rowc) {
                 staged.push_back(h_blocks_[k]);
                 auto& r = staged.back();
@@ -1337,16 +1436,14 @@ void GpuIndex::block_ids(int32_t b, int64_t* out) const {
     std::lock_guard<std::mutex> lk(data_mu_);
     check_block(b);
     BIVF_CUDA(cudaSetDevice(device_));
-    BIVF_CUDA(cudaMemcpy(out, d_bids_.as<long long>() + (size_t)b * T_, (size_t)T_ * 8,
-                         cudaMemcpyDeviceToHost));
+    BIVF_CUDA(d2h(out, d_bids_.as<long long>() + (size_t)b * T_, (size_t)T_ * 8));
 }
 
 void GpuIndex::block_payload(int32_t b, float* out) const {
     std::lock_guard<std::mutex> lk(data_mu_);
     check_block(b);
     BIVF_CUDA(cudaSetDevice(device_));
-    BIVF_CUDA(cudaMemcpy(out, d_arena_.as<float>() + (size_t)b * PS_, (size_t)PS_ * 4,
-                         cudaMemcpyDeviceToHost));
+    BIVF_CUDA(d2h(out, d_arena_.as<float>() + (size_t)b * PS_, (size_t)PS_ * 4));
 }
 
 uint64_t GpuIndex::cluster_contents(uint32_t c, int64_t* ids, float* vecs) const {
@@ -1361,10 +1458,8 @@ uint64_t GpuIndex::cluster_contents(uint32_t c, int64_t* ids, float* vecs) const
         std::vector<float> pay(groups * 32 * D_);
         std::vector<long long> oid(noff);
         const uint64_t s0 = h_off_start_[c];
-        BIVF_CUDA(cudaMemcpy(pay.data(), d_off_pay_.as<float>() + s0 * D_, pay.size() * 4,
-                             cudaMemcpyDeviceToHost));
-        BIVF_CUDA(cudaMemcpy(oid.data(), d_off_ids_.as<long long>() + s0, noff * 8,
-                             cudaMemcpyDeviceToHost));
+        BIVF_CUDA(d2h(pay.data(), d_off_pay_.as<float>() + s0 * D_, pay.size() * 4));
+        BIVF_CUDA(d2h(oid.data(), d_off_ids_.as<long long>() + s0, noff * 8));
         for (uint64_t i = 0; i < noff; ++i, ++n) {
             ids[n] = oid[i];
             const float* base = pay.data() + (i / 32) * 32 * D_ + i % 32;
@@ -1377,10 +1472,8 @@ uint64_t GpuIndex::cluster_contents(uint32_t c, int64_t* ids, float* vecs) const
     for (int32_t b : h_blocks_[c]) {
         if (!left) break;
         const uint32_t m = (uint32_t)std::min<uint64_t>(T_, left);
-        BIVF_CUDA(cudaMemcpy(pay.data(), d_arena_.as<float>() + (size_t)b * PS_, PS_ * 4,
-                             cudaMemcpyDeviceToHost));
-        BIVF_CUDA(cudaMemcpy(bid.data(), d_bids_.as<long long>() + (size_t)b * T_, (size_t)T_ * 8,
-                             cudaMemcpyDeviceToHost));
+        BIVF_CUDA(d2h(pay.data(), d_arena_.as<float>() + (size_t)b * PS_, PS_ * 4));
+        BIVF_CUDA(d2h(bid.data(), d_bids_.as<long long>() + (size_t)b * T_, (size_t)T_ * 8));
         for (uint32_t s = 0; s < m; ++s, ++n) {
             ids[n] = bid[s];
             const float* base = pay.data() + (s / 32) * 32 * D_ + s % 32;
@@ -1398,7 +1491,7 @@ std::string GpuIndex::dump_pool() const {
     std::vector<long long> all((size_t)h_cursor_ * T_);
     if (h_cursor_) {
         BIVF_CUDA(cudaSetDevice(device_));
-        BIVF_CUDA(cudaMemcpy(all.data(), d_bids_.p, all.size() * 8, cudaMemcpyDeviceToHost));
+        BIVF_CUDA(d2h(all.data(), d_bids_.p, all.size() * 8));
     }
     for (uint32_t b = 0; b < h_cursor_; ++b) {
         const uint32_t sz = committed_of((int32_t)b);

@@ -35,6 +35,7 @@
 
 #include "../../include/bivf.h"
 #include "insert.cuh"
+#include "mirror.cuh"
 #include "scan.cuh"
 #include "scan_tc.cuh"
 
@@ -165,11 +166,17 @@ public:
     void record_timings(Lease& l);
 
 private:
-    // --- device storage
+    // --- device storage (copies/memsets stream-ordered on data_stream_, then synced)
+    cudaError_t h2d(void* dst, const void* src, size_t n) const;
+    cudaError_t d2h(void* dst, const void* src, size_t n) const;
+    cudaError_t dset(void* p, int v, size_t n) const;
     void alloc_device();
     void ensure_offline_capacity(uint64_t slots);
     DevLists dev_lists() const;
     InsertState insert_state();
+    MirrorView mirror_view() const;
+    const MirrorView* mirror_ptr() const { return mir_on_ ? &mirror_ : nullptr; }
+    void rebuild_mirror();
     void upload_centroids();
 
     // --- leases / maintenance fencing
@@ -201,6 +208,11 @@ private:
     DevBuf d_off_pay_, d_off_ids_, d_off_start_, d_off_count_;
     uint64_t off_slots_cap_ = 0;
     DevBuf d_arena_, d_bids_, d_owner_;
+    // tensor-core scan mirror (mirror.cuh); allocated when the TC scan can serve this index
+    DevBuf d_off_mir_, d_arena_mir_;
+    bool mir_on_ = false;
+    uint64_t GF_ = 0, MPS_ = 0;
+    MirrorView mirror_{};
     DevBuf d_cursor_, d_len_, d_nblocks_, d_fail_, d_table_;
     DevBuf d_run_, d_failfrom_, d_newlen_;
     // data-lane staging

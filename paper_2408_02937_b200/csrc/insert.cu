@@ -193,13 +193,17 @@ __global__ void seed_update(const float* pts_il, uint32_t n, uint32_t D, const f
 
 cudaError_t launch_insert(const InsertState& S, uint32_t n, const float* x, const long long* ids,
                           const uint32_t* asg, int32_t* out_blk, uint32_t* out_did,
-                          cudaStream_t s) {
+                          const MirrorView* mirror, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     reset_scratch<<<(S.C + 255) / 256, 256, 0, s>>>(S.C, S.run, S.fail_from, S.newlen, S.len);
     layout_kernel<<<1, kLayoutThreads, 0, s>>>(S, n, asg, out_blk, out_did);
     const uint64_t total = (uint64_t)n * S.D;
     const unsigned wg = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
     write_kernel<<<wg, 256, 0, s>>>(S, n, x, ids, out_blk, out_did);
+    if (mirror) {
+        const cudaError_t e = launch_mirror_insert(*mirror, n, x, asg, out_blk, out_did, s);
+        if (e != cudaSuccess) return e;
+    }
     publish_kernel<<<(n + 255) / 256, 256, 0, s>>>(S, n, asg, out_blk, out_did);
     count_launch(4);
     return cudaGetLastError();

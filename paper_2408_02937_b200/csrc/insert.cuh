@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "mirror.cuh"
+
 namespace bivf {
 
 // Mutable device state touched by an insert batch (device pointers).
@@ -24,12 +26,13 @@ struct InsertState {
 
 // asg[i] = cluster of vector i (0xffffffff = rejected before assignment).
 // out_blk[i] = pool block the vector landed in (-1 = failed), out_did[i] =
-// its position in the list.  Release-publishes the list lengths last.
+// its position in the list.  The scan mirror (if any) is written with the
+// payload.  Release-publishes the list lengths last.
 // Block headers (prev/next/head/tail) are derived on the host from the new
 // blocks' owners, in allocation order (GpuIndex::absorb_new_blocks).
 cudaError_t launch_insert(const InsertState& S, uint32_t n, const float* x, const long long* ids,
                           const uint32_t* asg, int32_t* out_blk, uint32_t* out_did,
-                          cudaStream_t s);
+                          const MirrorView* mirror, cudaStream_t s);
 
 // offline segment build: row i -> slot dest[i] of the concatenated,
 // group-aligned offline segments (ivf_index.cpp:61-82 layout).

@@ -32,14 +32,15 @@ __global__ void block_move_kernel(float* arena, long long* bids, uint64_t PS, ui
     if (m >= nmoves) return;
     const uint64_t b = phase == 0 ? (uint64_t)src[m] : (uint64_t)dst[m];
     float* blk_pay = arena + b * PS;
-    long long* blk_ids = bids + b * T;
+    long long* blk_ids = bids ? bids + b * T : nullptr;
     float* sp = scr_pay + (uint64_t)m * PS;
-    long long* si = scr_ids + (uint64_t)m * T;
+    long long* si = scr_ids ? scr_ids + (uint64_t)m * T : nullptr;
     const float4* from4 = reinterpret_cast<const float4*>(phase == 0 ? blk_pay : sp);
     float4* to4 = reinterpret_cast<float4*>(phase == 0 ? sp : blk_pay);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < PS / 4;
          i += (uint64_t)gridDim.x * blockDim.x)
         to4[i] = from4[i];
+    if (!bids) return;  // payload-only move (the scan mirror)
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T;
          i += (uint64_t)gridDim.x * blockDim.x) {
         if (phase == 0) si[i] = blk_ids[i];

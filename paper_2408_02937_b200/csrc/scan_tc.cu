@@ -6,30 +6,34 @@
 // under TopK's (dist, id) order (include/blockivf/topk.hpp:14-28).
 //
 // Design.  Exact distances are sequential fp32 sums, so
-// tensor cores can only FILTER: per work item (list c, tile of <=128 queries,
-// chunk of groups) a persistent CTA
-//   producer warp : TMA (cp.async.bulk.tensor.2d, SWIZZLE_128B_ATOM_32B) of
-//                   each 32-vector group, dims as rows -> MN-major B tile
-//   math warps    : centre the tile in place (x - c_list), per-slot residual
-//                   norms, and build A = centred queries (K-major SW128)
-//   MMA warp      : tcgen05.mma.kind::tf32 128x32xD into TMEM (4 buffers)
-//   math warps    : tcgen05.ld the 32 dot products of their query, form the
-//                   approximate distance a = |r|^2 + |s|^2 - 2 r.s and a
-//                   PROVEN bound eps (TF32 + fp32 rounding, see err_bound),
-//                   keep the k smallest upper bounds (a+eps) and every vector
-//                   whose lower bound (a-eps) can still enter the top-k.
+// tensor cores can only FILTER.  Per work item (list c, tile of <=128 queries,
+// chunk of groups) a persistent CTA (one per SM) runs
+//   producer warp : two TMA boxes per 32-vector group from the scan mirror
+//                   (mirror.cuh: list-centred residual s = x - c pre-split into
+//                   TF32 hi/lo planes + |s|^2, |s|) -> MN-major B tiles
+//   MMA warp      : 3xTF32 tcgen05.mma 128x32xD (A = centred queries, hi/lo in
+//                   TMEM; B hi/lo from smem) into one of 8 TMEM accumulators
+//   2 math warpgroups (alternate groups): build A once per item, then per
+//                   group tcgen05.ld the 32 dot products of their query, form
+//                   a = |r|^2 + |s|^2 - 2 r.s and a PROVEN bound eps (TF32 +
+//                   fp32 rounding, see err_bound), keep the k smallest upper
+//                   bounds (a+eps) and every vector whose lower bound (a-eps)
+//                   can still enter the top-k (one run per warpgroup).
 // A refine kernel (one warp per query) takes the k-th smallest upper bound
-// over all of the query's items as threshold, recomputes the EXACT distance
-// (sequential fp32, the reference's bits) of every surviving candidate and
-// builds the exact top-k; an item whose candidate buffer overflowed is
-// rescanned exactly.  Pruned vectors provably cannot be in the top-k.
+// over all of the query's runs as threshold, recomputes the EXACT distance
+// (sequential fp32 over the reference-layout payload, the reference's bits) of
+// every surviving candidate and builds the exact top-k; a chunk whose candidate
+// buffer overflowed is rescanned exactly.  Pruned vectors provably cannot be in
+// the top-k.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
+#include "mirror.cuh"
 #include "launches.h"
 #include "scan.cuh"
 #include "scan_common.cuh"
@@ -39,15 +43,18 @@ namespace bivf {
 
 namespace {
 
-constexpr int kTcThreads = 192;     // warp0 TMA, warp1 MMA, warps 2-5 math
-constexpr int kM = 128;             // queries per tile (MMA M, TMEM lanes)
-constexpr int kNS = 4;              // smem stages (one group each)
-constexpr int kNB = 4;              // TMEM accumulator buffers (32 columns each)
+constexpr int kWG = 2;                     // math warpgroups
+constexpr int kTcThreads = 64 + 128 * kWG;  // warp0 TMA, warp1 MMA, warps 2.. math
+constexpr int kM = 128;                    // queries per tile (MMA M, TMEM lanes)
+constexpr int kNS = 6;                     // smem stages (one group each; even)
+constexpr int kNB = 8;                     // TMEM accumulators (32 columns each; even)
 constexpr int kMaxD = 128;
-constexpr int kStageBytes = kMaxD * 128;       // 128 rows (dims) x 128 B
-constexpr int kStagePair = 2 * kStageBytes;    // s_hi (TMA target, split in place) + s_lo
+// a stage = two 1024-aligned regions of (D+1) 128-byte rows: [s_hi | |s|^2], [s_lo | |s|]
+constexpr int kRegion = (((kMaxD + 1) * 128) + 1023) & ~1023;
+constexpr int kStage = 2 * kRegion;
 // TMEM columns: A_hi [0,128), A_lo [128,256), accumulators [256, 256 + 32*kNB)
 constexpr uint32_t kColAlo = 128, kColAcc = 256, kTmemCols = 512;
+static_assert(kColAcc + 32 * kNB <= kTmemCols, "TMEM budget");
 
 struct TcParams {
     DevLists L;
@@ -63,7 +70,7 @@ struct TcParams {
     const uint32_t* n_items_ptr;
     const uint32_t* plist;
     uint32_t* item_ctr;
-    // per (pair, chunk) outputs
+    // per run outputs; run = ((pair * maxch + chunk) << 1) | warpgroup
     float* ub;          // [runs][k]
     uint32_t* ccount;   // [runs]   (kKC+1 = overflow)
     float* clb;         // [runs][kKC]
@@ -206,34 +213,62 @@ __device__ __forceinline__ TcItem tc_decode(const TcParams& p, uint32_t it) {
     return d;
 }
 
-// TMA row coordinate of group j (rows of 32 floats = one dim of one group)
+// TMA row of group j's mirror (rows of 32 floats; a group spans 2D+2 rows)
 __device__ __forceinline__ void group_row(const DevLists& L, uint32_t c, uint32_t off,
                                           uint32_t j, bool& arena, int& row) {
     const uint32_t og = (off + 31u) >> 5;
+    const uint32_t R = 2u * L.D + 2u;
     if (j < og) {
         arena = false;
-        row = (int)((L.off_start[c] / 32u + j) * L.D);
+        row = (int)((L.off_start[c] / 32u + j) * R);
     } else {
         const uint32_t jj = j - og;
         const uint32_t mid = jj / L.gpb, gi = jj - mid * L.gpb;
         const int32_t blk = L.table[(uint64_t)c * L.MLB + mid];
         arena = true;
-        row = (int)(((uint64_t)blk * L.gpb + gi) * L.D);
+        row = (int)(((uint64_t)blk * L.gpb + gi) * R);
     }
 }
 
-// One accumulator buffer (32 dot products of this thread's query) -> bounds,
-// k smallest upper bounds, candidate buffer.
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+    return v;
+}
+// Row r of a region written by TMA with SWIZZLE_128B_ATOM_32B: slot n lives in
+// 32-byte chunk (n / 8) ^ (r % 4) of the row.
+__device__ __forceinline__ void load_row32(uint32_t region, uint32_t r, float (&v)[32]) {
+    const uint32_t base = region + r * 128u;
+#pragma unroll
+    for (uint32_t j = 0; j < 4; ++j) {
+        const uint32_t a = base + ((j ^ (r & 3u)) << 5);
+        const float4 x = lds4(a), y = lds4(a + 16);
+        v[8 * j + 0] = x.x;
+        v[8 * j + 1] = x.y;
+        v[8 * j + 2] = x.z;
+        v[8 * j + 3] = x.w;
+        v[8 * j + 4] = y.x;
+        v[8 * j + 5] = y.y;
+        v[8 * j + 6] = y.z;
+        v[8 * j + 7] = y.w;
+    }
+}
+
+// One group (unit u, group j of the item) for this thread's query: 32 dot
+// products from TMEM + the group's norms from the stage -> bounds, the k
+// smallest upper bounds, and the candidates whose lower bound can still
+// enter the top-k (written straight to the run's global buffer; rare).
 template <int KT>
-__device__ __forceinline__ void tc_epilogue(const TcParams& p, const TcItem& d, uint32_t eunit,
-                                            uint32_t j, uint64_t* acc_full, uint64_t* acc_empty,
-                                            const float* nsum, const float* ssq, uint32_t tmem_base,
-                                            uint32_t taddr_lane, int lane, bool active, float nq,
-                                            float sqq, float (&ubl)[KT], float& ubk,
-                                            uint32_t& ncand, bool& overflow, float* my_lb,
-                                            uint32_t* my_loc, float* scratch) {
-    const uint32_t b = eunit % kNB;
-    mbar_wait(&acc_full[b], (eunit / kNB) & 1);
+__device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint32_t u, uint32_t j,
+                                        uint64_t* full, uint64_t* empty, uint64_t* acc_full,
+                                        uint64_t* acc_empty, uint32_t stages, uint32_t tmem_base,
+                                        uint32_t taddr_lane, int lane, bool active, float nq,
+                                        float sqq, float (&ubl)[KT], float& ubk, uint32_t& ncand,
+                                        bool& overflow, float* clb, uint32_t* cloc) {
+    const uint32_t b = u % kNB, st = u % kNS;
+    mbar_wait(&acc_full[b], (u / kNB) & 1);
     __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread spin
     tc_fence_after();
     float dot[32];
@@ -241,6 +276,15 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, const TcItem& d, 
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&acc_empty[b]);
+    // the group's norms (row D of both regions); full[st] has completed this
+    // phase already (its MMA did), the wait makes the TMA writes visible here
+    mbar_wait(&full[st], (u / kNS) & 1);
+    float ns[32], ss[32];
+    const uint32_t sbase = stages + st * (uint32_t)kStage;
+    load_row32(sbase, p.D, ns);
+    load_row32(sbase + kRegion, p.D, ss);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
     if (!active) return;
     // valid slots of group j, from the snapshot (no table lookups)
     uint32_t nvalid;
@@ -253,40 +297,37 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, const TcItem& d, 
             nvalid = min(32u, min(p.L.T, d.len - mid * p.L.T) - 32u * gi);
         }
     }
-    const float* ns = nsum + b * 32;
-    const float* ss = ssq + b * 32;
-    const uint32_t jl = j << 5;
-    // pass 1 (unrolled, registers only): which slots could still enter the top-k
+    const uint32_t vmask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+    // pass 1 (registers only): which slots could still enter the top-k
     uint32_t need = 0;
+    const float ce = kEpsCross * sqq;
 #pragma unroll
     for (uint32_t n = 0; n < 32; ++n) {
-        const float nx = ns[n];
-        const float a = fmaf(-2.f, dot[n], nq + nx);
-        // err_bound(nq, nx, a) with sqrt(nq*nx) = sqrt(nq)*sqrt(nx) precomputed
-        const float e = fmaf(kEpsCross * sqq, ss[n],
-                             fmaf(kEpsRel, fabsf(a), fmaf(kEpsRel, nq + nx, 1e-30f)));
-        need |= (n < nvalid && a - e <= ubk) ? (1u << n) : 0u;  // hi < ubk implies lo <= ubk
+        const float t = nq + ns[n];
+        const float a = fmaf(-2.f, dot[n], t);
+        // err_bound(nq, ns, a) with sqrt(nq*ns) = sqrt(nq)*sqrt(ns) precomputed
+        const float e = fmaf(ce, ss[n], fmaf(kEpsRel, fabsf(a), fmaf(kEpsRel, t, 1e-30f)));
+        need |= (a - e <= ubk) ? (1u << n) : 0u;
     }
+    need &= vmask;
     if (!need) return;
-    // pass 2 (rare): park the dot products in this thread's scratch, walk the slots in order
+    // pass 2 (rare): the slots in order
+    const uint32_t jl = j << 5;
 #pragma unroll
-    for (uint32_t n = 0; n < 32; ++n) scratch[n * kM] = dot[n];
-    while (need) {
-        const uint32_t n = __ffs(need) - 1;
-        need &= need - 1;
-        const float nx = ns[n];
-        const float a = fmaf(-2.f, scratch[n * kM], nq + nx);
-        const float e = fmaf(kEpsCross * sqq, ss[n],
-                             fmaf(kEpsRel, fabsf(a), fmaf(kEpsRel, nq + nx, 1e-30f)));
+    for (uint32_t n = 0; n < 32; ++n) {
+        if (!(need & (1u << n))) continue;
+        const float t = nq + ns[n];
+        const float a = fmaf(-2.f, dot[n], t);
+        const float e = fmaf(ce, ss[n], fmaf(kEpsRel, fabsf(a), fmaf(kEpsRel, t, 1e-30f)));
         const float h = a + e, l = a - e;
         if (h < ubk) {  // keep the k smallest upper bounds, sorted
             float x = h;
 #pragma unroll
             for (int i = 0; i < KT; ++i) {
                 if (i < (int)p.k && x < ubl[i]) {
-                    const float t = ubl[i];
+                    const float tt = ubl[i];
                     ubl[i] = x;
-                    x = t;
+                    x = tt;
                 }
             }
             float kk = ubl[0];
@@ -298,17 +339,20 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, const TcItem& d, 
         if (l <= ubk && !overflow) {
             if (ncand == kKC) {  // compact against the tighter threshold
                 uint32_t w = 0;
-                for (uint32_t i = 0; i < kKC; ++i)
-                    if (my_lb[i * kM] <= ubk) {
-                        my_lb[w * kM] = my_lb[i * kM];
-                        my_loc[w * kM] = my_loc[i * kM];
+                for (uint32_t i = 0; i < kKC; ++i) {
+                    const float li = clb[i];
+                    if (li <= ubk) {
+                        const uint32_t ci = cloc[i];
+                        clb[w] = li;
+                        cloc[w] = ci;
                         ++w;
                     }
+                }
                 ncand = w;
             }
             if (ncand < kKC) {
-                my_lb[ncand * kM] = l;
-                my_loc[ncand * kM] = jl | n;
+                clb[ncand] = l;
+                cloc[ncand] = jl | n;
                 ++ncand;
             } else {
                 overflow = true;
@@ -323,25 +367,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                    const __grid_constant__ CUtensorMap map_arena) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-align the dynamic smem base (SWIZZLE_128B atoms)
-    unsigned char* smem = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    unsigned char* sB = smem;                                  // kNS * kStagePair
-    float* cent_s = reinterpret_cast<float*>(sB + kNS * kStagePair);        // kMaxD
-    float* npart = cent_s + kMaxD;                             // [kNB][16][32]
-    float* nsum = npart + kNB * 16 * 32;                       // [kNB][32]
-    float* ssq = nsum + kNB * 32;                              // [kNB][32] sqrt(nsum)
-    float* cand_lb = ssq + kNB * 32;                           // [kKC][128] (index-major)
-    uint32_t* cand_loc = reinterpret_cast<uint32_t*>(cand_lb + kM * kKC);
-    float* scr = reinterpret_cast<float*>(cand_loc + kM * kKC);  // [32][128] epilogue scratch
-    uint64_t* bars = reinterpret_cast<uint64_t*>(scr + 32 * kM);
-    uint64_t* full = bars;                // kNS
-    uint64_t* empty = full + kNS;         // kNS
-    uint64_t* cent_full = empty + kNS;    // kNS
-    uint64_t* acc_full = cent_full + kNS; // kNB
-    uint64_t* acc_empty = acc_full + kNB; // kNB
-    uint64_t* a_full = acc_empty + kNB;   // 1
-    uint64_t* it_full = a_full + 1;       // 2
-    uint64_t* it_empty = it_full + 2;     // 2
+    const uint32_t raw_s = smem_u32(smem_raw);
+    const uint32_t pad = ((raw_s + 1023u) & ~1023u) - raw_s;
+    unsigned char* sB = smem_raw + pad;                        // kNS * kStage
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kNS * kStage);
+    uint64_t* full = bars;                 // kNS
+    uint64_t* empty = full + kNS;          // kNS
+    uint64_t* acc_full = empty + kNS;      // kNB
+    uint64_t* acc_empty = acc_full + kNB;  // kNB
+    uint64_t* a_full = acc_empty + kNB;    // 1
+    uint64_t* a_free = a_full + 1;         // 1
+    uint64_t* it_full = a_free + 1;        // 2
+    uint64_t* it_empty = it_full + 2;      // 2
     int* ring = reinterpret_cast<int*>(it_empty + 2);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 2);
 
@@ -350,30 +387,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < kNS; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-            mbar_init(&cent_full[s], 1);
+            mbar_init(&empty[s], 1 + 4);  // MMA commit + the owning warpgroup's 4 warps
         }
         for (int b = 0; b < kNB; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], 4);
         }
-        mbar_init(a_full, 1);
+        mbar_init(a_full, kWG);
+        mbar_init(a_free, 1);
         for (int s = 0; s < 2; ++s) {
             mbar_init(&it_full[s], 1);
-            mbar_init(&it_empty[s], 5);
+            mbar_init(&it_empty[s], 1 + 4 * kWG);
         }
         fence_mbar_init();
     }
-    // zero the K-padding rows (D..Dk) of A and of every stage once: TMA never writes them
-    if (p.Dk != D) {
-        for (uint32_t i = threadIdx.x; i < kNS * (p.Dk - D) * 32; i += blockDim.x) {
-            const uint32_t s = i / ((p.Dk - D) * 32), r = i % ((p.Dk - D) * 32);
-            reinterpret_cast<float*>(sB + s * kStagePair + D * 128)[r] = 0.f;
-            reinterpret_cast<float*>(sB + s * kStagePair + kStageBytes + D * 128)[r] = 0.f;
-        }
-    }
-    fence_proxy_async();  // the zeroed padding rows are read by the async proxy
-    if (warp == 1) {  // TMEM: kNB accumulators x 32 fp32 columns
+    // zero the stages once: rows past D+1 (K padding up to Dk) are never
+    // written by TMA and must read as finite zeros
+    for (uint32_t i = threadIdx.x; i < kNS * kStage / 16; i += blockDim.x)
+        reinterpret_cast<float4*>(sB)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    fence_proxy_async();
+    if (warp == 1) {  // TMEM: A hi/lo + kNB accumulators
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
                      "r"(kTmemCols)
@@ -385,6 +418,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t n_items = *p.n_items_ptr;
+    const uint32_t stages = smem_u32(sB);
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
@@ -405,8 +439,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     bool ar;
                     int row;
                     group_row(p.L, d.c, d.off, j, ar, row);
-                    mbar_arrive_expect_tx(&full[st], D * 128u);
-                    tma_load_2d(sB + st * kStagePair, ar ? &map_arena : &map_off, 0, row, &full[st]);
+                    mbar_arrive_expect_tx(&full[st], 2u * (D + 1u) * 128u);
+                    const CUtensorMap* map = ar ? &map_arena : &map_off;
+                    tma_load_2d(sB + st * kStage, map, 0, row, &full[st]);
+                    tma_load_2d(sB + st * kStage + kRegion, map, 0, row + (int)D + 1, &full[st]);
                 }
             }
         }
@@ -414,7 +450,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // ------------------------------------------------ MMA issuer
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) |
                                ((32u >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
-        uint32_t unit = 0, aphase = 0;
+        uint32_t unit = 0, ne = 0;
         for (uint32_t seq = 0;; ++seq) {
             const uint32_t rs = seq & 1;
             mbar_wait(&it_full[rs], (seq >> 1) & 1);
@@ -424,17 +460,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (v < 0) break;
             const TcItem d = tc_decode(p, (uint32_t)v);
             if (d.g1 <= d.g0) continue;
-            mbar_wait(a_full, aphase & 1);
-            ++aphase;
+            mbar_wait(a_full, ne & 1);
+            ++ne;
             for (uint32_t j = d.g0; j < d.g1; ++j, ++unit) {
                 const uint32_t st = unit % kNS, b = unit % kNB;
-                mbar_wait(&cent_full[st], (unit / kNS) & 1);
+                mbar_wait(&full[st], (unit / kNS) & 1);
                 mbar_wait(&acc_empty[b], ((unit / kNB) & 1) ^ 1);
                 __syncwarp();
                 tc_fence_after();
                 if (lane == 0) {
                     // 3xTF32: A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (A from TMEM, B from smem)
-                    const uint32_t bh0 = smem_u32(sB + st * kStagePair), bl0 = bh0 + kStageBytes;
+                    const uint32_t bh0 = stages + st * (uint32_t)kStage, bl0 = bh0 + kRegion;
                     const uint32_t dcol = tmem_base + kColAcc + b * 32;
                     for (uint32_t ks = 0; ks < p.Dk / 8; ++ks) {
                         const uint64_t bh = umma_desc(bh0 + ks * 1024, 16384, 512, 1);
@@ -449,16 +485,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 __syncwarp();
             }
+            if (lane == 0) mma_commit(a_free);  // A may be rewritten once these MMAs retire
+            __syncwarp();
         }
     } else {
-        // ------------------------------------------------ math warps (128 threads)
-        const int mt = threadIdx.x - 64;             // 0..127
-        const int m = 32 * (warp & 3) + lane;        // TMEM lane / query row of the tile
-        const uint32_t taddr_lane = (uint32_t)(32 * (warp & 3)) << 16;
-        float* my_lb = cand_lb + m;       // entry i at my_lb[i * kM]
-        uint32_t* my_loc = cand_loc + m;
-        float* my_scr = scr + m;
-        uint32_t unit = 0;
+        // ------------------------------------------------ math warpgroups
+        const int wg = (warp - 2) >> 2;               // 0: builds A_hi, 1: builds A_lo
+        const int q4 = warp & 3;                      // TMEM lane quarter of this warp
+        const int m = 32 * q4 + lane;                 // query row of the tile
+        const int wt = threadIdx.x - 64 - 128 * wg;   // 0..127 within the warpgroup
+        const uint32_t taddr_lane = (uint32_t)(32 * q4) << 16;
+        uint32_t unit = 0, ne = 0;
         for (uint32_t seq = 0;; ++seq) {
             const uint32_t rs = seq & 1;
             mbar_wait(&it_full[rs], (seq >> 1) & 1);
@@ -467,122 +504,79 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0) mbar_arrive(&it_empty[rs]);
             if (v < 0) break;
             const TcItem d = tc_decode(p, (uint32_t)v);
-            // centroid of the list
-            for (uint32_t i = mt; i < D; i += 128) cent_s[i] = p.centroids[(uint64_t)d.c * D + i];
-            named_bar(1, 128);
-            // A = centred queries r = q - c, split r = r_hi + r_lo (r_hi = TF32 truncation,
-            // r_lo exact in fp32) into TMEM: lane m = query row, columns = dims.
             const bool active = (uint32_t)m < d.npairs;
-            uint32_t pair = 0;
-            float nq = 0.f;
-            const float* q = nullptr;
-            if (active) {
-                pair = d.pairs[m];
-                q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
-            }
-            __syncwarp();  // tcgen05.st is .sync.aligned
-            for (uint32_t c0 = 0; c0 < p.Dk; c0 += 32) {
-                uint32_t vh[32], vl[32];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const uint32_t k = c0 + i;
-                    float r = 0.f;
-                    if (active && k < D) r = __fsub_rn(q[k], cent_s[k]);
-                    nq = __fadd_rn(nq, __fmul_rn(r, r));
-                    const float h = tf32_trunc(r);
-                    vh[i] = __float_as_uint(h);
-                    vl[i] = __float_as_uint(__fsub_rn(r, h));
-                }
-                __syncwarp();
-                BIVF_TMEM_ST32(tmem_base + taddr_lane + c0, vh);
-                BIVF_TMEM_ST32(tmem_base + taddr_lane + kColAlo + c0, vl);
-            }
-            __syncwarp();
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            named_bar(1, 128);
-            if (mt == 0 && d.g1 > d.g0) mbar_arrive(a_full);
-
-            // per-query running state
+            const uint32_t pair = active ? d.pairs[m] : 0u;
+            const uint64_t run = ((((uint64_t)pair * p.maxch + d.chunk) << 1) | (uint32_t)wg);
+            float* clb = p.clb + run * kKC;
+            uint32_t* cloc = p.cloc + run * kKC;
             float ubl[KT];
 #pragma unroll
             for (int i = 0; i < KT; ++i) ubl[i] = __int_as_float(0x7f800000);
             float ubk = __int_as_float(0x7f800000);
             uint32_t ncand = 0;
             bool overflow = false;
-
-            const float sqq = sqrtf(nq);
-            for (uint32_t j = d.g0; j < d.g1; ++j, ++unit) {
-                const uint32_t st = unit % kNS, b = unit % kNB;
-                mbar_wait(&full[st], (unit / kNS) & 1);
-                // centre in place; thread -> slots 4*(mt&7)..+3, rows (mt>>3) + 16i.
-                // 128B_ATOM_32B swizzle: 32-byte chunk (slot/8) ^ (row % 4).
-                {
-                    const uint32_t sq = mt & 7, r0 = mt >> 3;
-                    unsigned char* base = sB + st * kStagePair;
-                    float4 part = make_float4(0.f, 0.f, 0.f, 0.f);
-                    for (uint32_t k = r0; k < D; k += 16) {
-                        const uint32_t off = k * 128 + (((sq >> 1) ^ (k & 3)) << 5) + (sq & 1) * 16;
-                        float4* px = reinterpret_cast<float4*>(base + off);
-                        float4* pl = reinterpret_cast<float4*>(base + kStageBytes + off);
-                        float4 v = *px;
-                        const float cc = cent_s[k];
-                        v.x = __fsub_rn(v.x, cc);
-                        v.y = __fsub_rn(v.y, cc);
-                        v.z = __fsub_rn(v.z, cc);
-                        v.w = __fsub_rn(v.w, cc);
-                        part.x = fmaf(v.x, v.x, part.x);
-                        part.y = fmaf(v.y, v.y, part.y);
-                        part.z = fmaf(v.z, v.z, part.z);
-                        part.w = fmaf(v.w, v.w, part.w);
-                        const float4 h = make_float4(tf32_trunc(v.x), tf32_trunc(v.y), tf32_trunc(v.z),
-                                                     tf32_trunc(v.w));
-                        *px = h;
-                        *pl = make_float4(__fsub_rn(v.x, h.x), __fsub_rn(v.y, h.y),
-                                          __fsub_rn(v.z, h.z), __fsub_rn(v.w, h.w));
-                    }
-                    *reinterpret_cast<float4*>(npart + (b * 16 + r0) * 32 + 4 * sq) = part;
-                }
-                fence_proxy_async();
-                named_bar(1, 128);
-                if (mt < 32) {
-                    const float* pp = npart + b * 512 + mt;
-                    float t = 0.f;
+            if (d.g1 > d.g0) {
+                // A = centred queries r = q - c of the tile, r = r_hi + r_lo (r_hi = TF32
+                // truncation, r_lo exact in fp32): lane m = query row, columns = dims.
+                if (ne > 0) mbar_wait(a_free, (ne - 1) & 1);
+                ++ne;
+                const float* q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
+                const float* cen = p.centroids + (uint64_t)d.c * D;
+                float nq = 0.f;
+                __syncwarp();
+                tc_fence_after();
+                for (uint32_t c0 = 0; c0 < p.Dk; c0 += 32) {
+                    uint32_t vv[32];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) t += pp[32 * i];
-                    nsum[b * 32 + mt] = t;
-                    ssq[b * 32 + mt] = sqrtf(t);
+                    for (int i = 0; i < 32; i += 4) {
+                        const uint32_t k = c0 + i;
+                        float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (active && k < p.Dp) qv = *reinterpret_cast<const float4*>(q + k);
+                        const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            float r = 0.f;
+                            if (active && k + e < D) r = __fsub_rn(qa[e], __ldg(cen + k + e));
+                            nq = __fadd_rn(nq, __fmul_rn(r, r));
+                            const float h = tf32_trunc(r);
+                            vv[i + e] = __float_as_uint(wg == 0 ? h : __fsub_rn(r, h));
+                        }
+                    }
+                    __syncwarp();
+                    BIVF_TMEM_ST32(tmem_base + taddr_lane + (wg ? kColAlo : 0u) + c0, vv);
                 }
-                if (mt == 0) mbar_arrive(&cent_full[st]);
-                named_bar(1, 128);
-                if (j > d.g0)
-                    tc_epilogue<KT>(p, d, unit - 1, j - 1, acc_full, acc_empty, nsum, ssq, tmem_base,
-                                    taddr_lane, lane, active, nq, sqq, ubl, ubk, ncand, overflow,
-                                    my_lb, my_loc, my_scr);
+                __syncwarp();
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                tc_fence_before();
+                named_bar(1 + wg, 128);
+                if (wt == 0) mbar_arrive(a_full);
+                const float sqq = sqrtf(nq);
+                for (uint32_t j = d.g0; j < d.g1; ++j, ++unit) {
+                    if ((unit & 1u) != (uint32_t)wg) continue;
+                    tc_unit<KT>(p, d, unit, j, full, empty, acc_full, acc_empty, stages, tmem_base,
+                                taddr_lane, lane, active, nq, sqq, ubl, ubk, ncand, overflow, clb,
+                                cloc);
+                }
             }
-            if (d.g1 > d.g0)
-                tc_epilogue<KT>(p, d, unit - 1, d.g1 - 1, acc_full, acc_empty, nsum, ssq, tmem_base,
-                                taddr_lane, lane, active, nq, sqq, ubl, ubk, ncand, overflow, my_lb,
-                                my_loc, my_scr);
-
-            // item output: k upper bounds + surviving candidates
+            // run output: k upper bounds + surviving candidates (compacted in place)
             if (active) {
-                const uint64_t run = (uint64_t)pair * p.maxch + d.chunk;
 #pragma unroll
                 for (int i = 0; i < KT; ++i)
                     if (i < (int)p.k) p.ub[run * p.k + i] = ubl[i];
                 uint32_t w = 0;
                 if (!overflow) {
-                    for (uint32_t i = 0; i < ncand; ++i)
-                        if (my_lb[i * kM] <= ubk) {
-                            p.clb[run * kKC + w] = my_lb[i * kM];
-                            p.cloc[run * kKC + w] = my_loc[i * kM];
+                    for (uint32_t i = 0; i < ncand; ++i) {
+                        const float li = clb[i];
+                        if (li <= ubk) {
+                            const uint32_t ci = cloc[i];
+                            clb[w] = li;
+                            cloc[w] = ci;
                             ++w;
                         }
+                    }
                 }
                 p.ccount[run] = overflow ? kKC + 1 : w;
             }
-            named_bar(1, 128);
         }
     }
     __syncthreads();
@@ -634,8 +628,8 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
     for (uint32_t pi = 0; pi < p.P; ++pi) {
         const uint32_t c = (uint32_t)probes[(uint64_t)q * p.P + pi];
         const uint32_t n = p.nch[c];
-        for (uint32_t h = 0; h < n; ++h) {
-            const uint64_t run = ((uint64_t)q * p.P + pi) * p.maxch + h;
+        for (uint32_t hw = 0; hw < 2 * n; ++hw) {  // (chunk, warpgroup) runs
+            const uint64_t run = ((((uint64_t)q * p.P + pi) * p.maxch) << 1) + hw;
             for (uint32_t e0 = 0; e0 < p.k; e0 += 32) {
                 const uint32_t e = e0 + lane;
                 const float v = e < p.k ? p.ub[run * p.k + e] : 0.f;
@@ -688,20 +682,24 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
         const uint32_t n = p.nch[c];
         const uint32_t off = p.snap_off[c], len = p.snap_len[c];
         for (uint32_t h = 0; h < n; ++h) {
-            const uint64_t run = ((uint64_t)q * p.P + pi) * p.maxch + h;
-            const uint32_t cnt = p.ccount[run];
-            if (cnt <= kKC) {
-                const bool pass = lane < cnt && p.clb[run * kKC + lane] <= theta;
-                const unsigned msk = __ballot_sync(0xffffffffu, pass);
-                const uint32_t np = __popc(msk);
-                if (qn + np > 32) flush();
-                if (pass) {
-                    const uint32_t slot = qn + __popc(msk & ((1u << lane) - 1u));
-                    qc[slot] = c;
-                    ql[slot] = p.cloc[run * kKC + lane];
+            const uint64_t run0 = ((((uint64_t)q * p.P + pi) * p.maxch + h) << 1);
+            const uint32_t cnt0 = p.ccount[run0], cnt1 = p.ccount[run0 + 1];
+            if (cnt0 <= kKC && cnt1 <= kKC) {
+                for (uint32_t w = 0; w < 2; ++w) {
+                    const uint64_t run = run0 + w;
+                    const uint32_t cnt = w ? cnt1 : cnt0;
+                    const bool pass = lane < cnt && p.clb[run * kKC + lane] <= theta;
+                    const unsigned msk = __ballot_sync(0xffffffffu, pass);
+                    const uint32_t np = __popc(msk);
+                    if (qn + np > 32) flush();
+                    if (pass) {
+                        const uint32_t slot = qn + __popc(msk & ((1u << lane) - 1u));
+                        qc[slot] = c;
+                        ql[slot] = p.cloc[run * kKC + lane];
+                    }
+                    qn += np;
+                    __syncwarp();
                 }
-                qn += np;
-                __syncwarp();
             } else {  // overflow: exact rescan of the chunk
                 const uint32_t ng = ivf_ngroups(p.L, off, len);
                 const uint32_t g0 = h * p.gc[c], g1 = min(ng, g0 + p.gc[c]);
@@ -729,8 +727,7 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
 }
 
 size_t tc_smem_bytes() {
-    return 1024 + kNS * kStagePair + kMaxD * 4 + kNB * 16 * 32 * 4 + 2 * kNB * 32 * 4 +
-           kM * kKC * 8 + 32 * kM * 4 + 32 * 8 + 64;
+    return 1024 + kNS * kStage + (2 * kNS + 2 * kNB + 6) * 8 + 16 + 16;
 }
 
 }  // namespace
@@ -755,12 +752,12 @@ bool tc_supported(uint32_t D, uint32_t k, int metric) {
     return metric == kL2 && D >= 8 && D <= (uint32_t)kMaxD && k <= 32;
 }
 
-cudaError_t make_group_map(const float* base, uint64_t rows, uint32_t D, CUtensorMap* out) {
+cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUtensorMap* out) {
     auto enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
-    cuuint64_t dims[2] = {32, std::max<cuuint64_t>(rows, 1)};
+    cuuint64_t dims[2] = {32, std::max<cuuint64_t>(groups * (2ull * D + 2), 1)};
     cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {32, D};
+    cuuint32_t box[2] = {32, D + 1};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -815,8 +812,10 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
         attr = true;
     }
     if (ev0) cudaEventRecord(ev0, s);
-    if (sh.k <= 16) scan_tc_kernel<16><<<num_sms, kTcThreads, sm, s>>>(p, map_off, map_arena);
-    else scan_tc_kernel<32><<<num_sms, kTcThreads, sm, s>>>(p, map_off, map_arena);
+    int grid = num_sms;
+    if (const char* g = std::getenv("BIVF_TC_GRID")) grid = std::max(1, atoi(g));  // debugging aid
+    if (sh.k <= 16) scan_tc_kernel<16><<<grid, kTcThreads, sm, s>>>(p, map_off, map_arena);
+    else scan_tc_kernel<32><<<grid, kTcThreads, sm, s>>>(p, map_off, map_arena);
     count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

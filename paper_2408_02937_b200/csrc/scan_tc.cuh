@@ -13,6 +13,7 @@ namespace bivf {
 constexpr uint32_t kKC = 32;  // candidate slots per (query, list chunk) run
 
 // per-search scratch of the TC path (lease workspace)
+// runs = pairs * maxch * 2 (one per chunk and math warpgroup)
 struct TcBufs {
     float* ub;          // [runs][k]  upper bounds (k smallest)
     uint32_t* ccount;   // [runs]     candidates kept (kKC + 1 = overflow -> exact rescan)
@@ -22,9 +23,9 @@ struct TcBufs {
 
 bool tc_supported(uint32_t D, uint32_t k, int metric);
 
-// 2-D TMA map over a region of 32-float rows (one dim of one 32-vector
-// group per row), box = {32, D}, SWIZZLE_128B_ATOM_32B.
-cudaError_t make_group_map(const float* base, uint64_t rows, uint32_t D, CUtensorMap* out);
+// 2-D TMA map over a scan mirror region (mirror.cuh: `groups` groups of
+// 2D+2 rows of 32 floats), box = {32, D+1}, SWIZZLE_128B_ATOM_32B.
+cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUtensorMap* out);
 
 cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,
                                  const float* queries, const float* centroids,
