@@ -46,7 +46,7 @@ namespace {
 constexpr int kWG = 2;                     // math warpgroups
 constexpr int kTcThreads = 64 + 128 * kWG;  // warp0 TMA, warp1 MMA, warps 2.. math
 constexpr int kM = 128;                    // queries per tile (MMA M, TMEM lanes)
-constexpr int kNS = 6;                     // smem stages (one group each; even)
+constexpr int kNS = 5;                     // smem stages (one group each)
 constexpr int kNB = 8;                     // TMEM accumulators (32 columns each; even)
 constexpr int kMaxD = 128;
 // a stage = two 1024-aligned regions of (D+1) 128-byte rows: [s_hi | |s|^2], [s_lo | |s|]
@@ -256,35 +256,14 @@ __device__ __forceinline__ void load_row32(uint32_t region, uint32_t r, float (&
     }
 }
 
-// One group (unit u, group j of the item) for this thread's query: 32 dot
-// products from TMEM + the group's norms from the stage -> bounds, the k
-// smallest upper bounds, and the candidates whose lower bound can still
-// enter the top-k (written straight to the run's global buffer; rare).
+// bounds + filtering of one group for this thread's query (see tc_unit)
 template <int KT>
-__device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint32_t u, uint32_t j,
-                                        uint64_t* full, uint64_t* empty, uint64_t* acc_full,
-                                        uint64_t* acc_empty, uint32_t stages, uint32_t tmem_base,
-                                        uint32_t taddr_lane, int lane, bool active, float nq,
-                                        float sqq, float (&ubl)[KT], float& ubk, uint32_t& ncand,
-                                        bool& overflow, float* clb, uint32_t* cloc) {
-    const uint32_t b = u % kNB, st = u % kNS;
-    mbar_wait(&acc_full[b], (u / kNB) & 1);
-    __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread spin
-    tc_fence_after();
-    float dot[32];
-    tmem_ld32(tmem_base + taddr_lane + kColAcc + b * 32, dot);
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&acc_empty[b]);
-    // the group's norms (row D of both regions); full[st] has completed this
-    // phase already (its MMA did), the wait makes the TMA writes visible here
-    mbar_wait(&full[st], (u / kNS) & 1);
-    float ns[32], ss[32];
-    const uint32_t sbase = stages + st * (uint32_t)kStage;
-    load_row32(sbase, p.D, ns);
-    load_row32(sbase + kRegion, p.D, ss);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+__device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, uint32_t j,
+                                          uint32_t sbase, bool active, float nq, float sqq,
+                                          const float (&dot)[32], const float (&ns)[32],
+                                          const float (&ss)[32], float (&ubl)[KT], float& ubk,
+                                          uint32_t& ncand, bool& overflow, float* clb,
+                                          uint32_t* cloc, float* scr) {
     if (!active) return;
     // valid slots of group j, from the snapshot (no table lookups)
     uint32_t nvalid;
@@ -311,30 +290,35 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
     }
     need &= vmask;
     if (!need) return;
-    // pass 2 (rare): the slots in order
-    const uint32_t jl = j << 5;
+    // pass 2 (a few slots per group): park the dot products in this thread's
+    // scratch column and walk the surviving slots in order
 #pragma unroll
-    for (uint32_t n = 0; n < 32; ++n) {
-        if (!(need & (1u << n))) continue;
-        const float t = nq + ns[n];
-        const float a = fmaf(-2.f, dot[n], t);
-        const float e = fmaf(ce, ss[n], fmaf(kEpsRel, fabsf(a), fmaf(kEpsRel, t, 1e-30f)));
+    for (uint32_t n = 0; n < 32; ++n) scr[n * kM] = dot[n];
+    const uint32_t jl = j << 5;
+    const uint32_t nrow0 = sbase + p.D * 128u, nrow1 = nrow0 + kRegion, rsw = p.D & 3u;
+    while (need) {
+        const uint32_t n = __ffs(need) - 1;
+        need &= need - 1;
+        const uint32_t so = (((n >> 3) ^ rsw) << 5) + (n & 7u) * 4u;
+        float nx, sx;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nx) : "r"(nrow0 + so));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(sx) : "r"(nrow1 + so));
+        const float t = nq + nx;
+        const float a = fmaf(-2.f, scr[n * kM], t);
+        const float e = fmaf(ce, sx, fmaf(kEpsRel, fabsf(a), fmaf(kEpsRel, t, 1e-30f)));
         const float h = a + e, l = a - e;
         if (h < ubk) {  // keep the k smallest upper bounds, sorted
+            // ubl: ascending; entries [0, KT-k) are -inf sentinels, [KT-k, KT) the
+            // k smallest upper bounds, so the k-th is always ubl[KT-1] (static
+            // register indices only; a min/max bubble drops the largest)
             float x = h;
 #pragma unroll
             for (int i = 0; i < KT; ++i) {
-                if (i < (int)p.k && x < ubl[i]) {
-                    const float tt = ubl[i];
-                    ubl[i] = x;
-                    x = tt;
-                }
+                const float lo = fminf(x, ubl[i]);
+                x = fmaxf(x, ubl[i]);
+                ubl[i] = lo;
             }
-            float kk = ubl[0];
-#pragma unroll
-            for (int i = 1; i < KT; ++i)
-                if (i == (int)p.k - 1) kk = ubl[i];
-            ubk = kk;
+            ubk = ubl[KT - 1];
         }
         if (l <= ubk && !overflow) {
             if (ncand == kKC) {  // compact against the tighter threshold
@@ -361,6 +345,40 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
     }
 }
 
+// One group (unit u, group j of the item) for this thread's query: 32 dot
+// products from TMEM + the group's norms from the stage -> bounds, the k
+// smallest upper bounds, and the candidates whose lower bound can still
+// enter the top-k (written straight to the run's global buffer; rare).
+template <int KT>
+__device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint32_t u, uint32_t j,
+                                        uint64_t* full, uint64_t* empty, uint64_t* acc_full,
+                                        uint64_t* acc_empty, uint32_t stages, uint32_t tmem_base,
+                                        uint32_t taddr_lane, int lane, bool active, float nq,
+                                        float sqq, float (&ubl)[KT], float& ubk, uint32_t& ncand,
+                                        bool& overflow, float* clb, uint32_t* cloc,
+                                        float* scr) {
+    const uint32_t b = u % kNB, st = u % kNS;
+    mbar_wait(&acc_full[b], (u / kNB) & 1);
+    __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread spin
+    tc_fence_after();
+    float dot[32];
+    tmem_ld32(tmem_base + taddr_lane + kColAcc + b * 32, dot);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&acc_empty[b]);
+    // the group's norms (row D of both regions); full[st] has completed this
+    // phase already (its MMA did), the wait makes the TMA writes visible here
+    mbar_wait(&full[st], (u / kNS) & 1);
+    float ns[32], ss[32];
+    const uint32_t sbase = stages + st * (uint32_t)kStage;
+    load_row32(sbase, p.D, ns);
+    load_row32(sbase + kRegion, p.D, ss);
+    tc_filter<KT>(p, d, j, sbase, active, nq, sqq, dot, ns, ss, ubl, ubk, ncand, overflow, clb,
+                  cloc, scr);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // norms read: the stage may be refilled
+}
+
 template <int KT>
 __global__ void __launch_bounds__(kTcThreads, 1)
     scan_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_off,
@@ -370,7 +388,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint32_t raw_s = smem_u32(smem_raw);
     const uint32_t pad = ((raw_s + 1023u) & ~1023u) - raw_s;
     unsigned char* sB = smem_raw + pad;                        // kNS * kStage
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kNS * kStage);
+    float* scratch = reinterpret_cast<float*>(sB + kNS * kStage);  // [kWG][32][kM] pass-2 dots
+    uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + kWG * 32 * kM);
     uint64_t* full = bars;                 // kNS
     uint64_t* empty = full + kNS;          // kNS
     uint64_t* acc_full = empty + kNS;      // kNB
@@ -511,7 +530,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             uint32_t* cloc = p.cloc + run * kKC;
             float ubl[KT];
 #pragma unroll
-            for (int i = 0; i < KT; ++i) ubl[i] = __int_as_float(0x7f800000);
+            for (int i = 0; i < KT; ++i)
+                ubl[i] = i < KT - (int)p.k ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
             float ubk = __int_as_float(0x7f800000);
             uint32_t ncand = 0;
             bool overflow = false;
@@ -555,14 +575,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     if ((unit & 1u) != (uint32_t)wg) continue;
                     tc_unit<KT>(p, d, unit, j, full, empty, acc_full, acc_empty, stages, tmem_base,
                                 taddr_lane, lane, active, nq, sqq, ubl, ubk, ncand, overflow, clb,
-                                cloc);
+                                cloc, scratch + wg * 32 * kM + m);
                 }
             }
             // run output: k upper bounds + surviving candidates (compacted in place)
             if (active) {
 #pragma unroll
                 for (int i = 0; i < KT; ++i)
-                    if (i < (int)p.k) p.ub[run * p.k + i] = ubl[i];
+                    if (i >= KT - (int)p.k) p.ub[run * p.k + (i - (KT - (int)p.k))] = ubl[i];
                 uint32_t w = 0;
                 if (!overflow) {
                     for (uint32_t i = 0; i < ncand; ++i) {
@@ -727,7 +747,7 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
 }
 
 size_t tc_smem_bytes() {
-    return 1024 + kNS * kStage + (2 * kNS + 2 * kNB + 6) * 8 + 16 + 16;
+    return 1024 + kNS * kStage + kWG * 32 * kM * 4 + (2 * kNS + 2 * kNB + 6) * 8 + 16 + 16;
 }
 
 }  // namespace

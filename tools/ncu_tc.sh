@@ -1,5 +1,5 @@
 #!/bin/bash
-# ncu captures of the tensor-core scan + refine (run on the GPU box)
+# ncu capture of the tensor-core scan + refine (run on the GPU box): tools/ncu_tc.sh <tag>
 tag=${1:-r01}
 PROF_REPS=2 timeout -s KILL 600 ncu --set full --clock-control none --import-source on \
   -k "regex:scan_tc_kernel|refine_kernel" -s 2 -c 2 -o gpurun_out/prof_tc_$tag \
