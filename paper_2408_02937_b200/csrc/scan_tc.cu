@@ -46,7 +46,7 @@ namespace {
 constexpr int kWG = 2;                     // math warpgroups
 constexpr int kTcThreads = 64 + 128 * kWG;  // warp0 TMA, warp1 MMA, warps 2.. math
 constexpr int kM = 128;                    // queries per tile (MMA M, TMEM lanes)
-constexpr int kNS = 5;                     // smem stages (one group each)
+constexpr int kNS = 4;                     // smem stages (one group each)
 constexpr int kNB = 8;                     // TMEM accumulators (32 columns each; even)
 constexpr int kMaxD = 128;
 // a stage = two 1024-aligned regions of (D+1) 128-byte rows: [s_hi | |s|^2], [s_lo | |s|]
@@ -324,19 +324,19 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
             if (ncand == kKC) {  // compact against the tighter threshold
                 uint32_t w = 0;
                 for (uint32_t i = 0; i < kKC; ++i) {
-                    const float li = clb[i];
+                    const float li = clb[i * kM];
                     if (li <= ubk) {
-                        const uint32_t ci = cloc[i];
-                        clb[w] = li;
-                        cloc[w] = ci;
+                        const uint32_t ci = cloc[i * kM];
+                        clb[w * kM] = li;
+                        cloc[w * kM] = ci;
                         ++w;
                     }
                 }
                 ncand = w;
             }
             if (ncand < kKC) {
-                clb[ncand] = l;
-                cloc[ncand] = jl | n;
+                clb[ncand * kM] = l;
+                cloc[ncand * kM] = jl | n;
                 ++ncand;
             } else {
                 overflow = true;
@@ -389,7 +389,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint32_t pad = ((raw_s + 1023u) & ~1023u) - raw_s;
     unsigned char* sB = smem_raw + pad;                        // kNS * kStage
     float* scratch = reinterpret_cast<float*>(sB + kNS * kStage);  // [kWG][32][kM] pass-2 dots
-    uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + kWG * 32 * kM);
+    float* cand_lb = scratch + kWG * 32 * kM;                        // [kWG][kKC][kM]
+    uint32_t* cand_loc = reinterpret_cast<uint32_t*>(cand_lb + kWG * kKC * kM);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(cand_loc + kWG * kKC * kM);
     uint64_t* full = bars;                 // kNS
     uint64_t* empty = full + kNS;          // kNS
     uint64_t* acc_full = empty + kNS;      // kNB
@@ -526,8 +528,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const bool active = (uint32_t)m < d.npairs;
             const uint32_t pair = active ? d.pairs[m] : 0u;
             const uint64_t run = ((((uint64_t)pair * p.maxch + d.chunk) << 1) | (uint32_t)wg);
-            float* clb = p.clb + run * kKC;
-            uint32_t* cloc = p.cloc + run * kKC;
+            float* clb = cand_lb + wg * kKC * kM + m;      // this thread's candidate column
+            uint32_t* cloc = cand_loc + wg * kKC * kM + m;
             float ubl[KT];
 #pragma unroll
             for (int i = 0; i < KT; ++i)
@@ -586,11 +588,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 uint32_t w = 0;
                 if (!overflow) {
                     for (uint32_t i = 0; i < ncand; ++i) {
-                        const float li = clb[i];
+                        const float li = clb[i * kM];
                         if (li <= ubk) {
-                            const uint32_t ci = cloc[i];
-                            clb[w] = li;
-                            cloc[w] = ci;
+                            p.clb[run * kKC + w] = li;
+                            p.cloc[run * kKC + w] = cloc[i * kM];
                             ++w;
                         }
                     }
@@ -747,7 +748,8 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
 }
 
 size_t tc_smem_bytes() {
-    return 1024 + kNS * kStage + kWG * 32 * kM * 4 + (2 * kNS + 2 * kNB + 6) * 8 + 16 + 16;
+    return 1024 + kNS * kStage + kWG * 32 * kM * 4 + kWG * kKC * kM * 8 +
+           (2 * kNS + 2 * kNB + 6) * 8 + 16 + 16;
 }
 
 }  // namespace

@@ -10,7 +10,7 @@
 
 namespace bivf {
 
-constexpr uint32_t kKC = 32;  // candidate slots per (query, list chunk) run
+constexpr uint32_t kKC = 24;  // candidate slots per run (query, list chunk, warpgroup)
 
 // per-search scratch of the TC path (lease workspace)
 // runs = pairs * maxch * 2 (one per chunk and math warpgroup)
