@@ -213,6 +213,8 @@ void GpuIndex::alloc_device() {
     if (mir_on_) {
         d_arena_mir_.alloc((size_t)NB_ * MPS_ * 4);
         BIVF_CUDA(dset(d_arena_mir_.p, 0, d_arena_mir_.bytes));
+        d_arena_nrm_.alloc((size_t)NB_ * gpb_ * kNormFloats * 4);
+        BIVF_CUDA(dset(d_arena_nrm_.p, 0, d_arena_nrm_.bytes));
         tc_ok_ = make_mirror_map(d_arena_mir_.as<float>(), (uint64_t)NB_ * gpb_, D_, &map_arena_) ==
                  cudaSuccess;
     }
@@ -253,6 +255,8 @@ void GpuIndex::ensure_offline_capacity(uint64_t slots) {
     if (mir_on_) {
         d_off_mir_.alloc((size_t)(slots / 32) * GF_ * 4);
         BIVF_CUDA(dset(d_off_mir_.p, 0, d_off_mir_.bytes));
+        d_off_nrm_.alloc((size_t)(slots / 32) * kNormFloats * 4);
+        BIVF_CUDA(dset(d_off_nrm_.p, 0, d_off_nrm_.bytes));
         if (make_mirror_map(d_off_mir_.as<float>(), slots / 32, D_, &map_off_) != cudaSuccess)
             tc_ok_ = false;
     }
@@ -263,8 +267,11 @@ MirrorView GpuIndex::mirror_view() const {
     MirrorView M{};
     M.off_mir = d_off_mir_.as<float>();
     M.arena_mir = d_arena_mir_.as<float>();
+    M.off_nrm = d_off_nrm_.as<float>();
+    M.arena_nrm = d_arena_nrm_.as<float>();
     M.cent = d_cent_.as<float>();
     M.D = D_;
+    M.K = mirror_k(D_);
     M.T = T_;
     M.gpb = gpb_;
     M.GF = GF_;
@@ -625,7 +632,8 @@ void GpuIndex::enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uin
     ss.metric = cfg_.metric;
     if (use_tc(k)) {
         BIVF_CUDA(launch_ivf_search_tc(dev_lists(), w.plan, w.probes, w.queries,
-                                       d_cent_.as<float>(), ss, map_off_, map_arena_, w.tc, w.out_d,
+                                       d_cent_.as<float>(), ss, map_off_, map_arena_,
+                                       d_off_nrm_.as<float>(), d_arena_nrm_.as<float>(), w.tc, w.out_d,
                                        w.out_i, w.out_cnt, num_sms_, l.stream,
                                        timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr));
     } else {
@@ -1088,7 +1096,7 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
     DevBuf dpa, dia, dscr_p, dscr_i, dclr, dli, dlv, doi, dov;
     dpa.alloc(std::max<size_t>(pa.size(), 1) * 8);
     dia.alloc(std::max<size_t>(ia.size(), 1) * 8);
-    dscr_p.alloc(std::max<size_t>((size_t)nm * (mir_on_ ? 2 * D_ + 2 : D_), 1) * 4);
+    dscr_p.alloc(std::max<size_t>((size_t)nm * (mir_on_ ? 2 * mirror_k(D_) + 2 : D_), 1) * 4);
     dscr_i.alloc(std::max<size_t>(nm, 1) * 8);
     dclr.alloc(std::max<size_t>(clear.size(), 1) * 8);
     dli.alloc(std::max<size_t>(len_idx.size(), 1) * 4);
@@ -1334,10 +1342,14 @@ void GpuIndex::rearrange(uint32_t c) {
             BIVF_CUDA(launch_block_moves(d_arena_.as<float>(), d_bids_.as<long long>(), PS_, T_,
                                          ds.as<int32_t>(), dd.as<int32_t>(), nm, sp.as<float>(),
                                          si.as<long long>(), st));
-            if (mir_on_)
+            if (mir_on_) {
                 BIVF_CUDA(launch_block_moves(d_arena_mir_.as<float>(), nullptr, MPS_, T_,
                                              ds.as<int32_t>(), dd.as<int32_t>(), nm, sp.as<float>(),
                                              nullptr, st));
+                BIVF_CUDA(launch_block_moves(d_arena_nrm_.as<float>(), nullptr,
+                                             (uint64_t)gpb_ * kNormFloats, T_, ds.as<int32_t>(),
+                                             dd.as<int32_t>(), nm, sp.as<float>(), nullptr, st));
+            }
             for (uint32_t k : rowc) {
                 staged.push_back(h_blocks_[k]);
                 auto& r = staged.back();

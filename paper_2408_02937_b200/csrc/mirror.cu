@@ -13,29 +13,36 @@ __device__ __forceinline__ float tf32_trunc_m(float x) {
     return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-// one vector -> its mirror column `lane` of group `g`.  x[d * xs] is dim d.
-__device__ __forceinline__ void mirror_column(float* g, uint32_t lane, const float* x, uint32_t xs,
-                                              const float* c, uint32_t D) {
+// one vector -> its mirror column `lane` of group `g` (+ the group's norm block
+// `nrm`).  x[d * xs] is dim d.
+__device__ __forceinline__ void mirror_column(float* g, float* nrm, uint32_t lane, const float* x,
+                                              uint32_t xs, const float* c, uint32_t D,
+                                              uint32_t K) {
     float n2 = 0.f;
     for (uint32_t d = 0; d < D; ++d) {
         const float s = __fsub_rn(x[(uint64_t)d * xs], c[d]);
         const float h = tf32_trunc_m(s);
         g[(uint64_t)d * 32u + lane] = h;
-        g[(uint64_t)(D + 1 + d) * 32u + lane] = __fsub_rn(s, h);
+        g[(uint64_t)(K + d) * 32u + lane] = __fsub_rn(s, h);
         n2 = __fadd_rn(n2, __fmul_rn(s, s));
     }
-    g[(uint64_t)D * 32u + lane] = n2;
-    g[(uint64_t)(2 * D + 1) * 32u + lane] = sqrtf(n2);
+    nrm[lane] = n2;
+    nrm[32 + lane] = sqrtf(n2);
 }
 
-__device__ __forceinline__ float* mirror_slot(const MirrorView& M, uint64_t a, uint32_t& lane) {
+// group base (mirror planes) and norm block of a slot address
+__device__ __forceinline__ float* mirror_slot(const MirrorView& M, uint64_t a, uint32_t& lane,
+                                              float*& nrm) {
     if (a >> 63) {
         const uint64_t gs = a & ~(1ull << 63);
         const uint64_t blk = gs / M.T, slot = gs - blk * M.T;
         lane = (uint32_t)(slot & 31u);
-        return M.arena_mir + blk * M.MPS + (slot >> 5) * M.GF;
+        const uint64_t g = blk * M.gpb + (slot >> 5);
+        nrm = M.arena_nrm + g * kNormFloats;
+        return M.arena_mir + g * M.GF;
     }
     lane = (uint32_t)(a & 31u);
+    nrm = M.off_nrm + (a >> 5) * kNormFloats;
     return M.off_mir + (a >> 5) * M.GF;
 }
 
@@ -46,8 +53,9 @@ __global__ void mirror_insert_kernel(MirrorView M, uint32_t n, const float* x, c
     const int32_t b = out_blk[i];
     if (b < 0) return;
     const uint32_t slot = out_did[i] % M.T;
-    float* g = M.arena_mir + (uint64_t)b * M.MPS + (uint64_t)(slot >> 5) * M.GF;
-    mirror_column(g, slot & 31u, x + (uint64_t)i * M.D, 1, M.cent + (uint64_t)asg[i] * M.D, M.D);
+    const uint64_t g = (uint64_t)b * M.gpb + (slot >> 5);
+    mirror_column(M.arena_mir + g * M.GF, M.arena_nrm + g * kNormFloats, slot & 31u,
+                  x + (uint64_t)i * M.D, 1, M.cent + (uint64_t)asg[i] * M.D, M.D, M.K);
 }
 
 __global__ void mirror_offline_kernel(MirrorView M, uint32_t n, const float* x,
@@ -55,8 +63,9 @@ __global__ void mirror_offline_kernel(MirrorView M, uint32_t n, const float* x,
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t s = dest[i];
-    mirror_column(M.off_mir + (s >> 5) * M.GF, (uint32_t)(s & 31u), x + (uint64_t)i * M.D, 1,
-                  M.cent + (uint64_t)asg[i] * M.D, M.D);
+    mirror_column(M.off_mir + (s >> 5) * M.GF, M.off_nrm + (s >> 5) * kNormFloats,
+                  (uint32_t)(s & 31u), x + (uint64_t)i * M.D, 1, M.cent + (uint64_t)asg[i] * M.D,
+                  M.D, M.K);
 }
 
 // warp per group, lane = slot: payload group rows are coalesced
@@ -66,33 +75,34 @@ __global__ void mirror_groups_kernel(MirrorView M, const float* payload, int are
     if (w >= n) return;
     const uint64_t gi = groups[w];
     const float* src;
-    float* dst;
+    float *dst, *nrm;
     if (arena) {
         const uint64_t blk = gi / M.gpb, j = gi - blk * M.gpb;
         src = payload + blk * PS + j * 32ull * M.D;
-        dst = M.arena_mir + blk * M.MPS + j * M.GF;
+        dst = M.arena_mir + gi * M.GF;
+        nrm = M.arena_nrm + gi * kNormFloats;
     } else {
         src = payload + gi * 32ull * M.D;
         dst = M.off_mir + gi * M.GF;
+        nrm = M.off_nrm + gi * kNormFloats;
     }
-    mirror_column(dst, lane, src + lane, 32, M.cent + (uint64_t)cl[w] * M.D, M.D);
+    mirror_column(dst, nrm, lane, src + lane, 32, M.cent + (uint64_t)cl[w] * M.D, M.D, M.K);
 }
 
 __global__ void mirror_slot_move_kernel(MirrorView M, const uint64_t* id_addr, uint32_t n,
                                         float* scr, int phase) {
-    const uint32_t R = 2 * M.D + 2;
+    // per slot: 2K plane rows + 2 norm entries
+    const uint32_t R = 2 * M.K + 2;
     const uint64_t total = (uint64_t)n * R;
     for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
          o += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t m = (uint32_t)(o / R), r = (uint32_t)(o - (uint64_t)m * R);
         uint32_t lane;
-        if (phase == 0) {
-            const float* g = mirror_slot(M, id_addr[m], lane);
-            scr[o] = g[(uint64_t)r * 32u + lane];
-        } else {
-            float* g = mirror_slot(M, id_addr[n + m], lane);
-            g[(uint64_t)r * 32u + lane] = scr[o];
-        }
+        float* nrm;
+        float* g = mirror_slot(M, id_addr[phase == 0 ? m : n + m], lane, nrm);
+        float* e = r < 2 * M.K ? g + (uint64_t)r * 32u + lane : nrm + (r - 2 * M.K) * 32u + lane;
+        if (phase == 0) scr[o] = *e;
+        else *e = scr[o];
     }
 }
 
@@ -127,7 +137,7 @@ cudaError_t launch_mirror_groups(const MirrorView& M, const float* payload, bool
 cudaError_t launch_mirror_slot_moves(const MirrorView& M, const uint64_t* id_addr, uint32_t n,
                                      float* scratch, cudaStream_t s) {
     if (!n || !M.off_mir) return cudaSuccess;
-    const uint64_t total = (uint64_t)n * (2 * M.D + 2);
+    const uint64_t total = (uint64_t)n * (2 * M.K + 2);
     const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148 * 16));
     for (int phase = 0; phase < 2; ++phase) {
         mirror_slot_move_kernel<<<g, 256, 0, s>>>(M, id_addr, n, scratch, phase);

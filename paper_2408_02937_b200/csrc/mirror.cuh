@@ -4,13 +4,13 @@
 // reference-layout payload (which stays the source of truth and of every exact
 // distance), the list-centred residual s = fl(x - c) pre-split for 3xTF32:
 // s_hi = TF32 truncation of s, s_lo = s - s_hi (exact in fp32), plus |s|^2 and
-// |s|.  Layout per 32-vector group (same group indexing as the payload, so
-// slot/block moves map one-to-one), rows of 32 floats (one per slot):
-//     rows [0, D)        s_hi, dim d
-//     row  D             |s|^2   (sequential fp32)
-//     rows [D+1, 2D+1)   s_lo, dim d
-//     row  2D+1          |s|
-// Two TMA boxes of {32, D+1} rows stage a group's B operands + norms.  The
+// |s|.  Same group indexing as the payload, so slot/block moves map one-to-one.
+// Planes, per 32-vector group, rows of 32 floats (one per slot), K = D rounded
+// up to 8 (rows D..K-1 stay zero: the MMA's K padding):
+//     rows [0, K)      s_hi, dim d
+//     rows [K, 2K)     s_lo, dim d
+// Norms, per group, a separate array of 64 floats: [|s|^2 (sequential fp32) x 32][|s| x 32].
+// One TMA box of {32, 2K} rows stages a group's two B operands.  The
 // mirror is written by the same data-lane operations that write the payload
 // (bulk load, insert, delete slot moves, rearrangement block moves), before
 // the list length that exposes the slots is release-published.
@@ -24,13 +24,17 @@ namespace bivf {
 struct MirrorView {
     float* off_mir;        // offline groups x GF
     float* arena_mir;      // num_blocks x MPS
+    float* off_nrm;        // offline groups x 64
+    float* arena_nrm;      // num_blocks x gpb x 64
     const float* cent;     // [C][D] row-major centroids
-    uint32_t D, T, gpb;
-    uint64_t GF;           // floats per group  = (2D+2)*32
+    uint32_t D, K, T, gpb; // K = D rounded up to 8
+    uint64_t GF;           // floats per group  = 2K*32
     uint64_t MPS;          // floats per block  = gpb*GF
 };
 
-inline uint64_t mirror_group_floats(uint32_t D) { return (2ull * D + 2) * 32ull; }
+inline uint32_t mirror_k(uint32_t D) { return (D + 7u) & ~7u; }
+inline uint64_t mirror_group_floats(uint32_t D) { return 2ull * mirror_k(D) * 32ull; }
+constexpr uint32_t kNormFloats = 64;  // per group
 
 // insert: vector i (row-major x[i*D..]) landed in block out_blk[i] (-1 = failed)
 // at list position out_did[i]; its list is asg[i].
@@ -47,7 +51,7 @@ cudaError_t launch_mirror_groups(const MirrorView& M, const float* payload, bool
                                  uint32_t n, cudaStream_t s);
 // delete compaction: the same moves as launch_slot_moves, on the mirror
 // (id_addr[2n] = sources then destinations; bit 63 = arena, value = the slot's
-// id index).  scratch: n * (2D+2) floats.
+// id index).  scratch: n * (2K+2) floats.
 cudaError_t launch_mirror_slot_moves(const MirrorView& M, const uint64_t* id_addr, uint32_t n,
                                      float* scratch, cudaStream_t s);
 

@@ -46,15 +46,16 @@ namespace {
 constexpr int kWG = 2;                     // math warpgroups
 constexpr int kTcThreads = 64 + 128 * kWG;  // warp0 TMA, warp1 MMA, warps 2.. math
 constexpr int kM = 128;                    // queries per tile (MMA M, TMEM lanes)
-constexpr int kNS = 4;                     // smem stages (one group each)
-constexpr int kNB = 8;                     // TMEM accumulators (32 columns each; even)
+constexpr int kGU = 2;                     // groups per unit (MMA N = 32 * kGU)
+constexpr int kNS = 4;                     // smem stages (one group each), kNS / kGU unit slots
+constexpr int kNB = 4;                     // TMEM accumulators (32 * kGU columns each; even)
+constexpr int kNU = kNS / kGU;             // unit slots in the stage ring
 constexpr int kMaxD = 128;
-// a stage = two 1024-aligned regions of (D+1) 128-byte rows: [s_hi | |s|^2], [s_lo | |s|]
-constexpr int kRegion = (((kMaxD + 1) * 128) + 1023) & ~1023;
-constexpr int kStage = 2 * kRegion;
+// a stage = one group's mirror planes: 2K rows of 128 bytes ([s_hi], [s_lo])
+constexpr int kStage = 2 * kMaxD * 128;
 // TMEM columns: A_hi [0,128), A_lo [128,256), accumulators [256, 256 + 32*kNB)
 constexpr uint32_t kColAlo = 128, kColAcc = 256, kTmemCols = 512;
-static_assert(kColAcc + 32 * kNB <= kTmemCols, "TMEM budget");
+static_assert(kColAcc + 32 * kGU * kNB <= kTmemCols, "TMEM budget");
 
 struct TcParams {
     DevLists L;
@@ -70,6 +71,8 @@ struct TcParams {
     const uint32_t* n_items_ptr;
     const uint32_t* plist;
     uint32_t* item_ctr;
+    const float* off_nrm;       // mirror norms (mirror.cuh), 64 floats per group
+    const float* arena_nrm;
     // per run outputs; run = ((pair * maxch + chunk) << 1) | warpgroup
     float* ub;          // [runs][k]
     uint32_t* ccount;   // [runs]   (kKC+1 = overflow)
@@ -145,6 +148,30 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
 __device__ __forceinline__ float tf32_trunc(float x) {
     return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
+// Warp-collective issue of one 3xTF32 K-step (A_hi*B_hi, A_hi*B_lo, A_lo*B_hi):
+// the whole (converged) warp executes it, elect.sync picks the issuing lane
+// inside the asm, so no per-MMA elect loop is generated around it.
+__device__ __forceinline__ void mma3_tf32_elect(uint32_t dcol, uint32_t ah, uint32_t al, uint64_t bh,
+                                                uint64_t bl, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "setp.eq.b32 t, 0, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, t;\n\t}" ::"r"(dcol),
+        "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -217,7 +244,7 @@ __device__ __forceinline__ TcItem tc_decode(const TcParams& p, uint32_t it) {
 __device__ __forceinline__ void group_row(const DevLists& L, uint32_t c, uint32_t off,
                                           uint32_t j, bool& arena, int& row) {
     const uint32_t og = (off + 31u) >> 5;
-    const uint32_t R = 2u * L.D + 2u;
+    const uint32_t R = 2u * ((L.D + 7u) & ~7u);
     if (j < og) {
         arena = false;
         row = (int)((L.off_start[c] / 32u + j) * R);
@@ -230,36 +257,10 @@ __device__ __forceinline__ void group_row(const DevLists& L, uint32_t c, uint32_
     }
 }
 
-__device__ __forceinline__ float4 lds4(uint32_t addr) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "r"(addr));
-    return v;
-}
-// Row r of a region written by TMA with SWIZZLE_128B_ATOM_32B: slot n lives in
-// 32-byte chunk (n / 8) ^ (r % 4) of the row.
-__device__ __forceinline__ void load_row32(uint32_t region, uint32_t r, float (&v)[32]) {
-    const uint32_t base = region + r * 128u;
-#pragma unroll
-    for (uint32_t j = 0; j < 4; ++j) {
-        const uint32_t a = base + ((j ^ (r & 3u)) << 5);
-        const float4 x = lds4(a), y = lds4(a + 16);
-        v[8 * j + 0] = x.x;
-        v[8 * j + 1] = x.y;
-        v[8 * j + 2] = x.z;
-        v[8 * j + 3] = x.w;
-        v[8 * j + 4] = y.x;
-        v[8 * j + 5] = y.y;
-        v[8 * j + 6] = y.z;
-        v[8 * j + 7] = y.w;
-    }
-}
-
 // bounds + filtering of one group for this thread's query (see tc_unit)
 template <int KT>
 __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, uint32_t j,
-                                          uint32_t sbase, bool active, float nq, float sqq,
+                                          const float* wn, bool active, float nq, float sqq,
                                           const float (&dot)[32], const float (&ns)[32],
                                           const float (&ss)[32], float (&ubl)[KT], float& ubk,
                                           uint32_t& ncand, bool& overflow, float* clb,
@@ -295,14 +296,10 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
 #pragma unroll
     for (uint32_t n = 0; n < 32; ++n) scr[n * kM] = dot[n];
     const uint32_t jl = j << 5;
-    const uint32_t nrow0 = sbase + p.D * 128u, nrow1 = nrow0 + kRegion, rsw = p.D & 3u;
     while (need) {
         const uint32_t n = __ffs(need) - 1;
         need &= need - 1;
-        const uint32_t so = (((n >> 3) ^ rsw) << 5) + (n & 7u) * 4u;
-        float nx, sx;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nx) : "r"(nrow0 + so));
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(sx) : "r"(nrow1 + so));
+        const float nx = wn[n], sx = wn[32 + n];
         const float t = nq + nx;
         const float a = fmaf(-2.f, scr[n * kM], t);
         const float e = fmaf(ce, sx, fmaf(kEpsRel, fabsf(a), fmaf(kEpsRel, t, 1e-30f)));
@@ -350,33 +347,62 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
 // smallest upper bounds, and the candidates whose lower bound can still
 // enter the top-k (written straight to the run's global buffer; rare).
 template <int KT>
-__device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint32_t u, uint32_t j,
-                                        uint64_t* full, uint64_t* empty, uint64_t* acc_full,
-                                        uint64_t* acc_empty, uint32_t stages, uint32_t tmem_base,
+__device__ __forceinline__ void tc_group(const TcParams& p, const TcItem& d, uint32_t j,
+                                         uint32_t acol, uint32_t tmem_base, uint32_t taddr_lane,
+                                         int lane, bool active, float nq, float sqq, float (&ubl)[KT],
+                                         float& ubk, uint32_t& ncand, bool& overflow, float* clb,
+                                         uint32_t* cloc, float* scr, float* wn) {
+    // the group's norms (64 floats, global, broadcast) -> this warp's smem slab
+    const float* gn;
+    {
+        const uint32_t og = (d.off + 31u) >> 5;
+        uint64_t g;
+        if (j < og) {
+            g = p.L.off_start[d.c] / 32u + j;
+            gn = p.off_nrm;
+        } else {
+            const uint32_t jj = j - og, mid = jj / p.L.gpb, gi = jj - mid * p.L.gpb;
+            g = (uint64_t)p.L.table[(uint64_t)d.c * p.L.MLB + mid] * p.L.gpb + gi;
+            gn = p.arena_nrm;
+        }
+        gn += g * kNormFloats;
+    }
+    if (lane < 16) reinterpret_cast<float4*>(wn)[lane] = __ldg(reinterpret_cast<const float4*>(gn) + lane);
+    float dot[32];
+    tmem_ld32(tmem_base + taddr_lane + acol, dot);
+    __syncwarp();
+    float ns[32], ss[32];
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+        const float4 a = reinterpret_cast<const float4*>(wn)[i / 4];
+        const float4 c = reinterpret_cast<const float4*>(wn)[8 + i / 4];
+        ns[i] = a.x, ns[i + 1] = a.y, ns[i + 2] = a.z, ns[i + 3] = a.w;
+        ss[i] = c.x, ss[i + 1] = c.y, ss[i + 2] = c.z, ss[i + 3] = c.w;
+    }
+    tc_filter<KT>(p, d, j, wn, active, nq, sqq, dot, ns, ss, ubl, ubk, ncand, overflow, clb, cloc,
+                  scr);
+    __syncwarp();  // wn is rewritten by this warp's next group
+}
+
+// One unit (kGU consecutive groups j0.. of the item, accumulator u % kNB).
+template <int KT>
+__device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint32_t u, uint32_t j0,
+                                        uint64_t* acc_full, uint64_t* acc_empty, uint32_t tmem_base,
                                         uint32_t taddr_lane, int lane, bool active, float nq,
                                         float sqq, float (&ubl)[KT], float& ubk, uint32_t& ncand,
                                         bool& overflow, float* clb, uint32_t* cloc,
-                                        float* scr) {
-    const uint32_t b = u % kNB, st = u % kNS;
+                                        float* scr, float* wn) {
+    const uint32_t b = u % kNB;
     mbar_wait(&acc_full[b], (u / kNB) & 1);
     __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread spin
     tc_fence_after();
-    float dot[32];
-    tmem_ld32(tmem_base + taddr_lane + kColAcc + b * 32, dot);
+    const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
+    for (uint32_t h = 0; h < ng; ++h)
+        tc_group<KT>(p, d, j0 + h, kColAcc + b * 32 * kGU + 32 * h, tmem_base, taddr_lane, lane,
+                     active, nq, sqq, ubl, ubk, ncand, overflow, clb, cloc, scr, wn);
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&acc_empty[b]);
-    // the group's norms (row D of both regions); full[st] has completed this
-    // phase already (its MMA did), the wait makes the TMA writes visible here
-    mbar_wait(&full[st], (u / kNS) & 1);
-    float ns[32], ss[32];
-    const uint32_t sbase = stages + st * (uint32_t)kStage;
-    load_row32(sbase, p.D, ns);
-    load_row32(sbase + kRegion, p.D, ss);
-    tc_filter<KT>(p, d, j, sbase, active, nq, sqq, dot, ns, ss, ubl, ubk, ncand, overflow, clb,
-                  cloc, scr);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);  // norms read: the stage may be refilled
 }
 
 template <int KT>
@@ -391,10 +417,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     float* scratch = reinterpret_cast<float*>(sB + kNS * kStage);  // [kWG][32][kM] pass-2 dots
     float* cand_lb = scratch + kWG * 32 * kM;                        // [kWG][kKC][kM]
     uint32_t* cand_loc = reinterpret_cast<uint32_t*>(cand_lb + kWG * kKC * kM);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(cand_loc + kWG * kKC * kM);
-    uint64_t* full = bars;                 // kNS
-    uint64_t* empty = full + kNS;          // kNS
-    uint64_t* acc_full = empty + kNS;      // kNB
+    float* wnorm = reinterpret_cast<float*>(cand_loc + kWG * kKC * kM);  // [math warp][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wnorm + 4 * kWG * kNormFloats);
+    uint64_t* full = bars;                 // kNU
+    uint64_t* empty = full + kNU;          // kNU
+    uint64_t* acc_full = empty + kNU;      // kNB
     uint64_t* acc_empty = acc_full + kNB;  // kNB
     uint64_t* a_full = acc_empty + kNB;    // 1
     uint64_t* a_free = a_full + 1;         // 1
@@ -406,9 +433,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t D = p.D;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kNS; ++s) {
+        for (int s = 0; s < kNU; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1 + 4);  // MMA commit + the owning warpgroup's 4 warps
+            mbar_init(&empty[s], 1);  // MMA commit
         }
         for (int b = 0; b < kNB; ++b) {
             mbar_init(&acc_full[b], 1);
@@ -422,11 +449,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         fence_mbar_init();
     }
-    // zero the stages once: rows past D+1 (K padding up to Dk) are never
-    // written by TMA and must read as finite zeros
-    for (uint32_t i = threadIdx.x; i < kNS * kStage / 16; i += blockDim.x)
-        reinterpret_cast<float4*>(sB)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    fence_proxy_async();
     if (warp == 1) {  // TMEM: A hi/lo + kNB accumulators
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
@@ -454,23 +476,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 mbar_arrive(&it_full[rs]);
                 if (v < 0) break;
                 const TcItem d = tc_decode(p, it);
-                for (uint32_t j = d.g0; j < d.g1; ++j, ++unit) {
-                    const uint32_t st = unit % kNS;
-                    mbar_wait(&empty[st], ((unit / kNS) & 1) ^ 1);
-                    bool ar;
-                    int row;
-                    group_row(p.L, d.c, d.off, j, ar, row);
-                    mbar_arrive_expect_tx(&full[st], 2u * (D + 1u) * 128u);
-                    const CUtensorMap* map = ar ? &map_arena : &map_off;
-                    tma_load_2d(sB + st * kStage, map, 0, row, &full[st]);
-                    tma_load_2d(sB + st * kStage + kRegion, map, 0, row + (int)D + 1, &full[st]);
+                for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
+                    const uint32_t us = unit % kNU;
+                    mbar_wait(&empty[us], ((unit / kNU) & 1) ^ 1);
+                    const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
+                    mbar_arrive_expect_tx(&full[us], ng * 2u * p.Dk * 128u);
+                    for (uint32_t h = 0; h < ng; ++h) {
+                        bool ar;
+                        int row;
+                        group_row(p.L, d.c, d.off, j0 + h, ar, row);
+                        tma_load_2d(sB + (us * kGU + h) * kStage, ar ? &map_arena : &map_off, 0, row,
+                                    &full[us]);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
+        // N = 32*kGU: the unit's groups sit in consecutive stages, kStage apart (LBO)
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) |
-                               ((32u >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
+                               (((32u * kGU) >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
         uint32_t unit = 0, ne = 0;
         for (uint32_t seq = 0;; ++seq) {
             const uint32_t rs = seq & 1;
@@ -483,30 +508,29 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (d.g1 <= d.g0) continue;
             mbar_wait(a_full, ne & 1);
             ++ne;
-            for (uint32_t j = d.g0; j < d.g1; ++j, ++unit) {
-                const uint32_t st = unit % kNS, b = unit % kNB;
-                mbar_wait(&full[st], (unit / kNS) & 1);
+            for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
+                const uint32_t us = unit % kNU, b = unit % kNB;
+                mbar_wait(&full[us], (unit / kNU) & 1);
                 mbar_wait(&acc_empty[b], ((unit / kNB) & 1) ^ 1);
                 __syncwarp();
                 tc_fence_after();
-                if (lane == 0) {
-                    // 3xTF32: A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (A from TMEM, B from smem)
-                    const uint32_t bh0 = stages + st * (uint32_t)kStage, bl0 = bh0 + kRegion;
-                    const uint32_t dcol = tmem_base + kColAcc + b * 32;
-                    for (uint32_t ks = 0; ks < p.Dk / 8; ++ks) {
-                        const uint64_t bh = umma_desc(bh0 + ks * 1024, 16384, 512, 1);
-                        const uint64_t bl = umma_desc(bl0 + ks * 1024, 16384, 512, 1);
-                        const uint32_t ah = tmem_base + ks * 8, al = tmem_base + kColAlo + ks * 8;
-                        mma_tf32_ts(dcol, ah, bh, idesc, ks > 0 ? 1u : 0u);
-                        mma_tf32_ts(dcol, ah, bl, idesc, 1u);
-                        mma_tf32_ts(dcol, al, bh, idesc, 1u);
-                    }
-                    mma_commit(&acc_full[b]);
-                    mma_commit(&empty[st]);
+                {
+                    // 3xTF32: A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (A from TMEM, B from smem);
+                    // descriptors advance 1024 B (64 in the >>4 address field) per K-step
+                    const uint32_t bh0 = stages + us * kGU * (uint32_t)kStage, bl0 = bh0 + p.Dk * 128u;
+                    const uint32_t dcol = tmem_base + kColAcc + b * 32 * kGU;
+                    const uint64_t bh = umma_desc(bh0, kStage, 512, 1);
+                    const uint64_t bl = umma_desc(bl0, kStage, 512, 1);
+                    const uint32_t nks = p.Dk / 8;
+                    for (uint32_t ks = 0; ks < nks; ++ks)
+                        mma3_tf32_elect(dcol, tmem_base + ks * 8, tmem_base + kColAlo + ks * 8,
+                                        bh + ks * 64ull, bl + ks * 64ull, idesc, ks);
+                    mma_commit_elect(&acc_full[b]);
+                    mma_commit_elect(&empty[us]);
                 }
                 __syncwarp();
             }
-            if (lane == 0) mma_commit(a_free);  // A may be rewritten once these MMAs retire
+            mma_commit_elect(a_free);  // A may be rewritten once these MMAs retire
             __syncwarp();
         }
     } else {
@@ -573,11 +597,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 named_bar(1 + wg, 128);
                 if (wt == 0) mbar_arrive(a_full);
                 const float sqq = sqrtf(nq);
-                for (uint32_t j = d.g0; j < d.g1; ++j, ++unit) {
+                for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
                     if ((unit & 1u) != (uint32_t)wg) continue;
-                    tc_unit<KT>(p, d, unit, j, full, empty, acc_full, acc_empty, stages, tmem_base,
-                                taddr_lane, lane, active, nq, sqq, ubl, ubk, ncand, overflow, clb,
-                                cloc, scratch + wg * 32 * kM + m);
+                    tc_unit<KT>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
+                                active, nq, sqq, ubl, ubk, ncand, overflow, clb, cloc,
+                                scratch + wg * 32 * kM + m, wnorm + (warp - 2) * kNormFloats);
                 }
             }
             // run output: k upper bounds + surviving candidates (compacted in place)
@@ -749,7 +773,7 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
 
 size_t tc_smem_bytes() {
     return 1024 + kNS * kStage + kWG * 32 * kM * 4 + kWG * kKC * kM * 8 +
-           (2 * kNS + 2 * kNB + 6) * 8 + 16 + 16;
+           4 * kWG * kNormFloats * 4 + (2 * kNU + 2 * kNB + 6) * 8 + 16 + 16;
 }
 
 }  // namespace
@@ -777,9 +801,10 @@ bool tc_supported(uint32_t D, uint32_t k, int metric) {
 cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUtensorMap* out) {
     auto enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
-    cuuint64_t dims[2] = {32, std::max<cuuint64_t>(groups * (2ull * D + 2), 1)};
+    const uint32_t K = mirror_k(D);
+    cuuint64_t dims[2] = {32, std::max<cuuint64_t>(groups * 2ull * K, 1)};
     cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {32, D + 1};
+    cuuint32_t box[2] = {32, 2 * K};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -791,7 +816,8 @@ cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUte
 cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,
                                  const float* queries, const float* centroids,
                                  const SearchShape& sh, const CUtensorMap& map_off,
-                                 const CUtensorMap& map_arena, const TcBufs& T, float* out_d,
+                                 const CUtensorMap& map_arena, const float* off_nrm,
+                                 const float* arena_nrm, const TcBufs& T, float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
     if (sh.nq == 0) return cudaSuccess;
@@ -818,6 +844,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     p.n_items_ptr = B.n_items;
     p.plist = B.plist;
     p.item_ctr = B.item_ctr;
+    p.off_nrm = off_nrm;
+    p.arena_nrm = arena_nrm;
     p.ub = T.ub;
     p.ccount = T.ccount;
     p.clb = T.clb;

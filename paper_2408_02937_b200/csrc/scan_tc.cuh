@@ -24,13 +24,14 @@ struct TcBufs {
 bool tc_supported(uint32_t D, uint32_t k, int metric);
 
 // 2-D TMA map over a scan mirror region (mirror.cuh: `groups` groups of
-// 2D+2 rows of 32 floats), box = {32, D+1}, SWIZZLE_128B_ATOM_32B.
+// 2K rows of 32 floats), box = {32, 2K}, SWIZZLE_128B_ATOM_32B.
 cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUtensorMap* out);
 
 cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,
                                  const float* queries, const float* centroids,
                                  const SearchShape& sh, const CUtensorMap& map_off,
-                                 const CUtensorMap& map_arena, const TcBufs& T, float* out_d,
+                                 const CUtensorMap& map_arena, const float* off_nrm,
+                                 const float* arena_nrm, const TcBufs& T, float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0 = nullptr,
                                  cudaEvent_t ev1 = nullptr);
