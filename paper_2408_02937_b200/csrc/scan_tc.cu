@@ -352,25 +352,9 @@ __device__ __forceinline__ void tc_group(const TcParams& p, const TcItem& d, uin
                                          int lane, bool active, float nq, float sqq, float (&ubl)[KT],
                                          float& ubk, uint32_t& ncand, bool& overflow, float* clb,
                                          uint32_t* cloc, float* scr, float* wn) {
-    // the group's norms (64 floats, global, broadcast) -> this warp's smem slab
-    const float* gn;
-    {
-        const uint32_t og = (d.off + 31u) >> 5;
-        uint64_t g;
-        if (j < og) {
-            g = p.L.off_start[d.c] / 32u + j;
-            gn = p.off_nrm;
-        } else {
-            const uint32_t jj = j - og, mid = jj / p.L.gpb, gi = jj - mid * p.L.gpb;
-            g = (uint64_t)p.L.table[(uint64_t)d.c * p.L.MLB + mid] * p.L.gpb + gi;
-            gn = p.arena_nrm;
-        }
-        gn += g * kNormFloats;
-    }
-    if (lane < 16) reinterpret_cast<float4*>(wn)[lane] = __ldg(reinterpret_cast<const float4*>(gn) + lane);
+    // wn: the group's norms in the unit's norm slot (staged by the producer)
     float dot[32];
     tmem_ld32(tmem_base + taddr_lane + acol, dot);
-    __syncwarp();
     float ns[32], ss[32];
 #pragma unroll
     for (int i = 0; i < 32; i += 4) {
@@ -381,7 +365,6 @@ __device__ __forceinline__ void tc_group(const TcParams& p, const TcItem& d, uin
     }
     tc_filter<KT>(p, d, j, wn, active, nq, sqq, dot, ns, ss, ubl, ubk, ncand, overflow, clb, cloc,
                   scr);
-    __syncwarp();  // wn is rewritten by this warp's next group
 }
 
 // One unit (kGU consecutive groups j0.. of the item, accumulator u % kNB).
@@ -391,15 +374,17 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                                         uint32_t taddr_lane, int lane, bool active, float nq,
                                         float sqq, float (&ubl)[KT], float& ubk, uint32_t& ncand,
                                         bool& overflow, float* clb, uint32_t* cloc,
-                                        float* scr, float* wn) {
+                                        float* scr, float* nslots, uint64_t* nfull) {
     const uint32_t b = u % kNB;
+    mbar_wait(&nfull[b], (u / kNB) & 1);
     mbar_wait(&acc_full[b], (u / kNB) & 1);
     __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread spin
     tc_fence_after();
     const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
     for (uint32_t h = 0; h < ng; ++h)
         tc_group<KT>(p, d, j0 + h, kColAcc + b * 32 * kGU + 32 * h, tmem_base, taddr_lane, lane,
-                     active, nq, sqq, ubl, ubk, ncand, overflow, clb, cloc, scr, wn);
+                     active, nq, sqq, ubl, ubk, ncand, overflow, clb, cloc, scr,
+                     nslots + (b * kGU + h) * kNormFloats);
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&acc_empty[b]);
@@ -417,8 +402,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     float* scratch = reinterpret_cast<float*>(sB + kNS * kStage);  // [kWG][32][kM] pass-2 dots
     float* cand_lb = scratch + kWG * 32 * kM;                        // [kWG][kKC][kM]
     uint32_t* cand_loc = reinterpret_cast<uint32_t*>(cand_lb + kWG * kKC * kM);
-    float* wnorm = reinterpret_cast<float*>(cand_loc + kWG * kKC * kM);  // [math warp][64]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(wnorm + 4 * kWG * kNormFloats);
+    float* nslots = reinterpret_cast<float*>(cand_loc + kWG * kKC * kM);  // [kNB][kGU][64] norms
+    uint64_t* bars = reinterpret_cast<uint64_t*>(nslots + kNB * kGU * kNormFloats);
     uint64_t* full = bars;                 // kNU
     uint64_t* empty = full + kNU;          // kNU
     uint64_t* acc_full = empty + kNU;      // kNB
@@ -427,7 +412,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t* a_free = a_full + 1;         // 1
     uint64_t* it_full = a_free + 1;        // 2
     uint64_t* it_empty = it_full + 2;      // 2
-    int* ring = reinterpret_cast<int*>(it_empty + 2);
+    uint64_t* nfull = it_empty + 2;        // kNB
+    int* ring = reinterpret_cast<int*>(nfull + kNB);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -440,6 +426,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int b = 0; b < kNB; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], 4);
+            mbar_init(&nfull[b], 1);
         }
         mbar_init(a_full, kWG);
         mbar_init(a_free, 1);
@@ -481,13 +468,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     mbar_wait(&empty[us], ((unit / kNU) & 1) ^ 1);
                     const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
                     mbar_arrive_expect_tx(&full[us], ng * 2u * p.Dk * 128u);
+                    const uint32_t b = unit % kNB;
+                    uint64_t ng_idx[kGU];
+                    bool ng_ar[kGU];
                     for (uint32_t h = 0; h < ng; ++h) {
                         bool ar;
                         int row;
                         group_row(p.L, d.c, d.off, j0 + h, ar, row);
                         tma_load_2d(sB + (us * kGU + h) * kStage, ar ? &map_arena : &map_off, 0, row,
                                     &full[us]);
+                        ng_idx[h] = (uint64_t)row / (2u * p.Dk);
+                        ng_ar[h] = ar;
                     }
+                    // the unit's group norms -> norm slot b, once unit - kNB released it
+                    mbar_wait(&acc_empty[b], ((unit / kNB) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&nfull[b], ng * kNormFloats * 4u);
+                    for (uint32_t h = 0; h < ng; ++h)
+                        bulk_g2s(nslots + (b * kGU + h) * kNormFloats,
+                                 (ng_ar[h] ? p.arena_nrm : p.off_nrm) + ng_idx[h] * kNormFloats,
+                                 kNormFloats * 4u, &nfull[b]);
                 }
             }
         }
@@ -601,7 +600,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     if ((unit & 1u) != (uint32_t)wg) continue;
                     tc_unit<KT>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
                                 active, nq, sqq, ubl, ubk, ncand, overflow, clb, cloc,
-                                scratch + wg * 32 * kM + m, wnorm + (warp - 2) * kNormFloats);
+                                scratch + wg * 32 * kM + m, nslots, nfull);
                 }
             }
             // run output: k upper bounds + surviving candidates (compacted in place)
@@ -773,7 +772,7 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
 
 size_t tc_smem_bytes() {
     return 1024 + kNS * kStage + kWG * 32 * kM * 4 + kWG * kKC * kM * 8 +
-           4 * kWG * kNormFloats * 4 + (2 * kNU + 2 * kNB + 6) * 8 + 16 + 16;
+           kNB * kGU * kNormFloats * 4 + (2 * kNU + 3 * kNB + 6) * 8 + 16 + 16;
 }
 
 }  // namespace
