@@ -27,7 +27,7 @@ __device__ __forceinline__ void mirror_column(float* g, float* nrm, uint32_t lan
         n2 = __fadd_rn(n2, __fmul_rn(s, s));
     }
     nrm[lane] = n2;
-    nrm[32 + lane] = sqrtf(n2);
+    nrm[32 + lane] = n2 * kVScale;
 }
 
 // group base (mirror planes) and norm block of a slot address

@@ -9,7 +9,8 @@
 // up to 8 (rows D..K-1 stay zero: the MMA's K padding):
 //     rows [0, K)      s_hi, dim d
 //     rows [K, 2K)     s_lo, dim d
-// Norms, per group, a separate array of 64 floats: [|s|^2 (sequential fp32) x 32][|s| x 32].
+// Norms, per group, a separate array of 64 floats: [|s|^2 (sequential fp32) x 32]
+// [kVScale * |s|^2 x 32] (the per-slot term of the scan's pass-1 threshold, scan_tc.cu).
 // One TMA box of {32, 2K} rows stages a group's two B operands.  The
 // mirror is written by the same data-lane operations that write the payload
 // (bulk load, insert, delete slot moves, rearrangement block moves), before
@@ -31,6 +32,15 @@ struct MirrorView {
     uint64_t GF;           // floats per group  = 2K*32
     uint64_t MPS;          // floats per block  = gpb*GF
 };
+
+// Error-bound constants of the tensor-core filter (D <= 128):
+//   |a - e| <= kEpsCross*|r||s| + kEpsRel*(|r|^2+|s|^2) + kEpsRel*|a|  (2x margin), and with
+//   |r||s| <= (|r|^2+|s|^2)/2:  eps' = kEpsT*(nq+ns) + kEpsRel*|a|,  kEpsT = kEpsRel + kEpsCross/2.
+// For a >= 0 the lower bound a - eps' <= ubk  <=>  dot >= kVScale*(nq+ns) - ubk/(2(1-kEpsRel)).
+constexpr float kEpsCross = 1.0f / 16384.0f;  // 2 * 2^-15 >= 2 * 2 * 2^-16 on |r||s|
+constexpr float kEpsRel = 1.0f / 32768.0f;    // 2^-15 on (nq+ns) and on |a|
+constexpr float kEpsT = kEpsRel + 0.5f * kEpsCross;
+constexpr float kVScale = (1.0f - kEpsRel - kEpsT) / (2.0f * (1.0f - kEpsRel));
 
 inline uint32_t mirror_k(uint32_t D) { return (D + 7u) & ~7u; }
 inline uint64_t mirror_group_floats(uint32_t D) { return 2ull * mirror_k(D) * 32ull; }

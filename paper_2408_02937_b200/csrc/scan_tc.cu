@@ -16,7 +16,7 @@
 //   2 math warpgroups (alternate groups): build A once per item, then per
 //                   group tcgen05.ld the 32 dot products of their query, form
 //                   a = |r|^2 + |s|^2 - 2 r.s and a PROVEN bound eps (TF32 +
-//                   fp32 rounding, see err_bound), keep the k smallest upper
+//                   fp32 rounding, mirror.cuh), keep the k smallest upper
 //                   bounds (a+eps) and every vector whose lower bound (a-eps)
 //                   can still enter the top-k (one run per warpgroup).
 // A refine kernel (one warp per query) takes the k-th smallest upper bound
@@ -204,13 +204,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // 3*D/8 MMA steps adds <= 48*2^-24 sum|r_d s_d| (D=128): |P - r.s| <= 2^-16 |r||s|
 // (measured worst 2^-20.3 on B200, tools/tc_probe_ts.cu).  Norms: sequential fp32,
 // |nq - |r|^2| <= (D+1) 2^-24 |r|^2; exact value: |e - |q-x|^2| <= (D+2) 2^-24 |q-x|^2;
-// centring: | |r-s|^2 - |q-x|^2 | <= 2^-22 (|r|^2 + |s|^2).  Constants carry >= 2x margin.
-constexpr float kEpsCross = 1.0f / 16384.0f;  // 2 * 2^-15 >= 2 * 2 * 2^-16 on |r||s|
-constexpr float kEpsRel = 1.0f / 32768.0f;    // 2^-15 on (nq+ns) and on |a|
-__device__ __forceinline__ float err_bound(float nq, float ns, float a) {
-    return kEpsCross * sqrtf(nq * ns) + kEpsRel * (nq + ns) + kEpsRel * fabsf(a) + 1e-30f;
-}
-
+// centring: | |r-s|^2 - |q-x|^2 | <= 2^-22 (|r|^2 + |s|^2).  Constants (mirror.cuh)
+// carry >= 2x margin; |r||s| is bounded by (|r|^2+|s|^2)/2 so every term is a
+// function of (nq + ns) and |a|:  eps' = kEpsT*(nq+ns) + kEpsRel*|a| + 1e-30.
 struct TcItem {
     uint32_t c, npairs, g0, g1, chunk, off, len;
     const uint32_t* pairs;
@@ -260,9 +256,8 @@ __device__ __forceinline__ void group_row(const DevLists& L, uint32_t c, uint32_
 // bounds + filtering of one group for this thread's query (see tc_unit)
 template <int KT>
 __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, uint32_t j,
-                                          const float* wn, bool active, float nq, float sqq,
-                                          const float (&dot)[32], const float (&ns)[32],
-                                          const float (&ss)[32], float (&ubl)[KT], float& ubk,
+                                          const float* wn, bool active, float nq,
+                                          const float (&dot)[32], float (&ubl)[KT], float& ubk,
                                           uint32_t& ncand, bool& overflow, float* clb,
                                           uint32_t* cloc, float* scr) {
     if (!active) return;
@@ -278,16 +273,18 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
         }
     }
     const uint32_t vmask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
-    // pass 1 (registers only): which slots could still enter the top-k
+    // pass 1: slot n can still enter the top-k only if its lower bound a - eps' <= ubk,
+    // i.e. dot >= V[n] + W (V = kVScale*ns from the mirror norms; a < 0 passes too,
+    // since ubk > 0).  Three instructions per slot.
+    const float W = fmaf(kVScale, nq, -ubk * (0.5f / (1.0f - kEpsRel)));
     uint32_t need = 0;
-    const float ce = kEpsCross * sqq;
 #pragma unroll
-    for (uint32_t n = 0; n < 32; ++n) {
-        const float t = nq + ns[n];
-        const float a = fmaf(-2.f, dot[n], t);
-        // err_bound(nq, ns, a) with sqrt(nq*ns) = sqrt(nq)*sqrt(ns) precomputed
-        const float e = fmaf(ce, ss[n], fmaf(kEpsRel, fabsf(a), fmaf(kEpsRel, t, 1e-30f)));
-        need |= (a - e <= ubk) ? (1u << n) : 0u;
+    for (uint32_t n = 0; n < 32; n += 4) {
+        const float4 v = reinterpret_cast<const float4*>(wn + 32)[n / 4];
+        need |= (dot[n] >= v.x + W) ? (1u << n) : 0u;
+        need |= (dot[n + 1] >= v.y + W) ? (2u << n) : 0u;
+        need |= (dot[n + 2] >= v.z + W) ? (4u << n) : 0u;
+        need |= (dot[n + 3] >= v.w + W) ? (8u << n) : 0u;
     }
     need &= vmask;
     if (!need) return;
@@ -299,10 +296,9 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
     while (need) {
         const uint32_t n = __ffs(need) - 1;
         need &= need - 1;
-        const float nx = wn[n], sx = wn[32 + n];
-        const float t = nq + nx;
+        const float t = nq + wn[n];
         const float a = fmaf(-2.f, scr[n * kM], t);
-        const float e = fmaf(ce, sx, fmaf(kEpsRel, fabsf(a), fmaf(kEpsRel, t, 1e-30f)));
+        const float e = fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, t, 1e-30f));
         const float h = a + e, l = a - e;
         if (h < ubk) {  // keep the k smallest upper bounds, sorted
             // ubl: ascending; entries [0, KT-k) are -inf sentinels, [KT-k, KT) the
@@ -342,29 +338,16 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
     }
 }
 
-// One group (unit u, group j of the item) for this thread's query: 32 dot
-// products from TMEM + the group's norms from the stage -> bounds, the k
-// smallest upper bounds, and the candidates whose lower bound can still
-// enter the top-k (written straight to the run's global buffer; rare).
 template <int KT>
 __device__ __forceinline__ void tc_group(const TcParams& p, const TcItem& d, uint32_t j,
                                          uint32_t acol, uint32_t tmem_base, uint32_t taddr_lane,
-                                         int lane, bool active, float nq, float sqq, float (&ubl)[KT],
-                                         float& ubk, uint32_t& ncand, bool& overflow, float* clb,
-                                         uint32_t* cloc, float* scr, float* wn) {
+                                         bool active, float nq, float (&ubl)[KT], float& ubk,
+                                         uint32_t& ncand, bool& overflow, float* clb,
+                                         uint32_t* cloc, float* scr, const float* wn) {
     // wn: the group's norms in the unit's norm slot (staged by the producer)
     float dot[32];
     tmem_ld32(tmem_base + taddr_lane + acol, dot);
-    float ns[32], ss[32];
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-        const float4 a = reinterpret_cast<const float4*>(wn)[i / 4];
-        const float4 c = reinterpret_cast<const float4*>(wn)[8 + i / 4];
-        ns[i] = a.x, ns[i + 1] = a.y, ns[i + 2] = a.z, ns[i + 3] = a.w;
-        ss[i] = c.x, ss[i + 1] = c.y, ss[i + 2] = c.z, ss[i + 3] = c.w;
-    }
-    tc_filter<KT>(p, d, j, wn, active, nq, sqq, dot, ns, ss, ubl, ubk, ncand, overflow, clb, cloc,
-                  scr);
+    tc_filter<KT>(p, d, j, wn, active, nq, dot, ubl, ubk, ncand, overflow, clb, cloc, scr);
 }
 
 // One unit (kGU consecutive groups j0.. of the item, accumulator u % kNB).
@@ -372,7 +355,7 @@ template <int KT>
 __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint32_t u, uint32_t j0,
                                         uint64_t* acc_full, uint64_t* acc_empty, uint32_t tmem_base,
                                         uint32_t taddr_lane, int lane, bool active, float nq,
-                                        float sqq, float (&ubl)[KT], float& ubk, uint32_t& ncand,
+                                        float (&ubl)[KT], float& ubk, uint32_t& ncand,
                                         bool& overflow, float* clb, uint32_t* cloc,
                                         float* scr, float* nslots, uint64_t* nfull) {
     const uint32_t b = u % kNB;
@@ -382,8 +365,8 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
     tc_fence_after();
     const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
     for (uint32_t h = 0; h < ng; ++h)
-        tc_group<KT>(p, d, j0 + h, kColAcc + b * 32 * kGU + 32 * h, tmem_base, taddr_lane, lane,
-                     active, nq, sqq, ubl, ubk, ncand, overflow, clb, cloc, scr,
+        tc_group<KT>(p, d, j0 + h, kColAcc + b * 32 * kGU + 32 * h, tmem_base, taddr_lane, active,
+                     nq, ubl, ubk, ncand, overflow, clb, cloc, scr,
                      nslots + (b * kGU + h) * kNormFloats);
     tc_fence_before();
     __syncwarp();
@@ -595,11 +578,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 tc_fence_before();
                 named_bar(1 + wg, 128);
                 if (wt == 0) mbar_arrive(a_full);
-                const float sqq = sqrtf(nq);
                 for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
                     if ((unit & 1u) != (uint32_t)wg) continue;
                     tc_unit<KT>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
-                                active, nq, sqq, ubl, ubk, ncand, overflow, clb, cloc,
+                                active, nq, ubl, ubk, ncand, overflow, clb, cloc,
                                 scratch + wg * 32 * kM + m, nslots, nfull);
                 }
             }
