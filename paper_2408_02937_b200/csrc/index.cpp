@@ -314,6 +314,114 @@ void GpuIndex::rebuild_mirror() {
     }
 }
 
+// The coarse quantizer as a tensor-core search: ONE list holding every
+// centroid (offline segment = the interleaved centroids, ids = cluster ids),
+// centred at the centroid mean.  TC filter + exact refine returns exactly the
+// CUDA-core quantizer's (dist, cluster) top-P (ivf_index.cpp:271-276).
+void GpuIndex::build_quantizer_mirror(const float* c) {
+    q_tc_ok_ = false;
+    if (!mir_on_ || C_ < 64) return;
+    const uint32_t ngq = ceil_div(C_, 32);
+    std::vector<float> mu(D_, 0.f);
+    for (uint32_t k = 0; k < C_; ++k)
+        for (uint32_t d = 0; d < D_; ++d) mu[d] += c[(size_t)k * D_ + d];
+    for (uint32_t d = 0; d < D_; ++d) mu[d] /= (float)C_;
+    d_q_mu_.alloc((size_t)D_ * 4);
+    BIVF_CUDA(h2d(d_q_mu_.p, mu.data(), (size_t)D_ * 4));
+    d_q_mir_.alloc((size_t)ngq * GF_ * 4);
+    BIVF_CUDA(dset(d_q_mir_.p, 0, d_q_mir_.bytes));
+    d_q_nrm_.alloc((size_t)ngq * kNormFloats * 4);
+    std::vector<long long> ids((size_t)ngq * 32);
+    for (size_t i = 0; i < ids.size(); ++i) ids[i] = i < C_ ? (long long)i : -1;
+    d_q_ids_.alloc(ids.size() * 8);
+    BIVF_CUDA(h2d(d_q_ids_.p, ids.data(), ids.size() * 8));
+    // meta: off_start u64[1] = 0 | off_count u32[1] = C | len u32[1] = 0 | table i32[1] = -1
+    struct {
+        uint64_t off_start;
+        uint32_t off_count, len;
+        int32_t table, pad;
+    } meta{0, C_, 0, -1, 0};
+    d_q_meta_.alloc(sizeof(meta));
+    BIVF_CUDA(h2d(d_q_meta_.p, &meta, sizeof(meta)));
+    d_q_zero_.alloc((size_t)65536 * 8);
+    BIVF_CUDA(dset(d_q_zero_.p, 0, d_q_zero_.bytes));
+    MirrorView M{};
+    M.off_mir = d_q_mir_.as<float>();
+    M.off_nrm = d_q_nrm_.as<float>();
+    M.cent = d_q_mu_.as<float>();
+    M.D = D_;
+    M.K = mirror_k(D_);
+    M.T = 32;
+    M.gpb = 1;
+    M.GF = GF_;
+    M.MPS = GF_;
+    std::vector<uint64_t> g(ngq);
+    std::vector<uint32_t> cl(ngq, 0);
+    for (uint32_t i = 0; i < ngq; ++i) g[i] = i;
+    DevBuf dg, dc;
+    dg.alloc(g.size() * 8);
+    dc.alloc(cl.size() * 4);
+    BIVF_CUDA(h2d(dg.p, g.data(), g.size() * 8));
+    BIVF_CUDA(h2d(dc.p, cl.data(), cl.size() * 4));
+    BIVF_CUDA(launch_mirror_groups(M, d_cent_il_.as<float>(), false, (uint64_t)32 * D_,
+                                   dg.as<uint64_t>(), dc.as<uint32_t>(), ngq, data_stream_));
+    BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+    q_tc_ok_ = make_mirror_map(d_q_mir_.as<float>(), ngq, D_, &map_q_) == cudaSuccess;
+}
+
+bool GpuIndex::use_tc_quantizer(uint32_t P) const {
+    return q_tc_ok_ && scan_mode_ != 1 && P <= 32 && P < C_;
+}
+
+uint32_t GpuIndex::quantizer_maxch(uint32_t nq) const {
+    const uint32_t tiles = ceil_div(nq, 128u), ngq = ceil_div(C_, 32u);
+    const uint32_t want = ceil_div((uint32_t)num_sms_ * 2u, std::max(1u, tiles));
+    return std::max(1u, std::min(want, std::max(1u, ngq / 4)));
+}
+
+DevLists GpuIndex::quantizer_lists() const {
+    DevLists L;
+    L.C = 1;
+    L.D = D_;
+    L.T = 32;
+    L.gpb = 1;
+    L.PS = (uint64_t)32 * D_;
+    L.MLB = 1;
+    char* m = d_q_meta_.as<char>();
+    L.off_payload = d_cent_il_.as<float>();
+    L.off_ids = d_q_ids_.as<long long>();
+    L.off_start = reinterpret_cast<const uint64_t*>(m);
+    L.off_count = reinterpret_cast<const uint32_t*>(m + 8);
+    L.len = reinterpret_cast<const uint32_t*>(m + 12);
+    L.table = reinterpret_cast<const int32_t*>(m + 16);
+    L.arena = nullptr;
+    L.bids = nullptr;
+    return L;
+}
+
+// w.queries -> w.probes (P lowest (key, cluster)) + w.pdist, on stream s.
+void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32_t fnch,
+                                 Workspace& w) {
+    if (use_tc_quantizer(P) && nq <= 65536) {
+        SearchShape qs;
+        qs.nq = nq;
+        qs.k = P;
+        qs.P = 1;
+        qs.maxch = quantizer_maxch(nq);
+        qs.gcmin = 2;
+        qs.QT = 128;
+        qs.metric = cfg_.metric;
+        BIVF_CUDA(launch_ivf_search_tc(quantizer_lists(), w.plan, d_q_zero_.as<long long>(),
+                                       w.queries, d_q_mu_.as<float>(), qs, map_q_, map_q_,
+                                       d_q_nrm_.as<float>(), nullptr, w.tc, w.pdist, w.probes,
+                                       nullptr, num_sms_, s));
+    } else {
+        BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, w.queries, nq, P, cfg_.metric,
+                                   fnch, w.fcand_d, w.fcand_i, w.pdist, w.probes, nullptr, w.ctr,
+                                   num_sms_, s));
+    }
+}
+
 DevLists GpuIndex::dev_lists() const {
     DevLists L;
     L.C = C_;
@@ -370,6 +478,7 @@ void GpuIndex::set_centroids(const float* c) {
     BIVF_CUDA(cudaSetDevice(device_));
     BIVF_CUDA(h2d(d_cent_.p, c, (size_t)C_ * D_ * 4));
     upload_centroids();
+    build_quantizer_mirror(c);
     trained_ = true;
     bool any = false;
     for (uint32_t k = 0; k < C_ && !any; ++k) any = h_off_count_[k] > 0 || h_len_[k] > 0;
@@ -524,8 +633,11 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     const size_t o_oc = take((size_t)nq * 4);
     const size_t o_ctr = take(16);
     const size_t o_plan = take((size_t)C_ * 4 * 5 + (size_t)(C_ + 1) * 4 * 2 + 16);
-    const size_t runs = npairs * maxch * 2;  // TC scan: one run per chunk and warpgroup
-    const size_t o_ub = take(runs * k * 4);
+    // TC scan: one run per (pair, chunk, warpgroup); the TC quantizer reuses the
+    // same buffers (nq pairs, quantizer_maxch chunks, P upper bounds per run)
+    const size_t qruns = (size_t)nq * quantizer_maxch(nq) * 2;
+    const size_t runs = std::max<size_t>(npairs * maxch * 2, qruns);
+    const size_t o_ub = take(std::max<size_t>(npairs * maxch * 2 * k, qruns * P) * 4);
     const size_t o_cc = take(runs * 4);
     const size_t o_clb = take(runs * kKC * 4);
     const size_t o_clo = take(runs * kKC * 4);
@@ -617,9 +729,7 @@ void GpuIndex::enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uin
     if (P == C_) {
         BIVF_CUDA(launch_all_probes(w.probes, nq, C_, l.stream));
     } else {
-        BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, w.queries, nq, P, cfg_.metric,
-                                   sh.fnch, w.fcand_d, w.fcand_i, w.pdist, w.probes, nullptr,
-                                   w.ctr, num_sms_, l.stream));
+        enqueue_quantizer(l.stream, nq, P, sh.fnch, w);
     }
     if (timing_) BIVF_CUDA(cudaEventRecord(l.t1, l.stream));
     SearchShape ss;
@@ -776,10 +886,7 @@ void GpuIndex::probes(const float* q, uint64_t nq, uint64_t nprobe, uint32_t* ou
         if (nprobe > 256) {  // == C_: every cluster (cluster-id order)
             BIVF_CUDA(launch_all_probes(w.probes, m, C_, l->stream));
         } else {
-            BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, w.queries, m,
-                                       (uint32_t)nprobe, cfg_.metric, sh.fnch, w.fcand_d,
-                                       w.fcand_i, w.pdist, w.probes, nullptr, w.ctr, num_sms_,
-                                       l->stream));
+            enqueue_quantizer(l->stream, m, (uint32_t)nprobe, sh.fnch, w);
         }
         BIVF_CUDA(cudaMemcpyAsync(tmp.data(), w.probes, tmp.size() * 8, cudaMemcpyDeviceToHost,
                                   l->stream));

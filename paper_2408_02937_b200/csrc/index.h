@@ -177,6 +177,11 @@ private:
     MirrorView mirror_view() const;
     const MirrorView* mirror_ptr() const { return mir_on_ ? &mirror_ : nullptr; }
     void rebuild_mirror();
+    void build_quantizer_mirror(const float* centroids_host);
+    bool use_tc_quantizer(uint32_t P) const;
+    uint32_t quantizer_maxch(uint32_t nq) const;
+    DevLists quantizer_lists() const;
+    void enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32_t fnch, Workspace& w);
     void upload_centroids();
 
     // --- leases / maintenance fencing
@@ -213,6 +218,11 @@ private:
     bool mir_on_ = false;
     uint64_t GF_ = 0, MPS_ = 0;
     MirrorView mirror_{};
+    // tensor-core coarse quantizer: the centroid set as ONE list (centred at the
+    // centroid mean mu, its own scan mirror) searched by the TC filter + exact refine
+    DevBuf d_q_mir_, d_q_nrm_, d_q_ids_, d_q_meta_, d_q_zero_, d_q_mu_;
+    CUtensorMap map_q_{};
+    bool q_tc_ok_ = false;
     DevBuf d_cursor_, d_len_, d_nblocks_, d_fail_, d_table_;
     DevBuf d_run_, d_failfrom_, d_newlen_;
     // data-lane staging

@@ -47,9 +47,15 @@ constexpr int kWG = 2;                     // math warpgroups
 constexpr int kTcThreads = 64 + 128 * kWG;  // warp0 TMA, warp1 MMA, warps 2.. math
 constexpr int kM = 128;                    // queries per tile (MMA M, TMEM lanes)
 constexpr int kGU = 2;                     // groups per unit (MMA N = 32 * kGU)
-constexpr int kNS = 4;                     // smem stages (one group each), kNS / kGU unit slots
+// smem stages (one group each; kNS / kGU unit slots) and smem candidate slots
+// per thread, by top-k width: k <= 16 -> 4 stages, 24 slots; k <= 32 -> 2, 48
+template <int KT>
+struct TcCfg {
+    static constexpr int NS = KT <= 16 ? 4 : 2;
+    static constexpr int KC = KT <= 16 ? 24 : 48;
+    static constexpr int NU = NS / 2;
+};
 constexpr int kNB = 4;                     // TMEM accumulators (32 * kGU columns each; even)
-constexpr int kNU = kNS / kGU;             // unit slots in the stage ring
 constexpr int kMaxD = 128;
 // a stage = one group's mirror planes: 2K rows of 128 bytes ([s_hi], [s_lo])
 constexpr int kStage = 2 * kMaxD * 128;
@@ -75,7 +81,7 @@ struct TcParams {
     const float* arena_nrm;
     // per run outputs; run = ((pair * maxch + chunk) << 1) | warpgroup
     float* ub;          // [runs][k]
-    uint32_t* ccount;   // [runs]   (kKC+1 = overflow)
+    uint32_t* ccount;   // [runs]   (kOverflow = overflow)
     float* clb;         // [runs][kKC]
     uint32_t* cloc;     // [runs][kKC]   (group << 5 | slot)
 };
@@ -314,9 +320,9 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
             ubk = ubl[KT - 1];
         }
         if (l <= ubk && !overflow) {
-            if (ncand == kKC) {  // compact against the tighter threshold
+            if (ncand == (uint32_t)TcCfg<KT>::KC) {  // compact against the tighter threshold
                 uint32_t w = 0;
-                for (uint32_t i = 0; i < kKC; ++i) {
+                for (uint32_t i = 0; i < (uint32_t)TcCfg<KT>::KC; ++i) {
                     const float li = clb[i * kM];
                     if (li <= ubk) {
                         const uint32_t ci = cloc[i * kM];
@@ -327,7 +333,7 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
                 }
                 ncand = w;
             }
-            if (ncand < kKC) {
+            if (ncand < (uint32_t)TcCfg<KT>::KC) {
                 clb[ncand * kM] = l;
                 cloc[ncand * kM] = jl | n;
                 ++ncand;
@@ -381,11 +387,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // 1024-align the dynamic smem base (SWIZZLE_128B atoms)
     const uint32_t raw_s = smem_u32(smem_raw);
     const uint32_t pad = ((raw_s + 1023u) & ~1023u) - raw_s;
+    constexpr int kNS = TcCfg<KT>::NS, kNU = TcCfg<KT>::NU, kKCs = TcCfg<KT>::KC;
     unsigned char* sB = smem_raw + pad;                        // kNS * kStage
     float* scratch = reinterpret_cast<float*>(sB + kNS * kStage);  // [kWG][32][kM] pass-2 dots
-    float* cand_lb = scratch + kWG * 32 * kM;                        // [kWG][kKC][kM]
-    uint32_t* cand_loc = reinterpret_cast<uint32_t*>(cand_lb + kWG * kKC * kM);
-    float* nslots = reinterpret_cast<float*>(cand_loc + kWG * kKC * kM);  // [kNB][kGU][64] norms
+    float* cand_lb = scratch + kWG * 32 * kM;                        // [kWG][kKCs][kM]
+    uint32_t* cand_loc = reinterpret_cast<uint32_t*>(cand_lb + kWG * kKCs * kM);
+    float* nslots = reinterpret_cast<float*>(cand_loc + kWG * kKCs * kM);  // [kNB][kGU][64] norms
     uint64_t* bars = reinterpret_cast<uint64_t*>(nslots + kNB * kGU * kNormFloats);
     uint64_t* full = bars;                 // kNU
     uint64_t* empty = full + kNU;          // kNU
@@ -534,8 +541,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const bool active = (uint32_t)m < d.npairs;
             const uint32_t pair = active ? d.pairs[m] : 0u;
             const uint64_t run = ((((uint64_t)pair * p.maxch + d.chunk) << 1) | (uint32_t)wg);
-            float* clb = cand_lb + wg * kKC * kM + m;      // this thread's candidate column
-            uint32_t* cloc = cand_loc + wg * kKC * kM + m;
+            float* clb = cand_lb + wg * kKCs * kM + m;      // this thread's candidate column
+            uint32_t* cloc = cand_loc + wg * kKCs * kM + m;
             float ubl[KT];
 #pragma unroll
             for (int i = 0; i < KT; ++i)
@@ -601,7 +608,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         }
                     }
                 }
-                p.ccount[run] = overflow ? kKC + 1 : w;
+                p.ccount[run] = overflow ? kOverflow : w;
             }
         }
     }
@@ -710,21 +717,24 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
         for (uint32_t h = 0; h < n; ++h) {
             const uint64_t run0 = ((((uint64_t)q * p.P + pi) * p.maxch + h) << 1);
             const uint32_t cnt0 = p.ccount[run0], cnt1 = p.ccount[run0 + 1];
-            if (cnt0 <= kKC && cnt1 <= kKC) {
+            if (cnt0 != kOverflow && cnt1 != kOverflow) {
                 for (uint32_t w = 0; w < 2; ++w) {
                     const uint64_t run = run0 + w;
                     const uint32_t cnt = w ? cnt1 : cnt0;
-                    const bool pass = lane < cnt && p.clb[run * kKC + lane] <= theta;
-                    const unsigned msk = __ballot_sync(0xffffffffu, pass);
-                    const uint32_t np = __popc(msk);
-                    if (qn + np > 32) flush();
-                    if (pass) {
-                        const uint32_t slot = qn + __popc(msk & ((1u << lane) - 1u));
-                        qc[slot] = c;
-                        ql[slot] = p.cloc[run * kKC + lane];
+                    for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
+                        const uint32_t e = c0 + lane;
+                        const bool pass = e < cnt && p.clb[run * kKC + e] <= theta;
+                        const unsigned msk = __ballot_sync(0xffffffffu, pass);
+                        const uint32_t np = __popc(msk);
+                        if (qn + np > 32) flush();
+                        if (pass) {
+                            const uint32_t slot = qn + __popc(msk & ((1u << lane) - 1u));
+                            qc[slot] = c;
+                            ql[slot] = p.cloc[run * kKC + e];
+                        }
+                        qn += np;
+                        __syncwarp();
                     }
-                    qn += np;
-                    __syncwarp();
                 }
             } else {  // overflow: exact rescan of the chunk
                 const uint32_t ng = ivf_ngroups(p.L, off, len);
@@ -752,9 +762,10 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
     if (lane == 0 && out_cnt) out_cnt[q] = cntq;
 }
 
+template <int KT>
 size_t tc_smem_bytes() {
-    return 1024 + kNS * kStage + kWG * 32 * kM * 4 + kWG * kKC * kM * 8 +
-           kNB * kGU * kNormFloats * 4 + (2 * kNU + 3 * kNB + 6) * 8 + 16 + 16;
+    return 1024 + TcCfg<KT>::NS * kStage + kWG * 32 * kM * 4 + kWG * TcCfg<KT>::KC * kM * 8 +
+           kNB * kGU * kNormFloats * 4 + (2 * TcCfg<KT>::NU + 3 * kNB + 6) * 8 + 16 + 16;
 }
 
 }  // namespace
@@ -831,22 +842,22 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     p.ccount = T.ccount;
     p.clb = T.clb;
     p.cloc = T.cloc;
-    const size_t sm = tc_smem_bytes();
+    const size_t sm16 = tc_smem_bytes<16>(), sm32 = tc_smem_bytes<32>();
     static bool attr = false;
     if (!attr) {
         e = cudaFuncSetAttribute(scan_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sm);
+                                 (int)sm32);
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(scan_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sm);
+                                 (int)sm16);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     if (ev0) cudaEventRecord(ev0, s);
     int grid = num_sms;
     if (const char* g = std::getenv("BIVF_TC_GRID")) grid = std::max(1, atoi(g));  // debugging aid
-    if (sh.k <= 16) scan_tc_kernel<16><<<grid, kTcThreads, sm, s>>>(p, map_off, map_arena);
-    else scan_tc_kernel<32><<<grid, kTcThreads, sm, s>>>(p, map_off, map_arena);
+    if (sh.k <= 16) scan_tc_kernel<16><<<grid, kTcThreads, sm16, s>>>(p, map_off, map_arena);
+    else scan_tc_kernel<32><<<grid, kTcThreads, sm32, s>>>(p, map_off, map_arena);
     count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -10,13 +10,16 @@
 
 namespace bivf {
 
-constexpr uint32_t kKC = 24;  // candidate slots per run (query, list chunk, warpgroup)
+// candidate slots per run (query, list chunk, warpgroup): 24 for k <= 16, 48 for
+// k <= 32; global buffers use the larger stride
+constexpr uint32_t kKC = 48;
+constexpr uint32_t kOverflow = 0xffffffffu;  // ccount marker: buffer overflowed -> exact rescan
 
 // per-search scratch of the TC path (lease workspace)
 // runs = pairs * maxch * 2 (one per chunk and math warpgroup)
 struct TcBufs {
     float* ub;          // [runs][k]  upper bounds (k smallest)
-    uint32_t* ccount;   // [runs]     candidates kept (kKC + 1 = overflow -> exact rescan)
+    uint32_t* ccount;   // [runs]     candidates kept (kOverflow -> exact rescan)
     float* clb;         // [runs][kKC] lower bounds
     uint32_t* cloc;     // [runs][kKC] group << 5 | slot
 };
