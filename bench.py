@@ -269,7 +269,6 @@ def run_ours(args, dist):
     result = None
     if rank == 0:
         peaks = read_peaks()
-        achieved = alg_bytes / (scan_avg * 1e-3) / 1e9
         qps = B * args.steps / (ms * 1e-3)
         # recall@10 vs exact (full probe == brute force over every list)
         nrec = 200
@@ -298,13 +297,7 @@ def run_ours(args, dist):
             "e2e": {"value": round(B * args.steps / e2e_s, 1), "unit": "queries/s",
                     "h2d_bytes_per_step": int(B * DIM * 4),
                     "d2h_bytes_per_step": int(B * K * 12 + B * 4)},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
-                         "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
-                         "frac": round(achieved / peaks.get("hbm_gbs", 6650.0), 3),
-                         "traffic": None, "kernel": "scan_kernel",
-                         "alg_bytes_per_launch": alg_bytes, "scan_ms": round(scan_avg, 3),
-                         "phase_ms": {"quantizer": round(ph[0], 3), "plan": round(ph[1], 3),
-                                      "scan": round(ph[2], 3), "merge": round(ph[3], 3)}},
+            "roofline": roofline(alg_bytes, scanned, scan_avg, ph, peaks),
             "gpu_launches": int(launches),
             "clocks": clk,
         }
@@ -315,6 +308,43 @@ def run_ours(args, dist):
     barrier(dist)
     ix.close()
     return result
+
+
+def roofline(alg_bytes, pairs, scan_ms, ph, peaks):
+    """Roofline of the dominant kernel (scan_tc_kernel).
+
+    Queries are grouped by list, so one staged 32-vector group serves up to 128
+    queries: the kernel streams each list from L2/HBM once per query tile and
+    is bound by the tensor pipe, not HBM.  Its algorithmic work per launch is
+    the 3xTF32 distance GEMM over every (query, probed vector) pair:
+    3 * 2 * D flops per pair.  Peak: dense TF32 = half the measured dense bf16
+    rate (MEASURED_PEAKS.json; tensor throughput halves from bf16 to tf32).
+    The north star's per-query HBM figure (bytes of every probed list, per
+    query) is reported beside it: query grouping makes it exceed HBM bandwidth.
+    `traffic` is the ncu DRAM read+write bytes per launch of this kernel from
+    profiles/r01_scan_tc_ncu.json (same index shape, tools/ncu_tc.sh)."""
+    bf16 = peaks.get("bf16_tflops", 1641.9)
+    tf32 = bf16 / 2.0
+    flops = 3.0 * 2.0 * DIM * pairs
+    achieved = flops / (scan_ms * 1e-3) / 1e12
+    hbm = peaks.get("hbm_gbs", 6548.2)
+    per_query_gbs = alg_bytes / (scan_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_scan_tc_ncu.json")) as f:
+            prof = json.load(f)
+        traffic = prof.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(tf32, 1),
+            "unit": "TFLOP/s", "frac": round(achieved / tf32, 3), "traffic": traffic,
+            "kernel": "scan_tc_kernel", "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32)",
+            "alg_flops_per_launch": flops, "pairs_per_launch": int(pairs), "scan_ms": round(scan_ms, 3),
+            "north_star_hbm": {"per_query_bytes_per_launch": alg_bytes,
+                               "achieved_gbs": round(per_query_gbs, 1), "peak_gbs": hbm,
+                               "frac": round(per_query_gbs / hbm, 3)},
+            "phase_ms": {"quantizer": round(ph[0], 3), "plan": round(ph[1], 3),
+                         "scan": round(ph[2], 3), "refine": round(ph[3], 3)}}
 
 
 LAT_QPS = 1000.0      # search requests / s (x 10 queries each)

@@ -28,7 +28,9 @@ def main():
     cent, _, _ = bivf.kmeans(base[:100_000], 1024, 10, 42)
     ix = bivf.ClusterIndex.empty(128, 1024, block_capacity=1024, num_blocks=4096)
     ix.set_centroids(cent)
+    ix.set_scan_mode("cuda")  # build-time assignment on the CUDA-core quantizer (not captured)
     ix.bulk_load(base, ix.assign_batch(base))
+    ix.set_scan_mode("auto")
     ix.set_timing(True)
     for r in range(reps):
         t = time.perf_counter()
