@@ -641,6 +641,7 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     const size_t o_cc = take(runs * 4);
     const size_t o_clb = take(runs * kKC * 4);
     const size_t o_clo = take(runs * kKC * 4);
+    const size_t o_qthr = take((size_t)nq * 4);
     const size_t o_ppos = take(npairs * 4);
     const size_t o_plist = take(npairs * 4);
     if (off > l.ws.bytes && l.stream) {
@@ -676,6 +677,7 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     w.tc.ccount = reinterpret_cast<uint32_t*>(b + o_cc);
     w.tc.clb = reinterpret_cast<float*>(b + o_clb);
     w.tc.cloc = reinterpret_cast<uint32_t*>(b + o_clo);
+    w.tc.qthr = reinterpret_cast<float*>(b + o_qthr);
     w.plan.ppos = reinterpret_cast<uint32_t*>(b + o_ppos);
     w.plan.plist = reinterpret_cast<uint32_t*>(b + o_plist);
     return w;

@@ -77,6 +77,7 @@ struct TcParams {
     const uint32_t* n_items_ptr;
     const uint32_t* plist;
     uint32_t* item_ctr;
+    float* qthr;                // [nq] per-query threshold shared by all its runs (float bits, atomicMin)
     const float* off_nrm;       // mirror norms (mirror.cuh), 64 floats per group
     const float* arena_nrm;
     // per run outputs; run = ((pair * maxch + chunk) << 1) | warpgroup
@@ -317,7 +318,7 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
                 x = fmaxf(x, ubl[i]);
                 ubl[i] = lo;
             }
-            ubk = ubl[KT - 1];
+            ubk = fminf(ubk, ubl[KT - 1]);  // ubk = min(own k-th UB, the query's shared one)
         }
         if (l <= ubk && !overflow) {
             if (ncand == (uint32_t)TcCfg<KT>::KC) {  // compact against the tighter threshold
@@ -363,13 +364,18 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                                         uint32_t taddr_lane, int lane, bool active, float nq,
                                         float (&ubl)[KT], float& ubk, uint32_t& ncand,
                                         bool& overflow, float* clb, uint32_t* cloc,
-                                        float* scr, float* nslots, uint64_t* nfull) {
+                                        float* scr, float* nslots, uint64_t* nfull, float* qt) {
     const uint32_t b = u % kNB;
+    // the query's shared threshold: the smallest k-th upper bound any of its runs
+    // has published (a valid filter bound for every run of the query)
+    const float qshared = active ? __ldcg(qt) : ubk;
     mbar_wait(&nfull[b], (u / kNB) & 1);
     mbar_wait(&acc_full[b], (u / kNB) & 1);
     __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread spin
     tc_fence_after();
     const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
+    ubk = fminf(ubk, qshared);
+    const float ubk0 = ubk;
     for (uint32_t h = 0; h < ng; ++h)
         tc_group<KT>(p, d, j0 + h, kColAcc + b * 32 * kGU + 32 * h, tmem_base, taddr_lane, active,
                      nq, ubl, ubk, ncand, overflow, clb, cloc, scr,
@@ -377,6 +383,8 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&acc_empty[b]);
+    // publish an improved threshold (positive floats order like their bit patterns)
+    if (active && ubk < ubk0) atomicMin(reinterpret_cast<int*>(qt), __float_as_int(ubk));
 }
 
 template <int KT>
@@ -589,7 +597,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     if ((unit & 1u) != (uint32_t)wg) continue;
                     tc_unit<KT>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
                                 active, nq, ubl, ubk, ncand, overflow, clb, cloc,
-                                scratch + wg * 32 * kM + m, nslots, nfull);
+                                scratch + wg * 32 * kM + m, nslots, nfull,
+                                p.qthr + (active ? pair / p.P : 0u));
                 }
             }
             // run output: k upper bounds + surviving candidates (compacted in place)
@@ -837,6 +846,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     p.plist = B.plist;
     p.item_ctr = B.item_ctr;
     p.off_nrm = off_nrm;
+    p.qthr = T.qthr;
     p.arena_nrm = arena_nrm;
     p.ub = T.ub;
     p.ccount = T.ccount;
@@ -853,6 +863,9 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    // shared per-query thresholds start at +inf-ish (0x7f7f7f7f = 3.4e38)
+    e = cudaMemsetAsync(T.qthr, 0x7f, (size_t)sh.nq * 4, s);
+    if (e != cudaSuccess) return e;
     if (ev0) cudaEventRecord(ev0, s);
     int grid = num_sms;
     if (const char* g = std::getenv("BIVF_TC_GRID")) grid = std::max(1, atoi(g));  // debugging aid

@@ -22,6 +22,7 @@ struct TcBufs {
     uint32_t* ccount;   // [runs]     candidates kept (kOverflow -> exact rescan)
     float* clb;         // [runs][kKC] lower bounds
     uint32_t* cloc;     // [runs][kKC] group << 5 | slot
+    float* qthr;        // [nq]       shared per-query threshold (reset per launch)
 };
 
 bool tc_supported(uint32_t D, uint32_t k, int metric);
