@@ -375,7 +375,7 @@ bool GpuIndex::use_tc_quantizer(uint32_t P) const {
 
 uint32_t GpuIndex::quantizer_maxch(uint32_t nq) const {
     const uint32_t tiles = ceil_div(nq, 128u), ngq = ceil_div(C_, 32u);
-    const uint32_t want = ceil_div((uint32_t)num_sms_ * 2u, std::max(1u, tiles));
+    const uint32_t want = ceil_div((uint32_t)num_sms_, std::max(1u, tiles));
     return std::max(1u, std::min(want, std::max(1u, ngq / 4)));
 }
 
