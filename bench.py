@@ -66,43 +66,78 @@ def make_data(gen):
 
 
 class Clocks:
-    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + throttle-reason sampler for the timed region (B200_PROFILING.md
+    clocks line).  NVML (nvidia-ml-py) polled every 2 ms in a thread, so even a
+    ~20 ms timed region gets samples; nvidia-smi -lms 200 as the fallback."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
+        self.samples, self.reasons, self.mx = [], set(), None
+        self.stop_ev = threading.Event()
         self.p = None
+        self.th = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.stop_ev.is_set():
+                    try:
+                        self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for n, bit in self.REASONS.items():
+                            if r & bit:
+                                self.reasons.add(n)
+                    except pynvml.NVMLError:
+                        pass
+                    self.stop_ev.wait(0.002)
+
+            self.th = threading.Thread(target=poll, daemon=True)
+            self.th.start()
+            return
+        except Exception:
+            self.th = None
         try:
             self.p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", "-i", str(index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.p = None
 
     def stop(self):
+        if self.th is not None:
+            self.stop_ev.set()
+            self.th.join()
+            return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                    "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples), "source": "nvml 2 ms"}
         if not self.p:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         self.p.terminate()
         out, _ = self.p.communicate(timeout=10)
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [v.strip() for v in line.split(",")]
-            if len(f) < 7:
+            if len(f) < 6:
                 continue
             try:
                 sm.append(float(f[0]))
                 mx = float(f[1])
             except ValueError:
                 continue
-            for n, v in zip(names, f[3:7]):
+            for n, v in zip(names, f[2:6]):
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi 200 ms"}
 
 
 class Inserter(threading.Thread):
@@ -235,6 +270,8 @@ def run_ours(args, dist):
 
     # --- e2e: same steps through the host C-ABI call (H2D + D2H inside)
     hq = queries
+    for _ in range(args.warmup):  # pinned staging buffers, OpenMP pool
+        ix.search_batch(hq, K, NPROBE)
     barrier(dist)
     t = time.perf_counter()
     for _ in range(args.steps):
@@ -317,14 +354,17 @@ def roofline(alg_bytes, pairs, scan_ms, ph, peaks):
     queries: the kernel streams each list from L2/HBM once per query tile and
     is bound by the tensor pipe, not HBM.  Its algorithmic work per launch is
     the 3xTF32 distance GEMM over every (query, probed vector) pair:
-    3 * 2 * D flops per pair.  Peak: dense TF32 = half the measured dense bf16
-    rate (MEASURED_PEAKS.json; tensor throughput halves from bf16 to tf32).
+    3 * 2 * D flops per pair.  Peak: the dense TF32 tcgen05 rate measured by tools/tc_probe_n.cu (4096
+    flop/clk/SM) at MEASURED_PEAKS.json's max SM clock (= 1.19 PFLOP/s; the
+    driver-measured cuBLAS bf16 rate / 2 would give 821).
     The north star's per-query HBM figure (bytes of every probed list, per
     query) is reported beside it: query grouping makes it exceed HBM bandwidth.
     `traffic` is the ncu DRAM read+write bytes per launch of this kernel from
     profiles/r01_scan_tc_ncu.json (same index shape, tools/ncu_tc.sh)."""
-    bf16 = peaks.get("bf16_tflops", 1641.9)
-    tf32 = bf16 / 2.0
+    # dense TF32 tcgen05 rate: 4096 flop/clk/SM (tools/tc_probe_n.cu: a 128x256x8
+    # kind::tf32 MMA retires every 128 cycles) x 148 SMs x max SM clock
+    mhz = peaks.get("sm_max_mhz", 1965.0)
+    tf32 = 4096.0 * 148 * mhz * 1e6 / 1e12
     flops = 3.0 * 2.0 * DIM * pairs
     achieved = flops / (scan_ms * 1e-3) / 1e12
     hbm = peaks.get("hbm_gbs", 6548.2)
@@ -338,7 +378,7 @@ def roofline(alg_bytes, pairs, scan_ms, ph, peaks):
         pass
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(tf32, 1),
             "unit": "TFLOP/s", "frac": round(achieved / tf32, 3), "traffic": traffic,
-            "kernel": "scan_tc_kernel", "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32)",
+            "kernel": "scan_tc_kernel", "peak_source": "dense TF32 tcgen05 4096 flop/clk/SM (tools/tc_probe_n.cu) x 148 SMs x sm_max_mhz",
             "alg_flops_per_launch": flops, "pairs_per_launch": int(pairs), "scan_ms": round(scan_ms, 3),
             "north_star_hbm": {"per_query_bytes_per_launch": alg_bytes,
                                "achieved_gbs": round(per_query_gbs, 1), "peak_gbs": hbm,
@@ -358,6 +398,8 @@ def latency_phase(ix, queries, inserts):
     ex = Executor(ix, num_lanes=32)
     common = dict(k=K, nprobe=NPROBE, search_batch=10, insert_batch=INSERT_BATCH, seed=1,
                   poisson=True)
+    # untimed warm-up: every lane's lease workspace and staging buffers get allocated
+    replay(ex, queries, inserts, LAT_QPS, INSERT_RATE / INSERT_BATCH, 0.5, **common)
     base = replay(ex, queries, inserts, LAT_QPS, 0.0, LAT_SECONDS, **common)
     live = replay(ex, queries, inserts, LAT_QPS, INSERT_RATE / INSERT_BATCH, LAT_SECONDS, **common)
     ex.shutdown()

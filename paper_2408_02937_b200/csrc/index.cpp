@@ -60,6 +60,24 @@ void PinBuf::ensure(size_t n) {
     bytes = grow;
 }
 
+// Host staging copies of the search path (user buffers <-> pinned lease
+// buffers) on the OpenMP pool: one thread moves ~6-10 GB/s, the copy of a
+// 10K x 128 query batch would otherwise be a sizeable part of the call.
+static void par_memcpy(void* dst, const void* src, size_t n) {
+    constexpr size_t kChunk = 256 * 1024;
+    if (n < 4 * kChunk) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    const long nch = (long)((n + kChunk - 1) / kChunk);
+#pragma omp parallel for num_threads(8) schedule(static)
+    for (long i = 0; i < nch; ++i) {
+        const size_t o = (size_t)i * kChunk;
+        std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                    std::min(kChunk, n - o));
+    }
+}
+
 cudaError_t GpuIndex::h2d(void* dst, const void* src, size_t n) const {
     if (!n) return cudaSuccess;
     cudaError_t e = cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, data_stream_);
@@ -776,7 +794,7 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
         const size_t out_b = (size_t)m * k * 12 + (size_t)m * 4;
         l->pin.ensure(in_b + out_b + 256);
         char* pin = l->pin.as<char>();
-        std::memcpy(pin, q + s * D_, in_b);
+        par_memcpy(pin, q + s * D_, in_b);
         float* pd = reinterpret_cast<float*>(pin + align_up(in_b, 64));
         long long* pi = reinterpret_cast<long long*>(pd + (size_t)m * k + ((m * k) & 1));
         uint32_t* pc = reinterpret_cast<uint32_t*>(pi + (size_t)m * k);
@@ -795,8 +813,8 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
             BIVF_CUDA(cudaEventRecord(l->done, l->stream));
         }
         BIVF_CUDA(cudaEventSynchronize(l->done));
-        std::memcpy(out_d + s * k, pd, (size_t)m * k * 4);
-        std::memcpy(out_ids + s * k, pi, (size_t)m * k * 8);
+        par_memcpy(out_d + s * k, pd, (size_t)m * k * 4);
+        par_memcpy(out_ids + s * k, pi, (size_t)m * k * 8);
         if (out_cnt) std::memcpy(out_cnt + s, pc, (size_t)m * 4);
         if (timing_) record_timings(*l);
     }
