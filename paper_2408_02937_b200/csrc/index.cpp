@@ -233,6 +233,8 @@ void GpuIndex::alloc_device() {
         BIVF_CUDA(dset(d_arena_mir_.p, 0, d_arena_mir_.bytes));
         d_arena_nrm_.alloc((size_t)NB_ * gpb_ * kNormFloats * 4);
         BIVF_CUDA(dset(d_arena_nrm_.p, 0, d_arena_nrm_.bytes));
+        d_arena_rows_.alloc((size_t)NB_ * PS_ * 4);
+        BIVF_CUDA(dset(d_arena_rows_.p, 0, d_arena_rows_.bytes));
         tc_ok_ = make_mirror_map(d_arena_mir_.as<float>(), (uint64_t)NB_ * gpb_, D_, &map_arena_) ==
                  cudaSuccess;
     }
@@ -275,6 +277,8 @@ void GpuIndex::ensure_offline_capacity(uint64_t slots) {
         BIVF_CUDA(dset(d_off_mir_.p, 0, d_off_mir_.bytes));
         d_off_nrm_.alloc((size_t)(slots / 32) * kNormFloats * 4);
         BIVF_CUDA(dset(d_off_nrm_.p, 0, d_off_nrm_.bytes));
+        d_off_rows_.alloc((size_t)slots * D_ * 4);
+        BIVF_CUDA(dset(d_off_rows_.p, 0, d_off_rows_.bytes));
         if (make_mirror_map(d_off_mir_.as<float>(), slots / 32, D_, &map_off_) != cudaSuccess)
             tc_ok_ = false;
     }
@@ -287,6 +291,8 @@ MirrorView GpuIndex::mirror_view() const {
     M.arena_mir = d_arena_mir_.as<float>();
     M.off_nrm = d_off_nrm_.as<float>();
     M.arena_nrm = d_arena_nrm_.as<float>();
+    M.off_rows = d_off_rows_.as<float>();
+    M.arena_rows = d_arena_rows_.as<float>();
     M.cent = d_cent_.as<float>();
     M.D = D_;
     M.K = mirror_k(D_);
@@ -431,7 +437,8 @@ void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32
         qs.metric = cfg_.metric;
         BIVF_CUDA(launch_ivf_search_tc(quantizer_lists(), w.plan, d_q_zero_.as<long long>(),
                                        w.queries, d_q_mu_.as<float>(), qs, map_q_, map_q_,
-                                       d_q_nrm_.as<float>(), nullptr, w.tc, w.pdist, w.probes,
+                                       d_q_nrm_.as<float>(), nullptr, d_cent_.as<float>(), nullptr,
+                                       w.tc, w.pdist, w.probes,
                                        nullptr, num_sms_, s));
     } else {
         BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, w.queries, nq, P, cfg_.metric,
@@ -763,7 +770,8 @@ void GpuIndex::enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uin
     if (use_tc(k)) {
         BIVF_CUDA(launch_ivf_search_tc(dev_lists(), w.plan, w.probes, w.queries,
                                        d_cent_.as<float>(), ss, map_off_, map_arena_,
-                                       d_off_nrm_.as<float>(), d_arena_nrm_.as<float>(), w.tc, w.out_d,
+                                       d_off_nrm_.as<float>(), d_arena_nrm_.as<float>(),
+                                       d_off_rows_.as<float>(), d_arena_rows_.as<float>(), w.tc, w.out_d,
                                        w.out_i, w.out_cnt, num_sms_, l.stream,
                                        timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr));
     } else {
@@ -1223,7 +1231,7 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
     DevBuf dpa, dia, dscr_p, dscr_i, dclr, dli, dlv, doi, dov;
     dpa.alloc(std::max<size_t>(pa.size(), 1) * 8);
     dia.alloc(std::max<size_t>(ia.size(), 1) * 8);
-    dscr_p.alloc(std::max<size_t>((size_t)nm * (mir_on_ ? 2 * mirror_k(D_) + 2 : D_), 1) * 4);
+    dscr_p.alloc(std::max<size_t>((size_t)nm * (mir_on_ ? 2 * mirror_k(D_) + 2 + D_ : D_), 1) * 4);
     dscr_i.alloc(std::max<size_t>(nm, 1) * 8);
     dclr.alloc(std::max<size_t>(clear.size(), 1) * 8);
     dli.alloc(std::max<size_t>(len_idx.size(), 1) * 4);
@@ -1476,6 +1484,9 @@ void GpuIndex::rearrange(uint32_t c) {
                 BIVF_CUDA(launch_block_moves(d_arena_nrm_.as<float>(), nullptr,
                                              (uint64_t)gpb_ * kNormFloats, T_, ds.as<int32_t>(),
                                              dd.as<int32_t>(), nm, sp.as<float>(), nullptr, st));
+                BIVF_CUDA(launch_block_moves(d_arena_rows_.as<float>(), nullptr, PS_, T_,
+                                             ds.as<int32_t>(), dd.as<int32_t>(), nm, sp.as<float>(),
+                                             nullptr, st));
             }
             for (uint32_t k : rowc) {
                 staged.push_back(h_blocks_[k]);

@@ -214,7 +214,7 @@ private:
     uint64_t off_slots_cap_ = 0;
     DevBuf d_arena_, d_bids_, d_owner_;
     // tensor-core scan mirror (mirror.cuh); allocated when the TC scan can serve this index
-    DevBuf d_off_mir_, d_arena_mir_, d_off_nrm_, d_arena_nrm_;
+    DevBuf d_off_mir_, d_arena_mir_, d_off_nrm_, d_arena_nrm_, d_off_rows_, d_arena_rows_;
     bool mir_on_ = false;
     uint64_t GF_ = 0, MPS_ = 0;
     MirrorView mirror_{};

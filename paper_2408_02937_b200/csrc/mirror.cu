@@ -15,12 +15,14 @@ __device__ __forceinline__ float tf32_trunc_m(float x) {
 
 // one vector -> its mirror column `lane` of group `g` (+ the group's norm block
 // `nrm`).  x[d * xs] is dim d.
-__device__ __forceinline__ void mirror_column(float* g, float* nrm, uint32_t lane, const float* x,
-                                              uint32_t xs, const float* c, uint32_t D,
-                                              uint32_t K) {
+__device__ __forceinline__ void mirror_column(float* g, float* nrm, float* row, uint32_t lane,
+                                              const float* x, uint32_t xs, const float* c,
+                                              uint32_t D, uint32_t K) {
     float n2 = 0.f;
     for (uint32_t d = 0; d < D; ++d) {
-        const float s = __fsub_rn(x[(uint64_t)d * xs], c[d]);
+        const float xd = x[(uint64_t)d * xs];
+        if (row) row[d] = xd;
+        const float s = __fsub_rn(xd, c[d]);
         const float h = tf32_trunc_m(s);
         g[(uint64_t)d * 32u + lane] = h;
         g[(uint64_t)(K + d) * 32u + lane] = __fsub_rn(s, h);
@@ -32,17 +34,19 @@ __device__ __forceinline__ void mirror_column(float* g, float* nrm, uint32_t lan
 
 // group base (mirror planes) and norm block of a slot address
 __device__ __forceinline__ float* mirror_slot(const MirrorView& M, uint64_t a, uint32_t& lane,
-                                              float*& nrm) {
+                                              float*& nrm, float*& row) {
     if (a >> 63) {
         const uint64_t gs = a & ~(1ull << 63);
         const uint64_t blk = gs / M.T, slot = gs - blk * M.T;
         lane = (uint32_t)(slot & 31u);
         const uint64_t g = blk * M.gpb + (slot >> 5);
         nrm = M.arena_nrm + g * kNormFloats;
+        row = M.arena_rows ? M.arena_rows + (g * 32u + lane) * M.D : nullptr;
         return M.arena_mir + g * M.GF;
     }
     lane = (uint32_t)(a & 31u);
     nrm = M.off_nrm + (a >> 5) * kNormFloats;
+    row = M.off_rows ? M.off_rows + (a >> 5 << 5 | lane) * (uint64_t)M.D : nullptr;
     return M.off_mir + (a >> 5) * M.GF;
 }
 
@@ -54,7 +58,8 @@ __global__ void mirror_insert_kernel(MirrorView M, uint32_t n, const float* x, c
     if (b < 0) return;
     const uint32_t slot = out_did[i] % M.T;
     const uint64_t g = (uint64_t)b * M.gpb + (slot >> 5);
-    mirror_column(M.arena_mir + g * M.GF, M.arena_nrm + g * kNormFloats, slot & 31u,
+    float* row = M.arena_rows ? M.arena_rows + (g * 32u + (slot & 31u)) * M.D : nullptr;
+    mirror_column(M.arena_mir + g * M.GF, M.arena_nrm + g * kNormFloats, row, slot & 31u,
                   x + (uint64_t)i * M.D, 1, M.cent + (uint64_t)asg[i] * M.D, M.D, M.K);
 }
 
@@ -63,7 +68,8 @@ __global__ void mirror_offline_kernel(MirrorView M, uint32_t n, const float* x,
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t s = dest[i];
-    mirror_column(M.off_mir + (s >> 5) * M.GF, M.off_nrm + (s >> 5) * kNormFloats,
+    float* row = M.off_rows ? M.off_rows + s * M.D : nullptr;
+    mirror_column(M.off_mir + (s >> 5) * M.GF, M.off_nrm + (s >> 5) * kNormFloats, row,
                   (uint32_t)(s & 31u), x + (uint64_t)i * M.D, 1, M.cent + (uint64_t)asg[i] * M.D,
                   M.D, M.K);
 }
@@ -75,32 +81,39 @@ __global__ void mirror_groups_kernel(MirrorView M, const float* payload, int are
     if (w >= n) return;
     const uint64_t gi = groups[w];
     const float* src;
-    float *dst, *nrm;
+    float *dst, *nrm, *rows;
     if (arena) {
         const uint64_t blk = gi / M.gpb, j = gi - blk * M.gpb;
         src = payload + blk * PS + j * 32ull * M.D;
         dst = M.arena_mir + gi * M.GF;
         nrm = M.arena_nrm + gi * kNormFloats;
+        rows = M.arena_rows;
     } else {
         src = payload + gi * 32ull * M.D;
         dst = M.off_mir + gi * M.GF;
         nrm = M.off_nrm + gi * kNormFloats;
+        rows = M.off_rows;
     }
-    mirror_column(dst, nrm, lane, src + lane, 32, M.cent + (uint64_t)cl[w] * M.D, M.D, M.K);
+    float* row = rows ? rows + (gi * 32u + lane) * M.D : nullptr;
+    mirror_column(dst, nrm, row, lane, src + lane, 32, M.cent + (uint64_t)cl[w] * M.D, M.D, M.K);
 }
 
 __global__ void mirror_slot_move_kernel(MirrorView M, const uint64_t* id_addr, uint32_t n,
                                         float* scr, int phase) {
-    // per slot: 2K plane rows + 2 norm entries
-    const uint32_t R = 2 * M.K + 2;
+    // per slot: 2K plane rows + 2 norm entries + D row entries
+    const uint32_t R = 2 * M.K + 2 + M.D;
     const uint64_t total = (uint64_t)n * R;
     for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
          o += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t m = (uint32_t)(o / R), r = (uint32_t)(o - (uint64_t)m * R);
         uint32_t lane;
-        float* nrm;
-        float* g = mirror_slot(M, id_addr[phase == 0 ? m : n + m], lane, nrm);
-        float* e = r < 2 * M.K ? g + (uint64_t)r * 32u + lane : nrm + (r - 2 * M.K) * 32u + lane;
+        float *nrm, *row;
+        float* g = mirror_slot(M, id_addr[phase == 0 ? m : n + m], lane, nrm, row);
+        float* e;
+        if (r < 2 * M.K) e = g + (uint64_t)r * 32u + lane;
+        else if (r < 2 * M.K + 2) e = nrm + (r - 2 * M.K) * 32u + lane;
+        else if (row) e = row + (r - 2 * M.K - 2);
+        else continue;
         if (phase == 0) scr[o] = *e;
         else *e = scr[o];
     }
@@ -137,7 +150,7 @@ cudaError_t launch_mirror_groups(const MirrorView& M, const float* payload, bool
 cudaError_t launch_mirror_slot_moves(const MirrorView& M, const uint64_t* id_addr, uint32_t n,
                                      float* scratch, cudaStream_t s) {
     if (!n || !M.off_mir) return cudaSuccess;
-    const uint64_t total = (uint64_t)n * (2 * M.K + 2);
+    const uint64_t total = (uint64_t)n * (2 * M.K + 2 + M.D);
     const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148 * 16));
     for (int phase = 0; phase < 2; ++phase) {
         mirror_slot_move_kernel<<<g, 256, 0, s>>>(M, id_addr, n, scratch, phase);

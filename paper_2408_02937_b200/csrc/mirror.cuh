@@ -11,6 +11,9 @@
 //     rows [K, 2K)     s_lo, dim d
 // Norms, per group, a separate array of 64 floats: [|s|^2 (sequential fp32) x 32]
 // [kVScale * |s|^2 x 32] (the per-slot term of the scan's pass-1 threshold, scan_tc.cu).
+// Rows, per group, a slot-major copy of the exact payload (32 x D fp32): the
+// refine's candidate gathers read 4 contiguous 128-byte lines per vector instead
+// of D scattered 32-byte sectors of the interleaved layout.
 // One TMA box of {32, 2K} rows stages a group's two B operands.  The
 // mirror is written by the same data-lane operations that write the payload
 // (bulk load, insert, delete slot moves, rearrangement block moves), before
@@ -27,6 +30,8 @@ struct MirrorView {
     float* arena_mir;      // num_blocks x MPS
     float* off_nrm;        // offline groups x 64
     float* arena_nrm;      // num_blocks x gpb x 64
+    float* off_rows;       // offline groups x 32 x D
+    float* arena_rows;     // num_blocks x gpb x 32 x D
     const float* cent;     // [C][D] row-major centroids
     uint32_t D, K, T, gpb; // K = D rounded up to 8
     uint64_t GF;           // floats per group  = 2K*32
@@ -61,7 +66,7 @@ cudaError_t launch_mirror_groups(const MirrorView& M, const float* payload, bool
                                  uint32_t n, cudaStream_t s);
 // delete compaction: the same moves as launch_slot_moves, on the mirror
 // (id_addr[2n] = sources then destinations; bit 63 = arena, value = the slot's
-// id index).  scratch: n * (2K+2) floats.
+// id index).  scratch: n * (2K+2+D) floats.
 cudaError_t launch_mirror_slot_moves(const MirrorView& M, const uint64_t* id_addr, uint32_t n,
                                      float* scratch, cudaStream_t s);
 

@@ -78,6 +78,8 @@ struct TcParams {
     const uint32_t* plist;
     uint32_t* item_ctr;
     float* qthr;                // [nq] per-query threshold shared by all its runs (float bits, atomicMin)
+    const float* off_rows;      // mirror rows (mirror.cuh): slot-major exact payload copy
+    const float* arena_rows;
     const float* off_nrm;       // mirror norms (mirror.cuh), 64 floats per group
     const float* arena_nrm;
     // per run outputs; run = ((pair * maxch + chunk) << 1) | warpgroup
@@ -651,6 +653,39 @@ __device__ __forceinline__ float exact_l2(const float* qs, const float* x, uint3
     return acc;
 }
 
+// exact distance over a contiguous row (the mirror's slot-major copy): same
+// ascending-d sequential fp32 sum, so the same bits as over the interleaved payload
+__device__ __forceinline__ float exact_l2_row(const float* qs, const float* x, uint32_t D) {
+    float acc = 0.f;
+    uint32_t d0 = 0;
+    if ((D & 3u) == 0) {
+        for (; d0 + 16 <= D; d0 += 16) {
+            float4 v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = __ldg(reinterpret_cast<const float4*>(x + d0) + i);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc = l2_step(acc, qs[d0 + 4 * i + 0], v[i].x);
+                acc = l2_step(acc, qs[d0 + 4 * i + 1], v[i].y);
+                acc = l2_step(acc, qs[d0 + 4 * i + 2], v[i].z);
+                acc = l2_step(acc, qs[d0 + 4 * i + 3], v[i].w);
+            }
+        }
+    }
+    for (; d0 < D; ++d0) acc = l2_step(acc, qs[d0], __ldg(x + d0));
+    return acc;
+}
+
+// row of slot (group j of list c, slot s) in the mirror's row copy
+__device__ __forceinline__ const float* cand_row(const TcParams& p, uint32_t c, uint32_t off,
+                                                 uint32_t j, uint32_t s) {
+    const uint32_t og = (off + 31u) >> 5;
+    if (j < og) return p.off_rows + (p.L.off_start[c] + 32ull * j + s) * p.D;
+    const uint32_t jj = j - og, mid = jj / p.L.gpb, gi = jj - mid * p.L.gpb;
+    const uint64_t g = (uint64_t)p.L.table[(uint64_t)c * p.L.MLB + mid] * p.L.gpb + gi;
+    return p.arena_rows + (g * 32u + s) * p.D;
+}
+
 template <int KPL>
 __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d, long long* out_i,
                               uint32_t* out_cnt, uint32_t nq) {
@@ -712,7 +747,8 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
         if (ok) {
             const uint32_t c = qc[lane], loc = ql[lane];
             const GroupRef g = ivf_group(p.L, c, p.snap_off[c], p.snap_len[c], loc >> 5);
-            dist = exact_l2(qs, g.base + (loc & 31), p.D);
+            dist = p.off_rows ? exact_l2_row(qs, cand_row(p, c, p.snap_off[c], loc >> 5, loc & 31), p.D)
+                              : exact_l2(qs, g.base + (loc & 31), p.D);
             id = g.ids[loc & 31];
         }
         offer(dist, id, ok);
@@ -818,7 +854,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  const float* queries, const float* centroids,
                                  const SearchShape& sh, const CUtensorMap& map_off,
                                  const CUtensorMap& map_arena, const float* off_nrm,
-                                 const float* arena_nrm, const TcBufs& T, float* out_d,
+                                 const float* arena_nrm, const float* off_rows,
+                                 const float* arena_rows, const TcBufs& T, float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
     if (sh.nq == 0) return cudaSuccess;
@@ -846,6 +883,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     p.plist = B.plist;
     p.item_ctr = B.item_ctr;
     p.off_nrm = off_nrm;
+    p.off_rows = off_rows;
+    p.arena_rows = arena_rows;
     p.qthr = T.qthr;
     p.arena_nrm = arena_nrm;
     p.ub = T.ub;

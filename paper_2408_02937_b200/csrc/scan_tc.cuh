@@ -35,7 +35,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  const float* queries, const float* centroids,
                                  const SearchShape& sh, const CUtensorMap& map_off,
                                  const CUtensorMap& map_arena, const float* off_nrm,
-                                 const float* arena_nrm, const TcBufs& T, float* out_d,
+                                 const float* arena_nrm, const float* off_rows,
+                                 const float* arena_rows, const TcBufs& T, float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0 = nullptr,
                                  cudaEvent_t ev1 = nullptr);

@@ -71,3 +71,63 @@ def test_tc_sift_like_scale(gpu_ready):
     # small request shape (latency path): 10 queries
     a, b = both(ix, q[:10], 10, 16)
     assert_same(a, b)
+
+
+def test_tc_after_rearrange_and_delete(gpu_ready):
+    """The scan mirror follows every data move: rearrangement block swaps and
+    delete tail-into-hole compaction (TC == CUDA-core == oracle)."""
+    D, C, T, nb = 96, 24, 64, 1200
+    base = bivf.synthetic_dataset(6000, D, 40, 31)
+    cent, asg, _ = bivf.kmeans(base, C, 5, 31)
+    ix = ClusterIndex.empty(D, C, block_capacity=T, num_blocks=nb, rearrange_threshold=80)
+    ix.set_centroids(cent)
+    ix.bulk_load(base, asg)
+    orc = O.OracleIndex(cent, base, asg, T, nb, 80)
+    rng = np.random.default_rng(5)
+    live = list(range(6000))
+    events = 0
+    for step in range(12):
+        x = bivf.synthetic_dataset(int(rng.integers(50, 400)), D, 40, 100 + step)
+        a = ix.insert(x)
+        orc.insert(x)
+        live += [int(v) for v in a if v >= 0]
+        req = [int(v) for v in rng.choice(live, size=60, replace=False)]
+        assert ix.remove(req)[0] == orc.remove(req)[0]
+        live = [v for v in live if v not in set(req)]
+        ix.rearrange_sweep()
+        orc.rearrange_sweep()
+        events += len(ix.take_events())
+        orc.take_events()
+    assert events > 0, "the scenario must exercise rearrangement"
+    assert ix.layout() == orc.layout()
+    q = bivf.synthetic_dataset(200, D, 40, 77)
+    for k, npb in ((10, 4), (16, 8), (32, C)):
+        a, b = both(ix, q, k, npb)
+        assert_same(a, b)
+        for j in range(0, 200, 23):
+            oi, od = orc.search(q[j], k, npb)
+            assert np.array_equal(b[0][j, : b[2][j]], oi) and np.array_equal(bits(b[1][j, : b[2][j]]), bits(od))
+
+
+@pytest.mark.parametrize("C,D", [(64, 32), (100, 96), (257, 128), (1024, 100)])
+def test_tc_quantizer_matches_exact(gpu_ready, C, D):
+    """The tensor-core coarse quantizer (centroids as one TC-scanned list + exact
+    refine) returns exactly the CUDA-core quantizer's (key, cluster) top-P."""
+    x = bivf.synthetic_dataset(20 * C + 3000, D, 2 * C, 9)
+    cent, _, _ = bivf.kmeans(x[: 20 * C], C, 3, 9)
+    ix = ClusterIndex.empty(D, C, block_capacity=64, num_blocks=64)
+    ix.set_centroids(cent)
+    q = x[20 * C:]
+    for P in (1, 7, 32):
+        ix.set_scan_mode("cuda")
+        a = ix.probes(q, P)
+        ix.set_scan_mode("auto")
+        b = ix.probes(q, P)
+        assert np.array_equal(a, b), (C, D, P)
+    # and against a numpy sequential-sum ground truth on a sample
+    for j in range(0, len(q), 311):
+        acc = np.zeros(C, np.float32)
+        for d in range(D):
+            t = (q[j, d] - cent[:, d]).astype(np.float32)
+            acc = (acc + (t * t).astype(np.float32)).astype(np.float32)
+        assert np.array_equal(b[j], np.lexsort((np.arange(C), acc))[:32])
