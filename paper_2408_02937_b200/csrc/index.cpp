@@ -397,6 +397,11 @@ bool GpuIndex::use_tc_quantizer(uint32_t P) const {
     return q_tc_ok_ && scan_mode_ != 1 && P <= 32 && P < C_;
 }
 
+uint32_t GpuIndex::quantizer_slice() const {
+    const uint64_t ld = (uint64_t)ceil_div(C_, 32) * 32;
+    return (uint32_t)std::max<uint64_t>(128, std::min<uint64_t>(65536, (1ull << 27) / ld));
+}
+
 uint32_t GpuIndex::quantizer_maxch(uint32_t nq) const {
     const uint32_t tiles = ceil_div(nq, 128u), ngq = ceil_div(C_, 32u);
     const uint32_t want = ceil_div((uint32_t)num_sms_, std::max(1u, tiles));
@@ -427,19 +432,28 @@ DevLists GpuIndex::quantizer_lists() const {
 void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32_t fnch,
                                  Workspace& w) {
     if (use_tc_quantizer(P) && nq <= 65536) {
-        SearchShape qs;
-        qs.nq = nq;
-        qs.k = P;
-        qs.P = 1;
-        qs.maxch = quantizer_maxch(nq);
-        qs.gcmin = 2;
-        qs.QT = 128;
-        qs.metric = cfg_.metric;
-        BIVF_CUDA(launch_ivf_search_tc(quantizer_lists(), w.plan, d_q_zero_.as<long long>(),
-                                       w.queries, d_q_mu_.as<float>(), qs, map_q_, map_q_,
-                                       d_q_nrm_.as<float>(), nullptr, d_cent_.as<float>(), nullptr,
-                                       w.tc, w.pdist, w.probes,
-                                       nullptr, num_sms_, s));
+        // dense mode: approximate distances of every (query, centroid) on the
+        // tensor cores, then a per-query selection + exact recompute of the few
+        // centroids whose lower bound can reach the P-th upper bound
+        const uint32_t ld = ceil_div(C_, 32) * 32, qsl = quantizer_slice();
+        for (uint32_t q0 = 0; q0 < nq; q0 += qsl) {
+            const uint32_t m = std::min(qsl, nq - q0);
+            SearchShape qs;
+            qs.nq = m;
+            qs.k = P;
+            qs.P = 1;
+            qs.maxch = quantizer_maxch(m);
+            qs.gcmin = 2;
+            qs.QT = 128;
+            qs.metric = cfg_.metric;
+            TcDense dn{w.qdense, w.qdense_nq, ld, C_};
+            BIVF_CUDA(launch_ivf_search_tc(quantizer_lists(), w.plan, d_q_zero_.as<long long>(),
+                                           w.queries + (size_t)q0 * Dp_, d_q_mu_.as<float>(), qs,
+                                           map_q_, map_q_, d_q_nrm_.as<float>(), nullptr,
+                                           d_cent_.as<float>(), nullptr, w.tc, &dn,
+                                           w.pdist + (size_t)q0 * P, w.probes + (size_t)q0 * P,
+                                           nullptr, num_sms_, s));
+        }
     } else {
         BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, w.queries, nq, P, cfg_.metric,
                                    fnch, w.fcand_d, w.fcand_i, w.pdist, w.probes, nullptr, w.ctr,
@@ -667,6 +681,9 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     const size_t o_clb = take(runs * kKC * 4);
     const size_t o_clo = take(runs * kKC * 4);
     const size_t o_qthr = take((size_t)nq * 4);
+    const size_t o_qdense = take(q_tc_ok_ ? (size_t)std::min<uint32_t>(nq, quantizer_slice()) *
+                                                ceil_div(C_, 32) * 32 * 4 : 16);
+    const size_t o_qdnq = take((size_t)nq * 4);
     const size_t o_ppos = take(npairs * 4);
     const size_t o_plist = take(npairs * 4);
     if (off > l.ws.bytes && l.stream) {
@@ -703,6 +720,8 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     w.tc.clb = reinterpret_cast<float*>(b + o_clb);
     w.tc.cloc = reinterpret_cast<uint32_t*>(b + o_clo);
     w.tc.qthr = reinterpret_cast<float*>(b + o_qthr);
+    w.qdense = reinterpret_cast<float*>(b + o_qdense);
+    w.qdense_nq = reinterpret_cast<float*>(b + o_qdnq);
     w.plan.ppos = reinterpret_cast<uint32_t*>(b + o_ppos);
     w.plan.plist = reinterpret_cast<uint32_t*>(b + o_plist);
     return w;
@@ -771,7 +790,8 @@ void GpuIndex::enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uin
         BIVF_CUDA(launch_ivf_search_tc(dev_lists(), w.plan, w.probes, w.queries,
                                        d_cent_.as<float>(), ss, map_off_, map_arena_,
                                        d_off_nrm_.as<float>(), d_arena_nrm_.as<float>(),
-                                       d_off_rows_.as<float>(), d_arena_rows_.as<float>(), w.tc, w.out_d,
+                                       d_off_rows_.as<float>(), d_arena_rows_.as<float>(), w.tc,
+                                       nullptr, w.out_d,
                                        w.out_i, w.out_cnt, num_sms_, l.stream,
                                        timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr));
     } else {

@@ -106,6 +106,8 @@ struct Workspace {  // carved from Lease::ws
     uint32_t* ctr;
     PlanBufs plan;
     TcBufs tc;
+    float* qdense;         // TC quantizer: [qslice][ceil(C/32)*32] approximate distances
+    float* qdense_nq;      // [nq] query norms
 };
 
 struct RearrangeEvent {
@@ -180,6 +182,7 @@ private:
     void build_quantizer_mirror(const float* centroids_host);
     bool use_tc_quantizer(uint32_t P) const;
     uint32_t quantizer_maxch(uint32_t nq) const;
+    uint32_t quantizer_slice() const;
     DevLists quantizer_lists() const;
     void enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32_t fnch, Workspace& w);
     void upload_centroids();

@@ -78,6 +78,12 @@ struct TcParams {
     const uint32_t* plist;
     uint32_t* item_ctr;
     float* qthr;                // [nq] per-query threshold shared by all its runs (float bits, atomicMin)
+    // dense mode (the coarse quantizer): approximate distances a = |r|^2 + |s|^2 - 2 r.s of
+    // every (query, slot of the single list) -> dense_out[query * dense_ld + slot], |r|^2 ->
+    // dense_nq[query]; no filtering (dense_select_kernel does the selection)
+    float* dense_out;
+    float* dense_nq;
+    uint32_t dense_ld;
     const float* off_rows;      // mirror rows (mirror.cuh): slot-major exact payload copy
     const float* arena_rows;
     const float* off_nrm;       // mirror norms (mirror.cuh), 64 floats per group
@@ -366,7 +372,8 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                                         uint32_t taddr_lane, int lane, bool active, float nq,
                                         float (&ubl)[KT], float& ubk, uint32_t& ncand,
                                         bool& overflow, float* clb, uint32_t* cloc,
-                                        float* scr, float* nslots, uint64_t* nfull, float* qt) {
+                                        float* scr, float* nslots, uint64_t* nfull, float* qt,
+                                        uint32_t qrow) {
     const uint32_t b = u % kNB;
     // the query's shared threshold: the smallest k-th upper bound any of its runs
     // has published (a valid filter bound for every run of the query)
@@ -376,6 +383,28 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
     __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread spin
     tc_fence_after();
     const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
+    if (p.dense_out) {  // dense mode: write the approximate distances, no filtering
+        for (uint32_t h = 0; h < ng; ++h) {
+            float dot[32];
+            tmem_ld32(tmem_base + taddr_lane + kColAcc + b * 32 * kGU + 32 * h, dot);
+            const float* wn = nslots + (b * kGU + h) * kNormFloats;
+            if (active) {
+                float4* o = reinterpret_cast<float4*>(p.dense_out + (uint64_t)qrow * p.dense_ld +
+                                                      32u * (j0 + h));
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    const float4 v = reinterpret_cast<const float4*>(wn)[i / 4];
+                    o[i / 4] = make_float4(fmaf(-2.f, dot[i], nq + v.x), fmaf(-2.f, dot[i + 1], nq + v.y),
+                                           fmaf(-2.f, dot[i + 2], nq + v.z),
+                                           fmaf(-2.f, dot[i + 3], nq + v.w));
+                }
+            }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[b]);
+        return;
+    }
     ubk = fminf(ubk, qshared);
     const float ubk0 = ubk;
     for (uint32_t h = 0; h < ng; ++h)
@@ -595,16 +624,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 tc_fence_before();
                 named_bar(1 + wg, 128);
                 if (wt == 0) mbar_arrive(a_full);
+                if (p.dense_out && wg == 0 && active && d.chunk == 0) p.dense_nq[pair / p.P] = nq;
                 for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
                     if ((unit & 1u) != (uint32_t)wg) continue;
                     tc_unit<KT>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
                                 active, nq, ubl, ubk, ncand, overflow, clb, cloc,
                                 scratch + wg * 32 * kM + m, nslots, nfull,
-                                p.qthr + (active ? pair / p.P : 0u));
+                                p.qthr + (active ? pair / p.P : 0u), pair / p.P);
                 }
             }
             // run output: k upper bounds + surviving candidates (compacted in place)
-            if (active) {
+            if (active && !p.dense_out) {
 #pragma unroll
                 for (int i = 0; i < KT; ++i)
                     if (i >= KT - (int)p.k) p.ub[run * p.k + (i - (KT - (int)p.k))] = ubl[i];
@@ -807,6 +837,129 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
     if (lane == 0 && out_cnt) out_cnt[q] = cntq;
 }
 
+// Dense selection (the coarse quantizer): one warp per query over the n
+// approximate distances of the dense mode.  Upper/lower bounds from the same
+// eps' as the filter (mirror.cuh), threshold = k-th smallest upper bound, every
+// slot whose lower bound is <= it recomputed EXACTLY (sequential fp32 over the
+// row-major source rows, the reference's bits) -> exact (dist, id) top-k.
+template <int KPL>
+__global__ void dense_select_kernel(const float* dense, uint32_t ld, const float* dnq,
+                                    const float* nrm, const float* rows, const float* queries,
+                                    uint32_t Dp, uint32_t D, uint32_t n, uint32_t nq, uint32_t k,
+                                    float* out_d, long long* out_i) {
+    extern __shared__ float qsm[];
+    const uint32_t nw = blockDim.x >> 5, wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t q = blockIdx.x * nw + wq;
+    if (q >= nq) return;
+    float* qs = qsm + wq * Dp;
+    for (uint32_t i = lane; i < D; i += 32) qs[i] = queries[(uint64_t)q * Dp + i];
+    __syncwarp();
+    const float nqv = dnq[q];
+    const float* row = dense + (uint64_t)q * ld;
+    const float inf = __int_as_float(0x7f800000);
+    auto ub_of = [&](uint32_t c) {
+        const float a = row[c];
+        const float ns = nrm[(c >> 5) * kNormFloats + (c & 31)];
+        return a + fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, nqv + ns, 1e-30f));
+    };
+    // phase A: an upper bound of the k-th smallest upper bound from each lane's
+    // two smallest values (64 values, k <= 64 of them sorted across the warp):
+    // the k-th smallest of any k values is >= the true k-th smallest
+    float pre = inf;
+    if (k <= 64 && n >= 64) {
+        float m1 = inf, m2 = inf;
+        for (uint32_t c = lane; c < n; c += 32) {
+            const float h = ub_of(c);
+            m2 = fminf(m2, fmaxf(m1, h));
+            m1 = fminf(m1, h);
+        }
+        // bitonic sort of the 64 values (lane holds m1 at index lane, m2 at 32 + lane)
+        float v0 = m1, v1 = m2;
+        for (uint32_t sz = 2; sz <= 64; sz <<= 1) {
+            for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
+                if (st == 32) {  // pairs (lane, 32 + lane)
+                    const bool up = ((lane & sz) == 0) || sz == 64;
+                    const float lo = fminf(v0, v1), hi = fmaxf(v0, v1);
+                    v0 = up ? lo : hi;
+                    v1 = up ? hi : lo;
+                } else {
+                    const float o0 = __shfl_xor_sync(0xffffffffu, v0, st);
+                    const float o1 = __shfl_xor_sync(0xffffffffu, v1, st);
+                    const bool lower = (lane & st) == 0;
+                    const bool up0 = ((lane & sz) == 0), up1 = (((32 + lane) & sz) == 0);
+                    v0 = (lower == up0) ? fminf(v0, o0) : fmaxf(v0, o0);
+                    v1 = (lower == up1) ? fminf(v1, o1) : fmaxf(v1, o1);
+                }
+            }
+        }
+        const uint32_t kk = k - 1;
+        pre = __shfl_sync(0xffffffffu, kk < 32 ? v0 : v1, kk & 31);
+    }
+    WarpTopK<KPL> th;
+    th.init();
+    for (uint32_t c0 = 0; c0 < n; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        const float h = c < n ? ub_of(c) : inf;
+        const bool pass = c < n && h <= pre && th.admits(h, (long long)c);
+        unsigned m = __ballot_sync(0xffffffffu, pass);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const float bh = __shfl_sync(0xffffffffu, h, src);
+            const long long bc = __shfl_sync(0xffffffffu, (long long)c, src);
+            if (th.admits(bh, bc)) th.insert(bh, bc, (int)k, lane);
+        }
+    }
+    const float theta = fminf(th.thr_d, pre);  // +inf when n < k
+    // pass 2: candidates (lower bound <= theta) queued 32 at a time, then one
+    // exact distance per lane (parallel sequential chains, not one per chunk)
+    WarpTopK<KPL> tk;
+    tk.init();
+    uint32_t* queue = reinterpret_cast<uint32_t*>(qsm + nw * Dp) + wq * 32;
+    uint32_t qn = 0;
+    auto flush = [&]() {
+        const bool ok = lane < qn;
+        const uint32_t c = ok ? queue[lane] : 0u;
+        const float dist = ok ? exact_l2_row(qs, rows + (uint64_t)c * D, D) : 0.f;
+        const bool pass = ok && tk.admits(dist, (long long)c);
+        unsigned m = __ballot_sync(0xffffffffu, pass);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const float bd = __shfl_sync(0xffffffffu, dist, src);
+            const long long bc = __shfl_sync(0xffffffffu, (long long)c, src);
+            if (tk.admits(bd, bc)) tk.insert(bd, bc, (int)k, lane);
+        }
+        qn = 0;
+        __syncwarp();
+    };
+    for (uint32_t c0 = 0; c0 < n; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        bool cand = false;
+        if (c < n) {
+            const float a = row[c];
+            const float ns = nrm[(c >> 5) * kNormFloats + (c & 31)];
+            const float l = a - fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, nqv + ns, 1e-30f));
+            cand = l <= theta;
+        }
+        const unsigned msk = __ballot_sync(0xffffffffu, cand);
+        const uint32_t np = __popc(msk);
+        if (qn + np > 32) flush();
+        if (cand) queue[qn + __popc(msk & ((1u << lane) - 1u))] = c;
+        qn += np;
+        __syncwarp();
+    }
+    if (qn) flush();
+#pragma unroll
+    for (int r = 0; r < KPL; ++r) {
+        const uint32_t e = r * 32 + lane;
+        if (e < k) {
+            out_d[(uint64_t)q * k + e] = tk.d[r];
+            out_i[(uint64_t)q * k + e] = tk.id[r];
+        }
+    }
+}
+
 template <int KT>
 size_t tc_smem_bytes() {
     return 1024 + TcCfg<KT>::NS * kStage + kWG * 32 * kM * 4 + kWG * TcCfg<KT>::KC * kM * 8 +
@@ -855,7 +1008,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  const SearchShape& sh, const CUtensorMap& map_off,
                                  const CUtensorMap& map_arena, const float* off_nrm,
                                  const float* arena_nrm, const float* off_rows,
-                                 const float* arena_rows, const TcBufs& T, float* out_d,
+                                 const float* arena_rows, const TcBufs& T, const TcDense* dense,
+                                 float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
     if (sh.nq == 0) return cudaSuccess;
@@ -886,6 +1040,11 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     p.off_rows = off_rows;
     p.arena_rows = arena_rows;
     p.qthr = T.qthr;
+    if (dense) {
+        p.dense_out = dense->out;
+        p.dense_nq = dense->nq;
+        p.dense_ld = dense->ld;
+    }
     p.arena_nrm = arena_nrm;
     p.ub = T.ub;
     p.ccount = T.ccount;
@@ -915,8 +1074,21 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     if (e != cudaSuccess) return e;
     if (ev1) cudaEventRecord(ev1, s);
     const uint32_t wpb = 4;
-    refine_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
-        p, probes, out_d, out_i, out_cnt, sh.nq);
+    if (dense) {
+        const uint32_t n = dense->n;
+        const size_t sm_sel = wpb * (p.Dp * 4 + 128);
+        if (sh.k <= 32)
+            dense_select_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
+                dense->out, dense->ld, dense->nq, off_nrm, off_rows, queries, p.Dp, p.D, n, sh.nq,
+                sh.k, out_d, out_i);
+        else
+            dense_select_kernel<8><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
+                dense->out, dense->ld, dense->nq, off_nrm, off_rows, queries, p.Dp, p.D, n, sh.nq,
+                sh.k, out_d, out_i);
+    } else {
+        refine_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
+            p, probes, out_d, out_i, out_cnt, sh.nq);
+    }
     count_launch();
     return cudaGetLastError();
 }

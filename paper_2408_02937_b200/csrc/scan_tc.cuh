@@ -27,6 +27,15 @@ struct TcBufs {
 
 bool tc_supported(uint32_t D, uint32_t k, int metric);
 
+// Dense mode of the TC scan (coarse quantizer): the single list's n slots,
+// approximate distances -> out[nq][ld], query norms -> nq; the selection
+// kernel then returns the exact top-k (dist, slot).
+struct TcDense {
+    float* out;
+    float* nq;
+    uint32_t ld, n;
+};
+
 // 2-D TMA map over a scan mirror region (mirror.cuh: `groups` groups of
 // 2K rows of 32 floats), box = {32, 2K}, SWIZZLE_128B_ATOM_32B.
 cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUtensorMap* out);
@@ -36,7 +45,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  const SearchShape& sh, const CUtensorMap& map_off,
                                  const CUtensorMap& map_arena, const float* off_nrm,
                                  const float* arena_nrm, const float* off_rows,
-                                 const float* arena_rows, const TcBufs& T, float* out_d,
+                                 const float* arena_rows, const TcBufs& T, const TcDense* dense,
+                                 float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0 = nullptr,
                                  cudaEvent_t ev1 = nullptr);

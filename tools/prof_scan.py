@@ -22,11 +22,14 @@ def main():
     nprobe = int(os.environ.get("PROF_NPROBE", 32))
     k = int(os.environ.get("PROF_K", 10))
     reps = int(os.environ.get("PROF_REPS", 4))
-    x = bivf.synthetic_dataset(n_base + nq, 128, 4096, 2)
+    D = int(os.environ.get("PROF_D", 128))
+    C = int(os.environ.get("PROF_NLIST", 1024))
+    metric = int(os.environ.get("PROF_METRIC", 0))
+    x = bivf.synthetic_dataset(n_base + nq, D, 4096, 2)
     np.maximum(np.rint(x, out=x), 0, out=x)
     base, q = x[:n_base], x[n_base:]
-    cent, _, _ = bivf.kmeans(base[:100_000], 1024, 10, 42)
-    ix = bivf.ClusterIndex.empty(128, 1024, block_capacity=1024, num_blocks=4096)
+    cent, _, _ = bivf.kmeans(base[:100_000], C, 10 if D <= 128 else 4, 42)
+    ix = bivf.ClusterIndex.empty(D, C, block_capacity=1024, num_blocks=4096, metric=metric)
     ix.set_centroids(cent)
     ix.set_scan_mode("cuda")  # build-time assignment on the CUDA-core quantizer (not captured)
     ix.bulk_load(base, ix.assign_batch(base))
