@@ -400,8 +400,14 @@ def latency_phase(ix, queries, inserts):
                   poisson=True)
     # untimed warm-up: every lane's lease workspace and staging buffers get allocated
     replay(ex, queries, inserts, LAT_QPS, INSERT_RATE / INSERT_BATCH, 0.5, **common)
-    base = replay(ex, queries, inserts, LAT_QPS, 0.0, LAT_SECONDS, **common)
-    live = replay(ex, queries, inserts, LAT_QPS, INSERT_RATE / INSERT_BATCH, LAT_SECONDS, **common)
+    base = replay(ex, queries, inserts, LAT_QPS, 0.0, LAT_SECONDS, raw=True, **common)
+    live = replay(ex, queries, inserts, LAT_QPS, INSERT_RATE / INSERT_BATCH, LAT_SECONDS, raw=True,
+                  **common)
+    for nm, r in (("idle", base), ("live", live)):  # stalls, for the log
+        sp = [(i, round(v / 1e3, 1)) for i, v in enumerate(r.pop("search_raw_us")) if v > 5000]
+        r.pop("insert_raw_us")
+        if sp:
+            log(f"latency {nm}: {len(sp)} requests > 5 ms, first {sp[:10]}")
     ex.shutdown()
     ex.close()
     p99a, p99b = base["search"]["p99_ms"], live["search"]["p99_ms"]

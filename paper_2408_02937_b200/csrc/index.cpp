@@ -1124,10 +1124,10 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
             hv[h] = (uint32_t)r;
         }
     }
-    DevBuf dk, dv, dloc;
-    dk.alloc(hcap * 8);
-    dv.alloc(hcap * 4);
-    dloc.alloc(n * 8);
+    DevBuf &dk = s_rm_[0], &dv = s_rm_[1], &dloc = s_rm_[2];
+    dk.ensure(hcap * 8);
+    dv.ensure(hcap * 4);
+    dloc.ensure(n * 8);
     BIVF_CUDA(cudaMemcpyAsync(dk.p, hk.data(), hcap * 8, cudaMemcpyHostToDevice, st));
     BIVF_CUDA(cudaMemcpyAsync(dv.p, hv.data(), hcap * 4, cudaMemcpyHostToDevice, st));
     BIVF_CUDA(cudaMemsetAsync(dloc.p, 0xff, n * 8, st));
@@ -1248,16 +1248,17 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
     std::vector<uint64_t> pa(msrc_p), ia(msrc_i);
     pa.insert(pa.end(), mdst_p.begin(), mdst_p.end());
     ia.insert(ia.end(), mdst_i.begin(), mdst_i.end());
-    DevBuf dpa, dia, dscr_p, dscr_i, dclr, dli, dlv, doi, dov;
-    dpa.alloc(std::max<size_t>(pa.size(), 1) * 8);
-    dia.alloc(std::max<size_t>(ia.size(), 1) * 8);
-    dscr_p.alloc(std::max<size_t>((size_t)nm * (mir_on_ ? 2 * mirror_k(D_) + 2 + D_ : D_), 1) * 4);
-    dscr_i.alloc(std::max<size_t>(nm, 1) * 8);
-    dclr.alloc(std::max<size_t>(clear.size(), 1) * 8);
-    dli.alloc(std::max<size_t>(len_idx.size(), 1) * 4);
-    dlv.alloc(std::max<size_t>(len_idx.size(), 1) * 4);
-    doi.alloc(std::max<size_t>(off_idx.size(), 1) * 4);
-    dov.alloc(std::max<size_t>(off_idx.size(), 1) * 4);
+    DevBuf &dpa = s_rm_[3], &dia = s_rm_[4], &dscr_p = s_rm_[5], &dscr_i = s_rm_[6],
+           &dclr = s_rm_[7], &dli = s_rm_[8], &dlv = s_rm_[9], &doi = s_rm_[10], &dov = s_rm_[11];
+    dpa.ensure(std::max<size_t>(pa.size(), 1) * 8);
+    dia.ensure(std::max<size_t>(ia.size(), 1) * 8);
+    dscr_p.ensure(std::max<size_t>((size_t)nm * (mir_on_ ? 2 * mirror_k(D_) + 2 + D_ : D_), 1) * 4);
+    dscr_i.ensure(std::max<size_t>(nm, 1) * 8);
+    dclr.ensure(std::max<size_t>(clear.size(), 1) * 8);
+    dli.ensure(std::max<size_t>(len_idx.size(), 1) * 4);
+    dlv.ensure(std::max<size_t>(len_idx.size(), 1) * 4);
+    doi.ensure(std::max<size_t>(off_idx.size(), 1) * 4);
+    dov.ensure(std::max<size_t>(off_idx.size(), 1) * 4);
     if (!pa.empty()) {
         BIVF_CUDA(cudaMemcpyAsync(dpa.p, pa.data(), pa.size() * 8, cudaMemcpyHostToDevice, st));
         BIVF_CUDA(cudaMemcpyAsync(dia.p, ia.data(), ia.size() * 8, cudaMemcpyHostToDevice, st));
@@ -1477,11 +1478,13 @@ void GpuIndex::rearrange(uint32_t c) {
         }
     if (!src.empty()) {
         const uint32_t nm = (uint32_t)src.size();
-        DevBuf ds, dd, sp, si, own;
-        ds.alloc(nm * 4);
-        dd.alloc(nm * 4);
-        sp.alloc((size_t)nm * std::max<uint64_t>(PS_, mir_on_ ? MPS_ : 0) * 4);
-        si.alloc((size_t)nm * T_ * 8);
+        // persistent grow-only scratch: a cudaMalloc/cudaFree per rearrangement
+        // would device-synchronize against every in-flight search
+        DevBuf &ds = s_rr_src_, &dd = s_rr_dst_, &sp = s_rr_pay_, &si = s_rr_ids_;
+        ds.ensure(nm * 4);
+        dd.ensure(nm * 4);
+        sp.ensure((size_t)nm * std::max<uint64_t>(PS_, mir_on_ ? MPS_ : 0) * 4);
+        si.ensure((size_t)nm * T_ * 8);
         cudaStream_t st = data_stream_;
         BIVF_CUDA(cudaMemcpyAsync(ds.p, src.data(), nm * 4, cudaMemcpyHostToDevice, st));
         BIVF_CUDA(cudaMemcpyAsync(dd.p, dst.data(), nm * 4, cudaMemcpyHostToDevice, st));

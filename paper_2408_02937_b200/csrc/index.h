@@ -233,6 +233,10 @@ private:
     DevBuf d_x_, d_ids_, d_asg_, d_blk_, d_did_, d_qtmp_, d_fc_d_, d_fc_i_, d_fo_d_, d_fo_i_,
         d_ctr_;
     PinBuf h_stage_;
+    // maintenance scratch (rearrangement block moves, delete), grow-only; used
+    // under data_mu_ only
+    DevBuf s_rr_src_, s_rr_dst_, s_rr_pay_, s_rr_ids_;
+    DevBuf s_rm_[12];
 
     // host mirror
     std::vector<uint32_t> h_len_, h_off_count_, h_nblocks_;

@@ -171,7 +171,7 @@ def summarize_latencies(samples_ms):
 
 
 def replay(executor, queries, inserts, qps_search, qps_insert, duration_s, k=10, nprobe=8,
-           search_batch=1, insert_batch=1, seed=1, poisson=False):
+           search_batch=1, insert_batch=1, seed=1, poisson=False, raw=False):
     """Open-loop replay (workload.cpp:114-269) in the native library; returns
     latency summaries (ms) plus rejected / error counts."""
     q = np.ascontiguousarray(queries, dtype=np.float32)
@@ -197,7 +197,11 @@ def replay(executor, queries, inserts, qps_search, qps_insert, duration_s, k=10,
                             C.byref(err)))
     sl = s_lat[: ns.value]
     il = i_lat[: ni.value]
-    return {"search": summarize_latencies([v / 1e3 for v in sl if v >= 0]),
-            "insert": summarize_latencies([v / 1e3 for v in il if v >= 0]),
-            "rejected": rej.value, "errors": err.value,
-            "search_issued": int(ns.value), "insert_issued": int(ni.value)}
+    out = {"search": summarize_latencies([v / 1e3 for v in sl if v >= 0]),
+           "insert": summarize_latencies([v / 1e3 for v in il if v >= 0]),
+           "rejected": rej.value, "errors": err.value,
+           "search_issued": int(ns.value), "insert_issued": int(ni.value)}
+    if raw:  # per-request latency in us, arrival order (-1 = rejected)
+        out["search_raw_us"] = sl.copy()
+        out["insert_raw_us"] = il.copy()
+    return out
