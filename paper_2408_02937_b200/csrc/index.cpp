@@ -64,8 +64,8 @@ void PinBuf::ensure(size_t n) {
 // buffers) on the OpenMP pool: one thread moves ~6-10 GB/s, the copy of a
 // 10K x 128 query batch would otherwise be a sizeable part of the call.
 static void par_memcpy(void* dst, const void* src, size_t n) {
-    constexpr size_t kChunk = 256 * 1024;
-    if (n < 4 * kChunk) {
+    constexpr size_t kChunk = 128 * 1024;
+    if (n < 2 * kChunk) {
         std::memcpy(dst, src, n);
         return;
     }
@@ -430,7 +430,7 @@ DevLists GpuIndex::quantizer_lists() const {
 
 // w.queries -> w.probes (P lowest (key, cluster)) + w.pdist, on stream s.
 void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32_t fnch,
-                                 Workspace& w) {
+                                 Workspace& w, uint32_t qbase) {
     if (use_tc_quantizer(P) && nq <= 65536) {
         // dense mode: approximate distances of every (query, centroid) on the
         // tensor cores, then a per-query selection + exact recompute of the few
@@ -447,17 +447,19 @@ void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32
             qs.QT = 128;
             qs.metric = cfg_.metric;
             TcDense dn{w.qdense, w.qdense_nq, ld, C_};
+            const size_t g0 = (size_t)qbase + q0;
             BIVF_CUDA(launch_ivf_search_tc(quantizer_lists(), w.plan, d_q_zero_.as<long long>(),
-                                           w.queries + (size_t)q0 * Dp_, d_q_mu_.as<float>(), qs,
+                                           w.queries + g0 * Dp_, d_q_mu_.as<float>(), qs,
                                            map_q_, map_q_, d_q_nrm_.as<float>(), nullptr,
                                            d_cent_.as<float>(), nullptr, w.tc, &dn,
-                                           w.pdist + (size_t)q0 * P, w.probes + (size_t)q0 * P,
+                                           w.pdist + g0 * P, w.probes + g0 * P,
                                            nullptr, num_sms_, s));
         }
     } else {
-        BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, w.queries, nq, P, cfg_.metric,
-                                   fnch, w.fcand_d, w.fcand_i, w.pdist, w.probes, nullptr, w.ctr,
-                                   num_sms_, s));
+        BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, w.queries + (size_t)qbase * Dp_,
+                                   nq, P, cfg_.metric, fnch, w.fcand_d, w.fcand_i,
+                                   w.pdist + (size_t)qbase * P, w.probes + (size_t)qbase * P,
+                                   nullptr, w.ctr, num_sms_, s));
     }
 }
 
@@ -767,16 +769,30 @@ void GpuIndex::validate_search(uint64_t k, uint64_t nprobe) const {
 
 // Enqueue one search slice on the lease stream: pad -> quantizer -> plan ->
 // scan -> merge.  Caller holds gate_ shared.
+// pad + coarse quantizer for queries [q0, q0 + m) of the slice (raw rows at
+// q_dev_raw_piece), on the lease stream; probes land at their slice offsets.
+// fnch: the slice's quantizer chunking (carve sized the CUDA-core quantizer's
+// candidate scratch with it).
+void GpuIndex::enqueue_probes(Lease& l, const float* q_dev_raw_piece, uint32_t q0, uint32_t m,
+                              uint32_t P, uint32_t fnch, Workspace& w) {
+    BIVF_CUDA(launch_pad_rows(q_dev_raw_piece, m, D_, Dp_, w.queries + (size_t)q0 * Dp_, l.stream));
+    if (P == C_) {
+        BIVF_CUDA(launch_all_probes(w.probes + (size_t)q0 * P, m, C_, l.stream));
+    } else {
+        enqueue_quantizer(l.stream, m, P, fnch, w, q0);
+    }
+}
+
 void GpuIndex::enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uint32_t k,
                               uint32_t P, Workspace& w) {
-    const LaunchShape sh = pick_shape(nq, k, P, C_, num_sms_);
     if (timing_) BIVF_CUDA(cudaEventRecord(l.t0, l.stream));
-    BIVF_CUDA(launch_pad_rows(q_dev_raw, nq, D_, Dp_, w.queries, l.stream));
-    if (P == C_) {
-        BIVF_CUDA(launch_all_probes(w.probes, nq, C_, l.stream));
-    } else {
-        enqueue_quantizer(l.stream, nq, P, sh.fnch, w);
-    }
+    enqueue_probes(l, q_dev_raw, 0, nq, P, pick_shape(nq, k, P, C_, num_sms_).fnch, w);
+    enqueue_scan(l, nq, k, P, w);
+}
+
+// plan + list scan + merge/refine over the slice's probes (after enqueue_probes).
+void GpuIndex::enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Workspace& w) {
+    const LaunchShape sh = pick_shape(nq, k, P, C_, num_sms_);
     if (timing_) BIVF_CUDA(cudaEventRecord(l.t1, l.stream));
     SearchShape ss;
     ss.nq = nq;
@@ -822,7 +838,6 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
         const size_t out_b = (size_t)m * k * 12 + (size_t)m * 4;
         l->pin.ensure(in_b + out_b + 256);
         char* pin = l->pin.as<char>();
-        par_memcpy(pin, q + s * D_, in_b);
         float* pd = reinterpret_cast<float*>(pin + align_up(in_b, 64));
         long long* pi = reinterpret_cast<long long*>(pd + (size_t)m * k + ((m * k) & 1));
         uint32_t* pc = reinterpret_cast<uint32_t*>(pi + (size_t)m * k);
@@ -833,7 +848,16 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
                 BIVF_CUDA(cudaStreamWaitEvent(l->stream, maint_evt_, 0));
                 l->seen_maint = gen;
             }
-            BIVF_CUDA(cudaMemcpyAsync(w.qraw, pin, in_b, cudaMemcpyHostToDevice, l->stream));
+            // stage the queries in ~1 MB pieces: the DMA of piece i overlaps the
+            // host copy of piece i+1 (a per-piece quantizer was measured slower:
+            // smaller quantizer launches cost more than the DMA they hide)
+            const size_t piece = std::max<size_t>(1u << 20, (size_t)D_ * 4 * 256);
+            for (size_t o = 0; o < in_b; o += piece) {
+                const size_t nb = std::min(piece, in_b - o);
+                par_memcpy(pin + o, reinterpret_cast<const char*>(q + s * D_) + o, nb);
+                BIVF_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(w.qraw) + o, pin + o, nb,
+                                          cudaMemcpyHostToDevice, l->stream));
+            }
             enqueue_search(*l, w.qraw, m, (uint32_t)k, (uint32_t)nprobe, w);
             BIVF_CUDA(cudaMemcpyAsync(pd, w.out_d, (size_t)m * k * 4, cudaMemcpyDeviceToHost, l->stream));
             BIVF_CUDA(cudaMemcpyAsync(pi, w.out_i, (size_t)m * k * 8, cudaMemcpyDeviceToHost, l->stream));

@@ -184,7 +184,8 @@ private:
     uint32_t quantizer_maxch(uint32_t nq) const;
     uint32_t quantizer_slice() const;
     DevLists quantizer_lists() const;
-    void enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32_t fnch, Workspace& w);
+    void enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32_t fnch, Workspace& w,
+                           uint32_t qbase = 0);
     void upload_centroids();
 
     // --- leases / maintenance fencing
@@ -192,6 +193,9 @@ private:
     void release_lease(Lease* l);
     Workspace carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_t maxch,
                     uint32_t fnch);
+    void enqueue_probes(Lease& l, const float* q_dev_raw_piece, uint32_t q0, uint32_t m,
+                        uint32_t P, uint32_t fnch, Workspace& w);
+    void enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Workspace& w);
     void enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uint32_t k,
                         uint32_t P, Workspace& w);
     void begin_maintenance();   // caller holds data_mu_; takes gate_ exclusively
