@@ -729,32 +729,42 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
     uint32_t* ql = qc + 32;                                                  // loc
     for (uint32_t i = lane; i < p.D; i += 32) qs[i] = p.queries[(uint64_t)q * p.Dp + i];
     __syncwarp();
-    // 1. threshold
+    // 1. threshold: the k-th smallest upper bound over every run of the query.
+    // All of the query's run slots are one contiguous block [P][maxch][2][k];
+    // lanes sweep it flat (slots of chunks h >= nch[c] were never written).
+    // Only values <= the scan's shared threshold (itself one run's k-th upper
+    // bound, so >= theta) can matter.
+    const float pre = __ldcg(p.qthr + q);
     WarpTopK<KPL> th;
     th.init();
-    for (uint32_t pi = 0; pi < p.P; ++pi) {
-        const uint32_t c = (uint32_t)probes[(uint64_t)q * p.P + pi];
-        const uint32_t n = p.nch[c];
-        for (uint32_t hw = 0; hw < 2 * n; ++hw) {  // (chunk, warpgroup) runs
-            const uint64_t run = ((((uint64_t)q * p.P + pi) * p.maxch) << 1) + hw;
-            for (uint32_t e0 = 0; e0 < p.k; e0 += 32) {
-                const uint32_t e = e0 + lane;
-                const float v = e < p.k ? p.ub[run * p.k + e] : 0.f;
-                const long long id = (long long)(run * p.k + e);
-                const bool pass = e < p.k && th.admits(v, id);
-                unsigned msk = __ballot_sync(0xffffffffu, pass);
-                if (!msk) break;
-                while (msk) {
-                    const int src = __ffs(msk) - 1;
-                    msk &= msk - 1;
-                    const float bv = __shfl_sync(0xffffffffu, v, src);
-                    const long long bi = __shfl_sync(0xffffffffu, id, src);
-                    if (th.admits(bv, bi)) th.insert(bv, bi, (int)p.k, lane);
+    {
+        const uint32_t per_probe = p.maxch * 2u * p.k;
+        const uint32_t total = p.P * per_probe;
+        const uint64_t base = (uint64_t)q * total;
+        for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+            const uint32_t f = f0 + lane;
+            bool pass = false;
+            float v = 0.f;
+            if (f < total) {
+                const uint32_t pi = f / per_probe, rem = f - pi * per_probe;
+                const uint32_t h = rem / (2u * p.k);
+                const uint32_t c = (uint32_t)probes[(uint64_t)q * p.P + pi];
+                if (h < p.nch[c]) {
+                    v = p.ub[base + f];
+                    pass = v <= pre && th.admits(v, (long long)(base + f));
                 }
+            }
+            unsigned msk = __ballot_sync(0xffffffffu, pass);
+            while (msk) {
+                const int src = __ffs(msk) - 1;
+                msk &= msk - 1;
+                const float bv = __shfl_sync(0xffffffffu, v, src);
+                const long long bi = (long long)(base + f0 + src);
+                if (th.admits(bv, bi)) th.insert(bv, bi, (int)p.k, lane);
             }
         }
     }
-    const float theta = th.thr_d;  // +inf if fewer than k vectors were scanned
+    const float theta = fminf(th.thr_d, pre);  // +inf if fewer than k vectors were scanned
     // 2. exact top-k over the surviving candidates
     WarpTopK<KPL> tk;
     tk.init();
