@@ -394,7 +394,7 @@ void GpuIndex::build_quantizer_mirror(const float* c) {
 }
 
 bool GpuIndex::use_tc_quantizer(uint32_t P) const {
-    return q_tc_ok_ && scan_mode_ != 1 && P <= 32 && P < C_;
+    return q_tc_ok_ && scan_mode_ != 1 && P <= 256 && P < C_;
 }
 
 uint32_t GpuIndex::quantizer_slice() const {
@@ -757,6 +757,11 @@ bool GpuIndex::use_tc(uint32_t k) const {
     return tc_supported(D_, k, cfg_.metric);
 }
 
+bool GpuIndex::use_tc_dense(uint32_t k) const {
+    if (scan_mode_ == 1 || !tc_ok_) return false;
+    return tc_dense_supported(D_, k, cfg_.metric);
+}
+
 void GpuIndex::validate_search(uint64_t k, uint64_t nprobe) const {
     // ivf_index.cpp:266-269
     if (k < 1) throw Error(BIVF_EINVAL, "search: k must be >= 1");
@@ -809,6 +814,39 @@ void GpuIndex::enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Works
                                        d_off_rows_.as<float>(), d_arena_rows_.as<float>(), w.tc,
                                        nullptr, w.out_d,
                                        w.out_i, w.out_cnt, num_sms_, l.stream,
+                                       timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr));
+    } else if (use_tc_dense(k)) {
+        // k > 32: the tensor cores write the approximate distance of every
+        // (query, probed vector) pair, a per-query selection takes the exact
+        // top-k (scan_tc.cu dense_ivf_select_kernel).  The rows' total size is
+        // read back once (one stream sync) to size the lease's dense buffer.
+        const uint32_t npairs = nq * P;
+        const size_t tmpb = dense_plan_tmp_bytes(npairs);
+        const size_t o_len = 0, o_off = align_up((size_t)npairs * 8),
+                     o_nq = o_off + align_up((size_t)npairs * 8),
+                     o_tot = o_nq + align_up((size_t)npairs * 4), o_tmp = o_tot + 256;
+        if (o_tmp + tmpb > l.dense_aux.bytes) BIVF_CUDA(cudaStreamSynchronize(l.stream));
+        l.dense_aux.ensure(o_tmp + tmpb);
+        char* ab = l.dense_aux.as<char>();
+        uint64_t* plen = reinterpret_cast<uint64_t*>(ab + o_len);
+        uint64_t* poff = reinterpret_cast<uint64_t*>(ab + o_off);
+        float* pnq = reinterpret_cast<float*>(ab + o_nq);
+        uint64_t* ptot = reinterpret_cast<uint64_t*>(ab + o_tot);
+        BIVF_CUDA(launch_dense_plan(dev_lists(), w.plan, w.probes, ss, plen, poff, ab + o_tmp, tmpb,
+                                    ptot, l.stream));
+        l.dpin.ensure(64);
+        BIVF_CUDA(cudaMemcpyAsync(l.dpin.p, ptot, 8, cudaMemcpyDeviceToHost, l.stream));
+        BIVF_CUDA(cudaStreamSynchronize(l.stream));
+        const uint64_t total = *l.dpin.as<uint64_t>();
+        const size_t rows_b = align_up(std::max<size_t>(total, 1) * 4);
+        l.dense.ensure(rows_b + std::max<size_t>(total / 32, 1) * 8);
+        TcDense dn{l.dense.as<float>(), pnq, 0, 0, poff,
+                   reinterpret_cast<float2*>(l.dense.as<char>() + rows_b)};
+        BIVF_CUDA(launch_ivf_search_tc(dev_lists(), w.plan, w.probes, w.queries,
+                                       d_cent_.as<float>(), ss, map_off_, map_arena_,
+                                       d_off_nrm_.as<float>(), d_arena_nrm_.as<float>(),
+                                       d_off_rows_.as<float>(), d_arena_rows_.as<float>(), w.tc,
+                                       &dn, w.out_d, w.out_i, w.out_cnt, num_sms_, l.stream,
                                        timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr));
     } else {
         BIVF_CUDA(launch_ivf_search(dev_lists(), w.plan, w.probes, w.queries, ss, w.cand_d,

@@ -87,6 +87,8 @@ struct Lease {
     cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr, t3 = nullptr, t4 = nullptr;
     DevBuf ws;
     PinBuf pin;
+    DevBuf dense, dense_aux;  // k > 32 TC path: dense distance rows + per-pair offsets
+    PinBuf dpin;
     uint64_t seen_maint = 0;
     bool busy = false;
 };
@@ -164,6 +166,7 @@ public:
     void set_timing(bool on) { timing_ = on; }
     void set_scan_mode(int m) { scan_mode_ = m; }
     bool use_tc(uint32_t k) const;
+    bool use_tc_dense(uint32_t k) const;
     void last_timings(float* out4) const;
     void record_timings(Lease& l);
 

@@ -28,6 +28,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -84,6 +86,8 @@ struct TcParams {
     float* dense_out;
     float* dense_nq;
     uint32_t dense_ld;
+    const uint64_t* dense_pair_off;  // IVF dense mode (k > 32): row of pair i at dense_pair_off[i]
+    float2* dense_gsum;              // IVF dense mode: per (pair, group) (min upper, min lower bound)
     const float* off_rows;      // mirror rows (mirror.cuh): slot-major exact payload copy
     const float* arena_rows;
     const float* off_nrm;       // mirror norms (mirror.cuh), 64 floats per group
@@ -373,7 +377,7 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                                         float (&ubl)[KT], float& ubk, uint32_t& ncand,
                                         bool& overflow, float* clb, uint32_t* cloc,
                                         float* scr, float* nslots, uint64_t* nfull, float* qt,
-                                        uint32_t qrow) {
+                                        uint64_t qrow) {
     const uint32_t b = u % kNB;
     // the query's shared threshold: the smallest k-th upper bound any of its runs
     // has published (a valid filter bound for every run of the query)
@@ -389,14 +393,36 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
             tmem_ld32(tmem_base + taddr_lane + kColAcc + b * 32 * kGU + 32 * h, dot);
             const float* wn = nslots + (b * kGU + h) * kNormFloats;
             if (active) {
-                float4* o = reinterpret_cast<float4*>(p.dense_out + (uint64_t)qrow * p.dense_ld +
-                                                      32u * (j0 + h));
+                float4* o = reinterpret_cast<float4*>(p.dense_out + qrow + 32u * (j0 + h));
+                float av[32];
 #pragma unroll
                 for (int i = 0; i < 32; i += 4) {
                     const float4 v = reinterpret_cast<const float4*>(wn)[i / 4];
-                    o[i / 4] = make_float4(fmaf(-2.f, dot[i], nq + v.x), fmaf(-2.f, dot[i + 1], nq + v.y),
-                                           fmaf(-2.f, dot[i + 2], nq + v.z),
-                                           fmaf(-2.f, dot[i + 3], nq + v.w));
+                    av[i] = fmaf(-2.f, dot[i], nq + v.x);
+                    av[i + 1] = fmaf(-2.f, dot[i + 1], nq + v.y);
+                    av[i + 2] = fmaf(-2.f, dot[i + 2], nq + v.z);
+                    av[i + 3] = fmaf(-2.f, dot[i + 3], nq + v.w);
+                    o[i / 4] = make_float4(av[i], av[i + 1], av[i + 2], av[i + 3]);
+                }
+                if (p.dense_gsum) {  // group summary: smallest upper / lower bound of its valid slots
+                    const uint32_t j = j0 + h, og = (d.off + 31u) >> 5;
+                    uint32_t nvalid;
+                    if (j < og) {
+                        nvalid = min(32u, d.off - 32u * j);
+                    } else {
+                        const uint32_t jj = j - og, mid = jj / p.L.gpb, gi = jj - mid * p.L.gpb;
+                        nvalid = min(32u, min(p.L.T, d.len - mid * p.L.T) - 32u * gi);
+                    }
+                    float mh = __int_as_float(0x7f800000), ml = mh;
+#pragma unroll
+                    for (uint32_t n = 0; n < 32; ++n) {
+                        const float e = fmaf(kEpsRel, fabsf(av[n]), fmaf(kEpsT, nq + wn[n], 1e-30f));
+                        if (n < nvalid) {
+                            mh = fminf(mh, av[n] + e);
+                            ml = fminf(ml, av[n] - e);
+                        }
+                    }
+                    p.dense_gsum[qrow / 32u + j] = make_float2(mh, ml);
                 }
             }
         }
@@ -624,13 +650,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 tc_fence_before();
                 named_bar(1 + wg, 128);
                 if (wt == 0) mbar_arrive(a_full);
-                if (p.dense_out && wg == 0 && active && d.chunk == 0) p.dense_nq[pair / p.P] = nq;
+                if (p.dense_out && wg == 0 && active && d.chunk == 0)
+                    p.dense_nq[p.dense_pair_off ? pair : pair / p.P] = nq;
                 for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
                     if ((unit & 1u) != (uint32_t)wg) continue;
                     tc_unit<KT>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
                                 active, nq, ubl, ubk, ncand, overflow, clb, cloc,
                                 scratch + wg * 32 * kM + m, nslots, nfull,
-                                p.qthr + (active ? pair / p.P : 0u), pair / p.P);
+                                p.qthr + (active ? pair / p.P : 0u),
+                                !p.dense_out ? 0ull
+                                : p.dense_pair_off ? (active ? p.dense_pair_off[pair] : 0ull)
+                                                   : (uint64_t)(pair / p.P) * p.dense_ld);
                 }
             }
             // run output: k upper bounds + surviving candidates (compacted in place)
@@ -970,6 +1000,211 @@ __global__ void dense_select_kernel(const float* dense, uint32_t ld, const float
     }
 }
 
+// ---------------------------------------------------------------- dense IVF (k > 32)
+// Group g's global index (norms / rows arrays) of group j of list c.
+__device__ __forceinline__ uint64_t ivf_group_index(const DevLists& L, uint32_t c, uint32_t off,
+                                                    uint32_t j, bool& arena) {
+    const uint32_t og = (off + 31u) >> 5;
+    if (j < og) {
+        arena = false;
+        return L.off_start[c] / 32u + j;
+    }
+    const uint32_t jj = j - og, mid = jj / L.gpb, gi = jj - mid * L.gpb;
+    arena = true;
+    return (uint64_t)L.table[(uint64_t)c * L.MLB + mid] * L.gpb + gi;
+}
+
+// One warp per query over the dense approximate distances of all its probed
+// lists (TC dense mode, rows at pair_off[pair]): (A) a pre-threshold from each
+// lane's 4 smallest upper bounds (the k-th of any 128 values bounds the k-th
+// overall, k <= 128), (B) the exact k-th smallest upper bound, (C) every slot
+// whose lower bound reaches it recomputed EXACTLY (mirror rows, the
+// reference's sequential fp32 bits) into the (dist, id) top-k.
+template <int KPL>
+__global__ void dense_ivf_select_kernel(TcParams p, const long long* probes, float* out_d,
+                                        long long* out_i, uint32_t* out_cnt, uint32_t nq) {
+    extern __shared__ float qsm[];
+    const uint32_t nw = blockDim.x >> 5, wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t q = blockIdx.x * nw + wq;
+    if (q >= nq) return;
+    float* qs = qsm + wq * p.Dp;
+    uint32_t* qc = reinterpret_cast<uint32_t*>(qsm + nw * p.Dp) + wq * 64;
+    uint32_t* ql = qc + 32;
+    for (uint32_t i = lane; i < p.D; i += 32) qs[i] = p.queries[(uint64_t)q * p.Dp + i];
+    __syncwarp();
+    const float inf = __int_as_float(0x7f800000);
+    // the query's groups, a flat index over its probes: lane-strided sweeps read
+    // the (min upper, min lower) group summaries; only groups that can matter
+    // are opened slot by slot
+    auto groups = [&](auto&& f) {  // f(pair, c, j, gflat, summary)
+        for (uint32_t pi = 0; pi < p.P; ++pi) {
+            const uint64_t pair = (uint64_t)q * p.P + pi;
+            const uint32_t c = (uint32_t)probes[pair];
+            const uint32_t ng = ivf_ngroups(p.L, p.snap_off[c], p.snap_len[c]);
+            const uint64_t g0 = p.dense_pair_off[pair] / 32u;
+            for (uint32_t j0 = 0; j0 < ng; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const float2 sm = j < ng ? p.dense_gsum[g0 + j] : make_float2(inf, inf);
+                f(pair, c, j0, j < ng, sm);
+            }
+        }
+    };
+    // open group j0 + src of `pair`: one slot per lane -> (valid, h, l)
+    auto open = [&](uint64_t pair, uint32_t c, uint32_t j, float& h, float& l) -> bool {
+        const uint32_t off = p.snap_off[c], len = p.snap_len[c];
+        bool ar;
+        const uint64_t g = ivf_group_index(p.L, c, off, j, ar);
+        const GroupRef gr = ivf_group(p.L, c, off, len, j);
+        h = inf;
+        l = inf;
+        if (lane < gr.nvalid) {
+            const float a = p.dense_out[p.dense_pair_off[pair] + 32u * j + lane];
+            const float ns = (ar ? p.arena_nrm : p.off_nrm)[g * kNormFloats + lane];
+            const float e = fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, p.dense_nq[pair] + ns, 1e-30f));
+            h = a + e;
+            l = a - e;
+        }
+        return lane < gr.nvalid;
+    };
+    // (A) pre-threshold: the k-th smallest of the group minima (each a real
+    // upper bound of a distinct slot) bounds the k-th smallest upper bound;
+    // each lane keeps its 4 smallest, 128 values sorted across the warp
+    float pre = inf;
+    if (p.k <= 128) {
+        float b[4] = {inf, inf, inf, inf};
+        groups([&](uint64_t, uint32_t, uint32_t, bool valid, float2 sm) {
+            if (!valid) return;
+            float x = sm.x;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float lo = fminf(x, b[i]);
+                x = fmaxf(x, b[i]);
+                b[i] = lo;
+            }
+        });
+        for (uint32_t sz = 2; sz <= 128; sz <<= 1) {
+            for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
+                if (st >= 32) {
+                    const uint32_t rs = st >> 5;
+#pragma unroll
+                    for (uint32_t r = 0; r < 4; ++r) {
+                        if (r & rs) continue;
+                        const uint32_t i = r * 32 + lane;
+                        const bool up = (i & sz) == 0;
+                        const float lo = fminf(b[r], b[r + rs]), hi = fmaxf(b[r], b[r + rs]);
+                        b[r] = up ? lo : hi;
+                        b[r + rs] = up ? hi : lo;
+                    }
+                } else {
+#pragma unroll
+                    for (uint32_t r = 0; r < 4; ++r) {
+                        const float o = __shfl_xor_sync(0xffffffffu, b[r], st);
+                        const uint32_t i = r * 32 + lane;
+                        const bool lower = (lane & st) == 0, up = (i & sz) == 0;
+                        b[r] = (lower == up) ? fminf(b[r], o) : fmaxf(b[r], o);
+                    }
+                }
+            }
+        }
+        const uint32_t kk = p.k - 1;
+        const float cand = kk < 32 ? b[0] : kk < 64 ? b[1] : kk < 96 ? b[2] : b[3];
+        pre = __shfl_sync(0xffffffffu, cand, kk & 31);
+    }
+    // (B) the exact k-th smallest upper bound: open the groups whose minimum
+    // upper bound is <= pre
+    WarpTopK<KPL> th;
+    th.init();
+    groups([&](uint64_t pair, uint32_t c, uint32_t j0, bool valid, float2 sm) {
+        unsigned gm = __ballot_sync(0xffffffffu, valid && sm.x <= pre);
+        while (gm) {
+            const int src = __ffs(gm) - 1;
+            gm &= gm - 1;
+            const uint32_t j = j0 + src;
+            float h, l;
+            const bool ok = open(pair, c, j, h, l);
+            const long long id = (long long)(((pair << 15) | j) << 5 | lane);
+            const bool pass = ok && h <= pre && th.admits(h, id);
+            unsigned m = __ballot_sync(0xffffffffu, pass);
+            while (m) {
+                const int s2 = __ffs(m) - 1;
+                m &= m - 1;
+                const float bh = __shfl_sync(0xffffffffu, h, s2);
+                const long long bi = __shfl_sync(0xffffffffu, id, s2);
+                if (th.admits(bh, bi)) th.insert(bh, bi, (int)p.k, lane);
+            }
+        }
+    });
+    const float theta = fminf(th.thr_d, pre);
+    // (C) exact top-k over the candidates (groups whose minimum lower bound
+    // reaches theta, then their slots), recomputed 32 at a time
+    WarpTopK<KPL> tk;
+    tk.init();
+    uint32_t qn = 0;
+    auto flush = [&]() {
+        const bool ok = lane < qn;
+        float dist = 0.f;
+        long long id = -1;
+        if (ok) {
+            const uint32_t c = qc[lane], loc = ql[lane];
+            const GroupRef g = ivf_group(p.L, c, p.snap_off[c], p.snap_len[c], loc >> 5);
+            dist = exact_l2_row(qs, cand_row(p, c, p.snap_off[c], loc >> 5, loc & 31), p.D);
+            id = g.ids[loc & 31];
+        }
+        const bool pass = ok && tk.admits(dist, id);
+        unsigned m = __ballot_sync(0xffffffffu, pass);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const float bd = __shfl_sync(0xffffffffu, dist, src);
+            const long long bi = __shfl_sync(0xffffffffu, id, src);
+            if (tk.admits(bd, bi)) tk.insert(bd, bi, (int)p.k, lane);
+        }
+        qn = 0;
+        __syncwarp();
+    };
+    groups([&](uint64_t pair, uint32_t c, uint32_t j0, bool valid, float2 sm) {
+        unsigned gm = __ballot_sync(0xffffffffu, valid && sm.y <= theta);
+        while (gm) {
+            const int src = __ffs(gm) - 1;
+            gm &= gm - 1;
+            const uint32_t j = j0 + src;
+            float h, l;
+            const bool cand = open(pair, c, j, h, l) && l <= theta;
+            const unsigned msk = __ballot_sync(0xffffffffu, cand);
+            const uint32_t np = __popc(msk);
+            if (!np) continue;
+            if (qn + np > 32) flush();
+            if (cand) {
+                const uint32_t slot = qn + __popc(msk & ((1u << lane) - 1u));
+                qc[slot] = c;
+                ql[slot] = (j << 5) | lane;
+            }
+            qn += np;
+            __syncwarp();
+        }
+    });
+    if (qn) flush();
+    uint32_t cntq = 0;
+#pragma unroll
+    for (int r = 0; r < KPL; ++r) {
+        const uint32_t e = r * 32 + lane;
+        cntq += __popc(__ballot_sync(0xffffffffu, e < p.k && tk.id[r] >= 0));
+        if (e < p.k) {
+            out_d[(uint64_t)q * p.k + e] = tk.d[r];
+            out_i[(uint64_t)q * p.k + e] = tk.id[r];
+        }
+    }
+    if (lane == 0 && out_cnt) out_cnt[q] = cntq;
+}
+
+__global__ void dense_pair_len_kernel(DevLists L, const long long* probes, const uint32_t* snap_off,
+                                      const uint32_t* snap_len, uint32_t npairs, uint64_t* len) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npairs) return;
+    const uint32_t c = (uint32_t)probes[i];
+    len[i] = 32ull * ivf_ngroups(L, snap_off[c], snap_len[c]);
+}
+
 template <int KT>
 size_t tc_smem_bytes() {
     return 1024 + TcCfg<KT>::NS * kStage + kWG * 32 * kM * 4 + kWG * TcCfg<KT>::KC * kM * 8 +
@@ -998,6 +1233,10 @@ bool tc_supported(uint32_t D, uint32_t k, int metric) {
     return metric == kL2 && D >= 8 && D <= (uint32_t)kMaxD && k <= 32;
 }
 
+bool tc_dense_supported(uint32_t D, uint32_t k, int metric) {
+    return metric == kL2 && D >= 8 && D <= (uint32_t)kMaxD && k > 32 && k <= 256;
+}
+
 cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUtensorMap* out) {
     auto enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
@@ -1013,6 +1252,37 @@ cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUte
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+namespace {
+__global__ void dense_total_kernel(const uint64_t* off, const uint64_t* len, uint32_t n,
+                                   uint64_t* total) {
+    *total = n ? off[n - 1] + len[n - 1] : 0;
+}
+}  // namespace
+
+size_t dense_plan_tmp_bytes(uint32_t npairs) {
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<const uint64_t*>(nullptr),
+                                  static_cast<uint64_t*>(nullptr), (int)npairs);
+    return b;
+}
+
+cudaError_t launch_dense_plan(const DevLists& L, const PlanBufs& B, const long long* probes,
+                              const SearchShape& sh, uint64_t* pair_len, uint64_t* pair_off,
+                              void* tmp, size_t tmp_bytes, uint64_t* total, cudaStream_t s) {
+    SearchShape s2 = sh;
+    s2.QT = kM;
+    cudaError_t e = launch_plan(L, B, probes, s2, s);
+    if (e != cudaSuccess) return e;
+    const uint32_t npairs = sh.nq * sh.P;
+    dense_pair_len_kernel<<<(npairs + 255) / 256, 256, 0, s>>>(L, probes, B.snap_off, B.snap_len,
+                                                               npairs, pair_len);
+    e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, pair_len, pair_off, (int)npairs, s);
+    if (e != cudaSuccess) return e;
+    dense_total_kernel<<<1, 1, 0, s>>>(pair_off, pair_len, npairs, total);
+    count_launch(3);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,
                                  const float* queries, const float* centroids,
                                  const SearchShape& sh, const CUtensorMap& map_off,
@@ -1025,8 +1295,11 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     if (sh.nq == 0) return cudaSuccess;
     SearchShape s2 = sh;
     s2.QT = kM;
-    cudaError_t e = launch_plan(L, B, probes, s2, s);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
+    if (!(dense && dense->pair_off)) {  // the IVF dense path planned in launch_dense_plan
+        e = launch_plan(L, B, probes, s2, s);
+        if (e != cudaSuccess) return e;
+    }
     TcParams p{};
     p.L = L;
     p.D = L.D;
@@ -1054,6 +1327,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
         p.dense_out = dense->out;
         p.dense_nq = dense->nq;
         p.dense_ld = dense->ld;
+        p.dense_pair_off = dense->pair_off;
+        p.dense_gsum = dense->gsum;
     }
     p.arena_nrm = arena_nrm;
     p.ub = T.ub;
@@ -1084,7 +1359,21 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     if (e != cudaSuccess) return e;
     if (ev1) cudaEventRecord(ev1, s);
     const uint32_t wpb = 4;
-    if (dense) {
+    if (dense && dense->pair_off) {
+        const size_t sm_sel = wpb * (p.Dp * 4 + 256);
+        if (sh.k <= 32)
+            dense_ivf_select_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
+                p, probes, out_d, out_i, out_cnt, sh.nq);
+        else if (sh.k <= 64)
+            dense_ivf_select_kernel<2><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
+                p, probes, out_d, out_i, out_cnt, sh.nq);
+        else if (sh.k <= 128)
+            dense_ivf_select_kernel<4><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
+                p, probes, out_d, out_i, out_cnt, sh.nq);
+        else
+            dense_ivf_select_kernel<8><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
+                p, probes, out_d, out_i, out_cnt, sh.nq);
+    } else if (dense) {
         const uint32_t n = dense->n;
         const size_t sm_sel = wpb * (p.Dp * 4 + 128);
         if (sh.k <= 32)

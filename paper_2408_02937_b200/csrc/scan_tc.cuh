@@ -26,6 +26,7 @@ struct TcBufs {
 };
 
 bool tc_supported(uint32_t D, uint32_t k, int metric);
+bool tc_dense_supported(uint32_t D, uint32_t k, int metric);
 
 // Dense mode of the TC scan (coarse quantizer): the single list's n slots,
 // approximate distances -> out[nq][ld], query norms -> nq; the selection
@@ -34,7 +35,17 @@ struct TcDense {
     float* out;
     float* nq;
     uint32_t ld, n;
+    const uint64_t* pair_off = nullptr;  // IVF dense mode (k > 32): per-pair row offsets
+    float2* gsum = nullptr;              // IVF dense mode: per-(pair, group) bound minima
 };
+
+// IVF dense mode (k > 32, exact top-k through the TC distances): plan + per-pair
+// row lengths (32 * groups of the probed list) + exclusive scan; *total (device)
+// = floats the dense rows need.
+size_t dense_plan_tmp_bytes(uint32_t npairs);
+cudaError_t launch_dense_plan(const DevLists& L, const PlanBufs& B, const long long* probes,
+                              const SearchShape& sh, uint64_t* pair_len, uint64_t* pair_off,
+                              void* tmp, size_t tmp_bytes, uint64_t* total, cudaStream_t s);
 
 // 2-D TMA map over a scan mirror region (mirror.cuh: `groups` groups of
 // 2K rows of 32 floats), box = {32, 2K}, SWIZZLE_128B_ATOM_32B.

@@ -1,6 +1,7 @@
-"""The tensor-core filtered scan (tcgen05 TF32 filter + exact refine) returns
-exactly the CUDA-core exact scan's and the oracle's results: same ids, same
-distance bits, at small and cfg2-like scale, with live inserts and deletes."""
+"""The tensor-core filtered scan (tcgen05 TF32 filter + exact refine; k > 32:
+dense TC distances + per-query exact selection) returns exactly the CUDA-core
+exact scan's and the oracle's results: same ids, same distance bits, at small
+and cfg2-like scale, with live inserts and deletes."""
 import numpy as np
 import pytest
 
@@ -46,7 +47,8 @@ def test_tc_equals_exact_and_oracle(gpu_ready, D, C, T, n, comps):
     ix.insert(extra)
     orc.insert(extra)
     q = bivf.synthetic_dataset(300, D, comps, 5)
-    for k, npb in ((1, 1), (10, min(4, C)), (32, min(8, C)), (10, C)):
+    for k, npb in ((1, 1), (10, min(4, C)), (32, min(8, C)), (10, C), (33, min(4, C)),
+                   (100, min(8, C)), (256, C)):
         a, b = both(ix, q, k, npb)
         assert_same(a, b)
         for j in range(0, 300, 37):
@@ -65,7 +67,7 @@ def test_tc_sift_like_scale(gpu_ready):
     ix.insert(x[200_000:210_000])
     ix.remove(np.arange(0, 200_000, 97))
     q = x[210_000:]
-    for k, npb in ((10, 16), (10, 1), (32, 32)):
+    for k, npb in ((10, 16), (10, 1), (32, 32), (100, 16)):
         a, b = both(ix, q, k, npb)
         assert_same(a, b)
     # small request shape (latency path): 10 queries
@@ -101,7 +103,7 @@ def test_tc_after_rearrange_and_delete(gpu_ready):
     assert events > 0, "the scenario must exercise rearrangement"
     assert ix.layout() == orc.layout()
     q = bivf.synthetic_dataset(200, D, 40, 77)
-    for k, npb in ((10, 4), (16, 8), (32, C)):
+    for k, npb in ((10, 4), (16, 8), (32, C), (64, 8), (128, C)):
         a, b = both(ix, q, k, npb)
         assert_same(a, b)
         for j in range(0, 200, 23):
@@ -118,7 +120,9 @@ def test_tc_quantizer_matches_exact(gpu_ready, C, D):
     ix = ClusterIndex.empty(D, C, block_capacity=64, num_blocks=64)
     ix.set_centroids(cent)
     q = x[20 * C:]
-    for P in (1, 7, 32):
+    for P in (1, 7, 32, 64, 100):
+        if P >= C:
+            continue
         ix.set_scan_mode("cuda")
         a = ix.probes(q, P)
         ix.set_scan_mode("auto")
@@ -130,4 +134,4 @@ def test_tc_quantizer_matches_exact(gpu_ready, C, D):
         for d in range(D):
             t = (q[j, d] - cent[:, d]).astype(np.float32)
             acc = (acc + (t * t).astype(np.float32)).astype(np.float32)
-        assert np.array_equal(b[j], np.lexsort((np.arange(C), acc))[:32])
+        assert np.array_equal(b[j], np.lexsort((np.arange(C), acc))[: b.shape[1]])
