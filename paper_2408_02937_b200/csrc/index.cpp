@@ -821,9 +821,9 @@ void GpuIndex::enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Works
         // top-k (scan_tc.cu dense_ivf_select_kernel).  The rows' total size is
         // read back once (one stream sync) to size the lease's dense buffer.
         const uint32_t npairs = nq * P;
-        const size_t tmpb = dense_plan_tmp_bytes(npairs);
-        const size_t o_len = 0, o_off = align_up((size_t)npairs * 8),
-                     o_nq = o_off + align_up((size_t)npairs * 8),
+        const size_t tmpb = dense_plan_tmp_bytes(C_);
+        const size_t o_len = 0, o_off = align_up((size_t)C_ * 8),
+                     o_nq = o_off + align_up((size_t)C_ * 8),
                      o_tot = o_nq + align_up((size_t)npairs * 4), o_tmp = o_tot + 256;
         if (o_tmp + tmpb > l.dense_aux.bytes) BIVF_CUDA(cudaStreamSynchronize(l.stream));
         l.dense_aux.ensure(o_tmp + tmpb);

@@ -86,7 +86,10 @@ struct TcParams {
     float* dense_out;
     float* dense_nq;
     uint32_t dense_ld;
-    const uint64_t* dense_pair_off;  // IVF dense mode (k > 32): row of pair i at dense_pair_off[i]
+    // IVF dense mode (k > 32): list c's tiles start at dense_list_base[c]; tile t of a
+    // list with ng groups holds [ng][32 slots][128 tile rows] (warp-coalesced writes)
+    const uint64_t* dense_list_base;
+    const uint32_t* dense_ppos;      // the plan's per-pair position in its list
     float2* dense_gsum;              // IVF dense mode: per (pair, group) (min upper, min lower bound)
     const float* off_rows;      // mirror rows (mirror.cuh): slot-major exact payload copy
     const float* arena_rows;
@@ -377,7 +380,7 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                                         float (&ubl)[KT], float& ubk, uint32_t& ncand,
                                         bool& overflow, float* clb, uint32_t* cloc,
                                         float* scr, float* nslots, uint64_t* nfull, float* qt,
-                                        uint64_t qrow) {
+                                        uint64_t qrow, uint32_t m) {
     const uint32_t b = u % kNB;
     // the query's shared threshold: the smallest k-th upper bound any of its runs
     // has published (a valid filter bound for every run of the query)
@@ -393,7 +396,6 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
             tmem_ld32(tmem_base + taddr_lane + kColAcc + b * 32 * kGU + 32 * h, dot);
             const float* wn = nslots + (b * kGU + h) * kNormFloats;
             if (active) {
-                float4* o = reinterpret_cast<float4*>(p.dense_out + qrow + 32u * (j0 + h));
                 float av[32];
 #pragma unroll
                 for (int i = 0; i < 32; i += 4) {
@@ -402,7 +404,15 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                     av[i + 1] = fmaf(-2.f, dot[i + 1], nq + v.y);
                     av[i + 2] = fmaf(-2.f, dot[i + 2], nq + v.z);
                     av[i + 3] = fmaf(-2.f, dot[i + 3], nq + v.w);
-                    o[i / 4] = make_float4(av[i], av[i + 1], av[i + 2], av[i + 3]);
+                }
+                if (p.dense_list_base) {  // IVF: element (j, n) at base + (32 j + n) * 128
+                    float* o = p.dense_out + qrow + (uint64_t)(32u * (j0 + h)) * kM;
+#pragma unroll
+                    for (int n = 0; n < 32; ++n) o[(uint64_t)n * kM] = av[n];
+                } else {  // quantizer: one contiguous row per query
+                    float4* o = reinterpret_cast<float4*>(p.dense_out + qrow + 32u * (j0 + h));
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) o[i / 4] = make_float4(av[i], av[i + 1], av[i + 2], av[i + 3]);
                 }
                 if (p.dense_gsum) {  // group summary: smallest upper / lower bound of its valid slots
                     const uint32_t j = j0 + h, og = (d.off + 31u) >> 5;
@@ -422,7 +432,9 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                             ml = fminf(ml, av[n] - e);
                         }
                     }
-                    p.dense_gsum[qrow / 32u + j] = make_float2(mh, ml);
+                    // summaries [tile][row m][group j]: the selection reads a row's groups contiguously
+                    const uint32_t ngl = ivf_ngroups(p.L, d.off, d.len);
+                    p.dense_gsum[(qrow - m) / 32u + (uint64_t)m * ngl + j] = make_float2(mh, ml);
                 }
             }
         }
@@ -651,16 +663,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 named_bar(1 + wg, 128);
                 if (wt == 0) mbar_arrive(a_full);
                 if (p.dense_out && wg == 0 && active && d.chunk == 0)
-                    p.dense_nq[p.dense_pair_off ? pair : pair / p.P] = nq;
+                    p.dense_nq[p.dense_list_base ? pair : pair / p.P] = nq;
+                uint64_t dbase = 0;  // dense mode: this thread's base element
+                if (p.dense_out) {
+                    if (p.dense_list_base) {
+                        const uint32_t tile = (uint32_t)((d.pairs - p.plist) - p.qoff[d.c]) / kM;
+                        const uint32_t ngl = ivf_ngroups(p.L, d.off, d.len);
+                        dbase = p.dense_list_base[d.c] + (uint64_t)tile * ngl * 32u * kM + m;
+                    } else {
+                        dbase = (uint64_t)(pair / p.P) * p.dense_ld;
+                    }
+                }
                 for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
                     if ((unit & 1u) != (uint32_t)wg) continue;
                     tc_unit<KT>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
                                 active, nq, ubl, ubk, ncand, overflow, clb, cloc,
                                 scratch + wg * 32 * kM + m, nslots, nfull,
                                 p.qthr + (active ? pair / p.P : 0u),
-                                !p.dense_out ? 0ull
-                                : p.dense_pair_off ? (active ? p.dense_pair_off[pair] : 0ull)
-                                                   : (uint64_t)(pair / p.P) * p.dense_ld);
+                                dbase, (uint32_t)m);
                 }
             }
             // run output: k upper bounds + surviving candidates (compacted in place)
@@ -1015,7 +1035,7 @@ __device__ __forceinline__ uint64_t ivf_group_index(const DevLists& L, uint32_t 
 }
 
 // One warp per query over the dense approximate distances of all its probed
-// lists (TC dense mode, rows at pair_off[pair]): (A) a pre-threshold from each
+// lists (TC dense mode, tiled rows at dense_list_base): (A) a pre-threshold from each
 // lane's 4 smallest upper bounds (the k-th of any 128 values bounds the k-th
 // overall, k <= 128), (B) the exact k-th smallest upper bound, (C) every slot
 // whose lower bound reaches it recomputed EXACTLY (mirror rows, the
@@ -1041,7 +1061,9 @@ __global__ void dense_ivf_select_kernel(TcParams p, const long long* probes, flo
             const uint64_t pair = (uint64_t)q * p.P + pi;
             const uint32_t c = (uint32_t)probes[pair];
             const uint32_t ng = ivf_ngroups(p.L, p.snap_off[c], p.snap_len[c]);
-            const uint64_t g0 = p.dense_pair_off[pair] / 32u;
+            const uint32_t pos = p.dense_ppos[pair], m = pos % kM;
+            const uint64_t blk = p.dense_list_base[c] + (uint64_t)(pos / kM) * ng * 32u * kM;
+            const uint64_t g0 = blk / 32u + (uint64_t)m * ng;
             for (uint32_t j0 = 0; j0 < ng; j0 += 32) {
                 const uint32_t j = j0 + lane;
                 const float2 sm = j < ng ? p.dense_gsum[g0 + j] : make_float2(inf, inf);
@@ -1058,7 +1080,10 @@ __global__ void dense_ivf_select_kernel(TcParams p, const long long* probes, flo
         h = inf;
         l = inf;
         if (lane < gr.nvalid) {
-            const float a = p.dense_out[p.dense_pair_off[pair] + 32u * j + lane];
+            const uint32_t pos = p.dense_ppos[pair];
+            const uint32_t ngl = ivf_ngroups(p.L, off, len);
+            const uint64_t blk = p.dense_list_base[c] + (uint64_t)(pos / kM) * ngl * 32u * kM;
+            const float a = p.dense_out[blk + (uint64_t)(32u * j + lane) * kM + pos % kM];
             const float ns = (ar ? p.arena_nrm : p.off_nrm)[g * kNormFloats + lane];
             const float e = fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, p.dense_nq[pair] + ns, 1e-30f));
             h = a + e;
@@ -1197,12 +1222,12 @@ __global__ void dense_ivf_select_kernel(TcParams p, const long long* probes, flo
     if (lane == 0 && out_cnt) out_cnt[q] = cntq;
 }
 
-__global__ void dense_pair_len_kernel(DevLists L, const long long* probes, const uint32_t* snap_off,
-                                      const uint32_t* snap_len, uint32_t npairs, uint64_t* len) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= npairs) return;
-    const uint32_t c = (uint32_t)probes[i];
-    len[i] = 32ull * ivf_ngroups(L, snap_off[c], snap_len[c]);
+__global__ void dense_list_len_kernel(DevLists L, const uint32_t* snap_off, const uint32_t* snap_len,
+                                      const uint32_t* qoff, uint32_t C, uint64_t* len) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const uint64_t tiles = (qoff[c + 1] - qoff[c] + kM - 1) / kM;
+    len[c] = tiles * ivf_ngroups(L, snap_off[c], snap_len[c]) * 32ull * kM;
 }
 
 template <int KT>
@@ -1259,26 +1284,25 @@ __global__ void dense_total_kernel(const uint64_t* off, const uint64_t* len, uin
 }
 }  // namespace
 
-size_t dense_plan_tmp_bytes(uint32_t npairs) {
+size_t dense_plan_tmp_bytes(uint32_t nlists) {
     size_t b = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<const uint64_t*>(nullptr),
-                                  static_cast<uint64_t*>(nullptr), (int)npairs);
+                                  static_cast<uint64_t*>(nullptr), (int)nlists);
     return b;
 }
 
 cudaError_t launch_dense_plan(const DevLists& L, const PlanBufs& B, const long long* probes,
-                              const SearchShape& sh, uint64_t* pair_len, uint64_t* pair_off,
+                              const SearchShape& sh, uint64_t* list_len, uint64_t* list_base,
                               void* tmp, size_t tmp_bytes, uint64_t* total, cudaStream_t s) {
     SearchShape s2 = sh;
     s2.QT = kM;
     cudaError_t e = launch_plan(L, B, probes, s2, s);
     if (e != cudaSuccess) return e;
-    const uint32_t npairs = sh.nq * sh.P;
-    dense_pair_len_kernel<<<(npairs + 255) / 256, 256, 0, s>>>(L, probes, B.snap_off, B.snap_len,
-                                                               npairs, pair_len);
-    e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, pair_len, pair_off, (int)npairs, s);
+    dense_list_len_kernel<<<(L.C + 255) / 256, 256, 0, s>>>(L, B.snap_off, B.snap_len, B.qoff, L.C,
+                                                            list_len);
+    e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, list_len, list_base, (int)L.C, s);
     if (e != cudaSuccess) return e;
-    dense_total_kernel<<<1, 1, 0, s>>>(pair_off, pair_len, npairs, total);
+    dense_total_kernel<<<1, 1, 0, s>>>(list_base, list_len, L.C, total);
     count_launch(3);
     return cudaGetLastError();
 }
@@ -1296,7 +1320,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     SearchShape s2 = sh;
     s2.QT = kM;
     cudaError_t e = cudaSuccess;
-    if (!(dense && dense->pair_off)) {  // the IVF dense path planned in launch_dense_plan
+    if (!(dense && dense->list_base)) {  // the IVF dense path planned in launch_dense_plan
         e = launch_plan(L, B, probes, s2, s);
         if (e != cudaSuccess) return e;
     }
@@ -1327,7 +1351,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
         p.dense_out = dense->out;
         p.dense_nq = dense->nq;
         p.dense_ld = dense->ld;
-        p.dense_pair_off = dense->pair_off;
+        p.dense_list_base = dense->list_base;
+        p.dense_ppos = B.ppos;
         p.dense_gsum = dense->gsum;
     }
     p.arena_nrm = arena_nrm;
@@ -1359,7 +1384,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     if (e != cudaSuccess) return e;
     if (ev1) cudaEventRecord(ev1, s);
     const uint32_t wpb = 4;
-    if (dense && dense->pair_off) {
+    if (dense && dense->list_base) {
         const size_t sm_sel = wpb * (p.Dp * 4 + 256);
         if (sh.k <= 32)
             dense_ivf_select_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(

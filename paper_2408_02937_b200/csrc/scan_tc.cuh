@@ -35,16 +35,16 @@ struct TcDense {
     float* out;
     float* nq;
     uint32_t ld, n;
-    const uint64_t* pair_off = nullptr;  // IVF dense mode (k > 32): per-pair row offsets
-    float2* gsum = nullptr;              // IVF dense mode: per-(pair, group) bound minima
+    const uint64_t* list_base = nullptr;  // IVF dense mode (k > 32): per-list tile block offsets
+    float2* gsum = nullptr;               // IVF dense mode: per-(pair, group) bound minima
 };
 
-// IVF dense mode (k > 32, exact top-k through the TC distances): plan + per-pair
-// row lengths (32 * groups of the probed list) + exclusive scan; *total (device)
-// = floats the dense rows need.
-size_t dense_plan_tmp_bytes(uint32_t npairs);
+// IVF dense mode (k > 32, exact top-k through the TC distances): plan + per-list
+// tile-block sizes (tiles x groups x 32 slots x 128 rows) + exclusive scan;
+// *total (device) = floats the dense blocks need.
+size_t dense_plan_tmp_bytes(uint32_t nlists);
 cudaError_t launch_dense_plan(const DevLists& L, const PlanBufs& B, const long long* probes,
-                              const SearchShape& sh, uint64_t* pair_len, uint64_t* pair_off,
+                              const SearchShape& sh, uint64_t* list_len, uint64_t* list_base,
                               void* tmp, size_t tmp_bytes, uint64_t* total, cudaStream_t s);
 
 // 2-D TMA map over a scan mirror region (mirror.cuh: `groups` groups of

@@ -12,7 +12,8 @@ where they apply.
         delete (3.3K ids/s) + search with in-place rearrangement sweeps
   cfg4s one shard (id mod 8 == 0) of IVF-Flat 100M x 128 (mixture: 65536 centres
         U(0,100)^128, sigma 3, SIFT-like rounding), nlist 16384, nprobe 64, k 100
-        (k > 32: the exact CUDA-core scan), i.e. what one of 8 B200s serves
+        (k > 32: tensor-core dense distances + exact selection), i.e. what one of
+        8 B200s serves
   cfg5  IVF-Flat 20M x 768 inner product (32768 unit centres, x = normalize(u +
         0.5 N(0,1)/sqrt(768))), nlist 4096, nprobe 32, k 10, 10K vec/s live inserts
         (IP: the exact CUDA-core scan)
@@ -243,8 +244,9 @@ def run(args):
                 "h2d_bytes_per_step": BATCH * D * 4, "d2h_bytes_per_step": BATCH * K * 12 + BATCH * 4},
         "phase_ms": {"quantizer": round(phm[0], 3), "plan": round(phm[1], 3), "scan": round(phm[2], 3),
                      "merge_or_refine": round(phm[3], 3)},
-        "scan_path": "tensor-core filter + exact refine" if (c["metric"] == 0 and D <= 128 and K <= 32)
-        else "CUDA-core exact scan",
+        "scan_path": ("tensor-core filter + exact refine" if K <= 32 else
+                      "tensor-core dense distances + exact selection")
+        if (c["metric"] == 0 and 8 <= D <= 128 and K <= 256) else "CUDA-core exact scan",
         "gpu_launches": int(launches),
     }
     if th is not None:

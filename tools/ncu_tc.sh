@@ -5,7 +5,7 @@
 # skipped, the second search's 4 captured.
 tag=${1:-r01}
 PROF_REPS=2 timeout -s KILL 600 ncu --set full --clock-control none --import-source on \
-  -k "regex:scan_tc_kernel|refine_kernel|dense_select" -s 4 -c 4 -o gpurun_out/prof_tc_$tag \
+  -k "regex:scan_tc_kernel|refine_kernel|dense_" -s 4 -c 4 -o gpurun_out/prof_tc_$tag \
   python tools/prof_scan.py > gpurun_out/ncu_tc_$tag.log 2>&1
 echo "ncu tc rc=$?"
 tail -2 gpurun_out/ncu_tc_$tag.log
