@@ -804,6 +804,13 @@ void GpuIndex::enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Works
     ss.k = k;
     ss.P = P;
     ss.maxch = sh.maxch;
+    if (use_tc(k)) {
+        // TC filter: a chunk is cheap to scan but every (pair, chunk) run is merged by
+        // the refine's one warp per query, so keep ~2 work items per SM, not 8
+        const uint64_t npairs = (uint64_t)nq * P;
+        ss.maxch = (uint32_t)std::min<uint64_t>(
+            ss.maxch, std::max<uint64_t>(1, (2ull * num_sms_ + npairs - 1) / npairs));
+    }
     ss.gcmin = sh.gcmin;
     ss.QT = qt_for(k, D_);
     ss.metric = cfg_.metric;

@@ -845,42 +845,58 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
         qn = 0;
         __syncwarp();
     };
-    for (uint32_t pi = 0; pi < p.P; ++pi) {
-        const uint32_t c = (uint32_t)probes[(uint64_t)q * p.P + pi];
-        const uint32_t n = p.nch[c];
-        const uint32_t off = p.snap_off[c], len = p.snap_len[c];
-        for (uint32_t h = 0; h < n; ++h) {
-            const uint64_t run0 = ((((uint64_t)q * p.P + pi) * p.maxch + h) << 1);
-            const uint32_t cnt0 = p.ccount[run0], cnt1 = p.ccount[run0 + 1];
-            if (cnt0 != kOverflow && cnt1 != kOverflow) {
-                for (uint32_t w = 0; w < 2; ++w) {
-                    const uint64_t run = run0 + w;
-                    const uint32_t cnt = w ? cnt1 : cnt0;
-                    for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
-                        const uint32_t e = c0 + lane;
-                        const bool pass = e < cnt && p.clb[run * kKC + e] <= theta;
-                        const unsigned msk = __ballot_sync(0xffffffffu, pass);
-                        const uint32_t np = __popc(msk);
-                        if (qn + np > 32) flush();
-                        if (pass) {
-                            const uint32_t slot = qn + __popc(msk & ((1u << lane) - 1u));
-                            qc[slot] = c;
-                            ql[slot] = p.cloc[run * kKC + e];
-                        }
-                        qn += np;
-                        __syncwarp();
-                    }
-                }
-            } else {  // overflow: exact rescan of the chunk
-                const uint32_t ng = ivf_ngroups(p.L, off, len);
-                const uint32_t g0 = h * p.gc[c], g1 = min(ng, g0 + p.gc[c]);
-                for (uint32_t j = g0; j < g1; ++j) {
-                    const GroupRef g = ivf_group(p.L, c, off, len, j);
-                    const bool ok = lane < g.nvalid;
-                    const float dist = exact_l2(qs, g.base + lane, p.D);
-                    offer(dist, ok ? g.ids[lane] : -1, ok);
-                }
+    // 2b. candidates, 32 runs at a time (lane = run of the contiguous block
+    // [P][maxch][2]): counts and candidate loads are independent across lanes,
+    // so small batches with many chunks per list do not serialise on latency
+    const uint32_t nruns = p.P * p.maxch * 2u;
+    const uint64_t rbase = (uint64_t)q * nruns;
+    for (uint32_t r0 = 0; r0 < nruns; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        uint32_t c = 0, cnt = 0, h = 0;
+        bool valid = false;
+        if (r < nruns) {
+            const uint32_t pi = r / (p.maxch * 2u);
+            h = (r >> 1) - pi * p.maxch;
+            c = (uint32_t)probes[(uint64_t)q * p.P + pi];
+            valid = h < p.nch[c];
+            if (valid) cnt = p.ccount[rbase + r];
+        }
+        // a chunk whose candidate buffer overflowed in either warpgroup run is rescanned
+        const uint32_t pcnt = __shfl_xor_sync(0xffffffffu, cnt, 1);
+        const bool ovf = valid && (cnt == kOverflow || pcnt == kOverflow);
+        unsigned om = __ballot_sync(0xffffffffu, ovf && (r & 1u) == 0);
+        while (om) {
+            const int src = __ffs(om) - 1;
+            om &= om - 1;
+            const uint32_t cc = __shfl_sync(0xffffffffu, c, src);
+            const uint32_t hh = __shfl_sync(0xffffffffu, h, src);
+            const uint32_t off = p.snap_off[cc], len = p.snap_len[cc];
+            const uint32_t ng = ivf_ngroups(p.L, off, len);
+            const uint32_t g0 = hh * p.gc[cc], g1 = min(ng, g0 + p.gc[cc]);
+            for (uint32_t j = g0; j < g1; ++j) {
+                const GroupRef g = ivf_group(p.L, cc, off, len, j);
+                const bool ok = lane < g.nvalid;
+                const float dist = exact_l2(qs, g.base + lane, p.D);
+                offer(dist, ok ? g.ids[lane] : -1, ok);
             }
+        }
+        const uint32_t mycnt = (valid && !ovf) ? cnt : 0u;
+        uint32_t mx = mycnt;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        for (uint32_t e = 0; e < mx; ++e) {
+            const bool pass = e < mycnt && p.clb[(rbase + r) * kKC + e] <= theta;
+            const unsigned msk = __ballot_sync(0xffffffffu, pass);
+            const uint32_t np = __popc(msk);
+            if (!np) continue;
+            if (qn + np > 32) flush();
+            if (pass) {
+                const uint32_t slot = qn + __popc(msk & ((1u << lane) - 1u));
+                qc[slot] = c;
+                ql[slot] = p.cloc[(rbase + r) * kKC + e];
+            }
+            qn += np;
+            __syncwarp();
         }
     }
     if (qn) flush();
