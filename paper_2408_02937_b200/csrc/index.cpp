@@ -171,7 +171,16 @@ GpuIndex::GpuIndex(const bivf_config& in) : cfg_(normalized(in)) {
     // every host<->device copy/memset of the index goes through data_stream_
     // (h2d/d2h/dset): the legacy stream does not order against the index's
     // non-blocking streams, and a pageable cudaMemcpy may return before its DMA lands.
-    BIVF_CUDA(cudaStreamCreateWithFlags(&data_stream_, cudaStreamNonBlocking));
+    {
+        // searches run on high-priority lease streams, the data lane (inserts,
+        // maintenance) on the lowest priority: pending search blocks are
+        // dispatched first when both contend for SMs
+        int lo = 0, hi = 0;
+        BIVF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        prio_hi_ = hi;
+        BIVF_CUDA(cudaStreamCreateWithPriority(&data_stream_, cudaStreamNonBlocking, lo));
+        data_lease_.stream = data_stream_;
+    }
     alloc_device();
     BIVF_CUDA(cudaEventCreateWithFlags(&maint_evt_, cudaEventDisableTiming));
     for (uint32_t i = 0; i < cfg_.num_leases; ++i) {
@@ -448,12 +457,16 @@ void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32
             qs.metric = cfg_.metric;
             TcDense dn{w.qdense, w.qdense_nq, ld, C_};
             const size_t g0 = (size_t)qbase + q0;
+            // work items = tiles x chunks (the centroid list has no online part)
+            const uint32_t ngq = ceil_div(C_, 32);
+            const uint32_t gcq = std::max(2u, ceil_div(ngq, qs.maxch));
+            const int items = (int)(ceil_div(m, 128) * ceil_div(ngq, gcq));
             BIVF_CUDA(launch_ivf_search_tc(quantizer_lists(), w.plan, d_q_zero_.as<long long>(),
                                            w.queries + g0 * Dp_, d_q_mu_.as<float>(), qs,
                                            map_q_, map_q_, d_q_nrm_.as<float>(), nullptr,
                                            d_cent_.as<float>(), nullptr, w.tc, &dn,
                                            w.pdist + g0 * P, w.probes + g0 * P,
-                                           nullptr, num_sms_, s));
+                                           nullptr, num_sms_, s, nullptr, nullptr, items));
         }
     } else {
         BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, w.queries + (size_t)qbase * Dp_,
@@ -630,7 +643,8 @@ Lease* GpuIndex::acquire_lease() {
                 l->busy = true;
                 if (!l->stream) {
                     BIVF_CUDA(cudaSetDevice(device_));
-                    BIVF_CUDA(cudaStreamCreateWithFlags(&l->stream, cudaStreamNonBlocking));
+                    BIVF_CUDA(cudaStreamCreateWithPriority(&l->stream, cudaStreamNonBlocking,
+                                                           prio_hi_));
                     BIVF_CUDA(cudaEventCreateWithFlags(&l->done, cudaEventDisableTiming));
                     for (cudaEvent_t* e : {&l->t0, &l->t1, &l->t2, &l->t3, &l->t4})
                         BIVF_CUDA(cudaEventCreate(e));
@@ -1104,15 +1118,24 @@ uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_
         cudaStream_t st = data_stream_;
         BIVF_CUDA(cudaMemcpyAsync(d_x_.p, px, (size_t)m * D_ * 4, cudaMemcpyHostToDevice, st));
         BIVF_CUDA(cudaMemcpyAsync(d_ids_.p, pid, (size_t)m * 8, cudaMemcpyHostToDevice, st));
-        // assign (ivf_index.cpp:93-105) = quantizer top-1 on device
-        BIVF_CUDA(launch_pad_rows(d_x_.as<float>(), m, D_, Dp_, d_qtmp_.as<float>(), st));
-        BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, d_qtmp_.as<float>(), m, 1,
-                                   cfg_.metric, sh.fnch, d_fc_d_.as<float>(),
-                                   d_fc_i_.as<long long>(), d_fo_d_.as<float>(),
-                                   d_fo_i_.as<long long>(), nullptr, d_ctr_.as<uint32_t>(),
-                                   num_sms_, st));
-        BIVF_CUDA(launch_make_asg(d_fo_i_.as<long long>(), d_ids_.as<long long>(), m,
-                                  d_asg_.as<uint32_t>(), st));
+        // assign (ivf_index.cpp:93-105) = quantizer top-1 on device; the TC
+        // quantizer sizes its grid to its few work items, so an insert beside
+        // live searches occupies a handful of SMs, not the whole GPU
+        const long long* nearest = d_fo_i_.as<long long>();
+        if (use_tc_quantizer(1) && m <= 65536) {
+            Workspace dw = carve(data_lease_, m, 1, 1, 1, sh.fnch);
+            BIVF_CUDA(launch_pad_rows(d_x_.as<float>(), m, D_, Dp_, dw.queries, st));
+            enqueue_quantizer(st, m, 1, sh.fnch, dw);
+            nearest = dw.probes;
+        } else {
+            BIVF_CUDA(launch_pad_rows(d_x_.as<float>(), m, D_, Dp_, d_qtmp_.as<float>(), st));
+            BIVF_CUDA(launch_flat_topk(d_cent_il_.as<float>(), C_, D_, d_qtmp_.as<float>(), m, 1,
+                                       cfg_.metric, sh.fnch, d_fc_d_.as<float>(),
+                                       d_fc_i_.as<long long>(), d_fo_d_.as<float>(),
+                                       d_fo_i_.as<long long>(), nullptr, d_ctr_.as<uint32_t>(),
+                                       num_sms_, st));
+        }
+        BIVF_CUDA(launch_make_asg(nearest, d_ids_.as<long long>(), m, d_asg_.as<uint32_t>(), st));
         const uint32_t cursor_old = h_cursor_;
         BIVF_CUDA(launch_insert(insert_state(), m, d_x_.as<float>(), d_ids_.as<long long>(),
                                 d_asg_.as<uint32_t>(), d_blk_.as<int32_t>(),

@@ -237,9 +237,11 @@ private:
     DevBuf d_run_, d_failfrom_, d_newlen_;
     // data-lane staging
     cudaStream_t data_stream_ = nullptr;
+    int prio_hi_ = 0;
     DevBuf d_x_, d_ids_, d_asg_, d_blk_, d_did_, d_qtmp_, d_fc_d_, d_fc_i_, d_fo_d_, d_fo_i_,
         d_ctr_;
     PinBuf h_stage_;
+    Lease data_lease_;  // the data lane's own workspace (insert-path TC quantizer); stream = data_stream_
     // maintenance scratch (rearrangement block moves, delete), grow-only; used
     // under data_mu_ only
     DevBuf s_rr_src_, s_rr_dst_, s_rr_pay_, s_rr_ids_;

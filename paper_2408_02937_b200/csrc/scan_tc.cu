@@ -1331,7 +1331,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  const float* arena_rows, const TcBufs& T, const TcDense* dense,
                                  float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
-                                 cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+                                 cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int max_grid) {
     if (sh.nq == 0) return cudaSuccess;
     SearchShape s2 = sh;
     s2.QT = kM;
@@ -1391,7 +1391,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     e = cudaMemsetAsync(T.qthr, 0x7f, (size_t)sh.nq * 4, s);
     if (e != cudaSuccess) return e;
     if (ev0) cudaEventRecord(ev0, s);
-    int grid = num_sms;
+    int grid = std::max(1, std::min(num_sms, max_grid));  // no idle CTAs holding whole SMs
     if (const char* g = std::getenv("BIVF_TC_GRID")) grid = std::max(1, atoi(g));  // debugging aid
     if (sh.k <= 16) scan_tc_kernel<16><<<grid, kTcThreads, sm16, s>>>(p, map_off, map_arena);
     else scan_tc_kernel<32><<<grid, kTcThreads, sm32, s>>>(p, map_off, map_arena);

@@ -60,6 +60,6 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0 = nullptr,
-                                 cudaEvent_t ev1 = nullptr);
+                                 cudaEvent_t ev1 = nullptr, int max_grid = 1 << 30);
 
 }  // namespace bivf

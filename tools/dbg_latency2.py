@@ -36,17 +36,23 @@ if mode != "plain":
 for _ in range(13):
     ix.search_batch(q, 10, 32)
 print("main", ins.finish(), flush=True)
+def evsum(ev):
+    ev = list(ev)
+    moved = [e for e in ev if e[1] != e[2] or e[3] > 0]
+    durs = sorted(e[4] for e in ev)
+    return {"n": len(ev), "changed": len(moved), "dur_us_p50": durs[len(durs)//2] if durs else 0,
+            "dur_us_max": durs[-1] if durs else 0, "dur_us_sum": round(sum(durs))}
 ex = Executor(ix, num_lanes=32)
 common = dict(k=10, nprobe=32, search_batch=10, insert_batch=128, seed=1, poisson=True, raw=True)
 inserts = pool[len(pool) // 2:]
 for name, iq in (("warm", 78.0), ("idle", 0.0), ("live", 78.0), ("live2", 78.0)):
-    ev0 = len(ix.take_events())
+    ix.take_rearrange_events()
     t = time.time()
     r = replay(ex, q, inserts, 1000.0, iq, 4.0 if name != "warm" else 0.5, **common)
     sr, ir = r["search_raw_us"], r["insert_raw_us"]
     spikes = [(i, round(v / 1e3, 1)) for i, v in enumerate(sr) if v > 5000]
     ispk = [(i, round(v / 1e3, 1)) for i, v in enumerate(ir) if v > 5000]
     print(name, "p99 %.3f max %.1f rej %d" % (r["search"]["p99_ms"], r["search"]["max_ms"], r["rejected"]),
-          "ins p99 %.2f" % r["insert"]["p99_ms"], "events", len(ix.take_events()),
+          "ins p99 %.2f" % r["insert"]["p99_ms"], "events", evsum(ix.take_rearrange_events()),
           "search spikes", spikes[:12], "insert spikes", ispk[:8], flush=True)
 ex.shutdown(); ex.close()
