@@ -239,19 +239,22 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const ScanParams p) {
                         const float x1 = xs[(dd + 1) * 32 + lane];
                         const float x2 = xs[(dd + 2) * 32 + lane];
                         const float x3 = xs[(dd + 3) * 32 + lane];
+                        // all QW chains every step (rows >= nqw hold stale data whose
+                        // results are ignored): no per-query branch, so the QW
+                        // independent sequential sums interleave (each chain keeps
+                        // its ascending-d order, the reference's bits)
+                        float4 qv[QW];
 #pragma unroll
-                        for (int qi = 0; qi < QW; ++qi) {
-                            if (qi < (int)nqw) {
-                                const float4 qv =
-                                    *reinterpret_cast<const float4*>(myq + qi * p.Dp + d0 + dd);
-                                float a = acc[qi];
-                                a = dstep<M>(a, qv.x, x0);
-                                a = dstep<M>(a, qv.y, x1);
-                                a = dstep<M>(a, qv.z, x2);
-                                a = dstep<M>(a, qv.w, x3);
-                                acc[qi] = a;
-                            }
-                        }
+                        for (int qi = 0; qi < QW; ++qi)
+                            qv[qi] = *reinterpret_cast<const float4*>(myq + qi * p.Dp + d0 + dd);
+#pragma unroll
+                        for (int qi = 0; qi < QW; ++qi) acc[qi] = dstep<M>(acc[qi], qv[qi].x, x0);
+#pragma unroll
+                        for (int qi = 0; qi < QW; ++qi) acc[qi] = dstep<M>(acc[qi], qv[qi].y, x1);
+#pragma unroll
+                        for (int qi = 0; qi < QW; ++qi) acc[qi] = dstep<M>(acc[qi], qv[qi].z, x2);
+#pragma unroll
+                        for (int qi = 0; qi < QW; ++qi) acc[qi] = dstep<M>(acc[qi], qv[qi].w, x3);
                     }
                     for (; dd < nd; ++dd) {
                         const float x = xs[dd * 32 + lane];
