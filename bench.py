@@ -366,20 +366,19 @@ def roofline(alg_bytes, pairs, scan_ms, ph, peaks):
 
     Queries are grouped by list, so one staged 32-vector group serves up to 128
     queries: the kernel streams each list from L2/HBM once per query tile and
-    is bound by the tensor pipe, not HBM.  Its algorithmic work per launch is
-    the 3xTF32 distance GEMM over every (query, probed vector) pair:
-    3 * 2 * D flops per pair.  Peak: the dense TF32 tcgen05 rate measured by tools/tc_probe_n.cu (4096
-    flop/clk/SM) at MEASURED_PEAKS.json's max SM clock (= 1.19 PFLOP/s; the
-    driver-measured cuBLAS bf16 rate / 2 would give 821).
+    is bound by the tensor pipe, not HBM.  Its algorithmic work per search step
+    is the 3xBF16 filter GEMM over every (query, probed vector) pair:
+    3 MMAs x 2 x K flops per pair (K = D rounded up to 16), summed over the two
+    launches of the two-phase scan (nearest list first, then the other P - 1).
+    Peak: the driver-measured dense bf16 rate (MEASURED_PEAKS.json bf16_tflops,
+    cuBLAS burst; the scan is ~1.4 ms of a ~1.8 ms step).
     The north star's per-query HBM figure (bytes of every probed list, per
     query) is reported beside it: query grouping makes it exceed HBM bandwidth.
-    `traffic` is the ncu DRAM read+write bytes per launch of this kernel from
-    profiles/r01_scan_tc_ncu.json (same index shape, tools/ncu_tc.sh)."""
-    # dense TF32 tcgen05 rate: 4096 flop/clk/SM (tools/tc_probe_n.cu: a 128x256x8
-    # kind::tf32 MMA retires every 128 cycles) x 148 SMs x max SM clock
-    mhz = peaks.get("sm_max_mhz", 1965.0)
-    tf32 = 4096.0 * 148 * mhz * 1e6 / 1e12
-    flops = 3.0 * 2.0 * DIM * pairs
+    `traffic` is the ncu DRAM read+write bytes of the scan launches per step
+    from profiles/r01_scan_tc_ncu.json (same index shape, tools/ncu_tc.sh)."""
+    peak = peaks.get("bf16_tflops", 1641.9)
+    K = (DIM + 15) // 16 * 16
+    flops = 3.0 * 2.0 * K * pairs
     achieved = flops / (scan_ms * 1e-3) / 1e12
     hbm = peaks.get("hbm_gbs", 6548.2)
     per_query_gbs = alg_bytes / (scan_ms * 1e-3) / 1e9
@@ -390,9 +389,10 @@ def roofline(alg_bytes, pairs, scan_ms, ph, peaks):
         traffic = prof.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
-    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(tf32, 1),
-            "unit": "TFLOP/s", "frac": round(achieved / tf32, 3), "traffic": traffic,
-            "kernel": "scan_tc_kernel", "peak_source": "dense TF32 tcgen05 4096 flop/clk/SM (tools/tc_probe_n.cu) x 148 SMs x sm_max_mhz",
+    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1),
+            "unit": "TFLOP/s", "frac": round(achieved / peak, 3), "traffic": traffic,
+            "kernel": "scan_tc_kernel (2 launches: rank-0 probes, then the rest)",
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense bf16, cuBLAS burst)",
             "alg_flops_per_launch": flops, "pairs_per_launch": int(pairs), "scan_ms": round(scan_ms, 3),
             "north_star_hbm": {"per_query_bytes_per_launch": alg_bytes,
                                "achieved_gbs": round(per_query_gbs, 1), "peak_gbs": hbm,

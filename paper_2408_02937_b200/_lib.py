@@ -11,7 +11,8 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbivf_gpu.so")
+# BIVF_LIB: an alternative in-tree build of the same library (kernel variants under test)
+LIB_PATH = os.environ.get("BIVF_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbivf_gpu.so")
 
 OK, EINVAL, EPOOL, ECORRUPT, ERANGE, ELOGIC, EIO, ECUDA, EBUSY, ENOMEM = range(10)
 METRIC_L2, METRIC_IP = 0, 1

@@ -829,6 +829,9 @@ void GpuIndex::enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Works
     ss.QT = qt_for(k, D_);
     ss.metric = cfg_.metric;
     if (use_tc(k)) {
+        static const bool stats = std::getenv("BIVF_TC_STATS") != nullptr;  // debugging aid
+        const uint64_t runs = (uint64_t)nq * P * ss.maxch * 2;
+        if (stats) BIVF_CUDA(cudaMemsetAsync(w.tc.ccount, 0, runs * 4, l.stream));
         BIVF_CUDA(launch_ivf_search_tc(dev_lists(), w.plan, w.probes, w.queries,
                                        d_cent_.as<float>(), ss, map_off_, map_arena_,
                                        d_off_nrm_.as<float>(), d_arena_nrm_.as<float>(),
@@ -836,6 +839,21 @@ void GpuIndex::enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Works
                                        nullptr, w.out_d,
                                        w.out_i, w.out_cnt, num_sms_, l.stream,
                                        timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr));
+        if (stats) {
+            std::vector<uint32_t> cc(runs);
+            BIVF_CUDA(cudaMemcpyAsync(cc.data(), w.tc.ccount, runs * 4, cudaMemcpyDeviceToHost,
+                                      l.stream));
+            BIVF_CUDA(cudaStreamSynchronize(l.stream));
+            uint64_t ovf = 0, cand = 0, nz = 0;
+            for (uint32_t c : cc) {
+                if (c == kOverflow) ++ovf;
+                else { cand += c; nz += c > 0; }
+            }
+            std::fprintf(stderr, "[tc-stats] nq=%u P=%u maxch=%u runs=%llu overflow=%llu cand=%llu "
+                         "(%.2f/query) nonempty=%llu\n", nq, P, ss.maxch, (unsigned long long)runs,
+                         (unsigned long long)ovf, (unsigned long long)cand, (double)cand / nq,
+                         (unsigned long long)nz);
+        }
     } else if (use_tc_dense(k)) {
         // k > 32: the tensor cores write the approximate distance of every
         // (query, probed vector) pair, a per-query selection takes the exact

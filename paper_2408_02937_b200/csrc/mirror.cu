@@ -1,4 +1,6 @@
 // Tensor-core scan mirror maintenance (see mirror.cuh).  sm_100a.
+#include <cuda_bf16.h>
+
 #include <algorithm>
 
 #include "launches.h"
@@ -9,23 +11,22 @@ namespace bivf {
 
 namespace {
 
-__device__ __forceinline__ float tf32_trunc_m(float x) {
-    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-}
-
 // one vector -> its mirror column `lane` of group `g` (+ the group's norm block
-// `nrm`).  x[d * xs] is dim d.
-__device__ __forceinline__ void mirror_column(float* g, float* nrm, float* row, uint32_t lane,
+// `nrm`).  x[d * xs] is dim d.  Planes are bf16 (mirror.cuh): s_hi = bf16_rn(s),
+// s_lo = bf16_rn(s - s_hi).
+__device__ __forceinline__ void mirror_column(float* gf, float* nrm, float* row, uint32_t lane,
                                               const float* x, uint32_t xs, const float* c,
                                               uint32_t D, uint32_t K) {
+    uint16_t* g = reinterpret_cast<uint16_t*>(gf);
     float n2 = 0.f;
     for (uint32_t d = 0; d < D; ++d) {
         const float xd = x[(uint64_t)d * xs];
         if (row) row[d] = xd;
         const float s = __fsub_rn(xd, c[d]);
-        const float h = tf32_trunc_m(s);
-        g[(uint64_t)d * 32u + lane] = h;
-        g[(uint64_t)(K + d) * 32u + lane] = __fsub_rn(s, h);
+        const __nv_bfloat16 h = __float2bfloat16_rn(s);
+        g[(uint64_t)d * 32u + lane] = __bfloat16_as_ushort(h);
+        g[(uint64_t)(K + d) * 32u + lane] =
+            __bfloat16_as_ushort(__float2bfloat16_rn(__fsub_rn(s, __bfloat162float(h))));
         n2 = __fadd_rn(n2, __fmul_rn(s, s));
     }
     nrm[lane] = n2;
@@ -109,9 +110,14 @@ __global__ void mirror_slot_move_kernel(MirrorView M, const uint64_t* id_addr, u
         uint32_t lane;
         float *nrm, *row;
         float* g = mirror_slot(M, id_addr[phase == 0 ? m : n + m], lane, nrm, row);
+        if (r < 2 * M.K) {  // bf16 plane element (carried in a float scratch slot)
+            uint16_t* e16 = reinterpret_cast<uint16_t*>(g) + (uint64_t)r * 32u + lane;
+            if (phase == 0) scr[o] = __uint_as_float(*e16);
+            else *e16 = (uint16_t)__float_as_uint(scr[o]);
+            continue;
+        }
         float* e;
-        if (r < 2 * M.K) e = g + (uint64_t)r * 32u + lane;
-        else if (r < 2 * M.K + 2) e = nrm + (r - 2 * M.K) * 32u + lane;
+        if (r < 2 * M.K + 2) e = nrm + (r - 2 * M.K) * 32u + lane;
         else if (row) e = row + (r - 2 * M.K - 2);
         else continue;
         if (phase == 0) scr[o] = *e;

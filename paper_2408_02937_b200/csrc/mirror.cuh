@@ -2,19 +2,20 @@
 //
 // For every stored vector x of list c the index keeps, next to the
 // reference-layout payload (which stays the source of truth and of every exact
-// distance), the list-centred residual s = fl(x - c) pre-split for 3xTF32:
-// s_hi = TF32 truncation of s, s_lo = s - s_hi (exact in fp32), plus |s|^2 and
-// |s|.  Same group indexing as the payload, so slot/block moves map one-to-one.
-// Planes, per 32-vector group, rows of 32 floats (one per slot), K = D rounded
-// up to 8 (rows D..K-1 stay zero: the MMA's K padding):
+// distance), the list-centred residual s = fl(x - c) pre-split for 3xBF16:
+// s_hi = bf16_rn(s), s_lo = bf16_rn(s - s_hi) (s - s_hi is exact in fp32), plus
+// |s|^2.  Same group indexing as the payload, so slot/block moves map one-to-one.
+// Planes, per 32-vector group, rows of 32 bf16 (64 bytes, one element per slot),
+// K = D rounded up to 16 (rows D..K-1 stay zero: the MMA's K padding):
 //     rows [0, K)      s_hi, dim d
 //     rows [K, 2K)     s_lo, dim d
+// A group's planes occupy 2K*64 bytes = K*32 "floats" of the float-typed buffers.
 // Norms, per group, a separate array of 64 floats: [|s|^2 (sequential fp32) x 32]
 // [kVScale * |s|^2 x 32] (the per-slot term of the scan's pass-1 threshold, scan_tc.cu).
 // Rows, per group, a slot-major copy of the exact payload (32 x D fp32): the
 // refine's candidate gathers read 4 contiguous 128-byte lines per vector instead
 // of D scattered 32-byte sectors of the interleaved layout.
-// One TMA box of {32, 2K} rows stages a group's two B operands.  The
+// One TMA box of {32, 2K} bf16 rows (SWIZZLE_64B) stages a group's two B operands.  The
 // mirror is written by the same data-lane operations that write the payload
 // (bulk load, insert, delete slot moves, rearrangement block moves), before
 // the list length that exposes the slots is release-published.
@@ -26,29 +27,31 @@
 namespace bivf {
 
 struct MirrorView {
-    float* off_mir;        // offline groups x GF
+    float* off_mir;        // offline groups x GF (bf16 planes, see above)
     float* arena_mir;      // num_blocks x MPS
     float* off_nrm;        // offline groups x 64
     float* arena_nrm;      // num_blocks x gpb x 64
     float* off_rows;       // offline groups x 32 x D
     float* arena_rows;     // num_blocks x gpb x 32 x D
     const float* cent;     // [C][D] row-major centroids
-    uint32_t D, K, T, gpb; // K = D rounded up to 8
-    uint64_t GF;           // floats per group  = 2K*32
+    uint32_t D, K, T, gpb; // K = D rounded up to 16
+    uint64_t GF;           // floats per group  = K*32 (2K*32 bf16)
     uint64_t MPS;          // floats per block  = gpb*GF
 };
 
 // Error-bound constants of the tensor-core filter (D <= 128):
-//   |a - e| <= kEpsCross*|r||s| + kEpsRel*(|r|^2+|s|^2) + kEpsRel*|a|  (2x margin), and with
+//   |a - e| <= kEpsCross*|r||s| + kEpsRel*(|r|^2+|s|^2) + kEpsRel*|a|  (>= 2x margin), and with
 //   |r||s| <= (|r|^2+|s|^2)/2:  eps' = kEpsT*(nq+ns) + kEpsRel*|a|,  kEpsT = kEpsRel + kEpsCross/2.
 // For a >= 0 the lower bound a - eps' <= ubk  <=>  dot >= kVScale*(nq+ns) - ubk/(2(1-kEpsRel)).
-constexpr float kEpsCross = 1.0f / 16384.0f;  // 2 * 2^-15 >= 2 * 2 * 2^-16 on |r||s|
+// 3xBF16 (scan_tc.cu): |P - r.s| <= (3.01*2^-16 + 24*2^-24)|r||s| <= 2^-14.3 |r||s|, so the
+// cross term of a = nq + ns - 2P is off by <= 2^-13.3 |r||s|; 2^-12 carries a 2.5x margin.
+constexpr float kEpsCross = 1.0f / 4096.0f;
 constexpr float kEpsRel = 1.0f / 32768.0f;    // 2^-15 on (nq+ns) and on |a|
 constexpr float kEpsT = kEpsRel + 0.5f * kEpsCross;
 constexpr float kVScale = (1.0f - kEpsRel - kEpsT) / (2.0f * (1.0f - kEpsRel));
 
-inline uint32_t mirror_k(uint32_t D) { return (D + 7u) & ~7u; }
-inline uint64_t mirror_group_floats(uint32_t D) { return 2ull * mirror_k(D) * 32ull; }
+inline uint32_t mirror_k(uint32_t D) { return (D + 15u) & ~15u; }
+inline uint64_t mirror_group_floats(uint32_t D) { return (uint64_t)mirror_k(D) * 32ull; }
 constexpr uint32_t kNormFloats = 64;  // per group
 
 // insert: vector i (row-major x[i*D..]) landed in block out_blk[i] (-1 = failed)
@@ -66,7 +69,7 @@ cudaError_t launch_mirror_groups(const MirrorView& M, const float* payload, bool
                                  uint32_t n, cudaStream_t s);
 // delete compaction: the same moves as launch_slot_moves, on the mirror
 // (id_addr[2n] = sources then destinations; bit 63 = arena, value = the slot's
-// id index).  scratch: n * (2K+2+D) floats.
+// id index).  scratch: n * (2K+2+D) floats (one per moved bf16 plane element).
 cudaError_t launch_mirror_slot_moves(const MirrorView& M, const uint64_t* id_addr, uint32_t n,
                                      float* scratch, cudaStream_t s);
 

@@ -417,10 +417,14 @@ __global__ void plan_snapshot(DevLists L, uint32_t maxch, uint32_t gcmin, uint32
     cnt[c] = 0;
 }
 
-__global__ void plan_count(const long long* probes, uint32_t npairs, uint32_t* cnt,
-                           uint32_t* ppos) {
+// pairs i = q * P + rank with rank in [lo, hi) only (the ranked plans of the
+// two-phase TC scan; [0, P) = every pair)
+__global__ void plan_count(const long long* probes, uint32_t npairs, uint32_t P, uint32_t lo,
+                           uint32_t hi, uint32_t* cnt, uint32_t* ppos) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= npairs) return;
+    const uint32_t r = i % P;
+    if (r < lo || r >= hi) return;
     ppos[i] = atomicAdd(&cnt[(uint32_t)probes[i]], 1u);
 }
 
@@ -492,10 +496,13 @@ __global__ void __launch_bounds__(1024) plan_scan(uint32_t C, uint32_t QT, const
     }
 }
 
-__global__ void plan_scatter(const long long* probes, uint32_t npairs, const uint32_t* qoff,
-                             const uint32_t* ppos, uint32_t* plist) {
+__global__ void plan_scatter(const long long* probes, uint32_t npairs, uint32_t P, uint32_t lo,
+                             uint32_t hi, const uint32_t* qoff, const uint32_t* ppos,
+                             uint32_t* plist) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= npairs) return;
+    const uint32_t r = i % P;
+    if (r < lo || r >= hi) return;
     plist[qoff[(uint32_t)probes[i]] + ppos[i]] = i;
 }
 
@@ -668,14 +675,26 @@ cudaError_t launch_flat_topk(const float* flat_il, uint32_t n, uint32_t D, const
 
 cudaError_t launch_plan(const DevLists& L, const PlanBufs& B, const long long* probes,
                         const SearchShape& sh, cudaStream_t s) {
+    return launch_plan_ranked(L, B, probes, sh, 0, sh.P, true, s);
+}
+
+cudaError_t launch_plan_ranked(const DevLists& L, const PlanBufs& B, const long long* probes,
+                               const SearchShape& sh, uint32_t lo, uint32_t hi, bool snapshot,
+                               cudaStream_t s) {
     const uint32_t npairs = sh.nq * sh.P;
-    plan_snapshot<<<(L.C + 255) / 256, 256, 0, s>>>(L, sh.maxch, sh.gcmin, B.snap_off, B.snap_len,
-                                                   B.gc, B.nch, B.cnt);
-    plan_count<<<(npairs + 255) / 256, 256, 0, s>>>(probes, npairs, B.cnt, B.ppos);
+    if (snapshot) {
+        plan_snapshot<<<(L.C + 255) / 256, 256, 0, s>>>(L, sh.maxch, sh.gcmin, B.snap_off,
+                                                       B.snap_len, B.gc, B.nch, B.cnt);
+    } else {
+        cudaError_t e = cudaMemsetAsync(B.cnt, 0, (size_t)L.C * 4, s);
+        if (e != cudaSuccess) return e;
+    }
+    plan_count<<<(npairs + 255) / 256, 256, 0, s>>>(probes, npairs, sh.P, lo, hi, B.cnt, B.ppos);
     plan_scan<<<1, 1024, 0, s>>>(L.C, sh.QT, B.cnt, B.nch, B.qoff, B.item_off, B.n_items,
                                  B.item_ctr);
-    plan_scatter<<<(npairs + 255) / 256, 256, 0, s>>>(probes, npairs, B.qoff, B.ppos, B.plist);
-    count_launch(4);
+    plan_scatter<<<(npairs + 255) / 256, 256, 0, s>>>(probes, npairs, sh.P, lo, hi, B.qoff,
+                                                      B.ppos, B.plist);
+    count_launch(snapshot ? 4 : 3);
     return cudaGetLastError();
 }
 
@@ -690,10 +709,11 @@ cudaError_t launch_ivf_search(const DevLists& L, const PlanBufs& B, const long l
     const uint32_t npairs = sh.nq * sh.P;
     plan_snapshot<<<(L.C + 255) / 256, 256, 0, s>>>(L, sh.maxch, sh.gcmin, B.snap_off, B.snap_len,
                                                    B.gc, B.nch, B.cnt);
-    plan_count<<<(npairs + 255) / 256, 256, 0, s>>>(probes, npairs, B.cnt, B.ppos);
+    plan_count<<<(npairs + 255) / 256, 256, 0, s>>>(probes, npairs, sh.P, 0, sh.P, B.cnt, B.ppos);
     plan_scan<<<1, 1024, 0, s>>>(L.C, sh.QT, B.cnt, B.nch, B.qoff, B.item_off, B.n_items,
                                  B.item_ctr);
-    plan_scatter<<<(npairs + 255) / 256, 256, 0, s>>>(probes, npairs, B.qoff, B.ppos, B.plist);
+    plan_scatter<<<(npairs + 255) / 256, 256, 0, s>>>(probes, npairs, sh.P, 0, sh.P, B.qoff,
+                                                      B.ppos, B.plist);
     count_launch(4);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

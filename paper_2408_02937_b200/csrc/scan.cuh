@@ -64,6 +64,11 @@ cudaError_t launch_all_probes(long long* probes, uint32_t nq, uint32_t C, cudaSt
 // Only the plan kernels (snapshot, count, scan, scatter) of launch_ivf_search.
 cudaError_t launch_plan(const DevLists& L, const PlanBufs& B, const long long* probes,
                         const SearchShape& sh, cudaStream_t s);
+// Plan over the pairs of probe rank [lo, hi) only; snapshot = false reuses the
+// previous plan's list snapshot (snap_off/snap_len/gc/nch) and only re-counts.
+cudaError_t launch_plan_ranked(const DevLists& L, const PlanBufs& B, const long long* probes,
+                               const SearchShape& sh, uint32_t lo, uint32_t hi, bool snapshot,
+                               cudaStream_t s);
 
 // Copy row-major fp32 rows [n][D] into the 32-interleaved group layout
 // (block_store.hpp:37-40), zero-padding the last group; and the query

@@ -8,14 +8,15 @@
 // Design.  Exact distances are sequential fp32 sums, so
 // tensor cores can only FILTER.  Per work item (list c, tile of <=128 queries,
 // chunk of groups) a persistent CTA (one per SM) runs
-//   producer warp : two TMA boxes per 32-vector group from the scan mirror
+//   producer warp : one TMA box per 32-vector group from the scan mirror
 //                   (mirror.cuh: list-centred residual s = x - c pre-split into
-//                   TF32 hi/lo planes + |s|^2, |s|) -> MN-major B tiles
-//   MMA warp      : 3xTF32 tcgen05.mma 128x32xD (A = centred queries, hi/lo in
-//                   TMEM; B hi/lo from smem) into one of 8 TMEM accumulators
+//                   bf16 hi/lo planes + |s|^2) -> MN-major B tiles (SWIZZLE_64B)
+//   MMA warp      : 3xBF16 tcgen05.mma kind::f16 128x64x16 per K-step (A =
+//                   centred queries, bf16 hi/lo pairs in TMEM; B hi/lo from smem)
+//                   into one of 4 TMEM accumulators (fp32)
 //   2 math warpgroups (alternate groups): build A once per item, then per
 //                   group tcgen05.ld the 32 dot products of their query, form
-//                   a = |r|^2 + |s|^2 - 2 r.s and a PROVEN bound eps (TF32 +
+//                   a = |r|^2 + |s|^2 - 2 r.s and a PROVEN bound eps (bf16 split +
 //                   fp32 rounding, mirror.cuh), keep the k smallest upper
 //                   bounds (a+eps) and every vector whose lower bound (a-eps)
 //                   can still enter the top-k (one run per warpgroup).
@@ -27,6 +28,7 @@
 // the top-k.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 
 #include <cub/device/device_scan.cuh>
 
@@ -50,24 +52,61 @@ constexpr int kTcThreads = 64 + 128 * kWG;  // warp0 TMA, warp1 MMA, warps 2.. m
 constexpr int kM = 128;                    // queries per tile (MMA M, TMEM lanes)
 constexpr int kGU = 2;                     // groups per unit (MMA N = 32 * kGU)
 // smem stages (one group each; kNS / kGU unit slots) and smem candidate slots
-// per thread, by top-k width: k <= 16 -> 4 stages, 24 slots; k <= 32 -> 2, 48
+// per thread, by top-k width: k <= 16 -> 6 stages, 40 slots; k <= 32 -> 4, 56
+// (24 slots overflow in the unseeded first phase: an overflowed run is rescanned)
 template <int KT>
 struct TcCfg {
-    static constexpr int NS = KT <= 16 ? 4 : 2;
-    static constexpr int KC = KT <= 16 ? 24 : 48;
+    static constexpr int NS = KT <= 16 ? 6 : 4;
+    static constexpr int KC = KT <= 16 ? 40 : 56;
     static constexpr int NU = NS / 2;
 };
+// release a unit's accumulator as soon as its dot products are in registers
+// (before filtering) instead of after the filter (measured: no gain, more registers)
+constexpr bool kEarlyRelease = false;
 constexpr int kNB = 4;                     // TMEM accumulators (32 * kGU columns each; even)
+constexpr int kRing = 4;                   // decoded work items in flight (producer lookahead)
+constexpr int kNR = 8;                     // norm slots (ring, one unit each; decoupled from kNB)
+
+// Per-role cycle accounting of the scan kernel (build with -DBIVF_TC_PROF=1; CTA 0
+// prints its producer / MMA / math-warp counters).  A no-op otherwise.
+#ifndef BIVF_TC_PROF
+#define BIVF_TC_PROF 0
+#endif
+struct TcProf {
+#if BIVF_TC_PROF
+    uint32_t t0 = 0, t00 = 0, acc[12] = {};
+    __device__ __forceinline__ void start() { t00 = t0 = (uint32_t)clock(); }
+    __device__ __forceinline__ void mark(int i) {
+        const uint32_t n = (uint32_t)clock();
+        acc[i] += n - t0;
+        t0 = n;
+    }
+    __device__ void report(const char* role, int warp) {
+        acc[11] = (uint32_t)clock() - t00;
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
+            printf("[tc-prof] %s w%d: %u %u %u %u %u %u %u %u %u %u %u total %u\n", role, warp, acc[0],
+                   acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7], acc[8], acc[9], acc[10],
+                   acc[11]);
+    }
+#else
+    __device__ __forceinline__ void start() {}
+    __device__ __forceinline__ void mark(int) {}
+    __device__ __forceinline__ void report(const char*, int) {}
+#endif
+};
 constexpr int kMaxD = 128;
-// a stage = one group's mirror planes: 2K rows of 128 bytes ([s_hi], [s_lo])
-constexpr int kStage = 2 * kMaxD * 128;
-// TMEM columns: A_hi [0,128), A_lo [128,256), accumulators [256, 256 + 32*kNB)
-constexpr uint32_t kColAlo = 128, kColAcc = 256, kTmemCols = 512;
+// a stage = one group's mirror planes: 2K rows of 64 bytes (32 bf16: [s_hi], [s_lo])
+constexpr int kStage = 2 * kMaxD * 64;
+// TMEM columns (a column holds two bf16 of a row): two A buffers (items alternate,
+// so the next item's A is written while the MMAs of the current one run), each
+// A_hi [0,64) + A_lo [64,128); accumulators [256, 256 + 64*kNB)
+constexpr uint32_t kColAlo = 64, kColA2 = 128, kColAcc = 256, kTmemCols = 512;
 static_assert(kColAcc + 32 * kGU * kNB <= kTmemCols, "TMEM budget");
 
 struct TcParams {
     DevLists L;
     uint32_t D, Dk, Dp, k, P, maxch;
+    uint32_t seed_groups;        // seeding pass: scan only the first seed_groups groups, no run output
     const float* centroids;      // [C][D] row-major
     const float* queries;        // [nq][Dp]
     const uint32_t* snap_off;
@@ -111,9 +150,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -123,11 +159,12 @@ __device__ __forceinline__ void tc_fence_after() {
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(n) : "memory");  // non-.aligned: tolerates divergence
 }
-// UMMA smem matrix descriptor (version 1).  layout 2 = SWIZZLE_128B (A: K-major,
-// 8 rows x 128 B atoms); layout 1 = SWIZZLE_128B_BASE32B (B: MN-major 32-bit,
-// 4 rows x 128 B atoms with 32-byte chunks swizzled by row, which is what TMA
-// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B writes; the plain 128B swizzle is not a
-// valid MN-major TF32 operand).  Verified on B200 by tools/tc_probe.cu.
+// UMMA smem matrix descriptor (version 1).  layout 4 = SWIZZLE_64B, MN-major
+// 16-bit B: atoms of 32 slots (64 B) x 8 K-rows = 512 B (SBO = 512 between K
+// atoms, LBO = the stride to the next 32 slots = the next stage), which is what
+// TMA CU_TENSOR_MAP_SWIZZLE_64B writes for a {32, 2K} bf16 box.  Verified on
+// B200 by tools/tc_probe_bf16.cu (exact small-integer products, N = 64 across
+// two stages, A bf16 pairs in TMEM).
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
                                               uint32_t layout) {
     uint64_t d = 0;
@@ -137,24 +174,6 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     d |= 1ull << 46;
     d |= (uint64_t)layout << 61;
     return d;
-}
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-        : "memory");
-}
-__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
-                                            uint32_t idesc, uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
-        : "memory");
 }
 #define BIVF_TMEM_ST32(addr, v)                                                                  \
     asm volatile(                                                                                \
@@ -167,22 +186,28 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
         "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),      \
         "r"(v[29]), "r"(v[30]), "r"(v[31])                                                       \
         : "memory")
-__device__ __forceinline__ float tf32_trunc(float x) {
-    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+// bf16 RN split of a pair of fp32 values into (hi pair, lo pair), each packed
+// low half = first element (the K order of A in TMEM, tools/tc_probe_bf16.cu)
+__device__ __forceinline__ void bf16_split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
+    const __nv_bfloat16 l0 = __float2bfloat16_rn(__fsub_rn(x0, __bfloat162float(h0)));
+    const __nv_bfloat16 l1 = __float2bfloat16_rn(__fsub_rn(x1, __bfloat162float(h1)));
+    hi = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+    lo = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
 }
-// Warp-collective issue of one 3xTF32 K-step (A_hi*B_hi, A_hi*B_lo, A_lo*B_hi):
+// Warp-collective issue of one 3xBF16 K-step (A_hi*B_hi, A_hi*B_lo, A_lo*B_hi):
 // the whole (converged) warp executes it, elect.sync picks the issuing lane
 // inside the asm, so no per-MMA elect loop is generated around it.
-__device__ __forceinline__ void mma3_tf32_elect(uint32_t dcol, uint32_t ah, uint32_t al, uint64_t bh,
+__device__ __forceinline__ void mma3_bf16_elect(uint32_t dcol, uint32_t ah, uint32_t al, uint64_t bh,
                                                 uint64_t bl, uint32_t idesc, uint32_t accum) {
     asm volatile(
         "{\n\t.reg .pred e, p, t;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %6, 0;\n\t"
         "setp.eq.b32 t, 0, 0;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, t;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, t;\n\t}" ::"r"(dcol),
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, t;\n\t}" ::"r"(dcol),
         "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(accum)
         : "memory");
 }
@@ -191,12 +216,6 @@ __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
         "{\n\t.reg .pred e;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-            smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(bar))
         : "memory");
 }
@@ -220,17 +239,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 // Bound on |a - e| where a = nq + ns - 2P is the tensor-core approximation and e
 // the reference's sequential fp32 l2_sqr (DESIGN.md §Scan-TC error bound).
-// r = fl(q-c), s = fl(x-c); 3xTF32: P = r_hi.s_hi + r_hi.s_lo + r_lo.s_hi with
-// explicit truncation (r = r_hi + r_lo exactly), so the dropped r_lo.s_lo and the
-// TF32 truncation of the lo parts are <= ~2^-20 sum|r_d s_d|; fp32 accumulation of
-// 3*D/8 MMA steps adds <= 48*2^-24 sum|r_d s_d| (D=128): |P - r.s| <= 2^-16 |r||s|
-// (measured worst 2^-20.3 on B200, tools/tc_probe_ts.cu).  Norms: sequential fp32,
+// r = fl(q-c), s = fl(x-c); 3xBF16: r = r0 + r1 + rho with r0 = bf16_rn(r),
+// r1 = bf16_rn(r - r0) (r - r0 exact), |r1| <= 2^-8|r|, |rho| <= 2^-16|r| (same for s);
+// bf16 products are exact in fp32, and P = r0.s0 + r0.s1 + r1.s0 drops r1.s1, rho.s
+// and r.sigma: <= 3.01*2^-16 sum|r_d s_d|; fp32 accumulation of 3*K/16 MMA steps adds
+// <= 24*2^-24 sum|r_d s_d| (K=128): |P - r.s| <= 2^-14.3 |r||s| (measured worst
+// 2^-19.0 on B200, tools/tc_probe_bf16.cu).  Norms: sequential fp32,
 // |nq - |r|^2| <= (D+1) 2^-24 |r|^2; exact value: |e - |q-x|^2| <= (D+2) 2^-24 |q-x|^2;
 // centring: | |r-s|^2 - |q-x|^2 | <= 2^-22 (|r|^2 + |s|^2).  Constants (mirror.cuh)
 // carry >= 2x margin; |r||s| is bounded by (|r|^2+|s|^2)/2 so every term is a
 // function of (nq + ns) and |a|:  eps' = kEpsT*(nq+ns) + kEpsRel*|a| + 1e-30.
 struct TcItem {
-    uint32_t c, npairs, g0, g1, chunk, off, len;
+    uint32_t c, npairs, g0, g1, chunk, off, len, valid;
     const uint32_t* pairs;
 };
 
@@ -242,6 +262,7 @@ __device__ __forceinline__ TcItem tc_decode(const TcParams& p, uint32_t it) {
         else hi = mid;
     }
     TcItem d;
+    d.valid = 1;
     d.c = lo;
     const uint32_t local = it - p.item_off[lo];
     const uint32_t nch = p.nch[lo];
@@ -254,25 +275,9 @@ __device__ __forceinline__ TcItem tc_decode(const TcParams& p, uint32_t it) {
     const uint32_t ng = ivf_ngroups(p.L, d.off, d.len);
     d.g0 = h * p.gc[lo];
     d.g1 = min(ng, d.g0 + p.gc[lo]);
+    if (p.seed_groups) d.g1 = min(d.g1, d.g0 + p.seed_groups);
     d.chunk = h;
     return d;
-}
-
-// TMA row of group j's mirror (rows of 32 floats; a group spans 2D+2 rows)
-__device__ __forceinline__ void group_row(const DevLists& L, uint32_t c, uint32_t off,
-                                          uint32_t j, bool& arena, int& row) {
-    const uint32_t og = (off + 31u) >> 5;
-    const uint32_t R = 2u * ((L.D + 7u) & ~7u);
-    if (j < og) {
-        arena = false;
-        row = (int)((L.off_start[c] / 32u + j) * R);
-    } else {
-        const uint32_t jj = j - og;
-        const uint32_t mid = jj / L.gpb, gi = jj - mid * L.gpb;
-        const int32_t blk = L.table[(uint64_t)c * L.MLB + mid];
-        arena = true;
-        row = (int)(((uint64_t)blk * L.gpb + gi) * R);
-    }
 }
 
 // bounds + filtering of one group for this thread's query (see tc_unit)
@@ -283,6 +288,22 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
                                           uint32_t& ncand, bool& overflow, float* clb,
                                           uint32_t* cloc, float* scr) {
     if (!active) return;
+    // pass 1: slot n can still enter the top-k only if its lower bound a - eps' <= ubk,
+    // i.e. dot >= V[n] + W (V = kVScale*ns from the mirror norms; a < 0 passes too,
+    // since ubk > 0).  Most groups have no such slot: test max_n (dot - V) >= W first
+    // (an FADD per slot, 3-input max, two independent chains), build the mask only
+    // when the group has a survivor.
+    const float W = fmaf(kVScale, nq, -ubk * (0.5f / (1.0f - kEpsRel)));
+    {
+        float m0 = -__int_as_float(0x7f800000), m1 = m0;
+#pragma unroll
+        for (uint32_t n = 0; n < 32; n += 4) {
+            const float4 v = reinterpret_cast<const float4*>(wn + 32)[n / 4];
+            m0 = fmaxf(m0, fmaxf(dot[n] - v.x, dot[n + 1] - v.y));  // FMNMX3
+            m1 = fmaxf(m1, fmaxf(dot[n + 2] - v.z, dot[n + 3] - v.w));
+        }
+        if (!(fmaxf(m0, m1) >= W)) return;
+    }
     // valid slots of group j, from the snapshot (no table lookups)
     uint32_t nvalid;
     {
@@ -295,10 +316,6 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
         }
     }
     const uint32_t vmask = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
-    // pass 1: slot n can still enter the top-k only if its lower bound a - eps' <= ubk,
-    // i.e. dot >= V[n] + W (V = kVScale*ns from the mirror norms; a < 0 passes too,
-    // since ubk > 0).  Three instructions per slot.
-    const float W = fmaf(kVScale, nq, -ubk * (0.5f / (1.0f - kEpsRel)));
     uint32_t need = 0;
 #pragma unroll
     for (uint32_t n = 0; n < 32; n += 4) {
@@ -360,50 +377,59 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
     }
 }
 
-template <int KT>
-__device__ __forceinline__ void tc_group(const TcParams& p, const TcItem& d, uint32_t j,
-                                         uint32_t acol, uint32_t tmem_base, uint32_t taddr_lane,
-                                         bool active, float nq, float (&ubl)[KT], float& ubk,
-                                         uint32_t& ncand, bool& overflow, float* clb,
-                                         uint32_t* cloc, float* scr, const float* wn) {
-    // wn: the group's norms in the unit's norm slot (staged by the producer)
-    float dot[32];
-    tmem_ld32(tmem_base + taddr_lane + acol, dot);
-    tc_filter<KT>(p, d, j, wn, active, nq, dot, ubl, ubk, ncand, overflow, clb, cloc, scr);
-}
-
-// One unit (kGU consecutive groups j0.. of the item, accumulator u % kNB).
+// One unit (kGU consecutive groups j0.. of the item, accumulator u % kNB, norm
+// slot u % kNR).  The accumulator is released as soon as its dot products are in
+// registers (the MMA of unit u + kNB can start while this unit is filtered); the
+// norm slot once the filter is done.
 template <int KT>
 __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint32_t u, uint32_t j0,
                                         uint64_t* acc_full, uint64_t* acc_empty, uint32_t tmem_base,
                                         uint32_t taddr_lane, int lane, bool active, float nq,
                                         float (&ubl)[KT], float& ubk, uint32_t& ncand,
                                         bool& overflow, float* clb, uint32_t* cloc,
-                                        float* scr, float* nslots, uint64_t* nfull, float* qt,
-                                        uint64_t qrow, uint32_t m) {
-    const uint32_t b = u % kNB;
+                                        float* scr, float* nslots, uint64_t* nfull,
+                                        uint64_t* nempty, float* qt, uint64_t qrow, uint32_t m,
+                                        TcProf& pf) {
+    const uint32_t b = u % kNB, ns = u % kNR;
     // the query's shared threshold: the smallest k-th upper bound any of its runs
     // has published (a valid filter bound for every run of the query)
     const float qshared = active ? __ldcg(qt) : ubk;
-    mbar_wait(&nfull[b], (u / kNB) & 1);
+    const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
+    pf.mark(8);
     mbar_wait(&acc_full[b], (u / kNB) & 1);
     __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread spin
+    pf.mark(4);
     tc_fence_after();
-    const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
+    const uint32_t acol = tmem_base + taddr_lane + kColAcc + b * 32 * kGU;
+    float dot[kEarlyRelease ? kGU : 1][32];
+    if constexpr (kEarlyRelease) {
+#pragma unroll
+        for (int h = 0; h < kGU; ++h)
+            if ((uint32_t)h < ng) tmem_ld32(acol + 32 * h, dot[h]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[b]);
+    }
+    pf.mark(5);
+    mbar_wait(&nfull[ns], (u / kNR) & 1);
+    pf.mark(6);
+    const float* wslot = nslots + ns * kGU * kNormFloats;
     if (p.dense_out) {  // dense mode: write the approximate distances, no filtering
-        for (uint32_t h = 0; h < ng; ++h) {
-            float dot[32];
-            tmem_ld32(tmem_base + taddr_lane + kColAcc + b * 32 * kGU + 32 * h, dot);
-            const float* wn = nslots + (b * kGU + h) * kNormFloats;
+#pragma unroll
+        for (int h = 0; h < kGU; ++h) {
+            if ((uint32_t)h >= ng) break;
+            const float* wn = wslot + h * kNormFloats;
+            const int hd = kEarlyRelease ? h : 0;
+            if constexpr (!kEarlyRelease) tmem_ld32(acol + 32 * h, dot[0]);
             if (active) {
                 float av[32];
 #pragma unroll
                 for (int i = 0; i < 32; i += 4) {
                     const float4 v = reinterpret_cast<const float4*>(wn)[i / 4];
-                    av[i] = fmaf(-2.f, dot[i], nq + v.x);
-                    av[i + 1] = fmaf(-2.f, dot[i + 1], nq + v.y);
-                    av[i + 2] = fmaf(-2.f, dot[i + 2], nq + v.z);
-                    av[i + 3] = fmaf(-2.f, dot[i + 3], nq + v.w);
+                    av[i] = fmaf(-2.f, dot[hd][i], nq + v.x);
+                    av[i + 1] = fmaf(-2.f, dot[hd][i + 1], nq + v.y);
+                    av[i + 2] = fmaf(-2.f, dot[hd][i + 2], nq + v.z);
+                    av[i + 3] = fmaf(-2.f, dot[hd][i + 3], nq + v.w);
                 }
                 if (p.dense_list_base) {  // IVF: element (j, n) at base + (32 j + n) * 128
                     float* o = p.dense_out + qrow + (uint64_t)(32u * (j0 + h)) * kM;
@@ -438,20 +464,30 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                 }
             }
         }
-        tc_fence_before();
+        if constexpr (!kEarlyRelease) tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[b]);
+        if (lane == 0) {
+            if constexpr (!kEarlyRelease) mbar_arrive(&acc_empty[b]);
+            mbar_arrive(&nempty[ns]);
+        }
         return;
     }
     ubk = fminf(ubk, qshared);
     const float ubk0 = ubk;
-    for (uint32_t h = 0; h < ng; ++h)
-        tc_group<KT>(p, d, j0 + h, kColAcc + b * 32 * kGU + 32 * h, tmem_base, taddr_lane, active,
-                     nq, ubl, ubk, ncand, overflow, clb, cloc, scr,
-                     nslots + (b * kGU + h) * kNormFloats);
-    tc_fence_before();
+#pragma unroll
+    for (int h = 0; h < kGU; ++h) {
+        if ((uint32_t)h >= ng) break;
+        if constexpr (!kEarlyRelease) tmem_ld32(acol + 32 * h, dot[0]);
+        tc_filter<KT>(p, d, j0 + h, wslot + h * kNormFloats, active, nq, dot[kEarlyRelease ? h : 0],
+                      ubl, ubk, ncand, overflow, clb, cloc, scr);
+    }
+    if constexpr (!kEarlyRelease) tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&acc_empty[b]);
+    pf.mark(7);
+    if (lane == 0) {
+        if constexpr (!kEarlyRelease) mbar_arrive(&acc_empty[b]);
+        mbar_arrive(&nempty[ns]);
+    }
     // publish an improved threshold (positive floats order like their bit patterns)
     if (active && ubk < ubk0) atomicMin(reinterpret_cast<int*>(qt), __float_as_int(ubk));
 }
@@ -461,7 +497,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     scan_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_off,
                    const __grid_constant__ CUtensorMap map_arena) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-align the dynamic smem base (SWIZZLE_128B atoms)
+    // 1024-align the dynamic smem base (swizzle atoms)
     const uint32_t raw_s = smem_u32(smem_raw);
     const uint32_t pad = ((raw_s + 1023u) & ~1023u) - raw_s;
     constexpr int kNS = TcCfg<KT>::NS, kNU = TcCfg<KT>::NU, kKCs = TcCfg<KT>::KC;
@@ -469,19 +505,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     float* scratch = reinterpret_cast<float*>(sB + kNS * kStage);  // [kWG][32][kM] pass-2 dots
     float* cand_lb = scratch + kWG * 32 * kM;                        // [kWG][kKCs][kM]
     uint32_t* cand_loc = reinterpret_cast<uint32_t*>(cand_lb + kWG * kKCs * kM);
-    float* nslots = reinterpret_cast<float*>(cand_loc + kWG * kKCs * kM);  // [kNB][kGU][64] norms
-    uint64_t* bars = reinterpret_cast<uint64_t*>(nslots + kNB * kGU * kNormFloats);
+    float* nslots = reinterpret_cast<float*>(cand_loc + kWG * kKCs * kM);  // [kNR][kGU][64] norms
+    uint64_t* bars = reinterpret_cast<uint64_t*>(nslots + kNR * kGU * kNormFloats);
     uint64_t* full = bars;                 // kNU
     uint64_t* empty = full + kNU;          // kNU
     uint64_t* acc_full = empty + kNU;      // kNB
     uint64_t* acc_empty = acc_full + kNB;  // kNB
-    uint64_t* a_full = acc_empty + kNB;    // 1
-    uint64_t* a_free = a_full + 1;         // 1
-    uint64_t* it_full = a_free + 1;        // 2
-    uint64_t* it_empty = it_full + 2;      // 2
-    uint64_t* nfull = it_empty + 2;        // kNB
-    int* ring = reinterpret_cast<int*>(nfull + kNB);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 2);
+    uint64_t* a_full = acc_empty + kNB;    // 2 (A buffers)
+    uint64_t* a_free = a_full + 2;         // 2
+    uint64_t* it_full = a_free + 2;        // kRing
+    uint64_t* it_empty = it_full + kRing;  // kRing
+    uint64_t* nfull = it_empty + kRing;    // kNR
+    uint64_t* nempty = nfull + kNR;        // kNR
+    TcItem* ring = reinterpret_cast<TcItem*>(nempty + kNR);  // kRing decoded items
+    float* cent_s = reinterpret_cast<float*>(ring + kRing);  // [kWG][kMaxD] the item's centroid
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cent_s + kWG * kMaxD);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t D = p.D;
@@ -493,17 +531,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int b = 0; b < kNB; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], 4);
-            mbar_init(&nfull[b], 1);
         }
-        mbar_init(a_full, kWG);
-        mbar_init(a_free, 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int r = 0; r < kNR; ++r) {
+            mbar_init(&nfull[r], 1);
+            mbar_init(&nempty[r], 4);  // the 4 warps of the unit's warpgroup
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&a_full[a], kWG);
+            mbar_init(&a_free[a], 1);
+        }
+        for (int s = 0; s < kRing; ++s) {
             mbar_init(&it_full[s], 1);
             mbar_init(&it_empty[s], 1 + 4 * kWG);
         }
         fence_mbar_init();
     }
-    if (warp == 1) {  // TMEM: A hi/lo + kNB accumulators
+    if (warp == 1) {  // TMEM: 2 A buffers + kNB accumulators
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
                      "r"(kTmemCols)
@@ -517,88 +560,138 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint32_t n_items = *p.n_items_ptr;
     const uint32_t stages = smem_u32(sB);
 
+    // Work items flow through a ring of kRing DECODED items: the producer claims
+    // and decodes item seq + 1 before it issues item seq's loads, so the math
+    // warpgroups can build item seq + 1's A operand (into the other TMEM A buffer)
+    // before they filter item seq — the MMAs never wait for an A build.
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
-            uint32_t unit = 0;
-            for (uint32_t seq = 0;; ++seq) {
-                const uint32_t rs = seq & 1;
-                mbar_wait(&it_empty[rs], ((seq >> 1) & 1) ^ 1);
+            TcProf pf;
+            pf.start();
+            auto fetch = [&](uint32_t seq) -> bool {
+                const uint32_t rs = seq % kRing;
+                mbar_wait(&it_empty[rs], ((seq / kRing) & 1) ^ 1);
                 const uint32_t it = atomicAdd(p.item_ctr, 1u);
-                const int v = it < n_items ? (int)it : -1;
-                ring[rs] = v;
-                mbar_arrive(&it_full[rs]);
-                if (v < 0) break;
-                const TcItem d = tc_decode(p, it);
+                TcItem d{};
+                if (it < n_items) d = tc_decode(p, it);
+                ring[rs] = d;
+                mbar_arrive(&it_full[rs]);  // release: the item is visible to the consumers
+                return d.valid != 0;
+            };
+            uint32_t unit = 0;
+            bool have = fetch(0);
+            pf.mark(1);
+            for (uint32_t seq = 0; have; ++seq) {
+                const TcItem d = ring[seq % kRing];
+                have = fetch(seq + 1);
+                pf.mark(1);
+                // hoisted per-item lookups: the offline segment's first group, the
+                // list's block-table row (one entry per gpb groups, cached)
+                const uint32_t og = (d.off + 31u) >> 5, R = 2u * p.Dk;
+                const uint64_t offg0 = og ? p.L.off_start[d.c] / 32u : 0ull;
+                const int32_t* trow = p.L.table + (uint64_t)d.c * p.L.MLB;
+                uint32_t cmid = 0xffffffffu;
+                uint64_t cblk = 0;
                 for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
                     const uint32_t us = unit % kNU;
                     mbar_wait(&empty[us], ((unit / kNU) & 1) ^ 1);
+                    pf.mark(2);
                     const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
-                    mbar_arrive_expect_tx(&full[us], ng * 2u * p.Dk * 128u);
-                    const uint32_t b = unit % kNB;
-                    uint64_t ng_idx[kGU];
-                    bool ng_ar[kGU];
-                    for (uint32_t h = 0; h < ng; ++h) {
-                        bool ar;
-                        int row;
-                        group_row(p.L, d.c, d.off, j0 + h, ar, row);
-                        tma_load_2d(sB + (us * kGU + h) * kStage, ar ? &map_arena : &map_off, 0, row,
-                                    &full[us]);
-                        ng_idx[h] = (uint64_t)row / (2u * p.Dk);
-                        ng_ar[h] = ar;
+                    mbar_arrive_expect_tx(&full[us], ng * 2u * p.Dk * 64u);
+                    const uint32_t nsl = unit % kNR;
+                    uint64_t gidx[kGU];
+                    bool gar[kGU];
+#pragma unroll
+                    for (int h = 0; h < kGU; ++h) {
+                        if ((uint32_t)h >= ng) break;
+                        const uint32_t j = j0 + h;
+                        if (j < og) {
+                            gar[h] = false;
+                            gidx[h] = offg0 + j;
+                        } else {
+                            const uint32_t jj = j - og, mid = jj / p.L.gpb, gi = jj - mid * p.L.gpb;
+                            if (mid != cmid) {
+                                cmid = mid;
+                                cblk = (uint64_t)trow[mid];
+                            }
+                            gar[h] = true;
+                            gidx[h] = cblk * p.L.gpb + gi;
+                        }
+                        tma_load_2d(sB + (us * kGU + h) * kStage, gar[h] ? &map_arena : &map_off, 0,
+                                    (int)(gidx[h] * R), &full[us]);
                     }
-                    // the unit's group norms -> norm slot b, once unit - kNB released it
-                    mbar_wait(&acc_empty[b], ((unit / kNB) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&nfull[b], ng * kNormFloats * 4u);
-                    for (uint32_t h = 0; h < ng; ++h)
-                        bulk_g2s(nslots + (b * kGU + h) * kNormFloats,
-                                 (ng_ar[h] ? p.arena_nrm : p.off_nrm) + ng_idx[h] * kNormFloats,
-                                 kNormFloats * 4u, &nfull[b]);
+                    pf.mark(3);
+                    // the unit's group norms -> norm slot nsl, once unit - kNR released it
+                    mbar_wait(&nempty[nsl], ((unit / kNR) & 1) ^ 1);
+                    pf.mark(4);
+                    mbar_arrive_expect_tx(&nfull[nsl], ng * kNormFloats * 4u);
+                    if (ng == 2 && gar[0] == gar[1] && gidx[1] == gidx[0] + 1) {  // adjacent: one copy
+                        bulk_g2s(nslots + nsl * kGU * kNormFloats,
+                                 (gar[0] ? p.arena_nrm : p.off_nrm) + gidx[0] * kNormFloats,
+                                 2 * kNormFloats * 4u, &nfull[nsl]);
+                    } else {
+                        for (uint32_t h = 0; h < ng; ++h)
+                            bulk_g2s(nslots + (nsl * kGU + h) * kNormFloats,
+                                     (gar[h] ? p.arena_nrm : p.off_nrm) + gidx[h] * kNormFloats,
+                                     kNormFloats * 4u, &nfull[nsl]);
+                    }
+                    pf.mark(3);
                 }
             }
+            pf.report("producer", warp);
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
         // N = 32*kGU: the unit's groups sit in consecutive stages, kStage apart (LBO)
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) |
+        // D fp32, A/B bf16, A K-major (TMEM), B MN-major, N = 32*kGU, M = 128
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
                                (((32u * kGU) >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
-        uint32_t unit = 0, ne = 0;
+        uint32_t unit = 0;
+        TcProf pf;
+        pf.start();
         for (uint32_t seq = 0;; ++seq) {
-            const uint32_t rs = seq & 1;
-            mbar_wait(&it_full[rs], (seq >> 1) & 1);
-            const int v = ring[rs];
+            const uint32_t rs = seq % kRing;
+            mbar_wait(&it_full[rs], (seq / kRing) & 1);
+            pf.mark(0);
+            const TcItem d = ring[rs];
             __syncwarp();
             if (lane == 0) mbar_arrive(&it_empty[rs]);
-            if (v < 0) break;
-            const TcItem d = tc_decode(p, (uint32_t)v);
-            if (d.g1 <= d.g0) continue;
-            mbar_wait(a_full, ne & 1);
-            ++ne;
+            if (!d.valid) break;
+            const uint32_t ab = seq & 1;  // this item's A buffer
+            mbar_wait(&a_full[ab], (seq >> 1) & 1);
+            pf.mark(2);
+            const uint32_t abase = tmem_base + ab * kColA2;
             for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
                 const uint32_t us = unit % kNU, b = unit % kNB;
                 mbar_wait(&full[us], (unit / kNU) & 1);
+                pf.mark(3);
                 mbar_wait(&acc_empty[b], ((unit / kNB) & 1) ^ 1);
+                pf.mark(4);
                 __syncwarp();
                 tc_fence_after();
                 {
-                    // 3xTF32: A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (A from TMEM, B from smem);
-                    // descriptors advance 1024 B (64 in the >>4 address field) per K-step
-                    const uint32_t bh0 = stages + us * kGU * (uint32_t)kStage, bl0 = bh0 + p.Dk * 128u;
+                    // 3xBF16: A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (A from TMEM, B from smem);
+                    // a K-step is 16 rows of 64 B: descriptors advance 1024 B (64 in the
+                    // >>4 address field), A 8 TMEM columns (16 bf16)
+                    const uint32_t bh0 = stages + us * kGU * (uint32_t)kStage, bl0 = bh0 + p.Dk * 64u;
                     const uint32_t dcol = tmem_base + kColAcc + b * 32 * kGU;
-                    const uint64_t bh = umma_desc(bh0, kStage, 512, 1);
-                    const uint64_t bl = umma_desc(bl0, kStage, 512, 1);
-                    const uint32_t nks = p.Dk / 8;
+                    const uint64_t bh = umma_desc(bh0, kStage, 512, 4);
+                    const uint64_t bl = umma_desc(bl0, kStage, 512, 4);
+                    const uint32_t nks = p.Dk / 16;
                     for (uint32_t ks = 0; ks < nks; ++ks)
-                        mma3_tf32_elect(dcol, tmem_base + ks * 8, tmem_base + kColAlo + ks * 8,
+                        mma3_bf16_elect(dcol, abase + ks * 8, abase + kColAlo + ks * 8,
                                         bh + ks * 64ull, bl + ks * 64ull, idesc, ks);
                     mma_commit_elect(&acc_full[b]);
                     mma_commit_elect(&empty[us]);
                 }
                 __syncwarp();
+                pf.mark(5);
             }
-            mma_commit_elect(a_free);  // A may be rewritten once these MMAs retire
+            mma_commit_elect(&a_free[ab]);  // the A buffer may be rewritten once these retire
             __syncwarp();
         }
+        pf.report("mma", warp);
     } else {
         // ------------------------------------------------ math warpgroups
         const int wg = (warp - 2) >> 2;               // 0: builds A_hi, 1: builds A_lo
@@ -606,15 +699,87 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int m = 32 * q4 + lane;                 // query row of the tile
         const int wt = threadIdx.x - 64 - 128 * wg;   // 0..127 within the warpgroup
         const uint32_t taddr_lane = (uint32_t)(32 * q4) << 16;
-        uint32_t unit = 0, ne = 0;
-        for (uint32_t seq = 0;; ++seq) {
-            const uint32_t rs = seq & 1;
-            mbar_wait(&it_full[rs], (seq >> 1) & 1);
-            const int v = ring[rs];
+        TcProf pf;
+        pf.start();
+        // read item seq from the ring and write its A operand (centred queries
+        // r = q - c of the tile, split r_hi = bf16_rn(r), r_lo = bf16_rn(r - r_hi);
+        // lane m = query row, column = a pair of dims) into A buffer seq & 1
+        auto build = [&](uint32_t seq, TcItem& d, float& nq) -> bool {
+            const uint32_t rs = seq % kRing;
+            mbar_wait(&it_full[rs], (seq / kRing) & 1);
+            d = ring[rs];
             __syncwarp();
             if (lane == 0) mbar_arrive(&it_empty[rs]);
-            if (v < 0) break;
-            const TcItem d = tc_decode(p, (uint32_t)v);
+            if (!d.valid) return false;
+            pf.mark(0);
+            const uint32_t ab = seq & 1;
+            if (seq >= 2) mbar_wait(&a_free[ab], ((seq - 2) >> 1) & 1);
+            pf.mark(2);
+            const bool active = (uint32_t)m < d.npairs;
+            const uint32_t pair = active ? d.pairs[m] : 0u;
+            const float* q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
+            // every load in flight at once: the thread's whole query row (registers)
+            // and the list centroid (one element per thread -> the warpgroup's smem row)
+            float4 qv[kMaxD / 4];
+#pragma unroll
+            for (int i = 0; i < kMaxD / 4; ++i)
+                qv[i] = (active && (uint32_t)(4 * i) < p.Dp)
+                            ? __ldg(reinterpret_cast<const float4*>(q) + i)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+            float* cs = cent_s + wg * kMaxD;
+            cs[wt] = (uint32_t)wt < D ? __ldg(p.centroids + (uint64_t)d.c * D + wt) : 0.f;
+            named_bar(1 + wg, 128);
+            pf.mark(9);
+            nq = 0.f;
+            __syncwarp();
+            tc_fence_after();
+#pragma unroll
+            for (int c0 = 0; c0 < kMaxD; c0 += 64) {
+                if ((uint32_t)c0 >= p.Dk) break;
+                uint32_t vv[32];
+#pragma unroll
+                for (int i = 0; i < 64; i += 4) {
+                    const int k = c0 + i;
+                    const float4 c4 = *reinterpret_cast<const float4*>(cs + k);
+                    const float qa[4] = {qv[k / 4].x, qv[k / 4].y, qv[k / 4].z, qv[k / 4].w};
+                    const float ca[4] = {c4.x, c4.y, c4.z, c4.w};
+                    float ra[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        // padded dims: q and the centroid row are zero there
+                        const float r = __fsub_rn(qa[e], ca[e]);
+                        nq = __fadd_rn(nq, __fmul_rn(r, r));
+                        ra[e] = r;
+                    }
+                    uint32_t h0, l0, h1, l1;
+                    bf16_split2(ra[0], ra[1], h0, l0);
+                    bf16_split2(ra[2], ra[3], h1, l1);
+                    vv[i / 2] = wg == 0 ? h0 : l0;
+                    vv[i / 2 + 1] = wg == 0 ? h1 : l1;
+                }
+                __syncwarp();
+                BIVF_TMEM_ST32(tmem_base + ab * kColA2 + taddr_lane + (wg ? kColAlo : 0u) + c0 / 2, vv);
+            }
+            pf.mark(3);
+            __syncwarp();
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            pf.mark(10);
+            tc_fence_before();
+            named_bar(1 + wg, 128);
+            if (wt == 0) mbar_arrive(&a_full[ab]);
+            if (p.dense_out && wg == 0 && active && d.chunk == 0)
+                p.dense_nq[p.dense_list_base ? pair : pair / p.P] = nq;
+            pf.mark(3);
+            return true;
+        };
+        uint32_t unit = 0;
+        TcItem d;
+        float nq = 0.f;
+        bool have = build(0, d, nq);
+        for (uint32_t seq = 0; have; ++seq) {
+            TcItem dn;
+            float nqn = 0.f;
+            const bool hn = build(seq + 1, dn, nqn);  // next item's A while this one's MMAs run
             const bool active = (uint32_t)m < d.npairs;
             const uint32_t pair = active ? d.pairs[m] : 0u;
             const uint64_t run = ((((uint64_t)pair * p.maxch + d.chunk) << 1) | (uint32_t)wg);
@@ -627,64 +792,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             float ubk = __int_as_float(0x7f800000);
             uint32_t ncand = 0;
             bool overflow = false;
-            if (d.g1 > d.g0) {
-                // A = centred queries r = q - c of the tile, r = r_hi + r_lo (r_hi = TF32
-                // truncation, r_lo exact in fp32): lane m = query row, columns = dims.
-                if (ne > 0) mbar_wait(a_free, (ne - 1) & 1);
-                ++ne;
-                const float* q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
-                const float* cen = p.centroids + (uint64_t)d.c * D;
-                float nq = 0.f;
-                __syncwarp();
-                tc_fence_after();
-                for (uint32_t c0 = 0; c0 < p.Dk; c0 += 32) {
-                    uint32_t vv[32];
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
-                        const uint32_t k = c0 + i;
-                        float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (active && k < p.Dp) qv = *reinterpret_cast<const float4*>(q + k);
-                        const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            float r = 0.f;
-                            if (active && k + e < D) r = __fsub_rn(qa[e], __ldg(cen + k + e));
-                            nq = __fadd_rn(nq, __fmul_rn(r, r));
-                            const float h = tf32_trunc(r);
-                            vv[i + e] = __float_as_uint(wg == 0 ? h : __fsub_rn(r, h));
-                        }
-                    }
-                    __syncwarp();
-                    BIVF_TMEM_ST32(tmem_base + taddr_lane + (wg ? kColAlo : 0u) + c0, vv);
-                }
-                __syncwarp();
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                tc_fence_before();
-                named_bar(1 + wg, 128);
-                if (wt == 0) mbar_arrive(a_full);
-                if (p.dense_out && wg == 0 && active && d.chunk == 0)
-                    p.dense_nq[p.dense_list_base ? pair : pair / p.P] = nq;
-                uint64_t dbase = 0;  // dense mode: this thread's base element
-                if (p.dense_out) {
-                    if (p.dense_list_base) {
-                        const uint32_t tile = (uint32_t)((d.pairs - p.plist) - p.qoff[d.c]) / kM;
-                        const uint32_t ngl = ivf_ngroups(p.L, d.off, d.len);
-                        dbase = p.dense_list_base[d.c] + (uint64_t)tile * ngl * 32u * kM + m;
-                    } else {
-                        dbase = (uint64_t)(pair / p.P) * p.dense_ld;
-                    }
-                }
-                for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
-                    if ((unit & 1u) != (uint32_t)wg) continue;
-                    tc_unit<KT>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
-                                active, nq, ubl, ubk, ncand, overflow, clb, cloc,
-                                scratch + wg * 32 * kM + m, nslots, nfull,
-                                p.qthr + (active ? pair / p.P : 0u),
-                                dbase, (uint32_t)m);
+            uint64_t dbase = 0;  // dense mode: this thread's base element
+            if (p.dense_out) {
+                if (p.dense_list_base) {
+                    const uint32_t tile = (uint32_t)((d.pairs - p.plist) - p.qoff[d.c]) / kM;
+                    const uint32_t ngl = ivf_ngroups(p.L, d.off, d.len);
+                    dbase = p.dense_list_base[d.c] + (uint64_t)tile * ngl * 32u * kM + m;
+                } else {
+                    dbase = (uint64_t)(pair / p.P) * p.dense_ld;
                 }
             }
+            pf.mark(1);
+            for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
+                if ((unit & 1u) != (uint32_t)wg) continue;
+                tc_unit<KT>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
+                            active, nq, ubl, ubk, ncand, overflow, clb, cloc,
+                            scratch + wg * 32 * kM + m, nslots, nfull, nempty,
+                            p.qthr + (active ? pair / p.P : 0u),
+                            dbase, (uint32_t)m, pf);
+            }
+            pf.mark(8);
             // run output: k upper bounds + surviving candidates (compacted in place)
-            if (active && !p.dense_out) {
+            if (active && !p.dense_out && !p.seed_groups) {
 #pragma unroll
                 for (int i = 0; i < KT; ++i)
                     if (i >= KT - (int)p.k) p.ub[run * p.k + (i - (KT - (int)p.k))] = ubl[i];
@@ -701,7 +830,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 p.ccount[run] = overflow ? kOverflow : w;
             }
+            pf.mark(8);
+            d = dn;
+            nq = nqn;
+            have = hn;
         }
+        pf.report("math", warp);
     }
     __syncthreads();
     if (warp == 1) {
@@ -1247,10 +1381,13 @@ __global__ void dense_list_len_kernel(DevLists L, const uint32_t* snap_off, cons
 }
 
 template <int KT>
-size_t tc_smem_bytes() {
+constexpr size_t tc_smem_bytes() {
     return 1024 + TcCfg<KT>::NS * kStage + kWG * 32 * kM * 4 + kWG * TcCfg<KT>::KC * kM * 8 +
-           kNB * kGU * kNormFloats * 4 + (2 * TcCfg<KT>::NU + 3 * kNB + 6) * 8 + 16 + 16;
+           kNR * kGU * kNormFloats * 4 +
+           (2 * TcCfg<KT>::NU + 2 * kNB + 2 * kNR + 2 * kRing + 4) * 8 + kRing * sizeof(TcItem) +
+           kWG * kMaxD * 4 + 16;
 }
+static_assert(tc_smem_bytes<16>() <= 232448 && tc_smem_bytes<32>() <= 232448, "smem budget");
 
 }  // namespace
 
@@ -1283,12 +1420,12 @@ cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUte
     if (!enc) return cudaErrorNotSupported;
     const uint32_t K = mirror_k(D);
     cuuint64_t dims[2] = {32, std::max<cuuint64_t>(groups * 2ull * K, 1)};
-    cuuint64_t strides[1] = {128};
+    cuuint64_t strides[1] = {64};
     cuuint32_t box[2] = {32, 2 * K};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+    CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<float*>(base), dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                     CU_TENSOR_MAP_SWIZZLE_64B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -1336,14 +1473,31 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     SearchShape s2 = sh;
     s2.QT = kM;
     cudaError_t e = cudaSuccess;
+    // Seeded filter scan (batches of >= 512 queries): a seeding pass scans the
+    // first unit (2 groups = 64 vectors) of every query's NEAREST list (probe
+    // rank 0) and publishes the k-th smallest upper bound as the query's shared
+    // threshold (a valid bound: those vectors are probed); the full scan then
+    // filters against it from its first group on (no per-run threshold warm-up,
+    // far fewer pass-2 slots).  The seeding pass writes no run output.
+    static const uint32_t two_min = [] {
+        const char* v = std::getenv("BIVF_TC_TWO_PHASE_MIN");  // tuning aid
+        return v ? (uint32_t)atoi(v) : 512u;
+    }();
+    static const uint32_t seed_g = [] {
+        const char* v = std::getenv("BIVF_TC_SEED_GROUPS");  // tuning aid
+        return v ? std::max(1u, (uint32_t)atoi(v)) : (uint32_t)kGU;
+    }();
+    const bool two = !dense && sh.P >= 2 && sh.nq >= two_min;
+    SearchShape sa = s2;  // seeding pass: rank-0 pairs, one chunk per list
+    sa.maxch = 1;
     if (!(dense && dense->list_base)) {  // the IVF dense path planned in launch_dense_plan
-        e = launch_plan(L, B, probes, s2, s);
+        e = two ? launch_plan_ranked(L, B, probes, sa, 0, 1, true, s) : launch_plan(L, B, probes, s2, s);
         if (e != cudaSuccess) return e;
     }
     TcParams p{};
     p.L = L;
     p.D = L.D;
-    p.Dk = (L.D + 7) & ~7u;
+    p.Dk = (L.D + 15) & ~15u;
     p.Dp = pad4(L.D);
     p.k = sh.k;
     p.P = sh.P;
@@ -1393,11 +1547,18 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     if (ev0) cudaEventRecord(ev0, s);
     int grid = std::max(1, std::min(num_sms, max_grid));  // no idle CTAs holding whole SMs
     if (const char* g = std::getenv("BIVF_TC_GRID")) grid = std::max(1, atoi(g));  // debugging aid
-    if (sh.k <= 16) scan_tc_kernel<16><<<grid, kTcThreads, sm16, s>>>(p, map_off, map_arena);
-    else scan_tc_kernel<32><<<grid, kTcThreads, sm32, s>>>(p, map_off, map_arena);
-    count_launch();
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    for (int phase = 0; phase < (two ? 2 : 1); ++phase) {
+        p.seed_groups = two && phase == 0 ? seed_g : 0u;
+        if (two && phase == 1) {
+            e = launch_plan(L, B, probes, s2, s);
+            if (e != cudaSuccess) return e;
+        }
+        if (sh.k <= 16) scan_tc_kernel<16><<<grid, kTcThreads, sm16, s>>>(p, map_off, map_arena);
+        else scan_tc_kernel<32><<<grid, kTcThreads, sm32, s>>>(p, map_off, map_arena);
+        count_launch();
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     if (ev1) cudaEventRecord(ev1, s);
     const uint32_t wpb = 4;
     if (dense && dense->list_base) {

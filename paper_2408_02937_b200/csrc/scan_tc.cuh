@@ -10,9 +10,9 @@
 
 namespace bivf {
 
-// candidate slots per run (query, list chunk, warpgroup): 24 for k <= 16, 48 for
+// candidate slots per run (query, list chunk, warpgroup): 40 for k <= 16, 56 for
 // k <= 32; global buffers use the larger stride
-constexpr uint32_t kKC = 48;
+constexpr uint32_t kKC = 56;
 constexpr uint32_t kOverflow = 0xffffffffu;  // ccount marker: buffer overflowed -> exact rescan
 
 // per-search scratch of the TC path (lease workspace)
@@ -48,7 +48,7 @@ cudaError_t launch_dense_plan(const DevLists& L, const PlanBufs& B, const long l
                               void* tmp, size_t tmp_bytes, uint64_t* total, cudaStream_t s);
 
 // 2-D TMA map over a scan mirror region (mirror.cuh: `groups` groups of
-// 2K rows of 32 floats), box = {32, 2K}, SWIZZLE_128B_ATOM_32B.
+// 2K rows of 32 bf16), box = {32, 2K}, SWIZZLE_64B.
 cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUtensorMap* out);
 
 cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,

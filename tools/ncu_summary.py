@@ -58,11 +58,14 @@ def rep_summary(rep, out):
                                   sorted(stalls.items(), key=lambda x: -x[1])[:6]}
         kernels.append(k)
     summ = {"source": rep, "kernels": kernels}
-    tc = [k for k in kernels if "scan_tc_kernel" in k["kernel"]]
-    if tc:  # the dominant launch (the list scan; the quantizer is the short <32> one)
-        k = max(tc, key=lambda x: x.get("gpu__time_duration.sum", 0))
-        summ["dram_bytes_per_launch"] = int(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0))
-        summ["duration_ms"] = k.get("gpu__time_duration.sum", 0) * 1e-6  # base unit: ns
+    # the list scan of one search = every scan_tc_kernel<16> launch captured (the two
+    # phases of the two-phase scan; the coarse quantizer is the <32> instantiation)
+    tc = [k for k in kernels if "scan_tc_kernel<16>" in k["kernel"]]
+    if tc:
+        summ["dram_bytes_per_launch"] = int(sum(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0)
+                                                for k in tc))
+        summ["duration_ms"] = sum(k.get("gpu__time_duration.sum", 0) for k in tc) * 1e-6  # base unit: ns
+        summ["scan_launches"] = len(tc)
     with open(out, "w") as f:
         json.dump(summ, f, indent=1)
     print(json.dumps(summ, indent=1)[:3000])
