@@ -268,8 +268,12 @@ def run_ours(args, dist):
     ms = e0.elapsed_time(e1)
     ms = max_over_ranks(dist, ms)
 
-    # --- e2e: same steps through the host C-ABI call (H2D + D2H inside)
-    hq = queries
+    # --- e2e: same steps through the host C-ABI call (H2D + D2H inside), inputs
+    # and outputs in page-locked host memory (bivf_host_alloc): DMA'd directly
+    hq = bivf.pinned_empty(queries.shape, np.float32)
+    hq[:] = queries
+    h_out = (bivf.pinned_empty((len(hq), K), np.int64), bivf.pinned_empty((len(hq), K), np.float32),
+             bivf.pinned_empty((len(hq),), np.uint32))
     if world > 1:  # the public sharded API: local search, NCCL all-gather, device merge, D2H
         from paper_2408_02937_b200.sharded import ShardedIndex
         sharded = ShardedIndex(ix, rank, world, next_id=N_BASE)
@@ -278,7 +282,7 @@ def run_ours(args, dist):
             return sharded.search(hq, K, NPROBE)
     else:
         def e2e_call():
-            return ix.search_batch(hq, K, NPROBE)
+            return ix.search_batch(hq, K, NPROBE, out=h_out)
     for _ in range(args.warmup):  # pinned staging buffers, OpenMP pool
         e2e_call()
     barrier(dist)

@@ -72,6 +72,10 @@ const char* bivf_last_error(void);
 const char* bivf_version(void);
 /* number of visible CUDA devices (0 on a host without GPU) */
 int bivf_device_count(void);
+/* Page-locked host memory for search inputs/outputs: bivf_search DMAs such
+ * buffers directly (no staging copy).  Plain host memory works too. */
+bivf_status bivf_host_alloc(size_t bytes, void** out);
+bivf_status bivf_host_free(void* p);
 
 /* ---- lifecycle ------------------------------------------------------- */
 /* ClusterIndex(IndexConfig) storage (ivf_index.cpp:36-45): allocates the whole

@@ -124,6 +124,8 @@ SIGNATURES = {
     "bivf_last_error": (C.c_char_p, []),
     "bivf_version": (C.c_char_p, []),
     "bivf_device_count": (C.c_int, []),
+    "bivf_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
+    "bivf_host_free": (C.c_int, [vp]),
     "bivf_create": (C.c_int, [C.POINTER(Config), C.POINTER(vp)]),
     "bivf_destroy": (C.c_int, [vp]),
     "bivf_get_config": (C.c_int, [vp, C.POINTER(Config)]),

@@ -73,6 +73,24 @@ int bivf_device_count(void) {
 }
 uint64_t bivf_kernel_launches(void) { return bivf::g_launches.load(); }
 
+bivf_status bivf_host_alloc(size_t bytes, void** out) {
+    return guard([&] {
+        need(out, "out");
+        *out = nullptr;
+        const cudaError_t e = cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw bivf::Error(BIVF_ECUDA, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+        }
+    });
+}
+
+bivf_status bivf_host_free(void* p) {
+    return guard([&] {
+        if (p) cudaFreeHost(p);
+    });
+}
+
 bivf_status bivf_create(const bivf_config* cfg, bivf_index** out) {
     return guard([&] {
         need(cfg, "cfg");

@@ -60,6 +60,18 @@ void PinBuf::ensure(size_t n) {
     bytes = grow;
 }
 
+// True for page-locked host memory (cudaHostAlloc / cudaHostRegister): the
+// search path DMAs such buffers directly instead of staging them.
+static bool is_pinned(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 // Host staging copies of the search path (user buffers <-> pinned lease
 // buffers) on the OpenMP pool: one thread moves ~6-10 GB/s, the copy of a
 // 10K x 128 query batch would otherwise be a sizeable part of the call.
@@ -913,6 +925,10 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
         Workspace w = carve(*l, m, (uint32_t)k, (uint32_t)nprobe, sh.maxch, sh.fnch);
         const size_t in_b = (size_t)m * D_ * 4;
         const size_t out_b = (size_t)m * k * 12 + (size_t)m * 4;
+        // page-locked user buffers are DMA'd directly (no host staging copy)
+        const bool q_pin = is_pinned(q + s * D_);
+        const bool o_pin = is_pinned(out_d + s * k) && is_pinned(out_ids + s * k) &&
+                           (!out_cnt || is_pinned(out_cnt + s));
         l->pin.ensure(in_b + out_b + 256);
         char* pin = l->pin.as<char>();
         float* pd = reinterpret_cast<float*>(pin + align_up(in_b, 64));
@@ -928,23 +944,32 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
             // stage the queries in ~1 MB pieces: the DMA of piece i overlaps the
             // host copy of piece i+1 (a per-piece quantizer was measured slower:
             // smaller quantizer launches cost more than the DMA they hide)
-            const size_t piece = std::max<size_t>(1u << 20, (size_t)D_ * 4 * 256);
-            for (size_t o = 0; o < in_b; o += piece) {
-                const size_t nb = std::min(piece, in_b - o);
-                par_memcpy(pin + o, reinterpret_cast<const char*>(q + s * D_) + o, nb);
-                BIVF_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(w.qraw) + o, pin + o, nb,
-                                          cudaMemcpyHostToDevice, l->stream));
+            if (q_pin) {
+                BIVF_CUDA(cudaMemcpyAsync(w.qraw, q + s * D_, in_b, cudaMemcpyHostToDevice, l->stream));
+            } else {
+                const size_t piece = std::max<size_t>(1u << 20, (size_t)D_ * 4 * 256);
+                for (size_t o = 0; o < in_b; o += piece) {
+                    const size_t nb = std::min(piece, in_b - o);
+                    par_memcpy(pin + o, reinterpret_cast<const char*>(q + s * D_) + o, nb);
+                    BIVF_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(w.qraw) + o, pin + o, nb,
+                                              cudaMemcpyHostToDevice, l->stream));
+                }
             }
             enqueue_search(*l, w.qraw, m, (uint32_t)k, (uint32_t)nprobe, w);
-            BIVF_CUDA(cudaMemcpyAsync(pd, w.out_d, (size_t)m * k * 4, cudaMemcpyDeviceToHost, l->stream));
-            BIVF_CUDA(cudaMemcpyAsync(pi, w.out_i, (size_t)m * k * 8, cudaMemcpyDeviceToHost, l->stream));
-            BIVF_CUDA(cudaMemcpyAsync(pc, w.out_cnt, (size_t)m * 4, cudaMemcpyDeviceToHost, l->stream));
+            float* hd = o_pin ? out_d + s * k : pd;
+            long long* hi = o_pin ? reinterpret_cast<long long*>(out_ids + s * k) : pi;
+            uint32_t* hc = o_pin && out_cnt ? out_cnt + s : pc;
+            BIVF_CUDA(cudaMemcpyAsync(hd, w.out_d, (size_t)m * k * 4, cudaMemcpyDeviceToHost, l->stream));
+            BIVF_CUDA(cudaMemcpyAsync(hi, w.out_i, (size_t)m * k * 8, cudaMemcpyDeviceToHost, l->stream));
+            BIVF_CUDA(cudaMemcpyAsync(hc, w.out_cnt, (size_t)m * 4, cudaMemcpyDeviceToHost, l->stream));
             BIVF_CUDA(cudaEventRecord(l->done, l->stream));
         }
         BIVF_CUDA(cudaEventSynchronize(l->done));
-        par_memcpy(out_d + s * k, pd, (size_t)m * k * 4);
-        par_memcpy(out_ids + s * k, pi, (size_t)m * k * 8);
-        if (out_cnt) std::memcpy(out_cnt + s, pc, (size_t)m * 4);
+        if (!o_pin) {
+            par_memcpy(out_d + s * k, pd, (size_t)m * k * 4);
+            par_memcpy(out_ids + s * k, pi, (size_t)m * k * 8);
+            if (out_cnt) std::memcpy(out_cnt + s, pc, (size_t)m * 4);
+        }
         if (timing_) record_timings(*l);
     }
 }

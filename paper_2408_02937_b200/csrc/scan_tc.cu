@@ -286,7 +286,7 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
                                           const float* wn, bool active, float nq,
                                           const float (&dot)[32], float (&ubl)[KT], float& ubk,
                                           uint32_t& ncand, bool& overflow, float* clb,
-                                          uint32_t* cloc, float* scr) {
+                                          uint32_t* cloc, float* scr, TcProf& pf) {
     if (!active) return;
     // pass 1: slot n can still enter the top-k only if its lower bound a - eps' <= ubk,
     // i.e. dot >= V[n] + W (V = kVScale*ns from the mirror norms; a < 0 passes too,
@@ -304,6 +304,7 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
         }
         if (!(fmaxf(m0, m1) >= W)) return;
     }
+
     // valid slots of group j, from the snapshot (no table lookups)
     uint32_t nvalid;
     {
@@ -477,9 +478,11 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
 #pragma unroll
     for (int h = 0; h < kGU; ++h) {
         if ((uint32_t)h >= ng) break;
+        pf.mark(7);
         if constexpr (!kEarlyRelease) tmem_ld32(acol + 32 * h, dot[0]);
+        pf.mark(10);
         tc_filter<KT>(p, d, j0 + h, wslot + h * kNormFloats, active, nq, dot[kEarlyRelease ? h : 0],
-                      ubl, ubk, ncand, overflow, clb, cloc, scr);
+                      ubl, ubk, ncand, overflow, clb, cloc, scr, pf);
     }
     if constexpr (!kEarlyRelease) tc_fence_before();
     __syncwarp();
@@ -760,10 +763,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 __syncwarp();
                 BIVF_TMEM_ST32(tmem_base + ab * kColA2 + taddr_lane + (wg ? kColAlo : 0u) + c0 / 2, vv);
             }
-            pf.mark(3);
             __syncwarp();
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            pf.mark(10);
             tc_fence_before();
             named_bar(1 + wg, 128);
             if (wt == 0) mbar_arrive(&a_full[ab]);

@@ -152,14 +152,26 @@ class ClusterIndex:
         ids, d, cnt = self.search_batch(q, k, nprobe)
         return ids[0, : cnt[0]].copy(), d[0, : cnt[0]].copy()
 
-    def search_batch(self, queries, k, nprobe):
-        """Batched search: ids [nq,k] (-1 padded), dists [nq,k], counts [nq]."""
+    def search_batch(self, queries, k, nprobe, out=None):
+        """Batched search: ids [nq,k] (-1 padded), dists [nq,k], counts [nq].
+
+        `out` = (ids, dists, counts) preallocated (e.g. pinned_empty) receives the
+        results; page-locked queries / outputs are DMA'd without a staging copy."""
         q = _as_matrix(queries)
         if q.shape[1] != self.dim:
             raise ValueError("dimension mismatch")
         nq = q.shape[0]
         if k < 1:
             raise ValueError("search: k must be >= 1")
+        if out is not None:
+            ids, d, cnt = out
+            if (ids.shape != (nq, k) or d.shape != (nq, k) or cnt.shape != (nq,) or ids.dtype != np.int64
+                    or d.dtype != np.float32 or cnt.dtype != np.uint32 or not all(
+                        a.flags.c_contiguous for a in out)):
+                raise ValueError("out: expected C-contiguous int64/float32 [nq,k] and uint32 [nq]")
+            if nq:
+                check(lib().bivf_search(self._h, ptr(q), nq, k, nprobe, ptr(ids), ptr(d), ptr(cnt)))
+            return ids, d, cnt
         ids = np.empty((max(nq, 1), k), np.int64)
         d = np.empty((max(nq, 1), k), np.float32)
         cnt = np.empty(max(nq, 1), np.uint32)
@@ -358,6 +370,30 @@ def kmeans(points, k, max_iters=25, seed=42, device=0):
     check(lib().bivf_kmeans(x, x.shape[0], x.shape[1], k, max_iters, seed, device, cent, asg,
                             C.byref(it)))
     return cent, asg, int(it.value)
+
+
+class _HostBlock:
+    """Owner of a bivf_host_alloc block (freed when the last array view dies)."""
+
+    def __init__(self, nbytes):
+        self.p = C.c_void_p()
+        check(lib().bivf_host_alloc(max(int(nbytes), 1), C.byref(self.p)))
+
+    def __del__(self):
+        if getattr(self, "p", None) and self.p.value:
+            lib().bivf_host_free(self.p)
+            self.p = None
+
+
+def pinned_empty(shape, dtype=np.float32):
+    """numpy array in page-locked host memory (bivf_host_alloc): search inputs
+    and outputs in such memory are DMA'd directly by bivf_search."""
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape)) if np.ndim(shape) else int(shape)
+    blk = _HostBlock(n * dt.itemsize)
+    buf = (C.c_char * max(n * dt.itemsize, 1)).from_address(blk.p.value)
+    buf._bivf_block = blk  # numpy views keep `buf` (and so the block) alive
+    return np.frombuffer(buf, dtype=dt, count=n).reshape(shape)
 
 
 def device_count():

@@ -1,4 +1,4 @@
-"""The tensor-core filtered scan (tcgen05 TF32 filter + exact refine; k > 32:
+"""The tensor-core filtered scan (tcgen05 3xBF16 filter + exact refine; k > 32:
 dense TC distances + per-query exact selection) returns exactly the CUDA-core
 exact scan's and the oracle's results: same ids, same distance bits, at small
 and cfg2-like scale, with live inserts and deletes."""
@@ -135,3 +135,47 @@ def test_tc_quantizer_matches_exact(gpu_ready, C, D):
             t = (q[j, d] - cent[:, d]).astype(np.float32)
             acc = (acc + (t * t).astype(np.float32)).astype(np.float32)
         assert np.array_equal(b[j], np.lexsort((np.arange(C), acc))[: b.shape[1]])
+
+
+@pytest.mark.parametrize("D,C,T,n,comps", [(8, 6, 4, 2000, 6), (100, 10, 16, 6000, 12),
+                                           (96, 32, 128, 20000, 64)])
+def test_tc_seeded_batches_equal_exact(gpu_ready, D, C, T, n, comps):
+    """Batches of >= 512 queries take the seeded filter scan (a first pass over
+    each query's nearest list seeds the shared thresholds): still exactly the
+    CUDA-core exact scan's ids and distance bits, with inserts and deletes."""
+    base = bivf.synthetic_dataset(n, D, comps, 13)
+    cent, asg, _ = bivf.kmeans(base, C, 5, 13)
+    ix = ClusterIndex.empty(D, C, block_capacity=T, num_blocks=max(64, 4 * n // T + 4 * C))
+    ix.set_centroids(cent)
+    ix.bulk_load(base, asg)
+    ix.insert(bivf.synthetic_dataset(n // 4 + 1, D, comps, 14))
+    ix.remove(np.arange(0, n, 11))
+    q = bivf.synthetic_dataset(1500, D, comps, 15)
+    for k, npb in ((10, min(4, C)), (1, 2), (16, C), (32, min(8, C))):
+        a, b = both(ix, q, k, npb)
+        assert_same(a, b)
+
+
+def test_pinned_search_matches(gpu_ready):
+    """Page-locked inputs/outputs (pinned_empty) are DMA'd directly by
+    bivf_search; results equal the staged path's."""
+    D, C = 64, 32
+    base = bivf.synthetic_dataset(20000, D, 64, 21)
+    cent, asg, _ = bivf.kmeans(base, C, 5, 21)
+    ix = ClusterIndex.empty(D, C, block_capacity=256, num_blocks=512)
+    ix.set_centroids(cent)
+    ix.bulk_load(base, asg)
+    q = bivf.synthetic_dataset(1000, D, 64, 22)
+    hq = bivf.pinned_empty(q.shape, np.float32)
+    hq[:] = q
+    out = (bivf.pinned_empty((1000, 10), np.int64), bivf.pinned_empty((1000, 10), np.float32),
+           bivf.pinned_empty((1000,), np.uint32))
+    r = ix.search_batch(hq, 10, 8, out=out)
+    assert r[0] is out[0]
+    ref = ix.search_batch(q, 10, 8)
+    assert_same(ref, r)
+    # pinned inputs, plain outputs and vice versa
+    assert_same(ref, ix.search_batch(hq, 10, 8))
+    out2 = (bivf.pinned_empty((1000, 10), np.int64), bivf.pinned_empty((1000, 10), np.float32),
+            bivf.pinned_empty((1000,), np.uint32))
+    assert_same(ref, ix.search_batch(q, 10, 8, out=out2))
