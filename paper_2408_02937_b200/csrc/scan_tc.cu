@@ -64,6 +64,15 @@ struct TcCfg {
 // (before filtering) instead of after the filter (measured: no gain, more registers)
 constexpr bool kEarlyRelease = false;
 constexpr int kNB = 4;                     // TMEM accumulators (32 * kGU columns each; even)
+// both math warpgroups work on every unit, warpgroup g on the unit's group g
+// (instead of alternating whole units): half the per-unit epilogue latency but
+// twice the per-unit fixed cost per warp (measured slower: 1.38 -> 1.65 ms)
+#ifndef BIVF_TC_COLSPLIT
+#define BIVF_TC_COLSPLIT 0
+#endif
+constexpr bool kColSplit = BIVF_TC_COLSPLIT != 0;
+static_assert(!kColSplit || kGU == 2, "column split assumes one group per warpgroup");
+constexpr uint32_t kUnitArrivals = kColSplit ? 8 : 4;  // warps releasing a unit's accumulator
 constexpr int kRing = 4;                   // decoded work items in flight (producer lookahead)
 constexpr int kNR = 8;                     // norm slots (ring, one unit each; decoupled from kNB)
 
@@ -389,12 +398,12 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                                         float (&ubl)[KT], float& ubk, uint32_t& ncand,
                                         bool& overflow, float* clb, uint32_t* cloc,
                                         float* scr, float* nslots, uint64_t* nfull,
-                                        uint64_t* nempty, float* qt, uint64_t qrow, uint32_t m,
-                                        TcProf& pf) {
+                                        uint64_t* nempty, float* qt, float qshared, uint64_t qrow,
+                                        uint32_t m, int wg, TcProf& pf) {
     const uint32_t b = u % kNB, ns = u % kNR;
-    // the query's shared threshold: the smallest k-th upper bound any of its runs
-    // has published (a valid filter bound for every run of the query)
-    const float qshared = active ? __ldcg(qt) : ubk;
+    // qshared: the query's shared threshold (the smallest k-th upper bound any of
+    // its runs has published, a valid filter bound for every run of the query),
+    // loaded by the caller one unit ahead
     const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
     pf.mark(8);
     mbar_wait(&acc_full[b], (u / kNB) & 1);
@@ -419,6 +428,7 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
 #pragma unroll
         for (int h = 0; h < kGU; ++h) {
             if ((uint32_t)h >= ng) break;
+            if (kColSplit && h != wg) continue;
             const float* wn = wslot + h * kNormFloats;
             const int hd = kEarlyRelease ? h : 0;
             if constexpr (!kEarlyRelease) tmem_ld32(acol + 32 * h, dot[0]);
@@ -478,6 +488,7 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
 #pragma unroll
     for (int h = 0; h < kGU; ++h) {
         if ((uint32_t)h >= ng) break;
+        if (kColSplit && h != wg) continue;
         pf.mark(7);
         if constexpr (!kEarlyRelease) tmem_ld32(acol + 32 * h, dot[0]);
         pf.mark(10);
@@ -533,11 +544,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         for (int b = 0; b < kNB; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], 4);
+            mbar_init(&acc_empty[b], kUnitArrivals);
         }
         for (int r = 0; r < kNR; ++r) {
             mbar_init(&nfull[r], 1);
-            mbar_init(&nempty[r], 4);  // the 4 warps of the unit's warpgroup
+            mbar_init(&nempty[r], kUnitArrivals);  // the warps that filtered the unit
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&a_full[a], kWG);
@@ -804,13 +815,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
             }
             pf.mark(1);
+            float* qt = p.qthr + (active ? pair / p.P : 0u);
+            float qsh = active ? __ldcg(qt) : ubk;
             for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
-                if ((unit & 1u) != (uint32_t)wg) continue;
+                if (!kColSplit && (unit & 1u) != (uint32_t)wg) continue;
+                const float qcur = qsh;
+                if (active) qsh = __ldcg(qt);  // in flight during this unit, used by the next
                 tc_unit<KT>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
                             active, nq, ubl, ubk, ncand, overflow, clb, cloc,
-                            scratch + wg * 32 * kM + m, nslots, nfull, nempty,
-                            p.qthr + (active ? pair / p.P : 0u),
-                            dbase, (uint32_t)m, pf);
+                            scratch + wg * 32 * kM + m, nslots, nfull, nempty, qt, qcur,
+                            dbase, (uint32_t)m, wg, pf);
             }
             pf.mark(8);
             // run output: k upper bounds + surviving candidates (compacted in place)
