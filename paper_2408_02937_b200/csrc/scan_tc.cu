@@ -198,11 +198,11 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 // bf16 RN split of a pair of fp32 values into (hi pair, lo pair), each packed
 // low half = first element (the K order of A in TMEM, tools/tc_probe_bf16.cu)
 __device__ __forceinline__ void bf16_split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
-    const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
-    const __nv_bfloat16 l0 = __float2bfloat16_rn(__fsub_rn(x0, __bfloat162float(h0)));
-    const __nv_bfloat16 l1 = __float2bfloat16_rn(__fsub_rn(x1, __bfloat162float(h1)));
-    hi = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-    lo = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+    const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);  // one packed convert (low = x0)
+    const float2 hf = __bfloat1622float2(h);
+    const __nv_bfloat162 l = __floats2bfloat162_rn(__fsub_rn(x0, hf.x), __fsub_rn(x1, hf.y));
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 // Warp-collective issue of one 3xBF16 K-step (A_hi*B_hi, A_hi*B_lo, A_lo*B_hi):
 // the whole (converged) warp executes it, elect.sync picks the issuing lane
@@ -533,7 +533,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t* nempty = nfull + kNR;        // kNR
     TcItem* ring = reinterpret_cast<TcItem*>(nempty + kNR);  // kRing decoded items
     float* cent_s = reinterpret_cast<float*>(ring + kRing);  // [kWG][kMaxD] the item's centroid
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cent_s + kWG * kMaxD);
+    float* nqx = cent_s + kWG * kMaxD;                          // [2][kWG][kM] partial |r|^2
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(nqx + 2 * kWG * kM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t D = p.D;
@@ -732,52 +733,56 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const bool active = (uint32_t)m < d.npairs;
             const uint32_t pair = active ? d.pairs[m] : 0u;
             const float* q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
-            // every load in flight at once: the thread's whole query row (registers)
-            // and the list centroid (one element per thread -> the warpgroup's smem row)
-            float4 qv[kMaxD / 4];
+            // warpgroup g writes dims [64g, 64g + 64) of both planes (A_hi and A_lo):
+            // its half of the thread's query row (registers, all loads in flight at
+            // once) minus its half of the list centroid (the warpgroup's smem row)
+            const int g0 = 64 * wg;
+            const bool mine = (uint32_t)g0 < p.Dk;
+            float4 qv[16];
 #pragma unroll
-            for (int i = 0; i < kMaxD / 4; ++i)
-                qv[i] = (active && (uint32_t)(4 * i) < p.Dp)
-                            ? __ldg(reinterpret_cast<const float4*>(q) + i)
+            for (int i = 0; i < 16; ++i)
+                qv[i] = (active && mine && (uint32_t)(g0 + 4 * i) < p.Dp)
+                            ? __ldg(reinterpret_cast<const float4*>(q + g0) + i)
                             : make_float4(0.f, 0.f, 0.f, 0.f);
             float* cs = cent_s + wg * kMaxD;
-            cs[wt] = (uint32_t)wt < D ? __ldg(p.centroids + (uint64_t)d.c * D + wt) : 0.f;
+            if (wt < 64) cs[wt] = (uint32_t)(g0 + wt) < D ? __ldg(p.centroids + (uint64_t)d.c * D + g0 + wt) : 0.f;
             named_bar(1 + wg, 128);
             pf.mark(9);
-            nq = 0.f;
+            float nqh = 0.f;  // |r|^2 over this warpgroup's dims
             __syncwarp();
             tc_fence_after();
-#pragma unroll
-            for (int c0 = 0; c0 < kMaxD; c0 += 64) {
-                if ((uint32_t)c0 >= p.Dk) break;
-                uint32_t vv[32];
+            if (mine) {
+                uint32_t vh[32], vl[32];
 #pragma unroll
                 for (int i = 0; i < 64; i += 4) {
-                    const int k = c0 + i;
-                    const float4 c4 = *reinterpret_cast<const float4*>(cs + k);
-                    const float qa[4] = {qv[k / 4].x, qv[k / 4].y, qv[k / 4].z, qv[k / 4].w};
+                    const float4 c4 = *reinterpret_cast<const float4*>(cs + i);
+                    const float qa[4] = {qv[i / 4].x, qv[i / 4].y, qv[i / 4].z, qv[i / 4].w};
                     const float ca[4] = {c4.x, c4.y, c4.z, c4.w};
                     float ra[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         // padded dims: q and the centroid row are zero there
                         const float r = __fsub_rn(qa[e], ca[e]);
-                        nq = __fadd_rn(nq, __fmul_rn(r, r));
+                        nqh = __fadd_rn(nqh, __fmul_rn(r, r));
                         ra[e] = r;
                     }
-                    uint32_t h0, l0, h1, l1;
-                    bf16_split2(ra[0], ra[1], h0, l0);
-                    bf16_split2(ra[2], ra[3], h1, l1);
-                    vv[i / 2] = wg == 0 ? h0 : l0;
-                    vv[i / 2 + 1] = wg == 0 ? h1 : l1;
+                    bf16_split2(ra[0], ra[1], vh[i / 2], vl[i / 2]);
+                    bf16_split2(ra[2], ra[3], vh[i / 2 + 1], vl[i / 2 + 1]);
                 }
                 __syncwarp();
-                BIVF_TMEM_ST32(tmem_base + ab * kColA2 + taddr_lane + (wg ? kColAlo : 0u) + c0 / 2, vv);
+                const uint32_t ta = tmem_base + ab * kColA2 + taddr_lane + (uint32_t)g0 / 2;
+                BIVF_TMEM_ST32(ta, vh);
+                BIVF_TMEM_ST32(ta + kColAlo, vl);
             }
+            // |r|^2 = the two halves' sums, added in a fixed order by both warpgroups
+            // (any summation order meets the (D+1) 2^-24 bound of mirror.cuh)
+            float* nqb = nqx + (seq & 1) * kWG * kM;  // double-buffered across builds
+            nqb[wg * kM + m] = nqh;
             __syncwarp();
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
-            named_bar(1 + wg, 128);
+            named_bar(3, 256);  // both warpgroups: A complete, partial norms visible
+            nq = __fadd_rn(nqb[m], nqb[kM + m]);
             if (wt == 0) mbar_arrive(&a_full[ab]);
             if (p.dense_out && wg == 0 && active && d.chunk == 0)
                 p.dense_nq[p.dense_list_base ? pair : pair / p.P] = nq;
@@ -1400,7 +1405,7 @@ constexpr size_t tc_smem_bytes() {
     return 1024 + TcCfg<KT>::NS * kStage + kWG * 32 * kM * 4 + kWG * TcCfg<KT>::KC * kM * 8 +
            kNR * kGU * kNormFloats * 4 +
            (2 * TcCfg<KT>::NU + 2 * kNB + 2 * kNR + 2 * kRing + 4) * 8 + kRing * sizeof(TcItem) +
-           kWG * kMaxD * 4 + 16;
+           kWG * kMaxD * 4 + 2 * kWG * kM * 4 + 16;
 }
 static_assert(tc_smem_bytes<16>() <= 232448 && tc_smem_bytes<32>() <= 232448, "smem budget");
 
