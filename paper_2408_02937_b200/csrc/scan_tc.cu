@@ -1067,6 +1067,37 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
     if (lane == 0 && out_cnt) out_cnt[q] = cntq;
 }
 
+// Ascending bitonic sort of 64 keys across a warp (lane holds keys lane and 32 + lane).
+__device__ __forceinline__ void warp_bitonic64(uint64_t& v0, uint64_t& v1, uint32_t lane) {
+#pragma unroll
+    for (uint32_t sz = 2; sz <= 64; sz <<= 1) {
+#pragma unroll
+        for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
+            if (st == 32) {  // pairs (lane, 32 + lane)
+                const bool up = ((lane & sz) == 0) || sz == 64;
+                const uint64_t lo = v0 < v1 ? v0 : v1, hi = v0 < v1 ? v1 : v0;
+                v0 = up ? lo : hi;
+                v1 = up ? hi : lo;
+            } else {
+                const uint64_t o0 = __shfl_xor_sync(0xffffffffu, v0, st);
+                const uint64_t o1 = __shfl_xor_sync(0xffffffffu, v1, st);
+                const bool lower = (lane & st) == 0;
+                const bool up0 = ((lane & sz) == 0), up1 = (((32 + lane) & sz) == 0);
+                v0 = (lower == up0) ? (v0 < o0 ? v0 : o0) : (v0 < o0 ? o0 : v0);
+                v1 = (lower == up1) ? (v1 < o1 ? v1 : o1) : (v1 < o1 ? o1 : v1);
+            }
+        }
+    }
+}
+// order-preserving float -> uint32 (negative values included)
+__device__ __forceinline__ uint32_t f2ord(float x) {
+    const uint32_t b = __float_as_uint(x);
+    return b ^ ((b >> 31) ? 0xffffffffu : 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t u) {
+    return __uint_as_float(u ^ ((u >> 31) ? 0x80000000u : 0xffffffffu));
+}
+
 // Dense selection (the coarse quantizer): one warp per query over the n
 // approximate distances of the dense mode.  Upper/lower bounds from the same
 // eps' as the filter (mirror.cuh), threshold = k-th smallest upper bound, every
@@ -1124,6 +1155,78 @@ __global__ void dense_select_kernel(const float* dense, uint32_t ld, const float
         }
         const uint32_t kk = k - 1;
         pre = __shfl_sync(0xffffffffu, kk < 32 ? v0 : v1, kk & 31);
+        // Fast path (no serialised warp inserts): every upper bound <= pre (>= k of
+        // them, <= 64 expected) compacted and bitonic-sorted -> theta = the k-th;
+        // every lower bound <= theta (<= 64) recomputed exactly and sorted by the
+        // (dist, id) key.  Lists longer than 64 fall through to the general path.
+        uint32_t* l1 = reinterpret_cast<uint32_t*>(qsm + nw * Dp) + nw * 32 + wq * 192;  // [64] key hi, [64] c, [64] cand
+        const uint32_t lt = (1u << lane) - 1u;
+        uint32_t n1 = 0;
+        bool ok = true;
+        for (uint32_t c0 = 0; c0 < n && ok; c0 += 32) {
+            const uint32_t c = c0 + lane;
+            const float h = c < n ? ub_of(c) : inf;
+            const bool pass = c < n && h <= pre;
+            const unsigned msk = __ballot_sync(0xffffffffu, pass);
+            if (n1 + __popc(msk) > 64) {
+                ok = false;
+            } else {
+                if (pass) {
+                    const uint32_t pos = n1 + __popc(msk & lt);
+                    l1[pos] = f2ord(h);
+                    l1[64 + pos] = c;
+                }
+                n1 += __popc(msk);
+            }
+        }
+        __syncwarp();
+        if (ok && n1 >= k) {
+            uint64_t a0 = lane < n1 ? ((uint64_t)l1[lane] << 32 | l1[64 + lane]) : ~0ull;
+            uint64_t a1 = lane + 32 < n1 ? ((uint64_t)l1[lane + 32] << 32 | l1[96 + lane]) : ~0ull;
+            warp_bitonic64(a0, a1, lane);
+            const uint64_t tk_key = __shfl_sync(0xffffffffu, kk < 32 ? a0 : a1, kk & 31);
+            const float theta = ord2f((uint32_t)(tk_key >> 32));
+            uint32_t* cq = l1 + 128;
+            uint32_t n2 = 0;
+            for (uint32_t c0 = 0; c0 < n && ok; c0 += 32) {
+                const uint32_t c = c0 + lane;
+                bool cand = false;
+                if (c < n) {
+                    const float a = row[c];
+                    const float ns = nrm[(c >> 5) * kNormFloats + (c & 31)];
+                    cand = a - fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, nqv + ns, 1e-30f)) <= theta;
+                }
+                const unsigned msk = __ballot_sync(0xffffffffu, cand);
+                if (n2 + __popc(msk) > 64) {
+                    ok = false;
+                } else {
+                    if (cand) cq[n2 + __popc(msk & lt)] = c;
+                    n2 += __popc(msk);
+                }
+            }
+            __syncwarp();
+            if (ok) {
+                uint64_t e0 = ~0ull, e1 = ~0ull;
+                if (lane < n2) {
+                    const uint32_t c = cq[lane];
+                    e0 = (uint64_t)f2ord(exact_l2_row(qs, rows + (uint64_t)c * D, D)) << 32 | c;
+                }
+                if (lane + 32 < n2) {
+                    const uint32_t c = cq[lane + 32];
+                    e1 = (uint64_t)f2ord(exact_l2_row(qs, rows + (uint64_t)c * D, D)) << 32 | c;
+                }
+                warp_bitonic64(e0, e1, lane);
+                if (lane < k) {
+                    out_d[(uint64_t)q * k + lane] = ord2f((uint32_t)(e0 >> 32));
+                    out_i[(uint64_t)q * k + lane] = (long long)(uint32_t)e0;
+                }
+                if (lane + 32 < k) {
+                    out_d[(uint64_t)q * k + lane + 32] = ord2f((uint32_t)(e1 >> 32));
+                    out_i[(uint64_t)q * k + lane + 32] = (long long)(uint32_t)e1;
+                }
+                return;
+            }
+        }
     }
     WarpTopK<KPL> th;
     th.init();
@@ -1597,7 +1700,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                 p, probes, out_d, out_i, out_cnt, sh.nq);
     } else if (dense) {
         const uint32_t n = dense->n;
-        const size_t sm_sel = wpb * (p.Dp * 4 + 128);
+        const size_t sm_sel = wpb * (p.Dp * 4 + 128 + 192 * 4);
         if (sh.k <= 32)
             dense_select_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
                 dense->out, dense->ld, dense->nq, off_nrm, off_rows, queries, p.Dp, p.D, n, sh.nq,
