@@ -1067,27 +1067,46 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
     if (lane == 0 && out_cnt) out_cnt[q] = cntq;
 }
 
-// Ascending bitonic sort of 64 keys across a warp (lane holds keys lane and 32 + lane).
-__device__ __forceinline__ void warp_bitonic64(uint64_t& v0, uint64_t& v1, uint32_t lane) {
+// Ascending bitonic sort of 32*R keys across a warp: element e = 32 j + lane is
+// v[j] of lane `lane` (partners 32 or more apart sit in the same lane).
+template <int R>
+__device__ __forceinline__ void warp_bitonic(uint64_t (&v)[R], uint32_t lane) {
 #pragma unroll
-    for (uint32_t sz = 2; sz <= 64; sz <<= 1) {
+    for (uint32_t sz = 2; sz <= 32u * R; sz <<= 1) {
 #pragma unroll
         for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
-            if (st == 32) {  // pairs (lane, 32 + lane)
-                const bool up = ((lane & sz) == 0) || sz == 64;
-                const uint64_t lo = v0 < v1 ? v0 : v1, hi = v0 < v1 ? v1 : v0;
-                v0 = up ? lo : hi;
-                v1 = up ? hi : lo;
+            if (st >= 32) {
+                const uint32_t js = st >> 5;
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    if (j & js) continue;
+                    const uint32_t e = 32u * j + lane;
+                    const bool up = (e & sz) == 0;
+                    const uint64_t a = v[j], b = v[j + js];
+                    const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+                    v[j] = up ? lo : hi;
+                    v[j + js] = up ? hi : lo;
+                }
             } else {
-                const uint64_t o0 = __shfl_xor_sync(0xffffffffu, v0, st);
-                const uint64_t o1 = __shfl_xor_sync(0xffffffffu, v1, st);
                 const bool lower = (lane & st) == 0;
-                const bool up0 = ((lane & sz) == 0), up1 = (((32 + lane) & sz) == 0);
-                v0 = (lower == up0) ? (v0 < o0 ? v0 : o0) : (v0 < o0 ? o0 : v0);
-                v1 = (lower == up1) ? (v1 < o1 ? v1 : o1) : (v1 < o1 ? o1 : v1);
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v[j], st);
+                    const bool up = ((32u * j + lane) & sz) == 0;
+                    v[j] = (lower == up) ? (v[j] < o ? v[j] : o) : (v[j] < o ? o : v[j]);
+                }
             }
         }
     }
+}
+// element e of a warp_bitonic array (warp-uniform e)
+template <int R>
+__device__ __forceinline__ uint64_t warp_elem(const uint64_t (&v)[R], uint32_t e) {
+    uint64_t x = v[0];
+#pragma unroll
+    for (int j = 1; j < R; ++j)
+        if (e >> 5 == (uint32_t)j) x = v[j];
+    return __shfl_sync(0xffffffffu, x, e & 31);
 }
 // order-preserving float -> uint32 (negative values included)
 __device__ __forceinline__ uint32_t f2ord(float x) {
@@ -1096,6 +1115,114 @@ __device__ __forceinline__ uint32_t f2ord(float x) {
 }
 __device__ __forceinline__ float ord2f(uint32_t u) {
     return __uint_as_float(u ^ ((u >> 31) ? 0x80000000u : 0xffffffffu));
+}
+
+// Fast selection of dense_select_kernel (R keys per lane, k <= 32R <= n): true when
+// the exact top-k was written (false: more than 32R values tie the bounds, the
+// caller's general path runs with *pre as its pre-threshold).
+template <int R, typename UbOf>
+__device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* nrm, float nqv,
+                                  const float* qs, const float* rows, uint32_t D, uint32_t n,
+                                  uint32_t k, uint32_t q, uint32_t lane, uint32_t* scratch,
+                                  float* out_d, long long* out_i, float* pre) {
+    const float inf = __int_as_float(0x7f800000);
+    // phase A: an upper bound of the k-th smallest upper bound from each lane's
+    // R smallest values (32R values sorted across the warp): the k-th smallest
+    // of any k values is >= the true k-th smallest
+    float m[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) m[j] = inf;
+    for (uint32_t c = lane; c < n; c += 32) {
+        float t = ub_of(c);
+#pragma unroll
+        for (int j = 0; j < R - 1; ++j) {
+            const float a = fminf(m[j], t);
+            t = fmaxf(m[j], t);
+            m[j] = a;
+        }
+        m[R - 1] = fminf(m[R - 1], t);
+    }
+    uint64_t v[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = (uint64_t)f2ord(m[j]) << 32;
+    warp_bitonic<R>(v, lane);
+    const uint32_t kk = k - 1;
+    *pre = ord2f((uint32_t)(warp_elem<R>(v, kk) >> 32));
+    // Fast path (no serialised warp inserts): every upper bound <= pre (>= k of
+    // them, <= 32R expected) compacted and bitonic-sorted -> theta = the k-th;
+    // every lower bound <= theta (<= 32R) recomputed exactly and sorted by the
+    // (dist, id) key.  Longer lists fall through to the general path.
+    uint32_t* l1 = scratch;  // [32R] key hi, [32R] c, [32R] cand
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t n1 = 0;
+    bool ok = true;
+    for (uint32_t c0 = 0; c0 < n && ok; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        const float h = c < n ? ub_of(c) : inf;
+        const bool pass = c < n && h <= *pre;
+        const unsigned msk = __ballot_sync(0xffffffffu, pass);
+        if (n1 + __popc(msk) > 32u * R) {
+            ok = false;
+        } else {
+            if (pass) {
+                const uint32_t pos = n1 + __popc(msk & lt);
+                l1[pos] = f2ord(h);
+                l1[32 * R + pos] = c;
+            }
+            n1 += __popc(msk);
+        }
+    }
+    __syncwarp();
+    if (ok && n1 >= k) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const uint32_t e = 32 * j + lane;
+            v[j] = e < n1 ? ((uint64_t)l1[e] << 32 | l1[32 * R + e]) : ~0ull;
+        }
+        warp_bitonic<R>(v, lane);
+        const float theta = ord2f((uint32_t)(warp_elem<R>(v, kk) >> 32));
+        uint32_t* cq = l1 + 64 * R;
+        uint32_t n2 = 0;
+        for (uint32_t c0 = 0; c0 < n && ok; c0 += 32) {
+            const uint32_t c = c0 + lane;
+            bool cand = false;
+            if (c < n) {
+                const float a = row[c];
+                const float ns = nrm[(c >> 5) * kNormFloats + (c & 31)];
+                cand = a - fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, nqv + ns, 1e-30f)) <= theta;
+            }
+            const unsigned msk = __ballot_sync(0xffffffffu, cand);
+            if (n2 + __popc(msk) > 32u * R) {
+                ok = false;
+            } else {
+                if (cand) cq[n2 + __popc(msk & lt)] = c;
+                n2 += __popc(msk);
+            }
+        }
+        __syncwarp();
+        if (ok) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const uint32_t e = 32 * j + lane;
+                v[j] = ~0ull;
+                if (e < n2) {
+                    const uint32_t c = cq[e];
+                    v[j] = (uint64_t)f2ord(exact_l2_row(qs, rows + (uint64_t)c * D, D)) << 32 | c;
+                }
+            }
+            warp_bitonic<R>(v, lane);
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const uint32_t e = 32 * j + lane;
+                if (e < k) {
+                    out_d[(uint64_t)q * k + e] = ord2f((uint32_t)(v[j] >> 32));
+                    out_i[(uint64_t)q * k + e] = (long long)(uint32_t)v[j];
+                }
+            }
+            return true;
+        }
+    }
+    return false;
 }
 
 // Dense selection (the coarse quantizer): one warp per query over the n
@@ -1123,110 +1250,16 @@ __global__ void dense_select_kernel(const float* dense, uint32_t ld, const float
         const float ns = nrm[(c >> 5) * kNormFloats + (c & 31)];
         return a + fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, nqv + ns, 1e-30f));
     };
-    // phase A: an upper bound of the k-th smallest upper bound from each lane's
-    // two smallest values (64 values, k <= 64 of them sorted across the warp):
-    // the k-th smallest of any k values is >= the true k-th smallest
+    // phase A (+ the fast selection when <= 32R values tie the bounds): the k-th
+    // smallest of each lane's R smallest upper bounds bounds the k-th smallest
     float pre = inf;
+    uint32_t* fscr = reinterpret_cast<uint32_t*>(qsm + nw * Dp) + nw * 32 + wq * 384;
     if (k <= 64 && n >= 64) {
-        float m1 = inf, m2 = inf;
-        for (uint32_t c = lane; c < n; c += 32) {
-            const float h = ub_of(c);
-            m2 = fminf(m2, fmaxf(m1, h));
-            m1 = fminf(m1, h);
-        }
-        // bitonic sort of the 64 values (lane holds m1 at index lane, m2 at 32 + lane)
-        float v0 = m1, v1 = m2;
-        for (uint32_t sz = 2; sz <= 64; sz <<= 1) {
-            for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
-                if (st == 32) {  // pairs (lane, 32 + lane)
-                    const bool up = ((lane & sz) == 0) || sz == 64;
-                    const float lo = fminf(v0, v1), hi = fmaxf(v0, v1);
-                    v0 = up ? lo : hi;
-                    v1 = up ? hi : lo;
-                } else {
-                    const float o0 = __shfl_xor_sync(0xffffffffu, v0, st);
-                    const float o1 = __shfl_xor_sync(0xffffffffu, v1, st);
-                    const bool lower = (lane & st) == 0;
-                    const bool up0 = ((lane & sz) == 0), up1 = (((32 + lane) & sz) == 0);
-                    v0 = (lower == up0) ? fminf(v0, o0) : fmaxf(v0, o0);
-                    v1 = (lower == up1) ? fminf(v1, o1) : fmaxf(v1, o1);
-                }
-            }
-        }
-        const uint32_t kk = k - 1;
-        pre = __shfl_sync(0xffffffffu, kk < 32 ? v0 : v1, kk & 31);
-        // Fast path (no serialised warp inserts): every upper bound <= pre (>= k of
-        // them, <= 64 expected) compacted and bitonic-sorted -> theta = the k-th;
-        // every lower bound <= theta (<= 64) recomputed exactly and sorted by the
-        // (dist, id) key.  Lists longer than 64 fall through to the general path.
-        uint32_t* l1 = reinterpret_cast<uint32_t*>(qsm + nw * Dp) + nw * 32 + wq * 192;  // [64] key hi, [64] c, [64] cand
-        const uint32_t lt = (1u << lane) - 1u;
-        uint32_t n1 = 0;
-        bool ok = true;
-        for (uint32_t c0 = 0; c0 < n && ok; c0 += 32) {
-            const uint32_t c = c0 + lane;
-            const float h = c < n ? ub_of(c) : inf;
-            const bool pass = c < n && h <= pre;
-            const unsigned msk = __ballot_sync(0xffffffffu, pass);
-            if (n1 + __popc(msk) > 64) {
-                ok = false;
-            } else {
-                if (pass) {
-                    const uint32_t pos = n1 + __popc(msk & lt);
-                    l1[pos] = f2ord(h);
-                    l1[64 + pos] = c;
-                }
-                n1 += __popc(msk);
-            }
-        }
-        __syncwarp();
-        if (ok && n1 >= k) {
-            uint64_t a0 = lane < n1 ? ((uint64_t)l1[lane] << 32 | l1[64 + lane]) : ~0ull;
-            uint64_t a1 = lane + 32 < n1 ? ((uint64_t)l1[lane + 32] << 32 | l1[96 + lane]) : ~0ull;
-            warp_bitonic64(a0, a1, lane);
-            const uint64_t tk_key = __shfl_sync(0xffffffffu, kk < 32 ? a0 : a1, kk & 31);
-            const float theta = ord2f((uint32_t)(tk_key >> 32));
-            uint32_t* cq = l1 + 128;
-            uint32_t n2 = 0;
-            for (uint32_t c0 = 0; c0 < n && ok; c0 += 32) {
-                const uint32_t c = c0 + lane;
-                bool cand = false;
-                if (c < n) {
-                    const float a = row[c];
-                    const float ns = nrm[(c >> 5) * kNormFloats + (c & 31)];
-                    cand = a - fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, nqv + ns, 1e-30f)) <= theta;
-                }
-                const unsigned msk = __ballot_sync(0xffffffffu, cand);
-                if (n2 + __popc(msk) > 64) {
-                    ok = false;
-                } else {
-                    if (cand) cq[n2 + __popc(msk & lt)] = c;
-                    n2 += __popc(msk);
-                }
-            }
-            __syncwarp();
-            if (ok) {
-                uint64_t e0 = ~0ull, e1 = ~0ull;
-                if (lane < n2) {
-                    const uint32_t c = cq[lane];
-                    e0 = (uint64_t)f2ord(exact_l2_row(qs, rows + (uint64_t)c * D, D)) << 32 | c;
-                }
-                if (lane + 32 < n2) {
-                    const uint32_t c = cq[lane + 32];
-                    e1 = (uint64_t)f2ord(exact_l2_row(qs, rows + (uint64_t)c * D, D)) << 32 | c;
-                }
-                warp_bitonic64(e0, e1, lane);
-                if (lane < k) {
-                    out_d[(uint64_t)q * k + lane] = ord2f((uint32_t)(e0 >> 32));
-                    out_i[(uint64_t)q * k + lane] = (long long)(uint32_t)e0;
-                }
-                if (lane + 32 < k) {
-                    out_d[(uint64_t)q * k + lane + 32] = ord2f((uint32_t)(e1 >> 32));
-                    out_i[(uint64_t)q * k + lane + 32] = (long long)(uint32_t)e1;
-                }
-                return;
-            }
-        }
+        if (dense_select_fast<2>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
+            return;
+    } else if (k <= 128 && n >= 128) {
+        if (dense_select_fast<4>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
+            return;
     }
     WarpTopK<KPL> th;
     th.init();
@@ -1700,7 +1733,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                 p, probes, out_d, out_i, out_cnt, sh.nq);
     } else if (dense) {
         const uint32_t n = dense->n;
-        const size_t sm_sel = wpb * (p.Dp * 4 + 128 + 192 * 4);
+        const size_t sm_sel = wpb * (p.Dp * 4 + 128 + 384 * 4);
         if (sh.k <= 32)
             dense_select_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
                 dense->out, dense->ld, dense->nq, off_nrm, off_rows, queries, p.Dp, p.D, n, sh.nq,
