@@ -242,7 +242,7 @@ void GpuIndex::alloc_device() {
     {
         const char* m = std::getenv("BIVF_SCAN");
         mir_on_ = tc_supported(D_, 1, cfg_.metric) && !(m && std::string(m) == "cuda");
-        GF_ = mirror_group_floats(D_);
+        GF_ = cfg_.metric == BIVF_METRIC_IP ? mirror_group_floats_wide(D_) : mirror_group_floats(D_);
         MPS_ = (uint64_t)gpb_ * GF_;
         tc_ok_ = mir_on_;
     }
@@ -254,9 +254,15 @@ void GpuIndex::alloc_device() {
         BIVF_CUDA(dset(d_arena_mir_.p, 0, d_arena_mir_.bytes));
         d_arena_nrm_.alloc((size_t)NB_ * gpb_ * kNormFloats * 4);
         BIVF_CUDA(dset(d_arena_nrm_.p, 0, d_arena_nrm_.bytes));
-        d_arena_rows_.alloc((size_t)NB_ * PS_ * 4);
-        BIVF_CUDA(dset(d_arena_rows_.p, 0, d_arena_rows_.bytes));
-        tc_ok_ = make_mirror_map(d_arena_mir_.as<float>(), (uint64_t)NB_ * gpb_, D_, &map_arena_) ==
+        // the slot-major row copy feeds the L2 refine's gathers; the inner-product
+        // (wide, D <= 768) refine reads the interleaved payload instead: at D = 768
+        // a second copy of the payload would not fit next to it in HBM
+        if (cfg_.metric != BIVF_METRIC_IP) {
+            d_arena_rows_.alloc((size_t)NB_ * PS_ * 4);
+            BIVF_CUDA(dset(d_arena_rows_.p, 0, d_arena_rows_.bytes));
+        }
+        tc_ok_ = make_mirror_map(d_arena_mir_.as<float>(), (uint64_t)NB_ * gpb_, D_, cfg_.metric == BIVF_METRIC_IP,
+                                 &map_arena_) ==
                  cudaSuccess;
     }
     mirror_ = mirror_view();
@@ -298,9 +304,12 @@ void GpuIndex::ensure_offline_capacity(uint64_t slots) {
         BIVF_CUDA(dset(d_off_mir_.p, 0, d_off_mir_.bytes));
         d_off_nrm_.alloc((size_t)(slots / 32) * kNormFloats * 4);
         BIVF_CUDA(dset(d_off_nrm_.p, 0, d_off_nrm_.bytes));
-        d_off_rows_.alloc((size_t)slots * D_ * 4);
-        BIVF_CUDA(dset(d_off_rows_.p, 0, d_off_rows_.bytes));
-        if (make_mirror_map(d_off_mir_.as<float>(), slots / 32, D_, &map_off_) != cudaSuccess)
+        if (cfg_.metric != BIVF_METRIC_IP) {  // see alloc_device: no row copy for the IP mirror
+            d_off_rows_.alloc((size_t)slots * D_ * 4);
+            BIVF_CUDA(dset(d_off_rows_.p, 0, d_off_rows_.bytes));
+        }
+        if (make_mirror_map(d_off_mir_.as<float>(), slots / 32, D_, cfg_.metric == BIVF_METRIC_IP, &map_off_) !=
+            cudaSuccess)
             tc_ok_ = false;
     }
     mirror_ = mirror_view();
@@ -316,7 +325,8 @@ MirrorView GpuIndex::mirror_view() const {
     M.arena_rows = d_arena_rows_.as<float>();
     M.cent = d_cent_.as<float>();
     M.D = D_;
-    M.K = mirror_k(D_);
+    M.wide = cfg_.metric == BIVF_METRIC_IP ? 1u : 0u;
+    M.K = M.wide ? mirror_k_wide(D_) : mirror_k(D_);
     M.T = T_;
     M.gpb = gpb_;
     M.GF = GF_;
@@ -366,6 +376,9 @@ void GpuIndex::rebuild_mirror() {
 void GpuIndex::build_quantizer_mirror(const float* c) {
     q_tc_ok_ = false;
     if (!mir_on_ || C_ < 64) return;
+    // L2: 3xBF16 over centroids centred at their mean (dense mode + selection);
+    // inner product: the wide 1xFP16 mirror of the raw centroids (filter + refine)
+    const bool wide = cfg_.metric == BIVF_METRIC_IP;
     const uint32_t ngq = ceil_div(C_, 32);
     std::vector<float> mu(D_, 0.f);
     for (uint32_t k = 0; k < C_; ++k)
@@ -395,7 +408,8 @@ void GpuIndex::build_quantizer_mirror(const float* c) {
     M.off_nrm = d_q_nrm_.as<float>();
     M.cent = d_q_mu_.as<float>();
     M.D = D_;
-    M.K = mirror_k(D_);
+    M.wide = wide ? 1u : 0u;
+    M.K = wide ? mirror_k_wide(D_) : mirror_k(D_);
     M.T = 32;
     M.gpb = 1;
     M.GF = GF_;
@@ -411,11 +425,12 @@ void GpuIndex::build_quantizer_mirror(const float* c) {
     BIVF_CUDA(launch_mirror_groups(M, d_cent_il_.as<float>(), false, (uint64_t)32 * D_,
                                    dg.as<uint64_t>(), dc.as<uint32_t>(), ngq, data_stream_));
     BIVF_CUDA(cudaStreamSynchronize(data_stream_));
-    q_tc_ok_ = make_mirror_map(d_q_mir_.as<float>(), ngq, D_, &map_q_) == cudaSuccess;
+    q_tc_ok_ = make_mirror_map(d_q_mir_.as<float>(), ngq, D_, wide, &map_q_) == cudaSuccess;
 }
 
 bool GpuIndex::use_tc_quantizer(uint32_t P) const {
-    return q_tc_ok_ && scan_mode_ != 1 && P <= 256 && P < C_;
+    // inner product: filter mode (k = P <= 32); L2: dense mode up to 256
+    return q_tc_ok_ && scan_mode_ != 1 && P <= (cfg_.metric == BIVF_METRIC_IP ? 32u : 256u) && P < C_;
 }
 
 uint32_t GpuIndex::quantizer_slice() const {
@@ -468,6 +483,7 @@ void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32
             qs.QT = 128;
             qs.metric = cfg_.metric;
             TcDense dn{w.qdense, w.qdense_nq, ld, C_};
+            const bool ip = cfg_.metric == BIVF_METRIC_IP;  // filter + exact refine (no dense rows)
             const size_t g0 = (size_t)qbase + q0;
             // work items = tiles x chunks (the centroid list has no online part)
             const uint32_t ngq = ceil_div(C_, 32);
@@ -476,7 +492,7 @@ void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32
             BIVF_CUDA(launch_ivf_search_tc(quantizer_lists(), w.plan, d_q_zero_.as<long long>(),
                                            w.queries + g0 * Dp_, d_q_mu_.as<float>(), qs,
                                            map_q_, map_q_, d_q_nrm_.as<float>(), nullptr,
-                                           d_cent_.as<float>(), nullptr, w.tc, &dn,
+                                           d_cent_.as<float>(), nullptr, w.tc, ip ? nullptr : &dn,
                                            w.pdist + g0 * P, w.probes + g0 * P,
                                            nullptr, num_sms_, s, nullptr, nullptr, items));
         }

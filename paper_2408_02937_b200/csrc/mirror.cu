@@ -1,5 +1,6 @@
 // Tensor-core scan mirror maintenance (see mirror.cuh).  sm_100a.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 
@@ -16,9 +17,23 @@ namespace {
 // s_lo = bf16_rn(s - s_hi).
 __device__ __forceinline__ void mirror_column(float* gf, float* nrm, float* row, uint32_t lane,
                                               const float* x, uint32_t xs, const float* c,
-                                              uint32_t D, uint32_t K) {
+                                              uint32_t D, uint32_t K, uint32_t wide) {
     uint16_t* g = reinterpret_cast<uint16_t*>(gf);
     float n2 = 0.f;
+    if (wide) {  // inner product: uncentred fp16 plane scaled by 2^ev, norms [2^-ev][|x|]
+        float mx = 0.f;
+        for (uint32_t d = 0; d < D; ++d) mx = fmaxf(mx, fabsf(x[(uint64_t)d * xs]));
+        const int ev = wide_scale_exp(mx);
+        for (uint32_t d = 0; d < D; ++d) {
+            const float xd = x[(uint64_t)d * xs];
+            if (row) row[d] = xd;
+            g[(uint64_t)d * 32u + lane] = __half_as_ushort(__float2half_rn(ldexpf(xd, ev)));
+            n2 = __fadd_rn(n2, __fmul_rn(xd, xd));
+        }
+        nrm[lane] = ldexpf(1.f, -ev);
+        nrm[32 + lane] = sqrtf(n2);
+        return;
+    }
     for (uint32_t d = 0; d < D; ++d) {
         const float xd = x[(uint64_t)d * xs];
         if (row) row[d] = xd;
@@ -61,7 +76,7 @@ __global__ void mirror_insert_kernel(MirrorView M, uint32_t n, const float* x, c
     const uint64_t g = (uint64_t)b * M.gpb + (slot >> 5);
     float* row = M.arena_rows ? M.arena_rows + (g * 32u + (slot & 31u)) * M.D : nullptr;
     mirror_column(M.arena_mir + g * M.GF, M.arena_nrm + g * kNormFloats, row, slot & 31u,
-                  x + (uint64_t)i * M.D, 1, M.cent + (uint64_t)asg[i] * M.D, M.D, M.K);
+                  x + (uint64_t)i * M.D, 1, M.cent + (uint64_t)asg[i] * M.D, M.D, M.K, M.wide);
 }
 
 __global__ void mirror_offline_kernel(MirrorView M, uint32_t n, const float* x,
@@ -72,7 +87,7 @@ __global__ void mirror_offline_kernel(MirrorView M, uint32_t n, const float* x,
     float* row = M.off_rows ? M.off_rows + s * M.D : nullptr;
     mirror_column(M.off_mir + (s >> 5) * M.GF, M.off_nrm + (s >> 5) * kNormFloats, row,
                   (uint32_t)(s & 31u), x + (uint64_t)i * M.D, 1, M.cent + (uint64_t)asg[i] * M.D,
-                  M.D, M.K);
+                  M.D, M.K, M.wide);
 }
 
 // warp per group, lane = slot: payload group rows are coalesced
@@ -96,13 +111,14 @@ __global__ void mirror_groups_kernel(MirrorView M, const float* payload, int are
         rows = M.off_rows;
     }
     float* row = rows ? rows + (gi * 32u + lane) * M.D : nullptr;
-    mirror_column(dst, nrm, row, lane, src + lane, 32, M.cent + (uint64_t)cl[w] * M.D, M.D, M.K);
+    mirror_column(dst, nrm, row, lane, src + lane, 32, M.cent + (uint64_t)cl[w] * M.D, M.D, M.K, M.wide);
 }
 
 __global__ void mirror_slot_move_kernel(MirrorView M, const uint64_t* id_addr, uint32_t n,
                                         float* scr, int phase) {
-    // per slot: 2K plane rows + 2 norm entries + D row entries
-    const uint32_t R = 2 * M.K + 2 + M.D;
+    // per slot: 2K plane rows (K in wide mode) + 2 norm entries + D row entries
+    const uint32_t PR = M.wide ? M.K : 2 * M.K;
+    const uint32_t R = PR + 2 + M.D;
     const uint64_t total = (uint64_t)n * R;
     for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
          o += (uint64_t)gridDim.x * blockDim.x) {
@@ -110,15 +126,15 @@ __global__ void mirror_slot_move_kernel(MirrorView M, const uint64_t* id_addr, u
         uint32_t lane;
         float *nrm, *row;
         float* g = mirror_slot(M, id_addr[phase == 0 ? m : n + m], lane, nrm, row);
-        if (r < 2 * M.K) {  // bf16 plane element (carried in a float scratch slot)
+        if (r < PR) {  // bf16 plane element (carried in a float scratch slot)
             uint16_t* e16 = reinterpret_cast<uint16_t*>(g) + (uint64_t)r * 32u + lane;
             if (phase == 0) scr[o] = __uint_as_float(*e16);
             else *e16 = (uint16_t)__float_as_uint(scr[o]);
             continue;
         }
         float* e;
-        if (r < 2 * M.K + 2) e = nrm + (r - 2 * M.K) * 32u + lane;
-        else if (row) e = row + (r - 2 * M.K - 2);
+        if (r < PR + 2) e = nrm + (r - PR) * 32u + lane;
+        else if (row) e = row + (r - PR - 2);
         else continue;
         if (phase == 0) scr[o] = *e;
         else *e = scr[o];
@@ -156,7 +172,7 @@ cudaError_t launch_mirror_groups(const MirrorView& M, const float* payload, bool
 cudaError_t launch_mirror_slot_moves(const MirrorView& M, const uint64_t* id_addr, uint32_t n,
                                      float* scratch, cudaStream_t s) {
     if (!n || !M.off_mir) return cudaSuccess;
-    const uint64_t total = (uint64_t)n * (2 * M.K + 2 + M.D);
+    const uint64_t total = (uint64_t)n * ((M.wide ? M.K : 2 * M.K) + 2 + M.D);
     const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148 * 16));
     for (int phase = 0; phase < 2; ++phase) {
         mirror_slot_move_kernel<<<g, 256, 0, s>>>(M, id_addr, n, scratch, phase);

@@ -10,6 +10,11 @@
 //     rows [0, K)      s_hi, dim d
 //     rows [K, 2K)     s_lo, dim d
 // A group's planes occupy 2K*64 bytes = K*32 "floats" of the float-typed buffers.
+// Wide mode (inner product, D <= 768; scan_tc.cu's 1xFP16 filter): the UNcentred
+// vector scaled by 2^ev (max |x_d| 2^ev in [2^13, 2^14): fp16 keeps its 11-bit
+// relative precision, no overflow) in one fp16 plane (K rows, K = D rounded up to
+// 16, or to 128 when D > 128 so that 128-row K-chunks tile it), norms
+// [2^-ev x32][|x| x32]; K*16 floats per group.
 // Norms, per group, a separate array of 64 floats: [|s|^2 (sequential fp32) x 32]
 // [kVScale * |s|^2 x 32] (the per-slot term of the scan's pass-1 threshold, scan_tc.cu).
 // Rows, per group, a slot-major copy of the exact payload (32 x D fp32): the
@@ -21,6 +26,8 @@
 // the list length that exposes the slots is release-published.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -34,7 +41,8 @@ struct MirrorView {
     float* off_rows;       // offline groups x 32 x D
     float* arena_rows;     // num_blocks x gpb x 32 x D
     const float* cent;     // [C][D] row-major centroids
-    uint32_t D, K, T, gpb; // K = D rounded up to 16
+    uint32_t D, K, T, gpb; // K = D rounded up to 16 (wide: mirror_k_wide)
+    uint32_t wide;         // 1: inner-product wide mode (hi plane only, uncentred)
     uint64_t GF;           // floats per group  = K*32 (2K*32 bf16)
     uint64_t MPS;          // floats per block  = gpb*GF
 };
@@ -52,6 +60,23 @@ constexpr float kVScale = (1.0f - kEpsRel - kEpsT) / (2.0f * (1.0f - kEpsRel));
 
 inline uint32_t mirror_k(uint32_t D) { return (D + 15u) & ~15u; }
 inline uint64_t mirror_group_floats(uint32_t D) { return (uint64_t)mirror_k(D) * 32ull; }
+// wide mode: K-chunks of min(K, 128) rows
+inline uint32_t mirror_k_wide(uint32_t D) { return D <= 128 ? mirror_k(D) : (D + 127u) & ~127u; }
+inline uint32_t mirror_chunk_wide(uint32_t D) { return std::min<uint32_t>(mirror_k_wide(D), 128u); }
+inline uint64_t mirror_group_floats_wide(uint32_t D) { return (uint64_t)mirror_k_wide(D) * 16ull; }
+// the 1xFP16 inner-product filter over 2^e-scaled operands (max |v_d| in [2^13, 2^14)):
+// |fl(v) - v| <= 2^-11 |v| + 2^-25, so |P' - q'.x'| <= (2^-10 + 2^-22)|q'||x'| +
+// 2^-24.9 sqrt(D)(|q'| + |x'|) + D 2^-50, and with |q'|, |x'| >= 2^13 the last two
+// terms are < 2^-30 |q'||x'| (D <= 768): |P - q.x| <= 2^-9.99 |q||x| unscaled, plus
+// fp32 accumulation (48 K-steps) <= 2^-19 |q||x|; 2^-9 carries a ~2x margin.
+constexpr float kEpsIP = 1.0f / 512.0f;
+// the scale exponent: max |v_d| * 2^e in [2^13, 2^14) (e = 0 for a zero vector)
+__host__ __device__ inline int wide_scale_exp(float mx) {
+    if (!(mx > 0.f)) return 0;
+    int e = 0;
+    (void)frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1): mx in [2^(e-1), 2^e)
+    return 14 - e;
+}
 constexpr uint32_t kNormFloats = 64;  // per group
 
 // insert: vector i (row-major x[i*D..]) landed in block out_blk[i] (-1 = failed)

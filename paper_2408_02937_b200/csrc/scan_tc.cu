@@ -29,6 +29,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cub/device/device_scan.cuh>
 
@@ -53,26 +54,26 @@ constexpr int kM = 128;                    // queries per tile (MMA M, TMEM lane
 constexpr int kGU = 2;                     // groups per unit (MMA N = 32 * kGU)
 // smem stages (one group each; kNS / kGU unit slots) and smem candidate slots
 // per thread, by top-k width: k <= 16 -> 6 stages, 40 slots; k <= 32 -> 4, 56
-// (24 slots overflow in the unseeded first phase: an overflowed run is rescanned)
+// (an overflowed run is rescanned exactly by the refine)
 template <int KT>
 struct TcCfg {
     static constexpr int NS = KT <= 16 ? 6 : 4;
     static constexpr int KC = KT <= 16 ? 40 : 56;
     static constexpr int NU = NS / 2;
 };
-// release a unit's accumulator as soon as its dot products are in registers
-// (before filtering) instead of after the filter (measured: no gain, more registers)
-constexpr bool kEarlyRelease = false;
+// Measured and dropped: releasing a unit's accumulator before filtering (no gain,
+// more registers), both warpgroups on every unit (twice the per-unit fixed cost).
 constexpr int kNB = 4;                     // TMEM accumulators (32 * kGU columns each; even)
-// both math warpgroups work on every unit, warpgroup g on the unit's group g
-// (instead of alternating whole units): half the per-unit epilogue latency but
-// twice the per-unit fixed cost per warp (measured slower: 1.38 -> 1.65 ms)
-#ifndef BIVF_TC_COLSPLIT
-#define BIVF_TC_COLSPLIT 0
-#endif
-constexpr bool kColSplit = BIVF_TC_COLSPLIT != 0;
-static_assert(!kColSplit || kGU == 2, "column split assumes one group per warpgroup");
-constexpr uint32_t kUnitArrivals = kColSplit ? 8 : 4;  // warps releasing a unit's accumulator
+constexpr uint32_t kUnitArrivals = 4;      // warps releasing a unit's accumulator (its warpgroup)
+// Wide mode W (inner product, D <= 768): 1xFP16 over 2^e-scaled operands (mirror.cuh),
+// queries uncentred, the B mirror streamed in 128-row K-chunks, A = the query rows'
+// fp16 plane (<= 384 TMEM columns, one buffer), 2 accumulators.  Otherwise 3xBF16 L2 (D <= 128): two A
+// buffers (hi + lo, 128 columns each), 4 accumulators.
+template <bool W>
+struct TcMode {
+    static constexpr int NB = W ? 2 : 4;
+    static constexpr uint32_t ColAcc = W ? 384 : 256;
+};
 constexpr int kRing = 4;                   // decoded work items in flight (producer lookahead)
 constexpr int kNR = 8;                     // norm slots (ring, one unit each; decoupled from kNB)
 
@@ -115,6 +116,7 @@ static_assert(kColAcc + 32 * kGU * kNB <= kTmemCols, "TMEM budget");
 struct TcParams {
     DevLists L;
     uint32_t D, Dk, Dp, k, P, maxch;
+    uint32_t brow, gstride, nkc;  // TMA box rows, map rows per group, K-chunks per group (wide: Dk / brow)
     uint32_t seed_groups;        // seeding pass: scan only the first seed_groups groups, no run output
     const float* centroids;      // [C][D] row-major
     const float* queries;        // [nq][Dp]
@@ -127,7 +129,7 @@ struct TcParams {
     const uint32_t* n_items_ptr;
     const uint32_t* plist;
     uint32_t* item_ctr;
-    float* qthr;                // [nq] per-query threshold shared by all its runs (float bits, atomicMin)
+    float* qthr;                // [nq] per-query threshold shared by all its runs (f2ord bits, atomicMin)
     // dense mode (the coarse quantizer): approximate distances a = |r|^2 + |s|^2 - 2 r.s of
     // every (query, slot of the single list) -> dense_out[query * dense_ld + slot], |r|^2 ->
     // dense_nq[query]; no filtering (dense_select_kernel does the selection)
@@ -149,6 +151,22 @@ struct TcParams {
     float* clb;         // [runs][kKC]
     uint32_t* cloc;     // [runs][kKC]   (group << 5 | slot)
 };
+
+// order-preserving float -> uint32 (negative values included)
+__device__ __forceinline__ uint32_t f2ord(float x) {
+    const uint32_t b = __float_as_uint(x);
+    return b ^ ((b >> 31) ? 0xffffffffu : 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t u) {
+    return __uint_as_float(u ^ ((u >> 31) ? 0x80000000u : 0xffffffffu));
+}
+
+// The shared per-query thresholds (TcParams::qthr) hold f2ord-encoded keys so
+// atomicMin orders negative (inner-product) keys too; 0xffffffff (the memset
+// pattern) is "no threshold yet".
+__device__ __forceinline__ float qthr_dec(uint32_t u) {
+    return u == 0xffffffffu ? __int_as_float(0x7f800000) : ord2f(u);
+}
 
 // ----------------------------------------------------------------- PTX
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
@@ -218,6 +236,17 @@ __device__ __forceinline__ void mma3_bf16_elect(uint32_t dcol, uint32_t ah, uint
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, t;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, t;\n\t}" ::"r"(dcol),
         "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(accum)
+        : "memory");
+}
+// one 1xBF16 K-step (wide mode: A_hi * B_hi)
+__device__ __forceinline__ void mma1_bf16_elect(uint32_t dcol, uint32_t ah, uint64_t bh, uint32_t idesc,
+                                                uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %4, p;\n\t}" ::"r"(dcol),
+        "r"(ah), "l"(bh), "r"(accum), "r"(idesc)
         : "memory");
 }
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
@@ -290,28 +319,39 @@ __device__ __forceinline__ TcItem tc_decode(const TcParams& p, uint32_t it) {
 }
 
 // bounds + filtering of one group for this thread's query (see tc_unit)
-template <int KT>
+template <int KT, bool W>
 __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, uint32_t j,
-                                          const float* wn, bool active, float nq,
+                                          const float* wn, bool active, float nq, float sq,
                                           const float (&dot)[32], float (&ubl)[KT], float& ubk,
                                           uint32_t& ncand, bool& overflow, float* clb,
                                           uint32_t* cloc, float* scr, TcProf& pf) {
     if (!active) return;
-    // pass 1: slot n can still enter the top-k only if its lower bound a - eps' <= ubk,
+    // W (inner product): key a = -q.x, the MMA value P' = 2^(eq+ev_n) q.x (+ error
+    // <= kEpsIP |q||x| unscaled); `nq` holds kEpsIP |q| 2^eq, `sq` 2^eq, wn[n] 2^-ev_n,
+    // wn[32 + n] |x_n|.  Scaled by 2^eq: slot n can enter iff
+    // P'_n 2^-ev_n + nq |x_n| >= -ubk 2^eq.
+    const float Wt = W ? -ubk * sq : 0.f;
+    // pass 1 (L2): slot n can still enter the top-k only if its lower bound a - eps' <= ubk,
     // i.e. dot >= V[n] + W (V = kVScale*ns from the mirror norms; a < 0 passes too,
     // since ubk > 0).  Most groups have no such slot: test max_n (dot - V) >= W first
     // (an FADD per slot, 3-input max, two independent chains), build the mask only
     // when the group has a survivor.
-    const float W = fmaf(kVScale, nq, -ubk * (0.5f / (1.0f - kEpsRel)));
+    const float Wl = W ? 0.f : fmaf(kVScale, nq, -ubk * (0.5f / (1.0f - kEpsRel)));
     {
         float m0 = -__int_as_float(0x7f800000), m1 = m0;
 #pragma unroll
         for (uint32_t n = 0; n < 32; n += 4) {
             const float4 v = reinterpret_cast<const float4*>(wn + 32)[n / 4];
-            m0 = fmaxf(m0, fmaxf(dot[n] - v.x, dot[n + 1] - v.y));  // FMNMX3
-            m1 = fmaxf(m1, fmaxf(dot[n + 2] - v.z, dot[n + 3] - v.w));
+            if constexpr (W) {
+                const float4 s4 = reinterpret_cast<const float4*>(wn)[n / 4];
+                m0 = fmaxf(m0, fmaxf(fmaf(dot[n], s4.x, nq * v.x), fmaf(dot[n + 1], s4.y, nq * v.y)));
+                m1 = fmaxf(m1, fmaxf(fmaf(dot[n + 2], s4.z, nq * v.z), fmaf(dot[n + 3], s4.w, nq * v.w)));
+            } else {
+                m0 = fmaxf(m0, fmaxf(dot[n] - v.x, dot[n + 1] - v.y));  // FMNMX3
+                m1 = fmaxf(m1, fmaxf(dot[n + 2] - v.z, dot[n + 3] - v.w));
+            }
         }
-        if (!(fmaxf(m0, m1) >= W)) return;
+        if (!(fmaxf(m0, m1) >= (W ? Wt : Wl))) return;
     }
 
     // valid slots of group j, from the snapshot (no table lookups)
@@ -330,10 +370,18 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
 #pragma unroll
     for (uint32_t n = 0; n < 32; n += 4) {
         const float4 v = reinterpret_cast<const float4*>(wn + 32)[n / 4];
-        need |= (dot[n] >= v.x + W) ? (1u << n) : 0u;
-        need |= (dot[n + 1] >= v.y + W) ? (2u << n) : 0u;
-        need |= (dot[n + 2] >= v.z + W) ? (4u << n) : 0u;
-        need |= (dot[n + 3] >= v.w + W) ? (8u << n) : 0u;
+        if constexpr (W) {
+            const float4 s4 = reinterpret_cast<const float4*>(wn)[n / 4];
+            need |= (fmaf(dot[n], s4.x, nq * v.x) >= Wt) ? (1u << n) : 0u;
+            need |= (fmaf(dot[n + 1], s4.y, nq * v.y) >= Wt) ? (2u << n) : 0u;
+            need |= (fmaf(dot[n + 2], s4.z, nq * v.z) >= Wt) ? (4u << n) : 0u;
+            need |= (fmaf(dot[n + 3], s4.w, nq * v.w) >= Wt) ? (8u << n) : 0u;
+        } else {
+            need |= (dot[n] >= v.x + Wl) ? (1u << n) : 0u;
+            need |= (dot[n + 1] >= v.y + Wl) ? (2u << n) : 0u;
+            need |= (dot[n + 2] >= v.z + Wl) ? (4u << n) : 0u;
+            need |= (dot[n + 3] >= v.w + Wl) ? (8u << n) : 0u;
+        }
     }
     need &= vmask;
     if (!need) return;
@@ -345,10 +393,20 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
     while (need) {
         const uint32_t n = __ffs(need) - 1;
         need &= need - 1;
-        const float t = nq + wn[n];
-        const float a = fmaf(-2.f, scr[n * kM], t);
-        const float e = fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, t, 1e-30f));
-        const float h = a + e, l = a - e;
+        float h, l;
+        if constexpr (W) {
+            const float isq = 1.0f / sq;  // exact: a power of 2
+            const float a = -(scr[n * kM] * wn[n]) * isq;
+            const float e = fmaf(nq * isq, wn[32 + n], 1e-30f);
+            h = a + e;
+            l = a - e;
+        } else {
+            const float t = nq + wn[n];
+            const float a = fmaf(-2.f, scr[n * kM], t);
+            const float e = fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, t, 1e-30f));
+            h = a + e;
+            l = a - e;
+        }
         if (h < ubk) {  // keep the k smallest upper bounds, sorted
             // ubl: ascending; entries [0, KT-k) are -inf sentinels, [KT-k, KT) the
             // k smallest upper bounds, so the k-th is always ubl[KT-1] (static
@@ -388,59 +446,49 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
 }
 
 // One unit (kGU consecutive groups j0.. of the item, accumulator u % kNB, norm
-// slot u % kNR).  The accumulator is released as soon as its dot products are in
-// registers (the MMA of unit u + kNB can start while this unit is filtered); the
-// norm slot once the filter is done.
-template <int KT>
+// slot u % kNR), filtered by the warpgroup (u & 1); accumulator and norm slot
+// are released when the filter is done.
+template <int KT, bool W>
 __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint32_t u, uint32_t j0,
                                         uint64_t* acc_full, uint64_t* acc_empty, uint32_t tmem_base,
-                                        uint32_t taddr_lane, int lane, bool active, float nq,
+                                        uint32_t taddr_lane, int lane, bool active, float nq, float sq,
                                         float (&ubl)[KT], float& ubk, uint32_t& ncand,
                                         bool& overflow, float* clb, uint32_t* cloc,
                                         float* scr, float* nslots, uint64_t* nfull,
                                         uint64_t* nempty, float* qt, float qshared, uint64_t qrow,
-                                        uint32_t m, int wg, TcProf& pf) {
-    const uint32_t b = u % kNB, ns = u % kNR;
+                                        uint32_t m, TcProf& pf) {
+    constexpr int NB = TcMode<W>::NB;
+    const uint32_t b = u % NB, ns = u % kNR;
     // qshared: the query's shared threshold (the smallest k-th upper bound any of
     // its runs has published, a valid filter bound for every run of the query),
     // loaded by the caller one unit ahead
     const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
     pf.mark(8);
-    mbar_wait(&acc_full[b], (u / kNB) & 1);
+    mbar_wait(&acc_full[b], (u / NB) & 1);
     __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after the per-thread spin
     pf.mark(4);
     tc_fence_after();
-    const uint32_t acol = tmem_base + taddr_lane + kColAcc + b * 32 * kGU;
-    float dot[kEarlyRelease ? kGU : 1][32];
-    if constexpr (kEarlyRelease) {
-#pragma unroll
-        for (int h = 0; h < kGU; ++h)
-            if ((uint32_t)h < ng) tmem_ld32(acol + 32 * h, dot[h]);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[b]);
-    }
+    const uint32_t acol = tmem_base + taddr_lane + TcMode<W>::ColAcc + b * 32 * kGU;
+    float dot[32];
     pf.mark(5);
     mbar_wait(&nfull[ns], (u / kNR) & 1);
     pf.mark(6);
     const float* wslot = nslots + ns * kGU * kNormFloats;
-    if (p.dense_out) {  // dense mode: write the approximate distances, no filtering
+    if (!W && p.dense_out) {  // dense mode (L2): write the approximate distances, no filtering
 #pragma unroll
         for (int h = 0; h < kGU; ++h) {
             if ((uint32_t)h >= ng) break;
-            if (kColSplit && h != wg) continue;
             const float* wn = wslot + h * kNormFloats;
-            const int hd = kEarlyRelease ? h : 0;
-            if constexpr (!kEarlyRelease) tmem_ld32(acol + 32 * h, dot[0]);
+            tmem_ld32(acol + 32 * h, dot);
             if (active) {
                 float av[32];
 #pragma unroll
                 for (int i = 0; i < 32; i += 4) {
                     const float4 v = reinterpret_cast<const float4*>(wn)[i / 4];
-                    av[i] = fmaf(-2.f, dot[hd][i], nq + v.x);
-                    av[i + 1] = fmaf(-2.f, dot[hd][i + 1], nq + v.y);
-                    av[i + 2] = fmaf(-2.f, dot[hd][i + 2], nq + v.z);
-                    av[i + 3] = fmaf(-2.f, dot[hd][i + 3], nq + v.w);
+                    av[i] = fmaf(-2.f, dot[i], nq + v.x);
+                    av[i + 1] = fmaf(-2.f, dot[i + 1], nq + v.y);
+                    av[i + 2] = fmaf(-2.f, dot[i + 2], nq + v.z);
+                    av[i + 3] = fmaf(-2.f, dot[i + 3], nq + v.w);
                 }
                 if (p.dense_list_base) {  // IVF: element (j, n) at base + (32 j + n) * 128
                     float* o = p.dense_out + qrow + (uint64_t)(32u * (j0 + h)) * kM;
@@ -475,10 +523,10 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                 }
             }
         }
-        if constexpr (!kEarlyRelease) tc_fence_before();
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-            if constexpr (!kEarlyRelease) mbar_arrive(&acc_empty[b]);
+            mbar_arrive(&acc_empty[b]);
             mbar_arrive(&nempty[ns]);
         }
         return;
@@ -488,25 +536,24 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
 #pragma unroll
     for (int h = 0; h < kGU; ++h) {
         if ((uint32_t)h >= ng) break;
-        if (kColSplit && h != wg) continue;
         pf.mark(7);
-        if constexpr (!kEarlyRelease) tmem_ld32(acol + 32 * h, dot[0]);
+        tmem_ld32(acol + 32 * h, dot);
         pf.mark(10);
-        tc_filter<KT>(p, d, j0 + h, wslot + h * kNormFloats, active, nq, dot[kEarlyRelease ? h : 0],
-                      ubl, ubk, ncand, overflow, clb, cloc, scr, pf);
+        tc_filter<KT, W>(p, d, j0 + h, wslot + h * kNormFloats, active, nq, sq, dot, ubl, ubk, ncand,
+                         overflow, clb, cloc, scr, pf);
     }
-    if constexpr (!kEarlyRelease) tc_fence_before();
+    tc_fence_before();
     __syncwarp();
     pf.mark(7);
     if (lane == 0) {
-        if constexpr (!kEarlyRelease) mbar_arrive(&acc_empty[b]);
+        mbar_arrive(&acc_empty[b]);
         mbar_arrive(&nempty[ns]);
     }
-    // publish an improved threshold (positive floats order like their bit patterns)
-    if (active && ubk < ubk0) atomicMin(reinterpret_cast<int*>(qt), __float_as_int(ubk));
+    // publish an improved threshold
+    if (active && ubk < ubk0) atomicMin(reinterpret_cast<uint32_t*>(qt), f2ord(ubk));
 }
 
-template <int KT>
+template <int KT, bool W>
 __global__ void __launch_bounds__(kTcThreads, 1)
     scan_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_off,
                    const __grid_constant__ CUtensorMap map_arena) {
@@ -533,8 +580,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t* nempty = nfull + kNR;        // kNR
     TcItem* ring = reinterpret_cast<TcItem*>(nempty + kNR);  // kRing decoded items
     float* cent_s = reinterpret_cast<float*>(ring + kRing);  // [kWG][kMaxD] the item's centroid
-    float* nqx = cent_s + kWG * kMaxD;                          // [2][kWG][kM] partial |r|^2
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(nqx + 2 * kWG * kM);
+    float* nqx = cent_s + kWG * kMaxD;  // [2][kWG][kM] partial |r|^2, then (wide) [2][kWG][kM] maxima
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(nqx + 4 * kWG * kM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t D = p.D;
@@ -594,7 +641,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 mbar_arrive(&it_full[rs]);  // release: the item is visible to the consumers
                 return d.valid != 0;
             };
-            uint32_t unit = 0;
+            uint32_t unit = 0, step = 0;
             bool have = fetch(0);
             pf.mark(1);
             for (uint32_t seq = 0; have; ++seq) {
@@ -603,17 +650,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 pf.mark(1);
                 // hoisted per-item lookups: the offline segment's first group, the
                 // list's block-table row (one entry per gpb groups, cached)
-                const uint32_t og = (d.off + 31u) >> 5, R = 2u * p.Dk;
+                const uint32_t og = (d.off + 31u) >> 5;
                 const uint64_t offg0 = og ? p.L.off_start[d.c] / 32u : 0ull;
                 const int32_t* trow = p.L.table + (uint64_t)d.c * p.L.MLB;
                 uint32_t cmid = 0xffffffffu;
                 uint64_t cblk = 0;
                 for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
-                    const uint32_t us = unit % kNU;
-                    mbar_wait(&empty[us], ((unit / kNU) & 1) ^ 1);
-                    pf.mark(2);
                     const uint32_t ng = min((uint32_t)kGU, d.g1 - j0);
-                    mbar_arrive_expect_tx(&full[us], ng * 2u * p.Dk * 64u);
                     const uint32_t nsl = unit % kNR;
                     uint64_t gidx[kGU];
                     bool gar[kGU];
@@ -633,8 +676,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                             gar[h] = true;
                             gidx[h] = cblk * p.L.gpb + gi;
                         }
-                        tma_load_2d(sB + (us * kGU + h) * kStage, gar[h] ? &map_arena : &map_off, 0,
-                                    (int)(gidx[h] * R), &full[us]);
+                    }
+                    // one stage pair per K-chunk (a single chunk unless wide): box
+                    // {32, brow} rows from row gidx * gstride + kc * brow
+                    for (uint32_t kc = 0; kc < p.nkc; ++kc, ++step) {
+                        const uint32_t us = step % kNU;
+                        mbar_wait(&empty[us], ((step / kNU) & 1) ^ 1);
+                        pf.mark(2);
+                        mbar_arrive_expect_tx(&full[us], ng * p.brow * 64u);
+#pragma unroll
+                        for (int h = 0; h < kGU; ++h) {
+                            if ((uint32_t)h >= ng) break;
+                            tma_load_2d(sB + (us * kGU + h) * kStage, gar[h] ? &map_arena : &map_off, 0,
+                                        (int)(gidx[h] * p.gstride + kc * p.brow), &full[us]);
+                        }
                     }
                     pf.mark(3);
                     // the unit's group norms -> norm slot nsl, once unit - kNR released it
@@ -660,9 +715,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // ------------------------------------------------ MMA issuer
         // N = 32*kGU: the unit's groups sit in consecutive stages, kStage apart (LBO)
         // D fp32, A/B bf16, A K-major (TMEM), B MN-major, N = 32*kGU, M = 128
-        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+        // (wide: A/B fp16, format code 0)
+        const uint32_t idesc = (1u << 4) | (W ? 0u : (1u << 7) | (1u << 10)) | (1u << 16) |
                                (((32u * kGU) >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
-        uint32_t unit = 0;
+        uint32_t unit = 0, step = 0;
         TcProf pf;
         pf.start();
         for (uint32_t seq = 0;; ++seq) {
@@ -673,33 +729,43 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&it_empty[rs]);
             if (!d.valid) break;
-            const uint32_t ab = seq & 1;  // this item's A buffer
-            mbar_wait(&a_full[ab], (seq >> 1) & 1);
+            const uint32_t ab = W ? 0u : (seq & 1);  // this item's A buffer
+            mbar_wait(&a_full[ab], W ? (seq & 1) : ((seq >> 1) & 1));
             pf.mark(2);
             const uint32_t abase = tmem_base + ab * kColA2;
+            constexpr int NB = TcMode<W>::NB;
             for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
-                const uint32_t us = unit % kNU, b = unit % kNB;
-                mbar_wait(&full[us], (unit / kNU) & 1);
-                pf.mark(3);
-                mbar_wait(&acc_empty[b], ((unit / kNB) & 1) ^ 1);
+                const uint32_t b = unit % NB;
+                const uint32_t dcol = tmem_base + TcMode<W>::ColAcc + b * 32 * kGU;
+                mbar_wait(&acc_empty[b], ((unit / NB) & 1) ^ 1);
                 pf.mark(4);
-                __syncwarp();
-                tc_fence_after();
-                {
-                    // 3xBF16: A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (A from TMEM, B from smem);
+                for (uint32_t kc = 0; kc < p.nkc; ++kc, ++step) {
+                    const uint32_t us = step % kNU;
+                    mbar_wait(&full[us], (step / kNU) & 1);
+                    pf.mark(3);
+                    __syncwarp();
+                    tc_fence_after();
                     // a K-step is 16 rows of 64 B: descriptors advance 1024 B (64 in the
                     // >>4 address field), A 8 TMEM columns (16 bf16)
-                    const uint32_t bh0 = stages + us * kGU * (uint32_t)kStage, bl0 = bh0 + p.Dk * 64u;
-                    const uint32_t dcol = tmem_base + kColAcc + b * 32 * kGU;
+                    const uint32_t bh0 = stages + us * kGU * (uint32_t)kStage;
                     const uint64_t bh = umma_desc(bh0, kStage, 512, 4);
-                    const uint64_t bl = umma_desc(bl0, kStage, 512, 4);
-                    const uint32_t nks = p.Dk / 16;
-                    for (uint32_t ks = 0; ks < nks; ++ks)
-                        mma3_bf16_elect(dcol, abase + ks * 8, abase + kColAlo + ks * 8,
-                                        bh + ks * 64ull, bl + ks * 64ull, idesc, ks);
-                    mma_commit_elect(&acc_full[b]);
+                    if constexpr (W) {
+                        // 1xBF16: A_hi * B_hi over this 128-row K-chunk
+                        const uint32_t nks = p.brow / 16, a0 = abase + kc * (p.brow / 2);
+                        for (uint32_t ks = 0; ks < nks; ++ks)
+                            mma1_bf16_elect(dcol, a0 + ks * 8, bh + ks * 64ull, idesc, kc | ks);
+                    } else {
+                        // 3xBF16: A_hi*B_hi + A_hi*B_lo + A_lo*B_hi (A from TMEM, B from smem)
+                        const uint64_t bl = umma_desc(bh0 + p.Dk * 64u, kStage, 512, 4);
+                        const uint32_t nks = p.Dk / 16;
+                        for (uint32_t ks = 0; ks < nks; ++ks)
+                            mma3_bf16_elect(dcol, abase + ks * 8, abase + kColAlo + ks * 8,
+                                            bh + ks * 64ull, bl + ks * 64ull, idesc, ks);
+                    }
                     mma_commit_elect(&empty[us]);
+                    __syncwarp();
                 }
+                mma_commit_elect(&acc_full[b]);
                 __syncwarp();
                 pf.mark(5);
             }
@@ -719,7 +785,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // read item seq from the ring and write its A operand (centred queries
         // r = q - c of the tile, split r_hi = bf16_rn(r), r_lo = bf16_rn(r - r_hi);
         // lane m = query row, column = a pair of dims) into A buffer seq & 1
-        auto build = [&](uint32_t seq, TcItem& d, float& nq) -> bool {
+        auto build = [&](uint32_t seq, TcItem& d, float& nq, float& sq) -> bool {
             const uint32_t rs = seq % kRing;
             mbar_wait(&it_full[rs], (seq / kRing) & 1);
             d = ring[rs];
@@ -727,12 +793,74 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0) mbar_arrive(&it_empty[rs]);
             if (!d.valid) return false;
             pf.mark(0);
-            const uint32_t ab = seq & 1;
-            if (seq >= 2) mbar_wait(&a_free[ab], ((seq - 2) >> 1) & 1);
+            const uint32_t ab = W ? 0u : (seq & 1);
+            if (W && seq >= 1) mbar_wait(&a_free[0], (seq - 1) & 1);
+            if (!W && seq >= 2) mbar_wait(&a_free[ab], ((seq - 2) >> 1) & 1);
             pf.mark(2);
             const bool active = (uint32_t)m < d.npairs;
             const uint32_t pair = active ? d.pairs[m] : 0u;
             const float* q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
+            if constexpr (W) {
+                // inner product: A = the query rows (uncentred) scaled by 2^eq (max
+                // |q_d| 2^eq in [2^13, 2^14), mirror.cuh) as one fp16 plane; 64-dim
+                // chunks alternate between the warpgroups.  Pass 1: max |q_d| and
+                // |q|^2 (halves exchanged in smem); pass 2: scale, convert, store.
+                float mxh = 0.f, nqh = 0.f;
+                for (uint32_t c = wg; 64 * c < p.Dk; c += 2) {
+                    float4 qv[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        qv[i] = (active && 64 * c + 4 * i < p.Dp)
+                                    ? __ldg(reinterpret_cast<const float4*>(q + 64 * c) + i)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        mxh = fmaxf(mxh, fmaxf(fmaxf(fabsf(qv[i].x), fabsf(qv[i].y)),
+                                               fmaxf(fabsf(qv[i].z), fabsf(qv[i].w))));
+                        nqh = __fadd_rn(nqh, __fmul_rn(qv[i].x, qv[i].x));
+                        nqh = __fadd_rn(nqh, __fmul_rn(qv[i].y, qv[i].y));
+                        nqh = __fadd_rn(nqh, __fmul_rn(qv[i].z, qv[i].z));
+                        nqh = __fadd_rn(nqh, __fmul_rn(qv[i].w, qv[i].w));
+                    }
+                }
+                float* nqb = nqx + (seq & 1) * kWG * kM;                 // partial |q|^2
+                float* mxs = nqx + 2 * kWG * kM + (seq & 1) * kWG * kM;  // partial max |q_d|
+                nqb[wg * kM + m] = nqh;
+                mxs[wg * kM + m] = mxh;
+                named_bar(3, 256);
+                const float mx = fmaxf(mxs[m], mxs[kM + m]);
+                const int eq = wide_scale_exp(mx);
+                sq = ldexpf(1.f, eq);
+                nq = kEpsIP * sqrtf(__fadd_rn(nqb[m], nqb[kM + m])) * sq;
+                __syncwarp();
+                tc_fence_after();
+                for (uint32_t c = wg; 64 * c < p.Dk; c += 2) {
+                    float4 qv[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        qv[i] = (active && 64 * c + 4 * i < p.Dp)
+                                    ? __ldg(reinterpret_cast<const float4*>(q + 64 * c) + i)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                    uint32_t vh[32];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        // x 2^eq is exact (a power of 2, scaling toward [2^13, 2^14))
+                        const __half2 h0 = __floats2half2_rn(qv[i].x * sq, qv[i].y * sq);
+                        const __half2 h1 = __floats2half2_rn(qv[i].z * sq, qv[i].w * sq);
+                        vh[2 * i] = *reinterpret_cast<const uint32_t*>(&h0);
+                        vh[2 * i + 1] = *reinterpret_cast<const uint32_t*>(&h1);
+                    }
+                    __syncwarp();
+                    BIVF_TMEM_ST32(tmem_base + taddr_lane + 32 * c, vh);
+                }
+                __syncwarp();
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                tc_fence_before();
+                named_bar(3, 256);
+                if (wt == 0) mbar_arrive(&a_full[0]);
+                pf.mark(3);
+                return true;
+            }
             // warpgroup g writes dims [64g, 64g + 64) of both planes (A_hi and A_lo):
             // its half of the thread's query row (registers, all loads in flight at
             // once) minus its half of the list centroid (the warpgroup's smem row)
@@ -791,12 +919,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         };
         uint32_t unit = 0;
         TcItem d;
-        float nq = 0.f;
-        bool have = build(0, d, nq);
+        float nq = 0.f, sq = 1.f;
+        bool have = build(0, d, nq, sq);
         for (uint32_t seq = 0; have; ++seq) {
             TcItem dn;
-            float nqn = 0.f;
-            const bool hn = build(seq + 1, dn, nqn);  // next item's A while this one's MMAs run
+            float nqn = 0.f, sqn = 1.f;
+            bool hn = false;
+            // the next item's A while this one's MMAs run (two A buffers); wide mode
+            // has one A buffer: it is rewritten after this item's units
+            if constexpr (!W) hn = build(seq + 1, dn, nqn, sqn);
             const bool active = (uint32_t)m < d.npairs;
             const uint32_t pair = active ? d.pairs[m] : 0u;
             const uint64_t run = ((((uint64_t)pair * p.maxch + d.chunk) << 1) | (uint32_t)wg);
@@ -821,15 +952,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             pf.mark(1);
             float* qt = p.qthr + (active ? pair / p.P : 0u);
-            float qsh = active ? __ldcg(qt) : ubk;
+            float qsh = active ? qthr_dec(__ldcg(reinterpret_cast<const uint32_t*>(qt))) : ubk;
             for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
-                if (!kColSplit && (unit & 1u) != (uint32_t)wg) continue;
+                if ((unit & 1u) != (uint32_t)wg) continue;
                 const float qcur = qsh;
-                if (active) qsh = __ldcg(qt);  // in flight during this unit, used by the next
-                tc_unit<KT>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
-                            active, nq, ubl, ubk, ncand, overflow, clb, cloc,
+                if (active) qsh = qthr_dec(__ldcg(reinterpret_cast<const uint32_t*>(qt)));  // in flight during this unit, used by the next
+                tc_unit<KT, W>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
+                            active, nq, sq, ubl, ubk, ncand, overflow, clb, cloc,
                             scratch + wg * 32 * kM + m, nslots, nfull, nempty, qt, qcur,
-                            dbase, (uint32_t)m, wg, pf);
+                            dbase, (uint32_t)m, pf);
             }
             pf.mark(8);
             // run output: k upper bounds + surviving candidates (compacted in place)
@@ -851,8 +982,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 p.ccount[run] = overflow ? kOverflow : w;
             }
             pf.mark(8);
+            if constexpr (W) hn = build(seq + 1, dn, nqn, sqn);
             d = dn;
             nq = nqn;
+            sq = sqn;
             have = hn;
         }
         pf.report("math", warp);
@@ -910,6 +1043,54 @@ __device__ __forceinline__ float exact_l2_row(const float* qs, const float* x, u
     return acc;
 }
 
+// the exact key of either metric: L2 = the sequential l2 sum; IP = -(sequential
+// q.x), ip_step (common.cuh), the CUDA-core scan's bits
+template <int MET>
+__device__ __forceinline__ float exact_key_row(const float* qs, const float* x, uint32_t D) {
+    if constexpr (MET == kL2) {
+        return exact_l2_row(qs, x, D);
+    } else {
+        float acc = 0.f;
+        uint32_t d0 = 0;
+        if ((D & 3u) == 0) {
+            for (; d0 + 16 <= D; d0 += 16) {
+                float4 v[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v[i] = __ldg(reinterpret_cast<const float4*>(x + d0) + i);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    acc = ip_step(acc, qs[d0 + 4 * i + 0], v[i].x);
+                    acc = ip_step(acc, qs[d0 + 4 * i + 1], v[i].y);
+                    acc = ip_step(acc, qs[d0 + 4 * i + 2], v[i].z);
+                    acc = ip_step(acc, qs[d0 + 4 * i + 3], v[i].w);
+                }
+            }
+        }
+        for (; d0 < D; ++d0) acc = ip_step(acc, qs[d0], __ldg(x + d0));
+        return -acc;
+    }
+}
+template <int MET>
+__device__ __forceinline__ float exact_key(const float* qs, const float* x, uint32_t D) {
+    if constexpr (MET == kL2) {
+        return exact_l2(qs, x, D);
+    } else {
+        // interleaved slot (stride 32 floats): 32 loads in flight per batch, then
+        // the sequential chain over them
+        float acc = 0.f;
+        uint32_t d0 = 0;
+        for (; d0 + 32 <= D; d0 += 32) {
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = x[(uint64_t)(d0 + i) * 32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc = ip_step(acc, qs[d0 + i], v[i]);
+        }
+        for (; d0 < D; ++d0) acc = ip_step(acc, qs[d0], x[(uint64_t)d0 * 32]);
+        return -acc;
+    }
+}
+
 // row of slot (group j of list c, slot s) in the mirror's row copy
 __device__ __forceinline__ const float* cand_row(const TcParams& p, uint32_t c, uint32_t off,
                                                  uint32_t j, uint32_t s) {
@@ -920,7 +1101,7 @@ __device__ __forceinline__ const float* cand_row(const TcParams& p, uint32_t c, 
     return p.arena_rows + (g * 32u + s) * p.D;
 }
 
-template <int KPL>
+template <int KPL, int MET>
 __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d, long long* out_i,
                               uint32_t* out_cnt, uint32_t nq) {
     extern __shared__ float qsm[];  // [warps][Dp] queries, then [warps][32] x 2 queue
@@ -938,7 +1119,7 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
     // lanes sweep it flat (slots of chunks h >= nch[c] were never written).
     // Only values <= the scan's shared threshold (itself one run's k-th upper
     // bound, so >= theta) can matter.
-    const float pre = __ldcg(p.qthr + q);
+    const float pre = qthr_dec(__ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + q));
     WarpTopK<KPL> th;
     th.init();
     {
@@ -991,8 +1172,8 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
         if (ok) {
             const uint32_t c = qc[lane], loc = ql[lane];
             const GroupRef g = ivf_group(p.L, c, p.snap_off[c], p.snap_len[c], loc >> 5);
-            dist = p.off_rows ? exact_l2_row(qs, cand_row(p, c, p.snap_off[c], loc >> 5, loc & 31), p.D)
-                              : exact_l2(qs, g.base + (loc & 31), p.D);
+            dist = p.off_rows ? exact_key_row<MET>(qs, cand_row(p, c, p.snap_off[c], loc >> 5, loc & 31), p.D)
+                              : exact_key<MET>(qs, g.base + (loc & 31), p.D);
             id = g.ids[loc & 31];
         }
         offer(dist, id, ok);
@@ -1030,7 +1211,7 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
             for (uint32_t j = g0; j < g1; ++j) {
                 const GroupRef g = ivf_group(p.L, cc, off, len, j);
                 const bool ok = lane < g.nvalid;
-                const float dist = exact_l2(qs, g.base + lane, p.D);
+                const float dist = exact_key<MET>(qs, g.base + lane, p.D);
                 offer(dist, ok ? g.ids[lane] : -1, ok);
             }
         }
@@ -1108,15 +1289,6 @@ __device__ __forceinline__ uint64_t warp_elem(const uint64_t (&v)[R], uint32_t e
         if (e >> 5 == (uint32_t)j) x = v[j];
     return __shfl_sync(0xffffffffu, x, e & 31);
 }
-// order-preserving float -> uint32 (negative values included)
-__device__ __forceinline__ uint32_t f2ord(float x) {
-    const uint32_t b = __float_as_uint(x);
-    return b ^ ((b >> 31) ? 0xffffffffu : 0x80000000u);
-}
-__device__ __forceinline__ float ord2f(uint32_t u) {
-    return __uint_as_float(u ^ ((u >> 31) ? 0x80000000u : 0xffffffffu));
-}
-
 // Fast selection of dense_select_kernel (R keys per lane, k <= 32R <= n): true when
 // the exact top-k was written (false: more than 32R values tie the bounds, the
 // caller's general path runs with *pre as its pre-threshold).
@@ -1541,9 +1713,20 @@ constexpr size_t tc_smem_bytes() {
     return 1024 + TcCfg<KT>::NS * kStage + kWG * 32 * kM * 4 + kWG * TcCfg<KT>::KC * kM * 8 +
            kNR * kGU * kNormFloats * 4 +
            (2 * TcCfg<KT>::NU + 2 * kNB + 2 * kNR + 2 * kRing + 4) * 8 + kRing * sizeof(TcItem) +
-           kWG * kMaxD * 4 + 2 * kWG * kM * 4 + 16;
+           kWG * kMaxD * 4 + 4 * kWG * kM * 4 + 16;
 }
 static_assert(tc_smem_bytes<16>() <= 232448 && tc_smem_bytes<32>() <= 232448, "smem budget");
+
+template <int KT, bool W>
+cudaError_t tc_attr() {
+    static bool done = false;
+    if (done) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel<KT, W>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)tc_smem_bytes<KT>());
+    done = e == cudaSuccess;
+    return e;
+}
 
 }  // namespace
 
@@ -1564,20 +1747,26 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }  // namespace
 
 bool tc_supported(uint32_t D, uint32_t k, int metric) {
-    return metric == kL2 && D >= 8 && D <= (uint32_t)kMaxD && k <= 32;
+    if (k > 32 || D < 8) return false;
+    // L2: 3xBF16, D <= 128; inner product: the wide 1xBF16 mode, A (the query
+    // rows' hi plane) fits its 384 TMEM columns up to D = 768
+    return metric == kL2 ? D <= (uint32_t)kMaxD : mirror_k_wide(D) <= 768;
 }
 
 bool tc_dense_supported(uint32_t D, uint32_t k, int metric) {
     return metric == kL2 && D >= 8 && D <= (uint32_t)kMaxD && k > 32 && k <= 256;
 }
 
-cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUtensorMap* out) {
+cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, bool wide,
+                            CUtensorMap* out) {
     auto enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
-    const uint32_t K = mirror_k(D);
-    cuuint64_t dims[2] = {32, std::max<cuuint64_t>(groups * 2ull * K, 1)};
+    // rows per group: 2K (hi + lo planes) or, wide, K (hi plane) read in chunks
+    const uint32_t K = wide ? mirror_k_wide(D) : mirror_k(D);
+    const uint32_t rows = wide ? K : 2 * K, box_rows = wide ? mirror_chunk_wide(D) : 2 * K;
+    cuuint64_t dims[2] = {32, std::max<cuuint64_t>(groups * rows, 1)};
     cuuint64_t strides[1] = {64};
-    cuuint32_t box[2] = {32, 2 * K};
+    cuuint32_t box[2] = {32, box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<float*>(base), dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1626,6 +1815,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int max_grid) {
     if (sh.nq == 0) return cudaSuccess;
+    const bool wide = sh.metric == kIP;  // 1xBF16 inner-product mode (mirror.cuh wide mirror)
+    if (wide && dense) return cudaErrorInvalidValue;
     SearchShape s2 = sh;
     s2.QT = kM;
     cudaError_t e = cudaSuccess;
@@ -1653,7 +1844,10 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     TcParams p{};
     p.L = L;
     p.D = L.D;
-    p.Dk = (L.D + 15) & ~15u;
+    p.Dk = wide ? mirror_k_wide(L.D) : (L.D + 15) & ~15u;
+    p.brow = wide ? mirror_chunk_wide(L.D) : 2 * p.Dk;
+    p.gstride = wide ? p.Dk : 2 * p.Dk;
+    p.nkc = wide ? p.Dk / p.brow : 1;
     p.Dp = pad4(L.D);
     p.k = sh.k;
     p.P = sh.P;
@@ -1687,18 +1881,11 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     p.clb = T.clb;
     p.cloc = T.cloc;
     const size_t sm16 = tc_smem_bytes<16>(), sm32 = tc_smem_bytes<32>();
-    static bool attr = false;
-    if (!attr) {
-        e = cudaFuncSetAttribute(scan_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sm32);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(scan_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sm16);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    // shared per-query thresholds start at +inf-ish (0x7f7f7f7f = 3.4e38)
-    e = cudaMemsetAsync(T.qthr, 0x7f, (size_t)sh.nq * 4, s);
+    e = wide ? (sh.k <= 16 ? tc_attr<16, true>() : tc_attr<32, true>())
+             : (sh.k <= 16 ? tc_attr<16, false>() : tc_attr<32, false>());
+    if (e != cudaSuccess) return e;
+    // shared per-query thresholds start at "none" (0xffffffff, qthr_dec -> +inf)
+    e = cudaMemsetAsync(T.qthr, 0xff, (size_t)sh.nq * 4, s);
     if (e != cudaSuccess) return e;
     if (ev0) cudaEventRecord(ev0, s);
     int grid = std::max(1, std::min(num_sms, max_grid));  // no idle CTAs holding whole SMs
@@ -1709,8 +1896,13 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
             e = launch_plan(L, B, probes, s2, s);
             if (e != cudaSuccess) return e;
         }
-        if (sh.k <= 16) scan_tc_kernel<16><<<grid, kTcThreads, sm16, s>>>(p, map_off, map_arena);
-        else scan_tc_kernel<32><<<grid, kTcThreads, sm32, s>>>(p, map_off, map_arena);
+        if (wide) {
+            if (sh.k <= 16) scan_tc_kernel<16, true><<<grid, kTcThreads, sm16, s>>>(p, map_off, map_arena);
+            else scan_tc_kernel<32, true><<<grid, kTcThreads, sm32, s>>>(p, map_off, map_arena);
+        } else {
+            if (sh.k <= 16) scan_tc_kernel<16, false><<<grid, kTcThreads, sm16, s>>>(p, map_off, map_arena);
+            else scan_tc_kernel<32, false><<<grid, kTcThreads, sm32, s>>>(p, map_off, map_arena);
+        }
         count_launch();
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -1743,8 +1935,12 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                 dense->out, dense->ld, dense->nq, off_nrm, off_rows, queries, p.Dp, p.D, n, sh.nq,
                 sh.k, out_d, out_i);
     } else {
-        refine_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
-            p, probes, out_d, out_i, out_cnt, sh.nq);
+        if (wide)
+            refine_kernel<1, kIP><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
+                p, probes, out_d, out_i, out_cnt, sh.nq);
+        else
+            refine_kernel<1, kL2><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
+                p, probes, out_d, out_i, out_cnt, sh.nq);
     }
     count_launch();
     return cudaGetLastError();

@@ -47,9 +47,10 @@ cudaError_t launch_dense_plan(const DevLists& L, const PlanBufs& B, const long l
                               const SearchShape& sh, uint64_t* list_len, uint64_t* list_base,
                               void* tmp, size_t tmp_bytes, uint64_t* total, cudaStream_t s);
 
-// 2-D TMA map over a scan mirror region (mirror.cuh: `groups` groups of
-// 2K rows of 32 bf16), box = {32, 2K}, SWIZZLE_64B.
-cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, CUtensorMap* out);
+// 2-D TMA map over a scan mirror region (mirror.cuh: `groups` groups of 2K rows
+// of 32 bf16, box = {32, 2K}; wide: K rows, box = {32, min(K, 128)}), SWIZZLE_64B.
+cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, bool wide,
+                            CUtensorMap* out);
 
 cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,
                                  const float* queries, const float* centroids,

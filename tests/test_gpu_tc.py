@@ -179,3 +179,51 @@ def test_pinned_search_matches(gpu_ready):
     out2 = (bivf.pinned_empty((1000, 10), np.int64), bivf.pinned_empty((1000, 10), np.float32),
             bivf.pinned_empty((1000,), np.uint32))
     assert_same(ref, ix.search_batch(q, 10, 8, out=out2))
+
+
+@pytest.mark.parametrize("D,C,T,n,norm", [(8, 6, 16, 2000, False), (64, 16, 64, 8000, True),
+                                          (100, 10, 32, 5000, False), (200, 16, 64, 6000, True),
+                                          (768, 32, 128, 8000, True)])
+def test_tc_inner_product_equals_exact(gpu_ready, D, C, T, n, norm):
+    """Inner product on the tensor cores (wide mode: 1xBF16 over the uncentred
+    bf16 mirror, 128-row K-chunks for D > 128, proven bound kEpsIP |q||x|) returns
+    exactly the CUDA-core exact scan's ids and key bits (key = -sequential q.x),
+    small and seeded (>= 512-query) batches, with inserts and deletes."""
+    def data(m, seed):
+        x = bivf.synthetic_dataset(m, D, 3 * C, seed)
+        if norm:
+            x /= np.linalg.norm(x, axis=1, keepdims=True)
+        return np.ascontiguousarray(x, np.float32)
+    base = data(n, 41)
+    cent, asg, _ = bivf.kmeans(base, C, 5, 41)
+    ix = ClusterIndex.empty(D, C, block_capacity=T, num_blocks=max(64, 4 * n // T + 4 * C),
+                            metric=bivf.METRIC_IP)
+    ix.set_centroids(cent)
+    ix.bulk_load(base, ix.assign_batch(base))
+    ix.insert(data(n // 4 + 1, 42))
+    ix.remove(np.arange(0, n, 13))
+    for nq in (200, 1200):
+        q = data(nq, 43 + nq)
+        for k, npb in ((1, 2), (10, min(4, C)), (32, min(8, C))):
+            a, b = both(ix, q, k, npb)
+            assert_same(a, b)
+
+
+@pytest.mark.parametrize("C,D", [(100, 96), (257, 768)])
+def test_tc_inner_product_quantizer_matches_exact(gpu_ready, C, D):
+    """The inner-product coarse quantizer on the tensor cores (centroids as one
+    wide-mode list, filter + exact refine) returns exactly the CUDA-core
+    quantizer's (key, cluster) top-P (max inner product, lowest id on ties)."""
+    x = bivf.synthetic_dataset(20 * C + 2000, D, 2 * C, 19)
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    x = np.ascontiguousarray(x, np.float32)
+    cent, _, _ = bivf.kmeans(x[: 20 * C], C, 3, 19)
+    ix = ClusterIndex.empty(D, C, block_capacity=64, num_blocks=64, metric=bivf.METRIC_IP)
+    ix.set_centroids(cent)
+    q = x[20 * C:]
+    for P in (1, 7, 32):
+        ix.set_scan_mode("cuda")
+        a = ix.probes(q, P)
+        ix.set_scan_mode("auto")
+        b = ix.probes(q, P)
+        assert np.array_equal(a, b), (C, D, P)

@@ -16,7 +16,7 @@ where they apply.
         8 B200s serves
   cfg5  IVF-Flat 20M x 768 inner product (32768 unit centres, x = normalize(u +
         0.5 N(0,1)/sqrt(768))), nlist 4096, nprobe 32, k 10, 10K vec/s live inserts
-        (IP: the exact CUDA-core scan)
+        (IP: the tensor-core wide mode, 1xFP16 filter + exact refine)
 
 Data are synthetic, generated on the GPU with torch's Philox generator (a fixed
 seed per config; plumbing, not the measured path) and loaded through the
@@ -244,9 +244,11 @@ def run(args):
                 "h2d_bytes_per_step": BATCH * D * 4, "d2h_bytes_per_step": BATCH * K * 12 + BATCH * 4},
         "phase_ms": {"quantizer": round(phm[0], 3), "plan": round(phm[1], 3), "scan": round(phm[2], 3),
                      "merge_or_refine": round(phm[3], 3)},
-        "scan_path": ("tensor-core filter + exact refine" if K <= 32 else
+        "scan_path": ("tensor-core 3xBF16 filter + exact refine" if K <= 32 else
                       "tensor-core dense distances + exact selection")
-        if (c["metric"] == 0 and 8 <= D <= 128 and K <= 256) else "CUDA-core exact scan",
+        if (c["metric"] == 0 and 8 <= D <= 128 and K <= 256) else
+        ("tensor-core 1xFP16 inner-product filter (wide mode) + exact refine"
+         if (c["metric"] == 1 and 8 <= D <= 768 and K <= 32) else "CUDA-core exact scan"),
         "gpu_launches": int(launches),
     }
     if th is not None:
