@@ -53,13 +53,16 @@ constexpr int kTcThreads = 64 + 128 * kWG;  // warp0 TMA, warp1 MMA, warps 2.. m
 constexpr int kM = 128;                    // queries per tile (MMA M, TMEM lanes)
 constexpr int kGU = 2;                     // groups per unit (MMA N = 32 * kGU)
 // smem stages (one group each; kNS / kGU unit slots) and smem candidate slots
-// per thread, by top-k width: k <= 16 -> 6 stages, 40 slots; k <= 32 -> 4, 56
-// (an overflowed run is rescanned exactly by the refine)
-template <int KT>
+// per thread, by top-k width: k <= 16 -> 6 stages, 40 slots; k <= 32 -> 4, 56.
+// Wide mode stages hold one 128-row fp16 chunk (8 KB instead of 16 KB); the
+// smem freed goes to candidate slots (64 / 72: the looser inner-product bound
+// keeps more candidates).  An overflowed run is rescanned exactly by the refine.
+template <int KT, bool W = false>
 struct TcCfg {
     static constexpr int NS = KT <= 16 ? 6 : 4;
-    static constexpr int KC = KT <= 16 ? 40 : 56;
+    static constexpr int KC = W ? (KT <= 16 ? 64 : 72) : (KT <= 16 ? 40 : 56);
     static constexpr int NU = NS / 2;
+    static constexpr int STAGE = W ? 128 * 64 : 2 * 128 * 64;  // bytes per stage
 };
 // Measured and dropped: releasing a unit's accumulator before filtering (no gain,
 // more registers), both warpgroups on every unit (twice the per-unit fixed cost).
@@ -105,8 +108,8 @@ struct TcProf {
 #endif
 };
 constexpr int kMaxD = 128;
-// a stage = one group's mirror planes: 2K rows of 64 bytes (32 bf16: [s_hi], [s_lo])
-constexpr int kStage = 2 * kMaxD * 64;
+// a stage = one group's mirror planes: 2K rows of 64 bytes (32 bf16: [s_hi], [s_lo]);
+// wide mode: one 128-row K-chunk of the fp16 plane (TcCfg::STAGE)
 // TMEM columns (a column holds two bf16 of a row): two A buffers (items alternate,
 // so the next item's A is written while the MMAs of the current one run), each
 // A_hi [0,64) + A_lo [64,128); accumulators [256, 256 + 64*kNB)
@@ -421,9 +424,9 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
             ubk = fminf(ubk, ubl[KT - 1]);  // ubk = min(own k-th UB, the query's shared one)
         }
         if (l <= ubk && !overflow) {
-            if (ncand == (uint32_t)TcCfg<KT>::KC) {  // compact against the tighter threshold
+            if (ncand == (uint32_t)TcCfg<KT, W>::KC) {  // compact against the tighter threshold
                 uint32_t w = 0;
-                for (uint32_t i = 0; i < (uint32_t)TcCfg<KT>::KC; ++i) {
+                for (uint32_t i = 0; i < (uint32_t)TcCfg<KT, W>::KC; ++i) {
                     const float li = clb[i * kM];
                     if (li <= ubk) {
                         const uint32_t ci = cloc[i * kM];
@@ -434,7 +437,7 @@ __device__ __forceinline__ void tc_filter(const TcParams& p, const TcItem& d, ui
                 }
                 ncand = w;
             }
-            if (ncand < (uint32_t)TcCfg<KT>::KC) {
+            if (ncand < (uint32_t)TcCfg<KT, W>::KC) {
                 clb[ncand * kM] = l;
                 cloc[ncand * kM] = jl | n;
                 ++ncand;
@@ -455,7 +458,7 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                                         float (&ubl)[KT], float& ubk, uint32_t& ncand,
                                         bool& overflow, float* clb, uint32_t* cloc,
                                         float* scr, float* nslots, uint64_t* nfull,
-                                        uint64_t* nempty, float* qt, float qshared, uint64_t qrow,
+                                        uint64_t* nempty, float* qt, uint32_t qshared, uint64_t qrow,
                                         uint32_t m, TcProf& pf) {
     constexpr int NB = TcMode<W>::NB;
     const uint32_t b = u % NB, ns = u % kNR;
@@ -531,7 +534,7 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
         }
         return;
     }
-    ubk = fminf(ubk, qshared);
+    ubk = fminf(ubk, qthr_dec(qshared));
     const float ubk0 = ubk;
 #pragma unroll
     for (int h = 0; h < kGU; ++h) {
@@ -561,7 +564,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // 1024-align the dynamic smem base (swizzle atoms)
     const uint32_t raw_s = smem_u32(smem_raw);
     const uint32_t pad = ((raw_s + 1023u) & ~1023u) - raw_s;
-    constexpr int kNS = TcCfg<KT>::NS, kNU = TcCfg<KT>::NU, kKCs = TcCfg<KT>::KC;
+    constexpr int kNS = TcCfg<KT, W>::NS, kNU = TcCfg<KT, W>::NU, kKCs = TcCfg<KT, W>::KC;
+    constexpr int kStage = TcCfg<KT, W>::STAGE;
     unsigned char* sB = smem_raw + pad;                        // kNS * kStage
     float* scratch = reinterpret_cast<float*>(sB + kNS * kStage);  // [kWG][32][kM] pass-2 dots
     float* cand_lb = scratch + kWG * 32 * kM;                        // [kWG][kKCs][kM]
@@ -952,11 +956,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             pf.mark(1);
             float* qt = p.qthr + (active ? pair / p.P : 0u);
-            float qsh = active ? qthr_dec(__ldcg(reinterpret_cast<const uint32_t*>(qt))) : ubk;
+            // raw f2ord bits, decoded at use: the load stays in flight during a unit
+            uint32_t qsh = active ? __ldcg(reinterpret_cast<const uint32_t*>(qt)) : 0xffffffffu;
             for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
                 if ((unit & 1u) != (uint32_t)wg) continue;
-                const float qcur = qsh;
-                if (active) qsh = qthr_dec(__ldcg(reinterpret_cast<const uint32_t*>(qt)));  // in flight during this unit, used by the next
+                const uint32_t qcur = qsh;
+                if (active) qsh = __ldcg(reinterpret_cast<const uint32_t*>(qt));  // in flight during this unit, used by the next
                 tc_unit<KT, W>(p, d, unit, j0, acc_full, acc_empty, tmem_base, taddr_lane, lane,
                             active, nq, sq, ubl, ubk, ncand, overflow, clb, cloc,
                             scratch + wg * 32 * kM + m, nslots, nfull, nempty, qt, qcur,
@@ -1708,14 +1713,16 @@ __global__ void dense_list_len_kernel(DevLists L, const uint32_t* snap_off, cons
     len[c] = tiles * ivf_ngroups(L, snap_off[c], snap_len[c]) * 32ull * kM;
 }
 
-template <int KT>
+template <int KT, bool W>
 constexpr size_t tc_smem_bytes() {
-    return 1024 + TcCfg<KT>::NS * kStage + kWG * 32 * kM * 4 + kWG * TcCfg<KT>::KC * kM * 8 +
+    return 1024 + TcCfg<KT, W>::NS * TcCfg<KT, W>::STAGE + kWG * 32 * kM * 4 + kWG * TcCfg<KT, W>::KC * kM * 8 +
            kNR * kGU * kNormFloats * 4 +
-           (2 * TcCfg<KT>::NU + 2 * kNB + 2 * kNR + 2 * kRing + 4) * 8 + kRing * sizeof(TcItem) +
+           (2 * TcCfg<KT, W>::NU + 2 * kNB + 2 * kNR + 2 * kRing + 4) * 8 + kRing * sizeof(TcItem) +
            kWG * kMaxD * 4 + 4 * kWG * kM * 4 + 16;
 }
-static_assert(tc_smem_bytes<16>() <= 232448 && tc_smem_bytes<32>() <= 232448, "smem budget");
+static_assert(tc_smem_bytes<16, false>() <= 232448 && tc_smem_bytes<32, false>() <= 232448 &&
+                  tc_smem_bytes<16, true>() <= 232448 && tc_smem_bytes<32, true>() <= 232448,
+              "smem budget");
 
 template <int KT, bool W>
 cudaError_t tc_attr() {
@@ -1723,7 +1730,7 @@ cudaError_t tc_attr() {
     if (done) return cudaSuccess;
     const cudaError_t e = cudaFuncSetAttribute(scan_tc_kernel<KT, W>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)tc_smem_bytes<KT>());
+                                               (int)tc_smem_bytes<KT, W>());
     done = e == cudaSuccess;
     return e;
 }
@@ -1880,7 +1887,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     p.ccount = T.ccount;
     p.clb = T.clb;
     p.cloc = T.cloc;
-    const size_t sm16 = tc_smem_bytes<16>(), sm32 = tc_smem_bytes<32>();
+    const size_t sm16 = wide ? tc_smem_bytes<16, true>() : tc_smem_bytes<16, false>();
+    const size_t sm32 = wide ? tc_smem_bytes<32, true>() : tc_smem_bytes<32, false>();
     e = wide ? (sh.k <= 16 ? tc_attr<16, true>() : tc_attr<32, true>())
              : (sh.k <= 16 ? tc_attr<16, false>() : tc_attr<32, false>());
     if (e != cudaSuccess) return e;

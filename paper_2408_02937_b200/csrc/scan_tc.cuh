@@ -11,8 +11,8 @@
 namespace bivf {
 
 // candidate slots per run (query, list chunk, warpgroup): 40 for k <= 16, 56 for
-// k <= 32; global buffers use the larger stride
-constexpr uint32_t kKC = 56;
+// k <= 32 (inner-product wide mode: 64, 72); global buffers use the largest stride
+constexpr uint32_t kKC = 72;
 constexpr uint32_t kOverflow = 0xffffffffu;  // ccount marker: buffer overflowed -> exact rescan
 
 // per-search scratch of the TC path (lease workspace)
