@@ -1430,12 +1430,15 @@ __global__ void dense_select_kernel(const float* dense, uint32_t ld, const float
     // phase A (+ the fast selection when <= 32R values tie the bounds): the k-th
     // smallest of each lane's R smallest upper bounds bounds the k-th smallest
     float pre = inf;
-    uint32_t* fscr = reinterpret_cast<uint32_t*>(qsm + nw * Dp) + nw * 32 + wq * 384;
-    if (k <= 64 && n >= 64) {
+    uint32_t* fscr = reinterpret_cast<uint32_t*>(qsm + nw * Dp) + nw * 32 + wq * 768;
+    if (k <= 32 && n >= 64) {
         if (dense_select_fast<2>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
             return;
-    } else if (k <= 128 && n >= 128) {
+    } else if (k <= 64 && n >= 128) {
         if (dense_select_fast<4>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
+            return;
+    } else if (k <= 128 && n >= 256) {
+        if (dense_select_fast<8>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
             return;
     }
     WarpTopK<KPL> th;
@@ -1933,7 +1936,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                 p, probes, out_d, out_i, out_cnt, sh.nq);
     } else if (dense) {
         const uint32_t n = dense->n;
-        const size_t sm_sel = wpb * (p.Dp * 4 + 128 + 384 * 4);
+        const size_t sm_sel = wpb * (p.Dp * 4 + 128 + 768 * 4);
         if (sh.k <= 32)
             dense_select_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
                 dense->out, dense->ld, dense->nq, off_nrm, off_rows, queries, p.Dp, p.D, n, sh.nq,
