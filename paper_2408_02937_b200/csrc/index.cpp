@@ -483,7 +483,8 @@ void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32
             qs.QT = 128;
             qs.metric = cfg_.metric;
             TcDense dn{w.qdense, w.qdense_nq, ld, C_};
-            const bool ip = cfg_.metric == BIVF_METRIC_IP;  // filter + exact refine (no dense rows)
+            // inner product: filter + exact refine (L2 filter mode measured 0.39 vs 0.18 ms dense)
+            const bool ip = cfg_.metric == BIVF_METRIC_IP;
             const size_t g0 = (size_t)qbase + q0;
             // work items = tiles x chunks (the centroid list has no online part)
             const uint32_t ngq = ceil_div(C_, 32);
