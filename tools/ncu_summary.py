@@ -60,7 +60,7 @@ def rep_summary(rep, out):
     summ = {"source": rep, "kernels": kernels}
     # the list scan of one search = every scan_tc_kernel<16> launch captured (the two
     # phases of the two-phase scan; the coarse quantizer is the <32> instantiation)
-    tc = [k for k in kernels if "scan_tc_kernel<16>" in k["kernel"]]
+    tc = [k for k in kernels if "scan_tc_kernel<16" in k["kernel"]]
     if tc:
         summ["dram_bytes_per_launch"] = int(sum(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0)
                                                 for k in tc))

@@ -25,8 +25,20 @@ def main():
     D = int(os.environ.get("PROF_D", 128))
     C = int(os.environ.get("PROF_NLIST", 1024))
     metric = int(os.environ.get("PROF_METRIC", 0))
-    x = bivf.synthetic_dataset(n_base + nq, D, 4096, 2)
-    np.maximum(np.rint(x, out=x), 0, out=x)
+    if metric == 1:
+        # inner product, cfg5's generator (tools/bench_configs.py): unit centres u_j,
+        # x = normalize(u_j + 0.5 N(0,1)/sqrt(D))
+        rng = np.random.default_rng(5)
+        u = rng.standard_normal((8192, D), dtype=np.float32)
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        x = np.empty((n_base + nq, D), np.float32)
+        for i in range(0, len(x), 100_000):
+            m = min(100_000, len(x) - i)
+            y = u[rng.integers(0, len(u), m)] + (0.5 / np.sqrt(D)) * rng.standard_normal((m, D), dtype=np.float32)
+            x[i:i + m] = y / np.linalg.norm(y, axis=1, keepdims=True)
+    else:  # SIFT-like: non-negative integers
+        x = bivf.synthetic_dataset(n_base + nq, D, 4096, 2)
+        np.maximum(np.rint(x, out=x), 0, out=x)
     base, q = x[:n_base], x[n_base:]
     cent, _, _ = bivf.kmeans(base[:100_000], C, 10 if D <= 128 else 4, 42)
     ix = bivf.ClusterIndex.empty(D, C, block_capacity=1024, num_blocks=4096, metric=metric)
