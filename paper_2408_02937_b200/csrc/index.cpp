@@ -467,7 +467,11 @@ DevLists GpuIndex::quantizer_lists() const {
 // w.queries -> w.probes (P lowest (key, cluster)) + w.pdist, on stream s.
 void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32_t fnch,
                                  Workspace& w, uint32_t qbase) {
-    if (use_tc_quantizer(P) && nq <= 65536) {
+    static const uint32_t tcq_min = [] {  // smallest batch for the TC quantizer (tuning knob)
+        const char* v = std::getenv("BIVF_TCQ_MIN");
+        return v ? (uint32_t)atoi(v) : 0u;
+    }();
+    if (use_tc_quantizer(P) && nq <= 65536 && nq >= tcq_min) {
         // dense mode: approximate distances of every (query, centroid) on the
         // tensor cores, then a per-query selection + exact recompute of the few
         // centroids whose lower bound can reach the P-th upper bound
@@ -850,9 +854,13 @@ void GpuIndex::enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Works
     if (use_tc(k)) {
         // TC filter: a chunk is cheap to scan but every (pair, chunk) run is merged by
         // the refine's one warp per query, so keep ~2 work items per SM, not 8
+        static const uint64_t ipsm = [] {  // work items per SM target (tuning knob)
+            const char* v = std::getenv("BIVF_TC_ITEMS_PER_SM");
+            return v ? std::max<uint64_t>(1, (uint64_t)atoi(v)) : 2ull;
+        }();
         const uint64_t npairs = (uint64_t)nq * P;
         ss.maxch = (uint32_t)std::min<uint64_t>(
-            ss.maxch, std::max<uint64_t>(1, (2ull * num_sms_ + npairs - 1) / npairs));
+            ss.maxch, std::max<uint64_t>(1, (ipsm * num_sms_ + npairs - 1) / npairs));
     }
     ss.gcmin = sh.gcmin;
     ss.QT = qt_for(k, D_);

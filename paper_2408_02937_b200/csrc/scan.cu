@@ -429,10 +429,10 @@ __global__ void plan_count(const long long* probes, uint32_t npairs, uint32_t P,
 }
 
 // single CTA of 1024 threads: exclusive scans over lists
-__global__ void __launch_bounds__(1024) plan_scan(uint32_t C, uint32_t QT, const uint32_t* cnt,
-                                                  const uint32_t* nch, uint32_t* qoff,
-                                                  uint32_t* item_off, uint32_t* n_items,
-                                                  uint32_t* item_ctr) {
+__device__ __forceinline__ void plan_scan_block(uint32_t C, uint32_t QT, const uint32_t* cnt,
+                                                const uint32_t* nch, uint32_t* qoff,
+                                                uint32_t* item_off, uint32_t* n_items,
+                                                uint32_t* item_ctr) {
     __shared__ uint32_t wq[32], wi[32];
     __shared__ uint32_t carry_q, carry_i;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -493,6 +493,47 @@ __global__ void __launch_bounds__(1024) plan_scan(uint32_t C, uint32_t QT, const
         item_off[C] = carry_i;
         *n_items = carry_i;
         *item_ctr = 0;
+    }
+}
+
+__global__ void __launch_bounds__(1024) plan_scan(uint32_t C, uint32_t QT, const uint32_t* cnt,
+                                                  const uint32_t* nch, uint32_t* qoff,
+                                                  uint32_t* item_off, uint32_t* n_items,
+                                                  uint32_t* item_ctr) {
+    plan_scan_block(C, QT, cnt, nch, qoff, item_off, n_items, item_ctr);
+}
+
+// The whole plan (snapshot, count, scan, scatter) in ONE 1024-thread CTA for
+// small batches: the four-launch chain costs more than the work there.
+__global__ void __launch_bounds__(1024) plan_fused(DevLists L, uint32_t maxch, uint32_t gcmin,
+                                                   const long long* probes, uint32_t npairs,
+                                                   uint32_t P, uint32_t lo, uint32_t hi,
+                                                   int snapshot, uint32_t QT, PlanBufs B) {
+    const uint32_t t = threadIdx.x;
+    for (uint32_t c = t; c < L.C; c += 1024) {
+        if (snapshot) {
+            const uint32_t off = L.off_count[c];
+            const uint32_t len = ld_acquire_u32(L.len + c);
+            B.snap_off[c] = off;
+            B.snap_len[c] = len;
+            const uint32_t ng = ivf_ngroups(L, off, len);
+            const uint32_t g = max(gcmin, (ng + maxch - 1) / maxch);
+            B.gc[c] = g;
+            B.nch[c] = (ng + g - 1) / g;
+        }
+        B.cnt[c] = 0;
+    }
+    __syncthreads();
+    for (uint32_t i = t; i < npairs; i += 1024) {
+        const uint32_t r = i % P;
+        if (r >= lo && r < hi) B.ppos[i] = atomicAdd(&B.cnt[(uint32_t)probes[i]], 1u);
+    }
+    __syncthreads();
+    plan_scan_block(L.C, QT, B.cnt, B.nch, B.qoff, B.item_off, B.n_items, B.item_ctr);
+    __syncthreads();
+    for (uint32_t i = t; i < npairs; i += 1024) {
+        const uint32_t r = i % P;
+        if (r >= lo && r < hi) B.plist[B.qoff[(uint32_t)probes[i]] + B.ppos[i]] = i;
     }
 }
 
@@ -682,6 +723,12 @@ cudaError_t launch_plan_ranked(const DevLists& L, const PlanBufs& B, const long 
                                const SearchShape& sh, uint32_t lo, uint32_t hi, bool snapshot,
                                cudaStream_t s) {
     const uint32_t npairs = sh.nq * sh.P;
+    if (npairs <= 8192 && L.C <= 8192) {  // small batch: one launch
+        plan_fused<<<1, 1024, 0, s>>>(L, sh.maxch, sh.gcmin, probes, npairs, sh.P, lo, hi,
+                                      snapshot ? 1 : 0, sh.QT, B);
+        count_launch(1);
+        return cudaGetLastError();
+    }
     if (snapshot) {
         plan_snapshot<<<(L.C + 255) / 256, 256, 0, s>>>(L, sh.maxch, sh.gcmin, B.snap_off,
                                                        B.snap_len, B.gc, B.nch, B.cnt);
