@@ -227,3 +227,26 @@ def test_tc_inner_product_quantizer_matches_exact(gpu_ready, C, D):
         ix.set_scan_mode("auto")
         b = ix.probes(q, P)
         assert np.array_equal(a, b), (C, D, P)
+
+
+def test_tc_inner_product_at_scale(gpu_ready):
+    """Wide mode at a cfg5-like shape (D = 768 embeddings, cfg5's generator,
+    seeded batches, live inserts): ids and key bits equal the CUDA-core scan's."""
+    rng = np.random.default_rng(5)
+    D, C, n = 768, 256, 120_000
+    u = rng.standard_normal((2048, D), dtype=np.float32)
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+
+    def gen(m):
+        y = u[rng.integers(0, len(u), m)] + (0.5 / np.sqrt(D)) * rng.standard_normal((m, D), dtype=np.float32)
+        return np.ascontiguousarray(y / np.linalg.norm(y, axis=1, keepdims=True), np.float32)
+    base = gen(n)
+    cent, _, _ = bivf.kmeans(base[:30_000], C, 4, 5)
+    ix = ClusterIndex.empty(D, C, block_capacity=1024, num_blocks=3 * C, metric=bivf.METRIC_IP)
+    ix.set_centroids(cent)
+    ix.bulk_load(base, ix.assign_batch(base))
+    ix.insert(gen(20_000))
+    q = gen(2000)
+    for k, npb in ((10, 32), (32, 16)):
+        a, b = both(ix, q, k, npb)
+        assert_same(a, b)
