@@ -218,6 +218,7 @@ GpuIndex::~GpuIndex() {
     cudaSetDevice(device_);
     cudaDeviceSynchronize();
     for (auto& l : leases_) {
+        for (auto& g : l->graphs) cudaGraphExecDestroy(g.exec);
         if (l->stream) cudaStreamDestroy(l->stream);
         for (cudaEvent_t e : {l->done, l->t0, l->t1, l->t2, l->t3, l->t4})
             if (e) cudaEventDestroy(e);
@@ -835,6 +836,70 @@ void GpuIndex::enqueue_probes(Lease& l, const float* q_dev_raw_piece, uint32_t q
     }
 }
 
+// Small-batch searches (the latency path: executor requests of <= 10 queries,
+// up to 256) are launch-bound: ~10 dependent kernels and memsets of a few us each.
+// Their device work is captured once per (shape, workspace, device-buffer
+// signature) into a CUDA graph on the lease and replayed with one launch.  Every
+// kernel argument is a function of that key: buffer pointers (the signature),
+// the batch shape, and device-side state read at run time (list lengths, the
+// plan).  Not for timed runs (event records) or the k > 32 dense path (it reads
+// a size back to the host mid-search).
+uint64_t GpuIndex::graph_sig() const {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+    for (const DevBuf* b : {&d_off_pay_, &d_off_ids_, &d_off_mir_, &d_off_nrm_, &d_off_rows_, &d_q_mir_,
+                            &d_q_nrm_, &d_q_mu_, &d_q_ids_, &d_q_meta_, &d_q_zero_, &d_cent_, &d_cent_il_,
+                            &d_arena_, &d_arena_mir_})
+        mix(reinterpret_cast<uintptr_t>(b->p));
+    mix((uint64_t)scan_mode_);
+    mix((uint64_t)tc_ok_ | (uint64_t)q_tc_ok_ << 1 | (uint64_t)mir_on_ << 2);
+    return h;
+}
+
+bool GpuIndex::graph_search(Lease& l, uint32_t m, uint32_t k, uint32_t P, Workspace& w) {
+    static const bool env_on = [] {
+        const char* v = std::getenv("BIVF_GRAPHS");
+        return !(v && std::string(v) == "0");
+    }();
+    if (!env_on || !graphs_on_.load() || m > 256 || timing_ || use_tc_dense(k)) return false;
+    const uint64_t sig = graph_sig();
+    for (auto& g : l.graphs)
+        if (g.m == m && g.k == k && g.P == P && g.ws == l.ws.p && g.sig == sig) {
+            BIVF_CUDA(cudaGraphLaunch(g.exec, l.stream));
+            count_launch(g.launches);
+            return true;
+        }
+    const uint64_t t0 = t_launches;
+    if (cudaStreamBeginCapture(l.stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        graphs_on_ = false;
+        return false;
+    }
+    bool threw = false;
+    try {
+        enqueue_search(l, w.qraw, m, k, P, w);
+    } catch (...) {
+        threw = true;
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t ee = cudaStreamEndCapture(l.stream, &g);
+    cudaGraphExec_t ge = nullptr;
+    if (threw || ee != cudaSuccess || !g || cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        graphs_on_ = false;  // fall back to direct launches from now on
+        return false;
+    }
+    cudaGraphDestroy(g);
+    if (l.graphs.size() >= 8) {
+        cudaGraphExecDestroy(l.graphs.front().exec);
+        l.graphs.erase(l.graphs.begin());
+    }
+    l.graphs.push_back({m, k, P, l.ws.p, sig, ge, t_launches - t0});
+    BIVF_CUDA(cudaGraphLaunch(ge, l.stream));  // its launches were counted while recording
+    return true;
+}
+
 void GpuIndex::enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uint32_t k,
                               uint32_t P, Workspace& w) {
     if (timing_) BIVF_CUDA(cudaEventRecord(l.t0, l.stream));
@@ -980,7 +1045,8 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
                                               cudaMemcpyHostToDevice, l->stream));
                 }
             }
-            enqueue_search(*l, w.qraw, m, (uint32_t)k, (uint32_t)nprobe, w);
+            if (!graph_search(*l, m, (uint32_t)k, (uint32_t)nprobe, w))
+                enqueue_search(*l, w.qraw, m, (uint32_t)k, (uint32_t)nprobe, w);
             float* hd = o_pin ? out_d + s * k : pd;
             long long* hi = o_pin ? reinterpret_cast<long long*>(out_ids + s * k) : pi;
             uint32_t* hc = o_pin && out_cnt ? out_cnt + s : pc;

@@ -91,6 +91,16 @@ struct Lease {
     PinBuf dpin;
     uint64_t seen_maint = 0;
     bool busy = false;
+    // small-batch searches replayed as CUDA graphs (GpuIndex::search): one entry
+    // per (batch shape, workspace, index device-buffer signature)
+    struct Graph {
+        uint32_t m, k, P;
+        void* ws;
+        uint64_t sig;
+        cudaGraphExec_t exec;
+        uint64_t launches;
+    };
+    std::vector<Graph> graphs;
 };
 
 struct Workspace {  // carved from Lease::ws
@@ -199,6 +209,10 @@ private:
     void enqueue_probes(Lease& l, const float* q_dev_raw_piece, uint32_t q0, uint32_t m,
                         uint32_t P, uint32_t fnch, Workspace& w);
     void enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Workspace& w);
+    // the search's device work for a small batch as a cached CUDA graph
+    // (returns false when the shape is not graph-eligible: caller enqueues)
+    bool graph_search(Lease& l, uint32_t m, uint32_t k, uint32_t P, Workspace& w);
+    uint64_t graph_sig() const;
     void enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uint32_t k,
                         uint32_t P, Workspace& w);
     void begin_maintenance();   // caller holds data_mu_; takes gate_ exclusively
@@ -279,6 +293,7 @@ private:
     CUtensorMap map_off_{}, map_arena_{};
     bool tc_ok_ = false;
     int scan_mode_ = 0;  // 0 auto, 1 CUDA-core only, 2 tensor-core when supported
+    std::atomic<bool> graphs_on_{true};  // BIVF_GRAPHS=0 disables; a failed capture too
     bool timing_ = false;
     float last_ms_[4] = {-1, -1, -1, -1};
 };

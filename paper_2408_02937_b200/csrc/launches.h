@@ -6,5 +6,10 @@
 
 namespace bivf {
 extern std::atomic<uint64_t> g_launches;
-inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// per-thread count too: a CUDA-graph capture measures the launches it records
+inline thread_local uint64_t t_launches = 0;
+inline void count_launch(uint64_t n = 1) {
+    g_launches.fetch_add(n, std::memory_order_relaxed);
+    t_launches += n;
+}
 }  // namespace bivf

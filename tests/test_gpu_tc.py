@@ -250,3 +250,23 @@ def test_tc_inner_product_at_scale(gpu_ready):
     for k, npb in ((10, 32), (32, 16)):
         a, b = both(ix, q, k, npb)
         assert_same(a, b)
+
+
+def test_graph_replay_sees_new_data(gpu_ready):
+    """Small batches replay a captured CUDA graph: a replay after inserts and
+    deletes must see them (device state is read at run time)."""
+    D, C = 64, 32
+    base = bivf.synthetic_dataset(20000, D, 64, 31)
+    cent, asg, _ = bivf.kmeans(base, C, 5, 31)
+    ix = ClusterIndex.empty(D, C, block_capacity=256, num_blocks=1024)
+    ix.set_centroids(cent)
+    ix.bulk_load(base, asg)
+    q = bivf.synthetic_dataset(10, D, 64, 32)
+    for _ in range(3):  # capture, then replays
+        r1 = ix.search_batch(q, 5, 8)
+    new = ix.insert(q.copy())  # exact copies of the queries: their nearest neighbours now
+    r2 = ix.search_batch(q, 5, 8)
+    assert np.array_equal(r2[0][:, 0], new) and np.all(r2[1][:, 0] == 0.0)
+    ix.remove(new)
+    r3 = ix.search_batch(q, 5, 8)
+    assert np.array_equal(r3[0], r1[0]) and np.array_equal(bits(r3[1]), bits(r1[1]))
