@@ -132,6 +132,13 @@ bivf_status bivf_probes(bivf_index* h, const float* queries, uint64_t nq, uint64
 /* Delete (extension; the reference has none; rules in DESIGN.md
  * §Delete): in request order, fill each hole with the last vector of its part
  * (offline segment or online list).  found may be NULL. */
+/* The copy-based baseline backend (blockivf::BaselineIndex::insert,
+ * baseline_index.cpp:51-103) on device: each affected list is re-allocated at
+ * old + new, the old contents copied, the new vectors appended.  Searched by
+ * bivf_search like any index.  Counters: bivf_scalars_copied, bivf_reallocations. */
+bivf_status bivf_extend_copy(bivf_index* h, const float* x, uint64_t n, const int64_t* ids,
+                             int64_t* out_ids, uint64_t* inserted);
+bivf_status bivf_reallocations(const bivf_index* h, uint64_t* out);
 bivf_status bivf_remove(bivf_index* h, const int64_t* ids, uint64_t n, uint64_t* removed,
                         uint8_t* found);
 

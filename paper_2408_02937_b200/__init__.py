@@ -6,10 +6,11 @@ mirror of the reference's binding surface (blockivf._core) over that ABI.
 """
 from ._lib import (BivfError, BusyError, CorruptListError, CudaError, METRIC_IP, METRIC_L2,
                    PoolExhaustedError)
-from .index import ClusterIndex, device_count, kernel_launches, kmeans, pinned_empty, synthetic_dataset
+from .index import BaselineIndex, ClusterIndex, device_count, kernel_launches, kmeans, pinned_empty, synthetic_dataset
 
 __all__ = [
     "ClusterIndex",
+    "BaselineIndex",
     "pinned_empty",
     "PoolExhaustedError",
     "CorruptListError",

@@ -189,6 +189,19 @@ bivf_status bivf_add(bivf_index* h, const float* x, uint64_t n, const int64_t* i
     }
 }
 
+bivf_status bivf_extend_copy(bivf_index* h, const float* x, uint64_t n, const int64_t* ids,
+                             int64_t* out_ids, uint64_t* inserted) {
+    if (inserted) *inserted = 0;
+    return guard([&] {
+        if (n) {
+            need(x, "x");
+            need(out_ids, "out_ids");
+        }
+        const uint64_t r = I(h).extend_copy(x, n, ids, out_ids);
+        if (inserted) *inserted = r;
+    });
+}
+
 bivf_status bivf_search(bivf_index* h, const float* q, uint64_t nq, uint64_t k, uint64_t nprobe,
                         int64_t* out_ids, float* out_d, uint32_t* out_cnt) {
     return guard([&] {
@@ -286,6 +299,7 @@ bivf_status bivf_take_rearrange_events(bivf_index* h, double* out5, uint64_t cap
     }
 BIVF_GETTER(bivf_size, I(h).size())
 BIVF_GETTER(bivf_scalars_copied, I(h).scalars_copied())
+BIVF_GETTER(bivf_reallocations, I(h).reallocations())
 BIVF_GETTER(bivf_allocated_blocks, I(h).allocated_blocks())
 #undef BIVF_GETTER
 

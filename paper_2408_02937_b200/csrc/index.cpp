@@ -666,6 +666,123 @@ void GpuIndex::bulk_load(const float* x, uint64_t n, const uint32_t* assignment,
 }
 
 // ========================================================================
+// copy-based baseline backend (baseline_index.cpp:51-103)
+// ========================================================================
+
+// Grow the offline-segment area to `slots`, keeping every byte (the block-based
+// path never needs this: its area is sized once by bulk_load).
+void GpuIndex::grow_offline_preserving(uint64_t slots) {
+    slots = (slots + 31) / 32 * 32;
+    if (slots <= off_slots_cap_) return;
+    const uint64_t cap = std::max<uint64_t>(slots, off_slots_cap_ * 2);
+    BIVF_CUDA(cudaDeviceSynchronize());  // in-flight searches read the old buffers
+    auto regrow = [&](DevBuf& b, size_t new_bytes, int fill) {
+        DevBuf nb;
+        nb.alloc(new_bytes);
+        BIVF_CUDA(dset(nb.p, fill, nb.bytes));
+        if (b.p && b.bytes) BIVF_CUDA(cudaMemcpy(nb.p, b.p, std::min(b.bytes, new_bytes), cudaMemcpyDeviceToDevice));
+        std::swap(b.p, nb.p);
+        std::swap(b.bytes, nb.bytes);
+    };
+    regrow(d_off_pay_, (size_t)cap * D_ * 4, 0);
+    regrow(d_off_ids_, (size_t)cap * 8, 0xff);
+    if (mir_on_) {
+        regrow(d_off_mir_, (size_t)(cap / 32) * GF_ * 4, 0);
+        regrow(d_off_nrm_, (size_t)(cap / 32) * kNormFloats * 4, 0);
+        if (d_off_rows_.p) regrow(d_off_rows_, (size_t)cap * D_ * 4, 0);
+        if (make_mirror_map(d_off_mir_.as<float>(), cap / 32, D_, cfg_.metric == BIVF_METRIC_IP, &map_off_) !=
+            cudaSuccess)
+            tc_ok_ = false;
+    }
+    off_slots_cap_ = cap;
+    mirror_ = mirror_view();
+}
+
+uint64_t GpuIndex::extend_copy(const float* x, uint64_t n, const int64_t* ids, int64_t* out_ids) {
+    if (n == 0) return 0;
+    if (!trained_) throw Error(BIVF_ELOGIC, "insert: index has no centroids");
+    std::vector<uint32_t> asg(n);
+    assign(x, n, asg.data());  // ivf assign, lowest cluster id on ties (ivf_index.cpp:93-105)
+    // the baseline's extend excludes searches (baseline_index.cpp:66, :113 share one mutex)
+    std::unique_lock<std::shared_mutex> gx(gate_);
+    std::lock_guard<std::mutex> lk(data_mu_);
+    BIVF_CUDA(cudaSetDevice(device_));
+    // bucket the batch per cluster, batch order inside a bucket
+    std::vector<std::vector<uint64_t>> buckets(C_);
+    for (uint64_t i = 0; i < n; ++i) buckets[asg[i]].push_back(i);
+    int64_t base = -1;
+    if (!ids) {
+        base = next_id_;
+        next_id_ += (int64_t)n;
+    }
+    uint64_t top = 0;
+    for (uint32_t c = 0; c < C_; ++c) top = std::max<uint64_t>(top, h_off_start_[c] + (h_off_count_[c] + 31ull) / 32 * 32);
+    uint64_t need = top;
+    for (uint32_t c = 0; c < C_; ++c)
+        if (!buckets[c].empty()) need += (h_off_count_[c] + buckets[c].size() + 31ull) / 32 * 32;
+    grow_offline_preserving(need);
+    // the batch on device once; per list: copy old groups to a fresh region, append
+    DevBuf dx, ddest, dids, dasg;
+    dx.alloc(n * D_ * 4);
+    BIVF_CUDA(h2d(dx.p, x, n * D_ * 4));
+    std::vector<uint64_t> dest(n);
+    std::vector<long long> idv(n);
+    const uint64_t gfl = mir_on_ ? GF_ : 0;
+    for (uint32_t c = 0; c < C_; ++c) {
+        if (buckets[c].empty()) continue;
+        const uint64_t old_n = h_off_count_[c], add_n = buckets[c].size();
+        const uint64_t from = h_off_start_[c], to = top;
+        top += (old_n + add_n + 31) / 32 * 32;
+        const uint64_t og = (old_n + 31) / 32;  // whole groups of the old list
+        if (og) {
+            cudaStream_t st = data_stream_;
+            BIVF_CUDA(cudaMemcpyAsync(d_off_pay_.as<float>() + to * D_, d_off_pay_.as<float>() + from * D_,
+                                      og * 32 * D_ * 4, cudaMemcpyDeviceToDevice, st));
+            BIVF_CUDA(cudaMemcpyAsync(d_off_ids_.as<long long>() + to, d_off_ids_.as<long long>() + from,
+                                      og * 32 * 8, cudaMemcpyDeviceToDevice, st));
+            if (mir_on_) {
+                BIVF_CUDA(cudaMemcpyAsync(d_off_mir_.as<float>() + (to / 32) * gfl,
+                                          d_off_mir_.as<float>() + (from / 32) * gfl, og * gfl * 4,
+                                          cudaMemcpyDeviceToDevice, st));
+                BIVF_CUDA(cudaMemcpyAsync(d_off_nrm_.as<float>() + (to / 32) * kNormFloats,
+                                          d_off_nrm_.as<float>() + (from / 32) * kNormFloats,
+                                          og * kNormFloats * 4, cudaMemcpyDeviceToDevice, st));
+                if (d_off_rows_.p)
+                    BIVF_CUDA(cudaMemcpyAsync(d_off_rows_.as<float>() + to * D_,
+                                              d_off_rows_.as<float>() + from * D_, og * 32 * D_ * 4,
+                                              cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        for (uint64_t j = 0; j < add_n; ++j) {
+            const uint64_t i = buckets[c][j];
+            dest[i] = to + old_n + j;
+            idv[i] = ids ? (long long)ids[i] : (long long)(base + (int64_t)i);
+            if (out_ids) out_ids[i] = idv[i];
+        }
+        reallocations_ += 1;
+        scalars_copied_ += (old_n + add_n) * D_;
+        h_off_start_[c] = to;
+        h_off_count_[c] = (uint32_t)(old_n + add_n);
+    }
+    ddest.alloc(n * 8);
+    dids.alloc(n * 8);
+    BIVF_CUDA(h2d(ddest.p, dest.data(), n * 8));
+    BIVF_CUDA(h2d(dids.p, idv.data(), n * 8));
+    BIVF_CUDA(launch_scatter_rows(dx.as<float>(), (uint32_t)n, D_, ddest.as<uint64_t>(), dids.as<long long>(),
+                                  d_off_pay_.as<float>(), d_off_ids_.as<long long>(), data_stream_));
+    if (mir_on_) {
+        dasg.alloc(n * 4);
+        BIVF_CUDA(h2d(dasg.p, asg.data(), n * 4));
+        BIVF_CUDA(launch_mirror_offline(mirror_, (uint32_t)n, dx.as<float>(), ddest.as<uint64_t>(),
+                                        dasg.as<uint32_t>(), data_stream_));
+    }
+    BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+    BIVF_CUDA(h2d(d_off_start_.p, h_off_start_.data(), (size_t)C_ * 8));
+    BIVF_CUDA(h2d(d_off_count_.p, h_off_count_.data(), (size_t)C_ * 4));
+    return n;  // supplied ids do not move next_id (baseline_index.cpp:68-69)
+}
+
+// ========================================================================
 // leases
 // ========================================================================
 

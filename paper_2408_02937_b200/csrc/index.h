@@ -158,6 +158,12 @@ public:
 
     uint64_t size() const;
     uint64_t scalars_copied() const { return scalars_copied_; }
+    uint64_t reallocations() const { return reallocations_; }
+    // The copy-based baseline backend (baseline_index.cpp:51-103, the paper's
+    // Faiss/RAFT-style extend) on device: every affected list is re-allocated at
+    // old + new, its old contents copied, the new vectors appended, the old space
+    // dropped.  Lists live in the offline-segment area (searched as usual).
+    uint64_t extend_copy(const float* x, uint64_t n, const int64_t* ids, int64_t* out_ids);
     uint64_t list_length(uint32_t c) const;
     uint64_t offline_count(uint32_t c) const;
     uint64_t hop_count(uint32_t c) const;
@@ -276,7 +282,8 @@ private:
     int64_t next_id_ = 0, offline_end_ = 0;
     std::vector<std::pair<int64_t, int64_t>> auto_ranges_;
     std::unordered_set<int64_t> supplied_;
-    uint64_t scalars_copied_ = 0;
+    uint64_t scalars_copied_ = 0, reallocations_ = 0;
+    void grow_offline_preserving(uint64_t slots);  // copy-based extend: keep contents
 
     std::vector<RearrangeEvent> events_;
     std::mutex events_mu_;

@@ -1300,10 +1300,11 @@ __device__ __forceinline__ uint64_t warp_elem(const uint64_t (&v)[R], uint32_t e
         if (e >> 5 == (uint32_t)j) x = v[j];
     return __shfl_sync(0xffffffffu, x, e & 31);
 }
-// Fast selection of dense_select_kernel (R keys per lane, k <= 32R <= n): true when
+// Fast selection of dense_select_kernel (R pre-threshold keys per lane, lists of
+// 32 RL slots; k <= 32R <= n): true when
 // the exact top-k was written (false: more than 32R values tie the bounds, the
 // caller's general path runs with *pre as its pre-threshold).
-template <int R, typename UbOf>
+template <int R, int RL, typename UbOf>
 __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* nrm, float nqv,
                                   const float* qs, const float* rows, uint32_t D, uint32_t n,
                                   uint32_t k, uint32_t q, uint32_t lane, uint32_t* scratch,
@@ -1331,11 +1332,12 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
     warp_bitonic<R>(v, lane);
     const uint32_t kk = k - 1;
     *pre = ord2f((uint32_t)(warp_elem<R>(v, kk) >> 32));
+    uint64_t u[RL];  // the compacted lists (32 RL slots)
     // Fast path (no serialised warp inserts): every upper bound <= pre (>= k of
-    // them, <= 32R expected) compacted and bitonic-sorted -> theta = the k-th;
-    // every lower bound <= theta (<= 32R) recomputed exactly and sorted by the
+    // them, <= 32RL expected) compacted and bitonic-sorted -> theta = the k-th;
+    // every lower bound <= theta (<= 32RL) recomputed exactly and sorted by the
     // (dist, id) key.  Longer lists fall through to the general path.
-    uint32_t* l1 = scratch;  // [32R] key hi, [32R] c, [32R] cand
+    uint32_t* l1 = scratch;  // [32RL] key hi, [32RL] c, [32RL] cand
     const uint32_t lt = (1u << lane) - 1u;
     uint32_t n1 = 0;
     bool ok = true;
@@ -1344,13 +1346,13 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
         const float h = c < n ? ub_of(c) : inf;
         const bool pass = c < n && h <= *pre;
         const unsigned msk = __ballot_sync(0xffffffffu, pass);
-        if (n1 + __popc(msk) > 32u * R) {
+        if (n1 + __popc(msk) > 32u * RL) {
             ok = false;
         } else {
             if (pass) {
                 const uint32_t pos = n1 + __popc(msk & lt);
                 l1[pos] = f2ord(h);
-                l1[32 * R + pos] = c;
+                l1[32 * RL + pos] = c;
             }
             n1 += __popc(msk);
         }
@@ -1358,13 +1360,13 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
     __syncwarp();
     if (ok && n1 >= k) {
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
+        for (int j = 0; j < RL; ++j) {
             const uint32_t e = 32 * j + lane;
-            v[j] = e < n1 ? ((uint64_t)l1[e] << 32 | l1[32 * R + e]) : ~0ull;
+            u[j] = e < n1 ? ((uint64_t)l1[e] << 32 | l1[32 * RL + e]) : ~0ull;
         }
-        warp_bitonic<R>(v, lane);
-        const float theta = ord2f((uint32_t)(warp_elem<R>(v, kk) >> 32));
-        uint32_t* cq = l1 + 64 * R;
+        warp_bitonic<RL>(u, lane);
+        const float theta = ord2f((uint32_t)(warp_elem<RL>(u, kk) >> 32));
+        uint32_t* cq = l1 + 64 * RL;
         uint32_t n2 = 0;
         for (uint32_t c0 = 0; c0 < n && ok; c0 += 32) {
             const uint32_t c = c0 + lane;
@@ -1375,7 +1377,7 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
                 cand = a - fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, nqv + ns, 1e-30f)) <= theta;
             }
             const unsigned msk = __ballot_sync(0xffffffffu, cand);
-            if (n2 + __popc(msk) > 32u * R) {
+            if (n2 + __popc(msk) > 32u * RL) {
                 ok = false;
             } else {
                 if (cand) cq[n2 + __popc(msk & lt)] = c;
@@ -1385,21 +1387,21 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
         __syncwarp();
         if (ok) {
 #pragma unroll
-            for (int j = 0; j < R; ++j) {
+            for (int j = 0; j < RL; ++j) {
                 const uint32_t e = 32 * j + lane;
-                v[j] = ~0ull;
+                u[j] = ~0ull;
                 if (e < n2) {
                     const uint32_t c = cq[e];
-                    v[j] = (uint64_t)f2ord(exact_l2_row(qs, rows + (uint64_t)c * D, D)) << 32 | c;
+                    u[j] = (uint64_t)f2ord(exact_l2_row(qs, rows + (uint64_t)c * D, D)) << 32 | c;
                 }
             }
-            warp_bitonic<R>(v, lane);
+            warp_bitonic<RL>(u, lane);
 #pragma unroll
-            for (int j = 0; j < R; ++j) {
+            for (int j = 0; j < RL; ++j) {
                 const uint32_t e = 32 * j + lane;
                 if (e < k) {
-                    out_d[(uint64_t)q * k + e] = ord2f((uint32_t)(v[j] >> 32));
-                    out_i[(uint64_t)q * k + e] = (long long)(uint32_t)v[j];
+                    out_d[(uint64_t)q * k + e] = ord2f((uint32_t)(u[j] >> 32));
+                    out_i[(uint64_t)q * k + e] = (long long)(uint32_t)u[j];
                 }
             }
             return true;
@@ -1438,13 +1440,13 @@ __global__ void dense_select_kernel(const float* dense, uint32_t ld, const float
     float pre = inf;
     uint32_t* fscr = reinterpret_cast<uint32_t*>(qsm + nw * Dp) + nw * 32 + wq * 768;
     if (k <= 32 && n >= 64) {
-        if (dense_select_fast<2>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
+        if (dense_select_fast<2, 2>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
             return;
     } else if (k <= 64 && n >= 128) {
-        if (dense_select_fast<4>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
+        if (dense_select_fast<4, 8>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
             return;
     } else if (k <= 128 && n >= 256) {
-        if (dense_select_fast<8>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
+        if (dense_select_fast<8, 8>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
             return;
     }
     WarpTopK<KPL> th;

@@ -354,6 +354,40 @@ class ClusterIndex:
         return list(out)
 
 
+class BaselineIndex(ClusterIndex):
+    """blockivf.BaselineIndex (bindings.cpp:132-164) on the B200: the copy-based
+    extend of baseline_index.cpp:51-103 (every affected list re-allocated at
+    old + new, old contents copied, new vectors appended: the paper's Faiss/RAFT
+    comparison point) on device; trained, stored and searched like ClusterIndex.
+    Counters: scalars_copied ((old + new) * D per affected list), reallocations."""
+
+    def __init__(self, vectors, clusters=16, kmeans_iters=25, seed=42, *, metric=METRIC_L2,
+                 device=0):
+        super().__init__(vectors, clusters=clusters, block_capacity=64, rearrange_threshold=256,
+                         num_blocks=0, kmeans_iters=kmeans_iters, seed=seed, metric=metric,
+                         device=device)
+
+    def insert(self, vectors, ids=None):
+        """BaselineIndex::insert: auto ids next_id + i, or the supplied ids as given."""
+        x = _as_matrix(vectors)
+        if x.shape[1] != self.dim:
+            raise ValueError("insert: vectors extent does not match n * dim")
+        n = x.shape[0]
+        out = np.full(max(n, 1), -1, np.int64)
+        idarr = None
+        if ids is not None:
+            idarr = np.ascontiguousarray(ids, dtype=np.int64)
+            if idarr.size != n:
+                raise ValueError("insert: ids size does not match n")
+        ins = C.c_uint64(0)
+        check(lib().bivf_extend_copy(self._h, ptr(x), n, ptr(idarr), ptr(out), C.byref(ins)))
+        return out[:n]
+
+    @property
+    def reallocations(self):
+        return self._u64(lib().bivf_reallocations)
+
+
 def synthetic_dataset(n, dim, components=16, seed=42):
     """dataset.cpp:92-112 restated (bit-identical on this image)."""
     out = np.empty((n, dim), np.float32)
