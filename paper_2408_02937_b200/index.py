@@ -361,11 +361,11 @@ class BaselineIndex(ClusterIndex):
     comparison point) on device; trained, stored and searched like ClusterIndex.
     Counters: scalars_copied ((old + new) * D per affected list), reallocations."""
 
-    def __init__(self, vectors, clusters=16, kmeans_iters=25, seed=42, *, metric=METRIC_L2,
-                 device=0):
+    def __init__(self, vectors=None, clusters=16, kmeans_iters=25, seed=42, *, metric=METRIC_L2,
+                 device=0, _handle=None):
         super().__init__(vectors, clusters=clusters, block_capacity=64, rearrange_threshold=256,
                          num_blocks=0, kmeans_iters=kmeans_iters, seed=seed, metric=metric,
-                         device=device)
+                         device=device, _handle=_handle)
 
     def insert(self, vectors, ids=None):
         """BaselineIndex::insert: auto ids next_id + i, or the supplied ids as given."""
