@@ -487,7 +487,12 @@ void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32
             qs.gcmin = 2;
             qs.QT = 128;
             qs.metric = cfg_.metric;
-            TcDense dn{w.qdense, w.qdense_nq, ld, C_};
+            // per-(query, group) bound minima: the selection opens only the groups
+            // whose minimum can reach its thresholds
+            // (written only when selective: several groups per wanted probe, as the
+            // selection requires)
+            TcDense dn{w.qdense, w.qdense_nq, ld, C_, nullptr,
+                       ceil_div(C_, 32) >= 4 * P ? w.qgsum : nullptr};
             // inner product: filter + exact refine (L2 filter mode measured 0.39 vs 0.18 ms dense)
             const bool ip = cfg_.metric == BIVF_METRIC_IP;
             const size_t g0 = (size_t)qbase + q0;
@@ -851,6 +856,8 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     const size_t o_qdense = take(q_tc_ok_ ? (size_t)std::min<uint32_t>(nq, quantizer_slice()) *
                                                 ceil_div(C_, 32) * 32 * 4 : 16);
     const size_t o_qdnq = take((size_t)nq * 4);
+    const size_t o_qgsum = take(q_tc_ok_ ? (size_t)std::min<uint32_t>(nq, quantizer_slice()) *
+                                               ceil_div(C_, 32) * 8 : 16);
     const size_t o_ppos = take(npairs * 4);
     const size_t o_plist = take(npairs * 4);
     if (off > l.ws.bytes && l.stream) {
@@ -889,6 +896,7 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     w.tc.qthr = reinterpret_cast<float*>(b + o_qthr);
     w.qdense = reinterpret_cast<float*>(b + o_qdense);
     w.qdense_nq = reinterpret_cast<float*>(b + o_qdnq);
+    w.qgsum = reinterpret_cast<float2*>(b + o_qgsum);
     w.plan.ppos = reinterpret_cast<uint32_t*>(b + o_ppos);
     w.plan.plist = reinterpret_cast<uint32_t*>(b + o_plist);
     return w;

@@ -120,6 +120,7 @@ struct Workspace {  // carved from Lease::ws
     TcBufs tc;
     float* qdense;         // TC quantizer: [qslice][ceil(C/32)*32] approximate distances
     float* qdense_nq;      // [nq] query norms
+    float2* qgsum;         // TC quantizer: [qslice][ceil(C/32)] per-group (min upper, min lower) bounds
 };
 
 struct RearrangeEvent {

@@ -526,9 +526,13 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                             ml = fminf(ml, av[n] - e);
                         }
                     }
-                    // summaries [tile][row m][group j]: the selection reads a row's groups contiguously
+                    // summaries [tile][row m][group j] (IVF) / [query][group j] (quantizer):
+                    // the selection reads a row's groups contiguously
                     const uint32_t ngl = ivf_ngroups(p.L, d.off, d.len);
-                    p.dense_gsum[(qrow - m) / 32u + (uint64_t)m * ngl + j] = make_float2(mh, ml);
+                    if (p.dense_list_base)
+                        p.dense_gsum[(qrow - m) / 32u + (uint64_t)m * ngl + j] = make_float2(mh, ml);
+                    else
+                        p.dense_gsum[(qrow / p.dense_ld) * ngl + j] = make_float2(mh, ml);
                 }
             }
         }
@@ -1308,16 +1312,24 @@ template <int R, int RL, typename UbOf>
 __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* nrm, float nqv,
                                   const float* qs, const float* rows, uint32_t D, uint32_t n,
                                   uint32_t k, uint32_t q, uint32_t lane, uint32_t* scratch,
-                                  float* out_d, long long* out_i, float* pre) {
+                                  float* out_d, long long* out_i, float* pre,
+                                  const float2* gs) {
     const float inf = __int_as_float(0x7f800000);
+    // gs: this query's per-group (min upper, min lower) bounds from the TC kernel
+    // (null: none).  With them phase A reads one value per group and passes 2 and
+    // 3 open only the groups whose minimum can reach the threshold.
+    const uint32_t ngq = (n + 31) / 32;
+    // the k-th smallest group minimum bounds the k-th upper bound only if k <= groups,
+    // and is selective only with several groups per wanted slot
+    if (gs && 4 * k > ngq) gs = nullptr;
     // phase A: an upper bound of the k-th smallest upper bound from each lane's
     // R smallest values (32R values sorted across the warp): the k-th smallest
     // of any k values is >= the true k-th smallest
     float m[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) m[j] = inf;
-    for (uint32_t c = lane; c < n; c += 32) {
-        float t = ub_of(c);
+    for (uint32_t c = lane; c < (gs ? ngq : n); c += 32) {
+        float t = gs ? gs[c].x : ub_of(c);  // a group minimum is a real upper bound of a distinct slot
 #pragma unroll
         for (int j = 0; j < R - 1; ++j) {
             const float a = fminf(m[j], t);
@@ -1341,8 +1353,18 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
     const uint32_t lt = (1u << lane) - 1u;
     uint32_t n1 = 0;
     bool ok = true;
-    for (uint32_t c0 = 0; c0 < n && ok; c0 += 32) {
-        const uint32_t c = c0 + lane;
+    // groups [g0, g0 + 32) at a time; `open` selects the ones to read slot by slot
+    auto sweep = [&](auto&& open, auto&& slot) {
+        for (uint32_t g0 = 0; g0 < ngq && ok; g0 += 32) {
+            unsigned gm = __ballot_sync(0xffffffffu, g0 + lane < ngq && (!gs || open(gs[g0 + lane])));
+            while (gm && ok) {
+                const uint32_t g = g0 + __ffs(gm) - 1;
+                gm &= gm - 1;
+                slot(32 * g + lane);
+            }
+        }
+    };
+    sweep([&](float2 m) { return m.x <= *pre; }, [&](uint32_t c) {
         const float h = c < n ? ub_of(c) : inf;
         const bool pass = c < n && h <= *pre;
         const unsigned msk = __ballot_sync(0xffffffffu, pass);
@@ -1356,7 +1378,7 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
             }
             n1 += __popc(msk);
         }
-    }
+    });
     __syncwarp();
     if (ok && n1 >= k) {
 #pragma unroll
@@ -1368,8 +1390,7 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
         const float theta = ord2f((uint32_t)(warp_elem<RL>(u, kk) >> 32));
         uint32_t* cq = l1 + 64 * RL;
         uint32_t n2 = 0;
-        for (uint32_t c0 = 0; c0 < n && ok; c0 += 32) {
-            const uint32_t c = c0 + lane;
+        sweep([&](float2 m) { return m.y <= theta; }, [&](uint32_t c) {
             bool cand = false;
             if (c < n) {
                 const float a = row[c];
@@ -1383,7 +1404,7 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
                 if (cand) cq[n2 + __popc(msk & lt)] = c;
                 n2 += __popc(msk);
             }
-        }
+        });
         __syncwarp();
         if (ok) {
 #pragma unroll
@@ -1419,7 +1440,7 @@ template <int KPL>
 __global__ void dense_select_kernel(const float* dense, uint32_t ld, const float* dnq,
                                     const float* nrm, const float* rows, const float* queries,
                                     uint32_t Dp, uint32_t D, uint32_t n, uint32_t nq, uint32_t k,
-                                    float* out_d, long long* out_i) {
+                                    float* out_d, long long* out_i, const float2* gsum) {
     extern __shared__ float qsm[];
     const uint32_t nw = blockDim.x >> 5, wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t q = blockIdx.x * nw + wq;
@@ -1439,14 +1460,15 @@ __global__ void dense_select_kernel(const float* dense, uint32_t ld, const float
     // smallest of each lane's R smallest upper bounds bounds the k-th smallest
     float pre = inf;
     uint32_t* fscr = reinterpret_cast<uint32_t*>(qsm + nw * Dp) + nw * 32 + wq * 768;
+    const float2* gs = gsum ? gsum + (uint64_t)q * ((n + 31) / 32) : nullptr;
     if (k <= 32 && n >= 64) {
-        if (dense_select_fast<2, 2>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
+        if (dense_select_fast<2, 2>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre, gs))
             return;
     } else if (k <= 64 && n >= 128) {
-        if (dense_select_fast<4, 8>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
+        if (dense_select_fast<4, 8>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre, gs))
             return;
     } else if (k <= 128 && n >= 256) {
-        if (dense_select_fast<8, 8>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre))
+        if (dense_select_fast<8, 8>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre, gs))
             return;
     }
     WarpTopK<KPL> th;
@@ -1948,11 +1970,11 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
         if (sh.k <= 32)
             dense_select_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
                 dense->out, dense->ld, dense->nq, off_nrm, off_rows, queries, p.Dp, p.D, n, sh.nq,
-                sh.k, out_d, out_i);
+                sh.k, out_d, out_i, dense->gsum);
         else
             dense_select_kernel<8><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
                 dense->out, dense->ld, dense->nq, off_nrm, off_rows, queries, p.Dp, p.D, n, sh.nq,
-                sh.k, out_d, out_i);
+                sh.k, out_d, out_i, dense->gsum);
     } else {
         if (wide)
             refine_kernel<1, kIP><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
