@@ -55,18 +55,25 @@ constexpr int kGU = 2;                     // groups per unit (MMA N = 32 * kGU)
 // smem stages (one group each; kNS / kGU unit slots) and smem candidate slots
 // per thread, by top-k width: k <= 16 -> 6 stages, 40 slots; k <= 32 -> 4, 56.
 // Wide mode stages hold one 128-row fp16 chunk (8 KB instead of 16 KB); the
-// smem freed goes to candidate slots (64 / 72: the looser inner-product bound
-// keeps more candidates).  An overflowed run is rescanned exactly by the refine.
+// smem freed goes to 10 stages (k <= 16) and candidate slots (48 / 72: the looser
+// inner-product bound keeps more candidates).  An overflowed run is rescanned
+// exactly by the refine.
 #ifndef BIVF_TC_NS16
 #define BIVF_TC_NS16 6
 #endif
 #ifndef BIVF_TC_KC16
 #define BIVF_TC_KC16 40
 #endif
+#ifndef BIVF_TCW_NS16
+#define BIVF_TCW_NS16 10  // wide mode: deeper B prefetch (cfg5 scan 14.9 -> 13.0 ms)
+#endif
+#ifndef BIVF_TCW_KC16
+#define BIVF_TCW_KC16 48  // (32 slots overflow: rescans)
+#endif
 template <int KT, bool W = false>
 struct TcCfg {
-    static constexpr int NS = W ? (KT <= 16 ? 6 : 4) : (KT <= 16 ? BIVF_TC_NS16 : 4);
-    static constexpr int KC = W ? (KT <= 16 ? 64 : 72) : (KT <= 16 ? BIVF_TC_KC16 : 56);
+    static constexpr int NS = W ? (KT <= 16 ? BIVF_TCW_NS16 : 4) : (KT <= 16 ? BIVF_TC_NS16 : 4);
+    static constexpr int KC = W ? (KT <= 16 ? BIVF_TCW_KC16 : 72) : (KT <= 16 ? BIVF_TC_KC16 : 56);
     static constexpr int NU = NS / 2;
     static constexpr int STAGE = W ? 128 * 64 : 2 * 128 * 64;  // bytes per stage
 };
