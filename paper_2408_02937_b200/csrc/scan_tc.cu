@@ -153,7 +153,7 @@ struct TcParams {
     float* dense_nq;
     uint32_t dense_ld;
     // IVF dense mode (k > 32): list c's tiles start at dense_list_base[c]; tile t of a
-    // list with ng groups holds [ng][32 slots][128 tile rows] (warp-coalesced writes)
+    // list with ng groups holds [ng][128 tile rows][32 slots] (a row's group is one 128 B line)
     const uint64_t* dense_list_base;
     const uint32_t* dense_ppos;      // the plan's per-pair position in its list
     float2* dense_gsum;              // IVF dense mode: per (pair, group) (min upper, min lower bound)
@@ -491,30 +491,58 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
     pf.mark(6);
     const float* wslot = nslots + ns * kGU * kNormFloats;
     if (!W && p.dense_out) {  // dense mode (L2): write the approximate distances, no filtering
+        // this warp's 32 x 32 staging tile in the (otherwise unused) pass-2 scratch,
+        // 16 B chunks XOR-swizzled by row: each thread parks its row, then every
+        // store instruction writes four whole 128 B row segments
+        float4* sw = reinterpret_cast<float4*>(scr - m + (m & ~31u) * 32u);
+        const unsigned act = __ballot_sync(0xffffffffu, active);
+        // IVF: this warp's first row of the tile (the tile base from an active row)
+        float* wtile = nullptr;
+        if (p.dense_list_base && act)
+            wtile = p.dense_out +
+                    __shfl_sync(0xffffffffu, (unsigned long long)(qrow - m), __ffs(act) - 1) + (m & ~31u) * 32u;
 #pragma unroll
         for (int h = 0; h < kGU; ++h) {
             if ((uint32_t)h >= ng) break;
             const float* wn = wslot + h * kNormFloats;
             tmem_ld32(acol + 32 * h, dot);
-            if (active) {
-                float av[32];
+            float av[32];
 #pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                    const float4 v = reinterpret_cast<const float4*>(wn)[i / 4];
-                    av[i] = fmaf(-2.f, dot[i], nq + v.x);
-                    av[i + 1] = fmaf(-2.f, dot[i + 1], nq + v.y);
-                    av[i + 2] = fmaf(-2.f, dot[i + 2], nq + v.z);
-                    av[i + 3] = fmaf(-2.f, dot[i + 3], nq + v.w);
-                }
-                if (p.dense_list_base) {  // IVF: element (j, n) at base + (32 j + n) * 128
-                    float* o = p.dense_out + qrow + (uint64_t)(32u * (j0 + h)) * kM;
+            for (int i = 0; i < 32; i += 4) {
+                const float4 v = reinterpret_cast<const float4*>(wn)[i / 4];
+                av[i] = fmaf(-2.f, dot[i], nq + v.x);
+                av[i + 1] = fmaf(-2.f, dot[i + 1], nq + v.y);
+                av[i + 2] = fmaf(-2.f, dot[i + 2], nq + v.z);
+                av[i + 3] = fmaf(-2.f, dot[i + 3], nq + v.w);
+            }
+            if (act) {
 #pragma unroll
-                    for (int n = 0; n < 32; ++n) o[(uint64_t)n * kM] = av[n];
+                for (int c = 0; c < 8; ++c)
+                    sw[lane * 8 + (c ^ (lane & 7))] = make_float4(av[4 * c], av[4 * c + 1], av[4 * c + 2], av[4 * c + 3]);
+                __syncwarp();
+                if (p.dense_list_base) {
+                    // IVF: element (j, m, n) at tile + (j * 128 + m) * 32 + n, so the warp's
+                    // 32 rows are one contiguous 4 KB run (rows past the tile's pairs
+                    // are written too: the tile is allocated whole and never read there)
+                    float4* dst = reinterpret_cast<float4*>(wtile + (uint64_t)(j0 + h) * kM * 32u);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int r = i * 4 + (lane >> 3), ch = lane & 7;
+                        dst[i * 32 + lane] = sw[r * 8 + (ch ^ (r & 7))];
+                    }
                 } else {  // quantizer: one contiguous row per query
-                    float4* o = reinterpret_cast<float4*>(p.dense_out + qrow + 32u * (j0 + h));
+                    float* rowp = p.dense_out + qrow + 32u * (j0 + h);
 #pragma unroll
-                    for (int i = 0; i < 32; i += 4) o[i / 4] = make_float4(av[i], av[i + 1], av[i + 2], av[i + 3]);
+                    for (int i = 0; i < 8; ++i) {
+                        const int r = i * 4 + (lane >> 3), ch = lane & 7;
+                        float4* dst = reinterpret_cast<float4*>(
+                            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rowp), r));
+                        if ((act >> r) & 1u) dst[ch] = sw[r * 8 + (ch ^ (r & 7))];
+                    }
                 }
+                __syncwarp();
+            }
+            if (active) {
                 if (p.dense_gsum) {  // group summary: smallest upper / lower bound of its valid slots
                     const uint32_t j = j0 + h, og = (d.off + 31u) >> 5;
                     uint32_t nvalid;
@@ -1563,8 +1591,17 @@ __device__ __forceinline__ uint64_t ivf_group_index(const DevLists& L, uint32_t 
 // overall, k <= 128), (B) the exact k-th smallest upper bound, (C) every slot
 // whose lower bound reaches it recomputed EXACTLY (mirror rows, the
 // reference's sequential fp32 bits) into the (dist, id) top-k.
+constexpr uint32_t kSelMetaBytes = 40;  // per-probe metadata of dense_ivf_select_kernel
+constexpr uint32_t kSelChunk = 256;     // probes whose metadata one warp holds at a time
+
 template <int KPL>
-__global__ void dense_ivf_select_kernel(TcParams p, const long long* probes, float* out_d,
+#ifndef BIVF_SEL_MINB
+#define BIVF_SEL_MINB 6  // 80 registers: 6 blocks of 4 warps per SM
+#endif
+#ifndef BIVF_SEL_RING
+#define BIVF_SEL_RING 2  // group-summary chunks in flight per sweep
+#endif
+__global__ void __launch_bounds__(128, BIVF_SEL_MINB) dense_ivf_select_kernel(TcParams p, const long long* probes, float* out_d,
                                         long long* out_i, uint32_t* out_cnt, uint32_t nq) {
     extern __shared__ float qsm[];
     const uint32_t nw = blockDim.x >> 5, wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1575,40 +1612,109 @@ __global__ void dense_ivf_select_kernel(TcParams p, const long long* probes, flo
     uint32_t* ql = qc + 32;
     for (uint32_t i = lane; i < p.D; i += 32) qs[i] = p.queries[(uint64_t)q * p.Dp + i];
     __syncwarp();
+    // per-probe metadata of up to kSelChunk probes, gathered lane-parallel at the
+    // start of each chunk of a sweep (the sweeps would otherwise walk probes ->
+    // list -> plan position serially for every pair)
+    const uint32_t PC = min(p.P, kSelChunk);
+    char* meta = reinterpret_cast<char*>(qsm + nw * p.Dp) + nw * 256;
+    meta = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(meta) + 15) & ~uintptr_t(15)) +
+           (size_t)wq * PC * kSelMetaBytes;
+    uint64_t* m_blk = reinterpret_cast<uint64_t*>(meta);  // the pair's tile base in dense_out
+    uint64_t* m_g0 = m_blk + PC;                           // its first group summary
+    uint32_t* m_c = reinterpret_cast<uint32_t*>(m_g0 + PC);
+    uint32_t* m_off = m_c + PC;
+    uint32_t* m_len = m_off + PC;
+    uint32_t* m_ng = m_len + PC;
+    uint32_t* m_row = m_ng + PC;  // the pair's row in its tile
+    float* m_nq = reinterpret_cast<float*>(m_row + PC);
+    auto gather = [&](uint32_t pb, uint32_t pn) {
+        __syncwarp();
+        for (uint32_t pi = lane; pi < pn; pi += 32) {
+            const uint64_t pair = (uint64_t)q * p.P + pb + pi;
+            const uint32_t c = (uint32_t)probes[pair];
+            const uint32_t off = p.snap_off[c], len = p.snap_len[c], ng = ivf_ngroups(p.L, off, len);
+            const uint32_t pos = p.dense_ppos[pair];
+            const uint64_t blk = p.dense_list_base[c] + (uint64_t)(pos / kM) * ng * 32u * kM;
+            m_blk[pi] = blk;
+            m_g0[pi] = blk / 32u + (uint64_t)(pos % kM) * ng;
+            m_c[pi] = c;
+            m_off[pi] = off;
+            m_len[pi] = len;
+            m_ng[pi] = ng;
+            m_row[pi] = pos % kM;
+            m_nq[pi] = p.dense_nq[pair];
+        }
+        __syncwarp();
+    };
     const float inf = __int_as_float(0x7f800000);
     // the query's groups, a flat index over its probes: lane-strided sweeps read
-    // the (min upper, min lower) group summaries; only groups that can matter
-    // are opened slot by slot
-    auto groups = [&](auto&& f) {  // f(pair, c, j, gflat, summary)
-        for (uint32_t pi = 0; pi < p.P; ++pi) {
-            const uint64_t pair = (uint64_t)q * p.P + pi;
-            const uint32_t c = (uint32_t)probes[pair];
-            const uint32_t ng = ivf_ngroups(p.L, p.snap_off[c], p.snap_len[c]);
-            const uint32_t pos = p.dense_ppos[pair], m = pos % kM;
-            const uint64_t blk = p.dense_list_base[c] + (uint64_t)(pos / kM) * ng * 32u * kM;
-            const uint64_t g0 = blk / 32u + (uint64_t)m * ng;
-            for (uint32_t j0 = 0; j0 < ng; j0 += 32) {
-                const uint32_t j = j0 + lane;
-                const float2 sm = j < ng ? p.dense_gsum[g0 + j] : make_float2(inf, inf);
-                f(pair, c, j0, j < ng, sm);
+    // the (min upper, min lower) group summaries, four 32-group chunks in flight;
+    // only groups that can matter are opened slot by slot
+    auto groups = [&](auto&& f) {  // f(chunk-local probe, pair, first group of the chunk, valid, summary)
+        for (uint32_t pb = 0; pb < p.P; pb += kSelChunk) {
+            const uint32_t pn = min(kSelChunk, p.P - pb);
+            gather(pb, pn);
+            uint32_t hp = 0, hj = 0, tp = 0, tj = 0;  // consume / issue positions
+            auto issue = [&]() -> float2 {
+                float2 v = make_float2(inf, inf);
+                if (tp < pn) {
+                    const uint32_t ng = m_ng[tp];
+                    if (tj + lane < ng) v = p.dense_gsum[m_g0[tp] + tj + lane];
+                    tj += 32;
+                    if (tj >= ng) {
+                        ++tp;
+                        tj = 0;
+                    }
+                }
+                return v;
+            };
+            auto step = [&](float2& sl) {
+                const float2 cur = sl;
+                sl = issue();
+                const uint32_t ng = m_ng[hp];
+                f(hp, (uint64_t)q * p.P + pb + hp, hj, hj + lane < ng, cur);
+                hj += 32;
+                if (hj >= ng) {
+                    ++hp;
+                    hj = 0;
+                }
+            };
+#if BIVF_SEL_RING == 4
+            float2 s0 = issue(), s1 = issue(), s2 = issue(), s3 = issue();
+            while (hp < pn) {
+                step(s0);
+                if (hp >= pn) break;
+                step(s1);
+                if (hp >= pn) break;
+                step(s2);
+                if (hp >= pn) break;
+                step(s3);
             }
+#elif BIVF_SEL_RING == 2
+            float2 s0 = issue(), s1 = issue();
+            while (hp < pn) {
+                step(s0);
+                if (hp >= pn) break;
+                step(s1);
+            }
+#else
+            float2 s0 = issue();
+            while (hp < pn) step(s0);
+#endif
         }
     };
-    // open group j0 + src of `pair`: one slot per lane -> (valid, h, l)
-    auto open = [&](uint64_t pair, uint32_t c, uint32_t j, float& h, float& l) -> bool {
-        const uint32_t off = p.snap_off[c], len = p.snap_len[c];
+    // open group j of probe pi: one slot per lane -> (valid, h, l)
+    auto open = [&](uint32_t pi, uint32_t j, float& h, float& l) -> bool {
+        const uint32_t c = m_c[pi], off = m_off[pi];
         bool ar;
         const uint64_t g = ivf_group_index(p.L, c, off, j, ar);
-        const GroupRef gr = ivf_group(p.L, c, off, len, j);
+        const GroupRef gr = ivf_group(p.L, c, off, m_len[pi], j);
         h = inf;
         l = inf;
         if (lane < gr.nvalid) {
-            const uint32_t pos = p.dense_ppos[pair];
-            const uint32_t ngl = ivf_ngroups(p.L, off, len);
-            const uint64_t blk = p.dense_list_base[c] + (uint64_t)(pos / kM) * ngl * 32u * kM;
-            const float a = p.dense_out[blk + (uint64_t)(32u * j + lane) * kM + pos % kM];
+            const float a = p.dense_out[m_blk[pi] + ((uint64_t)j * kM + m_row[pi]) * 32u + lane];
             const float ns = (ar ? p.arena_nrm : p.off_nrm)[g * kNormFloats + lane];
-            const float e = fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, p.dense_nq[pair] + ns, 1e-30f));
+            const float e = fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, m_nq[pi] + ns, 1e-30f));
             h = a + e;
             l = a - e;
         }
@@ -1620,7 +1726,7 @@ __global__ void dense_ivf_select_kernel(TcParams p, const long long* probes, flo
     float pre = inf;
     if (p.k <= 128) {
         float b[4] = {inf, inf, inf, inf};
-        groups([&](uint64_t, uint32_t, uint32_t, bool valid, float2 sm) {
+        groups([&](uint32_t, uint64_t, uint32_t, bool valid, float2 sm) {
             if (!valid) return;
             float x = sm.x;
 #pragma unroll
@@ -1662,14 +1768,14 @@ __global__ void dense_ivf_select_kernel(TcParams p, const long long* probes, flo
     // upper bound is <= pre
     WarpTopK<KPL> th;
     th.init();
-    groups([&](uint64_t pair, uint32_t c, uint32_t j0, bool valid, float2 sm) {
+    groups([&](uint32_t pi, uint64_t pair, uint32_t j0, bool valid, float2 sm) {
         unsigned gm = __ballot_sync(0xffffffffu, valid && sm.x <= pre);
         while (gm) {
             const int src = __ffs(gm) - 1;
             gm &= gm - 1;
             const uint32_t j = j0 + src;
             float h, l;
-            const bool ok = open(pair, c, j, h, l);
+            const bool ok = open(pi, j, h, l);
             const long long id = (long long)(((pair << 15) | j) << 5 | lane);
             const bool pass = ok && h <= pre && th.admits(h, id);
             unsigned m = __ballot_sync(0xffffffffu, pass);
@@ -1710,21 +1816,21 @@ __global__ void dense_ivf_select_kernel(TcParams p, const long long* probes, flo
         qn = 0;
         __syncwarp();
     };
-    groups([&](uint64_t pair, uint32_t c, uint32_t j0, bool valid, float2 sm) {
+    groups([&](uint32_t pi, uint64_t, uint32_t j0, bool valid, float2 sm) {
         unsigned gm = __ballot_sync(0xffffffffu, valid && sm.y <= theta);
         while (gm) {
             const int src = __ffs(gm) - 1;
             gm &= gm - 1;
             const uint32_t j = j0 + src;
             float h, l;
-            const bool cand = open(pair, c, j, h, l) && l <= theta;
+            const bool cand = open(pi, j, h, l) && l <= theta;
             const unsigned msk = __ballot_sync(0xffffffffu, cand);
             const uint32_t np = __popc(msk);
             if (!np) continue;
             if (qn + np > 32) flush();
             if (cand) {
                 const uint32_t slot = qn + __popc(msk & ((1u << lane) - 1u));
-                qc[slot] = c;
+                qc[slot] = m_c[pi];
                 ql[slot] = (j << 5) | lane;
             }
             qn += np;
@@ -1958,7 +2064,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     if (ev1) cudaEventRecord(ev1, s);
     const uint32_t wpb = 4;
     if (dense && dense->list_base) {
-        const size_t sm_sel = wpb * (p.Dp * 4 + 256);
+        const size_t sm_sel = wpb * (p.Dp * 4 + 256) + 16 + wpb * std::min(sh.P, kSelChunk) * kSelMetaBytes;
         if (sh.k <= 32)
             dense_ivf_select_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
                 p, probes, out_d, out_i, out_cnt, sh.nq);
