@@ -117,6 +117,48 @@ struct WarpTopK {
     }
 };
 
+// The k smallest VALUES (no ids) across a warp, ascending, lane-strided like
+// WarpTopK: enough for a threshold (the k-th smallest value does not depend on
+// how ties are ordered), at half WarpTopK's shuffle traffic per insert.
+template <int KPL>
+struct WarpTopVal {
+    float d[KPL];
+    float thr;  // the k-th smallest so far (+inf until k were inserted)
+
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int r = 0; r < KPL; ++r) d[r] = __int_as_float(0x7f800000);
+        thr = __int_as_float(0x7f800000);
+    }
+    __device__ __forceinline__ bool admits(float x) const { return x < thr; }
+    // warp-uniform x; all 32 lanes must call
+    __device__ __forceinline__ void insert(float x, int k, int lane) {
+        int pos = 0;
+#pragma unroll
+        for (int r = 0; r < KPL; ++r) pos += __popc(__ballot_sync(0xffffffffu, (r * 32 + lane < k) && d[r] <= x));
+        if (pos >= k) return;
+        float carry = 0.f;
+#pragma unroll
+        for (int r = 0; r < KPL; ++r) {
+            const float up = __shfl_up_sync(0xffffffffu, d[r], 1);
+            const float top = __shfl_sync(0xffffffffu, d[r], 31);
+            const int e = r * 32 + lane;
+            const float prev = lane == 0 ? carry : up;
+            if (e == pos)
+                d[r] = x;
+            else if (e > pos)
+                d[r] = prev;
+            carry = top;
+        }
+        const int rk = (k - 1) >> 5;
+        float td = d[0];
+#pragma unroll
+        for (int r = 1; r < KPL; ++r)
+            if (r == rk) td = d[r];
+        thr = __shfl_sync(0xffffffffu, td, (k - 1) & 31);
+    }
+};
+
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -1765,10 +1765,10 @@ __global__ void __launch_bounds__(128, BIVF_SEL_MINB) dense_ivf_select_kernel(Tc
         pre = __shfl_sync(0xffffffffu, cand, kk & 31);
     }
     // (B) the exact k-th smallest upper bound: open the groups whose minimum
-    // upper bound is <= pre
-    WarpTopK<KPL> th;
+    // upper bound is <= pre (values only: ties do not move the k-th value)
+    WarpTopVal<KPL> th;
     th.init();
-    groups([&](uint32_t pi, uint64_t pair, uint32_t j0, bool valid, float2 sm) {
+    groups([&](uint32_t pi, uint64_t, uint32_t j0, bool valid, float2 sm) {
         unsigned gm = __ballot_sync(0xffffffffu, valid && sm.x <= pre);
         while (gm) {
             const int src = __ffs(gm) - 1;
@@ -1776,19 +1776,17 @@ __global__ void __launch_bounds__(128, BIVF_SEL_MINB) dense_ivf_select_kernel(Tc
             const uint32_t j = j0 + src;
             float h, l;
             const bool ok = open(pi, j, h, l);
-            const long long id = (long long)(((pair << 15) | j) << 5 | lane);
-            const bool pass = ok && h <= pre && th.admits(h, id);
+            const bool pass = ok && h <= pre && th.admits(h);
             unsigned m = __ballot_sync(0xffffffffu, pass);
             while (m) {
                 const int s2 = __ffs(m) - 1;
                 m &= m - 1;
                 const float bh = __shfl_sync(0xffffffffu, h, s2);
-                const long long bi = __shfl_sync(0xffffffffu, id, s2);
-                if (th.admits(bh, bi)) th.insert(bh, bi, (int)p.k, lane);
+                if (th.admits(bh)) th.insert(bh, (int)p.k, lane);
             }
         }
     });
-    const float theta = fminf(th.thr_d, pre);
+    const float theta = fminf(th.thr, pre);
     // (C) exact top-k over the candidates (groups whose minimum lower bound
     // reaches theta, then their slots), recomputed 32 at a time
     WarpTopK<KPL> tk;
