@@ -1593,13 +1593,14 @@ __device__ __forceinline__ uint64_t ivf_group_index(const DevLists& L, uint32_t 
 // reference's sequential fp32 bits) into the (dist, id) top-k.
 constexpr uint32_t kSelMetaBytes = 40;  // per-probe metadata of dense_ivf_select_kernel
 constexpr uint32_t kSelChunk = 256;     // probes whose metadata one warp holds at a time
+#ifndef BIVF_SEL_INFLIGHT
+#define BIVF_SEL_INFLIGHT 2
+#endif
+constexpr int kSelInflight = BIVF_SEL_INFLIGHT;  // group-summary loads in flight per lane
 
 template <int KPL>
 #ifndef BIVF_SEL_MINB
 #define BIVF_SEL_MINB 6  // 80 registers: 6 blocks of 4 warps per SM
-#endif
-#ifndef BIVF_SEL_RING
-#define BIVF_SEL_RING 2  // group-summary chunks in flight per sweep
 #endif
 __global__ void __launch_bounds__(128, BIVF_SEL_MINB) dense_ivf_select_kernel(TcParams p, const long long* probes, float* out_d,
                                         long long* out_i, uint32_t* out_cnt, uint32_t nq) {
@@ -1650,57 +1651,35 @@ __global__ void __launch_bounds__(128, BIVF_SEL_MINB) dense_ivf_select_kernel(Tc
     // the query's groups, a flat index over its probes: lane-strided sweeps read
     // the (min upper, min lower) group summaries, four 32-group chunks in flight;
     // only groups that can matter are opened slot by slot
-    auto groups = [&](auto&& f) {  // f(chunk-local probe, pair, first group of the chunk, valid, summary)
+    auto groups = [&](auto&& f) {  // f(chunk-local probe, group, valid, summary), per lane
+        // the order of a query's groups does not matter to any sweep, so each lane
+        // walks its own flat index (lane, lane + 32, ...) over the chunk's groups
+        // with kSelInflight summary loads in flight
         for (uint32_t pb = 0; pb < p.P; pb += kSelChunk) {
             const uint32_t pn = min(kSelChunk, p.P - pb);
             gather(pb, pn);
-            uint32_t hp = 0, hj = 0, tp = 0, tj = 0;  // consume / issue positions
-            auto issue = [&]() -> float2 {
-                float2 v = make_float2(inf, inf);
-                if (tp < pn) {
-                    const uint32_t ng = m_ng[tp];
-                    if (tj + lane < ng) v = p.dense_gsum[m_g0[tp] + tj + lane];
-                    tj += 32;
-                    if (tj >= ng) {
-                        ++tp;
-                        tj = 0;
-                    }
-                }
-                return v;
-            };
-            auto step = [&](float2& sl) {
-                const float2 cur = sl;
-                sl = issue();
-                const uint32_t ng = m_ng[hp];
-                f(hp, (uint64_t)q * p.P + pb + hp, hj, hj + lane < ng, cur);
-                hj += 32;
-                if (hj >= ng) {
-                    ++hp;
-                    hj = 0;
+            uint32_t pi = 0, j = lane;
+            auto norm = [&]() {
+                while (pi < pn && j >= m_ng[pi]) {
+                    j -= m_ng[pi];
+                    ++pi;
                 }
             };
-#if BIVF_SEL_RING == 4
-            float2 s0 = issue(), s1 = issue(), s2 = issue(), s3 = issue();
-            while (hp < pn) {
-                step(s0);
-                if (hp >= pn) break;
-                step(s1);
-                if (hp >= pn) break;
-                step(s2);
-                if (hp >= pn) break;
-                step(s3);
+            norm();
+            while (__any_sync(0xffffffffu, pi < pn)) {
+                uint32_t ps[kSelInflight], js[kSelInflight];
+                float2 v[kSelInflight];
+#pragma unroll
+                for (int u = 0; u < kSelInflight; ++u) {
+                    ps[u] = pi;
+                    js[u] = j;
+                    v[u] = pi < pn ? p.dense_gsum[m_g0[pi] + j] : make_float2(inf, inf);
+                    j += 32;
+                    norm();
+                }
+#pragma unroll
+                for (int u = 0; u < kSelInflight; ++u) f(ps[u], js[u], ps[u] < pn, v[u]);
             }
-#elif BIVF_SEL_RING == 2
-            float2 s0 = issue(), s1 = issue();
-            while (hp < pn) {
-                step(s0);
-                if (hp >= pn) break;
-                step(s1);
-            }
-#else
-            float2 s0 = issue();
-            while (hp < pn) step(s0);
-#endif
         }
     };
     // open group j of probe pi: one slot per lane -> (valid, h, l)
@@ -1726,7 +1705,7 @@ __global__ void __launch_bounds__(128, BIVF_SEL_MINB) dense_ivf_select_kernel(Tc
     float pre = inf;
     if (p.k <= 128) {
         float b[4] = {inf, inf, inf, inf};
-        groups([&](uint32_t, uint64_t, uint32_t, bool valid, float2 sm) {
+        groups([&](uint32_t, uint32_t, bool valid, float2 sm) {
             if (!valid) return;
             float x = sm.x;
 #pragma unroll
@@ -1768,12 +1747,12 @@ __global__ void __launch_bounds__(128, BIVF_SEL_MINB) dense_ivf_select_kernel(Tc
     // upper bound is <= pre (values only: ties do not move the k-th value)
     WarpTopVal<KPL> th;
     th.init();
-    groups([&](uint32_t pi, uint64_t, uint32_t j0, bool valid, float2 sm) {
+    groups([&](uint32_t gpi, uint32_t gj, bool valid, float2 sm) {
         unsigned gm = __ballot_sync(0xffffffffu, valid && sm.x <= pre);
         while (gm) {
             const int src = __ffs(gm) - 1;
             gm &= gm - 1;
-            const uint32_t j = j0 + src;
+            const uint32_t pi = __shfl_sync(0xffffffffu, gpi, src), j = __shfl_sync(0xffffffffu, gj, src);
             float h, l;
             const bool ok = open(pi, j, h, l);
             const bool pass = ok && h <= pre && th.admits(h);
@@ -1814,12 +1793,12 @@ __global__ void __launch_bounds__(128, BIVF_SEL_MINB) dense_ivf_select_kernel(Tc
         qn = 0;
         __syncwarp();
     };
-    groups([&](uint32_t pi, uint64_t, uint32_t j0, bool valid, float2 sm) {
+    groups([&](uint32_t gpi, uint32_t gj, bool valid, float2 sm) {
         unsigned gm = __ballot_sync(0xffffffffu, valid && sm.y <= theta);
         while (gm) {
             const int src = __ffs(gm) - 1;
             gm &= gm - 1;
-            const uint32_t j = j0 + src;
+            const uint32_t pi = __shfl_sync(0xffffffffu, gpi, src), j = __shfl_sync(0xffffffffu, gj, src);
             float h, l;
             const bool cand = open(pi, j, h, l) && l <= theta;
             const unsigned msk = __ballot_sync(0xffffffffu, cand);
