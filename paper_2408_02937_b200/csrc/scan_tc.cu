@@ -1333,11 +1333,15 @@ __device__ __forceinline__ void warp_bitonic(uint64_t (&v)[R], uint32_t lane) {
 // element e of a warp_bitonic array (warp-uniform e)
 template <int R>
 __device__ __forceinline__ uint64_t warp_elem(const uint64_t (&v)[R], uint32_t e) {
-    uint64_t x = v[0];
+    // shuffle every register row and keep row e / 32: a register select chain here
+    // gets folded into an indexed load, which moves the whole array to local memory
+    uint64_t x = 0;
 #pragma unroll
-    for (int j = 1; j < R; ++j)
-        if (e >> 5 == (uint32_t)j) x = v[j];
-    return __shfl_sync(0xffffffffu, x, e & 31);
+    for (int j = 0; j < R; ++j) {
+        const uint64_t t = __shfl_sync(0xffffffffu, v[j], e & 31);
+        if (e >> 5 == (uint32_t)j) x = t;
+    }
+    return x;
 }
 // Fast selection of dense_select_kernel (R pre-threshold keys per lane, lists of
 // 32 RL slots; k <= 32R <= n): true when
