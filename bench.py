@@ -1,25 +1,40 @@
 #!/usr/bin/env python3
-"""Benchmark of the B200 online IVF-Flat path — BASELINE.json configs[1]:
+"""Benchmark of the B200 online IVF-Flat path on the north-star workload
+(BASELINE.json north_star "Target"):
 
-    IVF-Flat 1M x 128 fp32 (SIFT-like synthetic), nlist=1024, nprobe=32, k=10,
-    with 10K vectors/s streaming inserts on one B200.
+    IVF-Flat 10M x 128 fp32 (SIFT-like synthetic), nlist=4096, nprobe=12, k=10,
+    with 10K vectors/s of concurrent inserts (+ 1K deletes/s) on one B200.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
 Data: the reference generator (dataset.cpp:92-112, bit-identical restatement)
-synthetic_dataset(1M + 10K + 600K, 128, 4096 components, seed 2), rounded and
-clamped at 0 (SIFT-like).  k-means (10 iters) on the first 100K rows, the 1M
-base rows bulk-loaded as offline segments, 10K held-out queries, the last 600K
-rows feed the live-insert stream.
+synthetic_dataset(10M + 10K + 1.2M, 128, 256 components, seed 2), rounded and
+clamped at 0 (SIFT-like).  256 Gaussian components under 4096 lists: every
+component spans ~16 lists, so recall depends on nprobe the way it does on real
+SIFT (tools/recall_sweep.py: nprobe 8 -> 0.855, 12 -> 0.974, 16 -> 0.998).
+NPROBE = 12 is the smallest value of that sweep with recall@10 >= 0.95; the run
+re-measures recall against exact ground truth (full-probe search = brute force).
+k-means (10 iters) on the first 256K rows, the 10M base rows bulk-loaded as
+offline segments, 10K held-out queries; the last 1.2M rows feed the live
+insert stream in Zipf(s=1) cluster order (workload.cpp:48-96), so a few lists
+grow block chains and the rearrangement (Alg. 3, T'_m = 2048) fires.
 
-A step = one search of the 10K-query batch (device-resident inputs) while a
-thread streams 10K vectors/s of inserts (128-vector batches, the executor's
-batch multiple) into the same index.  value = queries / device time (CUDA
+A step = one search of the 10K-query batch (device-resident inputs) while
+threads stream 10K vectors/s of inserts (128-vector batches, the executor's
+batch multiple, each followed by the rearrangement sweep, executor.cpp:380)
+and 1K deletes/s into the same index.  value = queries / device time (CUDA
 events, max over ranks).  e2e = the same through the host C-ABI call
-(bivf_search: H2D queries + D2H results inside the timed region).
+(bivf_search: H2D queries + D2H results inside the timed region).  The index
+(10M x 128 fp32 = 5.1 GB payload) is far larger than the 126 MB L2.
+
+--impl reference: the UNMODIFIED reference (oracle/_ref, compiled from
+/root/reference/proj/src) on the host cores, on the SAME index: the GPU build
+(bit-identical to the reference's offline build, tests/test_gpu_parity.py)
+saves a BIVFSNAP snapshot in the untimed setup and ClusterIndex::load reads it;
+the timed steps and the live inserts run only reference code.
 N > 1: the base is vector-sharded (id mod N); every rank searches
 the whole batch on its shard, top-k lists are all-gathered over NCCL and
-merged on device (bivf_merge_topk_device): strong scaling.
+merged on device (bivf_merge_topk_device).
 """
 from __future__ import annotations
 
@@ -37,20 +52,32 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_BASE = 1_000_000
+N_BASE = 10_000_000
 N_QUERY = 10_000
-N_INSERT = 600_000
+N_POOL = 1_200_000        # live-insert source (10K vec/s for the whole run)
 DIM = 128
-NLIST = 1024
-NPROBE = 32
+NLIST = 4096
+COMPS = 256
+SEED = 2
+NPROBE = 12
 K = 10
-TRAIN = 100_000
+TRAIN = 262_144
 KMEANS_ITERS = 10
-BLOCK = 1024            # T_m, paper default
-INSERT_RATE = 10_000.0  # vectors / s (BASELINE configs[1])
-INSERT_BATCH = 128      # executor batch multiple (executor.hpp:31)
+BLOCK = 1024              # T_m, paper default
+REARRANGE_T = 2048        # T'_m: two blocks (Zipf-hot lists exceed it within seconds)
+INSERT_RATE = 10_000.0    # vectors / s
+INSERT_BATCH = 128        # executor batch multiple (executor.hpp:31)
+DELETE_RATE = 1_000.0     # ids / s (extension: the reference has no delete)
+DELETE_BATCH = 64
+ZIPF_S = 1.0
 METRIC = "QPS at recall@10>=0.95 and p99 latency under live inserts, 1/2/4/8 B200"
-WORKLOAD = "IVF-Flat 1Mx128 fp32 SIFT-like synthetic, nlist=1024, nprobe=32, k=10, 10K vec/s live inserts"
+WORKLOAD = ("IVF-Flat 10Mx128 fp32 SIFT-like synthetic (256 components), nlist=4096, nprobe=12, "
+            "k=10, 10K vec/s Zipf live inserts + 1K deletes/s")
+SNAPSHOT = "/tmp/bivf_north_star.bivf"
+
+# mirror bytes per 32-vector group the TC scan streams (mirror.cuh): bf16 hi + lo
+# planes (2 x K x 32 x 2 B, K = D rounded to 16) + the norm block (64 fp32)
+MIRROR_GROUP_BYTES = 2 * ((DIM + 15) // 16 * 16) * 32 * 2 + 64 * 4
 
 
 def log(*a):
@@ -59,10 +86,62 @@ def log(*a):
 
 def make_data(gen):
     t = time.time()
-    x = gen(N_BASE + N_QUERY + N_INSERT, DIM, 4096, 2)
+    x = gen(N_BASE + N_QUERY + N_POOL, DIM, COMPS, SEED)
     np.maximum(np.rint(x, out=x), 0, out=x)  # SIFT-like: non-negative integers
     log(f"data {x.shape} in {time.time() - t:.1f}s")
     return x[:N_BASE], x[N_BASE:N_BASE + N_QUERY], x[N_BASE + N_QUERY:]
+
+
+def zipf_order(asg, nclusters, s=ZIPF_S, seed=7):
+    """Insert order after workload.cpp:48-96 (zipf_insertion_order): bucket the
+    held-out rows by assigned cluster; Zipf(s) over a seeded cluster permutation
+    picks the bucket of each emission.  The reference drains buckets (a hot
+    list's supply of ~300 held-out rows runs out within seconds); here each
+    emission draws a row of its bucket WITH replacement (and build_index adds
+    fresh noise to every drawn row), so the hot lists keep growing block
+    chains for the whole run."""
+    rng = np.random.default_rng(seed)
+    rank = rng.permutation(nclusters)
+    w = 1.0 / np.power(np.arange(1, nclusters + 1, dtype=np.float64), s)
+    cnt = np.bincount(asg, minlength=nclusters)
+    starts = np.zeros(nclusters + 1, np.int64)
+    np.cumsum(cnt, out=starts[1:])
+    nonempty = np.flatnonzero(cnt[rank] > 0)          # fall forward past empty buckets
+    nxt = nonempty[np.searchsorted(nonempty, np.arange(nclusters)) % len(nonempty)]
+    c = rank[nxt[rng.choice(nclusters, size=len(asg), p=w / w.sum())]]
+    order_by_c = np.argsort(asg, kind="stable")
+    return order_by_c[starts[c] + (rng.random(len(asg)) * cnt[c]).astype(np.int64)]
+
+
+def build_index(base, pool, dev, rank=0, world=1):
+    """GPU build: k-means (kmeans.cpp:31-142, bit-identical), exact assignment
+    (ivf_index.cpp:93-105), offline segments (ivf_index.cpp:61-82).  Returns the
+    index and the Zipf-ordered insert pool of this rank."""
+    import paper_2408_02937_b200 as bivf
+    t = time.time()
+    cent, _, its = bivf.kmeans(base[:TRAIN], NLIST, KMEANS_ITERS, 42, device=dev)
+    log(f"kmeans {TRAIN}x{DIM} -> {NLIST} in {time.time() - t:.1f}s ({its} iters)")
+    nblocks = (N_POOL // world + BLOCK - 1) // BLOCK + 2 * NLIST + 64
+    ix = bivf.ClusterIndex.empty(DIM, NLIST, block_capacity=BLOCK, num_blocks=nblocks,
+                                 rearrange_threshold=REARRANGE_T, device=dev)
+    ix.set_centroids(cent)
+    t = time.time()
+    mine = np.arange(rank, N_BASE, world, dtype=np.int64)
+    sub = base if world == 1 else np.ascontiguousarray(base[mine])
+    ix.bulk_load(sub, ix.assign_batch(sub), ids=mine if world > 1 else None)
+    del sub
+    order = zipf_order(ix.assign_batch(pool), NLIST)
+    # rows drawn more than once get fresh noise (the generator's N(0, 3^2)), rounded
+    # like the rest: a hot list receives new vectors of its component, not exact
+    # copies (hundreds of bit-identical duplicates would tie every distance)
+    ins = pool[order]
+    rng = np.random.default_rng(13)
+    for s in range(0, len(ins), 200_000):
+        blk = ins[s:s + 200_000]
+        blk += rng.normal(0.0, 3.0, blk.shape).astype(np.float32)
+        np.maximum(np.rint(blk, out=blk), 0, out=blk)
+    log(f"bulk load {len(mine)} + zipf order in {time.time() - t:.1f}s")
+    return ix, ins
 
 
 class Clocks:
@@ -140,12 +219,13 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi 200 ms"}
 
 
-class Inserter(threading.Thread):
-    """Paced live-insert stream (INSERT_RATE vec/s in INSERT_BATCH batches)."""
+class Paced(threading.Thread):
+    """A paced stream of `fn(chunk)` calls: `rate` items / s in `batch`-item
+    chunks of `pool` (inserts: vectors; deletes: ids)."""
 
-    def __init__(self, insert_fn, pool, rate=INSERT_RATE, batch=INSERT_BATCH):
+    def __init__(self, fn, pool, rate, batch):
         super().__init__(daemon=True)
-        self.fn, self.pool, self.rate, self.batch = insert_fn, pool, rate, batch
+        self.fn, self.pool, self.rate, self.batch = fn, pool, rate, batch
         self.stop_ev = threading.Event()
         self.done = 0
         self.pos = 0
@@ -160,9 +240,8 @@ class Inserter(threading.Thread):
             while not self.stop_ev.is_set():
                 if self.pos + self.batch > len(self.pool):
                     break
-                self.fn(self.pool[self.pos:self.pos + self.batch])
+                self.done += self.fn(self.pool[self.pos:self.pos + self.batch])
                 self.pos += self.batch
-                self.done += self.batch
                 nxt += period
                 dt = nxt - time.perf_counter()
                 if dt > 0:
@@ -177,13 +256,18 @@ class Inserter(threading.Thread):
         if self.err:
             raise self.err
         el = (self.t1 or time.perf_counter()) - (self.t0 or 0)
-        return {"vectors": self.done, "rate_vec_s": self.done / el if el > 0 else 0.0}
+        return {"items": self.done, "rate_per_s": round(self.done / el, 1) if el > 0 else 0.0}
+
+
+def delete_ids(rank, world, seed=11):
+    """The delete stream: distinct random base ids of this shard, seeded."""
+    rng = np.random.default_rng(seed)
+    ids = rng.choice(N_BASE, size=400_000, replace=False).astype(np.int64)
+    return np.ascontiguousarray(ids[ids % world == rank])
 
 
 # --------------------------------------------------------------------------- ours
 def run_ours(args, dist):
-    import ctypes as C
-
     import torch
 
     import paper_2408_02937_b200 as bivf
@@ -194,23 +278,8 @@ def run_ours(args, dist):
     torch.cuda.set_device(dev)
     L = _lib.lib()
     base, queries, pool = make_data(bivf.synthetic_dataset)
-    # training (k-means on the first TRAIN rows; identical on every rank)
-    t = time.time()
-    cent, _, its = bivf.kmeans(base[:TRAIN], NLIST, KMEANS_ITERS, 42, device=dev)
-    log(f"kmeans {TRAIN}x{DIM} -> {NLIST} in {time.time() - t:.1f}s ({its} iters)")
-    # shard by id mod world; ids are global row ids
-    mine = np.arange(rank, N_BASE, world, dtype=np.int64)
-    n_ins_total = int(INSERT_RATE * 600) // world  # capacity for 10 min of inserts
-    nblocks = (n_ins_total + BLOCK - 1) // BLOCK + 2 * NLIST + 64
-    ix = bivf.ClusterIndex.empty(DIM, NLIST, block_capacity=BLOCK, num_blocks=nblocks,
-                                 rearrange_threshold=256, device=dev)
-    ix.set_centroids(cent)
-    t = time.time()
-    sub = np.ascontiguousarray(base[mine])
-    asg = ix.assign_batch(sub)
-    ix.bulk_load(sub, asg, ids=mine if world > 1 else None)
-    log(f"bulk load {len(mine)} in {time.time() - t:.1f}s")
-    del sub
+    ix, ins_pool = build_index(base, pool, dev, rank, world)
+    del pool
 
     qd = torch.from_numpy(queries).to(f"cuda:{dev}")
     B = qd.shape[0]
@@ -235,9 +304,8 @@ def run_ours(args, dist):
                                                 md.data_ptr(), mi.data_ptr(), mc.data_ptr(),
                                                 stream.cuda_stream))
 
-    # live inserts: shard the stream the same way (id mod world) with global ids
-    ins_pool = pool[rank::world]
-    ins_ids = (N_BASE + np.arange(len(pool), dtype=np.int64))[rank::world]
+    # live inserts (global ids, sharded id mod world) + deletes, each on its own thread
+    ins_ids = (N_BASE + np.arange(len(ins_pool) * world, dtype=np.int64))[rank::world]
     state = {"pos": 0}
 
     def insert_fn(x):
@@ -246,9 +314,17 @@ def run_ours(args, dist):
         state["pos"] += len(x)
         ix.insert(x, ids)
         ix.rearrange_sweep()  # post_insert_maintenance (executor.cpp:380)
+        return len(x)
 
-    ins = Inserter(insert_fn, ins_pool, INSERT_RATE / world)
+    def delete_fn(ids):
+        return ix.remove(ids)[0]
+
+    del_ids = delete_ids(rank, world)
+    half = len(ins_pool) // 2
+    ins = Paced(insert_fn, ins_pool[:half], INSERT_RATE / world, INSERT_BATCH)
+    dels = Paced(delete_fn, del_ids[:len(del_ids) // 2], DELETE_RATE / world, DELETE_BATCH)
     ins.start()
+    dels.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -291,34 +367,30 @@ def run_ours(args, dist):
         e2e_call()
     e2e_s = max_over_ranks(dist, time.perf_counter() - t)
     ins_stats = ins.finish()
+    del_stats = dels.finish()
+    rr_events = len(ix.take_rearrange_events())
 
     # --- p50/p99 of executor requests (10-query batches, the reference's
-    # max_search_batch) without and with the 10K vec/s insert stream
+    # max_search_batch) without and with the live insert + delete streams
     latency = None
     if rank == 0 and world == 1 and not args.no_latency:
-        latency = latency_phase(ix, hq, pool[len(pool) // 2:])
+        latency = latency_phase(ix, hq, ins_pool[half:], del_ids[len(del_ids) // 2:], args.lat_seconds,
+                                args.lat_repeats)
 
-    # --- per-kernel timing of the dominant kernel (scan) on its lease stream
+    # --- per-phase timing of one search (CUDA events on the lease stream)
     ix.set_timing(True)
-    scan_ms = []
     phases = []
     for _ in range(max(3, args.steps)):
         ix.search_batch(hq, K, NPROBE)
-        tt = ix.last_timings()
-        phases.append(tt)
-        scan_ms.append(tt[2])
+        phases.append(ix.last_timings())
     ix.set_timing(False)
-    scan_avg = statistics.mean(scan_ms)
     ph = [statistics.mean(p[i] for p in phases) for i in range(4)]
 
-    # algorithmic bytes of one scan launch: committed vectors of every probed list
     probes = ix.probes(hq, NPROBE)
     sizes = np.array([ix.offline_count(c) + ix.list_length(c) for c in range(NLIST)], np.int64)
-    scanned = int(sizes[probes].sum())
-    alg_bytes = scanned * DIM * 4
     # recall@10 vs exact (full probe == brute force over every list), through the
     # same (sharded, for N > 1: a collective on every rank) search as the e2e leg
-    nrec = 200
+    nrec = 500
     if world > 1:
         gi_, _, _ = sharded.search(hq[:nrec], K, NPROBE)
         ti_, _, _ = sharded.search(hq[:nrec], K, NLIST)
@@ -342,17 +414,21 @@ def run_ours(args, dist):
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f32",
-            "data": "synthetic (reference generator dataset.cpp:92-112, SIFT-like rounding)",
+            "data": "synthetic (reference generator dataset.cpp:92-112, 256 components, SIFT-like rounding)",
             "config": {"workload": WORKLOAD, "n_base": N_BASE, "dim": DIM, "nlist": NLIST,
                        "nprobe": NPROBE, "k": K, "batch": B, "block_capacity": BLOCK,
-                       "insert_rate_vec_s": INSERT_RATE, "parallelism": f"vector-shard{world}",
-                       "l2_note": "index payload 512 MB > 126 MB L2 (inputs larger than L2)"},
+                       "rearrange_threshold": REARRANGE_T, "insert_rate_vec_s": INSERT_RATE,
+                       "delete_rate_ids_s": DELETE_RATE, "insert_order": f"zipf s={ZIPF_S}",
+                       "parallelism": f"vector-shard{world}",
+                       "l2_note": "index payload 5.1 GB > 126 MB L2 (inputs larger than L2)"},
             "recall_at_10": round(recall, 4),
             "live_inserts": ins_stats,
+            "live_deletes": del_stats,
+            "rearrange_events": rr_events,
             "e2e": {"value": round(B * args.steps / e2e_s, 1), "unit": "queries/s",
                     "h2d_bytes_per_step": int(B * DIM * 4),
                     "d2h_bytes_per_step": int(B * K * 12 + B * 4)},
-            "roofline": roofline(alg_bytes, scanned, scan_avg, ph, peaks),
+            "roofline": roofline(probes, sizes, ph, peaks),
             "gpu_launches": int(launches),
             "clocks": clk,
         }
@@ -365,77 +441,115 @@ def run_ours(args, dist):
     return result
 
 
-def roofline(alg_bytes, pairs, scan_ms, ph, peaks):
+def scan_bytes(probes, sizes, tile=128):
+    """Algorithmic bytes of one search's list scan: the TC scan
+    groups queries by list, ≤ `tile` queries per work item, and streams each
+    probed list's mirror once per item (MIRROR_GROUP_BYTES per 32-vector group),
+    plus the seeding pass (first unit, 2 groups, of every query's nearest list)."""
+    nl = len(sizes)
+    groups = (sizes + 31) // 32
+    q_per_list = np.bincount(probes.reshape(-1).astype(np.int64), minlength=nl)
+    tiles = (q_per_list + tile - 1) // tile
+    full = int((tiles * groups).sum()) * MIRROR_GROUP_BYTES
+    q_near = np.bincount(probes[:, 0].astype(np.int64), minlength=nl)
+    seed = int((((q_near + tile - 1) // tile) * np.minimum(groups, 2)).sum()) * MIRROR_GROUP_BYTES
+    pairs = int(sizes[probes].sum())
+    return full + seed, pairs
+
+
+def roofline(probes, sizes, ph, peaks):
     """Roofline of the dominant kernel (scan_tc_kernel).
 
-    Queries are grouped by list, so one staged 32-vector group serves up to 128
-    queries: the kernel streams each list from L2/HBM once per query tile and
-    is bound by the tensor pipe, not HBM.  Its algorithmic work per search step
-    is the 3xBF16 filter GEMM over every (query, probed vector) pair:
-    3 MMAs x 2 x K flops per pair (K = D rounded up to 16), summed over the two
-    launches of the two-phase scan (nearest list first, then the other P - 1).
-    Peak: the driver-measured dense bf16 rate (MEASURED_PEAKS.json bf16_tflops,
-    cuBLAS burst; the scan is ~1.4 ms of a ~1.8 ms step).
-    The north star's per-query HBM figure (bytes of every probed list, per
-    query) is reported beside it: query grouping makes it exceed HBM bandwidth.
-    `traffic` is the ncu DRAM read+write bytes of the scan launches per step
-    from profiles/r01_scan_tc_ncu.json (same index shape, tools/ncu_tc.sh)."""
-    peak = peaks.get("bf16_tflops", 1641.9)
-    K = (DIM + 15) // 16 * 16
-    flops = 3.0 * 2.0 * K * pairs
-    achieved = flops / (scan_ms * 1e-3) / 1e12
+    At 10M x 128 a 10K-query batch with nprobe 12 probes every list ~29 times,
+    and the TC scan serves all of a list's queries (≤128 per item) from one
+    pass over the list's scan mirror: the kernel streams the whole mirror from
+    HBM once per batch and is HBM-bound.  achieved = algorithmic bytes per
+    search (scan_bytes) / the scan phase's CUDA-event time; peak =
+    MEASURED_PEAKS.json hbm_gbs.  Beside it: the tensor work of the 3xBF16
+    filter (3 x 2 x K flops per (query, vector) pair) and its useful fp32
+    share (1 of the 3 MMAs).  `traffic` = ncu DRAM read+write bytes of the
+    scan launches of one search (profiles/r02_scan_tc_ncu.json, same workload)."""
+    alg_bytes, pairs = scan_bytes(probes, sizes)
+    scan_ms = ph[2]
     hbm = peaks.get("hbm_gbs", 6548.2)
-    per_query_gbs = alg_bytes / (scan_ms * 1e-3) / 1e9
+    achieved = alg_bytes / (scan_ms * 1e-3) / 1e9
+    tc_peak = peaks.get("bf16_tflops", 1641.9)
+    Kd = (DIM + 15) // 16 * 16
+    tflops = 3.0 * 2.0 * Kd * pairs / (scan_ms * 1e-3) / 1e12
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_scan_tc_ncu.json")) as f:
-            prof = json.load(f)
-        traffic = prof.get("dram_bytes_per_launch")
+        with open(os.path.join(ROOT, "profiles", "r02_scan_tc_ncu.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
-    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1),
-            "unit": "TFLOP/s", "frac": round(achieved / peak, 3), "traffic": traffic,
-            "kernel": "scan_tc_kernel (2 launches: rank-0 probes, then the rest)",
-            "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense bf16, cuBLAS burst)",
-            "alg_flops_per_launch": flops, "pairs_per_launch": int(pairs), "scan_ms": round(scan_ms, 3),
-            "north_star_hbm": {"per_query_bytes_per_launch": alg_bytes,
-                               "achieved_gbs": round(per_query_gbs, 1), "peak_gbs": hbm,
-                               "frac": round(per_query_gbs / hbm, 3)},
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": round(hbm, 1), "unit": "GB/s",
+            "frac": round(achieved / hbm, 3), "traffic": traffic,
+            "kernel": "scan_tc_kernel (2 launches per search: seeding pass, full scan)",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+            "alg_bytes_per_launch": alg_bytes,
+            "alg_bytes_rule": f"sum over (list, <=128-query item) of the list's mirror groups x "
+                              f"{MIRROR_GROUP_BYTES} B + seeding pass",
+            "scan_ms": round(scan_ms, 3),
+            "tensor": {"pairs": pairs, "achieved_tflops": round(tflops, 1), "peak_tflops": tc_peak,
+                       "frac": round(tflops / tc_peak, 3),
+                       "useful_fp32_frac": round(tflops / 3 / tc_peak, 3)},
             "phase_ms": {"quantizer": round(ph[0], 3), "plan": round(ph[1], 3),
                          "scan": round(ph[2], 3), "refine": round(ph[3], 3)}}
 
 
 LAT_QPS = 1000.0      # search requests / s (x 10 queries each)
-LAT_SECONDS = 4.0
 
 
-def latency_phase(ix, queries, inserts):
+def latency_phase(ix, queries, inserts, dels, seconds, repeats):
     """Open-loop replay through the native executor (32 lanes): p50/p99 search
-    latency with no inserts and with 10K vec/s inserts (78 req/s x 128)."""
-    from paper_2408_02937_b200.executor import Executor, replay
+    latency without and with the live streams (10K vec/s Zipf inserts through
+    the executor's batcher + rearrangement sweeps, 1K deletes/s), windows
+    alternated `repeats` times so box drift hits both sides alike."""
+    from paper_2408_02937_b200.executor import Executor, replay, summarize_latencies
     ex = Executor(ix, num_lanes=32)
-    common = dict(k=K, nprobe=NPROBE, search_batch=10, insert_batch=INSERT_BATCH, seed=1,
-                  poisson=True)
+    common = dict(k=K, nprobe=NPROBE, search_batch=10, insert_batch=INSERT_BATCH, poisson=True)
     # untimed warm-up: every lane's lease workspace and staging buffers get allocated
-    replay(ex, queries, inserts, LAT_QPS, INSERT_RATE / INSERT_BATCH, 0.5, **common)
-    base = replay(ex, queries, inserts, LAT_QPS, 0.0, LAT_SECONDS, raw=True, **common)
-    live = replay(ex, queries, inserts, LAT_QPS, INSERT_RATE / INSERT_BATCH, LAT_SECONDS, raw=True,
-                  **common)
-    for nm, r in (("idle", base), ("live", live)):  # stalls, for the log
-        sp = [(i, round(v / 1e3, 1)) for i, v in enumerate(r.pop("search_raw_us")) if v > 5000]
-        r.pop("insert_raw_us")
-        if sp:
-            log(f"latency {nm}: {len(sp)} requests > 5 ms, first {sp[:10]}")
+    replay(ex, queries, inserts[:100_000], LAT_QPS, INSERT_RATE / INSERT_BATCH, 0.5, seed=99, **common)
+    idle, live, ins_lat = [], [], []
+    rr = 0
+    dpos = 0
+    ipos = 100_000
+    ndel = 0
+    for r in range(repeats):
+        a = replay(ex, queries, None, LAT_QPS, 0.0, seconds, raw=True, seed=2 * r + 1, **common)
+        idle.append(a)
+        n_ins = int(INSERT_RATE * seconds) + 2 * INSERT_BATCH
+        chunk = inserts[ipos:ipos + n_ins]
+        ipos += n_ins
+        dchunk = dels[dpos:dpos + int(DELETE_RATE * seconds) + DELETE_BATCH]
+        dpos += len(dchunk)
+        dl = Paced(lambda i: ix.remove(i)[0], dchunk, DELETE_RATE, DELETE_BATCH)
+        ix.take_rearrange_events()
+        dl.start()
+        b = replay(ex, queries, chunk, LAT_QPS, INSERT_RATE / INSERT_BATCH, seconds, raw=True,
+                   seed=2 * r + 2, **common)
+        ndel += dl.finish()["items"]
+        rr += len(ix.take_rearrange_events())
+        live.append(b)
     ex.shutdown()
     ex.close()
-    p99a, p99b = base["search"]["p99_ms"], live["search"]["p99_ms"]
+
+    def merged(rs, key):
+        v = np.concatenate([x[key + "_raw_us"] for x in rs])
+        return summarize_latencies([u / 1e3 for u in v if u >= 0])
+
+    s_idle, s_live, s_ins = merged(idle, "search"), merged(live, "search"), merged(live, "insert")
+    per_rep = [round(b["search"]["p99_ms"] / a["search"]["p99_ms"], 3) for a, b in zip(idle, live)]
     return {"arrivals": "poisson", "search_req_s": LAT_QPS, "queries_per_req": 10,
-            "insert_vec_s": INSERT_RATE, "seconds": LAT_SECONDS,
-            "search_no_inserts_ms": {k2: round(v, 4) for k2, v in base["search"].items()},
-            "search_live_inserts_ms": {k2: round(v, 4) for k2, v in live["search"].items()},
-            "insert_request_ms": {k2: round(v, 4) for k2, v in live["insert"].items()},
-            "p99_ratio_live_vs_idle": round(p99b / p99a, 3) if p99a > 0 else None,
-            "rejected": base["rejected"] + live["rejected"]}
+            "insert_vec_s": INSERT_RATE, "delete_ids_s": DELETE_RATE, "seconds_per_window": seconds,
+            "repeats": repeats,
+            "search_no_inserts_ms": {k2: round(v, 4) for k2, v in s_idle.items()},
+            "search_live_inserts_ms": {k2: round(v, 4) for k2, v in s_live.items()},
+            "insert_request_ms": {k2: round(v, 4) for k2, v in s_ins.items()},
+            "p99_ratio_live_vs_idle": round(s_live["p99_ms"] / s_idle["p99_ms"], 3),
+            "p99_ratio_per_repeat": per_rep,
+            "rearrange_events": rr, "deleted": int(ndel),
+            "rejected": int(sum(x["rejected"] for x in idle + live))}
 
 
 def cpu_baseline_from_snapshot(ix, queries):
@@ -446,35 +560,37 @@ def cpu_baseline_from_snapshot(ix, queries):
     if not O.ref_available():
         return {"unavailable": "oracle/_ref not built"}
     import ctypes as C
-    path = "/tmp/bivf_bench_snapshot.bivf"
     t = time.time()
-    ix.save(path)
-    ref = O.RefIndex.load(path, BLOCK)
-    os.remove(path)
+    ix.save(SNAPSHOT)
+    ref = O.RefIndex.load(SNAPSHOT, BLOCK)
+    os.remove(SNAPSHOT)
     log(f"snapshot -> reference in {time.time() - t:.1f}s")
     cores = os.cpu_count() or 1
-    sample = queries[:2000]
+    sample = np.ascontiguousarray(queries[:1000])
     L = O.ref_lib()
     secs = C.c_double(0)
     ids = np.empty((len(sample), K), np.int64)
     d = np.empty((len(sample), K), np.float32)
-    rc = L.ref_search_threads(ref._h, np.ascontiguousarray(sample), len(sample), K, NPROBE, cores,
+    rc = L.ref_search_threads(ref._h, sample, len(sample), K, NPROBE, cores,
                               1, ids.ctypes.data, d.ctypes.data, C.byref(secs))
     if rc != 0:
         return {"unavailable": L.ref_last_error().decode()}
     qps = len(sample) / secs.value
     gi, gd, _ = ix.search_batch(sample, K, NPROBE)
     same = bool(np.array_equal(gi, ids) and np.array_equal(gd.view(np.uint32), d.view(np.uint32)))
+    del ref
     return {"value": round(qps, 1), "unit": "queries/s", "cores": cores, "kind": "reference",
             "sample": f"{len(sample)} queries of the same batch, nprobe={NPROBE}, k={K}, "
-                      f"reference ClusterIndex loaded from this index's BIVFSNAP snapshot",
+                      f"reference ClusterIndex loaded from this index's BIVFSNAP snapshot "
+                      f"(after the live inserts/deletes)",
             "results_identical_to_gpu": same}
 
 
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args, dist):
     """The reference's own CPU implementation (oracle/_ref, compiled from
-    /root/reference/proj/src) on the host cores, same workload, bounded sample."""
+    /root/reference/proj/src) on the host cores, on the same index and workload
+    (bounded query sample per step)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import ctypes as C
 
@@ -486,22 +602,38 @@ def run_reference(args, dist):
     L = O.ref_lib()
     base, queries, pool = make_data(O.ref_synthetic_dataset)
     cores = os.cpu_count() or 1
-    train_n, iters = 50_000, 2
+    # untimed setup: the identical index, built on the GPU, handed over as BIVFSNAP
     t = time.time()
-    ref = O.RefIndex.train(base[:train_n], NLIST, block_capacity=BLOCK, rearrange_threshold=256,
-                           num_blocks=(N_BASE + N_INSERT) // BLOCK + 2 * NLIST + 64,
-                           kmeans_iters=iters, seed=42)
-    log(f"reference kmeans ({train_n} rows, {iters} iters) {time.time() - t:.1f}s")
-    t = time.time()
-    rest = np.ascontiguousarray(base[train_n:])
-    if L.ref_insert_threads(ref._h, rest, len(rest), cores, 1024) != 0:
-        raise RuntimeError(L.ref_last_error().decode())
-    log(f"reference loaded {ref.size} vectors in {time.time() - t:.1f}s ({cores} threads)")
+    try:
+        import paper_2408_02937_b200 as bivf
+        if bivf.device_count() < 1:
+            raise RuntimeError("no CUDA device")
+        ix, ins_pool = build_index(base, pool, 0)
+        ix.save(SNAPSHOT)
+        ix.close()
+        build = "GPU build (bit-identical to the reference's offline build) -> BIVFSNAP -> ClusterIndex::load"
+    except Exception as e:  # no GPU: the reference trains itself on a bounded sample
+        log(f"GPU build unavailable ({e}); reference k-means on a bounded sample")
+        ref0 = O.RefIndex.train(base[:50_000], NLIST, block_capacity=BLOCK,
+                                rearrange_threshold=REARRANGE_T,
+                                num_blocks=N_POOL // BLOCK + 2 * NLIST + 64, kmeans_iters=2, seed=42)
+        if L.ref_insert_threads(ref0._h, np.ascontiguousarray(base[50_000:]), N_BASE - 50_000, cores,
+                                1024) != 0:
+            raise RuntimeError(L.ref_last_error().decode())
+        ref0.save(SNAPSHOT)
+        del ref0
+        ins_pool = pool
+        build = "reference k-means on 50K rows x 2 iters + threaded inserts (no GPU on this host)"
+    del base, pool
+    ref = O.RefIndex.load(SNAPSHOT, BLOCK)
+    os.remove(SNAPSHOT)
+    log(f"reference index ready in {time.time() - t:.1f}s ({build})")
     sample = np.ascontiguousarray(queries[:args.ref_sample])
 
     def insert_fn(x):
         ref.insert(x)
-        L.ref_rearrange_sweep(ref._h)
+        L.ref_rearrange_sweep(ref._h)  # post_insert_maintenance (executor.cpp:380)
+        return len(x)
 
     def step():
         secs = C.c_double(0)
@@ -511,7 +643,8 @@ def run_reference(args, dist):
             raise RuntimeError(L.ref_last_error().decode())
         return secs.value
 
-    ins = Inserter(insert_fn, pool)
+    half = len(ins_pool) // 2
+    ins = Paced(insert_fn, ins_pool[:half], INSERT_RATE, INSERT_BATCH)
     ins.start()
     for _ in range(args.warmup):
         step()
@@ -523,22 +656,24 @@ def run_reference(args, dist):
     lat = None
     if not args.no_latency:
         lat = ref_latency_phase(L, ref, np.ascontiguousarray(queries[:2000]),
-                                np.ascontiguousarray(pool[len(pool) // 2:]))
+                                np.ascontiguousarray(ins_pool[half:]))
     return {
         "metric": METRIC, "value": round(qps, 1), "unit": "queries/s", "n_gpus": dist["world"],
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (reference generator dataset.cpp:92-112, SIFT-like rounding)",
+        "data": "synthetic (reference generator dataset.cpp:92-112, 256 components, SIFT-like rounding)",
         "config": {"workload": WORKLOAD, "n_base": N_BASE, "dim": DIM, "nlist": NLIST,
                    "nprobe": NPROBE, "k": K, "batch": len(sample), "block_capacity": BLOCK,
-                   "insert_rate_vec_s": INSERT_RATE,
-                   "training": f"reference kmeans on {train_n} rows, {iters} iters (bounded)"},
+                   "rearrange_threshold": REARRANGE_T, "insert_rate_vec_s": INSERT_RATE,
+                   "delete_rate_ids_s": 0.0, "insert_order": f"zipf s={ZIPF_S}",
+                   "index": build, "same_index_as_gpu_arm": build.startswith("GPU build")},
         "impl": "reference",
         "live_inserts": ins_stats,
         "cpu_baseline": {"value": round(qps, 1), "unit": "queries/s", "cores": cores,
                          "kind": "reference",
-                         "sample": f"{len(sample)} queries per step, {cores} threads"},
+                         "sample": f"{len(sample)} queries per step, {cores} threads, reference "
+                                   f"ClusterIndex::search (no delete: the reference has none)"},
         "e2e": {"value": round(qps, 1), "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "latency": lat,
@@ -547,15 +682,16 @@ def run_reference(args, dist):
 
 def ref_latency_phase(L, ref, queries, inserts):
     """The reference Executor (32 lanes) under the same open-loop load; the
-    request rate is scaled down when the CPU cannot sustain it."""
+    request rate is scaled down to what the host cores can serve."""
     import ctypes as C
 
     from paper_2408_02937_b200.executor import summarize_latencies
     out = {}
-    qps = 50.0  # 10-query requests / s: what the host can serve without saturating
+    qps = 50.0  # 10-query requests / s
+    seconds = 4.0
     for name, irate in (("search_no_inserts_ms", 0.0), ("search_live_inserts_ms", INSERT_RATE)):
         ex = L.ref_exec_create(ref._h, 32, 0)
-        nreq = int(qps * LAT_SECONDS)
+        nreq = int(qps * seconds)
         lat = np.zeros(nreq, np.float64)
         rej = C.c_uint64(0)
         rc = L.ref_exec_replay_dim(ex, DIM, queries, nreq, 10, K, NPROBE, qps, inserts,
@@ -623,6 +759,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--lat-seconds", type=float, default=10.0)
+    ap.add_argument("--lat-repeats", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
