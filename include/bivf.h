@@ -153,6 +153,11 @@ bivf_status bivf_take_rearrange_events(bivf_index* h, double* out5, uint64_t cap
 /* ---- introspection (ivf_index.hpp:84-103, block_store.hpp:75-132) -------- */
 bivf_status bivf_size(const bivf_index* h, uint64_t* out);
 bivf_status bivf_scalars_copied(const bivf_index* h, uint64_t* out);
+/* maintenance operations (delete / rearrangement batches) that ran as
+ * read-copy-update (searches never wait) and that fell back to quiescence
+ * (oversized: more blocks than the scratch area, no free offline region) */
+bivf_status bivf_cow_ops(const bivf_index* h, uint64_t* out);
+bivf_status bivf_quiescent_ops(const bivf_index* h, uint64_t* out);
 bivf_status bivf_list_length(const bivf_index* h, uint32_t cluster, uint64_t* out);
 bivf_status bivf_offline_count(const bivf_index* h, uint32_t cluster, uint64_t* out);
 bivf_status bivf_hop_count(const bivf_index* h, uint32_t cluster, uint64_t* out);

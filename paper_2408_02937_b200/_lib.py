@@ -148,6 +148,8 @@ SIGNATURES = {
     "bivf_size": (C.c_int, [vp, pu64]),
     "bivf_scalars_copied": (C.c_int, [vp, pu64]),
     "bivf_reallocations": (C.c_int, [vp, pu64]),
+    "bivf_cow_ops": (C.c_int, [vp, pu64]),
+    "bivf_quiescent_ops": (C.c_int, [vp, pu64]),
     "bivf_extend_copy": (C.c_int, [vp, vp, u64, vp, vp, pu64]),
     "bivf_list_length": (C.c_int, [vp, u32, pu64]),
     "bivf_offline_count": (C.c_int, [vp, u32, pu64]),

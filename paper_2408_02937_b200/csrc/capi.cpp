@@ -300,6 +300,8 @@ bivf_status bivf_take_rearrange_events(bivf_index* h, double* out5, uint64_t cap
 BIVF_GETTER(bivf_size, I(h).size())
 BIVF_GETTER(bivf_scalars_copied, I(h).scalars_copied())
 BIVF_GETTER(bivf_reallocations, I(h).reallocations())
+BIVF_GETTER(bivf_cow_ops, I(h).cow_ops())
+BIVF_GETTER(bivf_quiescent_ops, I(h).quiescent_ops())
 BIVF_GETTER(bivf_allocated_blocks, I(h).allocated_blocks())
 #undef BIVF_GETTER
 

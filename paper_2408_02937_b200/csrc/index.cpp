@@ -10,6 +10,7 @@
 #include <deque>
 #include <fstream>
 #include <sstream>
+#include <set>
 #include <unordered_map>
 
 #include "launches.h"
@@ -170,7 +171,15 @@ GpuIndex::GpuIndex(const bivf_config& in) : cfg_(normalized(in)) {
     gpb_ = ceil_div(T_, 32);
     PS_ = (uint64_t)gpb_ * 32u * D_;
     NB_ = (uint32_t)cfg_.num_blocks;
-    MLB_ = std::min<uint32_t>(cfg_.max_list_blocks, NB_);
+    // block-table rows start small and grow on demand (grow_rows) up to the
+    // configured cap (default: the pool size, i.e. never an insert failure)
+    MLB_cap_ = std::max<uint32_t>(1, std::min<uint32_t>(cfg_.max_list_blocks, NB_));
+    MLB_ = std::min<uint32_t>(MLB_cap_, std::max<uint32_t>(8, 2 * ceil_div(NB_, C_)));
+    {
+        const char* v = std::getenv("BIVF_COW");
+        cow_on_ = !(v && std::string(v) == "0");
+        NS_ = cow_on_ ? std::min<uint32_t>(256, std::max<uint32_t>(16, NB_ / 8)) : 0;
+    }
     device_ = cfg_.device;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -193,6 +202,7 @@ GpuIndex::GpuIndex(const bivf_config& in) : cfg_(normalized(in)) {
         BIVF_CUDA(cudaStreamCreateWithPriority(&data_stream_, cudaStreamNonBlocking, lo));
         data_lease_.stream = data_stream_;
     }
+    h_sel_.assign(C_, 0);
     alloc_device();
     BIVF_CUDA(cudaEventCreateWithFlags(&maint_evt_, cudaEventDisableTiming));
     for (uint32_t i = 0; i < cfg_.num_leases; ++i) {
@@ -248,26 +258,28 @@ void GpuIndex::alloc_device() {
         tc_ok_ = mir_on_;
     }
     ensure_offline_capacity(32);
-    d_arena_.alloc((size_t)NB_ * PS_ * 4);
+    // the pool's blocks, then NS_ scratch blocks (copy-on-write maintenance)
+    const uint64_t NBS = (uint64_t)NB_ + NS_;
+    d_arena_.alloc((size_t)NBS * PS_ * 4);
     BIVF_CUDA(dset(d_arena_.p, 0, d_arena_.bytes));
     if (mir_on_) {
-        d_arena_mir_.alloc((size_t)NB_ * MPS_ * 4);
+        d_arena_mir_.alloc((size_t)NBS * MPS_ * 4);
         BIVF_CUDA(dset(d_arena_mir_.p, 0, d_arena_mir_.bytes));
-        d_arena_nrm_.alloc((size_t)NB_ * gpb_ * kNormFloats * 4);
+        d_arena_nrm_.alloc((size_t)NBS * gpb_ * kNormFloats * 4);
         BIVF_CUDA(dset(d_arena_nrm_.p, 0, d_arena_nrm_.bytes));
         // the slot-major row copy feeds the L2 refine's gathers; the inner-product
         // (wide, D <= 768) refine reads the interleaved payload instead: at D = 768
         // a second copy of the payload would not fit next to it in HBM
         if (cfg_.metric != BIVF_METRIC_IP) {
-            d_arena_rows_.alloc((size_t)NB_ * PS_ * 4);
+            d_arena_rows_.alloc((size_t)NBS * PS_ * 4);
             BIVF_CUDA(dset(d_arena_rows_.p, 0, d_arena_rows_.bytes));
         }
-        tc_ok_ = make_mirror_map(d_arena_mir_.as<float>(), (uint64_t)NB_ * gpb_, D_, cfg_.metric == BIVF_METRIC_IP,
+        tc_ok_ = make_mirror_map(d_arena_mir_.as<float>(), NBS * gpb_, D_, cfg_.metric == BIVF_METRIC_IP,
                                  &map_arena_) ==
                  cudaSuccess;
     }
     mirror_ = mirror_view();
-    d_bids_.alloc((size_t)NB_ * T_ * 8);
+    d_bids_.alloc((size_t)NBS * T_ * 8);
     BIVF_CUDA(dset(d_bids_.p, 0xff, d_bids_.bytes));
     d_owner_.alloc((size_t)NB_ * 4);
     BIVF_CUDA(dset(d_owner_.p, 0xff, d_owner_.bytes));
@@ -276,11 +288,19 @@ void GpuIndex::alloc_device() {
     d_len_.alloc((size_t)C_ * 4);
     d_nblocks_.alloc((size_t)C_ * 4);
     d_fail_.alloc((size_t)C_);
-    d_table_.alloc((size_t)C_ * MLB_ * 4);
     BIVF_CUDA(dset(d_len_.p, 0, d_len_.bytes));
     BIVF_CUDA(dset(d_nblocks_.p, 0, d_nblocks_.bytes));
     BIVF_CUDA(dset(d_fail_.p, 0, d_fail_.bytes));
-    BIVF_CUDA(dset(d_table_.p, 0xff, d_table_.bytes));
+    d_rows_.alloc((size_t)2 * C_ * MLB_ * 4);
+    BIVF_CUDA(dset(d_rows_.p, 0xff, d_rows_.bytes));
+    d_ver_.alloc((size_t)C_ * 4);
+    BIVF_CUDA(dset(d_ver_.p, 0, d_ver_.bytes));
+    d_rowptr_.alloc((size_t)C_ * 8);
+    {
+        std::vector<uint64_t> rp(C_);
+        for (uint32_t c = 0; c < C_; ++c) rp[c] = row_addr(c, 0);
+        BIVF_CUDA(h2d(d_rowptr_.p, rp.data(), rp.size() * 8));
+    }
     if (const char* m = std::getenv("BIVF_SCAN")) {
         if (std::string(m) == "cuda") scan_mode_ = 1;
         if (std::string(m) == "tc") scan_mode_ = 2;
@@ -295,6 +315,7 @@ void GpuIndex::alloc_device() {
 void GpuIndex::ensure_offline_capacity(uint64_t slots) {
     slots = std::max<uint64_t>(32, (slots + 31) / 32 * 32);
     if (slots <= off_slots_cap_) return;
+    ++gen_;  // cached search graphs embed the old buffers and TMA extents
     d_off_pay_.alloc((size_t)slots * D_ * 4);
     d_off_ids_.alloc((size_t)slots * 8);
     BIVF_CUDA(dset(d_off_pay_.p, 0, d_off_pay_.bytes));
@@ -394,12 +415,13 @@ void GpuIndex::build_quantizer_mirror(const float* c) {
     for (size_t i = 0; i < ids.size(); ++i) ids[i] = i < C_ ? (long long)i : -1;
     d_q_ids_.alloc(ids.size() * 8);
     BIVF_CUDA(h2d(d_q_ids_.p, ids.data(), ids.size() * 8));
-    // meta: off_start u64[1] = 0 | off_count u32[1] = C | len u32[1] = 0 | table i32[1] = -1
+    // meta: off_start u64 = 0 | off_count u32 = C | len u32 = 0 | rowptr u64 = 0 | ver u32 = 0
     struct {
         uint64_t off_start;
         uint32_t off_count, len;
-        int32_t table, pad;
-    } meta{0, C_, 0, -1, 0};
+        uint64_t rowptr;
+        uint32_t ver, pad;
+    } meta{0, C_, 0, 0, 0, 0};
     d_q_meta_.alloc(sizeof(meta));
     BIVF_CUDA(h2d(d_q_meta_.p, &meta, sizeof(meta)));
     d_q_zero_.alloc((size_t)65536 * 8);
@@ -452,14 +474,14 @@ DevLists GpuIndex::quantizer_lists() const {
     L.T = 32;
     L.gpb = 1;
     L.PS = (uint64_t)32 * D_;
-    L.MLB = 1;
     char* m = d_q_meta_.as<char>();
     L.off_payload = d_cent_il_.as<float>();
     L.off_ids = d_q_ids_.as<long long>();
     L.off_start = reinterpret_cast<const uint64_t*>(m);
     L.off_count = reinterpret_cast<const uint32_t*>(m + 8);
     L.len = reinterpret_cast<const uint32_t*>(m + 12);
-    L.table = reinterpret_cast<const int32_t*>(m + 16);
+    L.rowptr = reinterpret_cast<const int32_t* const*>(m + 16);
+    L.ver = reinterpret_cast<const uint32_t*>(m + 24);
     L.arena = nullptr;
     L.bids = nullptr;
     return L;
@@ -522,15 +544,15 @@ DevLists GpuIndex::dev_lists() const {
     L.T = T_;
     L.gpb = gpb_;
     L.PS = PS_;
-    L.MLB = MLB_;
     L.off_payload = d_off_pay_.as<float>();
     L.off_ids = d_off_ids_.as<long long>();
     L.off_start = d_off_start_.as<uint64_t>();
     L.off_count = d_off_count_.as<uint32_t>();
     L.arena = d_arena_.as<float>();
     L.bids = d_bids_.as<long long>();
-    L.table = d_table_.as<int32_t>();
+    L.rowptr = d_rowptr_.as<const int32_t* const>();
     L.len = d_len_.as<uint32_t>();
+    L.ver = d_ver_.as<uint32_t>();
     return L;
 }
 
@@ -549,7 +571,7 @@ InsertState GpuIndex::insert_state() {
     S.len = d_len_.as<uint32_t>();
     S.nblocks = d_nblocks_.as<uint32_t>();
     S.fail = d_fail_.as<uint8_t>();
-    S.table = d_table_.as<int32_t>();
+    S.rowptr = d_rowptr_.as<int32_t* const>();
     S.run = d_run_.as<uint32_t>();
     S.fail_from = d_failfrom_.as<uint32_t>();
     S.newlen = d_newlen_.as<uint32_t>();
@@ -569,6 +591,16 @@ void GpuIndex::upload_centroids() {
 void GpuIndex::set_centroids(const float* c) {
     std::lock_guard<std::mutex> lk(data_mu_);
     BIVF_CUDA(cudaSetDevice(device_));
+    // centroids, the quantizer mirror and the residual mirror change under the
+    // data: searches are quiesced
+    std::unique_lock<std::shared_mutex> gx(gate_);
+    begin_maintenance();
+    BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+    struct End {
+        GpuIndex* g;
+        ~End() { g->end_maintenance(); }
+    } end_guard{this};
+    ++gen_;
     BIVF_CUDA(h2d(d_cent_.p, c, (size_t)C_ * D_ * 4));
     upload_centroids();
     build_quantizer_mirror(c);
@@ -605,6 +637,14 @@ void GpuIndex::bulk_load(const float* x, uint64_t n, const uint32_t* assignment,
     }
     std::lock_guard<std::mutex> lk(data_mu_);
     BIVF_CUDA(cudaSetDevice(device_));
+    // a bulk load rewrites the offline area in place: searches are quiesced
+    std::unique_lock<std::shared_mutex> gx(gate_);
+    begin_maintenance();
+    BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+    struct End {
+        GpuIndex* g;
+        ~End() { g->end_maintenance(); }
+    } end_guard{this};
     // ivf_index.cpp:61-82: per-cluster counts; rows appended in ascending row
     // order; each segment padded to whole groups.
     std::vector<uint64_t> counts(C_, 0);
@@ -614,13 +654,24 @@ void GpuIndex::bulk_load(const float* x, uint64_t n, const uint32_t* assignment,
     }
     for (uint32_t c = 0; c < C_; ++c)
         if (counts[c] > 0xffffffffull) throw Error(BIVF_EINVAL, "bulk_load: list too long");
-    uint64_t total = 0;
+    uint64_t total = 0, maxseg = 0;
     for (uint32_t c = 0; c < C_; ++c) {
         h_off_start_[c] = total;
         total += (counts[c] + 31) / 32 * 32;
+        maxseg = std::max<uint64_t>(maxseg, (counts[c] + 31) / 32 * 32);
     }
-    ensure_offline_capacity(total);
+    // free space beside the segments: a delete writes a segment's new version
+    // there and frees the old one after a grace period (copy-on-write)
+    const uint64_t slack = cow_on_ ? std::max<uint64_t>(total / 8, 64 * maxseg) : 0;
+    ensure_offline_capacity(total + slack);
     BIVF_CUDA(dset(d_off_ids_.p, 0xff, d_off_ids_.bytes));
+    off_region_.clear();
+    off_free_.clear();
+    off_pending_.clear();
+    for (uint32_t c = 0; c < C_; ++c)
+        if (counts[c]) off_region_[h_off_start_[c]] = {c, (counts[c] + 31) / 32 * 32};
+    off_free_add(total, off_slots_cap_ - total);
+    copy_backend_ = false;
     std::vector<uint64_t> fill(C_, 0);
     const uint64_t chunk = 1ull << 20;
     DevBuf dx, ddest, dids, dasg;
@@ -689,6 +740,7 @@ void GpuIndex::grow_offline_preserving(uint64_t slots) {
         std::swap(b.p, nb.p);
         std::swap(b.bytes, nb.bytes);
     };
+    ++gen_;
     regrow(d_off_pay_, (size_t)cap * D_ * 4, 0);
     regrow(d_off_ids_, (size_t)cap * 8, 0xff);
     if (mir_on_) {
@@ -709,9 +761,19 @@ uint64_t GpuIndex::extend_copy(const float* x, uint64_t n, const int64_t* ids, i
     std::vector<uint32_t> asg(n);
     assign(x, n, asg.data());  // ivf assign, lowest cluster id on ties (ivf_index.cpp:93-105)
     // the baseline's extend excludes searches (baseline_index.cpp:66, :113 share one mutex)
+    std::lock_guard<std::mutex> lk(data_mu_);  // lock order: data_mu_, then gate_
     std::unique_lock<std::shared_mutex> gx(gate_);
-    std::lock_guard<std::mutex> lk(data_mu_);
     BIVF_CUDA(cudaSetDevice(device_));
+    begin_maintenance();
+    BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+    struct End {
+        GpuIndex* g;
+        ~End() { g->end_maintenance(); }
+    } end_guard{this};
+    // the copy-based backend owns the offline area from here on (no free-space
+    // bookkeeping; deletes take the quiescent path)
+    copy_backend_ = true;
+    off_free_.clear();
     // bucket the batch per cluster, batch order inside a bucket
     std::vector<std::vector<uint64_t>> buckets(C_);
     for (uint64_t i = 0; i < n; ++i) buckets[asg[i]].push_back(i);
@@ -766,6 +828,12 @@ uint64_t GpuIndex::extend_copy(const float* x, uint64_t n, const int64_t* ids, i
         }
         reallocations_ += 1;
         scalars_copied_ += (old_n + add_n) * D_;
+        // the abandoned region keeps no live ids (delete's locate scans the area)
+        if (og) {
+            BIVF_CUDA(cudaMemsetAsync(d_off_ids_.as<long long>() + from, 0xff, og * 32 * 8, data_stream_));
+            off_region_.erase(from);
+        }
+        off_region_[to] = {c, (old_n + add_n + 31) / 32 * 32};
         h_off_start_[c] = to;
         h_off_count_[c] = (uint32_t)(old_n + add_n);
     }
@@ -844,6 +912,7 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     const size_t o_oc = take((size_t)nq * 4);
     const size_t o_ctr = take(16);
     const size_t o_plan = take((size_t)C_ * 4 * 5 + (size_t)(C_ + 1) * 4 * 2 + 16);
+    const size_t o_snap = take((size_t)C_ * 8 * 2);  // snap_start, snap_row
     // TC scan: one run per (pair, chunk, warpgroup); the TC quantizer reuses the
     // same buffers (nq pairs, quantizer_maxch chunks, P upper bounds per run)
     const size_t qruns = (size_t)nq * quantizer_maxch(nq) * 2;
@@ -889,6 +958,8 @@ Workspace GpuIndex::carve(Lease& l, uint32_t nq, uint32_t k, uint32_t P, uint32_
     w.plan.item_off = pl + 6 * C_ + 1;
     w.plan.n_items = pl + 7 * C_ + 2;
     w.plan.item_ctr = pl + 7 * C_ + 3;
+    w.plan.snap_start = reinterpret_cast<uint64_t*>(b + o_snap);
+    w.plan.snap_row = w.plan.snap_start + C_;
     w.tc.ub = reinterpret_cast<float*>(b + o_ub);
     w.tc.ccount = reinterpret_cast<uint32_t*>(b + o_cc);
     w.tc.clb = reinterpret_cast<float*>(b + o_clb);
@@ -978,6 +1049,7 @@ uint64_t GpuIndex::graph_sig() const {
         mix(reinterpret_cast<uintptr_t>(b->p));
     mix((uint64_t)scan_mode_);
     mix((uint64_t)tc_ok_ | (uint64_t)q_tc_ok_ << 1 | (uint64_t)mir_on_ << 2);
+    mix(gen_.load());  // reallocations and centroid changes (buffer addresses can repeat)
     return h;
 }
 
@@ -1395,6 +1467,10 @@ uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_
                                        num_sms_, st));
         }
         BIVF_CUDA(launch_make_asg(nearest, d_ids_.as<long long>(), m, d_asg_.as<uint32_t>(), st));
+        // block-table rows with room for every block this chunk can open in one list
+        uint32_t mxb = 0;
+        for (uint32_t c = 0; c < C_; ++c) mxb = std::max(mxb, h_nblocks_[c]);
+        grow_rows(mxb + ceil_div(m, T_) + 1);
         const uint32_t cursor_old = h_cursor_;
         BIVF_CUDA(launch_insert(insert_state(), m, d_x_.as<float>(), d_ids_.as<long long>(),
                                 d_asg_.as<uint32_t>(), d_blk_.as<int32_t>(),
@@ -1443,6 +1519,184 @@ void GpuIndex::end_maintenance() {
 }
 
 // ========================================================================
+// read-copy-update maintenance (see index.h)
+// ========================================================================
+
+// Grace period.  (1) Everything enqueued on the data stream so far (the
+// publishes) has landed on the device.  (2) With gate_ held exclusively no
+// search is mid-enqueue, so every search either recorded its lease's `done`
+// event already — the data stream waits on it, on the device — or will be
+// enqueued after the publishes landed and so plans against the new state.
+// Work enqueued on the data stream after this call may reuse whatever the
+// old state referenced.  The host never waits for searches.
+void GpuIndex::grace() {
+    BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+    {
+        std::unique_lock<std::shared_mutex> g(gate_);
+        std::lock_guard<std::mutex> lk(lease_mu_);
+        for (auto& l : leases_)
+            if (l->done) BIVF_CUDA(cudaStreamWaitEvent(data_stream_, l->done, 0));
+    }
+    // offline regions retired before the grace: clear their ids (locate must
+    // not find stale copies), then they are free (data-stream order)
+    for (auto& r : off_pending_) {
+        BIVF_CUDA(cudaMemsetAsync(d_off_ids_.as<long long>() + r.first, 0xff, r.second * 8,
+                                  data_stream_));
+        off_free_add(r.first, r.second);
+    }
+    off_pending_.clear();
+    grace_pending_ = false;
+}
+
+uint64_t GpuIndex::row_addr(uint32_t c, uint32_t sel) const {
+    return reinterpret_cast<uint64_t>(d_rows_.as<int32_t>() + ((size_t)sel * C_ + c) * MLB_);
+}
+
+GpuIndex::ListPub GpuIndex::current_pub(uint32_t c) const {
+    return ListPub{c, h_off_start_[c], h_off_count_[c], row_addr(c, h_sel_[c]), h_len_[c]};
+}
+
+// One seqlocked publish of whole list states on the data stream (maint.cu).
+void GpuIndex::publish(const std::vector<ListPub>& pubs) {
+    const size_t n = pubs.size();
+    if (!n) return;
+    const size_t o_idx = 0, o_start = align_up(n * 4, 16), o_count = o_start + align_up(n * 8, 16),
+                 o_row = o_count + align_up(n * 4, 16), o_len = o_row + align_up(n * 8, 16),
+                 total = o_len + align_up(n * 4, 16);
+    h_pub_.ensure(total);
+    s_pub_.ensure(total);
+    char* h = h_pub_.as<char>();
+    for (size_t i = 0; i < n; ++i) {
+        reinterpret_cast<uint32_t*>(h + o_idx)[i] = pubs[i].c;
+        reinterpret_cast<uint64_t*>(h + o_start)[i] = pubs[i].start;
+        reinterpret_cast<uint32_t*>(h + o_count)[i] = pubs[i].count;
+        reinterpret_cast<uint64_t*>(h + o_row)[i] = pubs[i].row;
+        reinterpret_cast<uint32_t*>(h + o_len)[i] = pubs[i].len;
+    }
+    char* d = s_pub_.as<char>();
+    BIVF_CUDA(h2d(d, h, total));
+    BIVF_CUDA(launch_publish_lists((uint32_t)n, reinterpret_cast<uint32_t*>(d + o_idx),
+                                   reinterpret_cast<uint64_t*>(d + o_start),
+                                   reinterpret_cast<uint32_t*>(d + o_count),
+                                   reinterpret_cast<uint64_t*>(d + o_row),
+                                   reinterpret_cast<uint32_t*>(d + o_len), d_off_start_.as<uint64_t>(),
+                                   d_off_count_.as<uint32_t>(), d_rowptr_.as<uint64_t>(),
+                                   d_len_.as<uint32_t>(), d_ver_.as<uint32_t>(), data_stream_));
+}
+
+// rows[i] (-1 padded to MLB_) -> copy sel[i] of list lists[i]'s row.
+void GpuIndex::write_rows(const std::vector<uint32_t>& lists,
+                          const std::vector<std::vector<int32_t>>& rows,
+                          const std::vector<uint8_t>& sel) {
+    if (lists.empty()) return;
+    std::vector<int32_t> flat((size_t)lists.size() * MLB_, -1);
+    for (size_t i = 0; i < lists.size(); ++i) {
+        if (rows[i].size() > MLB_) throw Error(BIVF_ECORRUPT, "block-table row above capacity");
+        std::copy(rows[i].begin(), rows[i].end(), flat.begin() + i * MLB_);
+    }
+    DevBuf& tmp = s_rows_;
+    tmp.ensure(flat.size() * 4);
+    BIVF_CUDA(h2d(tmp.p, flat.data(), flat.size() * 4));
+    for (size_t i = 0; i < lists.size(); ++i)
+        BIVF_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(row_addr(lists[i], sel[i])),
+                                  tmp.as<int32_t>() + i * MLB_, (size_t)MLB_ * 4,
+                                  cudaMemcpyDeviceToDevice, data_stream_));
+    BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+}
+
+// Row capacity >= need (<= MLB_cap_): a new double-buffered row array filled
+// from the host mirror, every list republished on copy 0; searches that
+// snapshotted the old array keep reading it (retired, never written again).
+void GpuIndex::grow_rows(uint32_t need) {
+    need = std::min(need, MLB_cap_);
+    if (need <= MLB_) return;
+    const uint32_t nm = std::min(MLB_cap_, std::max(need, 2 * MLB_));
+    auto nb = std::make_unique<DevBuf>();
+    nb->alloc((size_t)2 * C_ * nm * 4);
+    std::vector<int32_t> flat((size_t)C_ * nm, -1);
+    for (uint32_t c = 0; c < C_; ++c)
+        std::copy(h_blocks_[c].begin(), h_blocks_[c].end(), flat.begin() + (size_t)c * nm);
+    BIVF_CUDA(h2d(nb->p, flat.data(), flat.size() * 4));
+    BIVF_CUDA(dset(static_cast<int32_t*>(nb->p) + (size_t)C_ * nm, 0xff, (size_t)C_ * nm * 4));
+    auto old = std::make_unique<DevBuf>();
+    std::swap(old->p, d_rows_.p);
+    std::swap(old->bytes, d_rows_.bytes);
+    std::swap(d_rows_.p, nb->p);
+    std::swap(d_rows_.bytes, nb->bytes);
+    retired_.push_back(std::move(old));
+    MLB_ = nm;
+    std::vector<ListPub> pubs;
+    pubs.reserve(C_);
+    for (uint32_t c = 0; c < C_; ++c) {
+        h_sel_[c] = 0;
+        pubs.push_back(current_pub(c));
+    }
+    publish(pubs);
+    BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+}
+
+// Whole-block copies src[i] -> dst[i] of every per-block array (payload, ids,
+// scan mirror planes, norms, row copy).
+void GpuIndex::copy_block_set(const std::vector<int32_t>& src, const std::vector<int32_t>& dst) {
+    const uint32_t n = (uint32_t)src.size();
+    if (!n) return;
+    DevBuf &ds = s_rr_src_, &dd = s_rr_dst_;
+    ds.ensure((size_t)n * 4);
+    dd.ensure((size_t)n * 4);
+    BIVF_CUDA(cudaMemcpyAsync(ds.p, src.data(), (size_t)n * 4, cudaMemcpyHostToDevice, data_stream_));
+    BIVF_CUDA(cudaMemcpyAsync(dd.p, dst.data(), (size_t)n * 4, cudaMemcpyHostToDevice, data_stream_));
+    cudaStream_t st = data_stream_;
+    BIVF_CUDA(launch_copy_blocks(d_arena_.p, PS_ * 4, ds.as<int32_t>(), dd.as<int32_t>(), n, st));
+    BIVF_CUDA(launch_copy_blocks(d_bids_.p, (uint64_t)T_ * 8, ds.as<int32_t>(), dd.as<int32_t>(), n, st));
+    if (mir_on_) {
+        BIVF_CUDA(launch_copy_blocks(d_arena_mir_.p, MPS_ * 4, ds.as<int32_t>(), dd.as<int32_t>(), n, st));
+        BIVF_CUDA(launch_copy_blocks(d_arena_nrm_.p, (uint64_t)gpb_ * kNormFloats * 4, ds.as<int32_t>(),
+                                     dd.as<int32_t>(), n, st));
+        if (d_arena_rows_.p)
+            BIVF_CUDA(launch_copy_blocks(d_arena_rows_.p, PS_ * 4, ds.as<int32_t>(), dd.as<int32_t>(), n, st));
+    }
+    BIVF_CUDA(cudaStreamSynchronize(st));  // the pageable src/dst vectors
+}
+
+uint64_t GpuIndex::off_alloc(uint64_t slots) {
+    slots = std::max<uint64_t>(32, (slots + 31) / 32 * 32);
+    for (auto it = off_free_.begin(); it != off_free_.end(); ++it) {
+        if (it->second < slots) continue;
+        const uint64_t st = it->first, len = it->second;
+        off_free_.erase(it);
+        if (len > slots) off_free_[st + slots] = len - slots;
+        return st;
+    }
+    return ~0ull;
+}
+
+void GpuIndex::off_free_add(uint64_t start, uint64_t slots) {
+    if (!slots) return;
+    auto it = off_free_.emplace(start, slots).first;
+    auto nx = std::next(it);
+    if (nx != off_free_.end() && it->first + it->second == nx->first) {
+        it->second += nx->second;
+        off_free_.erase(nx);
+    }
+    if (it != off_free_.begin()) {
+        auto pv = std::prev(it);
+        if (pv->first + pv->second == it->first) {
+            pv->second += it->second;
+            off_free_.erase(it);
+        }
+    }
+}
+
+uint32_t GpuIndex::off_owner(uint64_t slot) const {
+    auto it = off_region_.upper_bound(slot);
+    if (it == off_region_.begin()) throw Error(BIVF_ECORRUPT, "delete: offline slot outside every segment");
+    --it;
+    if (slot >= it->first + it->second.second)
+        throw Error(BIVF_ECORRUPT, "delete: offline slot outside every segment");
+    return it->second.first;
+}
+
+// ========================================================================
 // delete (extension)
 // ========================================================================
 
@@ -1453,6 +1707,7 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
     std::lock_guard<std::mutex> lk(data_mu_);
     BIVF_CUDA(cudaSetDevice(device_));
     cudaStream_t st = data_stream_;
+    reclaim();  // retired offline regions: ids cleared before the locate below
     // request hash (first occurrence of each id)
     uint32_t hcap = 64;
     while (hcap < 2 * n) hcap <<= 1;
@@ -1482,10 +1737,8 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
     BIVF_CUDA(cudaMemcpyAsync(dk.p, hk.data(), hcap * 8, cudaMemcpyHostToDevice, st));
     BIVF_CUDA(cudaMemcpyAsync(dv.p, hv.data(), hcap * 4, cudaMemcpyHostToDevice, st));
     BIVF_CUDA(cudaMemsetAsync(dloc.p, 0xff, n * 8, st));
-    uint64_t off_total = 0;
-    for (uint32_t c = 0; c < C_; ++c)
-        off_total = std::max<uint64_t>(off_total, h_off_start_[c] + (h_off_count_[c] + 31) / 32 * 32);
-    BIVF_CUDA(launch_locate(d_off_ids_.as<long long>(), off_total, false, dk.as<long long>(),
+    // every offline slot outside a live segment holds id -1 (bulk_load, grace)
+    BIVF_CUDA(launch_locate(d_off_ids_.as<long long>(), off_slots_cap_, false, dk.as<long long>(),
                             dv.as<uint32_t>(), hcap - 1, dloc.as<uint64_t>(), st));
     BIVF_CUDA(launch_locate(d_bids_.as<long long>(), (uint64_t)h_cursor_ * T_, true,
                             dk.as<long long>(), dv.as<uint32_t>(), hcap - 1, dloc.as<uint64_t>(), st));
@@ -1501,7 +1754,7 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
         std::unordered_map<uint64_t, uint64_t> content;  // pos -> original pos
         std::unordered_map<uint64_t, uint64_t> where;    // original pos -> current pos
     };
-    std::unordered_map<uint64_t, Part> parts;
+    std::map<uint64_t, Part> parts;  // ordered: deterministic scratch / region assignment
     auto part_of = [&](uint64_t a, uint64_t& key, uint64_t& pos) {
         if (a & kArenaBit) {
             const uint64_t g = a & ~kArenaBit;
@@ -1510,10 +1763,7 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
             key = 2ull * (uint32_t)c + 1;
             pos = (uint64_t)h_mid_[b] * T_ + slot;
         } else {
-            // last cluster whose (group-aligned) segment starts at or before a;
-            // empty clusters share their start with the next one
-            const auto it = std::upper_bound(h_off_start_.begin(), h_off_start_.end(), a);
-            const uint32_t c = (uint32_t)(it - h_off_start_.begin()) - 1;
+            const uint32_t c = off_owner(a);
             key = 2ull * c;
             pos = a - h_off_start_[c];
         }
@@ -1549,45 +1799,240 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
         ++removed;
     }
     if (removed == 0) return 0;
-    // addresses
-    auto pay_addr = [&](uint64_t key, uint64_t pos) -> uint64_t {
-        const uint32_t c = (uint32_t)(key / 2);
-        if (key & 1) {
-            const int32_t b = h_blocks_[c][pos / T_];
-            const uint32_t slot = (uint32_t)(pos % T_);
-            return kArenaBit | ((uint64_t)b * PS_ + (uint64_t)(slot / 32) * 32 * D_ + slot % 32);
-        }
-        const uint64_t s = h_off_start_[c] + pos;
+    // slot addresses (maint.cuh): payload float offset / id index, arena bit 63
+    auto pay_at = [&](bool arena, uint64_t blk_or_start, uint64_t slot) -> uint64_t {
+        if (arena)
+            return kArenaBit | (blk_or_start * PS_ + (slot / 32) * 32 * D_ + slot % 32);
+        const uint64_t s = blk_or_start + slot;
         return (s / 32) * 32 * D_ + s % 32;
     };
-    auto id_addr = [&](uint64_t key, uint64_t pos) -> uint64_t {
-        const uint32_t c = (uint32_t)(key / 2);
-        if (key & 1) {
-            const int32_t b = h_blocks_[c][pos / T_];
-            return kArenaBit | ((uint64_t)b * T_ + pos % T_);
-        }
-        return h_off_start_[c] + pos;
+    auto id_at = [&](bool arena, uint64_t blk_or_start, uint64_t slot) -> uint64_t {
+        return arena ? kArenaBit | (blk_or_start * T_ + slot) : blk_or_start + slot;
     };
-    std::vector<uint64_t> msrc_p, mdst_p, msrc_i, mdst_i, clear;
+    std::vector<uint64_t> msrc_p, mdst_p, msrc_i, mdst_i, clear, pa, ia;
+    // stream-ordered on the data stream; the address vectors outlive the copies
+    auto apply_moves = [&]() {
+        const uint32_t nm = (uint32_t)msrc_p.size();
+        pa = msrc_p;
+        ia = msrc_i;
+        pa.insert(pa.end(), mdst_p.begin(), mdst_p.end());
+        ia.insert(ia.end(), mdst_i.begin(), mdst_i.end());
+        DevBuf &dpa = s_rm_[3], &dia = s_rm_[4], &dscr_p = s_rm_[5], &dscr_i = s_rm_[6],
+               &dclr = s_rm_[7];
+        dpa.ensure(std::max<size_t>(pa.size(), 1) * 8);
+        dia.ensure(std::max<size_t>(ia.size(), 1) * 8);
+        dscr_p.ensure(std::max<size_t>((size_t)nm * (mir_on_ ? 2 * mirror_k(D_) + 2 + D_ : D_), 1) * 4);
+        dscr_i.ensure(std::max<size_t>(nm, 1) * 8);
+        dclr.ensure(std::max<size_t>(clear.size(), 1) * 8);
+        if (!pa.empty()) {
+            BIVF_CUDA(cudaMemcpyAsync(dpa.p, pa.data(), pa.size() * 8, cudaMemcpyHostToDevice, st));
+            BIVF_CUDA(cudaMemcpyAsync(dia.p, ia.data(), ia.size() * 8, cudaMemcpyHostToDevice, st));
+        }
+        if (!clear.empty())
+            BIVF_CUDA(cudaMemcpyAsync(dclr.p, clear.data(), clear.size() * 8, cudaMemcpyHostToDevice, st));
+        BIVF_CUDA(launch_slot_moves(d_off_pay_.as<float>(), d_off_ids_.as<long long>(),
+                                    d_arena_.as<float>(), d_bids_.as<long long>(), D_,
+                                    dpa.as<uint64_t>(), dia.as<uint64_t>(), nm,
+                                    dscr_p.as<float>(), dscr_i.as<long long>(), st));
+        if (mir_on_)
+            BIVF_CUDA(launch_mirror_slot_moves(mirror_, dia.as<uint64_t>(), nm, dscr_p.as<float>(), st));
+        BIVF_CUDA(launch_clear_ids(d_off_ids_.as<long long>(), d_bids_.as<long long>(),
+                                   dclr.as<uint64_t>(), (uint32_t)clear.size(), st));
+    };
+
+    // ---- read-copy-update: new versions beside the published ones
+    uint32_t need_blocks = 0;
+    for (auto& kv : parts) {
+        if (!(kv.first & 1)) continue;
+        std::set<uint64_t> mids;
+        for (auto& pc : kv.second.content) mids.insert(pc.first / T_);
+        need_blocks += (uint32_t)mids.size();
+    }
+    std::map<uint32_t, uint64_t> new_region;  // offline part -> new segment start
+    bool cow = cow_on_ && !copy_backend_ && need_blocks <= NS_;
+    if (cow) {
+        for (auto& kv : parts) {
+            if (kv.first & 1) continue;
+            const uint32_t c = (uint32_t)(kv.first / 2);
+            const uint64_t slots = (kv.second.count + 31ull) / 32 * 32;
+            uint64_t r = 0;
+            if (slots && (r = off_alloc(slots)) == ~0ull) {
+                cow = false;
+                break;
+            }
+            new_region[c] = slots ? r : ~0ull;
+        }
+        if (!cow)  // give back what was taken
+            for (auto& nr : new_region)
+                if (nr.second != ~0ull)
+                    off_free_add(nr.second, (parts[2ull * nr.first].count + 31ull) / 32 * 32);
+    }
+    if (cow) {
+        ++cow_ops_;
+        std::map<uint32_t, ListPub> pubs;
+        auto pub_of = [&](uint32_t c) -> ListPub& {
+            auto it = pubs.find(c);
+            if (it == pubs.end()) it = pubs.emplace(c, current_pub(c)).first;
+            return it->second;
+        };
+        std::vector<int32_t> cp_src, cp_dst;                  // original block -> scratch
+        std::vector<uint32_t> row_lists;
+        std::vector<std::vector<int32_t>> rows1;
+        std::vector<uint8_t> sel1;
+        uint32_t next_sc = NB_;
+        for (auto& kv : parts) {
+            const uint32_t c = (uint32_t)(kv.first / 2);
+            Part& P = kv.second;
+            if (kv.first & 1) {
+                // online: every logical block the plan writes gets a scratch copy
+                std::map<uint32_t, int32_t> sc_of;
+                for (auto& pc : P.content) {
+                    const uint32_t m = (uint32_t)(pc.first / T_);
+                    if (!sc_of.count(m)) {
+                        sc_of[m] = (int32_t)next_sc++;
+                        cp_src.push_back(h_blocks_[c][m]);
+                        cp_dst.push_back(sc_of[m]);
+                    }
+                }
+                for (auto& pc : P.content) {
+                    const uint64_t pos = pc.first, orig = pc.second;
+                    const int32_t sb = sc_of[(uint32_t)(pos / T_)];
+                    if (pos >= P.count) {
+                        clear.push_back(id_at(true, (uint64_t)sb, pos % T_));
+                    } else if (orig != pos) {
+                        const int32_t ob = h_blocks_[c][orig / T_];
+                        msrc_p.push_back(pay_at(true, (uint64_t)ob, orig % T_));
+                        msrc_i.push_back(id_at(true, (uint64_t)ob, orig % T_));
+                        mdst_p.push_back(pay_at(true, (uint64_t)sb, pos % T_));
+                        mdst_i.push_back(id_at(true, (uint64_t)sb, pos % T_));
+                    }
+                }
+                std::vector<int32_t> r1 = h_blocks_[c];
+                for (auto& so : sc_of) r1[so.first] = so.second;
+                row_lists.push_back(c);
+                rows1.push_back(std::move(r1));
+                sel1.push_back((uint8_t)(1 - h_sel_[c]));
+                ListPub& pb = pub_of(c);
+                pb.row = row_addr(c, 1 - h_sel_[c]);
+                pb.len = P.count;
+            } else {
+                // offline: the segment's new version in a free region (live groups copied,
+                // then the tail-into-hole moves read from the old version)
+                const uint64_t r = new_region[c], old = h_off_start_[c];
+                const uint64_t groups = (P.count + 31ull) / 32;
+                if (groups) {
+                    auto cpy = [&](void* base, size_t per_slot_bytes) {
+                        BIVF_CUDA(cudaMemcpyAsync(static_cast<char*>(base) + r * per_slot_bytes,
+                                                  static_cast<char*>(base) + old * per_slot_bytes,
+                                                  groups * 32 * per_slot_bytes, cudaMemcpyDeviceToDevice, st));
+                    };
+                    cpy(d_off_pay_.p, (size_t)D_ * 4);
+                    cpy(d_off_ids_.p, 8);
+                    if (mir_on_) {
+                        BIVF_CUDA(cudaMemcpyAsync(d_off_mir_.as<float>() + (r / 32) * GF_,
+                                                  d_off_mir_.as<float>() + (old / 32) * GF_,
+                                                  groups * GF_ * 4, cudaMemcpyDeviceToDevice, st));
+                        BIVF_CUDA(cudaMemcpyAsync(d_off_nrm_.as<float>() + (r / 32) * kNormFloats,
+                                                  d_off_nrm_.as<float>() + (old / 32) * kNormFloats,
+                                                  groups * kNormFloats * 4, cudaMemcpyDeviceToDevice, st));
+                        if (d_off_rows_.p) cpy(d_off_rows_.p, (size_t)D_ * 4);
+                    }
+                }
+                for (auto& pc : P.content) {
+                    const uint64_t pos = pc.first, orig = pc.second;
+                    if (pos >= P.count) {
+                        if (pos < groups * 32) clear.push_back(id_at(false, r, pos));
+                    } else if (orig != pos) {
+                        msrc_p.push_back(pay_at(false, old, orig));
+                        msrc_i.push_back(id_at(false, old, orig));
+                        mdst_p.push_back(pay_at(false, r, pos));
+                        mdst_i.push_back(id_at(false, r, pos));
+                    }
+                }
+                ListPub& pb = pub_of(c);
+                pb.start = groups ? r : 0;
+                pb.count = P.count;
+            }
+        }
+        copy_block_set(cp_src, cp_dst);
+        apply_moves();
+        write_rows(row_lists, rows1, sel1);
+        std::vector<ListPub> pv;
+        for (auto& kv : pubs) pv.push_back(kv.second);
+        publish(pv);
+        // host mirror follows the published state; retired offline regions wait for a grace
+        for (auto& kv : pubs) {
+            const uint32_t c = kv.first;
+            const ListPub& pb = kv.second;
+            if (new_region.count(c)) {
+                auto it = off_region_.find(h_off_start_[c]);
+                if (h_off_count_[c] > 0 && it != off_region_.end() && it->second.first == c) {
+                    off_pending_.emplace_back(it->first, it->second.second);
+                    off_region_.erase(it);
+                }
+                if (pb.count > 0) off_region_[pb.start] = {c, (pb.count + 31ull) / 32 * 32};
+                h_off_start_[c] = pb.start;
+                h_off_count_[c] = pb.count;
+            }
+            h_len_[c] = pb.len;
+        }
+        for (size_t i = 0; i < row_lists.size(); ++i) h_sel_[row_lists[i]] = sel1[i];
+        grace();
+        // online: the new versions back into the reference's block positions
+        if (!cp_src.empty()) {
+            copy_block_set(cp_dst, cp_src);
+            std::vector<std::vector<int32_t>> rows2;
+            std::vector<uint8_t> sel2;
+            std::vector<ListPub> pv2;
+            for (uint32_t c : row_lists) {
+                rows2.push_back(h_blocks_[c]);
+                sel2.push_back((uint8_t)(1 - h_sel_[c]));
+            }
+            write_rows(row_lists, rows2, sel2);
+            for (size_t i = 0; i < row_lists.size(); ++i) {
+                h_sel_[row_lists[i]] = sel2[i];
+                pv2.push_back(current_pub(row_lists[i]));
+            }
+            publish(pv2);
+            BIVF_CUDA(cudaStreamSynchronize(st));
+        }
+        grace_pending_ = true;
+        return removed;
+    }
+
+    // ---- quiescent fallback: compaction in place, searches fenced
+    ++quiescent_ops_;
     std::vector<uint32_t> len_idx, len_val, off_idx, off_val;
     for (auto& kv : parts) {
         const uint64_t key = kv.first;
         Part& P = kv.second;
         const uint32_t c = (uint32_t)(key / 2);
-        const uint32_t old_count = (key & 1) ? h_len_[c] : h_off_count_[c];
+        const bool arena = key & 1;
         for (auto& pc : P.content) {
             const uint64_t pos = pc.first, orig = pc.second;
+            auto loc_of = [&](uint64_t q, uint64_t& base, uint64_t& slot) {
+                if (arena) {
+                    base = (uint64_t)h_blocks_[c][q / T_];
+                    slot = q % T_;
+                } else {
+                    base = h_off_start_[c];
+                    slot = q;
+                }
+            };
+            uint64_t b1, s1;
+            loc_of(pos, b1, s1);
             if (pos >= P.count) {
-                clear.push_back(id_addr(key, pos));
+                clear.push_back(id_at(arena, b1, s1));
             } else if (orig != pos) {
-                msrc_p.push_back(pay_addr(key, orig));
-                mdst_p.push_back(pay_addr(key, pos));
-                msrc_i.push_back(id_addr(key, orig));
-                mdst_i.push_back(id_addr(key, pos));
+                uint64_t b0, s0;
+                loc_of(orig, b0, s0);
+                msrc_p.push_back(pay_at(arena, b0, s0));
+                msrc_i.push_back(id_at(arena, b0, s0));
+                mdst_p.push_back(pay_at(arena, b1, s1));
+                mdst_i.push_back(id_at(arena, b1, s1));
             }
         }
-        (void)old_count;
-        if (key & 1) {
+        if (arena) {
             len_idx.push_back(c);
             len_val.push_back(P.count);
         } else {
@@ -1595,27 +2040,11 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
             off_val.push_back(P.count);
         }
     }
-    const uint32_t nm = (uint32_t)msrc_p.size();
-    std::vector<uint64_t> pa(msrc_p), ia(msrc_i);
-    pa.insert(pa.end(), mdst_p.begin(), mdst_p.end());
-    ia.insert(ia.end(), mdst_i.begin(), mdst_i.end());
-    DevBuf &dpa = s_rm_[3], &dia = s_rm_[4], &dscr_p = s_rm_[5], &dscr_i = s_rm_[6],
-           &dclr = s_rm_[7], &dli = s_rm_[8], &dlv = s_rm_[9], &doi = s_rm_[10], &dov = s_rm_[11];
-    dpa.ensure(std::max<size_t>(pa.size(), 1) * 8);
-    dia.ensure(std::max<size_t>(ia.size(), 1) * 8);
-    dscr_p.ensure(std::max<size_t>((size_t)nm * (mir_on_ ? 2 * mirror_k(D_) + 2 + D_ : D_), 1) * 4);
-    dscr_i.ensure(std::max<size_t>(nm, 1) * 8);
-    dclr.ensure(std::max<size_t>(clear.size(), 1) * 8);
+    DevBuf &dli = s_rm_[8], &dlv = s_rm_[9], &doi = s_rm_[10], &dov = s_rm_[11];
     dli.ensure(std::max<size_t>(len_idx.size(), 1) * 4);
     dlv.ensure(std::max<size_t>(len_idx.size(), 1) * 4);
     doi.ensure(std::max<size_t>(off_idx.size(), 1) * 4);
     dov.ensure(std::max<size_t>(off_idx.size(), 1) * 4);
-    if (!pa.empty()) {
-        BIVF_CUDA(cudaMemcpyAsync(dpa.p, pa.data(), pa.size() * 8, cudaMemcpyHostToDevice, st));
-        BIVF_CUDA(cudaMemcpyAsync(dia.p, ia.data(), ia.size() * 8, cudaMemcpyHostToDevice, st));
-    }
-    if (!clear.empty())
-        BIVF_CUDA(cudaMemcpyAsync(dclr.p, clear.data(), clear.size() * 8, cudaMemcpyHostToDevice, st));
     if (!len_idx.empty()) {
         BIVF_CUDA(cudaMemcpyAsync(dli.p, len_idx.data(), len_idx.size() * 4, cudaMemcpyHostToDevice, st));
         BIVF_CUDA(cudaMemcpyAsync(dlv.p, len_val.data(), len_val.size() * 4, cudaMemcpyHostToDevice, st));
@@ -1627,15 +2056,7 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
     {
         std::unique_lock<std::shared_mutex> g(gate_);
         begin_maintenance();
-        BIVF_CUDA(launch_slot_moves(d_off_pay_.as<float>(), d_off_ids_.as<long long>(),
-                                    d_arena_.as<float>(), d_bids_.as<long long>(), D_,
-                                    dpa.as<uint64_t>(), dia.as<uint64_t>(), nm,
-                                    dscr_p.as<float>(), dscr_i.as<long long>(), st));
-        if (mir_on_)
-            BIVF_CUDA(launch_mirror_slot_moves(mirror_, dia.as<uint64_t>(), nm, dscr_p.as<float>(),
-                                               st));
-        BIVF_CUDA(launch_clear_ids(d_off_ids_.as<long long>(), d_bids_.as<long long>(),
-                                   dclr.as<uint64_t>(), (uint32_t)clear.size(), st));
+        apply_moves();
         BIVF_CUDA(launch_set_u32(d_len_.as<uint32_t>(), dli.as<uint32_t>(), dlv.as<uint32_t>(),
                                  (uint32_t)len_idx.size(), st));
         BIVF_CUDA(launch_set_u32(d_off_count_.as<uint32_t>(), doi.as<uint32_t>(),
@@ -1798,8 +2219,21 @@ uint64_t GpuIndex::hop_count(uint32_t c) const {
 void GpuIndex::rearrange(uint32_t c) {
     if (c >= C_) throw Error(BIVF_ERANGE, "rearrange: bad cluster");
     std::lock_guard<std::mutex> lk(data_mu_);
+    rearrange_lists({c});
+}
+
+void GpuIndex::rearrange_sweep() {
+    // ivf_index.cpp:507-511: every list above T'_m, in cluster order; planned one
+    // after the other on the header mirror, the data moves applied once
+    std::lock_guard<std::mutex> lk(data_mu_);
+    std::vector<uint32_t> ex;
+    for (uint32_t c = 0; c < C_; ++c)
+        if ((uint64_t)h_len_[c] > cfg_.rearrange_threshold) ex.push_back(c);
+    if (!ex.empty()) rearrange_lists(ex);
+}
+
+void GpuIndex::rearrange_lists(const std::vector<uint32_t>& lists) {
     BIVF_CUDA(cudaSetDevice(device_));
-    const auto t0 = std::chrono::steady_clock::now();
     auto hops_of = [&](uint32_t k) {
         uint64_t hops = 0, visited = 0;
         for (int32_t b = h_head_[k]; b >= 0; b = h_next_[b]) {
@@ -1816,11 +2250,20 @@ void GpuIndex::rearrange(uint32_t c) {
     P.list_touched.assign(C_, 0);
     P.content_at.resize(h_cursor_);
     for (uint32_t b = 0; b < h_cursor_; ++b) P.content_at[b] = (int32_t)b;
-    RearrangeEvent ev{c, hops_of(c), 0, 0, 0.0};
-    P.rearrange(c);
-    ev.hops_after = hops_of(c);
-    ev.merges = P.merges;
-    // apply the accumulated permutation on device
+    std::vector<RearrangeEvent> evs;
+    for (uint32_t c : lists) {
+        const auto t0 = std::chrono::steady_clock::now();
+        RearrangeEvent ev{c, hops_of(c), 0, 0, 0.0};
+        const uint64_t m0 = P.merges;
+        P.rearrange(c);
+        ev.hops_after = hops_of(c);
+        ev.merges = P.merges - m0;
+        ev.duration_us =
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        evs.push_back(ev);
+    }
+    // the accumulated content permutation, applied on device
+    const auto t1 = std::chrono::steady_clock::now();
     std::vector<int32_t> src, dst;
     for (uint32_t x = 0; x < h_cursor_; ++x)
         if (P.content_at[x] != (int32_t)x) {
@@ -1828,69 +2271,118 @@ void GpuIndex::rearrange(uint32_t c) {
             dst.push_back((int32_t)x);
         }
     if (!src.empty()) {
-        const uint32_t nm = (uint32_t)src.size();
-        // persistent grow-only scratch: a cudaMalloc/cudaFree per rearrangement
-        // would device-synchronize against every in-flight search
-        DevBuf &ds = s_rr_src_, &dd = s_rr_dst_, &sp = s_rr_pay_, &si = s_rr_ids_;
-        ds.ensure(nm * 4);
-        dd.ensure(nm * 4);
-        sp.ensure((size_t)nm * std::max<uint64_t>(PS_, mir_on_ ? MPS_ : 0) * 4);
-        si.ensure((size_t)nm * T_ * 8);
-        cudaStream_t st = data_stream_;
-        BIVF_CUDA(cudaMemcpyAsync(ds.p, src.data(), nm * 4, cudaMemcpyHostToDevice, st));
-        BIVF_CUDA(cudaMemcpyAsync(dd.p, dst.data(), nm * 4, cudaMemcpyHostToDevice, st));
-        // updated table rows for every touched list, and owners
-        std::vector<int32_t> rows;
-        std::vector<uint32_t> rowc;
+        std::vector<uint32_t> touched;
         for (uint32_t k = 0; k < C_; ++k)
-            if (P.list_touched[k]) rowc.push_back(k);
-        std::vector<std::vector<int32_t>> staged;
-        {
-            std::unique_lock<std::shared_mutex> g(gate_);
-            begin_maintenance();
-            BIVF_CUDA(launch_block_moves(d_arena_.as<float>(), d_bids_.as<long long>(), PS_, T_,
+            if (P.list_touched[k]) touched.push_back(k);
+        apply_block_moves(src, dst, touched);
+    }
+    // the data moves are part of every rearrangement they serve
+    const double apply_us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t1).count();
+    std::lock_guard<std::mutex> lk2(events_mu_);
+    for (auto& ev : evs) {
+        ev.duration_us += apply_us;
+        events_.push_back(ev);
+    }
+}
+
+// Block contents move src[i] -> dst[i] (a permutation of pool blocks), the
+// touched lists' rows become h_blocks_ (already updated by the planner).
+void GpuIndex::apply_block_moves(const std::vector<int32_t>& src, const std::vector<int32_t>& dst,
+                                 const std::vector<uint32_t>& lists) {
+    const uint32_t nm = (uint32_t)src.size();
+    cudaStream_t st = data_stream_;
+    if (cow_on_ && nm <= NS_) {
+        ++cow_ops_;
+        reclaim();
+        // phase 1: the moving contents into scratch blocks; rows in final logical
+        // order, a moved content read from its scratch copy
+        std::vector<int32_t> sc(nm);
+        std::unordered_map<int32_t, int32_t> sc_of_dst;
+        for (uint32_t i = 0; i < nm; ++i) {
+            sc[i] = (int32_t)(NB_ + i);
+            sc_of_dst[dst[i]] = sc[i];
+        }
+        copy_block_set(src, sc);
+        std::vector<std::vector<int32_t>> rows;
+        std::vector<uint8_t> sel;
+        for (uint32_t k : lists) {
+            std::vector<int32_t> r = h_blocks_[k];
+            for (auto& x : r) {
+                auto it = sc_of_dst.find(x);
+                if (it != sc_of_dst.end()) x = it->second;
+            }
+            rows.push_back(std::move(r));
+            sel.push_back((uint8_t)(1 - h_sel_[k]));
+        }
+        write_rows(lists, rows, sel);
+        std::vector<ListPub> pubs;
+        for (size_t i = 0; i < lists.size(); ++i) {
+            h_sel_[lists[i]] = sel[i];
+            pubs.push_back(current_pub(lists[i]));
+        }
+        publish(pubs);
+        grace();
+        // phase 2: contents to their final (reference) blocks, rows to them
+        copy_block_set(sc, dst);
+        rows.clear();
+        for (size_t i = 0; i < lists.size(); ++i) {
+            rows.push_back(h_blocks_[lists[i]]);
+            sel[i] = (uint8_t)(1 - h_sel_[lists[i]]);
+        }
+        write_rows(lists, rows, sel);
+        pubs.clear();
+        for (size_t i = 0; i < lists.size(); ++i) {
+            h_sel_[lists[i]] = sel[i];
+            pubs.push_back(current_pub(lists[i]));
+        }
+        publish(pubs);
+        BIVF_CUDA(cudaMemcpyAsync(d_owner_.p, h_owner_.data(), (size_t)h_cursor_ * 4,
+                                  cudaMemcpyHostToDevice, st));
+        BIVF_CUDA(cudaStreamSynchronize(st));
+        grace_pending_ = true;
+        return;
+    }
+    // quiescent fallback: searches fenced, blocks permuted in place
+    ++quiescent_ops_;
+    DevBuf &ds = s_rr_src_, &dd = s_rr_dst_, &sp = s_rr_pay_, &si = s_rr_ids_;
+    ds.ensure(nm * 4);
+    dd.ensure(nm * 4);
+    sp.ensure((size_t)nm * std::max<uint64_t>(PS_, mir_on_ ? MPS_ : 0) * 4);
+    si.ensure((size_t)nm * T_ * 8);
+    BIVF_CUDA(cudaMemcpyAsync(ds.p, src.data(), nm * 4, cudaMemcpyHostToDevice, st));
+    BIVF_CUDA(cudaMemcpyAsync(dd.p, dst.data(), nm * 4, cudaMemcpyHostToDevice, st));
+    std::vector<std::vector<int32_t>> rows;
+    std::vector<uint8_t> sel;
+    for (uint32_t k : lists) {
+        rows.push_back(h_blocks_[k]);
+        sel.push_back(h_sel_[k]);
+    }
+    {
+        std::unique_lock<std::shared_mutex> g(gate_);
+        begin_maintenance();
+        BIVF_CUDA(launch_block_moves(d_arena_.as<float>(), d_bids_.as<long long>(), PS_, T_,
+                                     ds.as<int32_t>(), dd.as<int32_t>(), nm, sp.as<float>(),
+                                     si.as<long long>(), st));
+        if (mir_on_) {
+            BIVF_CUDA(launch_block_moves(d_arena_mir_.as<float>(), nullptr, MPS_, T_,
                                          ds.as<int32_t>(), dd.as<int32_t>(), nm, sp.as<float>(),
-                                         si.as<long long>(), st));
-            if (mir_on_) {
-                BIVF_CUDA(launch_block_moves(d_arena_mir_.as<float>(), nullptr, MPS_, T_,
-                                             ds.as<int32_t>(), dd.as<int32_t>(), nm, sp.as<float>(),
-                                             nullptr, st));
-                BIVF_CUDA(launch_block_moves(d_arena_nrm_.as<float>(), nullptr,
-                                             (uint64_t)gpb_ * kNormFloats, T_, ds.as<int32_t>(),
-                                             dd.as<int32_t>(), nm, sp.as<float>(), nullptr, st));
+                                         nullptr, st));
+            BIVF_CUDA(launch_block_moves(d_arena_nrm_.as<float>(), nullptr,
+                                         (uint64_t)gpb_ * kNormFloats, T_, ds.as<int32_t>(),
+                                         dd.as<int32_t>(), nm, sp.as<float>(), nullptr, st));
+            if (d_arena_rows_.p)
                 BIVF_CUDA(launch_block_moves(d_arena_rows_.as<float>(), nullptr, PS_, T_,
                                              ds.as<int32_t>(), dd.as<int32_t>(), nm, sp.as<float>(),
                                              nullptr, st));
-            }
-            for (uint32_t k : rowc) {
-                staged.push_back(h_blocks_[k]);
-                auto& r = staged.back();
-                if (!r.empty())
-                    BIVF_CUDA(cudaMemcpyAsync(d_table_.as<int32_t>() + (size_t)k * MLB_, r.data(),
-                                              r.size() * 4, cudaMemcpyHostToDevice, st));
-            }
-            BIVF_CUDA(cudaMemcpyAsync(d_owner_.p, h_owner_.data(), (size_t)h_cursor_ * 4,
-                                      cudaMemcpyHostToDevice, st));
-            end_maintenance();
         }
-        BIVF_CUDA(cudaStreamSynchronize(st));
+        // rows rewritten in place: no search runs until the maintenance event
+        write_rows(lists, rows, sel);
+        BIVF_CUDA(cudaMemcpyAsync(d_owner_.p, h_owner_.data(), (size_t)h_cursor_ * 4,
+                                  cudaMemcpyHostToDevice, st));
+        end_maintenance();
     }
-    ev.duration_us =
-        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-    std::lock_guard<std::mutex> lk2(events_mu_);
-    events_.push_back(ev);
-}
-
-void GpuIndex::rearrange_sweep() {
-    // ivf_index.cpp:507-511
-    for (uint32_t c = 0; c < C_; ++c) {
-        bool ex;
-        {
-            std::lock_guard<std::mutex> lk(data_mu_);
-            ex = (uint64_t)h_len_[c] > cfg_.rearrange_threshold;
-        }
-        if (ex) rearrange(c);
-    }
+    BIVF_CUDA(cudaStreamSynchronize(st));
 }
 
 std::vector<RearrangeEvent> GpuIndex::take_events() {

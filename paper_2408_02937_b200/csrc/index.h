@@ -15,9 +15,18 @@
 //     read only release-published prefixes (len) of append-only storage.
 //   insert / remove / rearrange: serialized on the data stream (data_mu_),
 //     like the reference's single data lane + insert_gate_.
-//   remove / rearrange vs search: quiescence — the data stream waits on every
-//     lease's last event, later searches wait on the maintenance event
-//     (stream-ordered, no host spin), so searches never observe a move.
+//   remove / rearrange vs search: read-copy-update, searches never wait.  A
+//     search snapshots every list's (offline start, count, block-table row,
+//     length) once, in its plan, under a per-list seqlock (scan_common.cuh
+//     snapshot_list).  Maintenance builds the new versions of the touched
+//     blocks / segments in storage no published state references (scratch
+//     blocks past the pool, free offline regions, the inactive copy of each
+//     double-buffered block-table row), publishes them (maint.cu
+//     publish_lists), and reuses old storage only after a grace period: the
+//     data stream waits, on the device, for every search enqueued before the
+//     publish (grace()).  Rearrangement and online deletes move data back into
+//     the reference's block positions in a second phase (layout parity).
+//     Oversized operations fall back to quiescence (begin/end_maintenance).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -26,6 +35,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <shared_mutex>
 #include <stdexcept>
@@ -156,6 +166,8 @@ public:
     void rearrange(uint32_t c);
     void rearrange_sweep();
     std::vector<RearrangeEvent> take_events();
+    uint64_t cow_ops() const { return cow_ops_; }
+    uint64_t quiescent_ops() const { return quiescent_ops_; }
 
     uint64_t size() const;
     uint64_t scalars_copied() const { return scalars_copied_; }
@@ -224,6 +236,30 @@ private:
                         uint32_t P, Workspace& w);
     void begin_maintenance();   // caller holds data_mu_; takes gate_ exclusively
     void end_maintenance();
+    // read-copy-update maintenance (caller holds data_mu_)
+    void grace();                                   // see the header comment
+    void reclaim() { if (grace_pending_) grace(); } // before reusing scratch / inactive rows
+    struct ListPub {                                // a list's new published state
+        uint32_t c;
+        uint64_t start;
+        uint32_t count;
+        uint64_t row;
+        uint32_t len;
+    };
+    void publish(const std::vector<ListPub>& pubs);
+    ListPub current_pub(uint32_t c) const;
+    uint64_t row_addr(uint32_t c, uint32_t sel) const;
+    // write rows (logical block order) into the given row copies of lists
+    void write_rows(const std::vector<uint32_t>& lists, const std::vector<std::vector<int32_t>>& rows,
+                    const std::vector<uint8_t>& sel);
+    void grow_rows(uint32_t need);                  // row capacity (MLB_) >= need
+    void apply_block_moves(const std::vector<int32_t>& src, const std::vector<int32_t>& dst,
+                           const std::vector<uint32_t>& lists);
+    void copy_block_set(const std::vector<int32_t>& src, const std::vector<int32_t>& dst);
+    // offline free space (slots, group aligned)
+    uint64_t off_alloc(uint64_t slots);             // ~0 when none
+    void off_free_add(uint64_t start, uint64_t slots);
+    uint32_t off_owner(uint64_t slot) const;        // cluster whose segment holds the slot
 
     // --- host mirror
     void absorb_new_blocks(uint32_t cursor_old, uint32_t cursor_new);
@@ -234,7 +270,8 @@ private:
     void validate_search(uint64_t k, uint64_t nprobe) const;
 
     bivf_config cfg_;
-    uint32_t C_, D_, Dp_, T_, gpb_, NB_, MLB_;
+    uint32_t C_, D_, Dp_, T_, gpb_, NB_, MLB_, MLB_cap_;
+    uint32_t NS_ = 0;  // scratch blocks past the pool (arena block ids NB_ .. NB_+NS_-1)
     uint64_t PS_;
     int device_;
     int num_sms_ = 148;
@@ -254,7 +291,19 @@ private:
     DevBuf d_q_mir_, d_q_nrm_, d_q_ids_, d_q_meta_, d_q_zero_, d_q_mu_;
     CUtensorMap map_q_{};
     bool q_tc_ok_ = false;
-    DevBuf d_cursor_, d_len_, d_nblocks_, d_fail_, d_table_;
+    DevBuf d_cursor_, d_len_, d_nblocks_, d_fail_;
+    // per-list block-table rows, double buffered: [2][C][MLB_] int32; d_rowptr_[c]
+    // points at copy h_sel_[c] of row c; d_ver_ is the per-list seqlock
+    DevBuf d_rows_, d_rowptr_, d_ver_;
+    std::vector<std::unique_ptr<DevBuf>> retired_;  // outgrown row buffers (searches may hold them)
+    std::vector<uint8_t> h_sel_;
+    bool grace_pending_ = false;
+    uint64_t cow_ops_ = 0, quiescent_ops_ = 0;  // maintenance ops by path (tests, bench)
+    void rearrange_lists(const std::vector<uint32_t>& lists);  // caller holds data_mu_  // scratch / inactive rows may still be read by searches
+    bool cow_on_ = true;          // BIVF_COW=0: quiescence for every maintenance op
+    bool copy_backend_ = false;   // extend_copy owns the offline area (no free-space COW)
+    DevBuf s_pub_, s_rows_;
+    PinBuf h_pub_;
     DevBuf d_run_, d_failfrom_, d_newlen_;
     // data-lane staging
     cudaStream_t data_stream_ = nullptr;
@@ -271,6 +320,9 @@ private:
     // host mirror
     std::vector<uint32_t> h_len_, h_off_count_, h_nblocks_;
     std::vector<uint64_t> h_off_start_;
+    std::map<uint64_t, uint64_t> off_free_;                       // start -> slots
+    std::vector<std::pair<uint64_t, uint64_t>> off_pending_;      // retired, freed at the next grace
+    std::map<uint64_t, std::pair<uint32_t, uint64_t>> off_region_;  // start -> (cluster, slots)
     std::vector<int32_t> h_prev_, h_next_, h_owner_, h_mid_;
     std::vector<uint8_t> h_merged_;
     std::vector<int32_t> h_head_, h_tail_;
@@ -297,6 +349,7 @@ private:
     std::vector<std::unique_ptr<Lease>> leases_;
     cudaEvent_t maint_evt_ = nullptr;
     std::atomic<uint64_t> maint_gen_{0};
+    std::atomic<uint64_t> gen_{0};  // device-buffer generation (graph_sig)
 
     CUtensorMap map_off_{}, map_arena_{};
     bool tc_ok_ = false;

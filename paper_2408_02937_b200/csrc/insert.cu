@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(InsertState S, u
         int32_t blk = -1;
         if (ok_open) {
             blk = (int32_t)(cursor0 + gidx);
-            S.table[(uint64_t)a * S.MLB + mid] = blk;
+            S.rowptr[a][mid] = blk;  // appended past every published entry
             S.owner[blk] = (int32_t)a;
             atomicMax(&S.nblocks[a], mid + 1);
         } else if (opener) {
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kLayoutThreads) layout_kernel(InsertState S, u
         __syncthreads();
         if (i < n) {
             bool ok = a != kInvalid && i < S.fail_from[a];
-            out_blk[i] = ok ? S.table[(uint64_t)a * S.MLB + mid] : -1;
+            out_blk[i] = ok ? S.rowptr[a][mid] : -1;
             out_did[i] = did;
             if (ok) atomicMax(&S.newlen[a], did + 1);
         }

@@ -19,7 +19,7 @@ struct InsertState {
     uint32_t* len;
     uint32_t* nblocks;
     uint8_t* fail;
-    int32_t* table;
+    int32_t* const* rowptr;   // per list: its live block-table row (MLB = row capacity)
     // per-batch scratch, [C] each
     uint32_t *run, *fail_from, *newlen;
 };

@@ -5,9 +5,13 @@
 // Reference semantics:
 //   swap_blocks data part       src/ivf_index.cpp:541-557 (ids + payload + committed)
 //   delete                      none in the reference; rules: DESIGN.md §Delete
-// Moves are planned on the host mirror; here every move is a gather of the
-// source slots/blocks into a scratch area followed by a scatter, so a whole
-// plan (any chain of swaps or tail moves) applies in two order-free passes.
+// Moves are planned on the host mirror.  Concurrent searches are never fenced:
+// new versions of the touched blocks / segments are built in storage no
+// published state references (scratch blocks past the pool, free offline
+// regions), published per list through the DevLists seqlock
+// (publish_lists_kernel), and the old storage is reused only after a grace
+// period (GpuIndex::grace).  The in-place gather/scatter kernels below remain
+// for the quiescent fallback path.
 #include <algorithm>
 
 #include "common.cuh"
@@ -87,6 +91,51 @@ __global__ void set_u32_kernel(uint32_t* arr, const uint32_t* idx, const uint32_
                                uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) arr[idx[i]] = val[i];
+}
+
+// Copy-on-write block copies (disjoint source / destination sets: pool
+// blocks <-> scratch blocks past the pool): n copies of `bytes` each (a
+// multiple of 8), block x at base + x * bytes.
+__global__ void copy_blocks_kernel(char* base, uint64_t bytes, const int32_t* src,
+                                   const int32_t* dst, uint32_t n) {
+    const uint32_t m = blockIdx.y;
+    if (m >= n) return;
+    const char* from = base + (uint64_t)src[m] * bytes;
+    char* to = base + (uint64_t)dst[m] * bytes;
+    if ((bytes & 15) == 0) {
+        const uint4* f = reinterpret_cast<const uint4*>(from);
+        uint4* t = reinterpret_cast<uint4*>(to);
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < bytes / 16;
+             i += (uint64_t)gridDim.x * blockDim.x)
+            t[i] = f[i];
+    } else {
+        const uint2* f = reinterpret_cast<const uint2*>(from);
+        uint2* t = reinterpret_cast<uint2*>(to);
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < bytes / 8;
+             i += (uint64_t)gridDim.x * blockDim.x)
+            t[i] = f[i];
+    }
+}
+
+// Publish new versions of lists (DevLists seqlock): ver odd, the fields, ver
+// even.  Everything the new versions point to was written by earlier work on
+// this stream.  A null field array leaves that field unchanged.
+__global__ void publish_lists_kernel(uint32_t n, const uint32_t* idx, const uint64_t* start,
+                                     const uint32_t* count, const uint64_t* row,
+                                     const uint32_t* len, uint64_t* L_start, uint32_t* L_count,
+                                     uint64_t* L_row, uint32_t* L_len, uint32_t* L_ver) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t c = idx[i];
+    const uint32_t v = L_ver[c];
+    *reinterpret_cast<volatile uint32_t*>(L_ver + c) = v + 1;
+    __threadfence();
+    if (start) *reinterpret_cast<volatile uint64_t*>(L_start + c) = start[i];
+    if (count) *reinterpret_cast<volatile uint32_t*>(L_count + c) = count[i];
+    if (row) *reinterpret_cast<volatile uint64_t*>(L_row + c) = row[i];
+    if (len) *reinterpret_cast<volatile uint32_t*>(L_len + c) = len[i];
+    __threadfence();
+    st_release_u32(L_ver + c, v + 2);
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -223,6 +272,28 @@ cudaError_t launch_locate(const long long* ids, uint64_t nslots, bool arena,
     if (!nslots) return cudaSuccess;
     locate_kernel<<<grid_for(nslots, 148 * 32), 256, 0, s>>>(ids, nslots, arena ? (1ull << 63) : 0,
                                                              hkeys, hvals, hmask, loc);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_copy_blocks(void* base, uint64_t bytes, const int32_t* src, const int32_t* dst,
+                               uint32_t n, cudaStream_t s) {
+    if (!n || !base || !bytes) return cudaSuccess;
+    if (bytes & 7) return cudaErrorInvalidValue;
+    const uint64_t units = bytes / ((bytes & 15) == 0 ? 16 : 8);
+    const unsigned gx = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((units + 255) / 256, 64));
+    copy_blocks_kernel<<<dim3(gx, n), 256, 0, s>>>(static_cast<char*>(base), bytes, src, dst, n);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_publish_lists(uint32_t n, const uint32_t* idx, const uint64_t* start,
+                                 const uint32_t* count, const uint64_t* row, const uint32_t* len,
+                                 uint64_t* L_start, uint32_t* L_count, uint64_t* L_row,
+                                 uint32_t* L_len, uint32_t* L_ver, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    publish_lists_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, idx, start, count, row, len, L_start,
+                                                         L_count, L_row, L_len, L_ver);
     count_launch();
     return cudaGetLastError();
 }

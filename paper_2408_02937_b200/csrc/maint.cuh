@@ -27,6 +27,16 @@ cudaError_t launch_merge_shards(const float* dists, const long long* ids, uint32
                                 uint32_t k, float* out_d, long long* out_i, uint32_t* out_cnt,
                                 cudaStream_t s);
 
+// n whole-block copies of `bytes` (multiple of 8) from block src[i] to dst[i]
+// of the array at `base` (source and destination sets disjoint).
+cudaError_t launch_copy_blocks(void* base, uint64_t bytes, const int32_t* src, const int32_t* dst,
+                               uint32_t n, cudaStream_t s);
+// publish new list versions (DevLists seqlock); null field arrays stay unchanged
+cudaError_t launch_publish_lists(uint32_t n, const uint32_t* idx, const uint64_t* start,
+                                 const uint32_t* count, const uint64_t* row, const uint32_t* len,
+                                 uint64_t* L_start, uint32_t* L_count, uint64_t* L_row,
+                                 uint32_t* L_len, uint32_t* L_ver, cudaStream_t s);
+
 constexpr uint64_t kArenaBit = 1ull << 63;
 
 }  // namespace bivf

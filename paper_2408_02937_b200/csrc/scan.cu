@@ -402,19 +402,21 @@ __global__ void merge_kernel(uint32_t nq, uint32_t P, uint32_t maxch, uint32_t k
 }
 
 // ------------------------------------------------------------------ plan
-__global__ void plan_snapshot(DevLists L, uint32_t maxch, uint32_t gcmin, uint32_t* snap_off,
-                              uint32_t* snap_len, uint32_t* gc, uint32_t* nch, uint32_t* cnt) {
+__global__ void plan_snapshot(DevLists L, uint32_t maxch, uint32_t gcmin, PlanBufs B) {
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= L.C) return;
-    const uint32_t off = L.off_count[c];
-    const uint32_t len = ld_acquire_u32(L.len + c);
-    snap_off[c] = off;
-    snap_len[c] = len;
+    uint32_t off, len;
+    uint64_t start, row;
+    snapshot_list(L, c, off, len, start, row);
+    B.snap_off[c] = off;
+    B.snap_len[c] = len;
+    B.snap_start[c] = start;
+    B.snap_row[c] = row;
     const uint32_t ng = ivf_ngroups(L, off, len);
     uint32_t g = max(gcmin, (ng + maxch - 1) / maxch);
-    gc[c] = g;
-    nch[c] = (ng + g - 1) / g;
-    cnt[c] = 0;
+    B.gc[c] = g;
+    B.nch[c] = (ng + g - 1) / g;
+    B.cnt[c] = 0;
 }
 
 // pairs i = q * P + rank with rank in [lo, hi) only (the ranked plans of the
@@ -512,10 +514,13 @@ __global__ void __launch_bounds__(1024) plan_fused(DevLists L, uint32_t maxch, u
     const uint32_t t = threadIdx.x;
     for (uint32_t c = t; c < L.C; c += 1024) {
         if (snapshot) {
-            const uint32_t off = L.off_count[c];
-            const uint32_t len = ld_acquire_u32(L.len + c);
+            uint32_t off, len;
+            uint64_t start, row;
+            snapshot_list(L, c, off, len, start, row);
             B.snap_off[c] = off;
             B.snap_len[c] = len;
+            B.snap_start[c] = start;
+            B.snap_row[c] = row;
             const uint32_t ng = ivf_ngroups(L, off, len);
             const uint32_t g = max(gcmin, (ng + maxch - 1) / maxch);
             B.gc[c] = g;
@@ -730,8 +735,7 @@ cudaError_t launch_plan_ranked(const DevLists& L, const PlanBufs& B, const long 
         return cudaGetLastError();
     }
     if (snapshot) {
-        plan_snapshot<<<(L.C + 255) / 256, 256, 0, s>>>(L, sh.maxch, sh.gcmin, B.snap_off,
-                                                       B.snap_len, B.gc, B.nch, B.cnt);
+        plan_snapshot<<<(L.C + 255) / 256, 256, 0, s>>>(L, sh.maxch, sh.gcmin, B);
     } else {
         cudaError_t e = cudaMemsetAsync(B.cnt, 0, (size_t)L.C * 4, s);
         if (e != cudaSuccess) return e;
@@ -754,8 +758,7 @@ cudaError_t launch_ivf_search(const DevLists& L, const PlanBufs& B, const long l
     const int kpl = kpl_for(sh.k);
     if (!kpl) return cudaErrorInvalidValue;
     const uint32_t npairs = sh.nq * sh.P;
-    plan_snapshot<<<(L.C + 255) / 256, 256, 0, s>>>(L, sh.maxch, sh.gcmin, B.snap_off, B.snap_len,
-                                                   B.gc, B.nch, B.cnt);
+    plan_snapshot<<<(L.C + 255) / 256, 256, 0, s>>>(L, sh.maxch, sh.gcmin, B);
     plan_count<<<(npairs + 255) / 256, 256, 0, s>>>(probes, npairs, sh.P, 0, sh.P, B.cnt, B.ppos);
     plan_scan<<<1, 1024, 0, s>>>(L.C, sh.QT, B.cnt, B.nch, B.qoff, B.item_off, B.n_items,
                                  B.item_ctr);
@@ -770,7 +773,7 @@ cudaError_t launch_ivf_search(const DevLists& L, const PlanBufs& B, const long l
     p.k = sh.k;
     p.P = sh.P;
     p.QT = sh.QT;
-    p.L = L;
+    p.L = snapshot_view(L, B);
     p.snap_off = B.snap_off;
     p.snap_len = B.snap_len;
     p.gc = B.gc;

@@ -7,24 +7,33 @@
 namespace bivf {
 
 // Device view of the index's storage (all pointers device memory).
+// Live view: the index's published per-list state.  A search reads it ONCE, in
+// its plan (snapshot_list: a per-list seqlock against maintenance publishes), and
+// every later kernel of the search gets a snapshot view (snapshot_view) whose
+// off_start / rowptr are the plan's copies: maintenance (delete, rearrangement)
+// never edits storage a published state points to; it writes new versions
+// elsewhere, publishes them, and reuses the old storage only after every search
+// that may have snapshotted it has finished (GpuIndex::grace).
 struct DevLists {
     uint32_t C, D, T, gpb;   // clusters, dim, block capacity, groups per block
     uint64_t PS;             // payload scalars per block = gpb*32*D
-    uint32_t MLB;            // max blocks per list (row length of `table`)
     const float* off_payload;     // offline segments, interleaved, group-aligned
     const long long* off_ids;     // per slot
     const uint64_t* off_start;    // per cluster, slot offset (multiple of 32)
-    const uint32_t* off_count;    // per cluster (changed only under quiescence)
-    const float* arena;           // pool payload, num_blocks * PS
-    const long long* bids;        // pool ids, num_blocks * T
-    const int32_t* table;         // per-list block table, C * MLB
+    const uint32_t* off_count;    // per cluster
+    const float* arena;           // pool payload, (num_blocks + scratch) * PS
+    const long long* bids;        // pool ids, (num_blocks + scratch) * T
+    const int32_t* const* rowptr; // per cluster: its block-table row (logical order)
     const uint32_t* len;          // per-list online length (published, acquire)
+    const uint32_t* ver;          // per-list seqlock: odd while a publish rewrites the list
 };
 
 // Per-search scratch (lease workspace), device pointers.
 struct PlanBufs {
     uint32_t* snap_off;   // [C]
     uint32_t* snap_len;   // [C]
+    uint64_t* snap_start; // [C] offline segment start at plan time
+    uint64_t* snap_row;   // [C] block-table row pointer at plan time
     uint32_t* gc;         // [C] groups per chunk
     uint32_t* nch;        // [C] chunks
     uint32_t* cnt;        // [C] pairs per list
@@ -40,6 +49,15 @@ struct SearchShape {
     uint32_t nq, k, P, maxch, gcmin, QT;
     int metric;
 };
+
+// The view every post-plan kernel of a search uses: the plan's snapshot of
+// the lists' offline starts and block-table rows.
+inline DevLists snapshot_view(const DevLists& L, const PlanBufs& B) {
+    DevLists v = L;
+    v.off_start = B.snap_start;
+    v.rowptr = reinterpret_cast<const int32_t* const*>(B.snap_row);
+    return v;
+}
 
 // Picks the device top-k width for k (1,2,4,8 registers per lane).
 int kpl_for(uint32_t k);

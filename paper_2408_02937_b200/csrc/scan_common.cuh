@@ -5,6 +5,7 @@
 
 #include <cstdint>
 
+#include "common.cuh"
 #include "scan.cuh"
 
 namespace bivf {
@@ -34,7 +35,7 @@ __device__ __forceinline__ GroupRef ivf_group(const DevLists& L, uint32_t c, uin
     } else {
         const uint32_t jj = j - og;
         const uint32_t mid = jj / L.gpb, gi = jj - mid * L.gpb;
-        const int32_t blk = L.table[(uint64_t)c * L.MLB + mid];
+        const int32_t blk = L.rowptr[c][mid];
         const uint32_t cnt_mid = min(L.T, len - mid * L.T);
         g.base = L.arena + (uint64_t)blk * L.PS + (uint64_t)gi * 32u * L.D;
         g.ids = L.bids + (uint64_t)blk * L.T + 32u * gi;
@@ -44,5 +45,23 @@ __device__ __forceinline__ GroupRef ivf_group(const DevLists& L, uint32_t c, uin
     return g;
 }
 
+
+// One list's published state, consistent against maintenance publishes
+// (maint.cu publish_lists: ver odd -> fields -> ver even).  Inserts only append
+// (entries past the old block count, slots past the old length) and release
+// the length, so they need no seqlock.
+__device__ __forceinline__ void snapshot_list(const DevLists& L, uint32_t c, uint32_t& off,
+                                              uint32_t& len, uint64_t& start, uint64_t& row) {
+    for (;;) {
+        const uint32_t v1 = ld_acquire_u32(L.ver + c);
+        if (v1 & 1u) continue;  // a publish kernel is rewriting this list right now
+        off = ld_acquire_u32(L.off_count + c);
+        len = ld_acquire_u32(L.len + c);
+        start = *reinterpret_cast<const volatile uint64_t*>(L.off_start + c);
+        row = *reinterpret_cast<const volatile uint64_t*>(reinterpret_cast<const uint64_t*>(L.rowptr) + c);
+        __threadfence();
+        if (*reinterpret_cast<const volatile uint32_t*>(L.ver + c) == v1) return;
+    }
+}
 
 }  // namespace bivf

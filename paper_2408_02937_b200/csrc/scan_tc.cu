@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 // list's block-table row (one entry per gpb groups, cached)
                 const uint32_t og = (d.off + 31u) >> 5;
                 const uint64_t offg0 = og ? p.L.off_start[d.c] / 32u : 0ull;
-                const int32_t* trow = p.L.table + (uint64_t)d.c * p.L.MLB;
+                const int32_t* trow = p.L.rowptr[d.c];
                 uint32_t cmid = 0xffffffffu;
                 uint64_t cblk = 0;
                 for (uint32_t j0 = d.g0; j0 < d.g1; j0 += kGU, ++unit) {
@@ -1147,7 +1147,7 @@ __device__ __forceinline__ const float* cand_row(const TcParams& p, uint32_t c, 
     const uint32_t og = (off + 31u) >> 5;
     if (j < og) return p.off_rows + (p.L.off_start[c] + 32ull * j + s) * p.D;
     const uint32_t jj = j - og, mid = jj / p.L.gpb, gi = jj - mid * p.L.gpb;
-    const uint64_t g = (uint64_t)p.L.table[(uint64_t)c * p.L.MLB + mid] * p.L.gpb + gi;
+    const uint64_t g = (uint64_t)p.L.rowptr[c][mid] * p.L.gpb + gi;
     return p.arena_rows + (g * 32u + s) * p.D;
 }
 
@@ -1589,7 +1589,7 @@ __device__ __forceinline__ uint64_t ivf_group_index(const DevLists& L, uint32_t 
     }
     const uint32_t jj = j - og, mid = jj / L.gpb, gi = jj - mid * L.gpb;
     arena = true;
-    return (uint64_t)L.table[(uint64_t)c * L.MLB + mid] * L.gpb + gi;
+    return (uint64_t)L.rowptr[c][mid] * L.gpb + gi;
 }
 
 // One warp per query over the dense approximate distances of all its probed
@@ -1979,7 +1979,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
         if (e != cudaSuccess) return e;
     }
     TcParams p{};
-    p.L = L;
+    p.L = snapshot_view(L, B);  // every kernel after the plan reads the plan's snapshot
     p.D = L.D;
     p.Dk = wide ? mirror_k_wide(L.D) : (L.D + 15) & ~15u;
     p.brow = wide ? mirror_chunk_wide(L.D) : 2 * p.Dk;

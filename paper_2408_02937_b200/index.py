@@ -255,6 +255,10 @@ class ClusterIndex:
     def scalars_copied(self):
         return self._u64(lib().bivf_scalars_copied)
 
+    def maintenance_stats(self):
+        """{'cow': ops run as read-copy-update, 'quiescent': ops that fenced searches}"""
+        return {"cow": self._u64(lib().bivf_cow_ops), "quiescent": self._u64(lib().bivf_quiescent_ops)}
+
     def list_length(self, cluster):
         return self._u64(lib().bivf_list_length, cluster)
 
