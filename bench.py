@@ -32,9 +32,11 @@ events, max over ranks).  e2e = the same through the host C-ABI call
 (bit-identical to the reference's offline build, tests/test_gpu_parity.py)
 saves a BIVFSNAP snapshot in the untimed setup and ClusterIndex::load reads it;
 the timed steps and the live inserts run only reference code.
-N > 1: the base is vector-sharded (id mod N); every rank searches
-the whole batch on its shard, top-k lists are all-gathered over NCCL and
-merged on device (bivf_merge_topk_device).
+N > 1: the base is vector-sharded (id mod N) behind the native
+group (csrc/group.cpp, bivf_group_*): each rank runs the coarse quantizer for
+1/N of the queries, the probe rows and the local top-k lists are all-gathered
+with NCCL on the lease stream and merged on device; inserts and deletes take
+the global stream on every rank and are routed by id.
 """
 from __future__ import annotations
 
@@ -286,45 +288,47 @@ def run_ours(args, dist):
     out_i = torch.empty((B, K), dtype=torch.int64, device=qd.device)
     out_d = torch.empty((B, K), dtype=torch.float32, device=qd.device)
     out_c = torch.empty((B,), dtype=torch.int32, device=qd.device)
-    if world > 1:
-        gi = torch.empty((world, B, K), dtype=torch.int64, device=qd.device)
-        gd = torch.empty((world, B, K), dtype=torch.float32, device=qd.device)
-        mi = torch.empty((B, K), dtype=torch.int64, device=qd.device)
-        md = torch.empty((B, K), dtype=torch.float32, device=qd.device)
-        mc = torch.empty((B,), dtype=torch.int32, device=qd.device)
     stream = torch.cuda.current_stream()
+    grp = None
+    if world > 1:
+        # the native sharded data plane (csrc/group.cpp): NCCL communicators from
+        # one unique id (broadcast here: plumbing only); channel 1 = searches,
+        # channel 0 = the insert / delete all-reduces
+        from paper_2408_02937_b200.sharded import ShardGroup
+        uid = [ShardGroup.unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        grp = ShardGroup.nccl(ix, uid[0], world, rank, channels=2)
 
     def step():
-        _lib.check(L.bivf_search_device(ix._h, qd.data_ptr(), B, K, NPROBE, out_i.data_ptr(),
-                                        out_d.data_ptr(), out_c.data_ptr(), stream.cuda_stream))
-        if world > 1:
-            torch.distributed.all_gather_into_tensor(gi.view(-1), out_i.view(-1))
-            torch.distributed.all_gather_into_tensor(gd.view(-1), out_d.view(-1))
-            _lib.check(L.bivf_merge_topk_device(dev, gd.data_ptr(), gi.data_ptr(), world, B, K,
-                                                md.data_ptr(), mi.data_ptr(), mc.data_ptr(),
-                                                stream.cuda_stream))
+        if grp is None:
+            _lib.check(L.bivf_search_device(ix._h, qd.data_ptr(), B, K, NPROBE, out_i.data_ptr(),
+                                            out_d.data_ptr(), out_c.data_ptr(), stream.cuda_stream))
+        else:
+            grp.search_device(qd.data_ptr(), B, K, NPROBE, out_i.data_ptr(), out_d.data_ptr(),
+                              out_c.data_ptr(), stream.cuda_stream, channel=1)
 
-    # live inserts (global ids, sharded id mod world) + deletes, each on its own thread
-    ins_ids = (N_BASE + np.arange(len(ins_pool) * world, dtype=np.int64))[rank::world]
-    state = {"pos": 0}
+    # live inserts + deletes: one data-lane thread per rank (every rank issues the
+    # same global batches in the same order: the group's collectives on channel 0)
+    del_ids = delete_ids(0, 1)
+    half = len(ins_pool) // 2
+    every = max(1, int(round((INSERT_RATE / INSERT_BATCH) / (DELETE_RATE / DELETE_BATCH))))
+    dstate = {"tick": 0, "pos": 0, "deleted": 0}
 
-    def insert_fn(x):
-        p = state["pos"]
-        ids = ins_ids[p:p + len(x)] if world > 1 else None
-        state["pos"] += len(x)
-        ix.insert(x, ids)
-        ix.rearrange_sweep()  # post_insert_maintenance (executor.cpp:380)
+    def data_fn(x):
+        if grp is None:
+            ix.insert(x)
+        else:
+            grp.insert(x)
+        ix.rearrange_sweep()  # post_insert_maintenance (executor.cpp:380), shard-local
+        dstate["tick"] += 1
+        if dstate["tick"] % every == 0 and dstate["pos"] + DELETE_BATCH <= len(del_ids) // 2:
+            d = del_ids[dstate["pos"]:dstate["pos"] + DELETE_BATCH]
+            dstate["pos"] += DELETE_BATCH
+            dstate["deleted"] += (ix.remove(d) if grp is None else grp.remove(d))[0]
         return len(x)
 
-    def delete_fn(ids):
-        return ix.remove(ids)[0]
-
-    del_ids = delete_ids(rank, world)
-    half = len(ins_pool) // 2
-    ins = Paced(insert_fn, ins_pool[:half], INSERT_RATE / world, INSERT_BATCH)
-    dels = Paced(delete_fn, del_ids[:len(del_ids) // 2], DELETE_RATE / world, DELETE_BATCH)
+    ins = Paced(data_fn, ins_pool[:half], INSERT_RATE, INSERT_BATCH)
     ins.start()
-    dels.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -350,12 +354,9 @@ def run_ours(args, dist):
     hq[:] = queries
     h_out = (bivf.pinned_empty((len(hq), K), np.int64), bivf.pinned_empty((len(hq), K), np.float32),
              bivf.pinned_empty((len(hq),), np.uint32))
-    if world > 1:  # the public sharded API: local search, NCCL all-gather, device merge, D2H
-        from paper_2408_02937_b200.sharded import ShardedIndex
-        sharded = ShardedIndex(ix, rank, world, next_id=N_BASE)
-
+    if grp is not None:  # the public sharded API: bivf_group_search (host buffers)
         def e2e_call():
-            return sharded.search(hq, K, NPROBE)
+            return grp.search(hq, K, NPROBE, channel=1, out=h_out)
     else:
         def e2e_call():
             return ix.search_batch(hq, K, NPROBE, out=h_out)
@@ -367,7 +368,8 @@ def run_ours(args, dist):
         e2e_call()
     e2e_s = max_over_ranks(dist, time.perf_counter() - t)
     ins_stats = ins.finish()
-    del_stats = dels.finish()
+    del_stats = {"items": int(dstate["deleted"]), "rate_per_s": round(
+        dstate["deleted"] / max(1e-9, ins.t1 - ins.t0), 1)}
     rr_events = len(ix.take_rearrange_events())
 
     # --- p50/p99 of executor requests (10-query batches, the reference's
@@ -391,9 +393,9 @@ def run_ours(args, dist):
     # recall@10 vs exact (full probe == brute force over every list), through the
     # same (sharded, for N > 1: a collective on every rank) search as the e2e leg
     nrec = 500
-    if world > 1:
-        gi_, _, _ = sharded.search(hq[:nrec], K, NPROBE)
-        ti_, _, _ = sharded.search(hq[:nrec], K, NLIST)
+    if grp is not None:
+        gi_, _, _ = grp.search(hq[:nrec], K, NPROBE, channel=1)
+        ti_, _, _ = grp.search(hq[:nrec], K, NLIST, channel=1)
     else:
         gi_, _, _ = ix.search_batch(hq[:nrec], K, NPROBE)
         ti_, _, _ = ix.search_batch(hq[:nrec], K, NLIST)
@@ -437,6 +439,8 @@ def run_ours(args, dist):
         if not args.no_cpu_baseline and world == 1:
             result["cpu_baseline"] = cpu_baseline_from_snapshot(ix, hq)
     barrier(dist)
+    if grp is not None:
+        grp.close()
     ix.close()
     return result
 
@@ -538,6 +542,12 @@ def latency_phase(ix, queries, inserts, dels, seconds, repeats):
         v = np.concatenate([x[key + "_raw_us"] for x in rs])
         return summarize_latencies([u / 1e3 for u in v if u >= 0])
 
+    for nm, rs in (("idle", idle), ("live", live)):  # stalls, for the log
+        for r, x in enumerate(rs):
+            raw = x["search_raw_us"]
+            slow = [(i, round(v / 1e3, 1)) for i, v in enumerate(raw) if v > 5000]
+            if slow:
+                log(f"latency {nm} window {r}: {len(slow)} requests > 5 ms of {len(raw)}, first {slow[:8]}")
     s_idle, s_live, s_ins = merged(idle, "search"), merged(live, "search"), merged(live, "insert")
     per_rep = [round(b["search"]["p99_ms"] / a["search"]["p99_ms"], 3) for a, b in zip(idle, live)]
     return {"arrivals": "poisson", "search_req_s": LAT_QPS, "queries_per_req": 10,

@@ -103,6 +103,12 @@ bivf_status bivf_save_snapshot(const bivf_index* h, const char* path);
 bivf_status bivf_load_snapshot(const char* path, const bivf_config* cfg_override,
                                bivf_index** out);
 
+/* One shard of a vector-sharded group from a whole-index snapshot: only the
+ * vectors with id mod nshards == shard are loaded (every shard
+ * keeps all centroids and the snapshot's next_id). */
+bivf_status bivf_load_snapshot_shard(const char* path, uint32_t shard, uint32_t nshards,
+                                     const bivf_config* cfg_override, bivf_index** out);
+
 /* ---- the hot path ----------------------------------------------------- */
 /* VectorIndex::insert (vector_index.hpp:25-27, ivf_index.cpp:122-164).
  * ids NULL -> contiguous auto ids.  out_ids[i] = id or -1 (rejected duplicate
@@ -174,6 +180,12 @@ bivf_status bivf_cluster_contents(const bivf_index* h, uint32_t cluster, int64_t
 /* dump_pool text (block_store.cpp:188-201); *len = bytes needed incl. NUL */
 bivf_status bivf_dump_pool(const bivf_index* h, char* buf, uint64_t cap, uint64_t* len);
 bivf_status bivf_next_id(const bivf_index* h, int64_t* out);
+/* one-shot utilization alert (block_store.cpp:41-46): *fired, and the number of
+ * blocks in use at the allocation that first exceeded the watermark */
+bivf_status bivf_pool_alert(const bivf_index* h, int32_t* fired, uint64_t* used_at);
+/* block_store.hpp set_next: raw header-link mutation (the reference pool's test
+ * hook; traversals then report cycles as BIVF_ECORRUPT) */
+bivf_status bivf_block_set_next(bivf_index* h, int32_t block, int32_t next);
 
 /* ---- data helpers (either side of the path) ----------------------------- */
 /* synthetic_dataset (dataset.cpp:92-112): same std::mt19937_64 stream, same
@@ -186,6 +198,14 @@ bivf_status bivf_kmeans(const float* points, uint64_t n, uint64_t dim, uint64_t 
                         uint64_t max_iters, uint64_t seed, int32_t device, float* centroids,
                         uint32_t* assignment, uint64_t* iters_run);
 
+/* Exact k nearest neighbours by brute force (oracle.cpp:11-49 exact_knn):
+ * sequential fp32 distances (L2: distance.hpp:11-18; IP: key = -q.x) over rows
+ * 0..n-1, ordered by (key, row id); counts = min(k, n).  k <= 256.  Ground
+ * truth for recall@k at scale, on the GPU (host buffers). */
+bivf_status bivf_exact_knn(const float* base, uint64_t n, uint64_t dim, const float* queries,
+                           uint64_t nq, uint64_t k, int32_t metric, int32_t device, int64_t* out_ids,
+                           float* out_dists, uint32_t* out_counts);
+
 /* ---- multi-GPU merge (north star (5)) ------------------------------------ */
 /* Merge G per-shard top-k lists ([G][nq][k], ascending runs, id -1 = empty)
  * into the global top-k under (dist, id) order — the step after the NCCL
@@ -193,6 +213,44 @@ bivf_status bivf_kmeans(const float* points, uint64_t n, uint64_t dim, uint64_t 
 bivf_status bivf_merge_topk_device(int32_t device, const float* dists, const int64_t* ids,
                                    uint64_t G, uint64_t nq, uint64_t k, float* out_dists,
                                    int64_t* out_ids, uint32_t* out_counts, void* stream);
+
+/* ---- vector-sharded groups (north star (5)) ------------------ */
+/* Shard g of a G-shard group owns the ids with id mod G == g; every shard holds
+ * all centroids, so the merged top-k equals the single index's bit for bit.
+ * A search splits the coarse quantizer by queries (shard g computes the probes
+ * of query slice g), all-gathers the probe rows, scans every shard's lists for
+ * the whole batch, all-gathers the local top-k lists and merges them on device
+ * (bivf_merge_topk_device's kernel).  Transports:
+ *   bivf_group_create_local: G shard handles of this process (any devices, one
+ *     device repeated included); peer copies between the shards' lease streams.
+ *   bivf_group_create_nccl: this process's shard is rank `rank` of `nranks`;
+ *     ncclAllGather / ncclAllReduce on the lease stream (libnccl loaded at run
+ *     time).  `uid128` = bivf_nccl_unique_id() of rank 0, broadcast by the caller.
+ *     `channels` communicators (ncclCommSplit): calls on one channel must be
+ *     issued in the same order on every rank; concurrent callers use distinct
+ *     channels (channel 0 also carries the all-reduces of inserts / deletes).  Every rank passes the same queries / insert batch / delete ids
+ *     and receives the whole result.
+ * Inserts: auto ids are the group's contiguous next_id range (ivf_index.cpp:
+ * 133-141); each shard inserts its rows with explicit ids.  The group does not
+ * own its shards: destroy the group first. */
+typedef struct bivf_group bivf_group;
+bivf_status bivf_nccl_unique_id(void* out128);
+bivf_status bivf_group_create_local(bivf_index* const* shards, uint32_t nshards, bivf_group** out);
+bivf_status bivf_group_create_nccl(bivf_index* shard, const void* uid128, int32_t nranks, int32_t rank,
+                                   uint32_t channels, bivf_group** out);
+void bivf_group_destroy(bivf_group* g);
+bivf_status bivf_group_size(const bivf_group* g, uint32_t* out);
+bivf_status bivf_group_search(bivf_group* g, const float* queries, uint64_t nq, uint64_t k,
+                              uint64_t nprobe, int64_t* out_ids, float* out_dists,
+                              uint32_t* out_counts, uint32_t channel);
+/* NCCL groups: device buffers on this rank's device, ordered after / before `stream` */
+bivf_status bivf_group_search_device(bivf_group* g, const float* queries_dev, uint64_t nq,
+                                     uint64_t k, uint64_t nprobe, int64_t* ids_dev, float* dists_dev,
+                                     uint32_t* counts_dev, void* stream, uint32_t channel);
+bivf_status bivf_group_insert(bivf_group* g, const float* vectors, uint64_t n, const int64_t* ids,
+                              int64_t* out_ids, uint64_t* inserted);
+bivf_status bivf_group_remove(bivf_group* g, const int64_t* ids, uint64_t n, uint64_t* removed,
+                              uint8_t* found);
 
 /* ---- executor: the multi-lane resource pool (Alg. 4) ---------------------- */
 /* Mirrors blockivf::Executor (include/blockivf/executor.hpp:21-196,

@@ -6,7 +6,8 @@ mirror of the reference's binding surface (blockivf._core) over that ABI.
 """
 from ._lib import (BivfError, BusyError, CorruptListError, CudaError, METRIC_IP, METRIC_L2,
                    PoolExhaustedError)
-from .index import BaselineIndex, ClusterIndex, device_count, kernel_launches, kmeans, pinned_empty, synthetic_dataset
+from .index import (BaselineIndex, ClusterIndex, device_count, exact_knn, kernel_launches, kmeans, pinned_empty,
+                    synthetic_dataset)
 
 __all__ = [
     "ClusterIndex",
@@ -19,6 +20,7 @@ __all__ = [
     "BivfError",
     "synthetic_dataset",
     "kmeans",
+    "exact_knn",
     "device_count",
     "kernel_launches",
     "METRIC_L2",

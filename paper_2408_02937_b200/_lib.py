@@ -135,6 +135,10 @@ SIGNATURES = {
     "bivf_bulk_load": (C.c_int, [vp, vp, u64, vp, vp]),
     "bivf_save_snapshot": (C.c_int, [vp, C.c_char_p]),
     "bivf_load_snapshot": (C.c_int, [C.c_char_p, C.POINTER(Config), C.POINTER(vp)]),
+    "bivf_load_snapshot_shard": (C.c_int, [C.c_char_p, u32, u32, C.POINTER(Config), C.POINTER(vp)]),
+    "bivf_pool_alert": (C.c_int, [vp, C.POINTER(i32), pu64]),
+    "bivf_block_set_next": (C.c_int, [vp, i32, i32]),
+    "bivf_exact_knn": (C.c_int, [vp, u64, u64, vp, u64, u64, i32, i32, vp, vp, vp]),
     "bivf_add": (C.c_int, [vp, vp, u64, vp, vp, pu64]),
     "bivf_search": (C.c_int, [vp, vp, u64, u64, u64, vp, vp, vp]),
     "bivf_search_device": (C.c_int, [vp, vp, u64, u64, u64, vp, vp, vp, vp]),
@@ -165,6 +169,15 @@ SIGNATURES = {
     "bivf_synthetic_dataset": (C.c_int, [u64, u64, u64, u64, _f32p]),
     "bivf_kmeans": (C.c_int, [_f32p, u64, u64, u64, u64, u64, i32, _f32p, _u32p, pu64]),
     "bivf_merge_topk_device": (C.c_int, [i32, vp, vp, u64, u64, u64, vp, vp, vp, vp]),
+    "bivf_nccl_unique_id": (C.c_int, [vp]),
+    "bivf_group_create_local": (C.c_int, [C.POINTER(vp), u32, C.POINTER(vp)]),
+    "bivf_group_create_nccl": (C.c_int, [vp, vp, i32, i32, u32, C.POINTER(vp)]),
+    "bivf_group_destroy": (None, [vp]),
+    "bivf_group_size": (C.c_int, [vp, C.POINTER(u32)]),
+    "bivf_group_search": (C.c_int, [vp, vp, u64, u64, u64, vp, vp, vp, u32]),
+    "bivf_group_search_device": (C.c_int, [vp, vp, u64, u64, u64, vp, vp, vp, vp, u32]),
+    "bivf_group_insert": (C.c_int, [vp, vp, u64, vp, vp, pu64]),
+    "bivf_group_remove": (C.c_int, [vp, vp, u64, pu64, vp]),
     "bivf_executor_create": (C.c_int, [vp, C.POINTER(ExecutorConfig), C.POINTER(vp)]),
     "bivf_executor_destroy": (C.c_int, [vp]),
     "bivf_executor_submit_search": (C.c_int, [vp, vp, u64, u64, u64, C.POINTER(vp)]),

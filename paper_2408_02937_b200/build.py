@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-ffp-contract=off", "-Xcompiler", "-fopenmp", "-Xcompiler", "-Wall", "-I", CSRC, "-I", os.path.join(ROOT, "include")]
 SOURCES = ["scan.cu", "scan_tc.cu", "insert.cu", "maint.cu", "mirror.cu", "index.cpp", "host_algos.cpp", "executor.cpp",
-           "capi.cpp"]
+           "capi.cpp", "group.cpp"]
 
 
 def nvcc() -> str:
@@ -57,7 +57,7 @@ def build(verbose: bool = False) -> str:
     if os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(o) for o in objs):
         return OUT
     tmp = OUT + ".tmp"
-    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread", "-lgomp"]
+    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread", "-lgomp", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -2,6 +2,7 @@
 // C++ exceptions to bivf_status + a thread-local message; nothing throws
 // across the ABI.
 #include <cstring>
+#include <functional>
 #include <string>
 
 #include "../../include/bivf.h"
@@ -58,6 +59,12 @@ void need(const T* p, const char* what) {
     if (!p) throw Error(BIVF_EINVAL, std::string(what) + " must not be NULL");
 }
 }  // namespace
+
+namespace bivf {
+// shared with group.cpp
+GpuIndex& index_of(bivf_index* h) { return I(h); }
+bivf_status run_guarded(const std::function<void()>& f) { return guard(f); }
+}  // namespace bivf
 
 extern "C" {
 
@@ -167,6 +174,45 @@ bivf_status bivf_load_snapshot(const char* path, const bivf_config* ov, bivf_ind
             throw;
         }
         *out = h;
+    });
+}
+
+bivf_status bivf_load_snapshot_shard(const char* path, uint32_t shard, uint32_t nshards,
+                                     const bivf_config* ov, bivf_index** out) {
+    return guard([&] {
+        need(path, "path");
+        need(out, "out");
+        *out = nullptr;
+        auto h = new bivf_index;
+        try {
+            h->impl = GpuIndex::load(path, ov, shard, nshards);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+bivf_status bivf_pool_alert(const bivf_index* h, int32_t* fired, uint64_t* used_at) {
+    return guard([&] { I(h).alert_state(fired, used_at); });
+}
+
+bivf_status bivf_block_set_next(bivf_index* h, int32_t block, int32_t next) {
+    return guard([&] { I(h).block_set_next(block, next); });
+}
+
+bivf_status bivf_exact_knn(const float* base, uint64_t n, uint64_t dim, const float* queries,
+                           uint64_t nq, uint64_t k, int32_t metric, int32_t device, int64_t* out_ids,
+                           float* out_d, uint32_t* out_counts) {
+    return guard([&] {
+        if (n) need(base, "base");
+        if (nq) {
+            need(queries, "queries");
+            need(out_ids, "out_ids");
+            need(out_d, "out_dists");
+        }
+        bivf::exact_knn_gpu(base, n, dim, queries, nq, k, metric, device, out_ids, out_d, out_counts);
     });
 }
 

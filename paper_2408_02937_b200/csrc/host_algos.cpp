@@ -203,4 +203,64 @@ uint64_t kmeans_gpu(const float* points, uint64_t n, uint64_t dim, uint64_t k, u
     return iters_run;
 }
 
+// oracle.cpp:11-49 exact_knn on the GPU: the rows as ONE flat interleaved list
+// scanned by the exact CUDA-core top-k kernel (sequential fp32 sums, (key, row)
+// order), query batches of up to 64K.
+void exact_knn_gpu(const float* base, uint64_t n, uint64_t dim, const float* q, uint64_t nq, uint64_t k,
+                   int metric, int device, int64_t* ids, float* d, uint32_t* cnt) {
+    if (dim == 0 || k == 0 || k > 256) throw Error(BIVF_EINVAL, "exact_knn: dim >= 1 and k in [1, 256]");
+    if (metric != BIVF_METRIC_L2 && metric != BIVF_METRIC_IP) throw Error(BIVF_EINVAL, "exact_knn: bad metric");
+    if (n > 0xffffffffull) throw Error(BIVF_EINVAL, "exact_knn: too many rows");
+    if (nq == 0) return;
+    const uint32_t D = (uint32_t)dim, Dp = pad4(D), N = (uint32_t)n, K = (uint32_t)k;
+    if (N == 0) {
+        for (uint64_t i = 0; i < nq * k; ++i) {
+            ids[i] = -1;
+            d[i] = 0.f;
+        }
+        if (cnt)
+            for (uint64_t i = 0; i < nq; ++i) cnt[i] = 0;
+        return;
+    }
+    BIVF_CUDA(cudaSetDevice(device));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaStream_t st;
+    BIVF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG {
+        cudaStream_t s;
+        ~SG() { cudaStreamDestroy(s); }
+    } sg{st};
+    DevBuf raw, il, dq, dqp, cd, ci, od, oi, oc, ctr;
+    raw.alloc((size_t)N * D * 4);
+    il.alloc((size_t)((N + 31) / 32) * 32 * D * 4);
+    ctr.alloc(16);
+    BIVF_CUDA(cudaMemcpyAsync(raw.p, base, (size_t)N * D * 4, cudaMemcpyHostToDevice, st));
+    BIVF_CUDA(launch_interleave(raw.as<float>(), N, D, il.as<float>(), st));
+    const uint64_t chunk = 65536;
+    const uint32_t ng = (N + 31) / 32;
+    for (uint64_t s = 0; s < nq; s += chunk) {
+        const uint32_t m = (uint32_t)std::min<uint64_t>(chunk, nq - s);
+        const uint32_t qt = qt_for(K, D);
+        const uint64_t tiles = (m + qt - 1) / qt;
+        const uint32_t nch = (uint32_t)std::min<uint64_t>(ng, std::max<uint64_t>(1, ((uint64_t)sms * 8 + tiles - 1) / tiles));
+        dq.ensure((size_t)m * D * 4);
+        dqp.ensure((size_t)m * Dp * 4);
+        cd.ensure((size_t)m * nch * K * 4);
+        ci.ensure((size_t)m * nch * K * 8);
+        od.ensure((size_t)m * K * 4);
+        oi.ensure((size_t)m * K * 8);
+        oc.ensure((size_t)m * 4);
+        BIVF_CUDA(cudaMemcpyAsync(dq.p, q + s * D, (size_t)m * D * 4, cudaMemcpyHostToDevice, st));
+        BIVF_CUDA(launch_pad_rows(dq.as<float>(), m, D, Dp, dqp.as<float>(), st));
+        BIVF_CUDA(launch_flat_topk(il.as<float>(), N, D, dqp.as<float>(), m, K, metric, nch, cd.as<float>(),
+                                   ci.as<long long>(), od.as<float>(), oi.as<long long>(), oc.as<uint32_t>(),
+                                   ctr.as<uint32_t>(), sms, st));
+        BIVF_CUDA(cudaMemcpyAsync(d + s * k, od.p, (size_t)m * K * 4, cudaMemcpyDeviceToHost, st));
+        BIVF_CUDA(cudaMemcpyAsync(ids + s * k, oi.p, (size_t)m * K * 8, cudaMemcpyDeviceToHost, st));
+        if (cnt) BIVF_CUDA(cudaMemcpyAsync(cnt + s, oc.p, (size_t)m * 4, cudaMemcpyDeviceToHost, st));
+        BIVF_CUDA(cudaStreamSynchronize(st));
+    }
+}
+
 }  // namespace bivf

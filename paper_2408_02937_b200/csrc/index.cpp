@@ -124,6 +124,27 @@ void log_warn(const std::string& m) {
     if (log_level() >= 1) std::fprintf(stderr, "[bivf] %s\n", m.c_str());
 }
 
+// Slow-event trace (BIVF_TRACE=<microseconds>): searches and maintenance
+// operations slower than the threshold print their phase breakdown.
+double trace_threshold_us() {
+    static const double t = [] {
+        const char* v = std::getenv("BIVF_TRACE");
+        return v ? std::max(1.0, atof(v)) : -1.0;
+    }();
+    return t;
+}
+using TClock = std::chrono::steady_clock;
+double us_since(TClock::time_point t) {
+    return std::chrono::duration<double, std::micro>(TClock::now() - t).count();
+}
+void trace(const char* what, double total_us, const std::string& detail) {
+    const double thr = trace_threshold_us();
+    if (thr > 0 && total_us >= thr)
+        std::fprintf(stderr, "[bivf-trace] %.3f %s %.0f us: %s\n",
+                     std::chrono::duration<double>(TClock::now().time_since_epoch()).count(), what, total_us,
+                     detail.c_str());
+}
+
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 uint32_t ceil_div(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
@@ -719,6 +740,7 @@ void GpuIndex::bulk_load(const float* x, uint64_t n, const uint32_t* assignment,
         next_id_ = (int64_t)n;
         offline_end_ = (int64_t)n;
     }
+    refresh_size();
 }
 
 // ========================================================================
@@ -852,6 +874,7 @@ uint64_t GpuIndex::extend_copy(const float* x, uint64_t n, const int64_t* ids, i
     BIVF_CUDA(cudaStreamSynchronize(data_stream_));
     BIVF_CUDA(h2d(d_off_start_.p, h_off_start_.data(), (size_t)C_ * 8));
     BIVF_CUDA(h2d(d_off_count_.p, h_off_count_.data(), (size_t)C_ * 4));
+    refresh_size();
     return n;  // supplied ids do not move next_id (baseline_index.cpp:68-69)
 }
 
@@ -1198,8 +1221,11 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
                       float* out_d, uint32_t* out_cnt) {
     validate_search(k, nprobe);
     if (nq == 0) return;
+    const auto t_in = TClock::now();
     BIVF_CUDA(cudaSetDevice(device_));
     Lease* l = acquire_lease();
+    const double us_lease = us_since(t_in);
+    double us_gate = 0, us_enq = 0, us_sync = 0;
     struct Rel {
         GpuIndex* g;
         Lease* l;
@@ -1222,7 +1248,10 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
         long long* pi = reinterpret_cast<long long*>(pd + (size_t)m * k + ((m * k) & 1));
         uint32_t* pc = reinterpret_cast<uint32_t*>(pi + (size_t)m * k);
         {
+            const auto t_g = TClock::now();
             std::shared_lock<std::shared_mutex> g(gate_);
+            us_gate += us_since(t_g);
+            const auto t_e = TClock::now();
             const uint64_t gen = maint_gen_.load();
             if (l->seen_maint != gen) {
                 BIVF_CUDA(cudaStreamWaitEvent(l->stream, maint_evt_, 0));
@@ -1251,8 +1280,11 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
             BIVF_CUDA(cudaMemcpyAsync(hi, w.out_i, (size_t)m * k * 8, cudaMemcpyDeviceToHost, l->stream));
             BIVF_CUDA(cudaMemcpyAsync(hc, w.out_cnt, (size_t)m * 4, cudaMemcpyDeviceToHost, l->stream));
             BIVF_CUDA(cudaEventRecord(l->done, l->stream));
+            us_enq += us_since(t_e);
         }
+        const auto t_s = TClock::now();
         BIVF_CUDA(cudaEventSynchronize(l->done));
+        us_sync += us_since(t_s);
         if (!o_pin) {
             par_memcpy(out_d + s * k, pd, (size_t)m * k * 4);
             par_memcpy(out_ids + s * k, pi, (size_t)m * k * 8);
@@ -1260,6 +1292,61 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
         }
         if (timing_) record_timings(*l);
     }
+    if (trace_threshold_us() > 0)
+        trace("search", us_since(t_in),
+              "nq=" + std::to_string(nq) + " lease=" + std::to_string((int)us_lease) + " gate=" +
+                  std::to_string((int)us_gate) + " enqueue=" + std::to_string((int)us_enq) + " device_wait=" +
+                  std::to_string((int)us_sync));
+}
+
+void GpuIndex::shard_open(ShardCtx& s, uint64_t nq, uint64_t k, uint64_t nprobe, uint32_t G) {
+    validate_search(k, nprobe);
+    if (nq == 0 || G == 0) throw Error(BIVF_EINVAL, "sharded search: empty batch or group");
+    if (nq > 0xffffffffull / std::max<uint64_t>(1, nprobe) / G)
+        throw Error(BIVF_EINVAL, "sharded search: nq * nprobe too large for one call");
+    BIVF_CUDA(cudaSetDevice(device_));
+    s.nq = (uint32_t)nq;
+    s.k = (uint32_t)k;
+    s.P = (uint32_t)nprobe;
+    s.slice = ceil_div(nq, G);
+    s.nq_pad = s.slice * G;
+    s.lease = acquire_lease();
+    const LaunchShape sh = pick_shape(s.nq_pad, s.k, s.P, C_, num_sms_);
+    s.w = carve(*s.lease, s.nq_pad, s.k, s.P, sh.maxch, sh.fnch);
+    s.gate = std::shared_lock<std::shared_mutex>(gate_);
+    const uint64_t gen = maint_gen_.load();
+    if (s.lease->seen_maint != gen) {
+        BIVF_CUDA(cudaStreamWaitEvent(s.lease->stream, maint_evt_, 0));
+        s.lease->seen_maint = gen;
+    }
+}
+
+void GpuIndex::shard_quantize(ShardCtx& s, uint32_t g) {
+    BIVF_CUDA(cudaSetDevice(device_));
+    cudaStream_t st = s.lease->stream;
+    BIVF_CUDA(launch_pad_rows(s.w.qraw, s.nq, D_, Dp_, s.w.queries, st));
+    const uint32_t q0 = g * s.slice;
+    if (q0 >= s.nq) return;
+    const uint32_t m = std::min(s.slice, s.nq - q0);
+    if (s.P == C_) {
+        BIVF_CUDA(launch_all_probes(s.w.probes + (size_t)q0 * s.P, m, C_, st));
+        return;
+    }
+    enqueue_quantizer(st, m, s.P, pick_shape(s.nq_pad, s.k, s.P, C_, num_sms_).fnch, s.w, q0);
+}
+
+void GpuIndex::shard_scan(ShardCtx& s) {
+    BIVF_CUDA(cudaSetDevice(device_));
+    enqueue_scan(*s.lease, s.nq, s.k, s.P, s.w);
+}
+
+void GpuIndex::shard_close(ShardCtx& s) {
+    if (!s.lease) return;
+    BIVF_CUDA(cudaSetDevice(device_));
+    BIVF_CUDA(cudaEventRecord(s.lease->done, s.lease->stream));
+    if (s.gate.owns_lock()) s.gate.unlock();
+    release_lease(s.lease);
+    s.lease = nullptr;
 }
 
 void GpuIndex::search_device(const float* q_dev, uint64_t nq, uint64_t k, uint64_t nprobe,
@@ -1393,12 +1480,28 @@ void GpuIndex::absorb_new_blocks(uint32_t cursor_old, uint32_t cursor_new) {
         h_nblocks_[c] = (uint32_t)h_blocks_[c].size();
     }
     h_cursor_ = cursor_new;
-    // one-shot utilization alert (block_store.cpp:41-46)
-    if (!alert_fired_ && (double)h_cursor_ / (double)NB_ > cfg_.alert_watermark) {
-        alert_fired_ = true;
-        log_warn("central pool utilization " + std::to_string(h_cursor_) + "/" +
-                 std::to_string(NB_) + " exceeds watermark");
-    }
+    // one-shot utilization alert (block_store.cpp:41-46): the first allocation
+    // whose used/total strictly exceeds the watermark, reported once
+    for (uint64_t used = (uint64_t)cursor_old + 1; !alert_fired_ && used <= cursor_new; ++used)
+        if ((double)used / (double)NB_ > cfg_.alert_watermark) {
+            alert_fired_ = true;
+            alert_used_ = used;
+            log_warn("central pool utilization " + std::to_string(used) + "/" + std::to_string(NB_) +
+                     " exceeds watermark");
+        }
+}
+
+void GpuIndex::alert_state(int32_t* fired, uint64_t* used_at) const {
+    std::lock_guard<std::mutex> lk(data_mu_);
+    if (fired) *fired = alert_fired_ ? 1 : 0;
+    if (used_at) *used_at = alert_used_;
+}
+
+void GpuIndex::block_set_next(int32_t b, int32_t next) {
+    std::lock_guard<std::mutex> lk(data_mu_);
+    check_block(b);
+    if (next >= 0) check_block(next);
+    h_next_[b] = next;
 }
 
 void GpuIndex::refresh_lengths() {
@@ -1409,7 +1512,17 @@ uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_
     for (uint64_t i = 0; i < n; ++i) out_ids[i] = -1;
     if (n == 0) return 0;
     if (!trained_) throw Error(BIVF_ELOGIC, "insert: index has no centroids");
+    const auto t_in = TClock::now();
     std::lock_guard<std::mutex> lk(data_mu_);
+    struct Tr {
+        TClock::time_point t;
+        double lock;
+        uint64_t n;
+        ~Tr() {
+            if (trace_threshold_us() > 0)
+                trace("insert", us_since(t), "n=" + std::to_string(n) + " data_mu=" + std::to_string((int)lock));
+        }
+    } tr{t_in, us_since(t_in), n};
     BIVF_CUDA(cudaSetDevice(device_));
     // ids: contiguous auto range, or supplied ids checked in batch order
     std::vector<long long> idv(n);
@@ -1493,6 +1606,7 @@ uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_
         }
     }
     scalars_copied_ += inserted * D_;
+    refresh_size();
     if (exhausted) {
         Error e(BIVF_EPOOL, "central memory pool exhausted after inserting " +
                                 std::to_string(inserted) + " vectors of the batch");
@@ -1530,7 +1644,10 @@ void GpuIndex::end_maintenance() {
 // Work enqueued on the data stream after this call may reuse whatever the
 // old state referenced.  The host never waits for searches.
 void GpuIndex::grace() {
+    const auto t0 = TClock::now();
     BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+    const double us_sync = us_since(t0);
+    const auto t1 = TClock::now();
     {
         std::unique_lock<std::shared_mutex> g(gate_);
         std::lock_guard<std::mutex> lk(lease_mu_);
@@ -1546,6 +1663,9 @@ void GpuIndex::grace() {
     }
     off_pending_.clear();
     grace_pending_ = false;
+    if (trace_threshold_us() > 0)
+        trace("grace", us_since(t0),
+              "data_stream_sync=" + std::to_string((int)us_sync) + " gate+waits=" + std::to_string((int)us_since(t1)));
 }
 
 uint64_t GpuIndex::row_addr(uint32_t c, uint32_t sel) const {
@@ -1704,7 +1824,17 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
     if (found)
         for (uint64_t i = 0; i < n; ++i) found[i] = 0;
     if (n == 0) return 0;
+    const auto t_in = TClock::now();
     std::lock_guard<std::mutex> lk(data_mu_);
+    struct Tr {
+        TClock::time_point t;
+        double lock;
+        uint64_t n;
+        ~Tr() {
+            if (trace_threshold_us() > 0)
+                trace("remove", us_since(t), "n=" + std::to_string(n) + " data_mu=" + std::to_string((int)lock));
+        }
+    } tr{t_in, us_since(t_in), n};
     BIVF_CUDA(cudaSetDevice(device_));
     cudaStream_t st = data_stream_;
     reclaim();  // retired offline regions: ids cleared before the locate below
@@ -1997,6 +2127,7 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
             BIVF_CUDA(cudaStreamSynchronize(st));
         }
         grace_pending_ = true;
+        refresh_size();
         return removed;
     }
 
@@ -2066,6 +2197,7 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
     BIVF_CUDA(cudaStreamSynchronize(st));
     for (size_t i = 0; i < len_idx.size(); ++i) h_len_[len_idx[i]] = len_val[i];
     for (size_t i = 0; i < off_idx.size(); ++i) h_off_count_[off_idx[i]] = off_val[i];
+    refresh_size();
     return removed;
 }
 
@@ -2234,6 +2366,18 @@ void GpuIndex::rearrange_sweep() {
 
 void GpuIndex::rearrange_lists(const std::vector<uint32_t>& lists) {
     BIVF_CUDA(cudaSetDevice(device_));
+    const auto t_in = TClock::now();
+    uint64_t moved = 0;
+    struct Tr {
+        TClock::time_point t;
+        const std::vector<uint32_t>& l;
+        uint64_t& moved;
+        ~Tr() {
+            if (trace_threshold_us() > 0)
+                trace("rearrange", us_since(t),
+                      "lists=" + std::to_string(l.size()) + " moved_blocks=" + std::to_string(moved));
+        }
+    } tr{t_in, lists, moved};
     auto hops_of = [&](uint32_t k) {
         uint64_t hops = 0, visited = 0;
         for (int32_t b = h_head_[k]; b >= 0; b = h_next_[b]) {
@@ -2270,6 +2414,7 @@ void GpuIndex::rearrange_lists(const std::vector<uint32_t>& lists) {
             src.push_back(P.content_at[x]);
             dst.push_back((int32_t)x);
         }
+    moved = src.size();
     if (!src.empty()) {
         std::vector<uint32_t> touched;
         for (uint32_t k = 0; k < C_; ++k)
@@ -2396,11 +2541,14 @@ std::vector<RearrangeEvent> GpuIndex::take_events() {
 // introspection
 // ========================================================================
 
-uint64_t GpuIndex::size() const {
-    std::lock_guard<std::mutex> lk(data_mu_);
+// lock-free (VectorIndex::size, an atomic load in the reference): the
+// executor's lanes read it per request and must not wait for the data lane
+uint64_t GpuIndex::size() const { return size_total_.load(std::memory_order_acquire); }
+
+void GpuIndex::refresh_size() {  // caller holds data_mu_
     uint64_t t = 0;
     for (uint32_t c = 0; c < C_; ++c) t += (uint64_t)h_off_count_[c] + h_len_[c];
-    return t;
+    size_total_.store(t, std::memory_order_release);
 }
 
 uint64_t GpuIndex::list_length(uint32_t c) const {
@@ -2576,7 +2724,9 @@ void GpuIndex::save(const std::string& path) const {
     if (!os) throw Error(BIVF_EIO, "snapshot: write failed for " + path);
 }
 
-std::unique_ptr<GpuIndex> GpuIndex::load(const std::string& path, const bivf_config* ov) {
+std::unique_ptr<GpuIndex> GpuIndex::load(const std::string& path, const bivf_config* ov, uint32_t shard,
+                                         uint32_t nshards) {
+    if (nshards == 0 || shard >= nshards) throw Error(BIVF_EINVAL, "load: shard out of [0, nshards)");
     std::ifstream is(path, std::ios::binary);
     if (!is) throw Error(BIVF_EIO, "snapshot: cannot open " + path);
     char magic[8];
@@ -2613,11 +2763,16 @@ std::unique_ptr<GpuIndex> GpuIndex::load(const std::string& path, const bivf_con
         ids.resize(r0 + n);
         asg.resize(r0 + n, (uint32_t)c);
         rows.resize((r0 + n) * D);
+        size_t kept = r0;
         for (uint64_t i = 0; i < n; ++i) {
-            ids[r0 + i] = get<int64_t>(is);
-            is.read(reinterpret_cast<char*>(rows.data() + (r0 + i) * D), (std::streamsize)D * 4);
+            ids[kept] = get<int64_t>(is);
+            is.read(reinterpret_cast<char*>(rows.data() + kept * D), (std::streamsize)D * 4);
             if (!is) throw Error(BIVF_EIO, "snapshot: truncated vectors in " + path);
+            if (nshards == 1 || (uint64_t)ids[kept] % nshards == shard) ++kept;
         }
+        ids.resize(kept);
+        asg.resize(kept);
+        rows.resize(kept * D);
     }
     idx->bulk_load(rows.data(), ids.size(), asg.data(), ids.data());
     // flattened contents carry every id ever handed out (ivf_index.cpp:615-617)

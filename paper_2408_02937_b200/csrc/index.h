@@ -190,7 +190,30 @@ public:
     int64_t next_id() const { return next_id_; }
 
     void save(const std::string& path) const;
-    static std::unique_ptr<GpuIndex> load(const std::string& path, const bivf_config* ov);
+    // shard/nshards: keep only the ids with id mod nshards == shard (one shard of
+    // a vector-sharded group); nshards 1 = the whole snapshot
+    static std::unique_ptr<GpuIndex> load(const std::string& path, const bivf_config* ov,
+                                          uint32_t shard = 0, uint32_t nshards = 1);
+    // one-shot utilization alert (block_store.cpp:41-46): fired, blocks used when it fired
+    void alert_state(int32_t* fired, uint64_t* used_at) const;
+    // block_store.hpp set_next: raw header mutation (the reference's pool test hook)
+    void block_set_next(int32_t b, int32_t next);
+
+    // ---- one shard's part of a vector-sharded search (group.cpp), on one of
+    // this index's leases: open (lease, workspace for nq rounded up to G slices,
+    // gate shared) -> queries -> quantize one slice of the queries -> (the
+    // caller all-gathers the probe rows) -> scan all queries -> close.
+    struct ShardCtx {
+        Lease* lease = nullptr;
+        Workspace w{};
+        std::shared_lock<std::shared_mutex> gate;
+        uint32_t nq = 0, nq_pad = 0, k = 0, P = 0, slice = 0;
+    };
+    void shard_open(ShardCtx& s, uint64_t nq, uint64_t k, uint64_t nprobe, uint32_t G);
+    void shard_quantize(ShardCtx& s, uint32_t g);  // pads every query; probes of slice g
+    void shard_scan(ShardCtx& s);                  // plan + scan + refine -> s.w.out_*
+    void shard_close(ShardCtx& s);
+    int device() const { return device_; }
 
     void set_timing(bool on) { timing_ = on; }
     void set_scan_mode(int m) { scan_mode_ = m; }
@@ -329,6 +352,7 @@ private:
     std::vector<std::vector<int32_t>> h_blocks_;  // per list, logical order (table row)
     uint32_t h_cursor_ = 0;
     bool alert_fired_ = false;
+    uint64_t alert_used_ = 0;
     bool trained_ = false;
 
     // ids (ivf_index.cpp:107-141)
@@ -350,6 +374,8 @@ private:
     cudaEvent_t maint_evt_ = nullptr;
     std::atomic<uint64_t> maint_gen_{0};
     std::atomic<uint64_t> gen_{0};  // device-buffer generation (graph_sig)
+    std::atomic<uint64_t> size_total_{0};  // stored vectors (size(), lock-free)
+    void refresh_size();
 
     CUtensorMap map_off_{}, map_arena_{};
     bool tc_ok_ = false;
@@ -364,5 +390,7 @@ void synthetic_dataset(uint64_t n, uint64_t dim, uint64_t comps, uint64_t seed, 
 uint64_t kmeans_gpu(const float* points, uint64_t n, uint64_t dim, uint64_t k, uint64_t iters,
                     uint64_t seed, int device, float* centroids, uint32_t* assignment);
 float host_l2(const float* a, const float* b, uint32_t dim);
+void exact_knn_gpu(const float* base, uint64_t n, uint64_t dim, const float* q, uint64_t nq, uint64_t k,
+                   int metric, int device, int64_t* ids, float* d, uint32_t* cnt);
 
 }  // namespace bivf

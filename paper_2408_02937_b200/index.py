@@ -334,6 +334,26 @@ class ClusterIndex:
     def save(self, path):
         check(lib().bivf_save_snapshot(self._h, str(path).encode()))
 
+    def pool_alert(self):
+        """(fired, blocks used at the allocation that first exceeded the watermark)."""
+        f, u = C.c_int32(0), C.c_uint64(0)
+        check(lib().bivf_pool_alert(self._h, C.byref(f), C.byref(u)))
+        return bool(f.value), int(u.value)
+
+    def block_set_next(self, block, nxt):
+        """block_store.hpp set_next (the reference pool's raw test hook)."""
+        check(lib().bivf_block_set_next(self._h, block, nxt))
+
+    @staticmethod
+    def load_shard(path, shard, nshards, device=0, num_leases=32):
+        """One shard (ids with id % nshards == shard) of a whole-index snapshot."""
+        ov = Config()
+        ov.device = device
+        ov.num_leases = num_leases
+        h = C.c_void_p()
+        check(lib().bivf_load_snapshot_shard(str(path).encode(), shard, nshards, C.byref(ov), C.byref(h)))
+        return ClusterIndex(_handle=h.value)
+
     @staticmethod
     def load(path, device=0, num_leases=32):
         ov = Config()
@@ -397,6 +417,22 @@ def synthetic_dataset(n, dim, components=16, seed=42):
     out = np.empty((n, dim), np.float32)
     check(lib().bivf_synthetic_dataset(n, dim, components, seed, out))
     return out
+
+
+def exact_knn(base, queries, k, metric=METRIC_L2, device=0):
+    """oracle.cpp:11-49 on the GPU: (ids [nq,k], dists [nq,k], counts [nq]),
+    sequential fp32 distances, (distance, row id) order."""
+    b = _as_matrix(base)
+    q = _as_matrix(queries)
+    if b.shape[1] != q.shape[1]:
+        raise ValueError("exact_knn: dimension mismatch")
+    nq = q.shape[0]
+    ids = np.empty((max(nq, 1), k), np.int64)
+    d = np.empty((max(nq, 1), k), np.float32)
+    cnt = np.empty(max(nq, 1), np.uint32)
+    check(lib().bivf_exact_knn(ptr(b), b.shape[0], b.shape[1], ptr(q), nq, k, metric, device, ptr(ids),
+                               ptr(d), ptr(cnt)))
+    return ids[:nq], d[:nq], cnt[:nq]
 
 
 def kmeans(points, k, max_iters=25, seed=42, device=0):

@@ -1,17 +1,21 @@
-"""Vector-sharded index over N GPUs (north star (5)).
+"""Vector-sharded indexes over several GPUs (north star (5)).
 
-One process per GPU (torchrun).  Shard g owns the vectors whose id satisfies
-``id % world == g``; every shard holds all centroids, so probe sets are the
-same on every GPU and the merged top-k equals the single-index result bit for
-bit.  Inserts: every rank sees the same global batch; auto ids are assigned
-globally (the reference's contiguous ``next_id`` ranges, ivf_index.cpp:133-141)
-and each rank inserts its own rows with those explicit ids.  Search: local
-top-k on each GPU, NCCL all-gather of ``[nq, k]`` (dist, id), then the device
-merge ``bivf_merge_topk_device`` (K8).
+The data plane is native: ``ShardGroup`` drives ``bivf_group_*``
+(csrc/group.cpp) — the coarse quantizer split by queries across shards, the
+probe rows and the local top-k lists all-gathered device to device (NCCL, or
+peer copies for the shards of one process), the merge on device.  Python only
+marshals arrays; no PyTorch on the data path.
 
-``local`` is any object with the ClusterIndex surface (``insert(x, ids)``,
-``search_batch(q, k, nprobe)``); ``gather`` / ``merge`` are injectable so the
-routing logic is testable with gloo on CPU (tests/test_sharded_gloo.py).
+Shard g owns the vectors whose id satisfies ``id % G == g``; every shard holds
+all centroids, so probe sets are the same on every shard and the merged top-k
+equals the single index's bit for bit.  Inserts take the global batch on every
+rank; auto ids are the group's contiguous ``next_id`` ranges
+(ivf_index.cpp:133-141) and each shard stores its rows under those ids.
+
+``ShardedIndex`` below is the same routing written in Python over any object
+with the ClusterIndex surface and an injectable all-gather: it is the host-side
+restatement the multi-process CPU tests (gloo, tests/test_sharded_gloo.py) run
+against, and the reference the native group is checked with.
 """
 from __future__ import annotations
 
@@ -19,19 +23,108 @@ import ctypes as C
 
 import numpy as np
 
+from ._lib import check, lib, ptr
+
 
 def owner_of(ids, world):
     return np.asarray(ids, dtype=np.int64) % world
 
 
+class ShardGroup:
+    """A vector-sharded group over the native C-ABI.
+
+    ``ShardGroup.local([ix0, ix1, ...])``: every shard in this process (any
+    devices; one device repeated works too).  ``ShardGroup.nccl(ix, uid,
+    nranks, rank)``: one shard per process, NCCL collectives; ``uid`` =
+    ``ShardGroup.unique_id()`` on rank 0, broadcast by the caller.  The group
+    does not own its shards (close the group first)."""
+
+    def __init__(self, handle, shards):
+        self._h = handle
+        self._shards = shards  # keep-alive
+        self.dim = shards[0].dim
+        n = C.c_uint32(0)
+        check(lib().bivf_group_size(self._h, C.byref(n)))
+        self.size = int(n.value)
+
+    @staticmethod
+    def unique_id():
+        buf = (C.c_char * 128)()
+        check(lib().bivf_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def local(cls, shards):
+        arr = (C.c_void_p * len(shards))(*[s._h for s in shards])
+        h = C.c_void_p()
+        check(lib().bivf_group_create_local(arr, len(shards), C.byref(h)))
+        return cls(h.value, list(shards))
+
+    @classmethod
+    def nccl(cls, shard, uid, nranks, rank, channels=1):
+        if len(uid) != 128:
+            raise ValueError("uid must be the 128 bytes of bivf_nccl_unique_id")
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(lib().bivf_group_create_nccl(shard._h, buf, nranks, rank, channels, C.byref(h)))
+        return cls(h.value, [shard])
+
+    def search(self, queries, k, nprobe, channel=0, out=None):
+        q = np.ascontiguousarray(queries, dtype=np.float32).reshape(-1, self.dim)
+        nq = q.shape[0]
+        if out is None:
+            out = (np.empty((max(nq, 1), k), np.int64), np.empty((max(nq, 1), k), np.float32),
+                   np.empty(max(nq, 1), np.uint32))
+        ids, d, cnt = out
+        if nq:
+            check(lib().bivf_group_search(self._h, ptr(q), nq, k, nprobe, ptr(ids), ptr(d), ptr(cnt),
+                                          channel))
+        return ids[:nq], d[:nq], cnt[:nq]
+
+    def search_device(self, q_ptr, nq, k, nprobe, ids_ptr, d_ptr, cnt_ptr, stream, channel=0):
+        """Device buffers on this rank's device (NCCL groups), ordered on `stream`."""
+        check(lib().bivf_group_search_device(self._h, q_ptr, nq, k, nprobe, ids_ptr, d_ptr, cnt_ptr,
+                                             stream, channel))
+
+    def insert(self, vectors, ids=None):
+        x = np.ascontiguousarray(vectors, dtype=np.float32).reshape(-1, self.dim)
+        n = x.shape[0]
+        i = None if ids is None else np.ascontiguousarray(ids, dtype=np.int64)
+        out = np.full(max(n, 1), -1, np.int64)
+        ins = C.c_uint64(0)
+        check(lib().bivf_group_insert(self._h, ptr(x), n, ptr(i), ptr(out), C.byref(ins)),
+              inserted=ins.value, ids=out[:n])
+        return out[:n]
+
+    def remove(self, ids):
+        ids = np.ascontiguousarray(ids, dtype=np.int64).reshape(-1)
+        found = np.zeros(max(ids.size, 1), np.uint8)
+        rem = C.c_uint64(0)
+        check(lib().bivf_group_remove(self._h, ptr(ids), ids.size, C.byref(rem), ptr(found)))
+        return rem.value, found[: ids.size].astype(bool)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().bivf_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class ShardedIndex:
-    def __init__(self, local, rank, world, gather=None, merge=None, next_id=0):
+    """Host-side restatement of the group's routing (see module docstring)."""
+
+    def __init__(self, local, rank, world, gather, merge, next_id=0):
         self.local = local
         self.rank = rank
         self.world = world
         self.next_id = int(next_id)
-        self._gather = gather or _torch_all_gather
-        self._merge = merge or _device_merge
+        self._gather = gather
+        self._merge = merge
 
     def insert(self, x, ids=None):
         """Global batch in, global ids out (-1 for vectors this rank's shard
@@ -56,33 +149,3 @@ class ShardedIndex:
         all_ids, all_d = self._gather(ids, d)          # [world, nq, k] each
         return self._merge(all_d, all_ids, k)
 
-
-def _torch_all_gather(ids, d):
-    import torch
-    import torch.distributed as dist
-    world = dist.get_world_size()
-    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-    ti = torch.from_numpy(np.ascontiguousarray(ids)).to(dev)
-    td = torch.from_numpy(np.ascontiguousarray(d)).to(dev)
-    gi = torch.empty((world,) + tuple(ti.shape), dtype=ti.dtype, device=dev)
-    gd = torch.empty((world,) + tuple(td.shape), dtype=td.dtype, device=dev)
-    dist.all_gather_into_tensor(gi.view(-1), ti.view(-1))
-    dist.all_gather_into_tensor(gd.view(-1), td.view(-1))
-    return gi, gd
-
-
-def _device_merge(all_d, all_ids, k):
-    """K8 on the GPU (bivf_merge_topk_device); inputs are CUDA tensors."""
-    import torch
-
-    from ._lib import check, lib
-    G, nq = all_d.shape[0], all_d.shape[1]
-    od = torch.empty((nq, k), dtype=torch.float32, device=all_d.device)
-    oi = torch.empty((nq, k), dtype=torch.int64, device=all_d.device)
-    oc = torch.empty((nq,), dtype=torch.int32, device=all_d.device)
-    s = torch.cuda.current_stream(all_d.device)
-    check(lib().bivf_merge_topk_device(all_d.device.index or 0, all_d.data_ptr(),
-                                       all_ids.data_ptr(), G, nq, k, od.data_ptr(),
-                                       oi.data_ptr(), oc.data_ptr(), C.c_void_p(s.cuda_stream)))
-    s.synchronize()
-    return oi.cpu().numpy(), od.cpu().numpy(), oc.cpu().numpy().astype(np.uint32)

@@ -17,7 +17,7 @@ from paper_2408_02937_b200 import _lib
 
 def header_symbols():
     txt = open(os.path.join(ROOT, "include", "bivf.h")).read()
-    decl = r"^(?:bivf_status|const char\*|int|uint64_t)\s+(bivf_[a-z0-9_]+)\("
+    decl = r"^(?:bivf_status|const char\*|int|uint64_t|void)\s+(bivf_[a-z0-9_]+)\("
     return sorted(set(re.findall(decl, txt, flags=re.M)))
 
 

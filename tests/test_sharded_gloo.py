@@ -15,7 +15,20 @@ import torch.multiprocessing as mp
 import oracle as O
 from helpers import load_scenario
 
-from paper_2408_02937_b200.sharded import ShardedIndex, _torch_all_gather
+from paper_2408_02937_b200.sharded import ShardedIndex
+
+
+def _torch_all_gather(ids, d):
+    """The collective under test: all-gather [nq, k] results over the gloo group."""
+    import torch
+    world = dist.get_world_size()
+    ti = torch.from_numpy(np.ascontiguousarray(ids))
+    td = torch.from_numpy(np.ascontiguousarray(d))
+    gi = torch.empty((world,) + tuple(ti.shape), dtype=ti.dtype)
+    gd = torch.empty((world,) + tuple(td.shape), dtype=td.dtype)
+    dist.all_gather_into_tensor(gi.view(-1), ti.view(-1))
+    dist.all_gather_into_tensor(gd.view(-1), td.view(-1))
+    return gi, gd
 
 
 class OracleShard:

@@ -1,4 +1,6 @@
-"""Profiling driver: build the bench's cfg2 index and run a few 10K-query
+"""Profiling driver: build the bench's index (env PROF_*: cfg2 by default;
+the north-star workload with PROF_NBASE=10000000 PROF_NLIST=4096
+PROF_COMPS=256 PROF_TRAIN=262144 PROF_NPROBE=12) and run a few 10K-query
 searches (no live inserts), for ncu captures of the scan kernel.
 
     ncu --set full --clock-control none --import-source on -k regex:scan_kernel \
@@ -25,6 +27,8 @@ def main():
     D = int(os.environ.get("PROF_D", 128))
     C = int(os.environ.get("PROF_NLIST", 1024))
     metric = int(os.environ.get("PROF_METRIC", 0))
+    comps = int(os.environ.get("PROF_COMPS", 4096))
+    train = int(os.environ.get("PROF_TRAIN", 100_000))
     if metric == 1:
         # inner product, cfg5's generator (tools/bench_configs.py): unit centres u_j,
         # x = normalize(u_j + 0.5 N(0,1)/sqrt(D))
@@ -37,11 +41,11 @@ def main():
             y = u[rng.integers(0, len(u), m)] + (0.5 / np.sqrt(D)) * rng.standard_normal((m, D), dtype=np.float32)
             x[i:i + m] = y / np.linalg.norm(y, axis=1, keepdims=True)
     else:  # SIFT-like: non-negative integers
-        x = bivf.synthetic_dataset(n_base + nq, D, 4096, 2)
+        x = bivf.synthetic_dataset(n_base + nq, D, comps, 2)
         np.maximum(np.rint(x, out=x), 0, out=x)
     base, q = x[:n_base], x[n_base:]
-    cent, _, _ = bivf.kmeans(base[:100_000], C, 10 if D <= 128 else 4, 42)
-    ix = bivf.ClusterIndex.empty(D, C, block_capacity=1024, num_blocks=4096, metric=metric)
+    cent, _, _ = bivf.kmeans(base[:train], C, 10 if D <= 128 else 4, 42)
+    ix = bivf.ClusterIndex.empty(D, C, block_capacity=1024, num_blocks=max(4096, 2 * C + 64), metric=metric)
     ix.set_centroids(cent)
     ix.set_scan_mode("cuda")  # build-time assignment on the CUDA-core quantizer (not captured)
     ix.bulk_load(base, ix.assign_batch(base))
