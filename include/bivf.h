@@ -153,7 +153,9 @@ bivf_status bivf_exceed(const bivf_index* h, uint32_t cluster, int* out);     /*
 bivf_status bivf_rearrange(bivf_index* h, uint32_t cluster);                  /* ivf_index.cpp:476-505 */
 bivf_status bivf_rearrange_sweep(bivf_index* h);                              /* ivf_index.cpp:507-511 */
 /* RearrangeEvent (ivf_index.hpp:33-39): 5 doubles per event (cluster,
- * hops_before, hops_after, merges, duration_us); returns count via *n */
+ * hops_before, hops_after, merges, duration_us).  Takes the oldest
+ * min(cap, pending) events (count via *n); the rest stay queued, so a caller
+ * loops until *n < cap. */
 bivf_status bivf_take_rearrange_events(bivf_index* h, double* out5, uint64_t cap, uint64_t* n);
 
 /* ---- introspection (ivf_index.hpp:84-103, block_store.hpp:75-132) -------- */

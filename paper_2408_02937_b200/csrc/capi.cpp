@@ -321,10 +321,9 @@ bivf_status bivf_rearrange_sweep(bivf_index* h) {
 bivf_status bivf_take_rearrange_events(bivf_index* h, double* out5, uint64_t cap, uint64_t* n) {
     return guard([&] {
         need(n, "n");
-        auto ev = I(h).take_events();
+        auto ev = I(h).take_events(out5 ? (size_t)cap : 0);
         uint64_t m = 0;
         for (auto& e : ev) {
-            if (m >= cap || !out5) break;
             out5[5 * m + 0] = e.cluster;
             out5[5 * m + 1] = (double)e.hops_before;
             out5[5 * m + 2] = (double)e.hops_after;

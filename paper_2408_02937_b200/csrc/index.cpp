@@ -2530,10 +2530,16 @@ void GpuIndex::apply_block_moves(const std::vector<int32_t>& src, const std::vec
     BIVF_CUDA(cudaStreamSynchronize(st));
 }
 
-std::vector<RearrangeEvent> GpuIndex::take_events() {
+// oldest `cap` events; the rest stay queued for the next call
+std::vector<RearrangeEvent> GpuIndex::take_events(size_t cap) {
     std::lock_guard<std::mutex> lk(events_mu_);
     std::vector<RearrangeEvent> out;
-    out.swap(events_);
+    if (cap >= events_.size()) {
+        out.swap(events_);
+    } else {
+        out.assign(events_.begin(), events_.begin() + (std::ptrdiff_t)cap);
+        events_.erase(events_.begin(), events_.begin() + (std::ptrdiff_t)cap);
+    }
     return out;
 }
 

@@ -165,7 +165,7 @@ public:
     bool exceed(uint32_t c) const;
     void rearrange(uint32_t c);
     void rearrange_sweep();
-    std::vector<RearrangeEvent> take_events();
+    std::vector<RearrangeEvent> take_events(size_t cap = SIZE_MAX);
     uint64_t cow_ops() const { return cow_ops_; }
     uint64_t quiescent_ops() const { return quiescent_ops_; }
 

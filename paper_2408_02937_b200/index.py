@@ -219,11 +219,16 @@ class ClusterIndex:
         check(lib().bivf_rearrange_sweep(self._h))
 
     def take_rearrange_events(self):
-        buf = np.zeros(5 * 4096, np.float64)
+        cap = 4096
+        buf = np.zeros(5 * cap, np.float64)
         n = C.c_uint64(0)
-        check(lib().bivf_take_rearrange_events(self._h, buf.ctypes.data, 4096, C.byref(n)))
-        return [(int(buf[5 * i]), int(buf[5 * i + 1]), int(buf[5 * i + 2]), int(buf[5 * i + 3]),
-                 float(buf[5 * i + 4])) for i in range(n.value)]
+        out = []
+        while True:  # the library hands out at most `cap` per call and keeps the rest
+            check(lib().bivf_take_rearrange_events(self._h, buf.ctypes.data, cap, C.byref(n)))
+            out += [(int(buf[5 * i]), int(buf[5 * i + 1]), int(buf[5 * i + 2]), int(buf[5 * i + 3]),
+                     float(buf[5 * i + 4])) for i in range(n.value)]
+            if n.value < cap:
+                return out
 
     def take_events(self):
         """(cluster, hops_before, hops_after, merges) — oracle-comparable form."""

@@ -29,19 +29,21 @@ def main():
     metric = int(os.environ.get("PROF_METRIC", 0))
     comps = int(os.environ.get("PROF_COMPS", 4096))
     train = int(os.environ.get("PROF_TRAIN", 100_000))
+    qoff = int(os.environ.get("PROF_QOFF", 0))  # 1: a fresh query slice per rep (no L2 reuse)
+    nq_tot = nq * reps if qoff else nq
     if metric == 1:
         # inner product, cfg5's generator (tools/bench_configs.py): unit centres u_j,
         # x = normalize(u_j + 0.5 N(0,1)/sqrt(D))
         rng = np.random.default_rng(5)
         u = rng.standard_normal((8192, D), dtype=np.float32)
         u /= np.linalg.norm(u, axis=1, keepdims=True)
-        x = np.empty((n_base + nq, D), np.float32)
+        x = np.empty((n_base + nq_tot, D), np.float32)
         for i in range(0, len(x), 100_000):
             m = min(100_000, len(x) - i)
             y = u[rng.integers(0, len(u), m)] + (0.5 / np.sqrt(D)) * rng.standard_normal((m, D), dtype=np.float32)
             x[i:i + m] = y / np.linalg.norm(y, axis=1, keepdims=True)
     else:  # SIFT-like: non-negative integers
-        x = bivf.synthetic_dataset(n_base + nq, D, comps, 2)
+        x = bivf.synthetic_dataset(n_base + nq_tot, D, comps, 2)
         np.maximum(np.rint(x, out=x), 0, out=x)
     base, q = x[:n_base], x[n_base:]
     cent, _, _ = bivf.kmeans(base[:train], C, 10 if D <= 128 else 4, 42)
@@ -53,7 +55,7 @@ def main():
     ix.set_timing(True)
     for r in range(reps):
         t = time.perf_counter()
-        ix.search_batch(q, k, nprobe)
+        ix.search_batch(q[(r * nq) % len(q):][:nq], k, nprobe)
         print(f"rep {r}: {1e3 * (time.perf_counter() - t):.2f} ms wall, phases(ms)="
               f"{[round(v, 3) for v in ix.last_timings()]}", flush=True)
 
