@@ -195,7 +195,9 @@ GpuIndex::GpuIndex(const bivf_config& in) : cfg_(normalized(in)) {
     // block-table rows start small and grow on demand (grow_rows) up to the
     // configured cap (default: the pool size, i.e. never an insert failure)
     MLB_cap_ = std::max<uint32_t>(1, std::min<uint32_t>(cfg_.max_list_blocks, NB_));
-    MLB_ = std::min<uint32_t>(MLB_cap_, std::max<uint32_t>(8, 2 * ceil_div(NB_, C_)));
+    // (64 entries per list: 2 x 256 B per list, so a Zipf-hot list's chain rarely
+    // forces a table reallocation while searches run)
+    MLB_ = std::min<uint32_t>(MLB_cap_, std::max<uint32_t>(64, 4 * ceil_div(NB_, C_)));
     {
         const char* v = std::getenv("BIVF_COW");
         cow_on_ = !(v && std::string(v) == "0");
@@ -298,6 +300,9 @@ void GpuIndex::alloc_device() {
         tc_ok_ = make_mirror_map(d_arena_mir_.as<float>(), NBS * gpb_, D_, cfg_.metric == BIVF_METRIC_IP,
                                  &map_arena_) ==
                  cudaSuccess;
+        maps_h_ok_ = cfg_.metric != BIVF_METRIC_IP &&
+                     make_mirror_map(d_arena_mir_.as<float>(), NBS * gpb_, D_, false, &maps_h_[1], true) ==
+                         cudaSuccess;
     }
     mirror_ = mirror_view();
     d_bids_.alloc((size_t)NBS * T_ * 8);
@@ -354,6 +359,9 @@ void GpuIndex::ensure_offline_capacity(uint64_t slots) {
         if (make_mirror_map(d_off_mir_.as<float>(), slots / 32, D_, cfg_.metric == BIVF_METRIC_IP, &map_off_) !=
             cudaSuccess)
             tc_ok_ = false;
+        if (cfg_.metric != BIVF_METRIC_IP &&
+            make_mirror_map(d_off_mir_.as<float>(), slots / 32, D_, false, &maps_h_[0], true) != cudaSuccess)
+            maps_h_ok_ = false;
     }
     mirror_ = mirror_view();
 }
@@ -772,6 +780,9 @@ void GpuIndex::grow_offline_preserving(uint64_t slots) {
         if (make_mirror_map(d_off_mir_.as<float>(), cap / 32, D_, cfg_.metric == BIVF_METRIC_IP, &map_off_) !=
             cudaSuccess)
             tc_ok_ = false;
+        if (cfg_.metric != BIVF_METRIC_IP &&
+            make_mirror_map(d_off_mir_.as<float>(), cap / 32, D_, false, &maps_h_[0], true) != cudaSuccess)
+            maps_h_ok_ = false;
     }
     off_slots_cap_ = cap;
     mirror_ = mirror_view();
@@ -1160,7 +1171,8 @@ void GpuIndex::enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Works
                                        d_off_rows_.as<float>(), d_arena_rows_.as<float>(), w.tc,
                                        nullptr, w.out_d,
                                        w.out_i, w.out_cnt, num_sms_, l.stream,
-                                       timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr));
+                                       timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr, 1 << 30,
+                                       maps_h_ok_ && d_arena_rows_.p ? maps_h_ : nullptr));
         if (stats) {
             std::vector<uint32_t> cc(runs);
             BIVF_CUDA(cudaMemcpyAsync(cc.data(), w.tc.ccount, runs * 4, cudaMemcpyDeviceToHost,
@@ -1225,7 +1237,7 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
     BIVF_CUDA(cudaSetDevice(device_));
     Lease* l = acquire_lease();
     const double us_lease = us_since(t_in);
-    double us_gate = 0, us_enq = 0, us_sync = 0;
+    double us_gate = 0, us_enq = 0, us_sync = 0, us_prep = 0;
     struct Rel {
         GpuIndex* g;
         Lease* l;
@@ -1234,6 +1246,7 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
     const uint64_t slice = 32768;
     for (uint64_t s = 0; s < nq; s += slice) {
         const uint32_t m = (uint32_t)std::min(slice, nq - s);
+        const auto t_p = TClock::now();
         const LaunchShape sh = pick_shape(m, (uint32_t)k, (uint32_t)nprobe, C_, num_sms_);
         Workspace w = carve(*l, m, (uint32_t)k, (uint32_t)nprobe, sh.maxch, sh.fnch);
         const size_t in_b = (size_t)m * D_ * 4;
@@ -1243,6 +1256,7 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
         const bool o_pin = is_pinned(out_d + s * k) && is_pinned(out_ids + s * k) &&
                            (!out_cnt || is_pinned(out_cnt + s));
         l->pin.ensure(in_b + out_b + 256);
+        us_prep += us_since(t_p);
         char* pin = l->pin.as<char>();
         float* pd = reinterpret_cast<float*>(pin + align_up(in_b, 64));
         long long* pi = reinterpret_cast<long long*>(pd + (size_t)m * k + ((m * k) & 1));
@@ -1294,7 +1308,8 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
     }
     if (trace_threshold_us() > 0)
         trace("search", us_since(t_in),
-              "nq=" + std::to_string(nq) + " lease=" + std::to_string((int)us_lease) + " gate=" +
+              "nq=" + std::to_string(nq) + " lease=" + std::to_string((int)us_lease) + " prep=" +
+                  std::to_string((int)us_prep) + " gate=" +
                   std::to_string((int)us_gate) + " enqueue=" + std::to_string((int)us_enq) + " device_wait=" +
                   std::to_string((int)us_sync));
 }
@@ -1325,13 +1340,13 @@ void GpuIndex::shard_quantize(ShardCtx& s, uint32_t g) {
     BIVF_CUDA(cudaSetDevice(device_));
     cudaStream_t st = s.lease->stream;
     BIVF_CUDA(launch_pad_rows(s.w.qraw, s.nq, D_, Dp_, s.w.queries, st));
+    if (s.P == C_) {  // every list probed: every shard fills all rows (no all-gather)
+        BIVF_CUDA(launch_all_probes(s.w.probes, s.nq, C_, st));
+        return;
+    }
     const uint32_t q0 = g * s.slice;
     if (q0 >= s.nq) return;
     const uint32_t m = std::min(s.slice, s.nq - q0);
-    if (s.P == C_) {
-        BIVF_CUDA(launch_all_probes(s.w.probes + (size_t)q0 * s.P, m, C_, st));
-        return;
-    }
     enqueue_quantizer(st, m, s.P, pick_shape(s.nq_pad, s.k, s.P, C_, num_sms_).fnch, s.w, q0);
 }
 
@@ -1683,8 +1698,11 @@ void GpuIndex::publish(const std::vector<ListPub>& pubs) {
     const size_t o_idx = 0, o_start = align_up(n * 4, 16), o_count = o_start + align_up(n * 8, 16),
                  o_row = o_count + align_up(n * 4, 16), o_len = o_row + align_up(n * 8, 16),
                  total = o_len + align_up(n * 4, 16);
-    h_pub_.ensure(total);
-    s_pub_.ensure(total);
+    // sized for every list at once on first use: pinned regrowth (cudaFreeHost +
+    // cudaHostAlloc) would stall the lease threads' CUDA calls mid-window
+    const size_t full = 48 * (size_t)C_ + 256;
+    h_pub_.ensure(std::max(total, full));
+    s_pub_.ensure(std::max(total, full));
     char* h = h_pub_.as<char>();
     for (size_t i = 0; i < n; ++i) {
         reinterpret_cast<uint32_t*>(h + o_idx)[i] = pubs[i].c;

@@ -378,6 +378,8 @@ private:
     void refresh_size();
 
     CUtensorMap map_off_{}, map_arena_{};
+    CUtensorMap maps_h_[2]{};  // hi-plane boxes of the same mirrors (scan_vm_kernel): offline, arena
+    bool maps_h_ok_ = false;
     bool tc_ok_ = false;
     int scan_mode_ = 0;  // 0 auto, 1 CUDA-core only, 2 tensor-core when supported
     std::atomic<bool> graphs_on_{true};  // BIVF_GRAPHS=0 disables; a failed capture too

@@ -134,6 +134,8 @@ struct TcParams {
     uint32_t D, Dk, Dp, k, P, maxch;
     uint32_t brow, gstride, nkc;  // TMA box rows, map rows per group, K-chunks per group (wide: Dk / brow)
     uint32_t seed_groups;        // seeding pass: scan only the first seed_groups groups, no run output
+    uint32_t qt;                 // plan tile: pairs per work item (kM, or kVmQ for scan_vm_kernel)
+    uint32_t dbg;                // BIVF_VM_DBG bits (debugging aid, 0 in production)
     const float* centroids;      // [C][D] row-major
     const float* queries;        // [nq][Dp]
     const uint32_t* snap_off;
@@ -275,18 +277,22 @@ __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
+    // the load and its wait in ONE asm statement: the destination registers are
+    // undefined until tcgen05.wait::ld, and with two statements the compiler may
+    // schedule their consumers between the two
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
         "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
           "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
           "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
           "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
           "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
           "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        : "r"(taddr)
+        : "memory");
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
@@ -321,9 +327,9 @@ __device__ __forceinline__ TcItem tc_decode(const TcParams& p, uint32_t it) {
     const uint32_t local = it - p.item_off[lo];
     const uint32_t nch = p.nch[lo];
     const uint32_t tile = local / nch, h = local - tile * nch;
-    const uint32_t q0 = p.qoff[lo] + tile * kM;
+    const uint32_t q0 = p.qoff[lo] + tile * p.qt;
     d.pairs = p.plist + q0;
-    d.npairs = min((uint32_t)kM, p.qoff[lo + 1] - q0);
+    d.npairs = min(p.qt, p.qoff[lo + 1] - q0);
     d.off = p.snap_off[lo];
     d.len = p.snap_len[lo];
     const uint32_t ng = ivf_ngroups(p.L, d.off, d.len);
@@ -1050,6 +1056,544 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
 }
 
+// ------------------------------------------------------------------ vector-major scan
+// scan_vm_kernel (L2, D <= 128, k <= 32): the list scan with the roles of the
+// MMA operands swapped.  A work item's queries (<= kVmQ centred residuals,
+// split into bf16 hi + lo planes) are the B operand (N <= 32 columns, written
+// once per item into shared memory); the list's stored vectors are the A
+// operand, 128 per MMA (M = a "unit" of four 32-slot groups), streamed from
+// the scan mirror's bf16 hi plane only (K rows x 64 B per group: half the bytes
+// of the 3xBF16 scan).  Every TMEM lane holds one vector against every query of
+// the tile, so a thread filters (vector, query) pairs with no idle rows when a
+// list has few queries (north-star: ~29 queries per list).
+// Bound (mirror.cuh): s_hi = bf16_rn(s) (unit roundoff 2^-8), |s_d - s_hi_d| <=
+// 2^-8 |s_d|; the query r = r_hi + r_lo + rho, |rho_d| <= 2^-16 |r_d|; bf16
+// products are exact in fp32: |P - r.s| <= ((1 + 2^-16) 2^-8 + 2^-16) sum|r_d s_d|
+// + fp32 accumulation (2K/16 MMA steps, <= 2^-17) <= 2^-7.98 |r||s|, so
+// a = nr + ns - 2P is off by <= 2^-6.98 |r||s| from |r-s|^2, plus the norm /
+// centring / exact-rounding terms of the 3xBF16 bound (kEpsRel).  kVmCross = 2^-6
+// carries a ~2x margin on the cross term.
+//   eps = kVmCross |r||s| + kEpsRel (nr + ns) + kEpsRel |a|
+// Pass 1 (every pair, superset of lb <= theta; |r||s| <= (nr+ns)/2):
+//   P >= U_n + V_s,  U_n = (c1 nr_n - c2 theta_n) / 2,  V_s = c1 ns / 2
+// The per-query threshold theta_n starts at the query's shared threshold (the
+// exact k-th distance over the first vectors of its nearest list, vm_seed_kernel,
+// tightened by every run) and shrinks with the k smallest upper bounds of the
+// candidates (one bookkeeping lane per query); candidates (lb, ub, slot) are
+// appended to per-(warpgroup, query) shared lists and compacted against theta.
+// Run output = the refine kernel's format (k upper bounds + candidates per
+// (pair, chunk, warpgroup)).
+constexpr int kVmQ = 32;       // query columns per work item (MMA N <= 32)
+constexpr int kVmNS = 4;       // A stage slots (one unit of 4 groups each)
+constexpr int kVmNR = 8;       // norm ring slots (a unit's 4 x 32 |s|^2)
+constexpr int kVmNB = 4;       // TMEM accumulators (32 columns each)
+constexpr int kVmKC = 48;      // candidate slots per (warpgroup, query)
+constexpr uint32_t kVmSlot = 4u * kMaxD * 64u;  // bytes per A slot (4 groups x K rows x 64 B, K <= 128)
+constexpr uint32_t kVmPlane = kMaxD * 64u;      // bytes per B plane (K rows x 32 queries bf16)
+constexpr float kVmCross = 1.0f / 64.0f;
+constexpr float kVmKappa = 0.5f * kVmCross + kEpsRel;
+constexpr float kVmC2 = 1.0f / (1.0f - kEpsRel);
+constexpr float kVmC1 = 1.0f - kVmKappa * kVmC2 - 1.0f / 262144.0f;  // 2^-18 slack for the test's roundings
+
+// byte offset of element (row k, query column n < 32) of a B plane: MN-major
+// SWIZZLE_64B (64-byte rows of 32 bf16, the 16-byte chunk index XOR (k >> 1) & 3),
+// the layout TMA writes for the A stages (tools/tc_probe_swap.cu checks both)
+__device__ __forceinline__ uint32_t vm_boff(uint32_t k, uint32_t n) {
+    return k * 64u + ((((n >> 3) ^ (k >> 1)) & 3u) << 4) + (n & 7u) * 2u;
+}
+
+// one K-step of the vector-major MMA: D += A * B_hi + A * B_lo (A, B from smem)
+__device__ __forceinline__ void mma_vm_elect(uint32_t dcol, uint64_t ad, uint64_t bh, uint64_t bl,
+                                             uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %5, 0;\n\t"
+        "setp.eq.b32 t, 0, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %4, t;\n\t}" ::"r"(dcol),
+        "l"(ad), "l"(bh), "l"(bl), "r"(idesc), "r"(accum)
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t vm_nvalid(const TcParams& p, const TcItem& d, uint32_t j) {
+    const uint32_t og = (d.off + 31u) >> 5;
+    if (j < og) return min(32u, d.off - 32u * j);
+    const uint32_t jj = j - og, mid = jj / p.L.gpb, gi = jj - mid * p.L.gpb;
+    return min(32u, min(p.L.T, d.len - mid * p.L.T) - 32u * gi);
+}
+
+__device__ __forceinline__ const float* cand_row(const TcParams& p, uint32_t c, uint32_t off, uint32_t j,
+                                                 uint32_t s);
+
+template <int KT>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    scan_vm_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_off,
+                   const __grid_constant__ CUtensorMap map_arena) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t raw_s = smem_u32(smem_raw);
+    const uint32_t pad = ((raw_s + 1023u) & ~1023u) - raw_s;
+    unsigned char* sA = smem_raw + pad;                               // kVmNS * kVmSlot
+    unsigned char* sB = sA + kVmNS * kVmSlot;                          // [2 items][hi, lo] planes
+    float2* cand = reinterpret_cast<float2*>(sB + 4 * kVmPlane);       // [2 wg][kVmQ][kVmKC] (lb, ub)
+    uint32_t* cloc = reinterpret_cast<uint32_t*>(cand + 2 * kVmQ * kVmKC);  // [2][kVmQ][kVmKC]
+    float* nslots = reinterpret_cast<float*>(cloc + 2 * kVmQ * kVmKC);  // [kVmNR][4 groups][32] |s|^2
+    float* q_thr = nslots + kVmNR * 4 * 32;    // [2 items][kVmQ] theta
+    float* q_u = q_thr + 2 * kVmQ;             // [2][kVmQ] pass-1 offsets U
+    float* q_nr = q_u + 2 * kVmQ;              // [2][kVmQ] |r|^2
+    float* q_rn = q_nr + 2 * kVmQ;             // [2][kVmQ] |r|
+    float* cent_s = q_rn + 2 * kVmQ;           // [kMaxD] the item's centroid
+    float* nrp = cent_s + kMaxD;               // [8][kVmQ] partial |r|^2
+    uint32_t* q_id = reinterpret_cast<uint32_t*>(nrp + 8 * kVmQ);  // [2][kVmQ] query index
+    uint32_t* q_cnt = q_id + 2 * kVmQ;         // [2 items][2 wg][kVmQ]
+    uint32_t* q_ovf = q_cnt + 4 * kVmQ;        // [2][2][kVmQ]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(q_ovf + 4 * kVmQ);
+    uint64_t* full = bars;                     // kVmNS
+    uint64_t* empty = full + kVmNS;            // kVmNS
+    uint64_t* acc_full = empty + kVmNS;        // kVmNB
+    uint64_t* acc_empty = acc_full + kVmNB;    // kVmNB
+    uint64_t* b_full = acc_empty + kVmNB;      // 2
+    uint64_t* b_free = b_full + 2;             // 2
+    uint64_t* it_full = b_free + 2;            // kRing
+    uint64_t* it_empty = it_full + kRing;      // kRing
+    uint64_t* nfull = it_empty + kRing;        // kVmNR
+    uint64_t* nempty = nfull + kVmNR;          // kVmNR
+    TcItem* ring = reinterpret_cast<TcItem*>(nempty + kVmNR);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t K = p.Dk;  // mirror rows per plane (D rounded up to 16)
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kVmNS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < kVmNB; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 4);  // the 4 warps of the unit's warpgroup
+        }
+        for (int r = 0; r < kVmNR; ++r) {
+            mbar_init(&nfull[r], 1);
+            mbar_init(&nempty[r], 4);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&b_full[a], 1);
+            mbar_init(&b_free[a], 1);
+        }
+        for (int s = 0; s < kRing; ++s) {
+            mbar_init(&it_full[s], 1);
+            mbar_init(&it_empty[s], 1 + 4 * kWG);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(32 * kVmNB)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t n_items = *p.n_items_ptr;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            auto fetch = [&](uint32_t seq) -> bool {
+                const uint32_t rs = seq % kRing;
+                mbar_wait(&it_empty[rs], ((seq / kRing) & 1) ^ 1);
+                const uint32_t it = atomicAdd(p.item_ctr, 1u);
+                TcItem d{};
+                if (it < n_items) d = tc_decode(p, it);
+                ring[rs] = d;
+                mbar_arrive(&it_full[rs]);
+                return d.valid != 0;
+            };
+            uint32_t unit = 0;
+            bool have = fetch(0);
+            for (uint32_t seq = 0; have; ++seq) {
+                const TcItem d = ring[seq % kRing];
+                have = fetch(seq + 1);
+                const uint32_t og = (d.off + 31u) >> 5;
+                const uint64_t offg0 = og ? p.L.off_start[d.c] / 32u : 0ull;
+                const int32_t* trow = p.L.rowptr[d.c];
+                uint32_t cmid = 0xffffffffu;
+                uint64_t cblk = 0;
+                for (uint32_t j0 = d.g0; j0 < d.g1; j0 += 4, ++unit) {
+                    const uint32_t ng = min(4u, d.g1 - j0);
+                    uint64_t gidx[4];
+                    bool gar[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        if ((uint32_t)h >= ng) break;
+                        const uint32_t j = j0 + h;
+                        if (j < og) {
+                            gar[h] = false;
+                            gidx[h] = offg0 + j;
+                        } else {
+                            const uint32_t jj = j - og, mid = jj / p.L.gpb, gi = jj - mid * p.L.gpb;
+                            if (mid != cmid) {
+                                cmid = mid;
+                                cblk = (uint64_t)trow[mid];
+                            }
+                            gar[h] = true;
+                            gidx[h] = cblk * p.L.gpb + gi;
+                        }
+                    }
+                    const uint32_t slot = unit % kVmNS;
+                    mbar_wait(&empty[slot], ((unit / kVmNS) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[slot], ng * K * 64u);
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        if ((uint32_t)h >= ng) break;
+                        // the group's hi plane: rows [0, K) of its 2K mirror rows
+                        tma_load_2d(sA + slot * kVmSlot + h * K * 64u, gar[h] ? &map_arena : &map_off, 0,
+                                    (int)(gidx[h] * p.gstride), &full[slot]);
+                    }
+                    if (p.dbg & 512u) mbar_wait(&full[slot], (unit / kVmNS) & 1);  // debugging aid
+                    const uint32_t nsl = unit % kVmNR;
+                    mbar_wait(&nempty[nsl], ((unit / kVmNR) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&nfull[nsl], ng * 128u);
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        if ((uint32_t)h >= ng) break;
+                        bulk_g2s(nslots + (nsl * 4 + h) * 32,
+                                 (gar[h] ? p.arena_nrm : p.off_nrm) + gidx[h] * kNormFloats, 128u, &nfull[nsl]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        // D f32, A bf16 MN-major (the stage's 4 groups, LBO = K*64), B bf16 MN-major
+        // (the item's query planes), M = 128, N = the item's columns rounded to 16
+        const uint32_t idesc0 = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | (8u << 24);
+        const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
+        uint32_t unit = 0;
+        for (uint32_t seq = 0;; ++seq) {
+            const uint32_t rs = seq % kRing;
+            mbar_wait(&it_full[rs], (seq / kRing) & 1);
+            const TcItem d = ring[rs];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&it_empty[rs]);
+            if (!d.valid) break;
+            const uint32_t ib = seq & 1;
+            mbar_wait(&b_full[ib], (seq >> 1) & 1);
+            const uint32_t N = max(16u, (d.npairs + 15u) & ~15u);
+            const uint32_t idesc = idesc0 | ((N >> 3) << 17);
+            const uint32_t bh0 = sb0 + ib * 2 * kVmPlane, bl0 = bh0 + kVmPlane;
+            for (uint32_t j0 = d.g0; j0 < d.g1; j0 += 4, ++unit) {
+                const uint32_t b = unit % kVmNB, slot = unit % kVmNS;
+                mbar_wait(&acc_empty[b], ((unit / kVmNB) & 1) ^ 1);
+                mbar_wait(&full[slot], (unit / kVmNS) & 1);
+                __syncwarp();
+                tc_fence_after();
+                const uint32_t dcol = tmem_base + b * 32u;
+                const uint32_t a0 = sa0 + slot * kVmSlot;
+                for (uint32_t ks = 0; ks < K / 16; ++ks)
+                    mma_vm_elect(dcol, umma_desc(a0 + ks * 1024u, K * 64u, 512, 4),
+                                 umma_desc(bh0 + ks * 1024u, kVmPlane, 512, 4),
+                                 umma_desc(bl0 + ks * 1024u, kVmPlane, 512, 4), idesc, ks);
+                mma_commit_elect(&empty[slot]);
+                __syncwarp();
+                mma_commit_elect(&acc_full[b]);
+                __syncwarp();
+                if (p.dbg & 256u) mbar_wait(&acc_full[b], (unit / kVmNB) & 1);  // debugging aid
+            }
+            mma_commit_elect(&b_free[ib]);
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------------------------ math warpgroups
+        const int wg = (warp - 2) >> 2;
+        const int q4 = warp & 3;                          // TMEM lane quarter = group of the unit
+        const int wt = threadIdx.x - 64 - 128 * wg;       // 0..127 within the warpgroup
+        const int t256 = threadIdx.x - 64;                // 0..255 over both warpgroups
+        const bool book = wt < 32;                        // bookkeeping lane of query column wt
+        // item seq's B planes + per-query state (buffer seq & 1), both warpgroups
+        auto build = [&](uint32_t seq, TcItem& d) -> bool {
+            const uint32_t rs = seq % kRing;
+            mbar_wait(&it_full[rs], (seq / kRing) & 1);
+            d = ring[rs];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&it_empty[rs]);
+            // both warpgroups are done with item seq - 2's state and with the run
+            // output of item seq - 2 (the candidate lists are reused by the item
+            // after it): taken for the end marker too
+            named_bar(3, 256);
+            if (!d.valid) return false;
+            const uint32_t ib = seq & 1;
+            if (seq >= 2) mbar_wait(&b_free[ib], ((seq - 2) >> 1) & 1);
+            if (t256 < (int)K) cent_s[t256] = (uint32_t)t256 < p.D ? __ldg(p.centroids + (uint64_t)d.c * p.D + t256) : 0.f;
+            named_bar(3, 256);
+            {
+                const uint32_t n = t256 & 31, h = t256 >> 5;  // column n, dims [16h, 16h + 16)
+                const bool act = n < d.npairs;
+                const uint32_t pair = act ? d.pairs[n] : 0u;
+                const float* q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
+                float nh = 0.f;
+                if (16 * h < K) {
+                    unsigned char* bh = sB + ib * 2 * kVmPlane;
+                    unsigned char* bl = bh + kVmPlane;
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4) {
+                        const uint32_t k0 = 16 * h + i;
+                        const float4 qv = (act && k0 < p.Dp) ? __ldg(reinterpret_cast<const float4*>(q + k0))
+                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float r = __fsub_rn(qa[e], act ? cent_s[k0 + e] : 0.f);
+                            nh = __fadd_rn(nh, __fmul_rn(r, r));
+                            const __nv_bfloat16 rh = __float2bfloat16_rn(r);
+                            const __nv_bfloat16 rl = __float2bfloat16_rn(__fsub_rn(r, __bfloat162float(rh)));
+                            *reinterpret_cast<__nv_bfloat16*>(bh + vm_boff(k0 + e, n)) = rh;
+                            *reinterpret_cast<__nv_bfloat16*>(bl + vm_boff(k0 + e, n)) = rl;
+                        }
+                    }
+                }
+                nrp[h * kVmQ + n] = nh;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // planes -> the MMA's async proxy
+            named_bar(3, 256);
+            if ((p.dbg & 8192u) && t256 == 0) __nanosleep(20000);  // debugging aid
+            if (t256 == 0) mbar_arrive(&b_full[ib]);
+            if (t256 < kVmQ) {
+                const uint32_t n = t256;
+                const bool act = n < d.npairs;
+                float nr = 0.f;
+#pragma unroll
+                for (int h = 0; h < 8; ++h) nr = __fadd_rn(nr, nrp[h * kVmQ + n]);  // fixed order
+                const uint32_t qi = act ? d.pairs[n] / p.P : 0u;
+                const float th = act ? qthr_dec(__ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + qi))
+                                     : -__int_as_float(0x7f800000);
+                q_id[ib * kVmQ + n] = qi;
+                q_nr[ib * kVmQ + n] = nr;
+                q_rn[ib * kVmQ + n] = sqrtf(nr);
+                q_thr[ib * kVmQ + n] = th;
+                q_u[ib * kVmQ + n] = act ? 0.5f * fmaf(kVmC1, nr, -kVmC2 * th) : __int_as_float(0x7f800000);
+                q_cnt[(ib * 2 + 0) * kVmQ + n] = 0;
+                q_cnt[(ib * 2 + 1) * kVmQ + n] = 0;
+                q_ovf[(ib * 2 + 0) * kVmQ + n] = 0;
+                q_ovf[(ib * 2 + 1) * kVmQ + n] = 0;
+            }
+            named_bar(3, 256);
+            return true;
+        };
+        uint32_t unit = 0;
+        TcItem d;
+        bool have = build(0, d);
+        for (uint32_t seq = 0; have; ++seq) {
+            TcItem dn;
+            const bool hn = build(seq + 1, dn);
+            const uint32_t ib = seq & 1;
+            const float* thr = q_thr + ib * kVmQ;
+            float* uu = q_u + ib * kVmQ;
+            const float* nrv = q_nr + ib * kVmQ;
+            const float* rnv = q_rn + ib * kVmQ;
+            uint32_t* cnt = q_cnt + (ib * 2 + wg) * kVmQ;
+            uint32_t* ovf = q_ovf + (ib * 2 + wg) * kVmQ;
+            float2* mycand = cand + wg * kVmQ * kVmKC;
+            uint32_t* myloc = cloc + wg * kVmQ * kVmKC;
+            // bookkeeping lane state (query column wt): the k smallest upper bounds of
+            // this warpgroup's candidates, ascending after -inf sentinels
+            float ubl[KT];
+#pragma unroll
+            for (int i = 0; i < KT; ++i)
+                ubl[i] = i < KT - (int)p.k ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
+            uint32_t seen = 0;
+            const bool bact = book && (uint32_t)wt < d.npairs;
+            const uint32_t bq = bact ? q_id[ib * kVmQ + wt] : 0u;
+            uint32_t qg = bact ? __ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + bq) : 0xffffffffu;
+            for (uint32_t j0 = d.g0; j0 < d.g1; j0 += 4, ++unit) {
+                if ((unit & 1u) != (uint32_t)wg) continue;
+                const uint32_t b = unit % kVmNB, nsl = unit % kVmNR;
+                mbar_wait(&acc_full[b], (unit / kVmNB) & 1);
+                __syncwarp();
+                tc_fence_after();
+                float P[32];
+                tmem_ld32(tmem_base + ((uint32_t)(32 * q4) << 16) + b * 32u, P);
+                mbar_wait(&nfull[nsl], (unit / kVmNR) & 1);
+                const uint32_t j = j0 + (uint32_t)q4;
+                const uint32_t nv = j < d.g1 ? vm_nvalid(p, d, j) : 0u;
+                const float nsv = nslots[(nsl * 4 + q4) * 32 + lane];
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {  // accumulator and norm slot are free again
+                    mbar_arrive(&acc_empty[b]);
+                    mbar_arrive(&nempty[nsl]);
+                }
+                const bool valid = (uint32_t)lane < nv;
+                const float V = 0.5f * kVmC1 * nsv;
+                // pass 1: max_n (P_n - U_n) >= V  (U_n = +inf for columns past the tile's pairs)
+                float m0 = -__int_as_float(0x7f800000), m1 = m0;
+#pragma unroll
+                for (int n = 0; n < kVmQ; n += 4) {
+                    const float4 u4 = *reinterpret_cast<const float4*>(uu + n);
+                    m0 = fmaxf(m0, fmaxf(P[n] - u4.x, P[n + 1] - u4.y));
+                    m1 = fmaxf(m1, fmaxf(P[n + 2] - u4.z, P[n + 3] - u4.w));
+                }
+                if (valid && (fmaxf(m0, m1) >= V || (p.dbg & 16u))) {
+                    // pass 2: exact bounds of the surviving pairs, append to the query lists
+                    const float sn = sqrtf(nsv);
+                    const uint32_t loc = (j << 5) | (uint32_t)lane;
+#pragma unroll
+                    for (int n = 0; n < kVmQ; ++n) {
+                        if (P[n] - uu[n] >= V || ((p.dbg & 16u) && n < (int)d.npairs)) {
+                            const float nr = nrv[n];
+                            const float a = fmaf(-2.f, P[n], nr + nsv);
+                            const float e = fmaf(kVmCross, rnv[n] * sn,
+                                                 fmaf(kEpsRel, nr + nsv, fmaf(kEpsRel, fabsf(a), 1e-30f)));
+                            const float lb = a - e;
+                            if (p.dbg & 16384u) {  // debugging aid: the bound at pass 2
+                                const uint32_t qi = q_id[ib * kVmQ + n];
+                                const float* xr = cand_row(p, d.c, d.off, j, (uint32_t)lane);
+                                float ex = 0.f;
+                                for (uint32_t dd = 0; dd < p.D; ++dd)
+                                    ex = l2_step(ex, p.queries[(uint64_t)qi * p.Dp + dd], xr[dd]);
+                                if (!(lb <= ex && ex <= a + e))
+                                    printf("[vm-p2] q=%u c=%u j=%u lane=%d n=%d P=%.9g nr=%.9g ns=%.9g a=%.9g e=%.9g exact=%.9g "
+                                           "unit=%u b=%u wg=%d\n", qi, d.c, j, lane, n, P[n], nr, nsv, a, e, ex, unit, b, wg);
+                            }
+                            if (lb <= thr[n]) {
+                                const uint32_t at = atomicAdd(&cnt[n], 1u);
+                                if (at < (uint32_t)kVmKC) {
+                                    mycand[n * kVmKC + at] = make_float2(lb, a + e);
+                                    myloc[n * kVmKC + at] = (p.dbg & 32768u) ? (loc | ((uint32_t)n << 24) | ((uint32_t)unit << 29)) : loc;
+                                } else {
+                                    ovf[n] = 1u;
+                                }
+                            }
+                        }
+                    }
+                }
+                named_bar(1 + wg, 128);  // this unit's appends are in
+                if (bact && (p.dbg & 131072u)) {  // debugging aid: every listed entry against the exact distance
+                    const uint32_t c = min(cnt[wt], (uint32_t)kVmKC);
+                    for (uint32_t i = 0; i < c; ++i) {
+                        const float2 v = mycand[wt * kVmKC + i];
+                        const uint32_t loc = myloc[wt * kVmKC + i];
+                        const float* xr = cand_row(p, d.c, d.off, loc >> 5, loc & 31u);
+                        float ex = 0.f;
+                        for (uint32_t dd = 0; dd < p.D; ++dd)
+                            ex = l2_step(ex, p.queries[(uint64_t)bq * p.Dp + dd], xr[dd]);
+                        if (!(v.x <= ex && ex <= v.y))
+                            printf("[vm-bk] q=%u c=%u unit=%u j0=%u i=%u c=%u seen=%u loc=%u lb=%.9g ub=%.9g exact=%.9g\n", bq,
+                                   d.c, unit, j0, i, c, seen, loc, v.x, v.y, ex);
+                    }
+                }
+                if (bact) {
+                    const uint32_t c = min(cnt[wt], (uint32_t)kVmKC);
+                    for (uint32_t i = seen; i < c; ++i) {
+                        float x = mycand[wt * kVmKC + i].y;
+                        if (x < ubl[KT - 1]) {
+#pragma unroll
+                            for (int r = 0; r < KT; ++r) {
+                                const float lo = fminf(x, ubl[r]);
+                                x = fmaxf(x, ubl[r]);
+                                ubl[r] = lo;
+                            }
+                        }
+                    }
+                    seen = c;
+                    const float tl = (p.dbg & 1u) ? __int_as_float(0x7f800000) : ubl[KT - 1];
+                    const float tg = (p.dbg & 4u) ? __int_as_float(0x7f800000) : qthr_dec(qg);
+                    const float t0 = q_thr[ib * kVmQ + wt];
+                    const float th = fminf(t0, fminf(tl, tg));
+                    if (th < t0) {
+                        q_thr[ib * kVmQ + wt] = th;
+                        uu[wt] = 0.5f * fmaf(kVmC1, nrv[wt], -kVmC2 * th);
+                    }
+                    if (tl < tg && !(p.dbg & 4u)) atomicMin(reinterpret_cast<uint32_t*>(p.qthr) + bq, f2ord(tl));
+                    if (c >= (uint32_t)kVmKC / 2 && !(p.dbg & 8u)) {  // compact against the current threshold
+                        uint32_t w = 0;
+                        for (uint32_t i = 0; i < c; ++i) {
+                            const float2 v = mycand[wt * kVmKC + i];
+                            if (v.x <= th) {
+                                mycand[wt * kVmKC + w] = v;
+                                myloc[wt * kVmKC + w] = myloc[wt * kVmKC + i];
+                                ++w;
+                            }
+                        }
+                        cnt[wt] = w;
+                        seen = w;
+                    }
+                    qg = __ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + bq);  // for the next unit
+                }
+                named_bar(1 + wg, 128);  // compaction done before the next unit appends
+            }
+            if ((p.dbg & 65536u) && bact) {  // debugging aid: B column wt holds query bq's residual
+                const unsigned char* bh = sB + ib * 2 * kVmPlane;
+                uint32_t badk = 0xffffffffu;
+                for (uint32_t kk = 0; kk < p.D; ++kk) {
+                    const float r = __fsub_rn(p.queries[(uint64_t)bq * p.Dp + kk], p.centroids[(uint64_t)d.c * p.D + kk]);
+                    const float h = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(bh + vm_boff(kk, wt)));
+                    if (h != __bfloat162float(__float2bfloat16_rn(r)) && badk == 0xffffffffu) badk = kk;
+                }
+                if (badk != 0xffffffffu)
+                    printf("[vm-B] column %d of item (c=%u g0=%u np=%u) is not query %u (first bad dim %u) seq=%u blk=%u\n", wt,
+                           d.c, d.g0, d.npairs, bq, badk, seq, blockIdx.x);
+            }
+            // run output (refine_kernel's format): k upper bounds + candidates
+            if (bact && !p.seed_groups) {
+                const uint32_t pair = d.pairs[wt];
+                const uint64_t run = (((uint64_t)pair * p.maxch + d.chunk) << 1) | (uint32_t)wg;
+#pragma unroll
+                for (int i = 0; i < KT; ++i)
+                    if (i >= KT - (int)p.k) p.ub[run * p.k + (i - (KT - (int)p.k))] = ubl[i];
+                const float th = q_thr[ib * kVmQ + wt];
+                const uint32_t c = min(cnt[wt], (uint32_t)kVmKC);
+                uint32_t w = 0;
+                if (!ovf[wt]) {
+                    for (uint32_t i = 0; i < c; ++i) {
+                        const float2 v = mycand[wt * kVmKC + i];
+                        if (p.dbg & 32u) {  // debugging aid: the kept bounds against the exact distance
+                            uint32_t loc = myloc[wt * kVmKC + i];
+                            if (p.dbg & 32768u) {
+                                if (((loc >> 24) & 31u) != (uint32_t)wt)
+                                    printf("[vm-col] entry of column %u in list %d (i=%u c=%u cnt=%u unit3=%u)\n", (loc >> 24) & 31u, wt, i, c, cnt[wt], loc >> 29);
+                                loc &= 0xffffffu;
+                            }
+                            const float* xr = cand_row(p, d.c, d.off, loc >> 5, loc & 31u);
+                            float ex = 0.f;
+                            for (uint32_t dd = 0; dd < p.D; ++dd)
+                                ex = l2_step(ex, p.queries[(uint64_t)bq * p.Dp + dd], xr[dd]);
+                            if (!(v.x <= ex && ex <= v.y))
+                                printf("[vm-bound] q=%u c=%u loc=%u lb=%.9g ub=%.9g exact=%.9g th=%.9g seq=%u ib=%u g0=%u g1=%u "
+                                       "np=%u n=%d wg=%d blk=%u\n", bq, d.c, loc, v.x, v.y, ex, th, seq, ib, d.g0, d.g1,
+                                       d.npairs, wt, wg, blockIdx.x);
+                        }
+                        if (v.x <= th) {
+                            p.clb[run * kKC + w] = v.x;
+                            p.cloc[run * kKC + w] = myloc[wt * kVmKC + i] & ((p.dbg & 32768u) ? 0xffffffu : 0xffffffffu);
+                            ++w;
+                        }
+                    }
+                }
+                p.ccount[run] = ovf[wt] ? kOverflow : w;
+                if ((p.dbg & 32u) && ovf[wt]) printf("[vm-ovf] q=%u c=%u chunk=%u wg=%d\n", bq, d.c, d.chunk, wg);
+                if (p.dbg & 32u) {  // the run's upper bounds must be sorted, finite count <= candidates seen
+                    for (int i = 1; i < KT; ++i)
+                        if (ubl[i] < ubl[i - 1]) printf("[vm-ubl] unsorted q=%u\n", bq);
+                }
+            }
+            d = dn;
+            have = hn;
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(32 * kVmNB)
+                     : "memory");
+    }
+}
+
 // ------------------------------------------------------------------ refine
 // One warp per query: threshold = k-th smallest upper bound over all of the
 // query's (probe, chunk) runs; the surviving candidates (lower bound <=
@@ -1342,6 +1886,46 @@ __device__ __forceinline__ uint64_t warp_elem(const uint64_t (&v)[R], uint32_t e
         if (e >> 5 == (uint32_t)j) x = t;
     }
     return x;
+}
+// Seed of scan_vm_kernel's per-query thresholds (one warp per query): the exact
+// k-th smallest distance (sequential fp32 over the mirror's row copy, the
+// reference's bits) among the first two groups (<= 64 stored vectors) met
+// walking the query's probes in rank order (rank 0 = its nearest list).  Those
+// vectors are probed, so the value bounds the final k-th distance; fewer than k
+// vectors leave the threshold at "none".
+__global__ void vm_seed_kernel(TcParams p, const long long* probes, uint32_t nq) {
+    extern __shared__ float qsm[];  // [warps][Dp]
+    const uint32_t nw = blockDim.x >> 5, wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t q = blockIdx.x * nw + wq;
+    if (q >= nq) return;
+    float* qs = qsm + wq * p.Dp;
+    for (uint32_t i = lane; i < p.D; i += 32) qs[i] = p.queries[(uint64_t)q * p.Dp + i];
+    __syncwarp();
+    uint64_t v[2] = {~0ull, ~0ull};
+    uint32_t rows = 0, nvec = 0;
+    for (uint32_t r = 0; r < p.P && rows < 2; ++r) {
+        const uint32_t c = (uint32_t)probes[(uint64_t)q * p.P + r];
+        const uint32_t off = p.snap_off[c], len = p.snap_len[c];
+        const uint32_t ng = ivf_ngroups(p.L, off, len);
+        for (uint32_t j = 0; j < ng && rows < 2; ++j) {
+            TcItem d{};
+            d.off = off;
+            d.len = len;
+            const uint32_t nv = vm_nvalid(p, d, j);
+            if (lane < nv) {
+                const float dist = exact_l2_row(qs, cand_row(p, c, off, j, lane), p.D);
+                const uint64_t key = ((uint64_t)f2ord(dist) << 32) | (32u * rows + lane);
+                if (rows == 0) v[0] = key;
+                else v[1] = key;
+            }
+            nvec += nv;
+            ++rows;
+        }
+    }
+    if (nvec < p.k) return;  // qthr stays "none"
+    warp_bitonic<2>(v, lane);
+    const uint64_t kth = warp_elem<2>(v, p.k - 1);
+    if (lane == 0) p.qthr[q] = __uint_as_float((uint32_t)(kth >> 32));
 }
 // Fast selection of dense_select_kernel (R pre-threshold keys per lane, lists of
 // 32 RL slots; k <= 32R <= n): true when
@@ -1854,6 +2438,23 @@ static_assert(tc_smem_bytes<16, false>() <= 232448 && tc_smem_bytes<32, false>()
                   tc_smem_bytes<16, true>() <= 232448 && tc_smem_bytes<32, true>() <= 232448,
               "smem budget");
 
+constexpr size_t vm_smem_bytes() {
+    return 1024 + kVmNS * kVmSlot + 4 * kVmPlane + 2 * kVmQ * kVmKC * 12 + kVmNR * 4 * 32 * 4 +
+           8 * kVmQ * 4 + kMaxD * 4 + 8 * kVmQ * 4 + 2 * kVmQ * 4 + 8 * kVmQ * 4 +
+           (2 * kVmNS + 2 * kVmNB + 4 + 2 * kRing + 2 * kVmNR) * 8 + kRing * sizeof(TcItem) + 16;
+}
+static_assert(vm_smem_bytes() <= 232448, "vm smem budget");
+
+template <int KT>
+cudaError_t vm_attr() {
+    static bool done = false;
+    if (done) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(scan_vm_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)vm_smem_bytes());
+    done = e == cudaSuccess;
+    return e;
+}
+
 template <int KT, bool W>
 cudaError_t tc_attr() {
     static bool done = false;
@@ -1895,12 +2496,14 @@ bool tc_dense_supported(uint32_t D, uint32_t k, int metric) {
 }
 
 cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, bool wide,
-                            CUtensorMap* out) {
+                            CUtensorMap* out, bool hi_only) {
     auto enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
-    // rows per group: 2K (hi + lo planes) or, wide, K (hi plane) read in chunks
+    // rows per group: 2K (hi + lo planes) or, wide, K (hi plane) read in chunks;
+    // hi_only (scan_vm_kernel): a box of the hi plane's K rows of a 2K-row group
     const uint32_t K = wide ? mirror_k_wide(D) : mirror_k(D);
-    const uint32_t rows = wide ? K : 2 * K, box_rows = wide ? mirror_chunk_wide(D) : 2 * K;
+    const uint32_t rows = wide ? K : 2 * K;
+    const uint32_t box_rows = wide ? mirror_chunk_wide(D) : hi_only ? K : 2 * K;
     cuuint64_t dims[2] = {32, std::max<cuuint64_t>(groups * rows, 1)};
     cuuint64_t strides[1] = {64};
     cuuint32_t box[2] = {32, box_rows};
@@ -1942,6 +2545,82 @@ cudaError_t launch_dense_plan(const DevLists& L, const PlanBufs& B, const long l
     return cudaGetLastError();
 }
 
+// The vector-major path (scan_vm_kernel): plan with kVmQ-pair tiles, exact
+// seeds, scan, refine.
+static cudaError_t launch_vm(const DevLists& L, const PlanBufs& B, const long long* probes, const float* queries,
+                             const float* centroids, const SearchShape& sh, const CUtensorMap* maps_hi,
+                             const float* off_nrm, const float* arena_nrm, const float* off_rows,
+                             const float* arena_rows, const TcBufs& T, float* out_d, long long* out_i,
+                             uint32_t* out_cnt, int num_sms, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                             int max_grid) {
+    SearchShape s2 = sh;
+    s2.QT = kVmQ;
+    cudaError_t e = launch_plan(L, B, probes, s2, s);
+    if (e != cudaSuccess) return e;
+    TcParams p{};
+    p.L = snapshot_view(L, B);
+    p.D = L.D;
+    p.Dk = (L.D + 15) & ~15u;
+    p.brow = p.Dk;
+    p.gstride = 2 * p.Dk;
+    p.nkc = 1;
+    p.Dp = pad4(L.D);
+    p.k = sh.k;
+    p.P = sh.P;
+    p.maxch = sh.maxch;
+    p.qt = kVmQ;
+    p.centroids = centroids;
+    p.queries = queries;
+    p.snap_off = B.snap_off;
+    p.snap_len = B.snap_len;
+    p.gc = B.gc;
+    p.nch = B.nch;
+    p.qoff = B.qoff;
+    p.item_off = B.item_off;
+    p.n_items_ptr = B.n_items;
+    p.plist = B.plist;
+    p.item_ctr = B.item_ctr;
+    p.off_nrm = off_nrm;
+    p.arena_nrm = arena_nrm;
+    p.off_rows = off_rows;
+    p.arena_rows = arena_rows;
+    p.qthr = T.qthr;
+    p.ub = T.ub;
+    p.ccount = T.ccount;
+    p.clb = T.clb;
+    p.cloc = T.cloc;
+    e = sh.k <= 16 ? vm_attr<16>() : vm_attr<32>();
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(T.qthr, 0xff, (size_t)sh.nq * 4, s);
+    if (e != cudaSuccess) return e;
+    if (ev0) cudaEventRecord(ev0, s);
+    const uint32_t wpb = 4;
+    static const uint32_t dbg = [] {
+        const char* v = std::getenv("BIVF_VM_DBG");
+        return v ? (uint32_t)atoi(v) : 0u;
+    }();
+    p.dbg = dbg;
+    if (!(dbg & 2u))
+        vm_seed_kernel<<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * p.Dp * 4, s>>>(p, probes, sh.nq);
+    if (dbg & 64u) {  // debugging aid: the seeds as the results' first distance, no scan
+        cudaMemsetAsync(out_d, 0, (size_t)sh.nq * sh.k * 4, s);
+        cudaMemcpy2DAsync(out_d, (size_t)sh.k * 4, T.qthr, 4, 4, sh.nq, cudaMemcpyDeviceToDevice, s);
+        return cudaGetLastError();
+    }
+    int grid = std::max(1, std::min(num_sms, max_grid));
+    if (const char* g = std::getenv("BIVF_TC_GRID")) grid = std::max(1, atoi(g));  // debugging aid
+    if (sh.k <= 16) scan_vm_kernel<16><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, maps_hi[0], maps_hi[1]);
+    else scan_vm_kernel<32><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, maps_hi[0], maps_hi[1]);
+    count_launch(2);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (ev1) cudaEventRecord(ev1, s);
+    refine_kernel<1, kL2><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(p, probes, out_d, out_i,
+                                                                                           out_cnt, sh.nq);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,
                                  const float* queries, const float* centroids,
                                  const SearchShape& sh, const CUtensorMap& map_off,
@@ -1950,10 +2629,18 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  const float* arena_rows, const TcBufs& T, const TcDense* dense,
                                  float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
-                                 cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int max_grid) {
+                                 cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int max_grid,
+                                 const CUtensorMap* maps_hi) {
     if (sh.nq == 0) return cudaSuccess;
     const bool wide = sh.metric == kIP;  // 1xBF16 inner-product mode (mirror.cuh wide mirror)
     if (wide && dense) return cudaErrorInvalidValue;
+    static const bool vm_env = [] {
+        const char* v = std::getenv("BIVF_TC_VM");  // 1: the vector-major scan (scan_vm_kernel)
+        return v && v[0] == '1';
+    }();
+    if (maps_hi && vm_env && !wide && !dense && L.D <= (uint32_t)kMaxD)
+        return launch_vm(L, B, probes, queries, centroids, sh, maps_hi, off_nrm, arena_nrm, off_rows,
+                         arena_rows, T, out_d, out_i, out_cnt, num_sms, s, ev0, ev1, max_grid);
     SearchShape s2 = sh;
     s2.QT = kM;
     cudaError_t e = cudaSuccess;
@@ -1989,6 +2676,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     p.k = sh.k;
     p.P = sh.P;
     p.maxch = sh.maxch;
+    p.qt = kM;
     p.centroids = centroids;
     p.queries = queries;
     p.snap_off = B.snap_off;

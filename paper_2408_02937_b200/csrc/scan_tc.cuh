@@ -50,7 +50,7 @@ cudaError_t launch_dense_plan(const DevLists& L, const PlanBufs& B, const long l
 // 2-D TMA map over a scan mirror region (mirror.cuh: `groups` groups of 2K rows
 // of 32 bf16, box = {32, 2K}; wide: K rows, box = {32, min(K, 128)}), SWIZZLE_64B.
 cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, bool wide,
-                            CUtensorMap* out);
+                            CUtensorMap* out, bool hi_only = false);
 
 cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,
                                  const float* queries, const float* centroids,
@@ -61,6 +61,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0 = nullptr,
-                                 cudaEvent_t ev1 = nullptr, int max_grid = 1 << 30);
+                                 cudaEvent_t ev1 = nullptr, int max_grid = 1 << 30,
+                                 const CUtensorMap* maps_hi = nullptr);
 
 }  // namespace bivf
