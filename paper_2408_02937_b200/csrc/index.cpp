@@ -301,7 +301,7 @@ void GpuIndex::alloc_device() {
                                  &map_arena_) ==
                  cudaSuccess;
         maps_h_ok_ = cfg_.metric != BIVF_METRIC_IP &&
-                     make_mirror_map(d_arena_mir_.as<float>(), NBS * gpb_, D_, false, &maps_h_[1], true) ==
+                     make_vm_maps(d_arena_mir_.as<float>(), d_arena_nrm_.as<float>(), NBS * gpb_, D_, &maps_h_[3]) ==
                          cudaSuccess;
     }
     mirror_ = mirror_view();
@@ -360,7 +360,7 @@ void GpuIndex::ensure_offline_capacity(uint64_t slots) {
             cudaSuccess)
             tc_ok_ = false;
         if (cfg_.metric != BIVF_METRIC_IP &&
-            make_mirror_map(d_off_mir_.as<float>(), slots / 32, D_, false, &maps_h_[0], true) != cudaSuccess)
+            make_vm_maps(d_off_mir_.as<float>(), d_off_nrm_.as<float>(), slots / 32, D_, &maps_h_[0]) != cudaSuccess)
             maps_h_ok_ = false;
     }
     mirror_ = mirror_view();
@@ -781,7 +781,7 @@ void GpuIndex::grow_offline_preserving(uint64_t slots) {
             cudaSuccess)
             tc_ok_ = false;
         if (cfg_.metric != BIVF_METRIC_IP &&
-            make_mirror_map(d_off_mir_.as<float>(), cap / 32, D_, false, &maps_h_[0], true) != cudaSuccess)
+            make_vm_maps(d_off_mir_.as<float>(), d_off_nrm_.as<float>(), cap / 32, D_, &maps_h_[0]) != cudaSuccess)
             maps_h_ok_ = false;
     }
     off_slots_cap_ = cap;

@@ -378,7 +378,7 @@ private:
     void refresh_size();
 
     CUtensorMap map_off_{}, map_arena_{};
-    CUtensorMap maps_h_[2]{};  // hi-plane boxes of the same mirrors (scan_vm_kernel): offline, arena
+    CUtensorMap maps_h_[6]{};  // scan_vm_kernel's maps (make_vm_maps): offline [0, 3), arena [3, 6)
     bool maps_h_ok_ = false;
     bool tc_ok_ = false;
     int scan_mode_ = 0;  // 0 auto, 1 CUDA-core only, 2 tensor-core when supported

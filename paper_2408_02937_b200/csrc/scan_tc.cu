@@ -135,7 +135,6 @@ struct TcParams {
     uint32_t brow, gstride, nkc;  // TMA box rows, map rows per group, K-chunks per group (wide: Dk / brow)
     uint32_t seed_groups;        // seeding pass: scan only the first seed_groups groups, no run output
     uint32_t qt;                 // plan tile: pairs per work item (kM, or kVmQ for scan_vm_kernel)
-    uint32_t dbg;                // BIVF_VM_DBG bits (debugging aid, 0 in production)
     const float* centroids;      // [C][D] row-major
     const float* queries;        // [nq][Dp]
     const uint32_t* snap_off;
@@ -170,6 +169,12 @@ struct TcParams {
     uint32_t* cloc;     // [runs][kKC]   (group << 5 | slot)
 };
 
+// the vector-major scan's tensor maps: [offline, arena][one group's hi plane,
+// four groups' hi planes, four groups' norm rows] (make_vm_maps)
+struct VmMaps {
+    CUtensorMap m[2][3];
+};
+
 // order-preserving float -> uint32 (negative values included)
 __device__ __forceinline__ uint32_t f2ord(float x) {
     const uint32_t b = __float_as_uint(x);
@@ -194,6 +199,30 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+// L2 prefetch of a 2-D tensor-map box (no shared memory, no completion)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1076,18 +1105,31 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 //   eps = kVmCross |r||s| + kEpsRel (nr + ns) + kEpsRel |a|
 // Pass 1 (every pair, superset of lb <= theta; |r||s| <= (nr+ns)/2):
 //   P >= U_n + V_s,  U_n = (c1 nr_n - c2 theta_n) / 2,  V_s = c1 ns / 2
-// The per-query threshold theta_n starts at the query's shared threshold (the
-// exact k-th distance over the first vectors of its nearest list, vm_seed_kernel,
-// tightened by every run) and shrinks with the k smallest upper bounds of the
-// candidates (one bookkeeping lane per query); candidates (lb, ub, slot) are
-// appended to per-(warpgroup, query) shared lists and compacted against theta.
-// Run output = the refine kernel's format (k upper bounds + candidates per
-// (pair, chunk, warpgroup)).
+// Filtering: each math warp of the unit's warpgroup reads its TMEM lane
+// quarter (one 32-vector group x the item's queries) and transposes it through
+// a shared-memory tile (XOR-swizzled, conflict-free both ways), so lane n holds
+// query n's 32 values; it filters them like the query-major kernel's math
+// threads: pass 1 = one FFMA + max per slot against W = (c1 nr - c2 theta) / 2
+// (a superset of lb <= theta, |r||s| <= (nr+ns)/2), pass 2 over the few
+// surviving slots = the exact bound, the upper bound offered to the query's
+// shared k-best set, the candidate (lb, slot) appended to the lane's shared
+// column (compacted against theta when full).  The k-best set is per (item,
+// query) in shared memory: k slots of f2ord upper bounds, a new value replaces
+// the current maximum by compare-and-swap, so its maximum is always the k-th
+// smallest upper bound of k distinct vectors seen by ANY of the query's 8 lanes
+// (4 warps x 2 warpgroups); theta = min(that maximum, the global per-query
+// threshold qthr, which every run of the query tightens).  At the end of an
+// item each warpgroup gathers its 4 lanes' candidates of a query into one run
+// of refine_kernel's format (warpgroup 0's run carries the k-best set).
 constexpr int kVmQ = 32;       // query columns per work item (MMA N <= 32)
-constexpr int kVmNS = 4;       // A stage slots (one unit of 4 groups each)
+constexpr int kVmNS = 3;       // A stage slots (one unit of 4 groups each)
+#ifndef BIVF_VM_PF
+#define BIVF_VM_PF 0
+#endif
+constexpr int kVmPF = BIVF_VM_PF;  // units prefetched into L2 ahead of the shared-memory ring
 constexpr int kVmNR = 8;       // norm ring slots (a unit's 4 x 32 |s|^2)
 constexpr int kVmNB = 4;       // TMEM accumulators (32 columns each)
-constexpr int kVmKC = 48;      // candidate slots per (warpgroup, query)
+constexpr int kVmKC = 24;      // candidate slots per (warp, query lane)
 constexpr uint32_t kVmSlot = 4u * kMaxD * 64u;  // bytes per A slot (4 groups x K rows x 64 B, K <= 128)
 constexpr uint32_t kVmPlane = kMaxD * 64u;      // bytes per B plane (K rows x 32 queries bf16)
 constexpr float kVmCross = 1.0f / 64.0f;
@@ -1123,31 +1165,31 @@ __device__ __forceinline__ uint32_t vm_nvalid(const TcParams& p, const TcItem& d
     return min(32u, min(p.L.T, d.len - mid * p.L.T) - 32u * gi);
 }
 
-__device__ __forceinline__ const float* cand_row(const TcParams& p, uint32_t c, uint32_t off, uint32_t j,
-                                                 uint32_t s);
-
 template <int KT>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    scan_vm_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_off,
-                   const __grid_constant__ CUtensorMap map_arena) {
+    scan_vm_kernel(const TcParams p, const __grid_constant__ VmMaps maps) {
+    const CUtensorMap* map_g1[2] = {&maps.m[0][0], &maps.m[1][0]};  // one group's hi plane
+    const CUtensorMap* map_g4[2] = {&maps.m[0][1], &maps.m[1][1]};  // four consecutive groups' hi planes
+    const CUtensorMap* map_n4[2] = {&maps.m[0][2], &maps.m[1][2]};  // their |s|^2 rows
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t raw_s = smem_u32(smem_raw);
     const uint32_t pad = ((raw_s + 1023u) & ~1023u) - raw_s;
-    unsigned char* sA = smem_raw + pad;                               // kVmNS * kVmSlot
-    unsigned char* sB = sA + kVmNS * kVmSlot;                          // [2 items][hi, lo] planes
-    float2* cand = reinterpret_cast<float2*>(sB + 4 * kVmPlane);       // [2 wg][kVmQ][kVmKC] (lb, ub)
-    uint32_t* cloc = reinterpret_cast<uint32_t*>(cand + 2 * kVmQ * kVmKC);  // [2][kVmQ][kVmKC]
-    float* nslots = reinterpret_cast<float*>(cloc + 2 * kVmQ * kVmKC);  // [kVmNR][4 groups][32] |s|^2
-    float* q_thr = nslots + kVmNR * 4 * 32;    // [2 items][kVmQ] theta
-    float* q_u = q_thr + 2 * kVmQ;             // [2][kVmQ] pass-1 offsets U
-    float* q_nr = q_u + 2 * kVmQ;              // [2][kVmQ] |r|^2
-    float* q_rn = q_nr + 2 * kVmQ;             // [2][kVmQ] |r|
-    float* cent_s = q_rn + 2 * kVmQ;           // [kMaxD] the item's centroid
-    float* nrp = cent_s + kMaxD;               // [8][kVmQ] partial |r|^2
-    uint32_t* q_id = reinterpret_cast<uint32_t*>(nrp + 8 * kVmQ);  // [2][kVmQ] query index
-    uint32_t* q_cnt = q_id + 2 * kVmQ;         // [2 items][2 wg][kVmQ]
-    uint32_t* q_ovf = q_cnt + 4 * kVmQ;        // [2][2][kVmQ]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(q_ovf + 4 * kVmQ);
+    unsigned char* sA = smem_raw + pad;                                  // kVmNS * kVmSlot
+    unsigned char* sB = sA + kVmNS * kVmSlot;                             // [2 items][hi, lo] planes
+    float* tiles = reinterpret_cast<float*>(sB + 4 * kVmPlane);           // [8 warps][32][32] transposes
+    float* cand_lb = tiles + 8 * 1024;                                    // [8 warps][kVmKC][32]
+    uint32_t* cand_loc = reinterpret_cast<uint32_t*>(cand_lb + 8 * kVmKC * 32);
+    float* nslots = reinterpret_cast<float*>(cand_loc + 8 * kVmKC * 32);  // [kVmNR][4 groups][32] |s|^2
+    uint32_t* q_thr = reinterpret_cast<uint32_t*>(nslots + kVmNR * 4 * 32);  // [2 items][kVmQ] f2ord theta
+    float* q_nr = reinterpret_cast<float*>(q_thr + 2 * kVmQ);             // [2][kVmQ] |r|^2
+    float* q_rn = q_nr + 2 * kVmQ;                                        // [2][kVmQ] |r|
+    float* cent_s = q_rn + 2 * kVmQ;                                      // [kMaxD] the item's centroid
+    float* nrp = cent_s + kMaxD;                                          // [8][kVmQ] partial |r|^2
+    uint32_t* q_id = reinterpret_cast<uint32_t*>(nrp + 8 * kVmQ);         // [2][kVmQ] query index
+    uint32_t* o_cnt = q_id + 2 * kVmQ;                                    // [2 wg][kVmQ] run fill
+    uint32_t* o_ovf = o_cnt + 2 * kVmQ;                                   // [2 wg][kVmQ]
+    uint32_t* kbest = o_ovf + 2 * kVmQ;                                   // [2 items][32 slots][kVmQ] f2ord
+    uint64_t* bars = reinterpret_cast<uint64_t*>(kbest + 2 * 32 * kVmQ);
     uint64_t* full = bars;                     // kVmNS
     uint64_t* empty = full + kVmNS;            // kVmNS
     uint64_t* acc_full = empty + kVmNS;        // kVmNB
@@ -1202,6 +1244,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
+            TcProf pf;
+            pf.start();
             auto fetch = [&](uint32_t seq) -> bool {
                 const uint32_t rs = seq % kRing;
                 mbar_wait(&it_empty[rs], ((seq / kRing) & 1) ^ 1);
@@ -1222,8 +1266,43 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const int32_t* trow = p.L.rowptr[d.c];
                 uint32_t cmid = 0xffffffffu;
                 uint64_t cblk = 0;
+                // L2 prefetch of the groups kVmPF units ahead (the shared-memory ring
+                // holds only kVmNS units; the prefetched loads then hit L2)
+                uint32_t pmid = 0xffffffffu;
+                uint64_t pblk = 0;
+                auto prefetch_unit = [&](uint32_t pj0) {
+                    const uint32_t png = min(4u, d.g1 - pj0);
+                    for (uint32_t h = 0; h < png; ++h) {
+                        const uint32_t j = pj0 + h;
+                        uint64_t gi;
+                        bool ar;
+                        if (j < og) {
+                            ar = false;
+                            gi = offg0 + j;
+                        } else {
+                            const uint32_t jj = j - og, mid = jj / p.L.gpb, gq = jj - mid * p.L.gpb;
+                            if (mid != pmid) {
+                                pmid = mid;
+                                pblk = (uint64_t)trow[mid];
+                            }
+                            ar = true;
+                            gi = pblk * p.L.gpb + gq;
+                        }
+                        if (h == 0 && png == 4 && (j + 3 < og || j >= og) &&
+                            (j < og || (j - og) / p.L.gpb == (j + 3 - og) / p.L.gpb)) {
+                            // four consecutive groups (one list part, one block): one box each
+                            tma_prefetch_3d(map_g4[ar], 0, 0, (int)gi);
+                            tma_prefetch_2d(map_n4[ar], 0, (int)gi);
+                            break;
+                        }
+                        tma_prefetch_2d(map_g1[ar], 0, (int)(gi * p.gstride));
+                        bulk_prefetch_l2((ar ? p.arena_nrm : p.off_nrm) + gi * kNormFloats, 128u);
+                    }
+                };
+                for (uint32_t u = 0; u < (uint32_t)kVmPF && d.g0 + 4 * u < d.g1; ++u) prefetch_unit(d.g0 + 4 * u);
                 for (uint32_t j0 = d.g0; j0 < d.g1; j0 += 4, ++unit) {
                     const uint32_t ng = min(4u, d.g1 - j0);
+                    if (kVmPF > 0 && j0 + 4u * kVmPF < d.g1) prefetch_unit(j0 + 4u * kVmPF);
                     uint64_t gidx[4];
                     bool gar[4];
 #pragma unroll
@@ -1243,28 +1322,49 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                             gidx[h] = cblk * p.L.gpb + gi;
                         }
                     }
+                    // the unit's groups consecutive in one array: one 3-D box of hi planes
+                    // and one box of norm rows (groups past the list are loaded and ignored)
+                    bool con = true;
+#pragma unroll
+                    for (int h = 1; h < 4; ++h)
+                        if ((uint32_t)h < ng) con = con && gar[h] == gar[0] && gidx[h] == gidx[0] + (uint64_t)h;
                     const uint32_t slot = unit % kVmNS;
+                    pf.mark(0);
                     mbar_wait(&empty[slot], ((unit / kVmNS) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&full[slot], ng * K * 64u);
+                    pf.mark(1);
+                    if (con) {
+                        mbar_arrive_expect_tx(&full[slot], 4u * K * 64u);
+                        tma_load_3d(sA + slot * kVmSlot, map_g4[gar[0]], 0, 0, (int)gidx[0], &full[slot]);
+                    } else {
+                        mbar_arrive_expect_tx(&full[slot], ng * K * 64u);
 #pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        if ((uint32_t)h >= ng) break;
-                        // the group's hi plane: rows [0, K) of its 2K mirror rows
-                        tma_load_2d(sA + slot * kVmSlot + h * K * 64u, gar[h] ? &map_arena : &map_off, 0,
-                                    (int)(gidx[h] * p.gstride), &full[slot]);
+                        for (int h = 0; h < 4; ++h) {
+                            if ((uint32_t)h >= ng) break;
+                            // the group's hi plane: rows [0, K) of its 2K mirror rows
+                            tma_load_2d(sA + slot * kVmSlot + h * K * 64u, map_g1[gar[h]], 0,
+                                        (int)(gidx[h] * p.gstride), &full[slot]);
+                        }
                     }
-                    if (p.dbg & 512u) mbar_wait(&full[slot], (unit / kVmNS) & 1);  // debugging aid
                     const uint32_t nsl = unit % kVmNR;
+                    pf.mark(2);
                     mbar_wait(&nempty[nsl], ((unit / kVmNR) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&nfull[nsl], ng * 128u);
+                    pf.mark(3);
+                    if (con) {
+                        mbar_arrive_expect_tx(&nfull[nsl], 512u);
+                        tma_load_2d(nslots + nsl * 4 * 32, map_n4[gar[0]], 0, (int)gidx[0], &nfull[nsl]);
+                    } else {
+                        mbar_arrive_expect_tx(&nfull[nsl], ng * 128u);
 #pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        if ((uint32_t)h >= ng) break;
-                        bulk_g2s(nslots + (nsl * 4 + h) * 32,
-                                 (gar[h] ? p.arena_nrm : p.off_nrm) + gidx[h] * kNormFloats, 128u, &nfull[nsl]);
+                        for (int h = 0; h < 4; ++h) {
+                            if ((uint32_t)h >= ng) break;
+                            bulk_g2s(nslots + (nsl * 4 + h) * 32,
+                                     (gar[h] ? p.arena_nrm : p.off_nrm) + gidx[h] * kNormFloats, 128u, &nfull[nsl]);
+                        }
                     }
+                    pf.mark(4);
                 }
             }
+            pf.report("vm-producer", warp);
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
@@ -1273,6 +1373,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t idesc0 = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | (8u << 24);
         const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
         uint32_t unit = 0;
+        TcProf pf;
+        pf.start();
         for (uint32_t seq = 0;; ++seq) {
             const uint32_t rs = seq % kRing;
             mbar_wait(&it_full[rs], (seq / kRing) & 1);
@@ -1281,14 +1383,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0) mbar_arrive(&it_empty[rs]);
             if (!d.valid) break;
             const uint32_t ib = seq & 1;
+            pf.mark(0);
             mbar_wait(&b_full[ib], (seq >> 1) & 1);
+            pf.mark(1);
             const uint32_t N = max(16u, (d.npairs + 15u) & ~15u);
             const uint32_t idesc = idesc0 | ((N >> 3) << 17);
             const uint32_t bh0 = sb0 + ib * 2 * kVmPlane, bl0 = bh0 + kVmPlane;
             for (uint32_t j0 = d.g0; j0 < d.g1; j0 += 4, ++unit) {
                 const uint32_t b = unit % kVmNB, slot = unit % kVmNS;
+                pf.mark(2);
                 mbar_wait(&acc_empty[b], ((unit / kVmNB) & 1) ^ 1);
+                pf.mark(3);
                 mbar_wait(&full[slot], (unit / kVmNS) & 1);
+                pf.mark(4);
                 __syncwarp();
                 tc_fence_after();
                 const uint32_t dcol = tmem_base + b * 32u;
@@ -1301,18 +1408,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 __syncwarp();
                 mma_commit_elect(&acc_full[b]);
                 __syncwarp();
-                if (p.dbg & 256u) mbar_wait(&acc_full[b], (unit / kVmNB) & 1);  // debugging aid
             }
             mma_commit_elect(&b_free[ib]);
             __syncwarp();
         }
+        pf.report("vm-mma", warp);
     } else {
         // ------------------------------------------------ math warpgroups
         const int wg = (warp - 2) >> 2;
         const int q4 = warp & 3;                          // TMEM lane quarter = group of the unit
-        const int wt = threadIdx.x - 64 - 128 * wg;       // 0..127 within the warpgroup
+        const int wl = (warp - 2) & 3;                    // warp index within the warpgroup (0: filter lanes)
         const int t256 = threadIdx.x - 64;                // 0..255 over both warpgroups
-        const bool book = wt < 32;                        // bookkeeping lane of query column wt
+        float* tp = tiles + (warp - 2) * 1024;            // this warp's transpose tile
+        float* clb = cand_lb + (warp - 2) * kVmKC * 32 + lane;   // this lane's candidate column
+        uint32_t* cloc = cand_loc + (warp - 2) * kVmKC * 32 + lane;
         // item seq's B planes + per-query state (buffer seq & 1), both warpgroups
         auto build = [&](uint32_t seq, TcItem& d) -> bool {
             const uint32_t rs = seq % kRing;
@@ -1320,9 +1429,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             d = ring[rs];
             __syncwarp();
             if (lane == 0) mbar_arrive(&it_empty[rs]);
-            // both warpgroups are done with item seq - 2's state and with the run
-            // output of item seq - 2 (the candidate lists are reused by the item
-            // after it): taken for the end marker too
+            // both warpgroups are done with item seq - 2's state: taken for the
+            // end marker too (no warp may run ahead of another's run output)
             named_bar(3, 256);
             if (!d.valid) return false;
             const uint32_t ib = seq & 1;
@@ -1359,7 +1467,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // planes -> the MMA's async proxy
             named_bar(3, 256);
-            if ((p.dbg & 8192u) && t256 == 0) __nanosleep(20000);  // debugging aid
             if (t256 == 0) mbar_arrive(&b_full[ib]);
             if (t256 < kVmQ) {
                 const uint32_t n = t256;
@@ -1368,221 +1475,194 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                 for (int h = 0; h < 8; ++h) nr = __fadd_rn(nr, nrp[h * kVmQ + n]);  // fixed order
                 const uint32_t qi = act ? d.pairs[n] / p.P : 0u;
-                const float th = act ? qthr_dec(__ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + qi))
-                                     : -__int_as_float(0x7f800000);
                 q_id[ib * kVmQ + n] = qi;
                 q_nr[ib * kVmQ + n] = nr;
                 q_rn[ib * kVmQ + n] = sqrtf(nr);
-                q_thr[ib * kVmQ + n] = th;
-                q_u[ib * kVmQ + n] = act ? 0.5f * fmaf(kVmC1, nr, -kVmC2 * th) : __int_as_float(0x7f800000);
-                q_cnt[(ib * 2 + 0) * kVmQ + n] = 0;
-                q_cnt[(ib * 2 + 1) * kVmQ + n] = 0;
-                q_ovf[(ib * 2 + 0) * kVmQ + n] = 0;
-                q_ovf[(ib * 2 + 1) * kVmQ + n] = 0;
+                q_thr[ib * kVmQ + n] = act ? __ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + qi) : 0u;
             }
+            for (int i = t256; i < 32 * kVmQ; i += 256) kbest[ib * 32 * kVmQ + i] = 0xffffffffu;
             named_bar(3, 256);
             return true;
         };
         uint32_t unit = 0;
         TcItem d;
+        TcProf pf;
+        pf.start();
         bool have = build(0, d);
         for (uint32_t seq = 0; have; ++seq) {
             TcItem dn;
+            pf.mark(0);
             const bool hn = build(seq + 1, dn);
+            pf.mark(1);
             const uint32_t ib = seq & 1;
-            const float* thr = q_thr + ib * kVmQ;
-            float* uu = q_u + ib * kVmQ;
-            const float* nrv = q_nr + ib * kVmQ;
-            const float* rnv = q_rn + ib * kVmQ;
-            uint32_t* cnt = q_cnt + (ib * 2 + wg) * kVmQ;
-            uint32_t* ovf = q_ovf + (ib * 2 + wg) * kVmQ;
-            float2* mycand = cand + wg * kVmQ * kVmKC;
-            uint32_t* myloc = cloc + wg * kVmQ * kVmKC;
-            // bookkeeping lane state (query column wt): the k smallest upper bounds of
-            // this warpgroup's candidates, ascending after -inf sentinels
-            float ubl[KT];
-#pragma unroll
-            for (int i = 0; i < KT; ++i)
-                ubl[i] = i < KT - (int)p.k ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000);
-            uint32_t seen = 0;
-            const bool bact = book && (uint32_t)wt < d.npairs;
-            const uint32_t bq = bact ? q_id[ib * kVmQ + wt] : 0u;
-            uint32_t qg = bact ? __ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + bq) : 0xffffffffu;
+            const int n = lane;                      // this lane's query column
+            const bool active = (uint32_t)n < d.npairs;
+            const uint32_t qi = q_id[ib * kVmQ + n];
+            const float nr = q_nr[ib * kVmQ + n], rn = q_rn[ib * kVmQ + n];
+            uint32_t* qts = q_thr + ib * kVmQ + n;   // theta of the query (f2ord, atomicMin)
+            uint32_t* kb0 = kbest + ib * 32 * kVmQ;  // k-best sets: query q's slot i at kb0[i * kVmQ + q]
+            uint32_t* kb = kb0 + n;                  // this lane's query
+            uint32_t ncand = 0;
+            bool overflow = false;
+            // the global threshold, loaded a unit ahead (its latency stays hidden)
+            uint32_t qg = active ? __ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + qi) : 0xffffffffu;
             for (uint32_t j0 = d.g0; j0 < d.g1; j0 += 4, ++unit) {
                 if ((unit & 1u) != (uint32_t)wg) continue;
                 const uint32_t b = unit % kVmNB, nsl = unit % kVmNR;
+                const uint32_t qcur = qg;
+                if (active) qg = __ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + qi);
+                pf.mark(2);
                 mbar_wait(&acc_full[b], (unit / kVmNB) & 1);
+                pf.mark(3);
                 __syncwarp();
                 tc_fence_after();
-                float P[32];
-                tmem_ld32(tmem_base + ((uint32_t)(32 * q4) << 16) + b * 32u, P);
-                mbar_wait(&nfull[nsl], (unit / kVmNR) & 1);
-                const uint32_t j = j0 + (uint32_t)q4;
-                const uint32_t nv = j < d.g1 ? vm_nvalid(p, d, j) : 0u;
-                const float nsv = nslots[(nsl * 4 + q4) * 32 + lane];
+                float dot[32];
+                tmem_ld32(tmem_base + ((uint32_t)(32 * q4) << 16) + b * 32u, dot);
+                // transpose: lane s writes vector s's 32 query values, lane n reads
+                // query n's 32 vector values
+#pragma unroll
+                for (int i = 0; i < 32; ++i) tp[lane * 32 + (i ^ lane)] = dot[i];
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) {  // accumulator and norm slot are free again
-                    mbar_arrive(&acc_empty[b]);
-                    mbar_arrive(&nempty[nsl]);
-                }
-                const bool valid = (uint32_t)lane < nv;
-                const float V = 0.5f * kVmC1 * nsv;
-                // pass 1: max_n (P_n - U_n) >= V  (U_n = +inf for columns past the tile's pairs)
-                float m0 = -__int_as_float(0x7f800000), m1 = m0;
+                if (lane == 0) mbar_arrive(&acc_empty[b]);
 #pragma unroll
-                for (int n = 0; n < kVmQ; n += 4) {
-                    const float4 u4 = *reinterpret_cast<const float4*>(uu + n);
-                    m0 = fmaxf(m0, fmaxf(P[n] - u4.x, P[n + 1] - u4.y));
-                    m1 = fmaxf(m1, fmaxf(P[n + 2] - u4.z, P[n + 3] - u4.w));
-                }
-                if (valid && (fmaxf(m0, m1) >= V || (p.dbg & 16u))) {
-                    // pass 2: exact bounds of the surviving pairs, append to the query lists
-                    const float sn = sqrtf(nsv);
-                    const uint32_t loc = (j << 5) | (uint32_t)lane;
+                for (int s = 0; s < 32; ++s) dot[s] = tp[s * 32 + (n ^ s)];
+                pf.mark(4);
+                mbar_wait(&nfull[nsl], (unit / kVmNR) & 1);
+                pf.mark(5);
+                const float* wn = nslots + (nsl * 4 + q4) * 32;  // |s|^2 of the group's 32 slots
+                const uint32_t j = j0 + (uint32_t)q4;
+                if (active && j < d.g1) {
+                    if (qcur < *reinterpret_cast<volatile uint32_t*>(qts)) atomicMin(qts, qcur);
+                    float th = qthr_dec(*reinterpret_cast<volatile uint32_t*>(qts));
+                    // pass 1: some slot s can enter iff dot_s - c1 ns_s / 2 >= W
+                    const float W = 0.5f * fmaf(kVmC1, nr, -kVmC2 * th);
+                    float m0 = -__int_as_float(0x7f800000), m1 = m0;
 #pragma unroll
-                    for (int n = 0; n < kVmQ; ++n) {
-                        if (P[n] - uu[n] >= V || ((p.dbg & 16u) && n < (int)d.npairs)) {
-                            const float nr = nrv[n];
-                            const float a = fmaf(-2.f, P[n], nr + nsv);
-                            const float e = fmaf(kVmCross, rnv[n] * sn,
-                                                 fmaf(kEpsRel, nr + nsv, fmaf(kEpsRel, fabsf(a), 1e-30f)));
-                            const float lb = a - e;
-                            if (p.dbg & 16384u) {  // debugging aid: the bound at pass 2
-                                const uint32_t qi = q_id[ib * kVmQ + n];
-                                const float* xr = cand_row(p, d.c, d.off, j, (uint32_t)lane);
-                                float ex = 0.f;
-                                for (uint32_t dd = 0; dd < p.D; ++dd)
-                                    ex = l2_step(ex, p.queries[(uint64_t)qi * p.Dp + dd], xr[dd]);
-                                if (!(lb <= ex && ex <= a + e))
-                                    printf("[vm-p2] q=%u c=%u j=%u lane=%d n=%d P=%.9g nr=%.9g ns=%.9g a=%.9g e=%.9g exact=%.9g "
-                                           "unit=%u b=%u wg=%d\n", qi, d.c, j, lane, n, P[n], nr, nsv, a, e, ex, unit, b, wg);
+                    for (int s = 0; s < 32; s += 4) {
+                        const float4 v = *reinterpret_cast<const float4*>(wn + s);
+                        m0 = fmaxf(m0, fmaxf(fmaf(-0.5f * kVmC1, v.x, dot[s]), fmaf(-0.5f * kVmC1, v.y, dot[s + 1])));
+                        m1 = fmaxf(m1, fmaxf(fmaf(-0.5f * kVmC1, v.z, dot[s + 2]), fmaf(-0.5f * kVmC1, v.w, dot[s + 3])));
+                    }
+                    pf.mark(6);
+                    if (fmaxf(m0, m1) >= W) {
+                        const uint32_t nv = vm_nvalid(p, d, j);
+                        uint32_t need = 0;
+#pragma unroll
+                        for (int s = 0; s < 32; ++s)
+                            need |= (fmaf(-0.5f * kVmC1, wn[s], dot[s]) >= W) ? (1u << s) : 0u;
+                        need &= nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
+                        // pass 2 (the tile column still holds this lane's values)
+                        while (need) {
+                            const uint32_t s = __ffs(need) - 1;
+                            need &= need - 1;
+                            const float ns = wn[s];
+                            const float a = fmaf(-2.f, tp[s * 32 + (n ^ s)], nr + ns);
+                            const float e = fmaf(kVmCross, rn * sqrtf(ns),
+                                                 fmaf(kEpsRel, nr + ns, fmaf(kEpsRel, fabsf(a), 1e-30f)));
+                            const float h = a + e, l = a - e;
+                            if (h < th) {
+                                // offer h to the query's k-best set: replace its maximum (CAS,
+                                // retried when another lane got there first)
+                                const uint32_t u = f2ord(h);
+                                for (;;) {
+                                    uint32_t mx = 0, mi = 0;
+                                    for (uint32_t r = 0; r < p.k; ++r) {
+                                        const uint32_t v = *reinterpret_cast<volatile uint32_t*>(kb + r * kVmQ);
+                                        if (v >= mx) {
+                                            mx = v;
+                                            mi = r;
+                                        }
+                                    }
+                                    if (u >= mx) break;
+                                    if (atomicCAS(kb + mi * kVmQ, mx, u) == mx) {
+                                        uint32_t nm = u;
+                                        for (uint32_t r = 0; r < p.k; ++r)
+                                            nm = max(nm, *reinterpret_cast<volatile uint32_t*>(kb + r * kVmQ));
+                                        if (nm < 0xffffffffu) {  // k values: a threshold for the query's runs
+                                            atomicMin(qts, nm);
+                                            atomicMin(reinterpret_cast<uint32_t*>(p.qthr) + qi, nm);
+                                        }
+                                        break;
+                                    }
+                                }
+                                th = qthr_dec(*reinterpret_cast<volatile uint32_t*>(qts));
                             }
-                            if (lb <= thr[n]) {
-                                const uint32_t at = atomicAdd(&cnt[n], 1u);
-                                if (at < (uint32_t)kVmKC) {
-                                    mycand[n * kVmKC + at] = make_float2(lb, a + e);
-                                    myloc[n * kVmKC + at] = (p.dbg & 32768u) ? (loc | ((uint32_t)n << 24) | ((uint32_t)unit << 29)) : loc;
+                            if (l <= th && !overflow) {
+                                if (ncand == (uint32_t)kVmKC) {  // compact against the tighter threshold
+                                    uint32_t w = 0;
+                                    for (uint32_t r = 0; r < (uint32_t)kVmKC; ++r) {
+                                        const float li = clb[r * 32];
+                                        if (li <= th) {
+                                            const uint32_t ci = cloc[r * 32];
+                                            clb[w * 32] = li;
+                                            cloc[w * 32] = ci;
+                                            ++w;
+                                        }
+                                    }
+                                    ncand = w;
+                                }
+                                if (ncand < (uint32_t)kVmKC) {
+                                    clb[ncand * 32] = l;
+                                    cloc[ncand * 32] = (j << 5) | s;
+                                    ++ncand;
                                 } else {
-                                    ovf[n] = 1u;
+                                    overflow = true;
                                 }
                             }
                         }
                     }
                 }
-                named_bar(1 + wg, 128);  // this unit's appends are in
-                if (bact && (p.dbg & 131072u)) {  // debugging aid: every listed entry against the exact distance
-                    const uint32_t c = min(cnt[wt], (uint32_t)kVmKC);
-                    for (uint32_t i = 0; i < c; ++i) {
-                        const float2 v = mycand[wt * kVmKC + i];
-                        const uint32_t loc = myloc[wt * kVmKC + i];
-                        const float* xr = cand_row(p, d.c, d.off, loc >> 5, loc & 31u);
-                        float ex = 0.f;
-                        for (uint32_t dd = 0; dd < p.D; ++dd)
-                            ex = l2_step(ex, p.queries[(uint64_t)bq * p.Dp + dd], xr[dd]);
-                        if (!(v.x <= ex && ex <= v.y))
-                            printf("[vm-bk] q=%u c=%u unit=%u j0=%u i=%u c=%u seen=%u loc=%u lb=%.9g ub=%.9g exact=%.9g\n", bq,
-                                   d.c, unit, j0, i, c, seen, loc, v.x, v.y, ex);
-                    }
-                }
-                if (bact) {
-                    const uint32_t c = min(cnt[wt], (uint32_t)kVmKC);
-                    for (uint32_t i = seen; i < c; ++i) {
-                        float x = mycand[wt * kVmKC + i].y;
-                        if (x < ubl[KT - 1]) {
-#pragma unroll
-                            for (int r = 0; r < KT; ++r) {
-                                const float lo = fminf(x, ubl[r]);
-                                x = fmaxf(x, ubl[r]);
-                                ubl[r] = lo;
-                            }
-                        }
-                    }
-                    seen = c;
-                    const float tl = (p.dbg & 1u) ? __int_as_float(0x7f800000) : ubl[KT - 1];
-                    const float tg = (p.dbg & 4u) ? __int_as_float(0x7f800000) : qthr_dec(qg);
-                    const float t0 = q_thr[ib * kVmQ + wt];
-                    const float th = fminf(t0, fminf(tl, tg));
-                    if (th < t0) {
-                        q_thr[ib * kVmQ + wt] = th;
-                        uu[wt] = 0.5f * fmaf(kVmC1, nrv[wt], -kVmC2 * th);
-                    }
-                    if (tl < tg && !(p.dbg & 4u)) atomicMin(reinterpret_cast<uint32_t*>(p.qthr) + bq, f2ord(tl));
-                    if (c >= (uint32_t)kVmKC / 2 && !(p.dbg & 8u)) {  // compact against the current threshold
-                        uint32_t w = 0;
-                        for (uint32_t i = 0; i < c; ++i) {
-                            const float2 v = mycand[wt * kVmKC + i];
-                            if (v.x <= th) {
-                                mycand[wt * kVmKC + w] = v;
-                                myloc[wt * kVmKC + w] = myloc[wt * kVmKC + i];
-                                ++w;
-                            }
-                        }
-                        cnt[wt] = w;
-                        seen = w;
-                    }
-                    qg = __ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + bq);  // for the next unit
-                }
-                named_bar(1 + wg, 128);  // compaction done before the next unit appends
+                pf.mark(9);
+                __syncwarp();  // the tile is rewritten by this warp's next unit; norm slot released
+                if (lane == 0) mbar_arrive(&nempty[nsl]);
+                pf.mark(10);
             }
-            if ((p.dbg & 65536u) && bact) {  // debugging aid: B column wt holds query bq's residual
-                const unsigned char* bh = sB + ib * 2 * kVmPlane;
-                uint32_t badk = 0xffffffffu;
-                for (uint32_t kk = 0; kk < p.D; ++kk) {
-                    const float r = __fsub_rn(p.queries[(uint64_t)bq * p.Dp + kk], p.centroids[(uint64_t)d.c * p.D + kk]);
-                    const float h = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(bh + vm_boff(kk, wt)));
-                    if (h != __bfloat162float(__float2bfloat16_rn(r)) && badk == 0xffffffffu) badk = kk;
-                }
-                if (badk != 0xffffffffu)
-                    printf("[vm-B] column %d of item (c=%u g0=%u np=%u) is not query %u (first bad dim %u) seq=%u blk=%u\n", wt,
-                           d.c, d.g0, d.npairs, bq, badk, seq, blockIdx.x);
+            pf.mark(7);
+            // run output: the warpgroup's 4 lanes of a query -> one run (refine_kernel's
+            // format); warpgroup 0's run carries the k-best set, warpgroup 1's +inf
+            if (wl == 0) {
+                o_cnt[wg * kVmQ + n] = 0;
+                o_ovf[wg * kVmQ + n] = 0;
             }
-            // run output (refine_kernel's format): k upper bounds + candidates
-            if (bact && !p.seed_groups) {
-                const uint32_t pair = d.pairs[wt];
+            named_bar(1 + wg, 128);
+            if (active) {
+                const uint32_t pair = d.pairs[n];
                 const uint64_t run = (((uint64_t)pair * p.maxch + d.chunk) << 1) | (uint32_t)wg;
-#pragma unroll
-                for (int i = 0; i < KT; ++i)
-                    if (i >= KT - (int)p.k) p.ub[run * p.k + (i - (KT - (int)p.k))] = ubl[i];
-                const float th = q_thr[ib * kVmQ + wt];
-                const uint32_t c = min(cnt[wt], (uint32_t)kVmKC);
+                const float th = qthr_dec(*reinterpret_cast<volatile uint32_t*>(qts));
                 uint32_t w = 0;
-                if (!ovf[wt]) {
-                    for (uint32_t i = 0; i < c; ++i) {
-                        const float2 v = mycand[wt * kVmKC + i];
-                        if (p.dbg & 32u) {  // debugging aid: the kept bounds against the exact distance
-                            uint32_t loc = myloc[wt * kVmKC + i];
-                            if (p.dbg & 32768u) {
-                                if (((loc >> 24) & 31u) != (uint32_t)wt)
-                                    printf("[vm-col] entry of column %u in list %d (i=%u c=%u cnt=%u unit3=%u)\n", (loc >> 24) & 31u, wt, i, c, cnt[wt], loc >> 29);
-                                loc &= 0xffffffu;
-                            }
-                            const float* xr = cand_row(p, d.c, d.off, loc >> 5, loc & 31u);
-                            float ex = 0.f;
-                            for (uint32_t dd = 0; dd < p.D; ++dd)
-                                ex = l2_step(ex, p.queries[(uint64_t)bq * p.Dp + dd], xr[dd]);
-                            if (!(v.x <= ex && ex <= v.y))
-                                printf("[vm-bound] q=%u c=%u loc=%u lb=%.9g ub=%.9g exact=%.9g th=%.9g seq=%u ib=%u g0=%u g1=%u "
-                                       "np=%u n=%d wg=%d blk=%u\n", bq, d.c, loc, v.x, v.y, ex, th, seq, ib, d.g0, d.g1,
-                                       d.npairs, wt, wg, blockIdx.x);
-                        }
-                        if (v.x <= th) {
-                            p.clb[run * kKC + w] = v.x;
-                            p.cloc[run * kKC + w] = myloc[wt * kVmKC + i] & ((p.dbg & 32768u) ? 0xffffffu : 0xffffffffu);
-                            ++w;
+                for (uint32_t i = 0; i < ncand; ++i) w += clb[i * 32] <= th;
+                const uint32_t at = overflow ? 0u : atomicAdd(&o_cnt[wg * kVmQ + n], w);
+                if (overflow || at + w > kKC) {
+                    o_ovf[wg * kVmQ + n] = 1;
+                } else {
+                    uint32_t o = at;
+                    for (uint32_t i = 0; i < ncand; ++i) {
+                        const float li = clb[i * 32];
+                        if (li <= th) {
+                            p.clb[run * kKC + o] = li;
+                            p.cloc[run * kKC + o] = cloc[i * 32];
+                            ++o;
                         }
                     }
                 }
-                p.ccount[run] = ovf[wt] ? kOverflow : w;
-                if ((p.dbg & 32u) && ovf[wt]) printf("[vm-ovf] q=%u c=%u chunk=%u wg=%d\n", bq, d.c, d.chunk, wg);
-                if (p.dbg & 32u) {  // the run's upper bounds must be sorted, finite count <= candidates seen
-                    for (int i = 1; i < KT; ++i)
-                        if (ubl[i] < ubl[i - 1]) printf("[vm-ubl] unsorted q=%u\n", bq);
-                }
+                if (wl == 0)
+                    for (uint32_t i = 0; i < p.k; ++i)
+                        p.ub[run * p.k + i] =
+                            wg == 0 ? qthr_dec(*reinterpret_cast<volatile uint32_t*>(kb0 + i * kVmQ + n))
+                                    : __int_as_float(0x7f800000);
             }
+            named_bar(1 + wg, 128);
+            if (wl == 0 && active) {
+                const uint32_t pair = d.pairs[n];
+                const uint64_t run = (((uint64_t)pair * p.maxch + d.chunk) << 1) | (uint32_t)wg;
+                p.ccount[run] = o_ovf[wg * kVmQ + n] ? kOverflow : o_cnt[wg * kVmQ + n];
+            }
+            pf.mark(8);
             d = dn;
             have = hn;
         }
+        pf.report("vm-math", warp);
     }
     __syncthreads();
     if (warp == 1) {
@@ -2439,8 +2519,8 @@ static_assert(tc_smem_bytes<16, false>() <= 232448 && tc_smem_bytes<32, false>()
               "smem budget");
 
 constexpr size_t vm_smem_bytes() {
-    return 1024 + kVmNS * kVmSlot + 4 * kVmPlane + 2 * kVmQ * kVmKC * 12 + kVmNR * 4 * 32 * 4 +
-           8 * kVmQ * 4 + kMaxD * 4 + 8 * kVmQ * 4 + 2 * kVmQ * 4 + 8 * kVmQ * 4 +
+    return 1024 + kVmNS * kVmSlot + 4 * kVmPlane + 8 * 1024 * 4 + 8 * kVmKC * 32 * 8 + kVmNR * 4 * 32 * 4 +
+           2 * kVmQ * 4 * 3 + kMaxD * 4 + 8 * kVmQ * 4 + 2 * kVmQ * 4 + 4 * kVmQ * 4 + 2 * 32 * kVmQ * 4 +
            (2 * kVmNS + 2 * kVmNB + 4 + 2 * kRing + 2 * kVmNR) * 8 + kRing * sizeof(TcItem) + 16;
 }
 static_assert(vm_smem_bytes() <= 232448, "vm smem budget");
@@ -2513,6 +2593,43 @@ cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, bool
                      CU_TENSOR_MAP_SWIZZLE_64B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t make_vm_maps(const float* mir, const float* nrm, uint64_t groups, uint32_t D, CUtensorMap* out3) {
+    auto enc = get_encode();
+    if (!enc) return cudaErrorNotSupported;
+    const uint32_t K = mirror_k(D);
+    const cuuint64_t g = std::max<cuuint64_t>(groups, 1);
+    cuuint32_t e2[2] = {1, 1}, e3[3] = {1, 1, 1};
+    CUresult r;
+    {  // one group's hi plane: rows [0, K) of its 2K rows
+        cuuint64_t dims[2] = {32, g * 2 * K};
+        cuuint64_t str[1] = {64};
+        cuuint32_t box[2] = {32, K};
+        r = enc(&out3[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<float*>(mir), dims, str, box, e2,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+    {  // four consecutive groups' hi planes: {32 slots, K rows, groups}, group stride 2K rows
+        cuuint64_t dims[3] = {32, K, g};
+        cuuint64_t str[2] = {64, (cuuint64_t)2 * K * 64};
+        cuuint32_t box[3] = {32, K, 4};
+        r = enc(&out3[1], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<float*>(mir), dims, str, box, e3,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+    {  // the |s|^2 rows (first 32 of each group's 64 norm floats) of four consecutive groups
+        cuuint64_t dims[2] = {kNormFloats, g};
+        cuuint64_t str[1] = {kNormFloats * 4};
+        cuuint32_t box[2] = {32, 4};
+        r = enc(&out3[2], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(nrm), dims, str, box, e2,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+    return cudaSuccess;
 }
 
 namespace {
@@ -2595,22 +2712,18 @@ static cudaError_t launch_vm(const DevLists& L, const PlanBufs& B, const long lo
     if (e != cudaSuccess) return e;
     if (ev0) cudaEventRecord(ev0, s);
     const uint32_t wpb = 4;
-    static const uint32_t dbg = [] {
-        const char* v = std::getenv("BIVF_VM_DBG");
-        return v ? (uint32_t)atoi(v) : 0u;
+    static const bool seed = [] {
+        const char* v = std::getenv("BIVF_VM_SEED");  // 1: exact seeds first (measured: no gain at the north star)
+        return v && v[0] == '1';
     }();
-    p.dbg = dbg;
-    if (!(dbg & 2u))
-        vm_seed_kernel<<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * p.Dp * 4, s>>>(p, probes, sh.nq);
-    if (dbg & 64u) {  // debugging aid: the seeds as the results' first distance, no scan
-        cudaMemsetAsync(out_d, 0, (size_t)sh.nq * sh.k * 4, s);
-        cudaMemcpy2DAsync(out_d, (size_t)sh.k * 4, T.qthr, 4, 4, sh.nq, cudaMemcpyDeviceToDevice, s);
-        return cudaGetLastError();
-    }
+    if (seed) vm_seed_kernel<<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * p.Dp * 4, s>>>(p, probes, sh.nq);
     int grid = std::max(1, std::min(num_sms, max_grid));
     if (const char* g = std::getenv("BIVF_TC_GRID")) grid = std::max(1, atoi(g));  // debugging aid
-    if (sh.k <= 16) scan_vm_kernel<16><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, maps_hi[0], maps_hi[1]);
-    else scan_vm_kernel<32><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, maps_hi[0], maps_hi[1]);
+    VmMaps vmaps;
+    for (int a = 0; a < 2; ++a)
+        for (int i = 0; i < 3; ++i) vmaps.m[a][i] = maps_hi[3 * a + i];
+    if (sh.k <= 16) scan_vm_kernel<16><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, vmaps);
+    else scan_vm_kernel<32><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, vmaps);
     count_launch(2);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -2635,8 +2748,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     const bool wide = sh.metric == kIP;  // 1xBF16 inner-product mode (mirror.cuh wide mirror)
     if (wide && dense) return cudaErrorInvalidValue;
     static const bool vm_env = [] {
-        const char* v = std::getenv("BIVF_TC_VM");  // 1: the vector-major scan (scan_vm_kernel)
-        return v && v[0] == '1';
+        const char* v = std::getenv("BIVF_TC_VM");  // 0: the query-major 3xBF16 scan (comparison aid)
+        return !(v && v[0] == '0');
     }();
     if (maps_hi && vm_env && !wide && !dense && L.D <= (uint32_t)kMaxD)
         return launch_vm(L, B, probes, queries, centroids, sh, maps_hi, off_nrm, arena_nrm, off_rows,

@@ -52,6 +52,12 @@ cudaError_t launch_dense_plan(const DevLists& L, const PlanBufs& B, const long l
 cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, bool wide,
                             CUtensorMap* out, bool hi_only = false);
 
+// the vector-major scan's maps over one mirror region (offline segments or the
+// arena): out3[0] one group's hi plane, out3[1] four consecutive groups' hi
+// planes (3-D), out3[2] their |s|^2 rows; launch_ivf_search_tc takes six
+// (offline then arena) as maps_hi.
+cudaError_t make_vm_maps(const float* mir, const float* nrm, uint64_t groups, uint32_t D, CUtensorMap* out3);
+
 cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,
                                  const float* queries, const float* centroids,
                                  const SearchShape& sh, const CUtensorMap& map_off,

@@ -11,4 +11,4 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler
   -Xcompiler -ffp-contract=off -I paper_2408_02937_b200/csrc -I include "$@" \
   -c paper_2408_02937_b200/csrc/scan_tc.cu -o build/var/scan_tc_$name.o
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static \
-  -o var/libbivf_$name.so $(ls build/bivf/*.o | grep -v scan_tc) build/var/scan_tc_$name.o -lpthread -lgomp
+  -o var/libbivf_$name.so $(ls build/bivf/*.o | grep -v scan_tc) build/var/scan_tc_$name.o -lpthread -lgomp -ldl
