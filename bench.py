@@ -77,9 +77,11 @@ WORKLOAD = ("IVF-Flat 10Mx128 fp32 SIFT-like synthetic (256 components), nlist=4
             "k=10, 10K vec/s Zipf live inserts + 1K deletes/s")
 SNAPSHOT = "/tmp/bivf_north_star.bivf"
 
-# mirror bytes per 32-vector group the TC scan streams (mirror.cuh): bf16 hi + lo
-# planes (2 x K x 32 x 2 B, K = D rounded to 16) + the norm block (64 fp32)
-MIRROR_GROUP_BYTES = 2 * ((DIM + 15) // 16 * 16) * 32 * 2 + 64 * 4
+# bytes per 32-vector group the vector-major TC scan streams (scan_tc.cu
+# scan_vm_kernel): the mirror's bf16 hi plane (K x 32 x 2 B, K = D rounded to 16)
+# + the group's |s|^2 row (32 fp32); queries are tiled 32 per work item
+MIRROR_GROUP_BYTES = ((DIM + 15) // 16 * 16) * 32 * 2 + 32 * 4
+SCAN_TILE = 32
 
 
 def log(*a):
@@ -445,58 +447,59 @@ def run_ours(args, dist):
     return result
 
 
-def scan_bytes(probes, sizes, tile=128):
-    """Algorithmic bytes of one search's list scan: the TC scan
-    groups queries by list, ≤ `tile` queries per work item, and streams each
-    probed list's mirror once per item (MIRROR_GROUP_BYTES per 32-vector group),
-    plus the seeding pass (first unit, 2 groups, of every query's nearest list)."""
+def scan_bytes(probes, sizes, tile=SCAN_TILE):
+    """Algorithmic bytes of one search's list scan: the scan groups
+    queries by list, <= `tile` queries per work item, and streams each probed
+    list's hi plane + norm rows once per item (MIRROR_GROUP_BYTES per 32-vector
+    group); a list with more than `tile` of the batch's queries is streamed once
+    per tile (the repeats mostly hit L2: compare `traffic`)."""
     nl = len(sizes)
     groups = (sizes + 31) // 32
     q_per_list = np.bincount(probes.reshape(-1).astype(np.int64), minlength=nl)
     tiles = (q_per_list + tile - 1) // tile
     full = int((tiles * groups).sum()) * MIRROR_GROUP_BYTES
-    q_near = np.bincount(probes[:, 0].astype(np.int64), minlength=nl)
-    seed = int((((q_near + tile - 1) // tile) * np.minimum(groups, 2)).sum()) * MIRROR_GROUP_BYTES
+    once = int(groups[q_per_list > 0].sum()) * MIRROR_GROUP_BYTES
     pairs = int(sizes[probes].sum())
-    return full + seed, pairs
+    return full, once, pairs
 
 
 def roofline(probes, sizes, ph, peaks):
-    """Roofline of the dominant kernel (scan_tc_kernel).
+    """Roofline of the dominant kernel (scan_vm_kernel).
 
     At 10M x 128 a 10K-query batch with nprobe 12 probes every list ~29 times,
-    and the TC scan serves all of a list's queries (≤128 per item) from one
-    pass over the list's scan mirror: the kernel streams the whole mirror from
-    HBM once per batch and is HBM-bound.  achieved = algorithmic bytes per
-    search (scan_bytes) / the scan phase's CUDA-event time; peak =
-    MEASURED_PEAKS.json hbm_gbs.  Beside it: the tensor work of the 3xBF16
-    filter (3 x 2 x K flops per (query, vector) pair) and its useful fp32
-    share (1 of the 3 MMAs).  `traffic` = ncu DRAM read+write bytes of the
-    scan launches of one search (profiles/r02_scan_tc_ncu.json, same workload)."""
-    alg_bytes, pairs = scan_bytes(probes, sizes)
+    and the scan serves a list's queries (<= 32 per work item) from one pass over
+    the list's bf16 hi plane + norm rows: the kernel streams the scan mirror's hi
+    half from HBM about once per batch and is HBM-bound.  achieved = algorithmic
+    bytes per search (scan_bytes: every item's groups) / the scan phase's
+    CUDA-event time; peak = MEASURED_PEAKS.json hbm_gbs.  Beside it: the bytes if
+    every probed list were streamed exactly once, and the tensor work (2 bf16
+    MMAs per K-step: 2 x 2 x K flops per pair, vector x (query hi + query lo)).
+    `traffic` = ncu DRAM read+write bytes of the scan launch of one search
+    (profiles/r02_scan_vm_ncu.json, same workload)."""
+    alg_bytes, once_bytes, pairs = scan_bytes(probes, sizes)
     scan_ms = ph[2]
     hbm = peaks.get("hbm_gbs", 6548.2)
     achieved = alg_bytes / (scan_ms * 1e-3) / 1e9
     tc_peak = peaks.get("bf16_tflops", 1641.9)
     Kd = (DIM + 15) // 16 * 16
-    tflops = 3.0 * 2.0 * Kd * pairs / (scan_ms * 1e-3) / 1e12
+    tflops = 2.0 * 2.0 * Kd * pairs / (scan_ms * 1e-3) / 1e12
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r02_scan_tc_ncu.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_scan_vm_ncu.json")) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": round(hbm, 1), "unit": "GB/s",
             "frac": round(achieved / hbm, 3), "traffic": traffic,
-            "kernel": "scan_tc_kernel (2 launches per search: seeding pass, full scan)",
+            "kernel": "scan_vm_kernel (1 launch per search)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
             "alg_bytes_per_launch": alg_bytes,
-            "alg_bytes_rule": f"sum over (list, <=128-query item) of the list's mirror groups x "
-                              f"{MIRROR_GROUP_BYTES} B + seeding pass",
+            "alg_bytes_rule": f"sum over (list, <=32-query item) of the list's groups x {MIRROR_GROUP_BYTES} B "
+                              f"(bf16 hi plane + |s|^2 row)",
+            "alg_bytes_each_list_once": once_bytes,
             "scan_ms": round(scan_ms, 3),
             "tensor": {"pairs": pairs, "achieved_tflops": round(tflops, 1), "peak_tflops": tc_peak,
-                       "frac": round(tflops / tc_peak, 3),
-                       "useful_fp32_frac": round(tflops / 3 / tc_peak, 3)},
+                       "frac": round(tflops / tc_peak, 3)},
             "phase_ms": {"quantizer": round(ph[0], 3), "plan": round(ph[1], 3),
                          "scan": round(ph[2], 3), "refine": round(ph[3], 3)}}
 

@@ -58,9 +58,10 @@ def rep_summary(rep, out):
                                   sorted(stalls.items(), key=lambda x: -x[1])[:6]}
         kernels.append(k)
     summ = {"source": rep, "kernels": kernels}
-    # the list scan of one search = every scan_tc_kernel<16> launch captured (the two
-    # phases of the two-phase scan; the coarse quantizer is the <32> instantiation)
-    tc = [k for k in kernels if "scan_tc_kernel<16" in k["kernel"]]
+    # the list scan of one search = the scan_vm_kernel launch (or, for the query-major
+    # kernel, every scan_tc_kernel<16> launch: its seeding and full passes)
+    tc = [k for k in kernels if "scan_vm_kernel" in k["kernel"]] or \
+        [k for k in kernels if "scan_tc_kernel<16" in k["kernel"]]
     if tc:
         summ["dram_bytes_per_launch"] = int(sum(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0)
                                                 for k in tc))

@@ -53,11 +53,19 @@ def main():
     ix.bulk_load(base, ix.assign_batch(base))
     ix.set_scan_mode("auto")
     ix.set_timing(True)
+    acc = []
     for r in range(reps):
         t = time.perf_counter()
         ix.search_batch(q[(r * nq) % len(q):][:nq], k, nprobe)
-        print(f"rep {r}: {1e3 * (time.perf_counter() - t):.2f} ms wall, phases(ms)="
-              f"{[round(v, 3) for v in ix.last_timings()]}", flush=True)
+        ph = ix.last_timings()
+        if r >= 2:
+            acc.append(ph)
+        if reps <= 8 or r >= reps - 2:
+            print(f"rep {r}: {1e3 * (time.perf_counter() - t):.2f} ms wall, phases(ms)="
+                  f"{[round(v, 3) for v in ph]}", flush=True)
+    if len(acc) > 2:
+        print(f"mean phases over reps 2..{reps - 1} (ms): {[round(float(np.mean([a[i] for a in acc])), 4) for i in range(4)]}",
+              flush=True)
 
 
 if __name__ == "__main__":
