@@ -494,7 +494,7 @@ static void wq_push(workq* w, uint32_t c) {
     w->n++;
 }
 
-/* ivf_index.cpp:527-539 */
+/* ivf_index.cpp:356-368 (remap_cluster_refs) */
 static void remap_refs(orc_index* h, int32_t c, int32_t a, int32_t b) {
     if (h->head[c] == a) h->head[c] = b;
     else if (h->head[c] == b) h->head[c] = a;
@@ -504,7 +504,7 @@ static void remap_refs(orc_index* h, int32_t c, int32_t a, int32_t b) {
 
 static int32_t remap1(int32_t x, int32_t a, int32_t b) { return x == a ? b : (x == b ? a : x); }
 
-/* ivf_index.cpp:541-583: exchange the contents (ids, payload, committed) of
+/* ivf_index.cpp:370-412 (swap_blocks): exchange the contents (ids, payload, committed) of
  * physical blocks a and b, then rewrite both headers and every neighbour /
  * list-head / list-tail reference so both logical lists are unchanged. */
 static void swap_blocks(orc_index* h, int32_t a, int32_t b) {
@@ -546,7 +546,7 @@ static void swap_blocks(orc_index* h, int32_t a, int32_t b) {
     if (ob >= 0 && ob != oa) remap_refs(h, ob, a, b);
 }
 
-/* ivf_index.cpp:585-605: break fused runs touching x; owners re-merge later */
+/* ivf_index.cpp:414-434 (split_runs_around): break fused runs touching x; owners re-merge later */
 static void split_runs_around(orc_index* h, int32_t x, workq* w) {
     if (h->merged[x]) {
         h->merged[x] = 0;
@@ -559,7 +559,7 @@ static void split_runs_around(orc_index* h, int32_t x, workq* w) {
     }
 }
 
-/* ivf_index.cpp:607-645 (Alg. 3): walk the list; for every logical link u->v
+/* ivf_index.cpp:436-474 (rearrange_locked) (Alg. 3): walk the list; for every logical link u->v
  * that is not fused, pull v into the physical successor p = u+1 (swap), or
  * just mark the fusion when v already is u+1. */
 static void rearrange_list(orc_index* h, uint32_t c, uint64_t* merges, workq* w) {
@@ -744,7 +744,7 @@ void orc_offline_segment(const orc_index* h, uint32_t c, int64_t* ids, float* pa
     memcpy(payload, h->off_pay[c], groups * h->G * h->D * sizeof(float));
 }
 
-/* ivf_index.cpp:505-523: offline then online (traverse order) */
+/* ivf_index.cpp:334-354 (cluster_contents): offline then online (traverse order) */
 uint64_t orc_cluster_contents(const orc_index* h, uint32_t c, int64_t* ids, float* vecs) {
     uint64_t n = 0;
     const uint64_t D = h->D, G = h->G;

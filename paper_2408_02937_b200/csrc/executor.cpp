@@ -84,6 +84,11 @@ Ticket Executor::submit_search(const float* q, uint32_t nq, uint32_t k, uint32_t
     if (k < 1) throw Error(BIVF_EINVAL, "submit_search: k must be >= 1");
     if (nprobe < 1 || nprobe > index_.C())
         throw Error(BIVF_EINVAL, "submit_search: nprobe out of [1, num_clusters]");
+    // the device path's limits (INTEGRATION.md "Limits"), rejected at submission
+    // rather than in the lane: the reference accepts any k and nprobe <= C
+    if (k > 256) throw Error(BIVF_EINVAL, "submit_search: k above the device top-k capacity (256)");
+    if (nprobe > 256 && nprobe != index_.C())
+        throw Error(BIVF_EINVAL, "submit_search: nprobe must be <= 256 or == num_clusters");
     Ticket t = make_ticket(RequestType::Search);
     if (!accepting_.load()) {
         t->start = t->end = Clock::now();

@@ -2262,7 +2262,7 @@ struct Planner {
             work.push_back((uint32_t)o);
         }
     }
-    // ivf_index.cpp:585-605
+    // ivf_index.cpp:414-434 (split_runs_around)
     void split_runs_around(int32_t x) {
         if (merged[x]) {
             merged[x] = 0;
@@ -2274,7 +2274,7 @@ struct Planner {
             enqueue(x);
         }
     }
-    // ivf_index.cpp:541-583 (headers), data via content_at
+    // ivf_index.cpp:370-412 (swap_blocks) (headers), data via content_at
     void swap_blocks(int32_t a, int32_t b) {
         if (a == b) return;
         const int32_t pa = prev[a], na = next[a], pb = prev[b], nb = next[b];
@@ -2306,7 +2306,7 @@ struct Planner {
         if (ob >= 0) blocks[ob][mb] = a;
         if (oa >= 0) blocks[oa][ma] = b;
     }
-    // ivf_index.cpp:607-645
+    // ivf_index.cpp:436-474 (rearrange_locked)
     void rearrange_list(uint32_t c) {
         int32_t u = head[c];
         if (u < 0) return;
@@ -2694,7 +2694,7 @@ std::string GpuIndex::dump_pool() const {
 }
 
 // ========================================================================
-// BIVFSNAP v1 (ivf_index.cpp:515-619)
+// BIVFSNAP v1 (ivf_index.cpp:513-619)
 // ========================================================================
 
 namespace {

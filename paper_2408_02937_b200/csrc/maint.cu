@@ -3,7 +3,7 @@
 // merge (K8) and small glue kernels.  sm_100a.
 //
 // Reference semantics:
-//   swap_blocks data part       src/ivf_index.cpp:541-557 (ids + payload + committed)
+//   swap_blocks data part       src/ivf_index.cpp:381-384 (save_to_scratch / copy_block_data / restore)
 //   delete                      none in the reference; rules: DESIGN.md §Delete
 // Moves are planned on the host mirror.  Concurrent searches are never fenced:
 // new versions of the touched blocks / segments are built in storage no

@@ -1775,13 +1775,17 @@ __device__ __forceinline__ const float* cand_row(const TcParams& p, uint32_t c, 
     return p.arena_rows + (g * 32u + s) * p.D;
 }
 
-template <int KPL, int MET>
+// WPQ warps per query (small batches: the latency path has only a few queries,
+// one warp each would leave the GPU idle): the warps split the query's runs,
+// then merge their thresholds / top-k lists through shared memory.
+template <int KPL, int MET, int WPQ>
 __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d, long long* out_i,
                               uint32_t* out_cnt, uint32_t nq) {
-    extern __shared__ float qsm[];  // [warps][Dp] queries, then [warps][32] x 2 queue
+    extern __shared__ float qsm[];  // [warps][Dp] queries, then [warps][32] x 2 queue, then (WPQ > 1) merge area
     const uint32_t nw = blockDim.x >> 5;
     const uint32_t wq = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t q = blockIdx.x * nw + wq;
+    const uint32_t q = blockIdx.x * (nw / WPQ) + wq / WPQ;
+    const uint32_t ws = wq % WPQ;  // this warp's share of the query's runs
     if (q >= nq) return;
     float* qs = qsm + wq * p.Dp;
     uint32_t* qc = reinterpret_cast<uint32_t*>(qsm + nw * p.Dp) + wq * 64;  // list
@@ -1800,7 +1804,7 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
         const uint32_t per_probe = p.maxch * 2u * p.k;
         const uint32_t total = p.P * per_probe;
         const uint64_t base = (uint64_t)q * total;
-        for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+        for (uint32_t f0 = 32 * ws; f0 < total; f0 += 32 * WPQ) {
             const uint32_t f = f0 + lane;
             bool pass = false;
             float v = 0.f;
@@ -1823,7 +1827,39 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
             }
         }
     }
-    const float theta = fminf(th.thr_d, pre);  // +inf if fewer than k vectors were scanned
+    float theta = fminf(th.thr_d, pre);  // +inf if fewer than k vectors were scanned
+    float* mrg = qsm + nw * p.Dp + nw * 64;  // (WPQ > 1) [warps][32 * KPL] floats + [warps][32 * KPL] ids
+    if constexpr (WPQ > 1) {
+        // the query's k-th smallest upper bound over every warp's share: the first
+        // warp folds the others' k smallest values in
+        float* mv = mrg + wq * 32 * KPL;
+#pragma unroll
+        for (int r = 0; r < KPL; ++r) mv[r * 32 + lane] = th.d[r];
+        named_bar(4, WPQ * 32 * (nw / WPQ));  // every warp of the block (whole blocks of queries)
+        if (ws == 0) {
+            for (uint32_t o = 1; o < (uint32_t)WPQ; ++o) {
+                const float* ov = mrg + (wq + o) * 32 * KPL;
+#pragma unroll
+                for (int r = 0; r < KPL; ++r) {
+                    const uint32_t e = r * 32 + lane;
+                    const float v = ov[r * 32 + lane];
+                    const bool pass = e < p.k && th.admits(v, (long long)(o * 4096u + e));
+                    unsigned msk = __ballot_sync(0xffffffffu, pass);
+                    while (msk) {
+                        const int src = __ffs(msk) - 1;
+                        msk &= msk - 1;
+                        const float bv = __shfl_sync(0xffffffffu, v, src);
+                        const long long bi = (long long)(o * 4096u + r * 32 + src);
+                        if (th.admits(bv, bi)) th.insert(bv, bi, (int)p.k, lane);
+                    }
+                }
+            }
+            if (lane == 0) mrg[wq * 32 * KPL] = fminf(th.thr_d, pre);
+        }
+        named_bar(4, WPQ * 32 * (nw / WPQ));
+        theta = mrg[(wq - ws) * 32 * KPL];
+        named_bar(4, WPQ * 32 * (nw / WPQ));  // the merge area is reused below
+    }
     // 2. exact top-k over the surviving candidates
     WarpTopK<KPL> tk;
     tk.init();
@@ -1859,7 +1895,7 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
     // so small batches with many chunks per list do not serialise on latency
     const uint32_t nruns = p.P * p.maxch * 2u;
     const uint64_t rbase = (uint64_t)q * nruns;
-    for (uint32_t r0 = 0; r0 < nruns; r0 += 32) {
+    for (uint32_t r0 = 32 * ws; r0 < nruns; r0 += 32 * WPQ) {
         const uint32_t r = r0 + lane;
         uint32_t c = 0, cnt = 0, h = 0;
         bool valid = false;
@@ -1909,6 +1945,23 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
         }
     }
     if (qn) flush();
+    if constexpr (WPQ > 1) {  // fold the other warps' exact top-k lists into the first warp's
+        float* md = mrg + wq * 32 * KPL * 3;
+        long long* mi = reinterpret_cast<long long*>(md + 32 * KPL);
+#pragma unroll
+        for (int r = 0; r < KPL; ++r) {
+            md[r * 32 + lane] = tk.d[r];
+            mi[r * 32 + lane] = tk.id[r];
+        }
+        named_bar(4, WPQ * 32 * (nw / WPQ));
+        if (ws != 0) return;
+        for (uint32_t o = 1; o < (uint32_t)WPQ; ++o) {
+            const float* od = mrg + (wq + o) * 32 * KPL * 3;
+            const long long* oi = reinterpret_cast<const long long*>(od + 32 * KPL);
+#pragma unroll
+            for (int r = 0; r < KPL; ++r) offer(od[r * 32 + lane], oi[r * 32 + lane], oi[r * 32 + lane] >= 0);
+        }
+    }
     uint32_t cntq = 0;
 #pragma unroll
     for (int r = 0; r < KPL; ++r) {
@@ -2728,8 +2781,15 @@ static cudaError_t launch_vm(const DevLists& L, const PlanBufs& B, const long lo
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (ev1) cudaEventRecord(ev1, s);
-    refine_kernel<1, kL2><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(p, probes, out_d, out_i,
-                                                                                           out_cnt, sh.nq);
+    // small batches: 8 warps per query (the refine is latency-bound per warp)
+    if (sh.nq * 8 <= (uint32_t)num_sms * 16) {
+        constexpr int WPQ = 8;
+        const size_t sm = WPQ * (p.Dp * 4 + 256) + WPQ * 32 * 1 * 12 + 16;
+        refine_kernel<1, kL2, WPQ><<<sh.nq, WPQ * 32, sm, s>>>(p, probes, out_d, out_i, out_cnt, sh.nq);
+    } else {
+        refine_kernel<1, kL2, 1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
+            p, probes, out_d, out_i, out_cnt, sh.nq);
+    }
     count_launch();
     return cudaGetLastError();
 }
@@ -2875,10 +2935,10 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                 sh.k, out_d, out_i, dense->gsum);
     } else {
         if (wide)
-            refine_kernel<1, kIP><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
+            refine_kernel<1, kIP, 1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
                 p, probes, out_d, out_i, out_cnt, sh.nq);
         else
-            refine_kernel<1, kL2><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
+            refine_kernel<1, kL2, 1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * (p.Dp * 4 + 256), s>>>(
                 p, probes, out_d, out_i, out_cnt, sh.nq);
     }
     count_launch();
