@@ -185,6 +185,11 @@ bivf_status bivf_next_id(const bivf_index* h, int64_t* out);
 /* one-shot utilization alert (block_store.cpp:41-46): *fired, and the number of
  * blocks in use at the allocation that first exceeded the watermark */
 bivf_status bivf_pool_alert(const bivf_index* h, int32_t* fired, uint64_t* used_at);
+/* the list scan's seed samples: per list up to 32 ids of
+ * central offline vectors, -1 for empty / deleted entries; writes
+ * min(cap, num_clusters * 32) ids (list-major), *n = num_clusters * 32, or 0
+ * when the index keeps no samples */
+bivf_status bivf_seed_samples(const bivf_index* h, int64_t* out, uint64_t cap, uint64_t* n);
 /* block_store.hpp set_next: raw header-link mutation (the reference pool's test
  * hook; traversals then report cycles as BIVF_ECORRUPT) */
 bivf_status bivf_block_set_next(bivf_index* h, int32_t block, int32_t next);

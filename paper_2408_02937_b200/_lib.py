@@ -137,6 +137,7 @@ SIGNATURES = {
     "bivf_load_snapshot": (C.c_int, [C.c_char_p, C.POINTER(Config), C.POINTER(vp)]),
     "bivf_load_snapshot_shard": (C.c_int, [C.c_char_p, u32, u32, C.POINTER(Config), C.POINTER(vp)]),
     "bivf_pool_alert": (C.c_int, [vp, C.POINTER(i32), pu64]),
+    "bivf_seed_samples": (C.c_int, [vp, vp, u64, pu64]),
     "bivf_block_set_next": (C.c_int, [vp, i32, i32]),
     "bivf_exact_knn": (C.c_int, [vp, u64, u64, vp, u64, u64, i32, i32, vp, vp, vp]),
     "bivf_add": (C.c_int, [vp, vp, u64, vp, vp, pu64]),

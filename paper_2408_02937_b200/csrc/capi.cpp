@@ -194,6 +194,13 @@ bivf_status bivf_load_snapshot_shard(const char* path, uint32_t shard, uint32_t 
     });
 }
 
+bivf_status bivf_seed_samples(const bivf_index* h, int64_t* out, uint64_t cap, uint64_t* n) {
+    return guard([&] {
+        need(n, "n");
+        *n = I(h).seed_samples(out, cap);
+    });
+}
+
 bivf_status bivf_pool_alert(const bivf_index* h, int32_t* fired, uint64_t* used_at) {
     return guard([&] { I(h).alert_state(fired, used_at); });
 }

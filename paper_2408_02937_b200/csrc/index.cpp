@@ -737,6 +737,16 @@ void GpuIndex::bulk_load(const float* x, uint64_t n, const uint32_t* assignment,
     for (uint32_t c = 0; c < C_; ++c) h_off_count_[c] = (uint32_t)counts[c];
     BIVF_CUDA(h2d(d_off_start_.p, h_off_start_.data(), (size_t)C_ * 8));
     BIVF_CUDA(h2d(d_off_count_.p, h_off_count_.data(), (size_t)C_ * 4));
+    // seed samples of the vector-major scan: central offline vectors per list
+    if (cfg_.metric != BIVF_METRIC_IP && D_ <= 128) {
+        d_samp_rows_.ensure((size_t)C_ * D_ * kSampS * 4);
+        d_samp_ids_.ensure((size_t)C_ * kSampS * 8);
+        BIVF_CUDA(launch_sample_build(d_off_pay_.as<float>(), d_off_ids_.as<long long>(), d_off_start_.as<uint64_t>(),
+                                      d_off_count_.as<uint32_t>(), d_cent_.as<float>(), C_, D_,
+                                      d_samp_rows_.as<float>(), d_samp_ids_.as<long long>(), data_stream_));
+        BIVF_CUDA(cudaStreamSynchronize(data_stream_));
+        samp_on_ = true;
+    }
     if (ids) {
         int64_t mx = -1;
         for (uint64_t i = 0; i < n; ++i) {
@@ -1172,7 +1182,9 @@ void GpuIndex::enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Works
                                        nullptr, w.out_d,
                                        w.out_i, w.out_cnt, num_sms_, l.stream,
                                        timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr, 1 << 30,
-                                       maps_h_ok_ && d_arena_rows_.p ? maps_h_ : nullptr));
+                                       maps_h_ok_ && d_arena_rows_.p ? maps_h_ : nullptr,
+                                       samp_on_ ? d_samp_rows_.as<float>() : nullptr,
+                                       samp_on_ ? d_samp_ids_.as<long long>() : nullptr));
         if (stats) {
             std::vector<uint32_t> cc(runs);
             BIVF_CUDA(cudaMemcpyAsync(cc.data(), w.tc.ccount, runs * 4, cudaMemcpyDeviceToHost,
@@ -1917,6 +1929,7 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
         }
     };
     uint64_t removed = 0;
+    std::vector<long long> gone;
     for (uint64_t r = 0; r < n; ++r) {
         if (loc[r] == ~0ull) continue;
         uint64_t key, pos0;
@@ -1944,9 +1957,21 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
         P.where[gone_orig] = ~0ull;
         P.count = (uint32_t)last;
         if (found) found[r] = 1;
+        gone.push_back(ids[r]);
         ++removed;
     }
     if (removed == 0) return 0;
+    // the seed samples drop the deleted ids before any list is republished: a
+    // search that plans against the new versions never seeds with them
+    if (samp_on_) {
+        std::sort(gone.begin(), gone.end());
+        DevBuf& dg = s_rm_[11];
+        dg.ensure(gone.size() * 8);
+        BIVF_CUDA(cudaMemcpyAsync(dg.p, gone.data(), gone.size() * 8, cudaMemcpyHostToDevice, st));
+        BIVF_CUDA(launch_sample_invalidate(d_samp_ids_.as<long long>(), (uint64_t)C_ * kSampS, dg.as<long long>(),
+                                           (uint32_t)gone.size(), st));
+        BIVF_CUDA(cudaStreamSynchronize(st));  // the host copy of `gone` is a pageable source
+    }
     // slot addresses (maint.cuh): payload float offset / id index, arena bit 63
     auto pay_at = [&](bool arena, uint64_t blk_or_start, uint64_t slot) -> uint64_t {
         if (arena)
@@ -2549,6 +2574,17 @@ void GpuIndex::apply_block_moves(const std::vector<int32_t>& src, const std::vec
 }
 
 // oldest `cap` events; the rest stay queued for the next call
+uint64_t GpuIndex::seed_samples(int64_t* out, uint64_t cap) const {
+    std::lock_guard<std::mutex> lk(data_mu_);
+    if (!samp_on_) return 0;
+    const uint64_t n = (uint64_t)C_ * kSampS;
+    if (out && cap) {
+        BIVF_CUDA(cudaSetDevice(device_));
+        BIVF_CUDA(cudaMemcpy(out, d_samp_ids_.p, std::min(cap, n) * 8, cudaMemcpyDeviceToHost));
+    }
+    return n;
+}
+
 std::vector<RearrangeEvent> GpuIndex::take_events(size_t cap) {
     std::lock_guard<std::mutex> lk(events_mu_);
     std::vector<RearrangeEvent> out;

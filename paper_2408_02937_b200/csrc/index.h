@@ -379,6 +379,13 @@ private:
 
     CUtensorMap map_off_{}, map_arena_{};
     CUtensorMap maps_h_[6]{};  // scan_vm_kernel's maps (make_vm_maps): offline [0, 3), arena [3, 6)
+    DevBuf d_samp_rows_, d_samp_ids_;  // seed samples (maint.cuh kSampS per list), built by bulk_load
+    bool samp_on_ = false;
+
+public:
+    uint64_t seed_samples(int64_t* out, uint64_t cap) const;
+
+private:
     bool maps_h_ok_ = false;
     bool tc_ok_ = false;
     int scan_mode_ = 0;  // 0 auto, 1 CUDA-core only, 2 tensor-core when supported

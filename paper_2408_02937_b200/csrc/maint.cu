@@ -312,4 +312,99 @@ cudaError_t launch_merge_shards(const float* dists, const long long* ids, uint32
     return cudaGetLastError();
 }
 
+// ---- seed samples (scan_tc.cu vm_seed_kernel) ----------------------------
+// Per list, kSampS stored vectors of its offline segment with small residual
+// norms |x - c|^2 (each of 512 threads keeps its 2 best, the block sorts the 1024
+// and takes the first kSampS), copied in the interleaved group layout
+// [list][d][slot] with their ids.  Any stored vectors make a valid seed; central
+// ones make a tight one (their distance to a query is close to |q - c|^2).
+namespace {
+__global__ void __launch_bounds__(512) sample_build_kernel(const float* off_pay, const long long* off_ids,
+                                                           const uint64_t* off_start, const uint32_t* off_count,
+                                                           const float* cent, uint32_t D, float* rows,
+                                                           long long* ids) {
+    __shared__ uint64_t key[1024];
+    const uint32_t c = blockIdx.x, t = threadIdx.x;
+    const uint32_t n = off_count[c];
+    const uint64_t start = off_start[c];
+    const float* cc = cent + (uint64_t)c * D;
+    uint64_t b0 = ~0ull, b1 = ~0ull;
+    for (uint32_t v = t; v < n; v += 512) {
+        const uint64_t slot = start + v;
+        const float* x = off_pay + (slot >> 5) * 32ull * D + (slot & 31u);
+        float s2 = 0.f;
+        for (uint32_t d = 0; d < D; ++d) {
+            const float r = x[(uint64_t)d * 32] - cc[d];
+            s2 = fmaf(r, r, s2);
+        }
+        const uint64_t k = ((uint64_t)__float_as_uint(s2) << 32) | v;  // s2 >= 0: bits order as values
+        if (k < b0) {
+            b1 = b0;
+            b0 = k;
+        } else if (k < b1) {
+            b1 = k;
+        }
+    }
+    key[2 * t] = b0;
+    key[2 * t + 1] = b1;
+    __syncthreads();
+    for (uint32_t sz = 2; sz <= 1024; sz <<= 1)  // bitonic sort, ascending
+        for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
+            for (uint32_t i = t; i < 1024; i += 512) {
+                const uint32_t j = i ^ st;
+                if (j > i) {
+                    const bool up = (i & sz) == 0;
+                    const uint64_t a = key[i], b = key[j];
+                    if ((a > b) == up) {
+                        key[i] = b;
+                        key[j] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (uint32_t e = t; e < kSampS * D; e += 512) {  // e = d * kSampS + slot
+        const uint32_t d = e / kSampS, sl = e % kSampS;
+        const uint64_t k = key[sl];
+        const bool ok = k != ~0ull;
+        const uint64_t slot = start + (uint32_t)k;
+        rows[((uint64_t)c * D + d) * kSampS + sl] =
+            ok ? off_pay[(slot >> 5) * 32ull * D + (uint64_t)d * 32 + (slot & 31u)] : 0.f;
+        if (d == 0) ids[(uint64_t)c * kSampS + sl] = ok ? off_ids[slot] : -1;
+    }
+}
+
+// a deleted id leaves every list's sample (gone: ascending)
+__global__ void sample_invalidate_kernel(long long* ids, uint64_t n, const long long* gone, uint32_t ng) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long v = ids[i];
+    if (v < 0) return;
+    uint32_t lo = 0, hi = ng;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (gone[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    if (lo < ng && gone[lo] == v) ids[i] = -1;
+}
+}  // namespace
+
+cudaError_t launch_sample_build(const float* off_pay, const long long* off_ids, const uint64_t* off_start,
+                                const uint32_t* off_count, const float* cent, uint32_t C, uint32_t D,
+                                float* rows, long long* ids, cudaStream_t s) {
+    if (!C) return cudaSuccess;
+    sample_build_kernel<<<C, 512, 0, s>>>(off_pay, off_ids, off_start, off_count, cent, D, rows, ids);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample_invalidate(long long* ids, uint64_t n, const long long* gone, uint32_t ng,
+                                     cudaStream_t s) {
+    if (!n || !ng) return cudaSuccess;
+    sample_invalidate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ids, n, gone, ng);
+    count_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace bivf

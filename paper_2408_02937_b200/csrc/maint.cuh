@@ -39,4 +39,13 @@ cudaError_t launch_publish_lists(uint32_t n, const uint32_t* idx, const uint64_t
 
 constexpr uint64_t kArenaBit = 1ull << 63;
 
+// seed samples of the vector-major scan: kSampS offline vectors per list with
+// small residual norms, [list][d][slot] + ids (-1 = empty / deleted)
+constexpr uint32_t kSampS = 32;
+cudaError_t launch_sample_build(const float* off_pay, const long long* off_ids, const uint64_t* off_start,
+                                const uint32_t* off_count, const float* cent, uint32_t C, uint32_t D,
+                                float* rows, long long* ids, cudaStream_t s);
+cudaError_t launch_sample_invalidate(long long* ids, uint64_t n, const long long* gone, uint32_t ng,
+                                     cudaStream_t s);
+
 }  // namespace bivf

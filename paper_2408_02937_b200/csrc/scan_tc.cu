@@ -38,6 +38,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "maint.cuh"
 #include "mirror.cuh"
 #include "launches.h"
 #include "scan.cuh"
@@ -135,6 +136,8 @@ struct TcParams {
     uint32_t brow, gstride, nkc;  // TMA box rows, map rows per group, K-chunks per group (wide: Dk / brow)
     uint32_t seed_groups;        // seeding pass: scan only the first seed_groups groups, no run output
     uint32_t qt;                 // plan tile: pairs per work item (kM, or kVmQ for scan_vm_kernel)
+    const float* samp_rows;      // seed samples (maint.cuh kSampS per list, [list][d][slot]) or null
+    const long long* samp_ids;   // their ids (-1: empty / deleted)
     const float* centroids;      // [C][D] row-major
     const float* queries;        // [nq][Dp]
     const uint32_t* snap_off;
@@ -1205,6 +1208,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t K = p.Dk;  // mirror rows per plane (D rounded up to 16)
+#if BIVF_TC_PROF
+    __shared__ uint32_t prof_ev[8];  // pass-1 survivors, k-best offers, CAS attempts, appends, compactions
+    if (threadIdx.x < 8) prof_ev[threadIdx.x] = 0;
+#endif
     if (threadIdx.x == 0) {
         for (int s = 0; s < kVmNS; ++s) {
             mbar_init(&full[s], 1);
@@ -1429,19 +1436,35 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             d = ring[rs];
             __syncwarp();
             if (lane == 0) mbar_arrive(&it_empty[rs]);
+            // this thread's query values and centroid value: global loads issued
+            // before the barrier (they write no shared state)
+            const uint32_t n = t256 & 31, h = t256 >> 5;  // column n, dims [16h, 16h + 16)
+            const bool act = d.valid && n < d.npairs;
+            float4 qv4[4];
+            {
+                const uint32_t pair = act ? d.pairs[n] : 0u;
+                const float* q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t k0 = 16 * h + 4 * i;
+                    qv4[i] = (act && k0 < p.Dp) ? __ldg(reinterpret_cast<const float4*>(q + k0))
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+            const float cv = (d.valid && (uint32_t)t256 < p.D) ? __ldg(p.centroids + (uint64_t)d.c * p.D + t256) : 0.f;
             // both warpgroups are done with item seq - 2's state: taken for the
             // end marker too (no warp may run ahead of another's run output)
             named_bar(3, 256);
+            if (t256 < 2 * kVmQ) {  // the run-output gather counters of item seq - 1 (output after this build)
+                o_cnt[t256] = 0;
+                o_ovf[t256] = 0;
+            }
             if (!d.valid) return false;
             const uint32_t ib = seq & 1;
             if (seq >= 2) mbar_wait(&b_free[ib], ((seq - 2) >> 1) & 1);
-            if (t256 < (int)K) cent_s[t256] = (uint32_t)t256 < p.D ? __ldg(p.centroids + (uint64_t)d.c * p.D + t256) : 0.f;
+            if (t256 < (int)K) cent_s[t256] = cv;
             named_bar(3, 256);
             {
-                const uint32_t n = t256 & 31, h = t256 >> 5;  // column n, dims [16h, 16h + 16)
-                const bool act = n < d.npairs;
-                const uint32_t pair = act ? d.pairs[n] : 0u;
-                const float* q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
                 float nh = 0.f;
                 if (16 * h < K) {
                     unsigned char* bh = sB + ib * 2 * kVmPlane;
@@ -1449,8 +1472,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 16; i += 4) {
                         const uint32_t k0 = 16 * h + i;
-                        const float4 qv = (act && k0 < p.Dp) ? __ldg(reinterpret_cast<const float4*>(q + k0))
-                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 qv = qv4[i / 4];
                         const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
@@ -1553,6 +1575,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                             need |= (fmaf(-0.5f * kVmC1, wn[s], dot[s]) >= W) ? (1u << s) : 0u;
                         need &= nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
                         // pass 2 (the tile column still holds this lane's values)
+#if BIVF_TC_PROF
+                        atomicAdd(&prof_ev[0], (uint32_t)__popc(need));
+#endif
                         while (need) {
                             const uint32_t s = __ffs(need) - 1;
                             need &= need - 1;
@@ -1565,20 +1590,33 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                                 // offer h to the query's k-best set: replace its maximum (CAS,
                                 // retried when another lane got there first)
                                 const uint32_t u = f2ord(h);
+#if BIVF_TC_PROF
+                                atomicAdd(&prof_ev[1], 1u);
+#endif
                                 for (;;) {
+#if BIVF_TC_PROF
+                                    atomicAdd(&prof_ev[2], 1u);
+#endif
+                                    // all k slots loaded first (independent loads in flight together),
+                                    // then the maximum; values only ever decrease, so a stale read
+                                    // can only over-estimate the set's maximum (a valid threshold)
+                                    uint32_t kv[KT];
+#pragma unroll
+                                    for (int r = 0; r < KT; ++r)
+                                        kv[r] = (uint32_t)r < p.k ? *reinterpret_cast<volatile uint32_t*>(kb + r * kVmQ) : 0u;
                                     uint32_t mx = 0, mi = 0;
-                                    for (uint32_t r = 0; r < p.k; ++r) {
-                                        const uint32_t v = *reinterpret_cast<volatile uint32_t*>(kb + r * kVmQ);
-                                        if (v >= mx) {
-                                            mx = v;
-                                            mi = r;
+#pragma unroll
+                                    for (int r = 0; r < KT; ++r)
+                                        if (kv[r] >= mx) {
+                                            mx = kv[r];
+                                            mi = (uint32_t)r;
                                         }
-                                    }
                                     if (u >= mx) break;
                                     if (atomicCAS(kb + mi * kVmQ, mx, u) == mx) {
                                         uint32_t nm = u;
-                                        for (uint32_t r = 0; r < p.k; ++r)
-                                            nm = max(nm, *reinterpret_cast<volatile uint32_t*>(kb + r * kVmQ));
+#pragma unroll
+                                        for (int r = 0; r < KT; ++r)
+                                            if ((uint32_t)r != mi) nm = max(nm, kv[r]);
                                         if (nm < 0xffffffffu) {  // k values: a threshold for the query's runs
                                             atomicMin(qts, nm);
                                             atomicMin(reinterpret_cast<uint32_t*>(p.qthr) + qi, nm);
@@ -1589,7 +1627,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                                 th = qthr_dec(*reinterpret_cast<volatile uint32_t*>(qts));
                             }
                             if (l <= th && !overflow) {
+#if BIVF_TC_PROF
+                                atomicAdd(&prof_ev[3], 1u);
+#endif
                                 if (ncand == (uint32_t)kVmKC) {  // compact against the tighter threshold
+#if BIVF_TC_PROF
+                                    atomicAdd(&prof_ev[4], 1u);
+#endif
                                     uint32_t w = 0;
                                     for (uint32_t r = 0; r < (uint32_t)kVmKC; ++r) {
                                         const float li = clb[r * 32];
@@ -1620,12 +1664,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             pf.mark(7);
             // run output: the warpgroup's 4 lanes of a query -> one run (refine_kernel's
-            // format); warpgroup 0's run carries the k-best set, warpgroup 1's +inf
-            if (wl == 0) {
-                o_cnt[wg * kVmQ + n] = 0;
-                o_ovf[wg * kVmQ + n] = 0;
-            }
-            named_bar(1 + wg, 128);
+            // format); warpgroup 0's run carries the k-best set, warpgroup 1's +inf.
+            // (The gather counters were reset by build(seq + 1) above.)
             if (active) {
                 const uint32_t pair = d.pairs[n];
                 const uint64_t run = (((uint64_t)pair * p.maxch + d.chunk) << 1) | (uint32_t)wg;
@@ -1665,6 +1705,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         pf.report("vm-math", warp);
     }
     __syncthreads();
+#if BIVF_TC_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("[tc-prof] vm-events survivors %u offers %u cas %u appends %u compactions %u units %u\n", prof_ev[0],
+               prof_ev[1], prof_ev[2], prof_ev[3], prof_ev[4], 0u);
+#endif
     if (warp == 1) {
         __syncwarp();
         tc_fence_after();
@@ -2034,26 +2079,21 @@ __global__ void vm_seed_kernel(TcParams p, const long long* probes, uint32_t nq)
     float* qs = qsm + wq * p.Dp;
     for (uint32_t i = lane; i < p.D; i += 32) qs[i] = p.queries[(uint64_t)q * p.Dp + i];
     __syncwarp();
+    // the samples (maint.cuh: central offline vectors of every list, interleaved
+    // [list][d][slot]) of the query's two nearest probes; an entry deleted before
+    // this search's plan snapshot was invalidated before that deletion was
+    // published, so every entry read here is a vector the scan probes
     uint64_t v[2] = {~0ull, ~0ull};
-    uint32_t rows = 0, nvec = 0;
-    for (uint32_t r = 0; r < p.P && rows < 2; ++r) {
+    uint32_t nvec = 0;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        if ((uint32_t)r >= p.P) break;
         const uint32_t c = (uint32_t)probes[(uint64_t)q * p.P + r];
-        const uint32_t off = p.snap_off[c], len = p.snap_len[c];
-        const uint32_t ng = ivf_ngroups(p.L, off, len);
-        for (uint32_t j = 0; j < ng && rows < 2; ++j) {
-            TcItem d{};
-            d.off = off;
-            d.len = len;
-            const uint32_t nv = vm_nvalid(p, d, j);
-            if (lane < nv) {
-                const float dist = exact_l2_row(qs, cand_row(p, c, off, j, lane), p.D);
-                const uint64_t key = ((uint64_t)f2ord(dist) << 32) | (32u * rows + lane);
-                if (rows == 0) v[0] = key;
-                else v[1] = key;
-            }
-            nvec += nv;
-            ++rows;
-        }
+        const long long id = *reinterpret_cast<const volatile long long*>(p.samp_ids + (uint64_t)c * kSampS + lane);
+        const bool ok = id >= 0;
+        const float dist = exact_l2(qs, p.samp_rows + (uint64_t)c * p.D * kSampS + lane, p.D);
+        if (ok) v[r] = ((uint64_t)f2ord(dist) << 32) | (32u * r + lane);
+        nvec += __popc(__ballot_sync(0xffffffffu, ok));
     }
     if (nvec < p.k) return;  // qthr stays "none"
     warp_bitonic<2>(v, lane);
@@ -2722,7 +2762,7 @@ static cudaError_t launch_vm(const DevLists& L, const PlanBufs& B, const long lo
                              const float* off_nrm, const float* arena_nrm, const float* off_rows,
                              const float* arena_rows, const TcBufs& T, float* out_d, long long* out_i,
                              uint32_t* out_cnt, int num_sms, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
-                             int max_grid) {
+                             int max_grid, const float* samp_rows, const long long* samp_ids) {
     SearchShape s2 = sh;
     s2.QT = kVmQ;
     cudaError_t e = launch_plan(L, B, probes, s2, s);
@@ -2739,6 +2779,8 @@ static cudaError_t launch_vm(const DevLists& L, const PlanBufs& B, const long lo
     p.P = sh.P;
     p.maxch = sh.maxch;
     p.qt = kVmQ;
+    p.samp_rows = samp_rows;
+    p.samp_ids = samp_ids;
     p.centroids = centroids;
     p.queries = queries;
     p.snap_off = B.snap_off;
@@ -2765,11 +2807,11 @@ static cudaError_t launch_vm(const DevLists& L, const PlanBufs& B, const long lo
     if (e != cudaSuccess) return e;
     if (ev0) cudaEventRecord(ev0, s);
     const uint32_t wpb = 4;
-    static const bool seed = [] {
-        const char* v = std::getenv("BIVF_VM_SEED");  // 1: exact seeds first (measured: no gain at the north star)
-        return v && v[0] == '1';
+    static const bool seed_env = [] {
+        const char* v = std::getenv("BIVF_VM_SEED");  // 0: no seed thresholds (tuning aid)
+        return !(v && v[0] == '0');
     }();
-    if (seed) vm_seed_kernel<<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * p.Dp * 4, s>>>(p, probes, sh.nq);
+    if (seed_env && samp_ids) vm_seed_kernel<<<(sh.nq + wpb - 1) / wpb, wpb * 32, wpb * p.Dp * 4, s>>>(p, probes, sh.nq);
     int grid = std::max(1, std::min(num_sms, max_grid));
     if (const char* g = std::getenv("BIVF_TC_GRID")) grid = std::max(1, atoi(g));  // debugging aid
     VmMaps vmaps;
@@ -2803,7 +2845,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int max_grid,
-                                 const CUtensorMap* maps_hi) {
+                                 const CUtensorMap* maps_hi, const float* samp_rows, const long long* samp_ids) {
     if (sh.nq == 0) return cudaSuccess;
     const bool wide = sh.metric == kIP;  // 1xBF16 inner-product mode (mirror.cuh wide mirror)
     if (wide && dense) return cudaErrorInvalidValue;
@@ -2813,7 +2855,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     }();
     if (maps_hi && vm_env && !wide && !dense && L.D <= (uint32_t)kMaxD)
         return launch_vm(L, B, probes, queries, centroids, sh, maps_hi, off_nrm, arena_nrm, off_rows,
-                         arena_rows, T, out_d, out_i, out_cnt, num_sms, s, ev0, ev1, max_grid);
+                         arena_rows, T, out_d, out_i, out_cnt, num_sms, s, ev0, ev1, max_grid, samp_rows, samp_ids);
     SearchShape s2 = sh;
     s2.QT = kM;
     cudaError_t e = cudaSuccess;

@@ -68,6 +68,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0 = nullptr,
                                  cudaEvent_t ev1 = nullptr, int max_grid = 1 << 30,
-                                 const CUtensorMap* maps_hi = nullptr);
+                                 const CUtensorMap* maps_hi = nullptr, const float* samp_rows = nullptr,
+                                 const long long* samp_ids = nullptr);
 
 }  // namespace bivf

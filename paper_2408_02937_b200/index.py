@@ -339,6 +339,15 @@ class ClusterIndex:
     def save(self, path):
         check(lib().bivf_save_snapshot(self._h, str(path).encode()))
 
+    def seed_samples(self):
+        """The list scan's seed samples: [num_clusters, 32] ids (-1 = empty / deleted)."""
+        n = C.c_uint64(0)
+        check(lib().bivf_seed_samples(self._h, None, 0, C.byref(n)))
+        out = np.full(n.value, -1, np.int64)
+        if n.value:
+            check(lib().bivf_seed_samples(self._h, out.ctypes.data, n.value, C.byref(n)))
+        return out.reshape(-1, 32)
+
     def pool_alert(self):
         """(fired, blocks used at the allocation that first exceeded the watermark)."""
         f, u = C.c_int32(0), C.c_uint64(0)

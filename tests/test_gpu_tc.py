@@ -270,3 +270,48 @@ def test_graph_replay_sees_new_data(gpu_ready):
     ix.remove(new)
     r3 = ix.search_batch(q, 5, 8)
     assert np.array_equal(r3[0], r1[0]) and np.array_equal(bits(r3[1]), bits(r1[1]))
+
+
+def test_vm_seed_samples_follow_deletes(gpu_ready):
+    """The list scan seeds each query's threshold with exact distances to its
+    nearest lists' central offline vectors.  Deleting sampled
+    vectors must drop them from the samples before the deletion is visible, so
+    searches stay exact (== the CUDA-core exact scan and the oracle)."""
+    D, C, T, n = 64, 16, 64, 6000
+    base = bivf.synthetic_dataset(n, D, 24, 3)
+    cent, asg, _ = bivf.kmeans(base, C, 5, 3)
+    ix = ClusterIndex.empty(D, C, block_capacity=T, num_blocks=4 * n // T + 4 * C)
+    ix.set_centroids(cent)
+    ix.bulk_load(base, asg)
+    orc = O.OracleIndex(cent, base, asg, T, 4 * n // T + 4 * C)
+    samp = ix.seed_samples()
+    assert samp.shape == (C, 32)
+    # every sample is a member of its list
+    for c in range(C):
+        ids, _ = ix.cluster_contents(c)
+        s = samp[c][samp[c] >= 0]
+        assert len(s) == min(32, len(ids)) and set(s) <= set(ids)
+    q = bivf.synthetic_dataset(400, D, 24, 5)
+    for stage in range(3):
+        if stage == 1:  # half of every list's samples
+            gone = samp[:, ::2].reshape(-1)
+        elif stage == 2:  # all of them, then fresh inserts
+            gone = samp.reshape(-1)
+        else:
+            gone = np.zeros(0, np.int64)
+        gone = gone[gone >= 0]
+        if len(gone):
+            r1, _ = ix.remove(gone)
+            r2, _ = orc.remove(gone)
+            assert r1 == r2
+            left = ix.seed_samples()
+            assert not np.isin(left[left >= 0], gone).any()
+        if stage == 2:
+            x = bivf.synthetic_dataset(500, D, 24, 9)
+            assert np.array_equal(ix.insert(x), orc.insert(x)[0])
+        for k, npb in ((10, 4), (32, 8), (10, C)):
+            a, b = both(ix, q, k, npb)
+            assert_same(a, b)
+            for j in range(0, 400, 53):
+                oi, od = orc.search(q[j], k, npb)
+                assert np.array_equal(b[0][j, : b[2][j]], oi) and np.array_equal(bits(b[1][j, : b[2][j]]), bits(od))
