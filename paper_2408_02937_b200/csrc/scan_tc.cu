@@ -1129,6 +1129,9 @@ constexpr int kVmNS = 3;       // A stage slots (one unit of 4 groups each)
 #ifndef BIVF_VM_PF
 #define BIVF_VM_PF 0
 #endif
+#ifndef BIVF_VM_SEED_LISTS
+#define BIVF_VM_SEED_LISTS 1  // nearest lists whose samples seed a query's threshold (power of 2; 1 measured fastest: 2 -> 1.03 ms, 4 -> 1.04, 8 -> 1.09 vs 1.00)
+#endif
 constexpr int kVmPF = BIVF_VM_PF;  // units prefetched into L2 ahead of the shared-memory ring
 constexpr int kVmNR = 8;       // norm ring slots (a unit's 4 x 32 |s|^2)
 constexpr int kVmNB = 4;       // TMEM accumulators (32 columns each)
@@ -2083,21 +2086,23 @@ __global__ void vm_seed_kernel(TcParams p, const long long* probes, uint32_t nq)
     // [list][d][slot]) of the query's two nearest probes; an entry deleted before
     // this search's plan snapshot was invalidated before that deletion was
     // published, so every entry read here is a vector the scan probes
-    uint64_t v[2] = {~0ull, ~0ull};
+    uint64_t v[BIVF_VM_SEED_LISTS];
+#pragma unroll
+    for (int r = 0; r < BIVF_VM_SEED_LISTS; ++r) v[r] = ~0ull;
     uint32_t nvec = 0;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < BIVF_VM_SEED_LISTS; ++r) {
         if ((uint32_t)r >= p.P) break;
         const uint32_t c = (uint32_t)probes[(uint64_t)q * p.P + r];
         const long long id = *reinterpret_cast<const volatile long long*>(p.samp_ids + (uint64_t)c * kSampS + lane);
         const bool ok = id >= 0;
         const float dist = exact_l2(qs, p.samp_rows + (uint64_t)c * p.D * kSampS + lane, p.D);
-        if (ok) v[r] = ((uint64_t)f2ord(dist) << 32) | (32u * r + lane);
+        if (ok) v[r] = ((uint64_t)f2ord(dist) << 32) | (32u * r + lane);  // (r static: unrolled)
         nvec += __popc(__ballot_sync(0xffffffffu, ok));
     }
     if (nvec < p.k) return;  // qthr stays "none"
-    warp_bitonic<2>(v, lane);
-    const uint64_t kth = warp_elem<2>(v, p.k - 1);
+    warp_bitonic<BIVF_VM_SEED_LISTS>(v, lane);
+    const uint64_t kth = warp_elem<BIVF_VM_SEED_LISTS>(v, p.k - 1);
     if (lane == 0) p.qthr[q] = __uint_as_float((uint32_t)(kth >> 32));
 }
 // Fast selection of dense_select_kernel (R pre-threshold keys per lane, lists of
