@@ -56,12 +56,12 @@ public:
 
     std::vector<blockivf::vector_id> insert(std::span<const float> vectors, std::size_t n,
                                             std::span<const blockivf::vector_id> ids = {}) override {
+        std::vector<blockivf::vector_id> out(n, -1);
+        if (n == 0) return out;  // before the extent checks, as ivf_index.cpp:124-129
         if (vectors.size() != n * dim())
             throw std::invalid_argument("insert: vectors extent does not match n * dim");
         if (!ids.empty() && ids.size() != n)
             throw std::invalid_argument("insert: ids size does not match n");
-        std::vector<blockivf::vector_id> out(n, -1);
-        if (n == 0) return out;
         uint64_t inserted = 0;
         const bivf_status s = bivf_add(h_, vectors.data(), n, ids.empty() ? nullptr : ids.data(),
                                        out.data(), &inserted);
