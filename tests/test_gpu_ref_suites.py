@@ -1,6 +1,7 @@
 """The reference's OWN test suites against the B200 index.
 
-proj/tests/test_ivf_index.cpp, test_rearrange.cpp and test_concurrency.cpp —
+proj/tests/test_ivf_index.cpp, test_rearrange.cpp, test_concurrency.cpp and
+test_executor.cpp (the reference Executor driving the GPU index) —
 unmodified — compiled by oracle/Makefile (`make -C oracle ref`) with
 oracle/gpu_suite_shim.hpp force-included: `ClusterIndex` becomes a class over
 the C-ABI (libbivf_gpu.so), so every search, insert, assign, rearrangement,
@@ -16,7 +17,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SUITES = ["ivf_index", "rearrange", "concurrency"]
+SUITES = ["ivf_index", "rearrange", "concurrency", "executor"]
 
 
 @pytest.mark.parametrize("suite", SUITES)
