@@ -478,6 +478,10 @@ void GpuIndex::build_quantizer_mirror(const float* c) {
                                    dg.as<uint64_t>(), dc.as<uint32_t>(), ngq, data_stream_));
     BIVF_CUDA(cudaStreamSynchronize(data_stream_));
     q_tc_ok_ = make_mirror_map(d_q_mir_.as<float>(), ngq, D_, wide, &map_q_) == cudaSuccess;
+    // the vector-major scan's maps over the same mirror (L2 quantizer through scan_vm_kernel)
+    q_vm_ok_ = !wide && D_ <= 128 && make_vm_maps(d_q_mir_.as<float>(), d_q_nrm_.as<float>(), ngq, D_, &q_vm_maps_[0]) ==
+                                         cudaSuccess;
+    for (int i = 0; i < 3; ++i) q_vm_maps_[3 + i] = q_vm_maps_[i];  // no arena part
 }
 
 bool GpuIndex::use_tc_quantizer(uint32_t P) const {
@@ -523,6 +527,34 @@ void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32
         const char* v = std::getenv("BIVF_TCQ_MIN");
         return v ? (uint32_t)atoi(v) : 0u;
     }();
+    static const bool vm_quant = [] {  // 1: the L2 quantizer through scan_vm_kernel (measured slower at the
+        const char* v = std::getenv("BIVF_VM_QUANT");  // north star: 0.37 vs 0.22 ms per 10K; kept for comparison)
+        return v && v[0] == '1';
+    }();
+    if (vm_quant && q_vm_ok_ && use_tc_quantizer(P) && P <= 32 && nq <= 65536 && nq >= tcq_min) {
+        // L2, nprobe <= 32: the centroid set as one list through the vector-major scan
+        // (tcgen05 filter over the centroid mirror's bf16 hi plane, exact top-nprobe by
+        // the refine over the row-major centroids: the reference's distance bits)
+        const uint32_t qsl = quantizer_slice();
+        for (uint32_t q0 = 0; q0 < nq; q0 += qsl) {
+            const uint32_t m = std::min(qsl, nq - q0);
+            SearchShape qs;
+            qs.nq = m;
+            qs.k = P;
+            qs.P = 1;
+            qs.maxch = quantizer_maxch(m);  // carve reserved nq x quantizer_maxch(nq) x 2 runs
+            qs.gcmin = 4;
+            qs.QT = 32;
+            qs.metric = cfg_.metric;
+            const size_t g0 = (size_t)qbase + q0;
+            BIVF_CUDA(launch_ivf_search_tc(quantizer_lists(), w.plan, d_q_zero_.as<long long>(),
+                                           w.queries + g0 * Dp_, d_q_mu_.as<float>(), qs, map_q_, map_q_,
+                                           d_q_nrm_.as<float>(), nullptr, d_cent_.as<float>(), nullptr, w.tc,
+                                           nullptr, w.pdist + g0 * P, w.probes + g0 * P, nullptr, num_sms_, s,
+                                           nullptr, nullptr, 1 << 30, q_vm_maps_));
+        }
+        return;
+    }
     if (use_tc_quantizer(P) && nq <= 65536 && nq >= tcq_min) {
         // dense mode: approximate distances of every (query, centroid) on the
         // tensor cores, then a per-query selection + exact recompute of the few

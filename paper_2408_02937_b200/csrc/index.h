@@ -379,6 +379,8 @@ private:
 
     CUtensorMap map_off_{}, map_arena_{};
     CUtensorMap maps_h_[6]{};  // scan_vm_kernel's maps (make_vm_maps): offline [0, 3), arena [3, 6)
+    CUtensorMap q_vm_maps_[6]{};       // scan_vm_kernel's maps over the quantizer mirror (L2)
+    bool q_vm_ok_ = false;
     DevBuf d_samp_rows_, d_samp_ids_;  // seed samples (maint.cuh kSampS per list), built by bulk_load
     bool samp_on_ = false;
 
