@@ -368,7 +368,31 @@ def run_ours(args, dist):
     t = time.perf_counter()
     for _ in range(args.steps):
         e2e_call()
-    e2e_s = max_over_ranks(dist, time.perf_counter() - t)
+    e2e_serial_s = max_over_ranks(dist, time.perf_counter() - t)
+    # the same K calls from E2E_CALLERS client threads (the index is thread-safe:
+    # each call leases its own stream + workspace, so one call's host<->device
+    # copies overlap another's kernels -- the multi-stream serving model,
+    # PAPER.md:207-237).  Every call still copies its 10K queries in and its
+    # results out; only the sharded group (one collective channel) stays serial.
+    callers = E2E_CALLERS if grp is None else 1
+    e2e_s = e2e_serial_s
+    if callers > 1:
+        outs = [h_out] + [(bivf.pinned_empty((len(hq), K), np.int64), bivf.pinned_empty((len(hq), K), np.float32),
+                           bivf.pinned_empty((len(hq),), np.uint32)) for _ in range(callers - 1)]
+        for o in outs[1:]:  # this caller's lease warm (staging, graphs)
+            ix.search_batch(hq, K, NPROBE, out=o)
+
+        def caller(j):
+            for _ in range(j, args.steps, callers):
+                ix.search_batch(hq, K, NPROBE, out=outs[j])
+
+        ths = [threading.Thread(target=caller, args=(j,)) for j in range(callers)]
+        t = time.perf_counter()
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        e2e_s = time.perf_counter() - t
     ins_stats = ins.finish()
     del_stats = {"items": int(dstate["deleted"]), "rate_per_s": round(
         dstate["deleted"] / max(1e-9, ins.t1 - ins.t0), 1)}
@@ -431,7 +455,10 @@ def run_ours(args, dist):
             "rearrange_events": rr_events,
             "e2e": {"value": round(B * args.steps / e2e_s, 1), "unit": "queries/s",
                     "h2d_bytes_per_step": int(B * DIM * 4),
-                    "d2h_bytes_per_step": int(B * K * 12 + B * 4)},
+                    "d2h_bytes_per_step": int(B * K * 12 + B * 4),
+                    "callers": callers, "serial_value": round(B * args.steps / e2e_serial_s, 1),
+                    "note": "bivf_search (pinned host queries in, host results out) per step; value: "
+                            f"{callers} client thread(s) sharing the K steps, serial_value: one caller"},
             "roofline": roofline(probes, sizes, ph, peaks),
             "gpu_launches": int(launches),
             "clocks": clk,
@@ -504,6 +531,7 @@ def roofline(probes, sizes, ph, peaks):
                          "scan": round(ph[2], 3), "refine": round(ph[3], 3)}}
 
 
+E2E_CALLERS = 2       # client threads of the e2e leg (bivf_search is thread-safe)
 LAT_QPS = 1000.0      # search requests / s (x 10 queries each)
 
 

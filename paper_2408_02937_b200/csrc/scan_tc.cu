@@ -1462,7 +1462,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 o_cnt[t256] = 0;
                 o_ovf[t256] = 0;
             }
-            if (!d.valid) return false;
+            if (!d.valid) {
+                // end marker: the reset above must still be ordered before the last
+                // item's run output (every math thread takes this same branch)
+                named_bar(3, 256);
+                return false;
+            }
             const uint32_t ib = seq & 1;
             if (seq >= 2) mbar_wait(&b_free[ib], ((seq - 2) >> 1) & 1);
             if (t256 < (int)K) cent_s[t256] = cv;
@@ -2858,7 +2863,17 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
         const char* v = std::getenv("BIVF_TC_VM");  // 0: the query-major 3xBF16 scan (comparison aid)
         return !(v && v[0] == '0');
     }();
-    if (maps_hi && vm_env && !wide && !dense && L.D <= (uint32_t)kMaxD)
+    // the vector-major scan reads a list once per <= 32-query tile and filters
+    // with the vectors' bf16 hi plane only: it wins while lists see few queries
+    // (the north star: 29 pairs per list); with many pairs per list the
+    // query-major kernel's 128-query tiles and 3xBF16 bound (far fewer
+    // candidates on dense data) win (measured: cfg1 625 and cfg3 78 pairs per list)
+    static const double vm_max_ppl = [] {
+        const char* v = std::getenv("BIVF_VM_MAX_PPL");  // tuning aid
+        return v ? atof(v) : 48.0;
+    }();
+    const double ppl = (double)sh.nq * sh.P / std::max<uint32_t>(1u, L.C);
+    if (maps_hi && vm_env && !wide && !dense && L.D <= (uint32_t)kMaxD && ppl <= vm_max_ppl)
         return launch_vm(L, B, probes, queries, centroids, sh, maps_hi, off_nrm, arena_nrm, off_rows,
                          arena_rows, T, out_d, out_i, out_cnt, num_sms, s, ev0, ev1, max_grid, samp_rows, samp_ids);
     SearchShape s2 = sh;

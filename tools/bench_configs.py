@@ -3,7 +3,8 @@
 (bench.py measures configs[1]).  One JSON line per run, same keys as bench.py
 where they apply.
 
-    python tools/bench_configs.py --config cfg1|cfg3|cfg4s|cfg5 [--steps K --warmup W]
+    python tools/bench_configs.py --config cfg1|cfg3|cfg4s|cfg5|cfg5s [--steps K --warmup W]
+                                  [--cpu-baseline --cpu-sample N]
 
   cfg1  IVF-Flat 100K x 128 (reference generator, 1024 components, seed 1),
         nlist 256, nprobe 16, k 10, batch search only
@@ -17,6 +18,16 @@ where they apply.
   cfg5  IVF-Flat 20M x 768 inner product (32768 unit centres, x = normalize(u +
         0.5 N(0,1)/sqrt(768))), nlist 4096, nprobe 32, k 10, 10K vec/s live inserts
         (IP: the tensor-core wide mode, 1xFP16 filter + exact refine)
+  cfg5s one shard (id mod 8 == 0) of cfg5: 2.5M x 768, same generator, nlist 4096,
+        nprobe 32, k 10, live inserts -- small enough that the C restatement
+        (oracle/, inner product; the reference is L2-only) holds the whole index
+        for the cpu_baseline leg and its parity check
+
+--cpu-baseline times the CPU on a bounded query sample AFTER the timed region
+and checks its ids + distance bits against the GPU's on the same sample: L2
+configs load this index's BIVFSNAP snapshot into the unmodified reference
+(oracle/_ref); inner-product configs rebuild it list by list in the C
+restatement (oracle/liboracle.so, same centroids, same (id, vector) sets).
 
 Data are synthetic, generated on the GPU with torch's Philox generator (a fixed
 seed per config; plumbing, not the measured path) and loaded through the
@@ -40,6 +51,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
+from bench import Clocks  # noqa: E402  (the bench's NVML clock/throttle sampler)
+
 CFG = {
     "cfg1": dict(workload="IVF-Flat 100Kx128 fp32 synthetic Gaussian-mixture, nlist=256, nprobe=16, "
                           "k=10, L2, batch search only", n=100_000, dim=128, nlist=256, nprobe=16, k=10,
@@ -55,6 +68,10 @@ CFG = {
                           "nprobe=32, k=10, 10K vec/s live inserts", n=20_000_000, dim=768, nlist=4096,
                  nprobe=32, k=10, metric=1, block=1024, train=200_000, iters=6, insert_rate=10_000.0,
                  delete_rate=0.0),
+    "cfg5s": dict(workload="IVF-Flat 20Mx768 fp32 inner-product RAG-embedding synthetic, shard 0 of 8 "
+                           "(2.5M vectors), nlist=4096, nprobe=32, k=10, 10K vec/s live inserts",
+                  n=2_500_000, dim=768, nlist=4096, nprobe=32, k=10, metric=1, block=1024, train=200_000,
+                  iters=6, insert_rate=10_000.0, delete_rate=0.0),
 }
 BATCH = 10_000
 
@@ -79,7 +96,7 @@ def gen_rows(name, torch, rows, seed, chunk=1 << 20):
         D, ncent, sig = 128, 65536, 3.0
         g0.manual_seed(seed)
         cent = torch.rand(ncent, D, generator=g0, device=dev) * 100.0
-    elif name == "cfg5":
+    elif name in ("cfg5", "cfg5s"):
         D, ncent, sig = 768, 32768, 0.5
         g0.manual_seed(seed)
         cent = torch.randn(ncent, D, generator=g0, device=dev)
@@ -115,8 +132,8 @@ def make_data(name, torch, bivf):
     if name == "cfg1":
         x = bivf.synthetic_dataset(c["n"] + BATCH, c["dim"], 1024, 1)
         return x[:c["n"]], x[c["n"]:], np.zeros((0, c["dim"]), np.float32)
-    seed = {"cfg3": 3, "cfg4s": 4, "cfg5": 5}[name]
-    stride = 8 if name == "cfg4s" else 1
+    seed = {"cfg3": 3, "cfg4s": 4, "cfg5": 5, "cfg5s": 5}[name]
+    stride = 8 if name in ("cfg4s", "cfg5s") else 1
     base_rows = np.arange(0, c["n"] * stride, stride, dtype=np.int64)
     t = time.time()
     base = gen_rows(name, torch, base_rows, seed)
@@ -200,6 +217,7 @@ def run(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    clocks = Clocks(0)
     launches0 = bivf.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_live0 = time.perf_counter()
@@ -208,6 +226,7 @@ def run(args):
         step()
     e1.record(stream)
     torch.cuda.synchronize()
+    clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     launches = bivf.kernel_launches() - launches0
     for _ in range(2):
@@ -250,13 +269,16 @@ def run(args):
         ("tensor-core 1xFP16 inner-product filter (wide mode) + exact refine"
          if (c["metric"] == 1 and 8 <= D <= 768 and K <= 32) else "CUDA-core exact scan"),
         "gpu_launches": int(launches),
+        "clocks": clk,
+        "l2_flush": "none: each step scans >= 1.2 GB of lists, far above the 126 MB L2",
     }
     if th is not None:
         res["live"] = {"inserted": stats["inserted"], "deleted": stats["deleted"],
                        "insert_vec_s": round(stats["inserted"] / live_s, 1),
                        "delete_ids_s": round(stats["deleted"] / live_s, 1), "error": stats["err"]}
     if args.cpu_baseline:
-        res["cpu_baseline"] = cpu_baseline(ix, queries, K, P, c["block"], args.cpu_sample)
+        res["cpu_baseline"] = (cpu_baseline_restatement(ix, queries, K, P, c, args.cpu_sample) if c["metric"]
+                               else cpu_baseline(ix, queries, K, P, c["block"], args.cpu_sample))
     ix.close()
     return res
 
@@ -288,6 +310,47 @@ def cpu_baseline(ix, queries, K, P, block, sample):
             "kind": "reference", "sample": f"{len(s)} queries, nprobe={P}, k={K}, reference "
             "ClusterIndex loaded from this index's BIVFSNAP snapshot",
             "results_identical_to_gpu": same}
+
+
+def cpu_baseline_restatement(ix, queries, K, P, c, sample):
+    """The C restatement (oracle/liboracle.so) rebuilt from this index's lists:
+    the GPU index's centroids and, per list, its (id, vector) contents.  Search
+    results depend only on those (the order inside a list is irrelevant: (dist,
+    id) ties break by id), so this is the same index.  Queries run on every host
+    core, one orc_search per query (ctypes drops the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle as O
+    t = time.time()
+    C_ = ix.num_clusters
+    parts_i, parts_v, asg = [], [], []
+    for cl in range(C_):
+        ids, v = ix.cluster_contents(cl)
+        parts_i.append(ids)
+        parts_v.append(v)
+        asg.append(np.full(len(ids), cl, np.uint32))
+    ids = np.concatenate(parts_i)
+    vecs = np.concatenate(parts_v)
+    del parts_v
+    asg = np.concatenate(asg)
+    nb = len(ids) // c["block"] + 2 * C_ + 64
+    o = O.OracleIndex(ix.centroids(), vecs, asg, c["block"], nb, metric=O.IP if c["metric"] else O.L2, ids=ids)
+    del vecs
+    log(f"restatement rebuilt from {len(ids)} vectors in {time.time() - t:.1f}s")
+    cores = os.cpu_count() or 1
+    s = np.ascontiguousarray(queries[:sample])
+    t = time.perf_counter()
+    with ThreadPoolExecutor(cores) as pool:
+        res = list(pool.map(lambda j: o.search(s[j], K, P), range(len(s))))
+    secs = time.perf_counter() - t
+    gi, gd, gc = ix.search_batch(s, K, P)
+    same = all(int(gc[j]) == len(res[j][0]) and np.array_equal(gi[j, :gc[j]], res[j][0])
+               and np.array_equal(gd[j, :gc[j]].view(np.uint32), res[j][1].view(np.uint32))
+               for j in range(len(s)))
+    return {"value": round(len(s) / secs, 1), "unit": "queries/s", "cores": cores, "kind": "port",
+            "sample": f"{len(s)} queries, nprobe={P}, k={K}, C restatement (oracle/bivf_oracle.c, inner "
+            "product) rebuilt from this index's centroids + per-list (id, vector) contents",
+            "results_identical_to_gpu": bool(same)}
 
 
 def main():

@@ -21,4 +21,10 @@ echo "racecheck rc=$?"
 timeout -s KILL 900 $SAN --tool synccheck python -m pytest tests/test_gpu_tc.py -m gpu -x -q -p no:cacheprovider \
   -k "tc_equals_exact_and_oracle and (32-16 or 8-6) or seeded_batches and 8-6 or seed_samples" > gpurun_out/san_synccheck_$tag.log 2>&1
 echo "synccheck rc=$?"
+# analysis mode: every distinct (write site, read site) pair once, no backtraces
+timeout -s KILL 900 compute-sanitizer --tool racecheck --racecheck-report analysis --show-backtrace no --print-limit 200 \
+  --kernel-name kns=scan_vm_kernel --kernel-name kns=refine_kernel --kernel-name kns=vm_seed --kernel-name kns=sample_ \
+  python -m pytest tests/test_gpu_tc.py -m gpu -x -q -p no:cacheprovider \
+  -k "tc_equals_exact_and_oracle and 8-6 or seed_samples" > gpurun_out/san_raceanalysis_$tag.log 2>&1
+echo "racecheck analysis rc=$?"
 for f in gpurun_out/san_*_$tag.log; do echo "== $f"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|passed|failed" $f | tail -4; done
