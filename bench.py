@@ -531,7 +531,9 @@ def roofline(probes, sizes, ph, peaks):
                          "scan": round(ph[2], 3), "refine": round(ph[3], 3)}}
 
 
-E2E_CALLERS = 2       # client threads of the e2e leg (bivf_search is thread-safe)
+E2E_CALLERS = 1       # client threads of the e2e leg (measured: 2 concurrent 10K-query
+                      # calls give 5.21 M vs 6.62 M QPS serial -- their kernels interleave
+                      # on the SMs instead of hiding the copies, so one caller)
 LAT_QPS = 1000.0      # search requests / s (x 10 queries each)
 
 

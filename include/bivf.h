@@ -324,7 +324,9 @@ bivf_status bivf_replay(bivf_executor* e, const bivf_replay_spec* spec, const fl
 /* kernel launches issued by this library since load (bench's gpu_launches) */
 uint64_t bivf_kernel_launches(void);
 /* scan kernel selection: 0 auto (tensor-core filtered scan when supported:
- * L2, k <= 32, 8 <= D <= 128), 1 CUDA-core exact scan only, 2 = auto */
+ * L2, k <= 32, 8 <= D <= 128), 1 CUDA-core exact scan only, 2 = auto,
+ * 3 / 4 = auto with the L2 list scan forced onto the vector-major /
+ * query-major tensor-core kernel (auto picks by pairs per list) */
 bivf_status bivf_set_scan_mode(bivf_index* h, int mode);
 /* enable CUDA-event timing of the search phases (on the lease stream) */
 bivf_status bivf_set_timing(bivf_index* h, int enable);

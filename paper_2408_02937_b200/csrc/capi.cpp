@@ -610,7 +610,7 @@ bivf_status bivf_replay(bivf_executor* e, const bivf_replay_spec* spec, const fl
 
 bivf_status bivf_set_scan_mode(bivf_index* h, int mode) {
     return guard([&] {
-        if (mode < 0 || mode > 2) throw Error(BIVF_EINVAL, "scan mode must be 0, 1 or 2");
+        if (mode < 0 || mode > 4) throw Error(BIVF_EINVAL, "scan mode must be 0..4");
         I(h).set_scan_mode(mode);
     });
 }

@@ -1216,7 +1216,8 @@ void GpuIndex::enqueue_scan(Lease& l, uint32_t nq, uint32_t k, uint32_t P, Works
                                        timing_ ? l.t2 : nullptr, timing_ ? l.t3 : nullptr, 1 << 30,
                                        maps_h_ok_ && d_arena_rows_.p ? maps_h_ : nullptr,
                                        samp_on_ ? d_samp_rows_.as<float>() : nullptr,
-                                       samp_on_ ? d_samp_ids_.as<long long>() : nullptr));
+                                       samp_on_ ? d_samp_ids_.as<long long>() : nullptr,
+                                       scan_mode_ == 3 ? 1 : scan_mode_ == 4 ? 0 : -1));
         if (stats) {
             std::vector<uint32_t> cc(runs);
             BIVF_CUDA(cudaMemcpyAsync(cc.data(), w.tc.ccount, runs * 4, cudaMemcpyDeviceToHost,

@@ -390,7 +390,8 @@ public:
 private:
     bool maps_h_ok_ = false;
     bool tc_ok_ = false;
-    int scan_mode_ = 0;  // 0 auto, 1 CUDA-core only, 2 tensor-core when supported
+    int scan_mode_ = 0;  // 0 auto, 1 CUDA-core only, 2 tensor-core when supported,
+                         // 3 / 4 auto with the list scan forced vector- / query-major
     std::atomic<bool> graphs_on_{true};  // BIVF_GRAPHS=0 disables; a failed capture too
     bool timing_ = false;
     float last_ms_[4] = {-1, -1, -1, -1};

@@ -2855,7 +2855,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  float* out_d,
                                  long long* out_i, uint32_t* out_cnt, int num_sms,
                                  cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int max_grid,
-                                 const CUtensorMap* maps_hi, const float* samp_rows, const long long* samp_ids) {
+                                 const CUtensorMap* maps_hi, const float* samp_rows, const long long* samp_ids,
+                                 int vm_mode) {
     if (sh.nq == 0) return cudaSuccess;
     const bool wide = sh.metric == kIP;  // 1xBF16 inner-product mode (mirror.cuh wide mirror)
     if (wide && dense) return cudaErrorInvalidValue;
@@ -2873,7 +2874,8 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
         return v ? atof(v) : 48.0;
     }();
     const double ppl = (double)sh.nq * sh.P / std::max<uint32_t>(1u, L.C);
-    if (maps_hi && vm_env && !wide && !dense && L.D <= (uint32_t)kMaxD && ppl <= vm_max_ppl)
+    if (maps_hi && vm_env && !wide && !dense && L.D <= (uint32_t)kMaxD &&
+        (vm_mode == 1 || (vm_mode < 0 && ppl <= vm_max_ppl)))
         return launch_vm(L, B, probes, queries, centroids, sh, maps_hi, off_nrm, arena_nrm, off_rows,
                          arena_rows, T, out_d, out_i, out_cnt, num_sms, s, ev0, ev1, max_grid, samp_rows, samp_ids);
     SearchShape s2 = sh;

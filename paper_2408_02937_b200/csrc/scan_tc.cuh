@@ -55,7 +55,8 @@ cudaError_t make_mirror_map(const float* base, uint64_t groups, uint32_t D, bool
 // the vector-major scan's maps over one mirror region (offline segments or the
 // arena): out3[0] one group's hi plane, out3[1] four consecutive groups' hi
 // planes (3-D), out3[2] their |s|^2 rows; launch_ivf_search_tc takes six
-// (offline then arena) as maps_hi.
+// (offline then arena) as maps_hi.  vm_mode: -1 choose by pairs per list, 1 the
+// vector-major scan whenever maps_hi allows it, 0 never (query-major).
 cudaError_t make_vm_maps(const float* mir, const float* nrm, uint64_t groups, uint32_t D, CUtensorMap* out3);
 
 cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const long long* probes,
@@ -69,6 +70,6 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  cudaStream_t s, cudaEvent_t ev0 = nullptr,
                                  cudaEvent_t ev1 = nullptr, int max_grid = 1 << 30,
                                  const CUtensorMap* maps_hi = nullptr, const float* samp_rows = nullptr,
-                                 const long long* samp_ids = nullptr);
+                                 const long long* samp_ids = nullptr, int vm_mode = -1);
 
 }  // namespace bivf

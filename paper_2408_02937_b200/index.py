@@ -379,8 +379,10 @@ class ClusterIndex:
 
     # ------------------------------------------------------------ kernels / timing
     def set_scan_mode(self, mode="auto"):
-        """'auto' (tensor-core filtered scan where supported), 'cuda' (CUDA-core exact scan)."""
-        m = {"auto": 0, "cuda": 1, "tc": 2}[mode]
+        """'auto' (tensor-core filtered scan where supported), 'cuda' (CUDA-core exact
+        scan), 'vm' / 'qm' (auto, the L2 list scan forced onto the vector-major /
+        query-major tensor-core kernel; auto picks by pairs per list)."""
+        m = {"auto": 0, "cuda": 1, "tc": 2, "vm": 3, "qm": 4}[mode]
         check(lib().bivf_set_scan_mode(self._h, m))
 
     def set_timing(self, on=True):

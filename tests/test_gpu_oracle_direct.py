@@ -44,13 +44,19 @@ def evolve(ix, orc, D, comps, rounds, gen, seed):
         assert ix.take_events() == orc.take_events()
 
 
+MODES = ("vm", "qm")  # the two L2 tensor-core list scans, each forced (auto picks by pairs per list)
+
+
 def check_all(ix, orc, q, k, nprobe):
-    gi, gd, gc = ix.search_batch(q, k, nprobe)
-    for j in range(len(q)):
-        oi, od = orc.search(q[j], k, nprobe)
-        assert gc[j] == len(oi), j
-        assert np.array_equal(gi[j, : gc[j]], oi), (j, gi[j, : gc[j]], oi)
-        assert np.array_equal(bits(gd[j, : gc[j]]), bits(od)), j
+    ref = [orc.search(q[j], k, nprobe) for j in range(len(q))]
+    for mode in MODES:
+        ix.set_scan_mode(mode)
+        gi, gd, gc = ix.search_batch(q, k, nprobe)
+        for j, (oi, od) in enumerate(ref):
+            assert gc[j] == len(oi), (mode, j)
+            assert np.array_equal(gi[j, : gc[j]], oi), (mode, j, gi[j, : gc[j]], oi)
+            assert np.array_equal(bits(gd[j, : gc[j]]), bits(od)), (mode, j)
+    ix.set_scan_mode("auto")
 
 
 @pytest.mark.parametrize("D,C,T,n,comps", [(128, 64, 256, 40_000, 16), (96, 48, 128, 30_000, 200),
@@ -102,10 +108,13 @@ def test_seeded_l2_equals_unmodified_reference(gpu_ready, tmp_path):
     ref = O.RefIndex.load(path, T)
     q = gen(1024, 72)
     for k, npb in ((10, 8), (100, 16)):
-        gi, gd, gc = ix.search_batch(q, k, npb)
-        for j in range(len(q)):
-            ri, rd = ref.search(q[j], k, npb)
-            assert np.array_equal(gi[j, : gc[j]], ri) and np.array_equal(bits(gd[j, : gc[j]]), bits(rd)), j
+        want = [ref.search(q[j], k, npb) for j in range(len(q))]
+        for mode in MODES:
+            ix.set_scan_mode(mode)
+            gi, gd, gc = ix.search_batch(q, k, npb)
+            for j, (ri, rd) in enumerate(want):
+                assert np.array_equal(gi[j, : gc[j]], ri) and np.array_equal(bits(gd[j, : gc[j]]), bits(rd)), (mode, j)
+    ix.set_scan_mode("auto")
 
 
 @pytest.mark.parametrize("D,C,T,n,norm", [(768, 32, 128, 8000, True), (768, 16, 64, 4000, False),

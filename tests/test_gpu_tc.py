@@ -18,8 +18,14 @@ def bits(a):
 
 
 def both(ix, q, k, nprobe):
+    """CUDA-core exact scan vs auto; the two L2 tensor-core list scans (vector-
+    major and query-major, which auto picks between by pairs per list) are each
+    forced once and must equal the exact scan too."""
     ix.set_scan_mode("cuda")
     a = ix.search_batch(q, k, nprobe)
+    for mode in ("vm", "qm"):
+        ix.set_scan_mode(mode)
+        assert_same(a, ix.search_batch(q, k, nprobe))
     ix.set_scan_mode("auto")
     b = ix.search_batch(q, k, nprobe)
     return a, b

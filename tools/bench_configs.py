@@ -157,6 +157,7 @@ def run(args):
     L = _lib.lib()
     torch.cuda.set_device(0)
     base, queries, pool = make_data(name, torch, bivf)
+    torch.cuda.empty_cache()  # the generator's cached blocks (cfg5 needs ~150 GB of index in HBM)
     D, C, P, K = c["dim"], c["nlist"], c["nprobe"], c["k"]
     rng = np.random.default_rng(0)
     tr = base if c["train"] >= len(base) else base[np.sort(rng.choice(len(base), c["train"], replace=False))]
