@@ -543,6 +543,7 @@ def latency_phase(ix, queries, inserts, dels, seconds, repeats):
     the executor's batcher + rearrangement sweeps, 1K deletes/s), windows
     alternated `repeats` times so box drift hits both sides alike."""
     from paper_2408_02937_b200.executor import Executor, replay, summarize_latencies
+    ix.prewarm(10, K, NPROBE)  # serving start-up: every lease set up for the request shape
     ex = Executor(ix, num_lanes=32)
     common = dict(k=K, nprobe=NPROBE, search_batch=10, insert_batch=INSERT_BATCH, poisson=True)
     # untimed warm-up: every lane's lease workspace and staging buffers get allocated

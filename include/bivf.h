@@ -323,6 +323,13 @@ bivf_status bivf_replay(bivf_executor* e, const bivf_replay_spec* spec, const fl
 /* ---- instrumentation ------------------------------------------------------ */
 /* kernel launches issued by this library since load (bench's gpu_launches) */
 uint64_t bivf_kernel_launches(void);
+/* serving start-up: one search of nq zero queries (k, nprobe) on every lease,
+ * all leases held at once, so each lease's stream, workspace, pinned staging and
+ * CUDA graph for that request shape exist before traffic (no first-use stalls
+ * when load first spreads over many leases).  Replaces nothing in the reference
+ * (its executor creates every lane and its cached scratch up front,
+ * executor.cpp:103-125). */
+bivf_status bivf_prewarm(bivf_index* h, uint64_t nq, uint64_t k, uint64_t nprobe);
 /* scan kernel selection: 0 auto (tensor-core filtered scan when supported:
  * L2, k <= 32, 8 <= D <= 128), 1 CUDA-core exact scan only, 2 = auto,
  * 3 / 4 = auto with the L2 list scan forced onto the vector-major /

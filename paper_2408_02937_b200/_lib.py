@@ -195,6 +195,7 @@ SIGNATURES = {
                               pu64, pu64, pu64]),
     "bivf_kernel_launches": (u64, []),
     "bivf_set_scan_mode": (C.c_int, [vp, C.c_int]),
+    "bivf_prewarm": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint64]),
     "bivf_set_timing": (C.c_int, [vp, C.c_int]),
     "bivf_last_timings": (C.c_int, [vp, C.POINTER(C.c_float)]),
 }

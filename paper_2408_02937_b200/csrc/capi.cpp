@@ -608,6 +608,10 @@ bivf_status bivf_replay(bivf_executor* e, const bivf_replay_spec* spec, const fl
     });
 }
 
+bivf_status bivf_prewarm(bivf_index* h, uint64_t nq, uint64_t k, uint64_t nprobe) {
+    return guard([&] { I(h).prewarm(nq, k, nprobe); });
+}
+
 bivf_status bivf_set_scan_mode(bivf_index* h, int mode) {
     return guard([&] {
         if (mode < 0 || mode > 4) throw Error(BIVF_EINVAL, "scan mode must be 0..4");

@@ -1282,12 +1282,44 @@ void GpuIndex::search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, 
     BIVF_CUDA(cudaSetDevice(device_));
     Lease* l = acquire_lease();
     const double us_lease = us_since(t_in);
-    double us_gate = 0, us_enq = 0, us_sync = 0, us_prep = 0;
     struct Rel {
         GpuIndex* g;
         Lease* l;
         ~Rel() { g->release_lease(l); }
     } rel{this, l};
+    search_on(l, q, nq, k, nprobe, out_ids, out_d, out_cnt, us_lease);
+}
+
+// Serving start-up: one search of `nq` zero queries on EVERY lease (all held at
+// once), so each lease's stream, events, workspace, pinned staging and CUDA graph
+// for that request shape exist before traffic arrives.  Without it a lease is
+// set up by the first request that finds the lower-numbered leases busy, and
+// that request (plus every lane waiting behind the device-wide cudaFree of a
+// workspace regrowth) pays milliseconds.
+void GpuIndex::prewarm(uint64_t nq, uint64_t k, uint64_t nprobe) {
+    validate_search(k, nprobe);
+    if (nq == 0) return;
+    BIVF_CUDA(cudaSetDevice(device_));
+    std::vector<float> q((size_t)nq * D_, 0.f);
+    std::vector<int64_t> ids((size_t)nq * k);
+    std::vector<float> d((size_t)nq * k);
+    std::vector<uint32_t> cnt(nq);
+    std::vector<Lease*> held;
+    struct RelAll {
+        GpuIndex* g;
+        std::vector<Lease*>& v;
+        ~RelAll() {
+            for (Lease* l : v) g->release_lease(l);
+        }
+    } rel{this, held};
+    for (size_t i = 0; i < leases_.size(); ++i) held.push_back(acquire_lease());
+    for (Lease* l : held) search_on(l, q.data(), nq, k, nprobe, ids.data(), d.data(), cnt.data(), 0.0);
+}
+
+void GpuIndex::search_on(Lease* l, const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, int64_t* out_ids,
+                         float* out_d, uint32_t* out_cnt, double us_lease) {
+    const auto t_in = TClock::now();
+    double us_gate = 0, us_enq = 0, us_sync = 0, us_prep = 0;
     const uint64_t slice = 32768;
     for (uint64_t s = 0; s < nq; s += slice) {
         const uint32_t m = (uint32_t)std::min(slice, nq - s);

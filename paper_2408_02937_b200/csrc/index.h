@@ -156,6 +156,8 @@ public:
     uint64_t insert(const float* x, uint64_t n, const int64_t* ids, int64_t* out_ids);
     void search(const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, int64_t* out_ids,
                 float* out_d, uint32_t* out_cnt);
+    // one zero-query search of this shape on every lease (serving start-up)
+    void prewarm(uint64_t nq, uint64_t k, uint64_t nprobe);
     void search_device(const float* q_dev, uint64_t nq, uint64_t k, uint64_t nprobe,
                        int64_t* ids_dev, float* d_dev, uint32_t* cnt_dev, cudaStream_t user);
     void assign(const float* y, uint64_t n, uint32_t* out);
@@ -255,6 +257,8 @@ private:
     // (returns false when the shape is not graph-eligible: caller enqueues)
     bool graph_search(Lease& l, uint32_t m, uint32_t k, uint32_t P, Workspace& w);
     uint64_t graph_sig() const;
+    void search_on(Lease* l, const float* q, uint64_t nq, uint64_t k, uint64_t nprobe, int64_t* out_ids,
+                   float* out_d, uint32_t* out_cnt, double us_lease);
     void enqueue_search(Lease& l, const float* q_dev_raw, uint32_t nq, uint32_t k,
                         uint32_t P, Workspace& w);
     void begin_maintenance();   // caller holds data_mu_; takes gate_ exclusively

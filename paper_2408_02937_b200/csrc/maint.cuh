@@ -41,7 +41,11 @@ constexpr uint64_t kArenaBit = 1ull << 63;
 
 // seed samples of the vector-major scan: kSampS offline vectors per list with
 // small residual norms, [list][d][slot] + ids (-1 = empty / deleted)
-constexpr uint32_t kSampS = 32;
+#ifndef BIVF_SAMP_S
+#define BIVF_SAMP_S 32
+#endif
+constexpr uint32_t kSampS = BIVF_SAMP_S;
+static_assert(kSampS % 32 == 0 && kSampS <= 1024, "seed samples: whole warps, <= the build's 1024 sorted keys");
 cudaError_t launch_sample_build(const float* off_pay, const long long* off_ids, const uint64_t* off_start,
                                 const uint32_t* off_count, const float* cent, uint32_t C, uint32_t D,
                                 float* rows, long long* ids, cudaStream_t s);

@@ -2091,23 +2091,34 @@ __global__ void vm_seed_kernel(TcParams p, const long long* probes, uint32_t nq)
     // [list][d][slot]) of the query's two nearest probes; an entry deleted before
     // this search's plan snapshot was invalidated before that deletion was
     // published, so every entry read here is a vector the scan probes
-    uint64_t v[BIVF_VM_SEED_LISTS];
+    constexpr int kPer = (int)(kSampS / 32), kR = BIVF_VM_SEED_LISTS * kPer;  // 32-sample blocks
+    uint64_t v[kR];
 #pragma unroll
-    for (int r = 0; r < BIVF_VM_SEED_LISTS; ++r) v[r] = ~0ull;
+    for (int r = 0; r < kR; ++r) v[r] = ~0ull;
     uint32_t nvec = 0;
 #pragma unroll
-    for (int r = 0; r < BIVF_VM_SEED_LISTS; ++r) {
-        if ((uint32_t)r >= p.P) break;
-        const uint32_t c = (uint32_t)probes[(uint64_t)q * p.P + r];
-        const long long id = *reinterpret_cast<const volatile long long*>(p.samp_ids + (uint64_t)c * kSampS + lane);
+    for (int r = 0; r < kR; ++r) {
+        if ((uint32_t)(r / kPer) >= p.P) break;
+        const uint32_t c = (uint32_t)probes[(uint64_t)q * p.P + r / kPer];
+        const uint32_t sl = 32u * (r % kPer) + lane;
+        const long long id = *reinterpret_cast<const volatile long long*>(p.samp_ids + (uint64_t)c * kSampS + sl);
         const bool ok = id >= 0;
-        const float dist = exact_l2(qs, p.samp_rows + (uint64_t)c * p.D * kSampS + lane, p.D);
+        const float* x = p.samp_rows + (uint64_t)c * p.D * kSampS + sl;
+        float dist = 0.f;  // exact_l2 over the [d][kSampS] sample rows
+        for (uint32_t d0 = 0; d0 < p.D; d0 += 16) {
+            float xv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) xv[i] = d0 + i < p.D ? x[(uint64_t)(d0 + i) * kSampS] : 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (d0 + i < p.D) dist = l2_step(dist, qs[d0 + i], xv[i]);
+        }
         if (ok) v[r] = ((uint64_t)f2ord(dist) << 32) | (32u * r + lane);  // (r static: unrolled)
         nvec += __popc(__ballot_sync(0xffffffffu, ok));
     }
     if (nvec < p.k) return;  // qthr stays "none"
-    warp_bitonic<BIVF_VM_SEED_LISTS>(v, lane);
-    const uint64_t kth = warp_elem<BIVF_VM_SEED_LISTS>(v, p.k - 1);
+    warp_bitonic<kR>(v, lane);
+    const uint64_t kth = warp_elem<kR>(v, p.k - 1);
     if (lane == 0) p.qthr[q] = __uint_as_float((uint32_t)(kth >> 32));
 }
 // Fast selection of dense_select_kernel (R pre-threshold keys per lane, lists of

@@ -340,13 +340,13 @@ class ClusterIndex:
         check(lib().bivf_save_snapshot(self._h, str(path).encode()))
 
     def seed_samples(self):
-        """The list scan's seed samples: [num_clusters, 32] ids (-1 = empty / deleted)."""
+        """The list scan's seed samples: [num_clusters, S] ids (S = 32 per list; -1 = empty / deleted)."""
         n = C.c_uint64(0)
         check(lib().bivf_seed_samples(self._h, None, 0, C.byref(n)))
         out = np.full(n.value, -1, np.int64)
         if n.value:
             check(lib().bivf_seed_samples(self._h, out.ctypes.data, n.value, C.byref(n)))
-        return out.reshape(-1, 32)
+        return out.reshape(self.num_clusters, -1)
 
     def pool_alert(self):
         """(fired, blocks used at the allocation that first exceeded the watermark)."""
@@ -376,6 +376,11 @@ class ClusterIndex:
         h = C.c_void_p()
         check(lib().bivf_load_snapshot(str(path).encode(), C.byref(ov), C.byref(h)))
         return ClusterIndex(_handle=h.value)
+
+    def prewarm(self, nq=10, k=10, nprobe=8):
+        """Serving start-up: one zero-query search of this shape on every lease
+        (streams, workspaces, pinned staging, CUDA graphs set up before traffic)."""
+        check(lib().bivf_prewarm(self._h, nq, k, nprobe))
 
     # ------------------------------------------------------------ kernels / timing
     def set_scan_mode(self, mode="auto"):

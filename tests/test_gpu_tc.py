@@ -321,3 +321,31 @@ def test_vm_seed_samples_follow_deletes(gpu_ready):
             for j in range(0, 400, 53):
                 oi, od = orc.search(q[j], k, npb)
                 assert np.array_equal(b[0][j, : b[2][j]], oi) and np.array_equal(bits(b[1][j, : b[2][j]]), bits(od))
+
+
+def test_prewarm_sets_up_every_lease(gpu_ready):
+    """bivf_prewarm runs one zero-query search per lease (all held at once); the
+    index's results are unchanged and concurrent callers afterwards agree."""
+    import threading
+    D, C = 32, 16
+    base = bivf.synthetic_dataset(4000, D, 24, 21)
+    cent, asg, _ = bivf.kmeans(base, C, 5, 21)
+    ix = ClusterIndex.empty(D, C, block_capacity=64, num_blocks=256)
+    ix.set_centroids(cent)
+    ix.bulk_load(base, asg)
+    q = bivf.synthetic_dataset(10, D, 24, 22)
+    before = ix.search_batch(q, 10, 4)
+    ix.prewarm(10, 10, 4)
+    outs = [None] * 8
+
+    def run(j):
+        outs[j] = ix.search_batch(q, 10, 4)
+    ths = [threading.Thread(target=run, args=(j,)) for j in range(8)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for o in outs:
+        assert_same(before, o)
+    with pytest.raises(ValueError):
+        ix.prewarm(10, 0, 4)
