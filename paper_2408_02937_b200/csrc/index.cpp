@@ -495,8 +495,12 @@ uint32_t GpuIndex::quantizer_slice() const {
 }
 
 uint32_t GpuIndex::quantizer_maxch(uint32_t nq) const {
+    static const uint32_t min_ch = [] {  // tuning aid: at least this many centroid chunks
+        const char* v = std::getenv("BIVF_QMAXCH");
+        return v ? (uint32_t)atoi(v) : 1u;
+    }();
     const uint32_t tiles = ceil_div(nq, 128u), ngq = ceil_div(C_, 32u);
-    const uint32_t want = ceil_div((uint32_t)num_sms_, std::max(1u, tiles));
+    const uint32_t want = std::max(min_ch, ceil_div((uint32_t)num_sms_, std::max(1u, tiles)));
     return std::max(1u, std::min(want, std::max(1u, ngq / 4)));
 }
 

@@ -1134,7 +1134,10 @@ constexpr int kVmNS = 3;       // A stage slots (one unit of 4 groups each)
 #endif
 constexpr int kVmPF = BIVF_VM_PF;  // units prefetched into L2 ahead of the shared-memory ring
 constexpr int kVmNR = 8;       // norm ring slots (a unit's 4 x 32 |s|^2)
-constexpr int kVmNB = 4;       // TMEM accumulators (32 columns each)
+#ifndef BIVF_VM_NB
+#define BIVF_VM_NB 4  // 8 measured equal (1.004 vs 1.005 ms): the math warps, not buffering, limit
+#endif
+constexpr int kVmNB = BIVF_VM_NB;  // TMEM accumulators (32 columns each; power of 2)
 constexpr int kVmKC = 24;      // candidate slots per (warp, query lane)
 constexpr uint32_t kVmSlot = 4u * kMaxD * 64u;  // bytes per A slot (4 groups x K rows x 64 B, K <= 128)
 constexpr uint32_t kVmPlane = kMaxD * 64u;      // bytes per B plane (K rows x 32 queries bf16)
@@ -2906,7 +2909,10 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
         const char* v = std::getenv("BIVF_TC_SEED_GROUPS");  // tuning aid
         return v ? std::max(1u, (uint32_t)atoi(v)) : (uint32_t)kGU;
     }();
-    const bool two = !dense && sh.P >= 2 && sh.nq >= two_min;
+    // (not for the inner-product wide mode: at D = 768 the seeding pass's item
+    // builds cost more than the seeded thresholds save -- measured 2.15 ms seeded
+    // vs 1.88 ms unseeded scan per 10K queries, 2M x 768, nprobe 32)
+    const bool two = !dense && !wide && sh.P >= 2 && sh.nq >= two_min;
     SearchShape sa = s2;  // seeding pass: rank-0 pairs, one chunk per list
     sa.maxch = 1;
     if (!(dense && dense->list_base)) {  // the IVF dense path planned in launch_dense_plan

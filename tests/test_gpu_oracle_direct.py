@@ -148,7 +148,7 @@ def test_inner_product_wide_mode_equals_oracle(gpu_ready, D, C, T, n, norm):
 
 def test_inner_product_cfg5_shape_equals_oracle(gpu_ready):
     """cfg5's generator at D = 768 (unit embeddings around 2048 directions),
-    120K vectors + live inserts: a 2000-query seeded batch on the wide mode
+    120K vectors + live inserts: a 2000-query batch on the wide mode
     equals the restatement on a 400-query sample (ids + key bits)."""
     rng = np.random.default_rng(5)
     D, C, n = 768, 256, 120_000
