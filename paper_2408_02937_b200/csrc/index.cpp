@@ -580,8 +580,13 @@ void GpuIndex::enqueue_quantizer(cudaStream_t s, uint32_t nq, uint32_t P, uint32
             // selection requires)
             TcDense dn{w.qdense, w.qdense_nq, ld, C_, nullptr,
                        ceil_div(C_, 32) >= 4 * P ? w.qgsum : nullptr};
-            // inner product: filter + exact refine (L2 filter mode measured 0.39 vs 0.18 ms dense)
-            const bool ip = cfg_.metric == BIVF_METRIC_IP;
+            // both metrics: dense keys + exact selection (measured: L2 filter mode 0.39 vs
+            // 0.18 ms dense; inner product, D = 768, filter + refine vs dense: see DESIGN 6)
+            static const bool ip_filter = [] {  // comparison aid: the round-1 IP filter mode
+                const char* v = std::getenv("BIVF_IPQ_FILTER");
+                return v && v[0] == '1';
+            }();
+            const bool ip = cfg_.metric == BIVF_METRIC_IP && ip_filter;
             const size_t g0 = (size_t)qbase + q0;
             // work items = tiles x chunks (the centroid list has no online part)
             const uint32_t ngq = ceil_div(C_, 32);

@@ -528,7 +528,7 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
     mbar_wait(&nfull[ns], (u / kNR) & 1);
     pf.mark(6);
     const float* wslot = nslots + ns * kGU * kNormFloats;
-    if (!W && p.dense_out) {  // dense mode (L2): write the approximate distances, no filtering
+    if (p.dense_out) {  // dense mode: write the approximate keys, no filtering
         // this warp's 32 x 32 staging tile in the (otherwise unused) pass-2 scratch,
         // 16 B chunks XOR-swizzled by row: each thread parks its row, then every
         // store instruction writes four whole 128 B row segments
@@ -545,13 +545,20 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
             const float* wn = wslot + h * kNormFloats;
             tmem_ld32(acol + 32 * h, dot);
             float av[32];
+            if constexpr (W) {
+                // inner product (tc_filter's W key): a = -(P' 2^-ev) 2^-eq, exact scalings
+                const float isq = 1.0f / sq;
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-                const float4 v = reinterpret_cast<const float4*>(wn)[i / 4];
-                av[i] = fmaf(-2.f, dot[i], nq + v.x);
-                av[i + 1] = fmaf(-2.f, dot[i + 1], nq + v.y);
-                av[i + 2] = fmaf(-2.f, dot[i + 2], nq + v.z);
-                av[i + 3] = fmaf(-2.f, dot[i + 3], nq + v.w);
+                for (int i = 0; i < 32; ++i) av[i] = -(dot[i] * wn[i]) * isq;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    const float4 v = reinterpret_cast<const float4*>(wn)[i / 4];
+                    av[i] = fmaf(-2.f, dot[i], nq + v.x);
+                    av[i + 1] = fmaf(-2.f, dot[i + 1], nq + v.y);
+                    av[i + 2] = fmaf(-2.f, dot[i + 2], nq + v.z);
+                    av[i + 3] = fmaf(-2.f, dot[i + 3], nq + v.w);
+                }
             }
             if (act) {
 #pragma unroll
@@ -593,7 +600,8 @@ __device__ __forceinline__ void tc_unit(const TcParams& p, const TcItem& d, uint
                     float mh = __int_as_float(0x7f800000), ml = mh;
 #pragma unroll
                     for (uint32_t n = 0; n < 32; ++n) {
-                        const float e = fmaf(kEpsRel, fabsf(av[n]), fmaf(kEpsT, nq + wn[n], 1e-30f));
+                        const float e = W ? fmaf(nq * (1.0f / sq), wn[32 + n], 1e-30f)
+                                          : fmaf(kEpsRel, fabsf(av[n]), fmaf(kEpsT, nq + wn[n], 1e-30f));
                         if (n < nvalid) {
                             mh = fminf(mh, av[n] + e);
                             ml = fminf(ml, av[n] - e);
@@ -919,6 +927,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const int eq = wide_scale_exp(mx);
                 sq = ldexpf(1.f, eq);
                 nq = kEpsIP * sqrtf(__fadd_rn(nqb[m], nqb[kM + m])) * sq;
+                if (p.dense_out && wg == 0 && active && d.chunk == 0)
+                    p.dense_nq[pair / p.P] = nq / sq;  // kEpsIP |q| (dense_select's IP bound)
                 __syncwarp();
                 tc_fence_after();
                 for (uint32_t c = wg; 64 * c < p.Dk; c += 2) {
@@ -2124,11 +2134,24 @@ __global__ void vm_seed_kernel(TcParams p, const long long* probes, uint32_t nq)
     const uint64_t kth = warp_elem<kR>(v, p.k - 1);
     if (lane == 0) p.qthr[q] = __uint_as_float((uint32_t)(kth >> 32));
 }
+// Bound half-width of a dense-mode approximate key a of slot c (mirror.cuh eps'):
+// L2 from |a|, |q|^2 (nqv) and |s|^2; inner product from kEpsIP |q| (nqv) and |x|
+// (the wide mirror's norm row, second half), as tc_filter's W pass 2.
+template <int MET>
+__device__ __forceinline__ float dsel_eps(float a, float nqv, const float* nrm, uint32_t c) {
+    if constexpr (MET == kL2) {
+        const float ns = nrm[(c >> 5) * kNormFloats + (c & 31)];
+        return fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, nqv + ns, 1e-30f));
+    } else {
+        return fmaf(nqv, nrm[(c >> 5) * kNormFloats + 32 + (c & 31)], 1e-30f);
+    }
+}
+
 // Fast selection of dense_select_kernel (R pre-threshold keys per lane, lists of
 // 32 RL slots; k <= 32R <= n): true when
 // the exact top-k was written (false: more than 32R values tie the bounds, the
 // caller's general path runs with *pre as its pre-threshold).
-template <int R, int RL, typename UbOf>
+template <int R, int RL, int MET, typename UbOf>
 __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* nrm, float nqv,
                                   const float* qs, const float* rows, uint32_t D, uint32_t n,
                                   uint32_t k, uint32_t q, uint32_t lane, uint32_t* scratch,
@@ -2214,8 +2237,7 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
             bool cand = false;
             if (c < n) {
                 const float a = row[c];
-                const float ns = nrm[(c >> 5) * kNormFloats + (c & 31)];
-                cand = a - fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, nqv + ns, 1e-30f)) <= theta;
+                cand = a - dsel_eps<MET>(a, nqv, nrm, c) <= theta;
             }
             const unsigned msk = __ballot_sync(0xffffffffu, cand);
             if (n2 + __popc(msk) > 32u * RL) {
@@ -2233,7 +2255,7 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
                 u[j] = ~0ull;
                 if (e < n2) {
                     const uint32_t c = cq[e];
-                    u[j] = (uint64_t)f2ord(exact_l2_row(qs, rows + (uint64_t)c * D, D)) << 32 | c;
+                    u[j] = (uint64_t)f2ord(exact_key_row<MET>(qs, rows + (uint64_t)c * D, D)) << 32 | c;
                 }
             }
             warp_bitonic<RL>(u, lane);
@@ -2259,7 +2281,7 @@ __device__ bool dense_select_fast(UbOf&& ub_of, const float* row, const float* n
 #ifndef BIVF_QSEL_MINB
 #define BIVF_QSEL_MINB 6  // 64 registers (measured: quantizer 0.47 -> 0.41 ms at nprobe 64)
 #endif
-template <int KPL>
+template <int KPL, int MET>
 __global__ void __launch_bounds__(128, BIVF_QSEL_MINB) dense_select_kernel(const float* dense, uint32_t ld, const float* dnq,
                                     const float* nrm, const float* rows, const float* queries,
                                     uint32_t Dp, uint32_t D, uint32_t n, uint32_t nq, uint32_t k,
@@ -2276,8 +2298,7 @@ __global__ void __launch_bounds__(128, BIVF_QSEL_MINB) dense_select_kernel(const
     const float inf = __int_as_float(0x7f800000);
     auto ub_of = [&](uint32_t c) {
         const float a = row[c];
-        const float ns = nrm[(c >> 5) * kNormFloats + (c & 31)];
-        return a + fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, nqv + ns, 1e-30f));
+        return a + dsel_eps<MET>(a, nqv, nrm, c);
     };
     // phase A (+ the fast selection when <= 32R values tie the bounds): the k-th
     // smallest of each lane's R smallest upper bounds bounds the k-th smallest
@@ -2285,13 +2306,13 @@ __global__ void __launch_bounds__(128, BIVF_QSEL_MINB) dense_select_kernel(const
     uint32_t* fscr = reinterpret_cast<uint32_t*>(qsm + nw * Dp) + nw * 32 + wq * 768;
     const float2* gs = gsum ? gsum + (uint64_t)q * ((n + 31) / 32) : nullptr;
     if (k <= 32 && n >= 64) {
-        if (dense_select_fast<2, 2>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre, gs))
+        if (dense_select_fast<2, 2, MET>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre, gs))
             return;
     } else if (k <= 64 && n >= 128) {
-        if (dense_select_fast<4, 8>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre, gs))
+        if (dense_select_fast<4, 8, MET>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre, gs))
             return;
     } else if (k <= 128 && n >= 256) {
-        if (dense_select_fast<8, 8>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre, gs))
+        if (dense_select_fast<8, 8, MET>(ub_of, row, nrm, nqv, qs, rows, D, n, k, q, lane, fscr, out_d, out_i, &pre, gs))
             return;
     }
     WarpTopK<KPL> th;
@@ -2319,7 +2340,7 @@ __global__ void __launch_bounds__(128, BIVF_QSEL_MINB) dense_select_kernel(const
     auto flush = [&]() {
         const bool ok = lane < qn;
         const uint32_t c = ok ? queue[lane] : 0u;
-        const float dist = ok ? exact_l2_row(qs, rows + (uint64_t)c * D, D) : 0.f;
+        const float dist = ok ? exact_key_row<MET>(qs, rows + (uint64_t)c * D, D) : 0.f;
         const bool pass = ok && tk.admits(dist, (long long)c);
         unsigned m = __ballot_sync(0xffffffffu, pass);
         while (m) {
@@ -2337,9 +2358,7 @@ __global__ void __launch_bounds__(128, BIVF_QSEL_MINB) dense_select_kernel(const
         bool cand = false;
         if (c < n) {
             const float a = row[c];
-            const float ns = nrm[(c >> 5) * kNormFloats + (c & 31)];
-            const float l = a - fmaf(kEpsRel, fabsf(a), fmaf(kEpsT, nqv + ns, 1e-30f));
-            cand = l <= theta;
+            cand = a - dsel_eps<MET>(a, nqv, nrm, c) <= theta;
         }
         const unsigned msk = __ballot_sync(0xffffffffu, cand);
         const uint32_t np = __popc(msk);
@@ -2873,7 +2892,7 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
                                  int vm_mode) {
     if (sh.nq == 0) return cudaSuccess;
     const bool wide = sh.metric == kIP;  // 1xBF16 inner-product mode (mirror.cuh wide mirror)
-    if (wide && dense) return cudaErrorInvalidValue;
+    if (wide && dense && dense->list_base) return cudaErrorInvalidValue;  // IVF dense mode: L2 only
     static const bool vm_env = [] {
         const char* v = std::getenv("BIVF_TC_VM");  // 0: the query-major 3xBF16 scan (comparison aid)
         return !(v && v[0] == '0');
@@ -3006,12 +3025,16 @@ cudaError_t launch_ivf_search_tc(const DevLists& L, const PlanBufs& B, const lon
     } else if (dense) {
         const uint32_t n = dense->n;
         const size_t sm_sel = wpb * (p.Dp * 4 + 128 + 768 * 4);
-        if (sh.k <= 32)
-            dense_select_kernel<1><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
+        if (wide)  // inner-product quantizer (k = nprobe <= 32)
+            dense_select_kernel<1, kIP><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
+                dense->out, dense->ld, dense->nq, off_nrm, off_rows, queries, p.Dp, p.D, n, sh.nq,
+                sh.k, out_d, out_i, dense->gsum);
+        else if (sh.k <= 32)
+            dense_select_kernel<1, kL2><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
                 dense->out, dense->ld, dense->nq, off_nrm, off_rows, queries, p.Dp, p.D, n, sh.nq,
                 sh.k, out_d, out_i, dense->gsum);
         else
-            dense_select_kernel<8><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
+            dense_select_kernel<8, kL2><<<(sh.nq + wpb - 1) / wpb, wpb * 32, sm_sel, s>>>(
                 dense->out, dense->ld, dense->nq, off_nrm, off_rows, queries, p.Dp, p.D, n, sh.nq,
                 sh.k, out_d, out_i, dense->gsum);
     } else {

@@ -10,6 +10,6 @@ timeout -s KILL 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dr
   --csv --log-file gpurun_out/launches_lat_$tag.csv python tools/prof_scan.py > gpurun_out/ncu_lat_launch_$tag.log 2>&1
 echo "ncu lat launches rc=$?"
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on \
-  -k "regex:scan_tc_kernel" -s 60 -c 3 -o gpurun_out/prof_lat_$tag \
+  -k "regex:scan_vm_kernel|scan_tc_kernel" -s 60 -c 3 -o gpurun_out/prof_lat_$tag \
   python tools/prof_scan.py > gpurun_out/ncu_lat_$tag.log 2>&1
 echo "ncu lat full rc=$?"
