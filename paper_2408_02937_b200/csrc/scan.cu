@@ -512,8 +512,19 @@ __global__ void __launch_bounds__(1024) plan_fused(DevLists L, uint32_t maxch, u
                                                    uint32_t P, uint32_t lo, uint32_t hi,
                                                    int snapshot, uint32_t QT, PlanBufs B) {
     const uint32_t t = threadIdx.x;
-    for (uint32_t c = t; c < L.C; c += 1024) {
-        if (snapshot) {
+    if (snapshot) {
+        // only the lists some pair of the batch probes (any rank: a later ranked
+        // plan with snapshot = 0 reuses these) are snapshotted; the others get no
+        // work items and nothing after the plan reads their snapshot
+        for (uint32_t c = t; c < L.C; c += 1024) {
+            B.cnt[c] = 0;
+            B.nch[c] = 0;
+        }
+        __syncthreads();
+        for (uint32_t i = t; i < npairs; i += 1024) B.nch[(uint32_t)probes[i]] = 1u;
+        __syncthreads();
+        for (uint32_t c = t; c < L.C; c += 1024) {
+            if (!B.nch[c]) continue;
             uint32_t off, len;
             uint64_t start, row;
             snapshot_list(L, c, off, len, start, row);
@@ -526,7 +537,8 @@ __global__ void __launch_bounds__(1024) plan_fused(DevLists L, uint32_t maxch, u
             B.gc[c] = g;
             B.nch[c] = (ng + g - 1) / g;
         }
-        B.cnt[c] = 0;
+    } else {
+        for (uint32_t c = t; c < L.C; c += 1024) B.cnt[c] = 0;
     }
     __syncthreads();
     for (uint32_t i = t; i < npairs; i += 1024) {

@@ -55,8 +55,12 @@ __device__ __forceinline__ void snapshot_list(const DevLists& L, uint32_t c, uin
     for (;;) {
         const uint32_t v1 = ld_acquire_u32(L.ver + c);
         if (v1 & 1u) continue;  // a publish kernel is rewriting this list right now
-        off = ld_acquire_u32(L.off_count + c);
-        len = ld_acquire_u32(L.len + c);
+        // the fields as relaxed loads, all in flight together (the acquire on the
+        // version keeps them after it); the fence below turns them into an
+        // acquire pattern, so a length read here synchronizes with the insert's
+        // release-publish of it and later kernels see the payload it covers
+        off = *reinterpret_cast<const volatile uint32_t*>(L.off_count + c);
+        len = *reinterpret_cast<const volatile uint32_t*>(L.len + c);
         start = *reinterpret_cast<const volatile uint64_t*>(L.off_start + c);
         row = *reinterpret_cast<const volatile uint64_t*>(reinterpret_cast<const uint64_t*>(L.rowptr) + c);
         __threadfence();
