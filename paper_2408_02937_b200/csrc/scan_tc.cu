@@ -1177,6 +1177,12 @@ __device__ __forceinline__ void mma_vm_elect(uint32_t dcol, uint64_t ad, uint64_
         : "memory");
 }
 
+// the math warps' 32 x 32 transpose tile: element (vector row s, query column n)
+// lives in 16 B chunk (n / 4) ^ (s & 7) of row s -- rows are written as 8 float4
+// chunks, columns read as 32 scalars, both without bank conflicts
+__device__ __forceinline__ uint32_t vm_tsw(uint32_t s, uint32_t n) {
+    return s * 32u + ((((n >> 2) ^ (s & 7u)) << 2) | (n & 3u));
+}
 __device__ __forceinline__ uint32_t vm_nvalid(const TcParams& p, const TcItem& d, uint32_t j) {
     const uint32_t og = (d.off + 31u) >> 5;
     if (j < og) return min(32u, d.off - 32u * j);
@@ -1564,12 +1570,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 // transpose: lane s writes vector s's 32 query values, lane n reads
                 // query n's 32 vector values
 #pragma unroll
-                for (int i = 0; i < 32; ++i) tp[lane * 32 + (i ^ lane)] = dot[i];
+                for (int c = 0; c < 8; ++c)  // 16 B chunks, XOR-swizzled by row (conflict-free)
+                    *reinterpret_cast<float4*>(tp + lane * 32 + ((c ^ (lane & 7)) << 2)) =
+                        make_float4(dot[4 * c], dot[4 * c + 1], dot[4 * c + 2], dot[4 * c + 3]);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty[b]);
 #pragma unroll
-                for (int s = 0; s < 32; ++s) dot[s] = tp[s * 32 + (n ^ s)];
+                for (int s = 0; s < 32; ++s) dot[s] = tp[vm_tsw(s, n)];
                 pf.mark(4);
                 mbar_wait(&nfull[nsl], (unit / kVmNR) & 1);
                 pf.mark(5);
@@ -1603,7 +1611,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                             const uint32_t s = __ffs(need) - 1;
                             need &= need - 1;
                             const float ns = wn[s];
-                            const float a = fmaf(-2.f, tp[s * 32 + (n ^ s)], nr + ns);
+                            const float a = fmaf(-2.f, tp[vm_tsw(s, n)], nr + ns);
                             const float e = fmaf(kVmCross, rn * sqrtf(ns),
                                                  fmaf(kEpsRel, nr + ns, fmaf(kEpsRel, fabsf(a), 1e-30f)));
                             const float h = a + e, l = a - e;
