@@ -1612,7 +1612,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                             need &= need - 1;
                             const float ns = wn[s];
                             const float a = fmaf(-2.f, tp[vm_tsw(s, n)], nr + ns);
-                            const float e = fmaf(kVmCross, rn * sqrtf(ns),
+                            // |s| from the hardware reciprocal square root (rel. error <= 2^-22),
+                            // rounded up by 2^-19: e only needs an upper bound
+                            const float sn = ns > 0.f ? ns * rsqrtf(ns) * (1.0f + 0x1p-19f) : 0.f;
+                            const float e = fmaf(kVmCross, rn * sn,
                                                  fmaf(kEpsRel, nr + ns, fmaf(kEpsRel, fabsf(a), 1e-30f)));
                             const float h = a + e, l = a - e;
                             if (h < th) {
