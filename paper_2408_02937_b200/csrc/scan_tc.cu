@@ -1588,20 +1588,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     float th = qthr_dec(*reinterpret_cast<volatile uint32_t*>(qts));
                     // pass 1: some slot s can enter iff dot_s - c1 ns_s / 2 >= W
                     const float W = 0.5f * fmaf(kVmC1, nr, -kVmC2 * th);
-                    float m0 = -__int_as_float(0x7f800000), m1 = m0;
+                    // (the survivor mask directly: one FFMA + compare per slot, the norm
+                    // row read once as 8 vector loads)
+                    uint32_t need = 0;
 #pragma unroll
                     for (int s = 0; s < 32; s += 4) {
                         const float4 v = *reinterpret_cast<const float4*>(wn + s);
-                        m0 = fmaxf(m0, fmaxf(fmaf(-0.5f * kVmC1, v.x, dot[s]), fmaf(-0.5f * kVmC1, v.y, dot[s + 1])));
-                        m1 = fmaxf(m1, fmaxf(fmaf(-0.5f * kVmC1, v.z, dot[s + 2]), fmaf(-0.5f * kVmC1, v.w, dot[s + 3])));
+                        need |= (fmaf(-0.5f * kVmC1, v.x, dot[s]) >= W) ? (1u << s) : 0u;
+                        need |= (fmaf(-0.5f * kVmC1, v.y, dot[s + 1]) >= W) ? (2u << s) : 0u;
+                        need |= (fmaf(-0.5f * kVmC1, v.z, dot[s + 2]) >= W) ? (4u << s) : 0u;
+                        need |= (fmaf(-0.5f * kVmC1, v.w, dot[s + 3]) >= W) ? (8u << s) : 0u;
                     }
                     pf.mark(6);
-                    if (fmaxf(m0, m1) >= W) {
+                    if (need) {
                         const uint32_t nv = vm_nvalid(p, d, j);
-                        uint32_t need = 0;
-#pragma unroll
-                        for (int s = 0; s < 32; ++s)
-                            need |= (fmaf(-0.5f * kVmC1, wn[s], dot[s]) >= W) ? (1u << s) : 0u;
                         need &= nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
                         // pass 2 (the tile column still holds this lane's values)
 #if BIVF_TC_PROF
