@@ -549,6 +549,7 @@ def latency_phase(ix, queries, inserts, dels, seconds, repeats):
     # untimed warm-up: every lane's lease workspace and staging buffers get allocated
     replay(ex, queries, inserts[:100_000], LAT_QPS, INSERT_RATE / INSERT_BATCH, 0.5, seed=99, **common)
     idle, live, ins_lat = [], [], []
+    m0 = ix.maintenance_stats()
     rr = 0
     dpos = 0
     ipos = 100_000
@@ -593,6 +594,7 @@ def latency_phase(ix, queries, inserts, dels, seconds, repeats):
             "p99_ratio_live_vs_idle": round(s_live["p99_ms"] / s_idle["p99_ms"], 3),
             "p99_ratio_per_repeat": per_rep,
             "rearrange_events": rr, "deleted": int(ndel),
+            "maintenance_ops": {k2: v - m0[k2] for k2, v in ix.maintenance_stats().items()},
             "rejected": int(sum(x["rejected"] for x in idle + live))}
 
 

@@ -732,7 +732,7 @@ void GpuIndex::bulk_load(const float* x, uint64_t n, const uint32_t* assignment,
     }
     // free space beside the segments: a delete writes a segment's new version
     // there and frees the old one after a grace period (copy-on-write)
-    const uint64_t slack = cow_on_ ? std::max<uint64_t>(total / 8, 64 * maxseg) : 0;
+    const uint64_t slack = cow_on_ ? std::max<uint64_t>(total / 4, 64 * maxseg) : 0;
     ensure_offline_capacity(total + slack);
     BIVF_CUDA(dset(d_off_ids_.p, 0xff, d_off_ids_.bytes));
     off_region_.clear();
@@ -809,6 +809,8 @@ void GpuIndex::bulk_load(const float* x, uint64_t n, const uint32_t* assignment,
 // Grow the offline-segment area to `slots`, keeping every byte (the block-based
 // path never needs this: its area is sized once by bulk_load).
 void GpuIndex::grow_offline_preserving(uint64_t slots) {
+    if (trace_threshold_us() > 0)
+        trace("grow_offline", trace_threshold_us(), "slots " + std::to_string(off_slots_cap_) + " -> " + std::to_string(slots));
     slots = (slots + 31) / 32 * 32;
     if (slots <= off_slots_cap_) return;
     const uint64_t cap = std::max<uint64_t>(slots, off_slots_cap_ * 2);
@@ -1619,11 +1621,22 @@ uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_
         TClock::time_point t;
         double lock;
         uint64_t n;
+        double ph[5] = {0, 0, 0, 0, 0};  // stage+quantizer enqueue, grow_rows, insert enqueue, sync, absorb
         ~Tr() {
             if (trace_threshold_us() > 0)
-                trace("insert", us_since(t), "n=" + std::to_string(n) + " data_mu=" + std::to_string((int)lock));
+                trace("insert", us_since(t), "n=" + std::to_string(n) + " data_mu=" + std::to_string((int)lock) +
+                                                 " enqueue=" + std::to_string((int)ph[0]) + " grow_rows=" +
+                                                 std::to_string((int)ph[1]) + " insert=" + std::to_string((int)ph[2]) +
+                                                 " sync=" + std::to_string((int)ph[3]) + " absorb=" +
+                                                 std::to_string((int)ph[4]));
         }
     } tr{t_in, us_since(t_in), n};
+    TClock::time_point tp0 = TClock::now();
+    auto lap = [&](int i) {
+        const auto now = TClock::now();
+        tr.ph[i] += std::chrono::duration<double, std::micro>(now - tp0).count();
+        tp0 = now;
+    };
     BIVF_CUDA(cudaSetDevice(device_));
     // ids: contiguous auto range, or supplied ids checked in batch order
     std::vector<long long> idv(n);
@@ -1644,18 +1657,24 @@ uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_
     std::vector<int32_t> blk;
     for (uint64_t s = 0; s < n; s += chunk) {
         const uint32_t m = (uint32_t)std::min(chunk, n - s);
-        d_x_.ensure((size_t)m * D_ * 4);
-        d_qtmp_.ensure((size_t)m * Dp_ * 4);
-        d_ids_.ensure((size_t)m * 8);
-        d_asg_.ensure((size_t)m * 4);
-        d_blk_.ensure((size_t)m * 4);
-        d_did_.ensure((size_t)m * 4);
+        // staging sized for at least the executor's largest batch (1024) on first
+        // use: a buffer regrowth mid-stream (cudaFree / cudaFreeHost synchronise)
+        // stalled an insert for ~0.4 s under live search traffic
+        const uint32_t mc = std::max<uint32_t>(m, 1024u);
+        d_x_.ensure((size_t)mc * D_ * 4);
+        d_qtmp_.ensure((size_t)mc * Dp_ * 4);
+        d_ids_.ensure((size_t)mc * 8);
+        d_asg_.ensure((size_t)mc * 4);
+        d_blk_.ensure((size_t)mc * 4);
+        d_did_.ensure((size_t)mc * 4);
         const LaunchShape sh = pick_shape(m, 1, 1, C_, num_sms_);
-        d_fc_d_.ensure((size_t)m * sh.fnch * 4);
-        d_fc_i_.ensure((size_t)m * sh.fnch * 8);
-        d_fo_i_.ensure((size_t)m * 8);
-        d_fo_d_.ensure((size_t)m * 4);
-        h_stage_.ensure((size_t)m * D_ * 4 + (size_t)m * 8 + 64);
+        const LaunchShape shc = pick_shape(mc, 1, 1, C_, num_sms_);
+        const size_t fc = std::max((size_t)m * sh.fnch, (size_t)mc * shc.fnch);
+        d_fc_d_.ensure(fc * 4);
+        d_fc_i_.ensure(fc * 8);
+        d_fo_i_.ensure((size_t)mc * 8);
+        d_fo_d_.ensure((size_t)mc * 4);
+        h_stage_.ensure((size_t)mc * D_ * 4 + (size_t)mc * 8 + 64);
         float* px = h_stage_.as<float>();
         std::memcpy(px, x + s * D_, (size_t)m * D_ * 4);
         long long* pid = reinterpret_cast<long long*>(h_stage_.as<char>() + align_up((size_t)m * D_ * 4, 64));
@@ -1668,7 +1687,8 @@ uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_
         // live searches occupies a handful of SMs, not the whole GPU
         const long long* nearest = d_fo_i_.as<long long>();
         if (use_tc_quantizer(1) && m <= 65536) {
-            Workspace dw = carve(data_lease_, m, 1, 1, 1, sh.fnch);
+            // carved for mc queries (the lease workspace keeps its largest size), used for m
+            Workspace dw = carve(data_lease_, mc, 1, 1, 1, std::max(sh.fnch, shc.fnch));
             BIVF_CUDA(launch_pad_rows(d_x_.as<float>(), m, D_, Dp_, dw.queries, st));
             enqueue_quantizer(st, m, 1, sh.fnch, dw);
             nearest = dw.probes;
@@ -1681,10 +1701,12 @@ uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_
                                        num_sms_, st));
         }
         BIVF_CUDA(launch_make_asg(nearest, d_ids_.as<long long>(), m, d_asg_.as<uint32_t>(), st));
+        lap(0);
         // block-table rows with room for every block this chunk can open in one list
         uint32_t mxb = 0;
         for (uint32_t c = 0; c < C_; ++c) mxb = std::max(mxb, h_nblocks_[c]);
         grow_rows(mxb + ceil_div(m, T_) + 1);
+        lap(1);
         const uint32_t cursor_old = h_cursor_;
         BIVF_CUDA(launch_insert(insert_state(), m, d_x_.as<float>(), d_ids_.as<long long>(),
                                 d_asg_.as<uint32_t>(), d_blk_.as<int32_t>(),
@@ -1694,8 +1716,11 @@ uint64_t GpuIndex::insert(const float* x, uint64_t n, const int64_t* ids, int64_
         BIVF_CUDA(cudaMemcpyAsync(blk.data(), d_blk_.p, (size_t)m * 4, cudaMemcpyDeviceToHost, st));
         BIVF_CUDA(cudaMemcpyAsync(h_len_.data(), d_len_.p, (size_t)C_ * 4, cudaMemcpyDeviceToHost, st));
         BIVF_CUDA(cudaMemcpyAsync(&cursor_new, d_cursor_.p, 4, cudaMemcpyDeviceToHost, st));
+        lap(2);
         BIVF_CUDA(cudaStreamSynchronize(st));
+        lap(3);
         absorb_new_blocks(cursor_old, cursor_new);
+        lap(4);
         for (uint32_t i = 0; i < m; ++i) {
             if (idv[s + i] < 0) continue;  // rejected duplicate
             if (blk[i] >= 0) {
@@ -1834,6 +1859,14 @@ void GpuIndex::write_rows(const std::vector<uint32_t>& lists,
 void GpuIndex::grow_rows(uint32_t need) {
     need = std::min(need, MLB_cap_);
     if (need <= MLB_) return;
+    const auto t_gr = TClock::now();
+    struct Tr {
+        TClock::time_point t;
+        uint32_t from, to;
+        ~Tr() {
+            if (trace_threshold_us() > 0) trace("grow_rows", us_since(t), "MLB " + std::to_string(from) + " -> " + std::to_string(to));
+        }
+    } tr{t_gr, MLB_, std::min(MLB_cap_, std::max(need, 2 * MLB_))};
     const uint32_t nm = std::min(MLB_cap_, std::max(need, 2 * MLB_));
     auto nb = std::make_unique<DevBuf>();
     nb->alloc((size_t)2 * C_ * nm * 4);
@@ -1883,15 +1916,22 @@ void GpuIndex::copy_block_set(const std::vector<int32_t>& src, const std::vector
 }
 
 uint64_t GpuIndex::off_alloc(uint64_t slots) {
+    // best fit: a delete's new segment version usually takes a hole left by an
+    // earlier version of similar size, so holes are not whittled into slivers
+    // (first fit fragmented the free space until most copy-on-write deletes fell
+    // back to the quiescent path under a sustained delete stream)
     slots = std::max<uint64_t>(32, (slots + 31) / 32 * 32);
-    for (auto it = off_free_.begin(); it != off_free_.end(); ++it) {
-        if (it->second < slots) continue;
-        const uint64_t st = it->first, len = it->second;
-        off_free_.erase(it);
-        if (len > slots) off_free_[st + slots] = len - slots;
-        return st;
-    }
-    return ~0ull;
+    auto best = off_free_.end();
+    for (auto it = off_free_.begin(); it != off_free_.end(); ++it)
+        if (it->second >= slots && (best == off_free_.end() || it->second < best->second)) {
+            best = it;
+            if (it->second == slots) break;
+        }
+    if (best == off_free_.end()) return ~0ull;
+    const uint64_t st = best->first, len = best->second;
+    off_free_.erase(best);
+    if (len > slots) off_free_[st + slots] = len - slots;
+    return st;
 }
 
 void GpuIndex::off_free_add(uint64_t start, uint64_t slots) {
@@ -2250,6 +2290,8 @@ uint64_t GpuIndex::remove(const int64_t* ids, uint64_t n, uint8_t* found) {
 
     // ---- quiescent fallback: compaction in place, searches fenced
     ++quiescent_ops_;
+    if (trace_threshold_us() > 0)
+        trace("remove_quiescent", 0.0 + trace_threshold_us(), "no copy-on-write space: need_blocks=" + std::to_string(need_blocks));
     std::vector<uint32_t> len_idx, len_val, off_idx, off_val;
     for (auto& kv : parts) {
         const uint64_t key = kv.first;
