@@ -1209,8 +1209,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     float* q_nr = reinterpret_cast<float*>(q_thr + 2 * kVmQ);             // [2][kVmQ] |r|^2
     float* q_rn = q_nr + 2 * kVmQ;                                        // [2][kVmQ] |r|
     float* cent_s = q_rn + 2 * kVmQ;                                      // [kMaxD] the item's centroid
-    float* nrp = cent_s + kMaxD;                                          // [8][kVmQ] partial |r|^2
-    uint32_t* q_id = reinterpret_cast<uint32_t*>(nrp + 8 * kVmQ);         // [2][kVmQ] query index
+    float* nrp = cent_s + kMaxD;                                          // [16][kVmQ] partial |r|^2
+    uint32_t* q_id = reinterpret_cast<uint32_t*>(nrp + 16 * kVmQ);        // [2][kVmQ] query index
     uint32_t* o_cnt = q_id + 2 * kVmQ;                                    // [2 wg][kVmQ] run fill
     uint32_t* o_ovf = o_cnt + 2 * kVmQ;                                   // [2 wg][kVmQ]
     uint32_t* kbest = o_ovf + 2 * kVmQ;                                   // [2 items][32 slots][kVmQ] f2ord
@@ -1460,17 +1460,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0) mbar_arrive(&it_empty[rs]);
             // this thread's query values and centroid value: global loads issued
             // before the barrier (they write no shared state)
-            const uint32_t n = t256 & 31, h = t256 >> 5;  // column n, dims [16h, 16h + 16)
-            const bool act = d.valid && n < d.npairs;
-            float4 qv4[4];
+            // columns n0, n0 + 1 (a bf16 pair: one 4 B store per plane row), dims [8h, 8h + 8)
+            const uint32_t n0 = 2u * (t256 & 15), h = t256 >> 4;
+            const bool act0 = d.valid && n0 < d.npairs, act1 = d.valid && n0 + 1 < d.npairs;
+            float4 qv4[4];  // [query 0: dims 0-3, 4-7][query 1: ...]
             {
-                const uint32_t pair = act ? d.pairs[n] : 0u;
-                const float* q = p.queries + (uint64_t)(pair / p.P) * p.Dp;
+                const float* q0 = p.queries + (uint64_t)((act0 ? d.pairs[n0] : 0u) / p.P) * p.Dp;
+                const float* q1 = p.queries + (uint64_t)((act1 ? d.pairs[n0 + 1] : 0u) / p.P) * p.Dp;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t k0 = 16 * h + 4 * i;
-                    qv4[i] = (act && k0 < p.Dp) ? __ldg(reinterpret_cast<const float4*>(q + k0))
-                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int i = 0; i < 2; ++i) {
+                    const uint32_t k0 = 8 * h + 4 * i;
+                    qv4[i] = (act0 && k0 < p.Dp) ? __ldg(reinterpret_cast<const float4*>(q0 + k0))
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+                    qv4[2 + i] = (act1 && k0 < p.Dp) ? __ldg(reinterpret_cast<const float4*>(q1 + k0))
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
             const float cv = (d.valid && (uint32_t)t256 < p.D) ? __ldg(p.centroids + (uint64_t)d.c * p.D + t256) : 0.f;
@@ -1492,27 +1495,30 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (t256 < (int)K) cent_s[t256] = cv;
             named_bar(3, 256);
             {
-                float nh = 0.f;
-                if (16 * h < K) {
+                float nh0 = 0.f, nh1 = 0.f;
+                if (8 * h < K) {
                     unsigned char* bh = sB + ib * 2 * kVmPlane;
                     unsigned char* bl = bh + kVmPlane;
+                    const float qa0[8] = {qv4[0].x, qv4[0].y, qv4[0].z, qv4[0].w, qv4[1].x, qv4[1].y, qv4[1].z, qv4[1].w};
+                    const float qa1[8] = {qv4[2].x, qv4[2].y, qv4[2].z, qv4[2].w, qv4[3].x, qv4[3].y, qv4[3].z, qv4[3].w};
 #pragma unroll
-                    for (int i = 0; i < 16; i += 4) {
-                        const uint32_t k0 = 16 * h + i;
-                        const float4 qv = qv4[i / 4];
-                        const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float r = __fsub_rn(qa[e], act ? cent_s[k0 + e] : 0.f);
-                            nh = __fadd_rn(nh, __fmul_rn(r, r));
-                            const __nv_bfloat16 rh = __float2bfloat16_rn(r);
-                            const __nv_bfloat16 rl = __float2bfloat16_rn(__fsub_rn(r, __bfloat162float(rh)));
-                            *reinterpret_cast<__nv_bfloat16*>(bh + vm_boff(k0 + e, n)) = rh;
-                            *reinterpret_cast<__nv_bfloat16*>(bl + vm_boff(k0 + e, n)) = rl;
-                        }
+                    for (int e = 0; e < 8; ++e) {
+                        const uint32_t k = 8 * h + e;
+                        const float c = cent_s[k];
+                        const float r0 = __fsub_rn(qa0[e], act0 ? c : 0.f);
+                        const float r1 = __fsub_rn(qa1[e], act1 ? c : 0.f);
+                        nh0 = __fadd_rn(nh0, __fmul_rn(r0, r0));
+                        nh1 = __fadd_rn(nh1, __fmul_rn(r1, r1));
+                        // the same hi / lo split as element-wise bf16_rn (one packed convert each)
+                        const __nv_bfloat162 hi = __floats2bfloat162_rn(r0, r1);
+                        const __nv_bfloat162 lo = __floats2bfloat162_rn(__fsub_rn(r0, __low2float(hi)),
+                                                                        __fsub_rn(r1, __high2float(hi)));
+                        *reinterpret_cast<__nv_bfloat162*>(bh + vm_boff(k, n0)) = hi;
+                        *reinterpret_cast<__nv_bfloat162*>(bl + vm_boff(k, n0)) = lo;
                     }
                 }
-                nrp[h * kVmQ + n] = nh;
+                nrp[h * kVmQ + n0] = nh0;
+                nrp[h * kVmQ + n0 + 1] = nh1;
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // planes -> the MMA's async proxy
             named_bar(3, 256);
@@ -1522,7 +1528,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const bool act = n < d.npairs;
                 float nr = 0.f;
 #pragma unroll
-                for (int h = 0; h < 8; ++h) nr = __fadd_rn(nr, nrp[h * kVmQ + n]);  // fixed order
+                for (int h = 0; h < 16; ++h) nr = __fadd_rn(nr, nrp[h * kVmQ + n]);  // fixed order
                 const uint32_t qi = act ? d.pairs[n] / p.P : 0u;
                 q_id[ib * kVmQ + n] = qi;
                 q_nr[ib * kVmQ + n] = nr;
@@ -2667,7 +2673,7 @@ static_assert(tc_smem_bytes<16, false>() <= 232448 && tc_smem_bytes<32, false>()
 
 constexpr size_t vm_smem_bytes() {
     return 1024 + kVmNS * kVmSlot + 4 * kVmPlane + 8 * 1024 * 4 + 8 * kVmKC * 32 * 8 + kVmNR * 4 * 32 * 4 +
-           2 * kVmQ * 4 * 3 + kMaxD * 4 + 8 * kVmQ * 4 + 2 * kVmQ * 4 + 4 * kVmQ * 4 + 2 * 32 * kVmQ * 4 +
+           2 * kVmQ * 4 * 3 + kMaxD * 4 + 16 * kVmQ * 4 + 2 * kVmQ * 4 + 4 * kVmQ * 4 + 2 * 32 * kVmQ * 4 +
            (2 * kVmNS + 2 * kVmNB + 4 + 2 * kRing + 2 * kVmNR) * 8 + kRing * sizeof(TcItem) + 16;
 }
 static_assert(vm_smem_bytes() <= 232448, "vm smem budget");
