@@ -2861,7 +2861,7 @@ static cudaError_t launch_vm(const DevLists& L, const PlanBufs& B, const long lo
     p.ccount = T.ccount;
     p.clb = T.clb;
     p.cloc = T.cloc;
-    e = sh.k <= 16 ? vm_attr<16>() : vm_attr<32>();
+    e = sh.k == 10 ? vm_attr<10>() : sh.k <= 16 ? vm_attr<16>() : vm_attr<32>();
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(T.qthr, 0xff, (size_t)sh.nq * 4, s);
     if (e != cudaSuccess) return e;
@@ -2877,7 +2877,9 @@ static cudaError_t launch_vm(const DevLists& L, const PlanBufs& B, const long lo
     VmMaps vmaps;
     for (int a = 0; a < 2; ++a)
         for (int i = 0; i < 3; ++i) vmaps.m[a][i] = maps_hi[3 * a + i];
-    if (sh.k <= 16) scan_vm_kernel<16><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, vmaps);
+    // KT = the k-best slots an offer reads: exactly 10 for the common k = 10
+    if (sh.k == 10) scan_vm_kernel<10><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, vmaps);
+    else if (sh.k <= 16) scan_vm_kernel<16><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, vmaps);
     else scan_vm_kernel<32><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, vmaps);
     count_launch(2);
     e = cudaGetLastError();
