@@ -135,7 +135,8 @@ struct TcParams {
     uint32_t D, Dk, Dp, k, P, maxch;
     uint32_t brow, gstride, nkc;  // TMA box rows, map rows per group, K-chunks per group (wide: Dk / brow)
     uint32_t seed_groups;        // seeding pass: scan only the first seed_groups groups, no run output
-    uint32_t qt;                 // plan tile: pairs per work item (kM, or kVmQ for scan_vm_kernel)
+    uint32_t qt;                 // plan tile: pairs per work item (kM, or kVmQ for scan_vm_kernel;
+                                 // kVmQ also marks runs whose upper bounds only warpgroup 0 writes)
     const float* samp_rows;      // seed samples (maint.cuh kSampS per list, [list][d][slot]) or null
     const long long* samp_ids;   // their ids (-1: empty / deleted)
     const float* centroids;      // [C][D] row-major
@@ -1724,7 +1725,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         }
                     }
                 }
-                if (wl == 0)
+                if (wl == 0)  // (warpgroup 1's +inf slots are skipped by the refine)
                     for (uint32_t i = 0; i < p.k; ++i)
                         p.ub[run * p.k + i] =
                             wg == 0 ? qthr_dec(*reinterpret_cast<volatile uint32_t*>(kb0 + i * kVmQ + n))
@@ -1887,11 +1888,18 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
         const uint32_t per_probe = p.maxch * 2u * p.k;
         const uint32_t total = p.P * per_probe;
         const uint64_t base = (uint64_t)q * total;
-        for (uint32_t f0 = 32 * ws; f0 < total; f0 += 32 * WPQ) {
-            const uint32_t f = f0 + lane;
+        // scan_vm_kernel: only warpgroup 0's runs (the first k of every 2k) hold
+        // values; the sweep visits those only
+        const uint32_t wsh = p.qt == (uint32_t)kVmQ ? 1u : 0u;
+        const uint32_t vis = total >> wsh;
+        for (uint32_t f0 = 32 * ws; f0 < vis; f0 += 32 * WPQ) {
+            const uint32_t g = f0 + lane;
             bool pass = false;
             float v = 0.f;
-            if (f < total) {
+            uint32_t f = 0;
+            if (g < vis) {
+                // g -> f: with wsh, g = (probe, chunk) * k + i maps to (probe, chunk) * 2k + i
+                f = wsh ? (g / p.k) * 2u * p.k + g % p.k : g;
                 const uint32_t pi = f / per_probe, rem = f - pi * per_probe;
                 const uint32_t h = rem / (2u * p.k);
                 const uint32_t c = (uint32_t)probes[(uint64_t)q * p.P + pi];
@@ -1905,7 +1913,7 @@ __global__ void refine_kernel(TcParams p, const long long* probes, float* out_d,
                 const int src = __ffs(msk) - 1;
                 msk &= msk - 1;
                 const float bv = __shfl_sync(0xffffffffu, v, src);
-                const long long bi = (long long)(base + f0 + src);
+                const long long bi = (long long)(base + __shfl_sync(0xffffffffu, f, src));
                 if (th.admits(bv, bi)) th.insert(bv, bi, (int)p.k, lane);
             }
         }
