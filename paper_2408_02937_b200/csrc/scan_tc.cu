@@ -1536,7 +1536,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 q_rn[ib * kVmQ + n] = sqrtf(nr);
                 q_thr[ib * kVmQ + n] = act ? __ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + qi) : 0u;
             }
-            for (int i = t256; i < 32 * kVmQ; i += 256) kbest[ib * 32 * kVmQ + i] = 0xffffffffu;
+            reinterpret_cast<uint4*>(kbest + ib * 32 * kVmQ)[t256] = make_uint4(~0u, ~0u, ~0u, ~0u);  // 32 x kVmQ slots
             named_bar(3, 256);
             return true;
         };
