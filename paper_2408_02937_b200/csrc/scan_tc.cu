@@ -1136,7 +1136,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // item each warpgroup gathers its 4 lanes' candidates of a query into one run
 // of refine_kernel's format (warpgroup 0's run carries the k-best set).
 constexpr int kVmQ = 32;       // query columns per work item (MMA N <= 32)
-constexpr int kVmNS = 3;       // A stage slots (one unit of 4 groups each)
+#ifndef BIVF_VM_WG
+#define BIVF_VM_WG 2  // math warpgroups (units go round-robin; warpgroups >= 1 share run slot 1)
+#endif
+#ifndef BIVF_VM_NS
+#define BIVF_VM_NS 3
+#endif
+#ifndef BIVF_VM_KC
+#define BIVF_VM_KC 24
+#endif
+constexpr int kVmWG = BIVF_VM_WG;
+constexpr int kVmMath = 128 * kVmWG;             // math threads
+constexpr int kVmThreads = 64 + kVmMath;         // + producer and MMA warps
+constexpr int kVmNS = BIVF_VM_NS;  // A stage slots (one unit of 4 groups each)
 #ifndef BIVF_VM_PF
 #define BIVF_VM_PF 0
 #endif
@@ -1149,7 +1161,7 @@ constexpr int kVmNR = 8;       // norm ring slots (a unit's 4 x 32 |s|^2)
 #define BIVF_VM_NB 4  // 8 measured equal (1.004 vs 1.005 ms): the math warps, not buffering, limit
 #endif
 constexpr int kVmNB = BIVF_VM_NB;  // TMEM accumulators (32 columns each; power of 2)
-constexpr int kVmKC = 24;      // candidate slots per (warp, query lane)
+constexpr int kVmKC = BIVF_VM_KC;  // candidate slots per (warp, query lane)
 constexpr uint32_t kVmSlot = 4u * kMaxD * 64u;  // bytes per A slot (4 groups x K rows x 64 B, K <= 128)
 constexpr uint32_t kVmPlane = kMaxD * 64u;      // bytes per B plane (K rows x 32 queries bf16)
 constexpr float kVmCross = 1.0f / 64.0f;
@@ -1192,7 +1204,7 @@ __device__ __forceinline__ uint32_t vm_nvalid(const TcParams& p, const TcItem& d
 }
 
 template <int KT>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kVmThreads, 1)
     scan_vm_kernel(const TcParams p, const __grid_constant__ VmMaps maps) {
     const CUtensorMap* map_g1[2] = {&maps.m[0][0], &maps.m[1][0]};  // one group's hi plane
     const CUtensorMap* map_g4[2] = {&maps.m[0][1], &maps.m[1][1]};  // four consecutive groups' hi planes
@@ -1202,10 +1214,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint32_t pad = ((raw_s + 1023u) & ~1023u) - raw_s;
     unsigned char* sA = smem_raw + pad;                                  // kVmNS * kVmSlot
     unsigned char* sB = sA + kVmNS * kVmSlot;                             // [2 items][hi, lo] planes
-    float* tiles = reinterpret_cast<float*>(sB + 4 * kVmPlane);           // [8 warps][32][32] transposes
-    float* cand_lb = tiles + 8 * 1024;                                    // [8 warps][kVmKC][32]
-    uint32_t* cand_loc = reinterpret_cast<uint32_t*>(cand_lb + 8 * kVmKC * 32);
-    float* nslots = reinterpret_cast<float*>(cand_loc + 8 * kVmKC * 32);  // [kVmNR][4 groups][32] |s|^2
+    float* tiles = reinterpret_cast<float*>(sB + 4 * kVmPlane);           // [math warps][32][32] transposes
+    float* cand_lb = tiles + 4 * kVmWG * 1024;                            // [math warps][kVmKC][32]
+    uint32_t* cand_loc = reinterpret_cast<uint32_t*>(cand_lb + 4 * kVmWG * kVmKC * 32);
+    float* nslots = reinterpret_cast<float*>(cand_loc + 4 * kVmWG * kVmKC * 32);  // [kVmNR][4 groups][32] |s|^2
     uint32_t* q_thr = reinterpret_cast<uint32_t*>(nslots + kVmNR * 4 * 32);  // [2 items][kVmQ] f2ord theta
     float* q_nr = reinterpret_cast<float*>(q_thr + 2 * kVmQ);             // [2][kVmQ] |r|^2
     float* q_rn = q_nr + 2 * kVmQ;                                        // [2][kVmQ] |r|
@@ -1254,7 +1266,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         for (int s = 0; s < kRing; ++s) {
             mbar_init(&it_full[s], 1);
-            mbar_init(&it_empty[s], 1 + 4 * kWG);
+            mbar_init(&it_empty[s], 1 + 4 * kVmWG);
         }
         fence_mbar_init();
     }
@@ -1446,6 +1458,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     } else {
         // ------------------------------------------------ math warpgroups
         const int wg = (warp - 2) >> 2;
+        const uint32_t rs = wg ? 1u : 0u;                 // run slot: warpgroup 0, or the others together
         const int q4 = warp & 3;                          // TMEM lane quarter = group of the unit
         const int wl = (warp - 2) & 3;                    // warp index within the warpgroup (0: filter lanes)
         const int t256 = threadIdx.x - 64;                // 0..255 over both warpgroups
@@ -1480,7 +1493,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const float cv = (d.valid && (uint32_t)t256 < p.D) ? __ldg(p.centroids + (uint64_t)d.c * p.D + t256) : 0.f;
             // both warpgroups are done with item seq - 2's state: taken for the
             // end marker too (no warp may run ahead of another's run output)
-            named_bar(3, 256);
+            named_bar(3, kVmMath);
             if (t256 < 2 * kVmQ) {  // the run-output gather counters of item seq - 1 (output after this build)
                 o_cnt[t256] = 0;
                 o_ovf[t256] = 0;
@@ -1488,13 +1501,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (!d.valid) {
                 // end marker: the reset above must still be ordered before the last
                 // item's run output (every math thread takes this same branch)
-                named_bar(3, 256);
+                named_bar(3, kVmMath);
                 return false;
             }
             const uint32_t ib = seq & 1;
             if (seq >= 2) mbar_wait(&b_free[ib], ((seq - 2) >> 1) & 1);
             if (t256 < (int)K) cent_s[t256] = cv;
-            named_bar(3, 256);
+            named_bar(3, kVmMath);
             {
                 float nh0 = 0.f, nh1 = 0.f;
                 if (8 * h < K) {
@@ -1518,11 +1531,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         *reinterpret_cast<__nv_bfloat162*>(bl + vm_boff(k, n0)) = lo;
                     }
                 }
-                nrp[h * kVmQ + n0] = nh0;
-                nrp[h * kVmQ + n0 + 1] = nh1;
+                if (h < 16) {
+                    nrp[h * kVmQ + n0] = nh0;
+                    nrp[h * kVmQ + n0 + 1] = nh1;
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // planes -> the MMA's async proxy
-            named_bar(3, 256);
+            named_bar(3, kVmMath);
             if (t256 == 0) mbar_arrive(&b_full[ib]);
             if (t256 < kVmQ) {
                 const uint32_t n = t256;
@@ -1536,8 +1551,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 q_rn[ib * kVmQ + n] = sqrtf(nr);
                 q_thr[ib * kVmQ + n] = act ? __ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + qi) : 0u;
             }
-            reinterpret_cast<uint4*>(kbest + ib * 32 * kVmQ)[t256] = make_uint4(~0u, ~0u, ~0u, ~0u);  // 32 x kVmQ slots
-            named_bar(3, 256);
+            if (t256 < 256)
+                reinterpret_cast<uint4*>(kbest + ib * 32 * kVmQ)[t256] = make_uint4(~0u, ~0u, ~0u, ~0u);  // 32 x kVmQ slots
+            named_bar(3, kVmMath);
             return true;
         };
         uint32_t unit = 0;
@@ -1563,7 +1579,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             // the global threshold, loaded a unit ahead (its latency stays hidden)
             uint32_t qg = active ? __ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + qi) : 0xffffffffu;
             for (uint32_t j0 = d.g0; j0 < d.g1; j0 += 4, ++unit) {
-                if ((unit & 1u) != (uint32_t)wg) continue;
+                if (unit % (uint32_t)kVmWG != (uint32_t)wg) continue;
                 const uint32_t b = unit % kVmNB, nsl = unit % kVmNR;
                 const uint32_t qcur = qg;
                 if (active) qg = __ldcg(reinterpret_cast<const uint32_t*>(p.qthr) + qi);
@@ -1707,13 +1723,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             // (The gather counters were reset by build(seq + 1) above.)
             if (active) {
                 const uint32_t pair = d.pairs[n];
-                const uint64_t run = (((uint64_t)pair * p.maxch + d.chunk) << 1) | (uint32_t)wg;
+                const uint64_t run = (((uint64_t)pair * p.maxch + d.chunk) << 1) | rs;
                 const float th = qthr_dec(*reinterpret_cast<volatile uint32_t*>(qts));
                 uint32_t w = 0;
                 for (uint32_t i = 0; i < ncand; ++i) w += clb[i * 32] <= th;
-                const uint32_t at = overflow ? 0u : atomicAdd(&o_cnt[wg * kVmQ + n], w);
+                const uint32_t at = overflow ? 0u : atomicAdd(&o_cnt[rs * kVmQ + n], w);
                 if (overflow || at + w > kKC) {
-                    o_ovf[wg * kVmQ + n] = 1;
+                    o_ovf[rs * kVmQ + n] = 1;
                 } else {
                     uint32_t o = at;
                     for (uint32_t i = 0; i < ncand; ++i) {
@@ -1725,17 +1741,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         }
                     }
                 }
-                if (wl == 0)  // (warpgroup 1's +inf slots are skipped by the refine)
+                if (wl == 0 && wg <= 1)  // (run slot 1's +inf values are skipped by the refine)
                     for (uint32_t i = 0; i < p.k; ++i)
                         p.ub[run * p.k + i] =
                             wg == 0 ? qthr_dec(*reinterpret_cast<volatile uint32_t*>(kb0 + i * kVmQ + n))
                                     : __int_as_float(0x7f800000);
             }
-            named_bar(1 + wg, 128);
-            if (wl == 0 && active) {
+            named_bar(1 + rs, rs ? 128 * (kVmWG - 1) : 128);  // the run slot's warpgroups
+            if (wl == 0 && wg <= 1 && active) {
                 const uint32_t pair = d.pairs[n];
-                const uint64_t run = (((uint64_t)pair * p.maxch + d.chunk) << 1) | (uint32_t)wg;
-                p.ccount[run] = o_ovf[wg * kVmQ + n] ? kOverflow : o_cnt[wg * kVmQ + n];
+                const uint64_t run = (((uint64_t)pair * p.maxch + d.chunk) << 1) | rs;
+                p.ccount[run] = o_ovf[rs * kVmQ + n] ? kOverflow : o_cnt[rs * kVmQ + n];
             }
             pf.mark(8);
             d = dn;
@@ -2680,7 +2696,7 @@ static_assert(tc_smem_bytes<16, false>() <= 232448 && tc_smem_bytes<32, false>()
               "smem budget");
 
 constexpr size_t vm_smem_bytes() {
-    return 1024 + kVmNS * kVmSlot + 4 * kVmPlane + 8 * 1024 * 4 + 8 * kVmKC * 32 * 8 + kVmNR * 4 * 32 * 4 +
+    return 1024 + kVmNS * kVmSlot + 4 * kVmPlane + 4 * kVmWG * 1024 * 4 + 4 * kVmWG * kVmKC * 32 * 8 + kVmNR * 4 * 32 * 4 +
            2 * kVmQ * 4 * 3 + kMaxD * 4 + 16 * kVmQ * 4 + 2 * kVmQ * 4 + 4 * kVmQ * 4 + 2 * 32 * kVmQ * 4 +
            (2 * kVmNS + 2 * kVmNB + 4 + 2 * kRing + 2 * kVmNR) * 8 + kRing * sizeof(TcItem) + 16;
 }
@@ -2886,9 +2902,9 @@ static cudaError_t launch_vm(const DevLists& L, const PlanBufs& B, const long lo
     for (int a = 0; a < 2; ++a)
         for (int i = 0; i < 3; ++i) vmaps.m[a][i] = maps_hi[3 * a + i];
     // KT = the k-best slots an offer reads: exactly 10 for the common k = 10
-    if (sh.k == 10) scan_vm_kernel<10><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, vmaps);
-    else if (sh.k <= 16) scan_vm_kernel<16><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, vmaps);
-    else scan_vm_kernel<32><<<grid, kTcThreads, vm_smem_bytes(), s>>>(p, vmaps);
+    if (sh.k == 10) scan_vm_kernel<10><<<grid, kVmThreads, vm_smem_bytes(), s>>>(p, vmaps);
+    else if (sh.k <= 16) scan_vm_kernel<16><<<grid, kVmThreads, vm_smem_bytes(), s>>>(p, vmaps);
+    else scan_vm_kernel<32><<<grid, kVmThreads, vm_smem_bytes(), s>>>(p, vmaps);
     count_launch(2);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
